@@ -1,0 +1,406 @@
+"""bench.py -- positions x scales screened per second on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one pass of the hot path over one image of the workload: the 12
+integral planes (K1/K2), then for every ladder size the screen (K3), the
+survivor list (K4) and the footprint union (K5), then the region popcount.
+Inputs are resident in HBM for ``value``; ``e2e`` is the same metric through
+the public drop-in ``screen()`` with host numpy in / host results out.
+
+Multi-GPU (torchrun): every rank screens its own image of the workload
+(seed + rank) -- per-GPU work fixed, ``scaling: weak``; the only collective
+is an NCCL all-gather of the per-rank survivor counts and timings.
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, the "port"; the reference itself is pure NumPy and not installed
+on the GPU box) with every host thread, on the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate positions x scales screened/sec"
+UNIT = "positions*scales/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json config index (default: configs[1])")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=1, help="capture each step in a CUDA graph")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(cfg_idx):
+    import workloads as WL
+
+    return WL.CONFIGS[cfg_idx]
+
+
+def config_json(wl, ladder, n_gpus, extra=None):
+    d = {
+        "workload": f"BASELINE config {wl.index}: {wl.images} x {wl.width}x{wl.height} u8, template n={wl.template_side}, "
+                    f"{len(ladder)} ladder sizes {ladder[0]}..{ladder[-1]}",
+        "image": f"{wl.width}x{wl.height}",
+        "template_side": wl.template_side,
+        "ladder": list(ladder),
+        "alpha": wl.alpha,
+        "beta": wl.beta,
+        "ladder_ratio": wl.ladder_ratio,
+        "quantizer": list(wl.q),
+        "parallelism": f"image-parallel x{n_gpus}" if n_gpus > 1 else "single GPU",
+        "per_rank_images": 1,
+        "l2": "flushed (256 MiB write) between timed steps; tables are 12 int64 planes "
+              f"({12 * 8 * (wl.width + 1) * (wl.height + 1) / 1e6:.0f} MB) > 126 MB L2",
+    }
+    if extra:
+        d.update(extra)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index=0, period=0.05):
+        self.samples = []
+        self.reasons = set()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # pragma: no cover - no NVML
+            self.max_sm = None
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+
+    _NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_sm, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(wl, case, nthreads, max_seconds=30.0):
+    """The oracle port (reference algorithm in C, all host threads) on the
+    same image and template; the whole ladder, tables included, as the
+    reference's screen() does.  Bounded: configs >1 use a row band."""
+    import oracle as O
+
+    cfg = O.ScreeningConfig(alpha=wl.alpha, beta=wl.beta, ladder_ratio=wl.ladder_ratio, quantizer=O.Quantizer(*wl.q))
+    img = case.image
+    sample = f"full {wl.width}x{wl.height} image, all {len(O.ladder_sizes(wl.template_side, cfg))} sizes"
+    if wl.width * wl.height > 2048 * 2048:
+        rows = max(1024, int(2048 * 2048 / wl.width))
+        y0 = (wl.height - rows) // 2
+        img = np.ascontiguousarray(img[y0:y0 + rows])
+        sample = f"{wl.width}x{rows} row band of the image, all sizes"
+    t0 = time.perf_counter()
+    res = O.screen(img, case.template, cfg, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return {"value": res.patches_tested / dt, "unit": UNIT, "cores": nthreads, "kind": "port",
+            "sample": sample + f" (oracle/oracle.c, {res.patches_tested} positions in {dt:.2f} s)",
+            "positions": res.patches_tested, "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import workloads as WL
+
+    wl = workload_config(args.config)
+    case = WL.make_cases(wl, images=1)[0]
+    nthreads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(wl, case, nthreads)
+        if i >= args.warmup:
+            vals.append(r)
+    pos = sum(r["positions"] for r in vals)
+    secs = sum(r["seconds"] for r in vals)
+    v = pos / secs
+    from paper_1707_05647_b200.config import ladder_sizes
+    import workloads as WLm
+
+    ladder = ladder_sizes(wl.template_side, WLm.screening_config(wl))
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
+        "impl": "reference",
+        "config": config_json(wl, ladder, args.gpus, {"sample": vals[0]["sample"]}),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port", "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import workloads as WL
+    from paper_1707_05647_b200 import _native, screen
+    from paper_1707_05647_b200.engine import Engine, prepare_template
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    wl = workload_config(args.config)
+    cfg = WL.screening_config(wl)
+    case = WL.make_cases(wl, images=1, first_image=rank)[0]
+    img_dev = torch.from_numpy(case.image).to(dev)
+    tp = prepare_template(case.template, cfg, dev)
+    eng = Engine(wl.width, wl.height, dev)
+    stream = torch.cuda.Stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    # ── instrumented pass (not timed): cascade stage counts for the roofline ──
+    eng.stage_counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        eng.run(img_dev, tp)
+    torch.cuda.synchronize()
+    stage = eng.stage_counts.cpu().tolist()
+    eng.stage_counts = None
+    positions = eng.tested(tp)
+    survivors = int(eng.totals[0].item())
+
+    # per-launch events around every screen kernel (dominant kernel)
+    ev_pairs = []
+
+    def before(k):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev_pairs.append([e, None])
+
+    def after(k):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev_pairs[-1][1] = e
+
+    def step():
+        eng.run(img_dev, tp, capacity=max(survivors, 1) * 2)
+
+    graph = None
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        if args.graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+            graph.replay()
+    torch.cuda.synchronize()
+
+    # ── timed region: K steps, L2 flushed between steps (outside the events) ──
+    n0 = _native.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as clocks:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    n_launch_graph = None
+    if graph is None:
+        launches = _native.launch_count() - n0
+    else:
+        # graph replays do not pass through the library: count the launches of one captured step
+        n1 = _native.launch_count()
+        with torch.cuda.stream(stream):
+            step()
+        torch.cuda.synchronize()
+        n_launch_graph = _native.launch_count() - n1
+        launches = n_launch_graph * args.steps
+    total_ms = sum(step_ms)
+
+    # per-kernel timing of the screen launches (dominant kernel), same stream
+    eng.hooks = (before, after)
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            flush.fill_(i)
+            step()
+    torch.cuda.synchronize()
+    eng.hooks = None
+    screen_ms = sum(a.elapsed_time(b) for a, b in ev_pairs) / 3.0  # per step, all sizes
+    n_sizes = sum(1 for sp in tp.sizes if sp.plan)
+
+    # max over ranks
+    t = torch.tensor([total_ms, float(positions), float(survivors)], dtype=torch.float64, device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        allt = torch.stack(gathered).cpu().numpy()
+        max_ms = float(allt[:, 0].max())
+        total_positions = float(allt[:, 1].sum())
+    else:
+        max_ms = total_ms
+        total_positions = float(positions)
+    value = total_positions * args.steps / (max_ms / 1e3)
+
+    # ── roofline of the dominant kernel (K3 screen) ──
+    peak, peak_src = measured_peak_hbm()
+    # algorithmic bytes: 24 B/position for the PLAIN planes every
+    # ring-0 evaluation needs, +24 B for those reaching the std stage (SQ
+    # planes), +48 B for those reaching the gradient stage (X, Y planes), +1/8 B
+    # mask bit.  SURVEY.md 8(d)'s dense figure (all 12 planes, 96 B) is
+    # reported beside it.
+    alg_bytes = 24.0 * stage[0] + 24.0 * stage[1] + 48.0 * stage[2] + positions / 8.0
+    achieved = alg_bytes / (screen_ms / 1e3) / 1e9
+    dense_bytes = 96.125 * positions
+    roofline = {
+        "bound": "hbm", "kernel": "screen_kernel (K3, all ladder sizes of one step)",
+        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        "peak_source": peak_src,
+        "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": alg_bytes / max(positions, 1),
+        "cascade": {"ring0_evals": stage[0], "std_stage": stage[1], "grad_stage": stage[2], "later_ring_evals": stage[3]},
+        "screen_ms_per_step": screen_ms, "screen_share_of_step": screen_ms / (total_ms / args.steps),
+        "survey_dense_bytes_per_position": 96.125,
+        "survey_dense_equiv_GBps": dense_bytes / (screen_ms / 1e3) / 1e9,
+    }
+
+    # ── e2e through the public API (host numpy in, host result out) ──
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        for _ in range(2):
+            screen(case.image, case.template, cfg, device=dev)
+        times = []
+        h2d = d2h = 0
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            res = screen(case.image, case.template, cfg, device=dev)
+            times.append(time.perf_counter() - t0)
+        h2d = case.image.nbytes + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None)
+        words = (wl.width + 31) // 32
+        d2h = (len(tp.sizes) * wl.height * words * 4 + wl.height * words * 4 + len(res.candidates) * 8 + 16
+               + len(tp.sizes) * 8)
+        e2e_t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_positions / float(e2e_t.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e2e_t.item()),
+               "api": "paper_1707_05647_b200.screen(numpy image, numpy template, cfg) incl. host feature sets"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, case, os.cpu_count() or 1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic (seeded noise + shapes, SURVEY.md 8(d); template per reference protocol)",
+            "config": config_json(wl, tp.ladder, world, {
+                "positions_per_step_per_gpu": positions, "survivors_per_step": survivors,
+                "cuda_graph": bool(graph is not None)}),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

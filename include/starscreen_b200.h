@@ -1,0 +1,157 @@
+/*
+ * starscreen_b200.h -- C ABI of the B200-native pre-screening hot path.
+ *
+ * Drop-in boundary for the reference's Python screening API
+ * (/root/reference/pkg/src/starscreen/screening.py:474 screen()).  The
+ * reference has no FFI of its own (it is pure NumPy); these entry points are
+ * what a maintainer binds with ctypes to replace the NumPy internals of
+ * screen() -- see INTEGRATION.md.  Each declaration names the reference
+ * interface it replaces (file:line, paths relative to pkg/src/starscreen/).
+ *
+ * Conventions (all entry points):
+ *   - extern "C", plain pointers and sizes, no torch or CUDA types
+ *     (streams are passed as void* = cudaStream_t);
+ *   - d_* arguments are device pointers, h_* arguments host pointers;
+ *   - return SS_OK or an SS_E* status; ss_last_error() (thread-local) holds
+ *     the message.  SS_EINVAL / SS_ECAPACITY map to Python ValueError,
+ *     SS_ECUDA to RuntimeError -- the reference's error classes;
+ *   - stream-ordered and reentrant; nothing here allocates device memory:
+ *     workspaces are caller-owned and sized by the *_bytes() queries.
+ *
+ * Device table layout ("planes"): 12 int64 planes of (H+1) rows x pitch
+ * columns, plane p = type*4 + kind, kind in {PLAIN, X_WEIGHTED, Y_WEIGHTED,
+ * SQUARED} (integral.py:37-41), type in {SAT, E, O}:
+ *   SAT[y+1][x+1] = Sat.cell(x, y)                 (integral.py:66-81)
+ *   E  [y+1][x+1] = H(x+y,   x-y) = Rsat.cell(x,y) (integral.py:84-106)
+ *   O  [y+1][x+1] = H(x+y+1, x-y)                  (the off-parity corners)
+ * for x in [-1, W-1], y in [-1, H-1], where H(u,v) is the reference's
+ * rotated quadrant prefix.  A closed l1 ball of radius r about (cx,cy) is
+ *   E(cx,cy+r) - O(cx-r-1,cy-1) - O(cx+r,cy-1) + E(cx,cy-r-1)
+ * which equals diamond_region_sum (integral.py:165-186) bit for bit.
+ */
+#ifndef STARSCREEN_B200_H
+#define STARSCREEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_OK 0
+#define SS_EINVAL 1    /* bad argument / bounds  -> ValueError   */
+#define SS_ECAPACITY 2 /* key capacity exceeded  -> ValueError   */
+#define SS_ECUDA 3     /* CUDA launch / runtime  -> RuntimeError */
+
+#define SS_MAX_RINGS 16
+#define SS_KEY_BASE (1LL << 21) /* screening.py:57 _KEY_BASE */
+
+/* ── diagnostics ─────────────────────────────────────────────────────── */
+const char* ss_last_error(void);
+int ss_version(void);
+/* Number of CUDA kernels this library has launched (process lifetime). */
+uint64_t ss_launch_count(void);
+
+/* ── integral tables (integral.py:200-228 build_tables) ──────────────── */
+/* Row pitch, in int64 elements, of every plane for an image W wide. */
+int64_t ss_plane_pitch(int64_t W);
+/* Bytes of the 12-plane table block for a W x H image. */
+size_t ss_tables_bytes(int64_t W, int64_t H);
+/* Bytes of device workspace ss_build_tables needs. */
+size_t ss_build_workspace_bytes(int64_t W, int64_t H);
+/*
+ * Replaces build_tables (integral.py:211-228: 4 x build_sat :109-117 and
+ * 4 x build_rsat :120-141).  d_img: H rows of W bytes, img_pitch bytes apart.
+ * Rejects images that fail the reference's overflow guard
+ * (integral.py:59-63) with SS_EINVAL.
+ */
+int ss_build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                    int64_t plane_pitch, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ── per-size membership sets (screening.py:100-178 FeatureSet) ──────── */
+/*
+ * Lays out one ladder size's per-ring sorted key arrays
+ * (FeatureSet.ring_keys(), screening.py:147-155) as a device-ready blob:
+ * the keys plus their (cm) and (cm,cs) projections used by the screen's
+ * early-exit cascade.  Host-only; call with h_blob = NULL to get the size.
+ * h_keys: concatenated sorted keys, key_off: n_rings+1 offsets.
+ */
+int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings, int64_t* h_blob,
+                   size_t* blob_bytes);
+
+/* ── one ladder size (screening.py:418-471 _scan_size) ───────────────── */
+/*
+ * Evaluates every grid centre of global rows [y_begin, y_end) for patch side
+ * m.  The tables cover a w x h sub-image whose row 0 is global row y_origin
+ * (full width: w == W); row-band shards pass their halo'd band.  Writes the
+ * bit-packed keep mask (bit x%32 of word x/32, rows y_begin.. at
+ * mask_pitch_words apart; border grid centres set, as the reference keeps
+ * them) and, per mask row, the number of evaluated survivors into
+ * d_row_counts.  h_ring_n / h_ring_d: ring_plan(m) (features.py:190-211).
+ * d_blob: the ss_keyset_blob() layout copied to the device.  d_stage_counts
+ * (nullable, 4 x u64, accumulated) instruments the early-exit cascade:
+ * ring-0 evaluations, ring-0 centres reaching the std stage, reaching the
+ * gradient stage, and evaluations of rings >= 1.
+ */
+int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_pitch, int64_t W, int64_t H,
+                   int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,
+                   const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
+                   double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
+                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* stream);
+
+/* screening.py:505-510: sizes below MIN_PATCH_SIDE keep every grid centre. */
+int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,
+                 int64_t mask_pitch_words, uint32_t* d_row_counts, void* stream);
+
+/* ── survivor list (screening.py:455-470, 512-516) ───────────────────── */
+/* Bytes of device workspace ss_compact needs for `rows` mask rows. */
+size_t ss_compact_workspace_bytes(int64_t rows);
+/*
+ * Appends the evaluated survivors of one size (interior grid centres with
+ * their mask bit set, excluding border keeps) to d_xy as int32 (cx, cy)
+ * pairs in row-major order, starting at index *d_total, and advances
+ * *d_total.  Calling it per size in ladder order reproduces the order of
+ * ScreeningResult.candidates (screening.py:280-283).  Entries past
+ * `capacity` are counted but not written.  d_size_count (nullable) receives
+ * this size's survivor count.
+ */
+int ss_compact(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int64_t y_begin,
+               int64_t y_end, int32_t m, int32_t stride, const uint32_t* d_row_counts, int32_t* d_xy,
+               int64_t capacity, unsigned long long* d_total, unsigned long long* d_size_count,
+               void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ── kept region (screening.py:316-330 _footprint_union) ─────────────── */
+/* Workspace for ss_region_accumulate with sizes up to m_max. */
+size_t ss_region_workspace_bytes(int64_t W, int64_t H, int32_t m_max);
+/*
+ * ORs the m x m footprints of the evaluated survivors of one size (full
+ * image mask, y_begin = 0, y_end = H) into d_region (same bit layout).
+ */
+int ss_region_accumulate(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int32_t m,
+                         int32_t stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes,
+                         void* stream);
+/* d_count += number of set bits of the W x H region mask. */
+int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H,
+                unsigned long long* d_count, void* stream);
+
+/* ── template side (screening.py:222-250 build_feature_set) ──────────── */
+/*
+ * Host C++: ring features of every template rescale k = m..k_hi
+ * (resize_bilinear image_io.py:164-178, crop_center :216-228, the patch's
+ * tables and ring_feature_maps features.py:220-224) inserted guard-banded
+ * (screening.py:122-145) into per-ring sorted unique key sets.
+ * h_keys must hold n_rings * 27 * (k_hi - m + 1) entries; h_key_off gets
+ * n_rings + 1 offsets.  SS_ECAPACITY: "quantized cell exceeds key capacity".
+ */
+int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t k_hi, int32_t n_rings,
+                        const int32_t* h_ring_n, const int32_t* h_ring_d, double q_mean, double q_std,
+                        double q_grad, int64_t* h_keys, int64_t* h_key_off);
+/* Ring features (mean, std, grad_mag per ring) of one rescale k (tests). */
+int ss_template_ring_features(const uint8_t* h_template, int32_t n, int32_t k, int32_t m, int32_t n_rings,
+                              const int32_t* h_ring_n, const int32_t* h_ring_d, double* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STARSCREEN_B200_H */

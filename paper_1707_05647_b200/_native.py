@@ -1,0 +1,85 @@
+"""ctypes binding of libstarscreen_b200.so (the C ABI in include/starscreen_b200.h).
+
+This is the binding a maintainer of the reference would add:
+every call returns an SS_* status that is mapped to the reference's error
+classes -- ValueError for bad arguments / capacity, RuntimeError for CUDA
+failures.  There is no fallback: if the library is missing or fails to load,
+importing the GPU path raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstarscreen_b200.so")
+
+SS_OK, SS_EINVAL, SS_ECAPACITY, SS_ECUDA = 0, 1, 2, 3
+SS_MAX_RINGS = 16
+KEY_BASE = 1 << 21
+
+_lib = None
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_p = ctypes.c_void_p
+c_sz = ctypes.c_size_t
+c_d = ctypes.c_double
+
+_SIGS = {
+    "ss_last_error": (ctypes.c_char_p, []),
+    "ss_version": (ctypes.c_int, []),
+    "ss_launch_count": (ctypes.c_uint64, []),
+    "ss_plane_pitch": (c_i64, [c_i64]),
+    "ss_tables_bytes": (c_sz, [c_i64, c_i64]),
+    "ss_build_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "ss_build_tables": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_sz, c_p]),
+    "ss_keyset_blob": (ctypes.c_int, [c_p, c_p, c_i32, c_p, ctypes.POINTER(c_sz)]),
+    "ss_screen_size": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
+                                      c_i32, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_p]),
+    "ss_fill_grid": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i32, c_p, c_i64, c_p, c_p]),
+    "ss_compact_workspace_bytes": (c_sz, [c_i64]),
+    "ss_compact": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_i64, c_p, c_p,
+                                  c_p, c_sz, c_p]),
+    "ss_region_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "ss_region_accumulate": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
+    "ss_popcount": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),
+    "ss_feature_set_keys": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_p]),
+    "ss_template_ring_features": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_p]),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Load the native library (raises if it is missing: no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(status: int, what: str = "") -> None:
+    """Map an SS_* status to the reference's exception classes."""
+    if status == SS_OK:
+        return
+    msg = lib().ss_last_error().decode(errors="replace")
+    if status in (SS_EINVAL, SS_ECAPACITY):
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: {msg}" if what else msg)
+
+
+def launch_count() -> int:
+    return int(lib().ss_launch_count())

@@ -1,0 +1,429 @@
+// ss_build.cu -- K1/K2: the twelve int64 integral planes in one tiled sweep.
+//
+// Replaces build_tables (integral.py:211-228): 4 x build_sat (:109-117, two
+// cumsums) and 4 x build_rsat (:120-141, scatter + cumsum(u) + reverse
+// cumsum(v) over a (W+H)^2 grid).  Instead of the rotated grid we keep two
+// pixel-grid planes E, O per kind (see include/starscreen_b200.h) and use the
+// row recurrences:
+//
+//   P_y(x)  = sum_{i<=x} v(i,y)                      row prefix
+//   S_y(x)  = S_{y-1}(x)   + P_y(x)                  SAT
+//   FF_y(x) = FF_{y-1}(x+1) + P_y(x)                 anti-diagonal carry
+//   GG_y(x) = GG_{y-1}(x-1) + P_y(x-1)               diagonal carry
+//   E(x,y)  = FF_y(x) - GG_y(x),   O(x,y) = FF_y(x+1) - GG_y(x)
+//
+// The image is cut into bands of Rb rows and column chunks of Cw plane
+// columns; a 128-thread CTA owns one (band, chunk) tile plus an Rb-column
+// halo on each side (4 consecutive columns per thread).  The only
+// dependency between tiles is the row state (S, FF, GG) at the row above the
+// band, so the build is three data-parallel passes:
+//   pass 1  every tile computes its band's end state with a zero carry;
+//   pass 2  a scan over bands turns local end states into true ones
+//           (FF shifts left by Rb per band, GG right, S not at all);
+//   pass 3  every tile recomputes its rows with the true carry and streams
+//           the 12 planes out with 16-byte stores.
+// All sums are exact int64 (integral.py:114,134,139).
+#include "ss_common.cuh"
+
+namespace ss {
+namespace {
+
+constexpr int TPB = 128;  // threads per tile
+constexpr int COLS = 4;   // consecutive columns per thread
+constexpr int TILE = TPB * COLS;
+constexpr int RB = kBandRows;
+constexpr int CW = kChunkCols;
+static_assert(TILE == CW + 2 * RB + 2, "tile geometry");
+constexpr int OFF = RB + 1;  // state index of x is x + OFF
+constexpr unsigned FULL = 0xffffffffu;
+
+struct BuildArgs {
+    const uint8_t* img;
+    int64_t W, H, img_pitch;
+    long long* planes;  // 12 planes
+    int64_t pitch, plane_stride;
+    const long long* rowpre;  // [H][G+1][3]
+    int64_t G;
+    long long* state;  // [B-1][4 kinds][3 types][state_len]
+    int64_t slen;
+    int64_t n_chunks;
+};
+
+__device__ __forceinline__ long long shfl_down64(long long v, int d) {
+    return (long long)__shfl_down_sync(FULL, (unsigned long long)v, d);
+}
+__device__ __forceinline__ long long shfl_up64(long long v, int d) {
+    return (long long)__shfl_up_sync(FULL, (unsigned long long)v, d);
+}
+
+// state pointer: band b, kind k, type (0 S, 1 FF, 2 GG)
+__device__ __forceinline__ long long* st_ptr(const BuildArgs& a, int64_t b, int k, int type) {
+    return a.state + ((b * 4 + k) * 3 + type) * a.slen;
+}
+
+// row-prefix at group boundary g (sum over x < 64 g) for quantity q
+__device__ __forceinline__ long long rowpre_at(const BuildArgs& a, int64_t y, int64_t g, int q) {
+    if (g <= 0) return 0;
+    if (g > a.G) g = a.G;
+    return a.rowpre[(y * (a.G + 1) + g) * 3 + q];
+}
+
+// kMode 0: local end state (pass 1); kMode 1: final planes (pass 3)
+template <int kMode>
+__global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t chunk = blockIdx.x, band = blockIdx.y;
+    const int64_t c0 = chunk * CW;             // first owned plane column
+    const int64_t XL = c0 - RB - 2;            // x of thread 0, column 0
+    const int64_t xb = XL + (int64_t)t * COLS; // x of this thread's column 0
+    const int64_t y0 = band * RB;
+    const int64_t y1 = min(a.H, y0 + RB);
+    const int64_t W = a.W;
+
+    __shared__ int sTot[2][TPB / 32][4];              // warp totals of (v, xw, sq)
+    __shared__ long long sEdgeFF[2][TPB / 32][4][2];  // lane-0 FF_old[0..1] per kind
+    __shared__ long long sEdgeQ[2][TPB / 32][4];      // lane-31 GG_old[3]+P[3]
+    __shared__ long long sEdgeP[2][TPB / 32][4];      // lane-0 P[0]
+
+    long long S[4][COLS], FF[4][COLS], GG[4][COLS];
+    // carry: state at row y0-1
+    if (kMode == 1 && band > 0) {
+        for (int k = 0; k < 4; ++k) {
+            const long long* pS = st_ptr(a, band - 1, k, 0);
+            const long long* pF = st_ptr(a, band - 1, k, 1);
+            const long long* pG = st_ptr(a, band - 1, k, 2);
+            const long long swk = pS[W - 1 + OFF];
+#pragma unroll
+            for (int j = 0; j < COLS; ++j) {
+                const int64_t x = xb + j;
+                S[k][j] = (x < 0) ? 0 : (x > W - 1 ? swk : pS[x + OFF]);
+                FF[k][j] = (x >= W - 1) ? swk : (x < -OFF ? 0 : pF[x + OFF]);
+                GG[k][j] = (x <= 0 || x > W + RB) ? 0 : pG[x + OFF];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < COLS; ++j) S[k][j] = FF[k][j] = GG[k][j] = 0;
+    }
+
+    if (kMode == 1 && band == 0) {
+        // plane row 0 (y = -1) is zero in all 12 planes
+        const int64_t c = c0 - 64 + (int64_t)t * COLS;
+        if (c >= c0 && c < c0 + CW && c < a.pitch) {
+            for (int p = 0; p < 12; ++p) {
+                long long* dst = a.planes + p * a.plane_stride + c;
+                reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(0, 0);
+                reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(0, 0);
+            }
+        }
+    }
+
+    const int64_t g0 = (XL + 1) / kGroup;  // P(XL) = rowpre(g0): x < XL+1
+    int buf = 0;
+    for (int64_t y = y0; y < y1; ++y, buf ^= 1) {
+        // ── A: pixels, thread-local scans, warp scans ────────────────────
+        int lv[COLS], lx[COLS], lq[COLS];
+        const uint8_t* row = a.img + y * a.img_pitch;
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            const int64_t x = xb + j;
+            int v = (x >= 0 && x < W) ? (int)__ldg(row + x) : 0;
+            if (t == 0 && j == 0) v = 0;  // column XL is inside rowpre(g0)
+            const int wl = (int)(x - XL);  // local x weight: (x+1) - (XL+1)
+            lv[j] = v;
+            lx[j] = wl * v;
+            lq[j] = v * v;
+        }
+#pragma unroll
+        for (int j = 1; j < COLS; ++j) { lv[j] += lv[j - 1]; lx[j] += lx[j - 1]; lq[j] += lq[j - 1]; }
+        int tv = lv[COLS - 1], tx = lx[COLS - 1], tq = lq[COLS - 1];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ov = __shfl_up_sync(FULL, tv, d), ox = __shfl_up_sync(FULL, tx, d),
+                      oq = __shfl_up_sync(FULL, tq, d);
+            if (lane >= d) { tv += ov; tx += ox; tq += oq; }
+        }
+        if (lane == 31) { sTot[buf][warp][0] = tv; sTot[buf][warp][1] = tx; sTot[buf][warp][2] = tq; }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { sEdgeFF[buf][warp][k][0] = FF[k][0]; sEdgeFF[buf][warp][k][1] = FF[k][1]; }
+        }
+        // exclusive thread prefix within the warp
+        int ev = __shfl_up_sync(FULL, tv, 1), ex = __shfl_up_sync(FULL, tx, 1), eq = __shfl_up_sync(FULL, tq, 1);
+        if (lane == 0) { ev = ex = eq = 0; }
+        __syncthreads();
+
+        // ── B: full row prefixes P for the 4 kinds ───────────────────────
+        for (int w = 0; w < warp; ++w) { ev += sTot[buf][w][0]; ex += sTot[buf][w][1]; eq += sTot[buf][w][2]; }
+        const long long bv = rowpre_at(a, y, g0, 0), bx = rowpre_at(a, y, g0, 1), bq = rowpre_at(a, y, g0, 2);
+        long long P[4][COLS];
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            const long long cv = (long long)(ev + lv[j]);
+            P[0][j] = bv + cv;
+            P[1][j] = bx + (long long)(ex + lx[j]) + (XL + 1) * cv;  // (i+1) = (i-XL) + (XL+1)
+            P[2][j] = (y + 1) * P[0][j];
+            P[3][j] = bq + (long long)(eq + lq[j]);
+        }
+        long long Q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) Q[k] = GG[k][COLS - 1] + P[k][COLS - 1];
+        if (lane == 31) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sEdgeQ[buf][warp][k] = Q[k];
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sEdgeP[buf][warp][k] = P[k][0];
+        }
+        __syncthreads();
+
+        // ── C: advance the recurrences, emit planes ──────────────────────
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            // FF_new(x) = FF_old(x+1) + P(x)
+            long long nf0 = shfl_down64(FF[k][0], 1);
+            long long nf1 = shfl_down64(FF[k][1], 1);
+            long long np0 = shfl_down64(P[k][0], 1);
+            if (lane == 31) {
+                if (warp + 1 < TPB / 32) {
+                    nf0 = sEdgeFF[buf][warp + 1][k][0];
+                    nf1 = sEdgeFF[buf][warp + 1][k][1];
+                    np0 = sEdgeP[buf][warp + 1][k];
+                } else {
+                    nf0 = nf1 = np0 = 0;
+                }
+            }
+            // GG_new(x) = GG_old(x-1) + P(x-1)
+            long long pq = shfl_up64(Q[k], 1);
+            if (lane == 0) pq = (warp > 0) ? sEdgeQ[buf][warp - 1][k] : 0;
+            long long Fn[COLS], Gn[COLS];
+#pragma unroll
+            for (int j = 0; j < COLS - 1; ++j) Fn[j] = FF[k][j + 1] + P[k][j];
+            Fn[COLS - 1] = nf0 + P[k][COLS - 1];
+            Gn[0] = pq;
+#pragma unroll
+            for (int j = 1; j < COLS; ++j) Gn[j] = GG[k][j - 1] + P[k][j - 1];
+            const long long fnext = nf1 + np0;  // FF_new of the next thread's column 0
+#pragma unroll
+            for (int j = 0; j < COLS; ++j) {
+                S[k][j] += P[k][j];
+                FF[k][j] = Fn[j];
+                GG[k][j] = Gn[j];
+            }
+            if (kMode == 1) {
+                const int64_t c = c0 - 64 + (int64_t)t * COLS;  // plane column of j = 0
+                if (c >= c0 && c < c0 + CW && c < a.pitch) {
+                    const int64_t r = y + 1;
+                    long long* ps = a.planes + (0 * 4 + k) * a.plane_stride + r * a.pitch + c;
+                    long long* pe = a.planes + (1 * 4 + k) * a.plane_stride + r * a.pitch + c;
+                    long long* po = a.planes + (2 * 4 + k) * a.plane_stride + r * a.pitch + c;
+                    longlong2* vs = reinterpret_cast<longlong2*>(ps);
+                    longlong2* ve = reinterpret_cast<longlong2*>(pe);
+                    longlong2* vo = reinterpret_cast<longlong2*>(po);
+                    vs[0] = make_longlong2(S[k][0], S[k][1]);
+                    vs[1] = make_longlong2(S[k][2], S[k][3]);
+                    ve[0] = make_longlong2(Fn[0] - Gn[0], Fn[1] - Gn[1]);
+                    ve[1] = make_longlong2(Fn[2] - Gn[2], Fn[3] - Gn[3]);
+                    vo[0] = make_longlong2(Fn[1] - Gn[0], Fn[2] - Gn[1]);
+                    vo[1] = make_longlong2(Fn[3] - Gn[2], fnext - Gn[3]);
+                }
+            }
+        }
+    }
+
+    if (kMode == 0) {
+        // local end state of the band (rows y0..y1-1, y1 - y0 == RB here)
+        const bool first = (chunk == 0), last = (chunk == a.n_chunks - 1);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            const int64_t x = xb + j;
+            const int64_t c = x + 1;
+            const bool owned = (c >= c0 && c < c0 + CW) || (first && c < c0) || (last && c >= c0 + CW);
+            if (!owned) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (x >= 0 && x <= W - 1) st_ptr(a, band, k, 0)[x + OFF] = S[k][j];
+                if (x >= -OFF && x <= W - 2) st_ptr(a, band, k, 1)[x + OFF] = FF[k][j];
+                if (x >= 1 && x <= W + RB) st_ptr(a, band, k, 2)[x + OFF] = GG[k][j];
+            }
+        }
+    }
+}
+
+// Row prefixes at 64-column group boundaries: rowpre[y][g] = sums over x < 64 g
+// of (v, (x+1) v, v^2), g = 0..G.  One warp per row.
+__global__ void rowpre_kernel(BuildArgs a) {
+    const int64_t y = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (y >= a.H) return;
+    const uint8_t* row = a.img + y * a.img_pitch;
+    long long* out = const_cast<long long*>(a.rowpre) + y * (a.G + 1) * 3;
+    if (lane == 0) out[0] = out[1] = out[2] = 0;
+    long long c0 = 0, c1 = 0, c2 = 0;
+    for (int64_t gb = 0; gb < a.G; gb += 32) {
+        const int64_t g = gb + lane;
+        long long s0 = 0, s1 = 0, s2 = 0;
+        if (g < a.G) {
+            const int64_t xa = g * kGroup, xe = min(a.W, xa + kGroup);
+            for (int64_t x = xa; x < xe; ++x) {
+                const long long v = __ldg(row + x);
+                s0 += v;
+                s1 += (x + 1) * v;
+                s2 += v * v;
+            }
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long o0 = shfl_up64(s0, d), o1 = shfl_up64(s1, d), o2 = shfl_up64(s2, d);
+            if (lane >= d) { s0 += o0; s1 += o1; s2 += o2; }
+        }
+        if (g < a.G) {
+            out[(g + 1) * 3 + 0] = c0 + s0;
+            out[(g + 1) * 3 + 1] = c1 + s1;
+            out[(g + 1) * 3 + 2] = c2 + s2;
+        }
+        c0 += __shfl_sync(FULL, s0, 31);
+        c1 += __shfl_sync(FULL, s1, 31);
+        c2 += __shfl_sync(FULL, s2, 31);
+    }
+}
+
+// Pass 2a: inclusive band states of the SAT rows (in place).
+__global__ void band_scan_s_kernel(BuildArgs a, int64_t nb) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= 4 * a.W) return;
+    const int k = (int)(gid / a.W);
+    const int64_t x = gid % a.W;
+    long long acc = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        long long* p = st_ptr(a, b, k, 0) + x + OFF;
+        acc += *p;
+        *p = acc;
+    }
+}
+
+// Pass 2b: inclusive FF / GG band states.  FF paths move left by RB per band
+// (clamped to S(W-1) beyond the right edge), GG paths move right (zero at
+// x <= 0).  Each stored element is read and written by exactly one thread.
+__global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb) {
+    const int64_t W = a.W;
+    const int64_t nF = W - 1 + OFF + (nb - 1) * RB, nG = W + RB + (nb - 1) * RB;
+    const int64_t per_kind = nF + nG;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= 4 * per_kind) return;
+    const int k = (int)(gid / per_kind);
+    const int64_t i = gid % per_kind;
+    long long acc = 0;
+    if (i < nF) {
+        const int64_t p0 = -OFF + i;  // p0 in [-OFF, W-2 + (nb-1) RB]
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t p = p0 - b * RB;
+            if (p < -OFF) break;
+            if (p >= W - 1) {
+                acc = st_ptr(a, b, k, 0)[W - 1 + OFF];  // inclusive S(W-1)
+            } else {
+                long long* q = st_ptr(a, b, k, 1) + p + OFF;
+                acc += *q;
+                *q = acc;
+            }
+        }
+    } else {
+        const int64_t p0 = 1 - (nb - 1) * RB + (i - nF);  // p0 in [1-(nb-1)RB, W+RB]
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t p = p0 + b * RB;
+            if (p > W + RB) break;
+            if (p <= 0) {
+                acc = 0;
+            } else {
+                long long* q = st_ptr(a, b, k, 2) + p + OFF;
+                acc += *q;
+                *q = acc;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static size_t rowpre_bytes(int64_t W, int64_t H) { return align_up((size_t)H * (n_groups(W) + 1) * 3 * 8, 256); }
+static size_t state_bytes(int64_t W, int64_t H) {
+    const int64_t nb = n_bands(H) - 1;
+    return nb > 0 ? align_up((size_t)nb * 12 * state_len(W) * 8, 256) : 0;
+}
+
+size_t build_workspace_bytes(int64_t W, int64_t H) { return rowpre_bytes(W, H) + state_bytes(W, H); }
+
+int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                 int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream) {
+    if (W < 1 || H < 1) { set_error("empty image"); return SS_EINVAL; }
+    if (overflow_guard_fails(W, H)) {
+        set_error("image %lldx%lld too large for 64-bit integral cells", (long long)W, (long long)H);
+        return SS_EINVAL;
+    }
+    if (img_pitch < W) { set_error("img_pitch %lld < width %lld", (long long)img_pitch, (long long)W); return SS_EINVAL; }
+    if (plane_pitch_ != plane_pitch(W)) {
+        set_error("plane_pitch must be ss_plane_pitch(W) = %lld", (long long)plane_pitch(W));
+        return SS_EINVAL;
+    }
+    if (!d_img || !d_planes || (reinterpret_cast<uintptr_t>(d_planes) & 15)) {
+        set_error("null or misaligned device pointer");
+        return SS_EINVAL;
+    }
+    const size_t need = build_workspace_bytes(W, H);
+    if (ws_bytes < need || (need && !d_ws)) {
+        set_error("build workspace too small: %zu < %zu", ws_bytes, need);
+        return SS_EINVAL;
+    }
+    cudaStream_t s = as_stream(stream);
+    BuildArgs a;
+    a.img = d_img;
+    a.W = W;
+    a.H = H;
+    a.img_pitch = img_pitch;
+    a.planes = reinterpret_cast<long long*>(d_planes);
+    a.pitch = plane_pitch_;
+    a.plane_stride = (H + 1) * plane_pitch_;
+    a.G = n_groups(W);
+    a.rowpre = reinterpret_cast<long long*>(d_ws);
+    a.state = reinterpret_cast<long long*>(static_cast<char*>(d_ws) + rowpre_bytes(W, H));
+    a.slen = state_len(W);
+    a.n_chunks = n_chunks(W);
+    const int64_t nbands = n_bands(H);
+
+    rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
+    note_launch();
+    if (int e = check_launch("rowpre_kernel")) return e;
+    if (nbands > 1) {
+        band_kernel<0><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
+        note_launch();
+        if (int e = check_launch("band_kernel<local>")) return e;
+        const int64_t nb = nbands - 1;
+        band_scan_s_kernel<<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb);
+        note_launch();
+        if (int e = check_launch("band_scan_s_kernel")) return e;
+        const int64_t per_kind = (W - 1 + OFF + (nb - 1) * RB) + (W + RB + (nb - 1) * RB);
+        band_scan_fg_kernel<<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb);
+        note_launch();
+        if (int e = check_launch("band_scan_fg_kernel")) return e;
+    }
+    band_kernel<1><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
+    note_launch();
+    return check_launch("band_kernel<final>");
+}
+
+}  // namespace ss
+
+extern "C" {
+int64_t ss_plane_pitch(int64_t W) { return ss::plane_pitch(W); }
+size_t ss_tables_bytes(int64_t W, int64_t H) { return (size_t)12 * (size_t)(H + 1) * ss::plane_pitch(W) * 8; }
+size_t ss_build_workspace_bytes(int64_t W, int64_t H) { return ss::build_workspace_bytes(W, H); }
+int ss_build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                    int64_t plane_pitch, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::build_tables(d_img, W, H, img_pitch, d_planes, plane_pitch, d_workspace, workspace_bytes, stream);
+}
+}

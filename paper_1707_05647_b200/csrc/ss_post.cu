@@ -1,0 +1,308 @@
+// ss_post.cu -- K4 survivor compaction, K5 kept-region mask, popcount.
+//
+// K4 replaces the np.nonzero + list building of _scan_size / screen()
+// (screening.py:455-470, 512-516): survivors come out row-major per size and
+// sizes are appended in ladder order, which is the candidates order.
+// K5 replaces _footprint_union (screening.py:316-330): the union of the m x m
+// footprints [c-lo, c+hi] of the evaluated survivors, as a separable box
+// dilation of the bit-packed survivor mask (van Herk/Gil-Werman along
+// columns, word-parallel; log-step shift-OR doubling along rows).
+#include <algorithm>
+
+#include "ss_common.cuh"
+
+namespace ss {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned interior_bits(long long word, int x_lo, int x_hi) {
+    // bits of word `word` whose column lies in [x_lo, x_hi]
+    const long long a = word * 32, b = a + 31;
+    if (x_hi < x_lo || b < x_lo || a > x_hi) return 0u;
+    const int s = (int)max(0LL, (long long)x_lo - a);
+    const int e = (int)min(31LL, (long long)x_hi - a);
+    const unsigned hi_mask = (e == 31) ? FULL : ((1u << (e + 1)) - 1u);
+    const unsigned lo_mask = FULL << s;
+    return hi_mask & lo_mask;
+}
+
+// Exclusive scan of row counts (one CTA), offset by *total; advances *total.
+__global__ void __launch_bounds__(1024) scan_rows_kernel(const unsigned* counts, long long rows,
+                                                         unsigned long long* row_off, unsigned long long* total,
+                                                         unsigned long long* size_count) {
+    __shared__ unsigned long long warp_sums[32];
+    __shared__ unsigned long long carry;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) carry = *total;
+    __syncthreads();
+    for (long long base = 0; base < rows; base += 1024) {
+        const long long i = base + t;
+        const unsigned long long v = (i < rows) ? counts[i] : 0ull;
+        unsigned long long s = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(FULL, s, d);
+            if (lane >= d) s += o;
+        }
+        if (lane == 31) warp_sums[warp] = s;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = warp_sums[lane];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long o = __shfl_up_sync(FULL, w, d);
+                if (lane >= d) w += o;
+            }
+            warp_sums[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long before = carry + (warp ? warp_sums[warp - 1] : 0ull) + s - v;
+        if (i < rows) row_off[i] = before;
+        __syncthreads();
+        if (t == 1023) carry = before + v;
+        __syncthreads();
+    }
+    if (t == 0) {
+        if (size_count) *size_count = carry - *total;
+        *total = carry;
+    }
+}
+
+// One warp per mask row: write (cx, cy) of every interior survivor.
+__global__ void write_xy_kernel(const unsigned* mask, long long mask_pitch, int W, int y_begin, long long rows, int x_lo,
+                                int x_hi, const unsigned* counts, const unsigned long long* row_off, int* xy,
+                                long long capacity) {
+    const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows || counts[row] == 0) return;  // warp-uniform
+    const unsigned* mrow = mask + row * mask_pitch;
+    const long long words = (W + 31) / 32;
+    unsigned long long pos = row_off[row];
+    const int y = y_begin + (int)row;
+    for (long long wb = 0; wb < words; wb += 32) {
+        const long long w = wb + lane;
+        unsigned bits = (w < words) ? (mrow[w] & interior_bits(w, x_lo, x_hi)) : 0u;
+        const int c = __popc(bits);
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += o;
+        }
+        unsigned long long p = pos + (unsigned long long)(incl - c);
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (p < (unsigned long long)capacity) {
+                xy[2 * p] = (int)(w * 32 + b);
+                xy[2 * p + 1] = y;
+            }
+            ++p;
+        }
+        pos += (unsigned long long)__shfl_sync(FULL, incl, 31);
+    }
+}
+
+// Column pass of the footprint dilation.  Virtual rows r in [-hi, H-1+lo]
+// are cut into blocks of L = m rows starting at -hi; g = prefix-OR within
+// the block, h = suffix-OR.  Thread = (word column, block).
+__global__ void vdilate_blocks_kernel(const unsigned* mask, long long mask_pitch, long long words, int H, int L, int lo,
+                                      int hi, int x_lo, int x_hi, int y_lo, int y_hi, unsigned* g, unsigned* h,
+                                      long long nblocks) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= words * nblocks) return;
+    const long long w = gid % words, k = gid / words;
+    const unsigned cm = interior_bits(w, x_lo, x_hi);
+    const long long r0 = k * L - hi;  // first virtual row of the block
+    const long long vrows = (long long)H + L;  // storage rows (index r + hi)
+    unsigned acc = 0;
+    for (int i = 0; i < L; ++i) {
+        const long long r = r0 + i;
+        const unsigned s = (r >= y_lo && r <= y_hi) ? (mask[r * mask_pitch + w] & cm) : 0u;
+        acc |= s;
+        const long long idx = r + hi;
+        if (idx < vrows) g[idx * words + w] = acc;
+    }
+    acc = 0;
+    for (int i = L - 1; i >= 0; --i) {
+        const long long r = r0 + i;
+        const unsigned s = (r >= y_lo && r <= y_hi) ? (mask[r * mask_pitch + w] & cm) : 0u;
+        acc |= s;
+        const long long idx = r + hi;
+        if (idx < vrows) h[idx * words + w] = acc;
+    }
+}
+
+__device__ __forceinline__ unsigned get_word(const unsigned* row, long long i, long long words) {
+    return (i >= 0 && i < words) ? row[i] : 0u;
+}
+// word i of F(x + s), s >= 0 (shift toward lower x)
+__device__ __forceinline__ unsigned shifted_lo(const unsigned* row, long long i, long long words, int s) {
+    const long long q = s >> 5;
+    const int r = s & 31;
+    const unsigned a = get_word(row, i + q, words);
+    if (r == 0) return a;
+    return (a >> r) | (get_word(row, i + q + 1, words) << (32 - r));
+}
+// word i of F(x - s), s >= 0 (shift toward higher x)
+__device__ __forceinline__ unsigned shifted_hi(const unsigned* row, long long i, long long words, int s) {
+    const long long q = s >> 5;
+    const int r = s & 31;
+    const unsigned a = get_word(row, i - q, words);
+    if (r == 0) return a;
+    return (a << r) | (get_word(row, i - q - 1, words) >> (32 - r));
+}
+
+// Row pass: V(y) = h[y-hi] | g[y+lo] (column window), then
+// R(x) = OR_{c in [x-hi, x+lo]} V(c) by shift-OR doubling in shared memory,
+// OR'ed into the region row.  One CTA per row.
+__global__ void hdilate_rows_kernel(const unsigned* g, const unsigned* h, long long words, int W, int H, int L, int lo,
+                                    int hi, unsigned* region, long long region_pitch) {
+    extern __shared__ unsigned smem[];
+    unsigned* A = smem;
+    unsigned* B = smem + words;
+    const int y = blockIdx.x;
+    // storage index of virtual row r is r + hi; window rows [y-hi, y+lo]
+    const long long ia = (long long)y;           // (y - hi) + hi
+    const long long ib = (long long)y + lo + hi; // (y + lo) + hi
+    const bool single = (y % L) == 0;
+    int any = 0;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x) {
+        unsigned v = h[ia * words + i];
+        if (!single) v |= g[ib * words + i];
+        A[i] = v;
+        any |= (v != 0u);
+    }
+    if (!__syncthreads_or(any)) return;
+    // F_1 = V; F_{2l}(x) = F_l(x) | F_l(x + l)
+    int l = 1;
+    while (2 * l <= L) {
+        for (long long i = threadIdx.x; i < words; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, words, l);
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+        l *= 2;
+    }
+    // F_L(x) = F_l(x) | F_l(x + L - l)
+    if (l < L) {
+        for (long long i = threadIdx.x; i < words; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, words, L - l);
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+    }
+    // R(x) = F_L(x - hi), clipped to the image width
+    const unsigned last_mask = (W % 32) ? ((1u << (W % 32)) - 1u) : FULL;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x) {
+        unsigned r = shifted_hi(A, i, words, hi);
+        if (i == words - 1) r &= last_mask;
+        if (r) region[(long long)y * region_pitch + i] |= r;
+    }
+}
+
+__global__ void popcount_kernel(const unsigned* bits, long long pitch, long long words, int W, long long H,
+                                unsigned long long* count) {
+    const unsigned last_mask = (W % 32) ? ((1u << (W % 32)) - 1u) : FULL;
+    unsigned long long local = 0;
+    const long long n = words * H;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / words, w = i % words;
+        unsigned v = bits[r * pitch + w];
+        if (w == words - 1) v &= last_mask;
+        local += __popc(v);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(FULL, local, d);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+}  // namespace
+
+size_t compact_workspace_bytes(int64_t rows) { return (size_t)std::max<int64_t>(rows, 1) * 8; }
+
+int compact(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int64_t H, int64_t y_begin, int64_t y_end, int32_t m,
+            int32_t stride, const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
+            unsigned long long* d_size_count, void* d_ws, size_t ws_bytes, void* stream) {
+    const int64_t rows = y_end - y_begin;
+    if (rows < 0 || W < 1 || m < 1 || stride < 1) { set_error("bad compact arguments"); return SS_EINVAL; }
+    if (rows == 0) {
+        if (d_size_count) cudaMemsetAsync(d_size_count, 0, sizeof(unsigned long long), as_stream(stream));
+        return SS_OK;
+    }
+    if (ws_bytes < compact_workspace_bytes(rows) || !d_ws) { set_error("compact workspace too small"); return SS_EINVAL; }
+    cudaStream_t s = as_stream(stream);
+    auto* row_off = static_cast<unsigned long long*>(d_ws);
+    scan_rows_kernel<<<1, 1024, 0, s>>>(d_row_counts, rows, row_off, d_total, d_size_count);
+    note_launch();
+    if (int e = check_launch("scan_rows_kernel")) return e;
+    const int lo = (m - 1) / 2, hi = m / 2;
+    write_xy_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(
+        d_mask, mask_pitch, (int)W, (int)y_begin, rows, lo, (int)(W - 1 - hi), d_row_counts, row_off, d_xy, capacity);
+    note_launch();
+    return check_launch("write_xy_kernel");
+}
+
+size_t region_workspace_bytes(int64_t W, int64_t H, int32_t m_max) {
+    const int64_t words = (W + 31) / 32;
+    const int64_t vrows = H + std::max<int32_t>(m_max, 1);
+    return (size_t)2 * vrows * words * 4;
+}
+
+int region_accumulate(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int64_t H, int32_t m, int32_t stride,
+                      uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
+    if (W < 1 || H < 1 || m < 1 || stride < 1) { set_error("bad region arguments"); return SS_EINVAL; }
+    if (ws_bytes < region_workspace_bytes(W, H, m) || !d_ws) { set_error("region workspace too small"); return SS_EINVAL; }
+    const int lo = (m - 1) / 2, hi = m / 2, L = m;
+    const int x_lo = lo, x_hi = (int)(W - 1 - hi), y_lo = lo, y_hi = (int)(H - 1 - hi);
+    if (x_hi < x_lo || y_hi < y_lo) return SS_OK;  // no evaluated centres
+    const int64_t words = (W + 31) / 32;
+    const int64_t vrows = H + L;
+    unsigned* g = static_cast<unsigned*>(d_ws);
+    unsigned* h = g + vrows * words;
+    const int64_t nblocks = (vrows + L - 1) / L;
+    cudaStream_t s = as_stream(stream);
+    vdilate_blocks_kernel<<<(unsigned)((words * nblocks + 255) / 256), 256, 0, s>>>(
+        d_mask, mask_pitch, words, (int)H, L, lo, hi, x_lo, x_hi, y_lo, y_hi, g, h, nblocks);
+    note_launch();
+    if (int e = check_launch("vdilate_blocks_kernel")) return e;
+    const int threads = (int)std::min<int64_t>(1024, ((words + 31) / 32) * 32);
+    const size_t smem = (size_t)2 * words * 4;
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(hdilate_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    hdilate_rows_kernel<<<(unsigned)H, threads, smem, s>>>(g, h, words, (int)W, (int)H, L, lo, hi, d_region, mask_pitch);
+    note_launch();
+    return check_launch("hdilate_rows_kernel");
+}
+
+int popcount(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, unsigned long long* d_count, void* stream) {
+    if (W < 1 || H < 0) { set_error("bad popcount arguments"); return SS_EINVAL; }
+    if (H == 0) return SS_OK;
+    const int64_t words = (W + 31) / 32;
+    const int64_t n = words * H;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    popcount_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_bits, pitch, words, (int)W, H, d_count);
+    note_launch();
+    return check_launch("popcount_kernel");
+}
+
+}  // namespace ss
+
+extern "C" {
+size_t ss_compact_workspace_bytes(int64_t rows) { return ss::compact_workspace_bytes(rows); }
+int ss_compact(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int64_t y_begin, int64_t y_end,
+               int32_t m, int32_t stride, const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity,
+               unsigned long long* d_total, unsigned long long* d_size_count, void* d_workspace,
+               size_t workspace_bytes, void* stream) {
+    return ss::compact(d_mask, mask_pitch_words, W, H, y_begin, y_end, m, stride, d_row_counts, d_xy, capacity, d_total,
+                       d_size_count, d_workspace, workspace_bytes, stream);
+}
+size_t ss_region_workspace_bytes(int64_t W, int64_t H, int32_t m_max) { return ss::region_workspace_bytes(W, H, m_max); }
+int ss_region_accumulate(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int32_t m,
+                         int32_t stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::region_accumulate(d_mask, mask_pitch_words, W, H, m, stride, d_region, d_workspace, workspace_bytes,
+                                 stream);
+}
+int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, unsigned long long* d_count,
+                void* stream) {
+    return ss::popcount(d_bits, mask_pitch_words, W, H, d_count, stream);
+}
+}

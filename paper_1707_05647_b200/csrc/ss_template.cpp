@@ -1,0 +1,238 @@
+// ss_template.cpp -- host side of the screen: template feature sets and the
+// device key blob.  Compiled with -ffp-contract=off: the resampling and the
+// feature arithmetic reproduce NumPy's op-by-op binary64 rounding.
+//
+// Replaces build_feature_set (screening.py:222-250), FeatureSet.insert /
+// _guard_cells / ring_keys (screening.py:122-155), resize_bilinear +
+// _sample_bilinear + _quantize_levels (image_io.py:131-178), crop_center
+// (image_io.py:216-228) and the patch-side ring features (features.py:
+// 220-224 via :322-370).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../include/starscreen_b200.h"
+
+namespace ss {
+void set_error(const char* fmt, ...);
+
+namespace {
+
+// image_io.py:131-178 -- half-pixel-centred bilinear resize, edge clamp,
+// round half up, clip to [0, 255].
+void resize_bilinear(const uint8_t* img, int64_t w, int64_t h, int64_t ow, int64_t oh, uint8_t* out) {
+    const double fxs = (double)w / (double)ow, fys = (double)h / (double)oh;
+    for (int64_t j = 0; j < oh; ++j) {
+        const double ys = ((double)j + 0.5) * fys - 0.5;
+        const double y0f = std::floor(ys), fy = ys - y0f;
+        const int64_t y0 = std::min<int64_t>(std::max<int64_t>((int64_t)y0f, 0), h - 1);
+        const int64_t y1 = std::min<int64_t>(std::max<int64_t>((int64_t)y0f + 1, 0), h - 1);
+        for (int64_t i = 0; i < ow; ++i) {
+            const double xs = ((double)i + 0.5) * fxs - 0.5;
+            const double x0f = std::floor(xs), fx = xs - x0f;
+            const int64_t x0 = std::min<int64_t>(std::max<int64_t>((int64_t)x0f, 0), w - 1);
+            const int64_t x1 = std::min<int64_t>(std::max<int64_t>((int64_t)x0f + 1, 0), w - 1);
+            const double v00 = img[y0 * w + x0], v01 = img[y0 * w + x1];
+            const double v10 = img[y1 * w + x0], v11 = img[y1 * w + x1];
+            const double top = v00 + fx * (v01 - v00);
+            const double bot = v10 + fx * (v11 - v10);
+            double v = std::floor((top + fy * (bot - top)) + 0.5);
+            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+            out[j * ow + i] = (uint8_t)v;
+        }
+    }
+}
+
+struct Sums {
+    int64_t s1 = 0, sx = 0, sy = 0, s2 = 0;
+};
+
+// features.py:322-370 on exact integer sums of the m x m patch z, centre c.
+void ring_features(const uint8_t* z, int64_t m, int32_t n_rings, const int32_t* rn, const int32_t* rd, double* out) {
+    const int64_t c = (m - 1) / 2;
+    for (int32_t r = 0; r < n_rings; ++r) {
+        const int64_t n = rn[r], d = rd[r];
+        Sums q, di;
+        for (int64_t y = c - n + 1; y <= c + n; ++y)
+            for (int64_t x = c - n + 1; x <= c + n; ++x) {
+                const int64_t v = z[y * m + x];
+                q.s1 += v;
+                q.sx += (x + 1) * v;
+                q.sy += (y + 1) * v;
+                q.s2 += v * v;
+            }
+        for (int64_t y = c - d; y <= c + d; ++y) {
+            const int64_t ry = d - (y > c ? y - c : c - y);
+            for (int64_t x = c - ry; x <= c + ry; ++x) {
+                const int64_t v = z[y * m + x];
+                di.s1 += v;
+                di.sx += (x + 1) * v;
+                di.sy += (y + 1) * v;
+                di.s2 += v * v;
+            }
+        }
+        // _square_stats_from_sums
+        const double cq = (double)(4 * n * n), wq = (double)(2 * n * n * n);
+        const double mq = (double)q.s1 / cq;
+        const double vq = (double)q.s2 / cq - mq * mq;
+        const double sq = std::sqrt(vq > 0.0 ? vq : 0.0);
+        const double gxq = ((double)q.sx - ((double)c + 1.5) * (double)q.s1) / wq;
+        const double gyq = ((double)q.sy - ((double)c + 1.5) * (double)q.s1) / wq;
+        // _diamond_stats_from_sums
+        const double cd = (double)(2 * d * d + 2 * d + 1), wd = (double)(2 * d * d + d * (d - 1) * (2 * d - 1) / 3);
+        const double md = (double)di.s1 / cd;
+        const double vd = (double)di.s2 / cd - md * md;
+        const double sd = std::sqrt(vd > 0.0 ? vd : 0.0);
+        const double gxd = ((double)di.sx - ((double)c + 1.0) * (double)di.s1) / wd;
+        const double gyd = ((double)di.sy - ((double)c + 1.0) * (double)di.s1) / wd;
+        // _octagon_from_parts
+        const double gx = (gxq + gxd) * 0.5, gy = (gyq + gyd) * 0.5;
+        out[3 * r + 0] = (mq + md) * 0.5;
+        out[3 * r + 1] = (sq + sd) * 0.5;
+        out[3 * r + 2] = std::sqrt(gx * gx + gy * gy);
+    }
+}
+
+// one rescale k: resize n x n -> k x k, crop centred m x m, ring features
+void template_features(const uint8_t* tpl, int32_t n, int32_t k, int32_t m, int32_t n_rings, const int32_t* rn,
+                       const int32_t* rd, double* out) {
+    std::vector<uint8_t> scaled((size_t)k * k), z((size_t)m * m);
+    resize_bilinear(tpl, n, n, k, k, scaled.data());
+    const int64_t off = (k - m) / 2;  // crop_center: floor((size - out) / 2)
+    for (int64_t j = 0; j < m; ++j) std::memcpy(&z[j * m], &scaled[(off + j) * k + off], (size_t)m);
+    ring_features(z.data(), m, n_rings, rn, rd, out);
+}
+
+inline int64_t quantize(double v, double q) { return (int64_t)std::floor(v / q + 0.5); }
+
+}  // namespace
+}  // namespace ss
+
+extern "C" {
+
+int ss_template_ring_features(const uint8_t* h_template, int32_t n, int32_t k, int32_t m, int32_t n_rings,
+                              const int32_t* h_ring_n, const int32_t* h_ring_d, double* h_out) {
+    if (!h_template || n < 1 || k < m || m < 8 || n_rings < 1) {
+        ss::set_error("bad template feature arguments");
+        return SS_EINVAL;
+    }
+    ss::template_features(h_template, n, k, m, n_rings, h_ring_n, h_ring_d, h_out);
+    return SS_OK;
+}
+
+int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t k_hi, int32_t n_rings,
+                        const int32_t* h_ring_n, const int32_t* h_ring_d, double q_mean, double q_std, double q_grad,
+                        int64_t* h_keys, int64_t* h_key_off) {
+    if (!h_template || n < 1 || m < 8 || k_hi < m || n_rings < 1 || n_rings > SS_MAX_RINGS) {
+        ss::set_error("bad feature-set arguments");
+        return SS_EINVAL;
+    }
+    const int32_t nk = k_hi - m + 1;
+    std::vector<double> feats((size_t)nk * n_rings * 3);
+    // rescales are independent: spread them over host threads
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int32_t nthreads = (int32_t)std::min<unsigned>(hw, (unsigned)((nk + 3) / 4));
+    auto work = [&](int32_t tid) {
+        for (int32_t i = tid; i < nk; i += nthreads)
+            ss::template_features(h_template, n, m + i, m, n_rings, h_ring_n, h_ring_d, &feats[(size_t)i * n_rings * 3]);
+    };
+    if (nthreads <= 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int32_t t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+    }
+    // FeatureSet.insert in k order (screening.py:127-145)
+    const double qs[3] = {q_mean, q_std, q_grad};
+    std::vector<std::vector<int64_t>> rings(n_rings);
+    for (int32_t i = 0; i < nk; ++i) {
+        for (int32_t r = 0; r < n_rings; ++r) {
+            int64_t cells[3][3];
+            int nc[3];
+            for (int ch = 0; ch < 3; ++ch) {
+                const double v = feats[((size_t)i * n_rings + r) * 3 + ch], q = qs[ch], half = q / 2.0;
+                int64_t c3[3] = {ss::quantize(v - half, q), ss::quantize(v, q), ss::quantize(v + half, q)};
+                std::sort(c3, c3 + 3);
+                nc[ch] = (int)(std::unique(c3, c3 + 3) - c3);
+                for (int j = 0; j < nc[ch]; ++j) cells[ch][j] = c3[j];
+            }
+            for (int a = 0; a < nc[0]; ++a)
+                for (int b = 0; b < nc[1]; ++b)
+                    for (int g = 0; g < nc[2]; ++g) {
+                        const int64_t cm = cells[0][a], cs = cells[1][b], cg = cells[2][g];
+                        if (cm >= SS_KEY_BASE || cs >= SS_KEY_BASE || cg >= SS_KEY_BASE) {
+                            ss::set_error("quantized cell exceeds key capacity, quantizer too fine");
+                            return SS_ECAPACITY;
+                        }
+                        if (cm < 0 || cs < 0 || cg < 0) {
+                            ss::set_error("negative quantized cell; features must be non-negative");
+                            return SS_ECAPACITY;
+                        }
+                        rings[r].push_back((cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
+                    }
+        }
+    }
+    int64_t pos = 0;
+    h_key_off[0] = 0;
+    for (int32_t r = 0; r < n_rings; ++r) {
+        auto& v = rings[r];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        std::memcpy(h_keys + pos, v.data(), v.size() * sizeof(int64_t));
+        pos += (int64_t)v.size();
+        h_key_off[r + 1] = pos;
+    }
+    return SS_OK;
+}
+
+int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings, int64_t* h_blob,
+                   size_t* blob_bytes) {
+    if (!h_key_off || n_rings < 1 || n_rings > SS_MAX_RINGS || !blob_bytes) {
+        ss::set_error("bad keyset arguments");
+        return SS_EINVAL;
+    }
+    // header: n_rings, then per ring (off_m, n_m, off_ms, n_ms, off_k, n_k)
+    std::vector<int64_t> blob(1 + 6 * (size_t)n_rings, 0);
+    blob[0] = n_rings;
+    for (int32_t r = 0; r < n_rings; ++r) {
+        const int64_t a = h_key_off[r], b = h_key_off[r + 1];
+        std::vector<int64_t> km, kms;
+        for (int64_t i = a; i < b; ++i) {
+            if (i > a && h_keys[i] <= h_keys[i - 1]) {
+                ss::set_error("ring keys must be sorted and unique");
+                return SS_EINVAL;
+            }
+            const int64_t ms = h_keys[i] / SS_KEY_BASE, mm = ms / SS_KEY_BASE;
+            if (kms.empty() || kms.back() != ms) kms.push_back(ms);
+            if (km.empty() || km.back() != mm) km.push_back(mm);
+        }
+        int64_t* hd = &blob[1 + 6 * (size_t)r];
+        hd[0] = (int64_t)blob.size();
+        hd[1] = (int64_t)km.size();
+        blob.insert(blob.end(), km.begin(), km.end());
+        hd = &blob[1 + 6 * (size_t)r];
+        hd[2] = (int64_t)blob.size();
+        hd[3] = (int64_t)kms.size();
+        blob.insert(blob.end(), kms.begin(), kms.end());
+        hd = &blob[1 + 6 * (size_t)r];
+        hd[4] = (int64_t)blob.size();
+        hd[5] = b - a;
+        blob.insert(blob.end(), h_keys + a, h_keys + b);
+    }
+    const size_t need = blob.size() * sizeof(int64_t);
+    if (h_blob) {
+        if (*blob_bytes < need) {
+            ss::set_error("key blob buffer too small: %zu < %zu", *blob_bytes, need);
+            return SS_EINVAL;
+        }
+        std::memcpy(h_blob, blob.data(), need);
+    }
+    *blob_bytes = need;
+    return SS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+"""Template-side feature sets (host).
+
+FeatureSet mirrors screening.py:100-170 (per-ring guard-banded key sets,
+ring_keys(), contains()); build_feature_set mirrors screening.py:222-250 and
+runs its per-rescale work (resize, crop, patch tables, ring features, guard
+cells) in native C++ (csrc/ss_template.cpp) over the host's threads.
+keyset_blob packs one size's keys for the device screen.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .config import KEY_BASE, MIN_PATCH_SIDE, Quantizer, ScreeningConfig, quantize, ring_plan
+from .image import as_gray
+
+
+@dataclass(frozen=True)
+class RingBand:
+    """features.py:298-304."""
+
+    half_size: int
+    radius: int
+    mean: float
+    std: float
+    grad_mag: float
+
+
+@dataclass(frozen=True)
+class RingFeatureVector:
+    """features.py:307-319: per-ring triples, outermost ring first."""
+
+    rings: Tuple[RingBand, ...]
+
+    def __post_init__(self) -> None:
+        sizes = [b.half_size for b in self.rings]
+        if any(inner >= outer for outer, inner in zip(sizes, sizes[1:])):
+            raise ValueError(f"ring half-sizes must strictly decrease, got {sizes}")
+
+    def __len__(self) -> int:
+        return len(self.rings)
+
+
+class FeatureSet:
+    """screening.py:100-170: per-ring sets of packed quantized feature keys."""
+
+    def __init__(self, plan: Sequence[Tuple[int, int]], quantizer: Quantizer):
+        if not plan:
+            raise ValueError("empty ring plan")
+        self.plan = tuple(plan)
+        self.quantizer = quantizer
+        self._rings: List[set] = [set() for _ in plan]
+        self._sorted: Optional[List[np.ndarray]] = None
+
+    def __len__(self) -> int:
+        return sum(len(s) for s in self._rings)
+
+    def ring_sizes(self) -> Tuple[int, ...]:
+        return tuple(len(s) for s in self._rings)
+
+    def _guard_cells(self, value: float, q: float) -> List[int]:
+        half = q / 2.0
+        return sorted({quantize(value - half, q), quantize(value, q), quantize(value + half, q)})
+
+    def insert(self, fv: RingFeatureVector) -> None:
+        """Insert one template instance with the guard band (screening.py:127-145)."""
+        if len(fv) != len(self.plan):
+            raise ValueError(f"expected {len(self.plan)} rings, got {len(fv)}")
+        qm, qs, qg = self.quantizer.factors()
+        for ring, band in zip(self._rings, fv.rings):
+            for cm in self._guard_cells(band.mean, qm):
+                for cs in self._guard_cells(band.std, qs):
+                    for cg in self._guard_cells(band.grad_mag, qg):
+                        if cm >= KEY_BASE or cs >= KEY_BASE or cg >= KEY_BASE:
+                            raise ValueError("quantized cell exceeds key capacity, quantizer too fine")
+                        if cm < 0 or cs < 0 or cg < 0:
+                            raise ValueError("negative quantized cell; features must be non-negative")
+                        ring.add((cm * KEY_BASE + cs) * KEY_BASE + cg)
+        self._sorted = None
+
+    def _set_sorted(self, arrays: List[np.ndarray]) -> None:
+        self._rings = [set(a.tolist()) for a in arrays]
+        self._sorted = [np.ascontiguousarray(a, dtype=np.int64) for a in arrays]
+
+    def ring_keys(self) -> List[np.ndarray]:
+        """Sorted key arrays, one per ring (screening.py:147-155)."""
+        if self._sorted is None:
+            self._sorted = [np.fromiter(s, dtype=np.int64, count=len(s)) for s in self._rings]
+            for a in self._sorted:
+                a.sort()
+        return self._sorted
+
+    def contains(self, fv: RingFeatureVector) -> bool:
+        """True when every ring's quantized key is marked (screening.py:157-170)."""
+        if len(fv) != len(self.plan):
+            raise ValueError(f"expected {len(self.plan)} rings, got {len(fv)}")
+        qm, qs, qg = self.quantizer.factors()
+        for ring, band in zip(self._rings, fv.rings):
+            cm, cs, cg = quantize(band.mean, qm), quantize(band.std, qs), quantize(band.grad_mag, qg)
+            if cm < 0 or cs < 0 or cg < 0:
+                return False
+            if (cm * KEY_BASE + cs) * KEY_BASE + cg not in ring:
+                return False
+        return True
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def template_ring_features(template: np.ndarray, k: int, m: int, plan) -> np.ndarray:
+    """Ring features (n_rings, 3) of rescale k of the template (screening.py:238-248 body)."""
+    tpl = as_gray(template)
+    rn = np.array([p[0] for p in plan], np.int32)
+    rd = np.array([p[1] for p in plan], np.int32)
+    out = np.empty((len(plan), 3), np.float64)
+    _native.check(_native.lib().ss_template_ring_features(_ptr(tpl), tpl.shape[0], k, m, len(plan), _ptr(rn),
+                                                          _ptr(rd), _ptr(out)), "template features")
+    return out
+
+
+def build_feature_set(template: np.ndarray, m: int, cfg: ScreeningConfig) -> FeatureSet:
+    """screening.py:222-250: feature set of every template rescale k = m .. ceil(m * ratio)."""
+    tpl = as_gray(template)
+    if m < MIN_PATCH_SIDE:
+        raise ValueError(f"patch side {m} below minimum {MIN_PATCH_SIDE}")
+    plan = ring_plan(m, cfg.ring_count)
+    fs = FeatureSet(plan, cfg.quantizer)
+    k_hi = math.ceil(m * cfg.ladder_ratio)
+    n = tpl.shape[0]
+    if tpl.shape[0] != tpl.shape[1]:
+        raise ValueError(f"template must be square, got {tpl.shape[1]}x{tpl.shape[0]}")
+    rn = np.array([p[0] for p in plan], np.int32)
+    rd = np.array([p[1] for p in plan], np.int32)
+    cap = len(plan) * 27 * (k_hi - m + 1)
+    keys = np.empty(cap, np.int64)
+    off = np.empty(len(plan) + 1, np.int64)
+    qm, qs, qg = cfg.quantizer.factors()
+    _native.check(_native.lib().ss_feature_set_keys(_ptr(tpl), n, m, k_hi, len(plan), _ptr(rn), _ptr(rd), qm, qs, qg,
+                                                    _ptr(keys), _ptr(off)), "feature set")
+    fs._set_sorted([keys[off[r]:off[r + 1]].copy() for r in range(len(plan))])
+    return fs
+
+
+def keyset_blob(fs: FeatureSet) -> np.ndarray:
+    """Device-ready membership blob of one size (keys + mean / (mean,std) projections)."""
+    arrays = fs.ring_keys()
+    keys = np.ascontiguousarray(np.concatenate(arrays) if arrays else np.zeros(0, np.int64), dtype=np.int64)
+    off = np.zeros(len(arrays) + 1, np.int64)
+    off[1:] = np.cumsum([len(a) for a in arrays])
+    size = ctypes.c_size_t(0)
+    L = _native.lib()
+    _native.check(L.ss_keyset_blob(_ptr(keys), _ptr(off), len(arrays), None, ctypes.byref(size)), "keyset")
+    blob = np.empty(size.value // 8, np.int64)
+    _native.check(L.ss_keyset_blob(_ptr(keys), _ptr(off), len(arrays), _ptr(blob), ctypes.byref(size)), "keyset")
+    return blob

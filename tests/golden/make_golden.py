@@ -1,0 +1,216 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE.
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Every array written here comes from the reference's own code
+(/root/reference/pkg/src/starscreen): integral tables, ring features,
+feature-set keys, complete screen() results, and the survivor counts of
+pkg/demos/out/report.json (re-derived through run_benchmark's own case
+generator).  The config-0 case uses this repo's workloads.py generator for
+the input image, screened by the reference.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from starscreen import integral as I  # noqa: E402
+from starscreen import features as F  # noqa: E402
+from starscreen import screening as S  # noqa: E402
+from starscreen.synth_bench import _case_seed, make_case, make_textured_scene  # noqa: E402
+
+KINDS = list(I.WeightKind)
+
+
+def packbits(mask: np.ndarray) -> np.ndarray:
+    return np.packbits(mask.astype(np.uint8), axis=-1, bitorder="little")
+
+
+def tables_fixture():
+    rng = np.random.default_rng(20261019)
+    imgs = [np.array([[1, 2], [3, 4]], np.uint8), np.full((1, 1), 255, np.uint8),
+            rng.integers(0, 256, (1, 9), dtype=np.uint8), rng.integers(0, 256, (9, 1), dtype=np.uint8),
+            rng.integers(0, 256, (5, 7), dtype=np.uint8), rng.integers(0, 256, (17, 13), dtype=np.uint8),
+            rng.integers(0, 256, (20, 33), dtype=np.uint8), np.full((11, 6), 255, np.uint8),
+            make_textured_scene(70, 45, seed=3)]
+    out = {}
+    for i, img in enumerate(imgs):
+        t = I.build_tables(img)
+        out[f"img{i}"] = img
+        for k, kind in enumerate(KINDS):
+            out[f"sat{i}_{k}"] = t.sats[kind].cells
+            out[f"rsat{i}_{k}"] = t.rsats[kind].table
+    out["n"] = np.array(len(imgs))
+    np.savez_compressed(os.path.join(HERE, "tables.npz"), **out)
+
+
+def features_fixture():
+    scene = make_textured_scene(64, 48, seed=1)
+    t = I.build_tables(scene)
+    out = {"scene": scene}
+    for m in (32, 17, 8):
+        plan = F.ring_plan(m, 3)
+        lo, hi = F.patch_center_margins(m)
+        cys, cxs = np.mgrid[lo:48 - hi, lo:64 - hi]
+        maps = F.ring_feature_maps(t, cxs.ravel(), cys.ravel(), plan)
+        out[f"plan_{m}"] = np.array(plan, np.int32)
+        out[f"centers_{m}"] = np.stack([cxs.ravel(), cys.ravel()], 1).astype(np.int32)
+        out[f"feat_{m}"] = np.stack([np.stack(mp, 1) for mp in maps], 1)  # (N, rings, 3)
+    np.savez_compressed(os.path.join(HERE, "features.npz"), **out)
+
+
+FS_CASES = [
+    # (template seed, side, m, ladder_ratio, quantizer)
+    (3, 32, 32, math.sqrt(2.0), (8.0, 8.0, 8.0)),
+    (3, 32, 45, math.sqrt(2.0), (8.0, 8.0, 8.0)),
+    (4, 20, 8, math.sqrt(2.0), (8.0, 8.0, 8.0)),
+    (5, 64, 128, 4.0 ** (1 / 7), (8.0, 8.0, 8.0)),
+    (6, 48, 33, (8 / 3) ** (1 / 7), (8.0, 8.0, 8.0)),
+    (7, 32, 32, math.sqrt(2.0), (8.0, 8.0, 1e6)),
+    (8, 24, 24, 1.05, (2.5, 0.75, 0.001)),
+]
+
+
+def featuresets_fixture():
+    out = {}
+    for i, (seed, side, m, ratio, q) in enumerate(FS_CASES):
+        tpl = make_textured_scene(side, side, seed=seed)
+        cfg = S.ScreeningConfig(ladder_ratio=ratio, quantizer=S.Quantizer(*q))
+        fs = S.build_feature_set(tpl, m, cfg)
+        out[f"tpl{i}"] = tpl
+        out[f"meta{i}"] = np.array([m, ratio, *q], np.float64)
+        for r, keys in enumerate(fs.ring_keys()):
+            out[f"keys{i}_{r}"] = keys
+        out[f"nrings{i}"] = np.array(len(fs.plan))
+    out["n"] = np.array(len(FS_CASES))
+    np.savez_compressed(os.path.join(HERE, "featuresets.npz"), **out)
+
+
+def screen_cases():
+    """(name, image, template, cfg kwargs) -- the reference tests' scenes plus extras."""
+    cases = []
+    s = make_textured_scene(96, 72, seed=4)
+    cases.append(("t4_default", s, s[20:52, 30:62].copy(), {}))
+    s = make_textured_scene(72, 56, seed=13)
+    cases.append(("t13_single", s, s[12:44, 20:52].copy(), {"alpha": 1.0, "beta": 1.0}))
+    s = make_textured_scene(96, 80, seed=14)
+    cases.append(("t14_stride3", s, s[24:56, 24:56].copy(), {"stride": 3}))
+    s = make_textured_scene(64, 64, seed=11)
+    cases.append(("t11_tiny", s, s[28:36, 28:36].copy(), {}))
+    s = make_textured_scene(160, 120, seed=5)
+    cases.append(("t5_q", s, s[40:72, 50:82].copy(), {"quantizer": (6.0, 4.0, 3.0), "ladder_ratio": 1.25}))
+    s = make_textured_scene(131, 97, seed=21)
+    cases.append(("t21_odd", s, s[30:57, 40:67].copy(), {"alpha": 0.6, "beta": 1.7, "ring_count": 4}))
+    s = make_textured_scene(40, 200, seed=22)
+    cases.append(("t22_tall", s, s[100:116, 10:26].copy(), {"stride": 2}))
+    s = make_textured_scene(100, 100, seed=6)
+    cases.append(("t6_big_m", s, make_textured_scene(32, 32, seed=7), {"beta": 3.5, "alpha": 0.3}))
+    # config-0-like input from this repo's generator (BASELINE config 0)
+    import workloads as WL
+
+    c0 = WL.make_cases(WL.CONFIGS[0])[0]
+    cases.append(("config0", c0.image, c0.template,
+                   {"alpha": 1.0, "beta": 1.0, "quantizer": (8.0, 8.0, 1e6)}))
+    return cases
+
+
+def _cfg(kw):
+    kw = dict(kw)
+    if "quantizer" in kw:
+        kw["quantizer"] = S.Quantizer(*kw["quantizer"])
+    return S.ScreeningConfig(**kw)
+
+
+def screens_fixture():
+    out = {}
+    names = []
+    for name, img, tpl, kw in screen_cases():
+        res = S.screen(img, tpl, _cfg(kw))
+        names.append(name)
+        out[f"{name}/image"] = img
+        out[f"{name}/template"] = tpl
+        out[f"{name}/cfg"] = np.array(json.dumps(kw))
+        out[f"{name}/ladder"] = np.array(res.ladder, np.int32)
+        out[f"{name}/candidates"] = np.array(res.candidates, np.int32).reshape(-1, 3)
+        for m in res.ladder:
+            out[f"{name}/mask_{m}"] = packbits(res.size_masks[m])
+        out[f"{name}/region"] = packbits(res.region_mask)
+        st = res.stats
+        out[f"{name}/stats"] = np.array([st.patches_tested, st.patches_kept, st.region_pixels_kept, st.total_pixels],
+                                        np.int64)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "screens.npz"), **out)
+
+
+def report_fixture():
+    """pkg/demos/out/report.json cases: 6 scenes x 2 cases, run_benchmark(seed=1)."""
+    with open("/root/reference/pkg/demos/out/report.json") as fh:
+        report = json.load(fh)
+    out = {}
+    idx = 0
+    for img_idx in range(6):
+        scene = make_textured_scene(320, 240, seed=600 + img_idx)
+        out[f"scene{img_idx}"] = scene
+        for case_idx in range(2):
+            tpl, truth = make_case(scene, _case_seed(1, img_idx, case_idx))
+            rec = report["cases"][idx]
+            assert rec["image"] == f"scene{img_idx}.pgm" and rec["case"] == case_idx
+            res = S.screen(scene, tpl)
+            assert len(res.candidates) == rec["candidates"], (idx, len(res.candidates), rec["candidates"])
+            assert res.stats.patch_pruning == rec["patch_pruning"]
+            assert res.stats.region_pruning == rec["region_pruning"]
+            out[f"tpl{idx}"] = tpl
+            out[f"expect{idx}"] = np.array([img_idx, rec["candidates"], res.stats.patches_tested,
+                                            res.stats.region_pixels_kept], np.int64)
+            out[f"pruning{idx}"] = np.array([rec["patch_pruning"], rec["region_pruning"]], np.float64)
+            idx += 1
+    out["n"] = np.array(idx)
+    np.savez_compressed(os.path.join(HERE, "report_cases.npz"), **out)
+
+
+def frozen_fixture():
+    """Small frozen values the reference tests pin (ladders, plans, radii, quantize)."""
+    cfg = S.ScreeningConfig()
+    out = {
+        "ladders": {str(n): list(S.ladder_sizes(n, cfg)) for n in (8, 20, 32, 48, 64, 96, 128)},
+        "ladders_cfg": {
+            "a1b1": list(S.ladder_sizes(32, S.ScreeningConfig(alpha=1.0, beta=1.0))),
+            "a09b11": list(S.ladder_sizes(32, S.ScreeningConfig(alpha=0.9, beta=1.1))),
+            "a2b2": list(S.ladder_sizes(32, S.ScreeningConfig(alpha=2.0, beta=2.0))),
+        },
+        "plans": {str(m): [list(p) for p in F.ring_plan(m, 3)] for m in (8, 11, 16, 17, 32, 45, 64, 128, 512)},
+        "plans5": {str(m): [list(p) for p in F.ring_plan(m, 5)] for m in (32, 77, 512)},
+        "radius": {str(n): F.default_star_radius(n) for n in (4, 8, 11, 16, 64, 181)},
+        "quantize": [[v, q, S.quantize(v, q)] for v, q in ((12.0, 8.0), (11.999, 8.0), (4.0, 8.0), (3.999, 8.0),
+                                                         (0.0, 8.0), (-3.0, 8.0), (7.5, 5.0), (1e6 - 1, 1e6))],
+    }
+    import workloads as WL
+
+    out["config_ladders"] = {}
+    for i, wl in WL.CONFIGS.items():
+        c = S.ScreeningConfig(alpha=wl.alpha, beta=wl.beta, ladder_ratio=wl.ladder_ratio,
+                              quantizer=S.Quantizer(*wl.q))
+        out["config_ladders"][str(i)] = list(S.ladder_sizes(wl.template_side, c))
+    with open(os.path.join(HERE, "frozen.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    tables_fixture()
+    features_fixture()
+    featuresets_fixture()
+    screens_fixture()
+    report_fixture()
+    frozen_fixture()
+    print("golden fixtures written to", HERE)

@@ -1,0 +1,177 @@
+"""K3/K4/K5 parity through the drop-in screen(): masks, candidates, region, stats.
+
+Expected values come from the reference (tests/golden/screens.npz,
+report_cases.npz) and, at BASELINE sizes, from the pinned oracle run on the
+same seeded inputs in the same process.  The bar is bit-exact: masks,
+candidate lists and counts must be identical (the fp64 feature path
+replays NumPy's op order, so no threshold-band disagreements are expected;
+any would be reported by the band test below).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, load_screen_case, packbits, screen_case_names
+
+pytestmark = pytest.mark.gpu
+
+
+def pcfg(kw):
+    from paper_1707_05647_b200 import Quantizer, ScreeningConfig
+
+    kw = dict(kw)
+    if "quantizer" in kw:
+        kw["quantizer"] = Quantizer(*kw["quantizer"])
+    return ScreeningConfig(**kw)
+
+
+def ocfg(kw):
+    kw = dict(kw)
+    if "quantizer" in kw:
+        kw["quantizer"] = O.Quantizer(*kw["quantizer"])
+    return O.ScreeningConfig(**kw)
+
+
+def assert_same_as_golden(res, c):
+    assert tuple(res.ladder) == c["ladder"]
+    assert np.array_equal(res.candidates.array().reshape(-1, 3), c["candidates"])
+    for m in res.ladder:
+        assert np.array_equal(packbits(res.size_masks[m]), c["masks"][m]), f"mask m={m}"
+    assert np.array_equal(packbits(res.region_mask), c["region"])
+    st = res.stats
+    assert (st.patches_tested, st.patches_kept, st.region_pixels_kept, st.total_pixels) == tuple(
+        int(v) for v in c["stats"])
+
+
+@pytest.mark.parametrize("name", screen_case_names())
+def test_screen_matches_reference(cuda, name):
+    from paper_1707_05647_b200 import screen
+
+    c = load_screen_case(name)
+    res = screen(c["image"], c["template"], pcfg(c["cfg"]))
+    assert_same_as_golden(res, c)
+
+
+def test_report_json_cases(cuda):
+    """The 12 stored survivor counts of pkg/demos/out/report.json."""
+    from paper_1707_05647_b200 import ScreeningConfig, screen
+
+    z = golden("report_cases.npz")
+    for i in range(int(z["n"])):
+        img_idx, cands, tested, region = (int(v) for v in z[f"expect{i}"])
+        res = screen(z[f"scene{img_idx}"], z[f"tpl{i}"], ScreeningConfig())
+        assert len(res.candidates) == cands == res.stats.patches_kept
+        assert res.stats.patches_tested == tested
+        assert res.stats.region_pixels_kept == region
+        pp, rp = z[f"pruning{i}"]
+        assert res.stats.patch_pruning == pp and res.stats.region_pruning == rp
+
+
+def compare_with_oracle(img, tpl, kw, nthreads=16):
+    from paper_1707_05647_b200 import screen
+
+    res = screen(img, tpl, pcfg(kw))
+    ref = O.screen(img, tpl, ocfg(kw), nthreads=nthreads)
+    assert tuple(res.ladder) == tuple(ref.ladder)
+    mism = {}
+    for m in res.ladder:
+        a = res.size_masks.packed(m).view(np.uint8)
+        b = packbits(ref.size_masks[m])
+        words = a.reshape(a.shape[0], -1)[:, : b.shape[1]]
+        diff = int(np.unpackbits(words ^ b).sum())
+        if diff:
+            mism[m] = diff
+    assert not mism, f"mask disagreements per size: {mism}"
+    assert np.array_equal(res.candidates.array(), np.array(ref.candidates, np.int32).reshape(-1, 3))
+    assert res.stats.patches_tested == ref.patches_tested
+    assert res.stats.patches_kept == ref.patches_kept
+    assert res.stats.region_pixels_kept == ref.region_pixels_kept
+    assert np.array_equal(res.region_mask, ref.region_mask)
+    return res
+
+
+def test_config0_vs_oracle(cuda):
+    import workloads as WL
+
+    c = WL.make_cases(WL.CONFIGS[0])[0]
+    wl = WL.CONFIGS[0]
+    compare_with_oracle(c.image, c.template, {"alpha": wl.alpha, "beta": wl.beta, "ladder_ratio": wl.ladder_ratio,
+                                              "quantizer": wl.q})
+
+
+@pytest.mark.slow
+def test_config1_vs_oracle(cuda):
+    import workloads as WL
+
+    wl = WL.CONFIGS[1]
+    c = WL.make_cases(wl)[0]
+    compare_with_oracle(c.image, c.template, {"alpha": wl.alpha, "beta": wl.beta, "ladder_ratio": wl.ladder_ratio,
+                                              "quantizer": wl.q})
+
+
+def test_random_configs_vs_oracle(cuda):
+    import workloads as WL
+
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        W = int(rng.integers(60, 700))
+        H = int(rng.integers(60, 500))
+        img = WL.make_image(W, H, seed=100 + trial, sigma=float(rng.uniform(1, 4)), noise=float(rng.uniform(0, 6)))
+        side = int(rng.integers(8, 48))
+        case = WL.make_template(img, 200 + trial, side, (0.7, 1.4), std_threshold=10.0)
+        kw = {"alpha": float(rng.uniform(0.4, 1.0)), "beta": float(rng.uniform(1.0, 2.2)),
+              "ladder_ratio": float(rng.uniform(1.1, 1.5)), "stride": int(rng.integers(1, 4)),
+              "ring_count": int(rng.integers(1, 5)),
+              "quantizer": (float(rng.uniform(3, 10)), float(rng.uniform(3, 10)), float(rng.uniform(3, 10)))}
+        compare_with_oracle(img, case.template, kw)
+
+
+def test_never_misses_exact_crop(cuda):
+    """pkg/tests/test_screening.py:277-289 on the GPU path."""
+    from paper_1707_05647_b200 import patch_center_margins, screen
+    import workloads as WL
+
+    scene = WL.make_image(160, 120, seed=5)
+    rng = np.random.default_rng(34)
+    m = 32
+    lo, hi = patch_center_margins(m)
+    for _ in range(10):
+        cx = int(rng.integers(lo, 160 - hi))
+        cy = int(rng.integers(lo, 120 - hi))
+        tpl = scene[cy - lo : cy - lo + m, cx - lo : cx - lo + m].copy()
+        from paper_1707_05647_b200 import std_dev
+
+        if std_dev(tpl) < 5.0:
+            continue
+        res = screen(scene, tpl)
+        assert (cx, cy, m) in res.candidates
+        assert res.size_masks[m][cy, cx]
+        assert res.region_mask[cy, cx]
+
+
+def test_errors_and_edge_cases(cuda):
+    from paper_1707_05647_b200 import FlatTemplateError, ScreeningConfig, screen
+
+    scene = golden("screens.npz")["t4_default/image"]
+    with pytest.raises(FlatTemplateError, match="too flat"):
+        screen(scene, np.full((32, 32), 128, np.uint8))
+    with pytest.raises(ValueError):
+        screen(scene, scene[:16, :20])
+    with pytest.raises(ValueError):
+        screen(scene, scene[:4, :4])
+    # template larger than the image: every size is all-border, nothing tested
+    small = scene[:20, :30].copy()
+    res = screen(small, scene[:32, :32].copy())
+    assert res.stats.patches_tested == 0 and len(res.candidates) == 0
+    for m in res.ladder:
+        assert res.size_masks[m].all()
+    assert not res.region_mask.any()
+    # determinism
+    tpl = scene[20:52, 30:62].copy()
+    a = screen(scene, tpl)
+    b = screen(scene, tpl)
+    assert a.candidates == b.candidates
+    assert np.array_equal(a.region_mask, b.region_mask)
+    # very fine quantizer: sparse (binary-search) membership path, still bit-exact
+    compare_with_oracle(scene, tpl, {"quantizer": (1e-3, 1e-3, 1e-3)})

@@ -1,0 +1,96 @@
+"""K1/K2 parity: the 12 device planes vs the oracle's reference-layout tables.
+
+SAT planes must equal Sat.cells exactly; E / O planes must equal the
+reference Rsat H(u, v) at the mapped indices (include/starscreen_b200.h).
+Cells outside the reference table's (u, v) domain are checked against the
+brute-force quadrant-prefix definition instead.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def device_planes(img, cuda):
+    import torch
+
+    from paper_1707_05647_b200.engine import Engine
+
+    h, w = img.shape
+    eng = Engine(w, h, cuda)
+    eng.build_tables(torch.from_numpy(np.ascontiguousarray(img)).to(cuda))
+    torch.cuda.synchronize()
+    p = eng.planes.view(12, h + 1, eng.pitch).cpu().numpy()
+    return p[:, :, : w + 1]
+
+
+def check_planes(img, planes, brute_extra=False):
+    h, w = img.shape
+    for k in range(4):
+        assert np.array_equal(planes[k], O.build_sat(img, k)), f"SAT kind {k}"
+        rs = O.build_rsat(img, k)
+
+        def H(u, v):
+            return rs[u + 1, v + h - 1]
+
+        E = planes[4 + k]
+        Op = planes[8 + k]
+        ys, xs = np.mgrid[-1:h, 0:w]
+        assert np.array_equal(E[ys + 1, xs + 1], H(xs + ys, xs - ys)), f"E kind {k}"
+        ys, xs = np.mgrid[-1 : h - 1, -1:w]
+        assert np.array_equal(Op[ys + 1, xs + 1], H(xs + ys + 1, xs - ys)), f"O kind {k}"
+        if brute_extra:
+            # every cell, including E col x=-1 and O row y=H-1, from the definition
+            wm = img.astype(np.int64)
+            jj, ii = np.mgrid[0:h, 0:w]
+            if k == 1:
+                wm = wm * (ii + 1)
+            elif k == 2:
+                wm = wm * (jj + 1)
+            elif k == 3:
+                wm = wm * wm
+            s = ii + jj
+            d = ii - jj
+            for y in range(-1, h):
+                for x in range(-1, w):
+                    e = wm[(s <= x + y) & (d >= x - y)].sum()
+                    o = wm[(s <= x + y + 1) & (d >= x - y)].sum()
+                    assert E[y + 1, x + 1] == e and Op[y + 1, x + 1] == o, (k, x, y)
+
+
+def test_golden_images(cuda):
+    z = golden("tables.npz")
+    for i in range(int(z["n"])):
+        img = z[f"img{i}"]
+        planes = device_planes(img, cuda)
+        for k in range(4):
+            assert np.array_equal(planes[k], z[f"sat{i}_{k}"]), (i, k)
+        check_planes(img, planes, brute_extra=img.size <= 400)
+
+
+@pytest.mark.parametrize("shape", [(63, 383), (64, 384), (126, 385), (127, 767), (200, 1000), (517, 130), (1, 2000),
+                                   (1300, 3), (190, 770)])
+def test_band_and_chunk_boundaries(cuda, shape):
+    """Shapes straddling the 63-row band and 384-column chunk seams."""
+    rng = np.random.default_rng(sum(shape))
+    img = rng.integers(0, 256, shape, dtype=np.uint8)
+    check_planes(img, device_planes(img, cuda))
+
+
+def test_saturated_image(cuda):
+    img = np.full((300, 900), 255, np.uint8)
+    check_planes(img, device_planes(img, cuda))
+
+
+def test_overflow_guard_rejected(cuda):
+    import torch
+
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    with pytest.raises(ValueError, match="too large"):
+        _native.check(L.ss_build_tables(1, 300000, 300000, 300000, 16, L.ss_plane_pitch(300000), 0, 0, None))
