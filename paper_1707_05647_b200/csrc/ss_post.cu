@@ -155,44 +155,48 @@ __device__ __forceinline__ unsigned shifted_hi(const unsigned* row, long long i,
 }
 
 // Row pass: V(y) = h[y-hi] | g[y+lo] (column window), then
-// R(x) = OR_{c in [x-hi, x+lo]} V(c) by shift-OR doubling in shared memory,
-// OR'ed into the region row.  One CTA per row.
-__global__ void hdilate_rows_kernel(const unsigned* g, const unsigned* h, long long words, int W, int H, int L, int lo,
-                                    int hi, unsigned* region, long long region_pitch) {
+// R(x) = OR_{c in [x-hi, x+lo]} V(c) = F_L(x - hi) with F_l(x) = OR V[x, x+l-1]
+// built by shift-OR doubling in shared memory, OR'ed into the region row.
+// The row is padded by P words on both sides so F at x < 0 is kept.  One CTA
+// per row.
+__global__ void hdilate_rows_kernel(const unsigned* g, const unsigned* h, long long words, long long P, int W, int H,
+                                    int L, int lo, int hi, unsigned* region, long long region_pitch) {
     extern __shared__ unsigned smem[];
+    const long long ext = words + 2 * P;
     unsigned* A = smem;
-    unsigned* B = smem + words;
+    unsigned* B = smem + ext;
     const int y = blockIdx.x;
     // storage index of virtual row r is r + hi; window rows [y-hi, y+lo]
-    const long long ia = (long long)y;           // (y - hi) + hi
-    const long long ib = (long long)y + lo + hi; // (y + lo) + hi
+    const long long ia = (long long)y;            // (y - hi) + hi
+    const long long ib = (long long)y + lo + hi;  // (y + lo) + hi
     const bool single = (y % L) == 0;
     int any = 0;
-    for (long long i = threadIdx.x; i < words; i += blockDim.x) {
-        unsigned v = h[ia * words + i];
-        if (!single) v |= g[ib * words + i];
+    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
+        const long long wi = i - P;
+        unsigned v = 0;
+        if (wi >= 0 && wi < words) {
+            v = h[ia * words + wi];
+            if (!single) v |= g[ib * words + wi];
+        }
         A[i] = v;
         any |= (v != 0u);
     }
     if (!__syncthreads_or(any)) return;
-    // F_1 = V; F_{2l}(x) = F_l(x) | F_l(x + l)
     int l = 1;
-    while (2 * l <= L) {
-        for (long long i = threadIdx.x; i < words; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, words, l);
+    while (2 * l <= L) {  // F_{2l}(x) = F_l(x) | F_l(x + l)
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, l);
         __syncthreads();
         unsigned* tmp = A; A = B; B = tmp;
         l *= 2;
     }
-    // F_L(x) = F_l(x) | F_l(x + L - l)
-    if (l < L) {
-        for (long long i = threadIdx.x; i < words; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, words, L - l);
+    if (l < L) {  // F_L(x) = F_l(x) | F_l(x + L - l), L - l < l
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, L - l);
         __syncthreads();
         unsigned* tmp = A; A = B; B = tmp;
     }
-    // R(x) = F_L(x - hi), clipped to the image width
     const unsigned last_mask = (W % 32) ? ((1u << (W % 32)) - 1u) : FULL;
     for (long long i = threadIdx.x; i < words; i += blockDim.x) {
-        unsigned r = shifted_hi(A, i, words, hi);
+        unsigned r = shifted_hi(A, i + P, ext, hi);  // F_L(x - hi)
         if (i == words - 1) r &= last_mask;
         if (r) region[(long long)y * region_pitch + i] |= r;
     }
@@ -263,12 +267,14 @@ int region_accumulate(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int
         d_mask, mask_pitch, words, (int)H, L, lo, hi, x_lo, x_hi, y_lo, y_hi, g, h, nblocks);
     note_launch();
     if (int e = check_launch("vdilate_blocks_kernel")) return e;
-    const int threads = (int)std::min<int64_t>(1024, ((words + 31) / 32) * 32);
-    const size_t smem = (size_t)2 * words * 4;
+    const int64_t P = (L + 31) / 32 + 1;
+    const int threads = (int)std::min<int64_t>(1024, ((words + 2 * P + 31) / 32) * 32);
+    const size_t smem = (size_t)2 * (words + 2 * P) * 4;
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(hdilate_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    hdilate_rows_kernel<<<(unsigned)H, threads, smem, s>>>(g, h, words, (int)W, (int)H, L, lo, hi, d_region, mask_pitch);
+    hdilate_rows_kernel<<<(unsigned)H, threads, smem, s>>>(g, h, words, P, (int)W, (int)H, L, lo, hi, d_region,
+                                                            mask_pitch);
     note_launch();
     return check_launch("hdilate_rows_kernel");
 }

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Usage (on the GPU box): bash scripts_profile.sh <tag>
+# 1) plain bench run (must exit 0), 2) ncu launch list, 3) ncu --set full on the screen kernel.
+set -u
+TAG=${1:-r1}
+mkdir -p gpurun_out
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --graph 0"
+$CMD > gpurun_out/plain_$TAG.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:screen_kernel -s 20 -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
+echo "profile rc=$?"
