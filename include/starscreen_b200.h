@@ -46,6 +46,8 @@ extern "C" {
 
 #define SS_MAX_RINGS 16
 #define SS_KEY_BASE (1LL << 21) /* screening.py:57 _KEY_BASE */
+#define SS_BLOB_HDR 16             /* int64 header slots per ring in a key blob */
+#define SS_BLOB_MAX_BITMAP_WORDS 8192 /* per-ring membership bitmap cap (32 KiB) */
 
 /* ── diagnostics ─────────────────────────────────────────────────────── */
 const char* ss_last_error(void);
@@ -73,8 +75,10 @@ int ss_build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitc
 /*
  * Lays out one ladder size's per-ring sorted key arrays
  * (FeatureSet.ring_keys(), screening.py:147-155) as a device-ready blob:
- * the keys plus their (cm) and (cm,cs) projections used by the screen's
- * early-exit cascade.  Host-only; call with h_blob = NULL to get the size.
+ * the keys, their (cm) and (cm,cs) projections used by the screen's
+ * early-exit cascade, and -- when the key bounding box is small enough --
+ * dense membership bitmaps of all three (layout in ss_template.cpp).
+ * Host-only; call with h_blob = NULL to get the size.
  * h_keys: concatenated sorted keys, key_off: n_rings+1 offsets.
  */
 int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings, int64_t* h_blob,
@@ -99,6 +103,15 @@ int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_
                    const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
                    double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
                    uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* stream);
+
+/*
+ * Device self-test of the screen's division routine: counts operands of
+ * family `mode` (0 consecutive integers from seed, 1 random integers < 2^43,
+ * 2 random wide-range doubles, 3 signed half-integers) whose quotient by
+ * `divisor` differs from IEEE __ddiv_rn; adds the count to *d_mismatches.
+ */
+int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, unsigned long long* d_mismatches,
+                    void* stream);
 
 /* screening.py:505-510: sizes below MIN_PATCH_SIDE keep every grid centre. */
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,

@@ -104,36 +104,6 @@ __global__ void write_xy_kernel(const unsigned* mask, long long mask_pitch, int 
     }
 }
 
-// Column pass of the footprint dilation.  Virtual rows r in [-hi, H-1+lo]
-// are cut into blocks of L = m rows starting at -hi; g = prefix-OR within
-// the block, h = suffix-OR.  Thread = (word column, block).
-__global__ void vdilate_blocks_kernel(const unsigned* mask, long long mask_pitch, long long words, int H, int L, int lo,
-                                      int hi, int x_lo, int x_hi, int y_lo, int y_hi, unsigned* g, unsigned* h,
-                                      long long nblocks) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= words * nblocks) return;
-    const long long w = gid % words, k = gid / words;
-    const unsigned cm = interior_bits(w, x_lo, x_hi);
-    const long long r0 = k * L - hi;  // first virtual row of the block
-    const long long vrows = (long long)H + L;  // storage rows (index r + hi)
-    unsigned acc = 0;
-    for (int i = 0; i < L; ++i) {
-        const long long r = r0 + i;
-        const unsigned s = (r >= y_lo && r <= y_hi) ? (mask[r * mask_pitch + w] & cm) : 0u;
-        acc |= s;
-        const long long idx = r + hi;
-        if (idx < vrows) g[idx * words + w] = acc;
-    }
-    acc = 0;
-    for (int i = L - 1; i >= 0; --i) {
-        const long long r = r0 + i;
-        const unsigned s = (r >= y_lo && r <= y_hi) ? (mask[r * mask_pitch + w] & cm) : 0u;
-        acc |= s;
-        const long long idx = r + hi;
-        if (idx < vrows) h[idx * words + w] = acc;
-    }
-}
-
 __device__ __forceinline__ unsigned get_word(const unsigned* row, long long i, long long words) {
     return (i >= 0 && i < words) ? row[i] : 0u;
 }
@@ -154,30 +124,60 @@ __device__ __forceinline__ unsigned shifted_hi(const unsigned* row, long long i,
     return (a << r) | (get_word(row, i - q - 1, words) >> (32 - r));
 }
 
-// Row pass: V(y) = h[y-hi] | g[y+lo] (column window), then
-// R(x) = OR_{c in [x-hi, x+lo]} V(c) = F_L(x - hi) with F_l(x) = OR V[x, x+l-1]
+// Column pass of the footprint dilation: V(y) = OR_{r in [y-hi, y+lo]} S(r)
+// = F_L(y - hi) with F_l(r) = OR S[r, r+l-1], by shift-OR doubling over the
+// rows of one 32-column word held in shared memory (padded by P >= L rows on
+// both sides so F at r < 0 is kept).  One CTA per word column.
+__global__ void vdilate_kernel(const unsigned* mask, long long mask_pitch, long long words, int H, int L, int hi,
+                               long long P, int x_lo, int x_hi, int y_lo, int y_hi, unsigned* V) {
+    extern __shared__ unsigned smem[];
+    const long long ext = (long long)H + 2 * P;
+    unsigned* A = smem;
+    unsigned* B = smem + ext;
+    const long long w = blockIdx.x;
+    const unsigned cm = interior_bits(w, x_lo, x_hi);
+    int any = 0;
+    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
+        const long long r = i - P;
+        const unsigned v = (r >= y_lo && r <= y_hi) ? (mask[r * mask_pitch + w] & cm) : 0u;
+        A[i] = v;
+        any |= (v != 0u);
+    }
+    if (!__syncthreads_or(any)) {
+        for (long long y = threadIdx.x; y < H; y += blockDim.x) V[y * words + w] = 0u;
+        return;
+    }
+    int l = 1;
+    while (2 * l <= L) {
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + l < ext ? A[i + l] : 0u);
+        __syncthreads();
+        unsigned* t = A; A = B; B = t;
+        l *= 2;
+    }
+    if (l < L) {
+        const int s = L - l;
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + s < ext ? A[i + s] : 0u);
+        __syncthreads();
+        unsigned* t = A; A = B; B = t;
+    }
+    for (long long y = threadIdx.x; y < H; y += blockDim.x) V[y * words + w] = A[y - hi + P];
+}
+
+// Row pass: R(x) = OR_{c in [x-hi, x+lo]} V(c) = F_L(x - hi) with F_l(x) = OR V[x, x+l-1]
 // built by shift-OR doubling in shared memory, OR'ed into the region row.
 // The row is padded by P words on both sides so F at x < 0 is kept.  One CTA
 // per row.
-__global__ void hdilate_rows_kernel(const unsigned* g, const unsigned* h, long long words, long long P, int W, int H,
-                                    int L, int lo, int hi, unsigned* region, long long region_pitch) {
+__global__ void hdilate_rows_kernel(const unsigned* V, long long words, long long P, int W, int L, int hi,
+                                    unsigned* region, long long region_pitch) {
     extern __shared__ unsigned smem[];
     const long long ext = words + 2 * P;
     unsigned* A = smem;
     unsigned* B = smem + ext;
     const int y = blockIdx.x;
-    // storage index of virtual row r is r + hi; window rows [y-hi, y+lo]
-    const long long ia = (long long)y;            // (y - hi) + hi
-    const long long ib = (long long)y + lo + hi;  // (y + lo) + hi
-    const bool single = (y % L) == 0;
     int any = 0;
     for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
         const long long wi = i - P;
-        unsigned v = 0;
-        if (wi >= 0 && wi < words) {
-            v = h[ia * words + wi];
-            if (!single) v |= g[ib * words + wi];
-        }
+        const unsigned v = (wi >= 0 && wi < words) ? V[(long long)y * words + wi] : 0u;
         A[i] = v;
         any |= (v != 0u);
     }
@@ -245,9 +245,8 @@ int compact(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int64_t H, in
 }
 
 size_t region_workspace_bytes(int64_t W, int64_t H, int32_t m_max) {
-    const int64_t words = (W + 31) / 32;
-    const int64_t vrows = H + std::max<int32_t>(m_max, 1);
-    return (size_t)2 * vrows * words * 4;
+    (void)m_max;
+    return (size_t)H * ((W + 31) / 32) * 4;
 }
 
 int region_accumulate(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int64_t H, int32_t m, int32_t stride,
@@ -258,23 +257,24 @@ int region_accumulate(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int
     const int x_lo = lo, x_hi = (int)(W - 1 - hi), y_lo = lo, y_hi = (int)(H - 1 - hi);
     if (x_hi < x_lo || y_hi < y_lo) return SS_OK;  // no evaluated centres
     const int64_t words = (W + 31) / 32;
-    const int64_t vrows = H + L;
-    unsigned* g = static_cast<unsigned*>(d_ws);
-    unsigned* h = g + vrows * words;
-    const int64_t nblocks = (vrows + L - 1) / L;
+    unsigned* V = static_cast<unsigned*>(d_ws);
     cudaStream_t s = as_stream(stream);
-    vdilate_blocks_kernel<<<(unsigned)((words * nblocks + 255) / 256), 256, 0, s>>>(
-        d_mask, mask_pitch, words, (int)H, L, lo, hi, x_lo, x_hi, y_lo, y_hi, g, h, nblocks);
-    note_launch();
-    if (int e = check_launch("vdilate_blocks_kernel")) return e;
+    {
+        const int64_t P = L;
+        const size_t smem = (size_t)2 * (H + 2 * P) * 4;
+        if (smem > 227 * 1024) { set_error("image too tall for the region pass"); return SS_EINVAL; }
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(vdilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        vdilate_kernel<<<(unsigned)words, 1024, smem, s>>>(d_mask, mask_pitch, words, (int)H, L, hi, P, x_lo, x_hi, y_lo,
+                                                           y_hi, V);
+        note_launch();
+        if (int e = check_launch("vdilate_kernel")) return e;
+    }
     const int64_t P = (L + 31) / 32 + 1;
     const int threads = (int)std::min<int64_t>(1024, ((words + 2 * P + 31) / 32) * 32);
     const size_t smem = (size_t)2 * (words + 2 * P) * 4;
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(hdilate_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    hdilate_rows_kernel<<<(unsigned)H, threads, smem, s>>>(g, h, words, P, (int)W, (int)H, L, lo, hi, d_region,
-                                                            mask_pitch);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(hdilate_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hdilate_rows_kernel<<<(unsigned)H, threads, smem, s>>>(V, words, P, (int)W, L, hi, d_region, mask_pitch);
     note_launch();
     return check_launch("hdilate_rows_kernel");
 }

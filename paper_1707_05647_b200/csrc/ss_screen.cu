@@ -3,18 +3,30 @@
 // Replaces _scan_size (screening.py:418-471) for one ladder size: the ring
 // features of _ring_maps_rect / _octagon_maps (screening.py:380-415,
 // features.py:322-382), _quantize_arr (screening.py:86-87), _pack_cells
-// (:90-97), _member_mask (:173-178) and the nonzero/mask bookkeeping.
+// (:90-97), _member_mask (:173-178) and the nonzero / mask bookkeeping.
 //
-// Bit-exactness: this file is compiled with -fmad=false and every fp64 op
-// is an IEEE-rounded add/sub/mul/div/sqrt in the reference's NumPy order
-// (SURVEY.md App. A); integer sums are exact int64 four-corner differences.
+// Bit-exactness: compiled with -fmad=false; every fp64 op is one IEEE-
+// rounded operation in the reference's NumPy order.
+// Divisions by the per-size constants (pixel counts, L1 masses, quantizer
+// steps) use a precomputed y = RN(1/b) and two FMA remainder corrections
+// (div_rn): by Markstein's theorem that is the correctly rounded quotient,
+// i.e. identical to IEEE division (ss_selftest_div checks it against
+// __ddiv_rn on the device; the parity tests check the whole path).
 //
-// Early-exit cascade (exact): a centre can only pass ring r if its mean cell
-// is among the ring's key means, then its (mean, std) pair among the key
-// pairs, then the full key.  The projections are implied by full membership,
-// so the decision is unchanged, but the X/Y/SQ planes and most of the fp64
-// work are only touched by centres that survive the cheaper tests.
+// Work decomposition: a warp owns a 256-centre segment of one row (8 chunks
+// of 32).  Stage 1 of ring 0 -- the mean cell, from the PLAIN planes only --
+// runs on all lanes.  A centre can only be a member if its mean cell is in
+// the ring's mean projection, so only those centres are pushed into a
+// per-warp shared-memory queue and finished (std stage on the SQUARED
+// planes, gradient stage on the X/Y planes, then rings >= 1) 32 at a time
+// with full lanes.  The decision is unchanged -- the projection tests are
+// implied by full membership -- but the X/Y/SQ planes and most fp64 work are
+// skipped for most centres and lane divergence stays bounded.  Membership
+// tests use dense bitmaps of the key bounding box in shared memory (binary
+// search over the sorted keys when the box is too large).
 #include <algorithm>
+#include <climits>
+#include <cmath>
 
 #include "ss_common.cuh"
 
@@ -22,33 +34,53 @@ namespace ss {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARPS = 8;   // rows per CTA
+constexpr int CHUNKS = 8;  // 32-centre chunks per warp
+constexpr int SEG = 32 * CHUNKS;
+constexpr int QCAP = 64;
+constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
 
 struct RingDev {
     int n, d;
-    double cnt_sq, w1_sq, cnt_di, w1_di;
-    // membership: offsets (int64 words into the blob) and counts
+    int sa, sb, sc, sd;  // SAT corners rel. to [cy][cx]: [+n+1][+n+1] [+n+1][-n+1] [-n+1][+n+1] [-n+1][-n+1]
+    int ea, ed;          // E corners: [+d+1][+1], [-d][+1]
+    int ob, oc;          // O corners: [0][-d], [0][+d+1]
+    double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
+    int cm_lo, cm_n, cs_lo, cs_n, cg_lo, cg_n;
+    int bm;        // shared-memory word offset of [m | ms | full] bits; -1: binary search
+    int wm, wms;   // words of the m and ms bitmaps
+    int bsrc;      // uint32 index of the bit section in the device blob (-1: zero fill)
+    int bwords;    // words to stage
     int off_m, n_m, off_ms, n_ms, off_k, n_k;
-    long long m_lo;            // dense mean-cell bitmap base
-    unsigned long long m_bits; // bit (cm - m_lo) set <=> cm in projection
-    int m_dense;               // 1 if the bitmap is exact
 };
 
 struct ScreenArgs {
     const long long* planes;
-    long long pitch, plane_stride;
-    int W, H;        // global image
-    int y_origin;    // global row of table row 0
-    int y_begin, y_end;
-    int m, stride, lo, hi;
-    int n_rings;
-    double qm, qs, qg;
+    long long pitch, ps;  // row pitch, plane stride (elements)
+    int W, H, y_origin, y_begin, y_end, stride, lo, hi, n_rings;
+    double qm, qs, qg, rqm, rqs, rqg;
     const long long* blob;
     unsigned* mask;
     long long mask_pitch;
     unsigned* row_counts;
-    unsigned long long* stage_counts;  // nullable: [ring0 evals, ring0 std-stage, ring0 grad-stage, ring>=1 evals]
+    unsigned long long* stage_counts;
     RingDev ring[SS_MAX_RINGS];
 };
+
+// Correctly rounded a / b given y = RN(1 / b) (Markstein): the first FMA pair
+// brings q within one ulp of a/b, the second rounds it exactly.
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+    double q = __dmul_rn(a, y);
+    double r = __fma_rn(-b, q, a);
+    q = __fma_rn(r, y, q);
+    r = __fma_rn(-b, q, a);
+    return __fma_rn(r, y, q);
+}
+
+// screening.py:86-87 floor(f / q + 0.5)
+__device__ __forceinline__ int quant(double f, double q, double rq) {
+    return (int)floor(__dadd_rn(div_rn(f, q, rq), 0.5));
+}
 
 __device__ __forceinline__ bool bsearch_eq(const long long* __restrict__ a, int n, long long key) {
     int lo = 0, hi = n;
@@ -59,116 +91,200 @@ __device__ __forceinline__ bool bsearch_eq(const long long* __restrict__ a, int 
     return lo < n && __ldg(a + lo) == key;
 }
 
-// four-corner square sum: cells[y+1][x+1] convention (integral.py:144-162)
-__device__ __forceinline__ long long sq_sum(const long long* __restrict__ p, long long pitch, int cx, int cy,
-                                            int n) {
-    const long long* top = p + (long long)(cy - n + 1) * pitch;
-    const long long* bot = p + (long long)(cy + n + 1) * pitch;
-    return __ldg(bot + cx + n + 1) - __ldg(bot + cx - n + 1) - __ldg(top + cx + n + 1) + __ldg(top + cx - n + 1);
-}
+__device__ __forceinline__ bool bit(const unsigned* s, int idx) { return (s[idx >> 5] >> (idx & 31)) & 1u; }
 
-// closed l1 ball via the E / O planes (integral.py:165-186 equivalent)
-__device__ __forceinline__ long long di_sum(const long long* __restrict__ e, const long long* __restrict__ o,
-                                            long long pitch, int cx, int cy, int r) {
-    const long long* orow = o + (long long)cy * pitch;
-    return __ldg(e + (long long)(cy + r + 1) * pitch + cx + 1) - __ldg(orow + cx - r) - __ldg(orow + cx + r + 1) +
-           __ldg(e + (long long)(cy - r) * pitch + cx + 1);
-}
-
-__device__ __forceinline__ long long quantize(double f, double q) {
-    // screening.py:86-87: floor(f / q + 0.5)
-    return (long long)floor(__dadd_rn(__ddiv_rn(f, q), 0.5));
-}
-
-// One ring of one centre.  Returns the cascade stage reached: 0 = rejected
-// on the mean, 1 = on (mean, std), 2 = on the full key, 3 = member.
-__device__ __forceinline__ int ring_member(const ScreenArgs& a, const RingDev& R, int cx, int cy) {
-    const long long ps = a.plane_stride;
-    const long long* sat = a.planes;
-    const long long* E = a.planes + 4 * ps;
-    const long long* O = a.planes + 8 * ps;
-    // ── stage 1: mean (PLAIN planes) ─────────────────────────────────────
-    const long long s1q = sq_sum(sat, a.pitch, cx, cy, R.n);
-    const long long s1d = di_sum(E, O, a.pitch, cx, cy, R.d);
-    const double mq = __ddiv_rn((double)s1q, R.cnt_sq);
-    const double md = __ddiv_rn((double)s1d, R.cnt_di);
-    const double mean = __dmul_rn(__dadd_rn(mq, md), 0.5);
-    const long long cm = quantize(mean, a.qm);
-    if (R.m_dense) {
-        const unsigned long long off = (unsigned long long)(cm - R.m_lo);
-        if (off >= 64ull || !((R.m_bits >> off) & 1ull)) return 0;
-    } else if (!bsearch_eq(a.blob + R.off_m, R.n_m, cm)) {
-        return 0;
+__device__ __forceinline__ bool member_m(const ScreenArgs& a, const RingDev& R, const unsigned* sb, int cm) {
+    if (R.bm >= 0) {
+        const unsigned i = (unsigned)(cm - R.cm_lo);
+        return i < (unsigned)R.cm_n && bit(sb + R.bm, (int)i);
     }
-    // ── stage 2: std (SQUARED planes) ────────────────────────────────────
-    const long long s2q = sq_sum(sat + 3 * ps, a.pitch, cx, cy, R.n);
-    const long long s2d = di_sum(E + 3 * ps, O + 3 * ps, a.pitch, cx, cy, R.d);
-    const double vq = __dsub_rn(__ddiv_rn((double)s2q, R.cnt_sq), __dmul_rn(mq, mq));
-    const double vd = __dsub_rn(__ddiv_rn((double)s2d, R.cnt_di), __dmul_rn(md, md));
-    const double sdq = __dsqrt_rn(vq > 0.0 ? vq : 0.0);
-    const double sdd = __dsqrt_rn(vd > 0.0 ? vd : 0.0);
-    const double sd = __dmul_rn(__dadd_rn(sdq, sdd), 0.5);
-    const long long cs = quantize(sd, a.qs);
-    const long long kms = cm * SS_KEY_BASE + cs;
-    if (!bsearch_eq(a.blob + R.off_ms, R.n_ms, kms)) return 1;
-    // ── stage 3: gradient (X / Y planes) ─────────────────────────────────
-    const long long sxq = sq_sum(sat + 1 * ps, a.pitch, cx, cy, R.n);
-    const long long syq = sq_sum(sat + 2 * ps, a.pitch, cx, cy, R.n);
-    const long long sxd = di_sum(E + 1 * ps, O + 1 * ps, a.pitch, cx, cy, R.d);
-    const long long syd = di_sum(E + 2 * ps, O + 2 * ps, a.pitch, cx, cy, R.d);
-    const double fs1q = (double)s1q, fs1d = (double)s1d;
-    // (cx + 1.5) * s1 and the subtraction are exact
-    const double gxq = __ddiv_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fs1q)), R.w1_sq);
-    const double gyq = __ddiv_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fs1q)), R.w1_sq);
-    const double gxd = __ddiv_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fs1d)), R.w1_di);
-    const double gyd = __ddiv_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fs1d)), R.w1_di);
-    const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);
+    return bsearch_eq(a.blob + R.off_m, R.n_m, cm);
+}
+__device__ __forceinline__ bool member_ms(const ScreenArgs& a, const RingDev& R, const unsigned* sb, int cm, int cs) {
+    if (R.bm >= 0) {
+        const unsigned j = (unsigned)(cs - R.cs_lo);
+        return j < (unsigned)R.cs_n && bit(sb + R.bm + R.wm, (cm - R.cm_lo) * R.cs_n + (int)j);
+    }
+    return bsearch_eq(a.blob + R.off_ms, R.n_ms, (long long)cm * SS_KEY_BASE + cs);
+}
+__device__ __forceinline__ bool member_k(const ScreenArgs& a, const RingDev& R, const unsigned* sb, int cm, int cs,
+                                         int cg) {
+    if (R.bm >= 0) {
+        const unsigned k = (unsigned)(cg - R.cg_lo);
+        return k < (unsigned)R.cg_n &&
+               bit(sb + R.bm + R.wm + R.wms, ((cm - R.cm_lo) * R.cs_n + (cs - R.cs_lo)) * R.cg_n + (int)k);
+    }
+    return bsearch_eq(a.blob + R.off_k, R.n_k, ((long long)cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
+}
+
+__device__ __forceinline__ long long ld(const long long* p) { return __ldg(p); }
+
+struct Stage1 {
+    long long s1q, s1d;
+    double mq, md;
+    int cm;
+};
+
+// Stage 1 (mean cell) of ring R for the centre whose PLAIN-SAT element is pc.
+__device__ __forceinline__ Stage1 stage1(const ScreenArgs& a, const RingDev& R, const long long* pc) {
+    Stage1 s;
+    const long long* pe = pc + 4 * a.ps;
+    const long long* po = pc + 8 * a.ps;
+    s.s1q = ld(pc + R.sa) - ld(pc + R.sb) - ld(pc + R.sc) + ld(pc + R.sd);
+    s.s1d = ld(pe + R.ea) - ld(po + R.ob) - ld(po + R.oc) + ld(pe + R.ed);
+    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);                   // features.py:325
+    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);                   // features.py:349
+    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
+    return s;
+}
+
+// Stages 2 (std) and 3 (gradient) of ring R given its stage 1.
+__device__ __forceinline__ bool finish_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sb,
+                                           const long long* pc, int cx, int cy, const Stage1& s, bool& grad) {
+    const long long ps = a.ps;
+    const long long* q2 = pc + 3 * ps;
+    const long long* e2 = pc + 7 * ps;
+    const long long* o2 = pc + 11 * ps;
+    const long long s2q = ld(q2 + R.sa) - ld(q2 + R.sb) - ld(q2 + R.sc) + ld(q2 + R.sd);
+    const long long s2d = ld(e2 + R.ea) - ld(o2 + R.ob) - ld(o2 + R.oc) + ld(e2 + R.ed);
+    // features.py:326, 350: sqrt(max(s2/count - mean*mean, 0))
+    const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
+    const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
+    const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
+    const int cs = quant(sd, a.qs, a.rqs);
+    if (!member_ms(a, R, sb, s.cm, cs)) return false;
+    grad = true;
+    const long long sxq = ld(pc + 1 * ps + R.sa) - ld(pc + 1 * ps + R.sb) - ld(pc + 1 * ps + R.sc) + ld(pc + 1 * ps + R.sd);
+    const long long syq = ld(pc + 2 * ps + R.sa) - ld(pc + 2 * ps + R.sb) - ld(pc + 2 * ps + R.sc) + ld(pc + 2 * ps + R.sd);
+    const long long sxd = ld(pc + 5 * ps + R.ea) - ld(pc + 9 * ps + R.ob) - ld(pc + 9 * ps + R.oc) + ld(pc + 5 * ps + R.ed);
+    const long long syd = ld(pc + 6 * ps + R.ea) - ld(pc + 10 * ps + R.ob) - ld(pc + 10 * ps + R.oc) + ld(pc + 6 * ps + R.ed);
+    const double fq = (double)s.s1q, fd = (double)s.s1d;
+    // features.py:328-329, 351-352: (s - (c + off) * s1) / w1; product and difference are exact
+    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
     const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
     const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    const long long cg = quantize(gm, a.qg);
-    return bsearch_eq(a.blob + R.off_k, R.n_k, kms * SS_KEY_BASE + cg) ? 3 : 2;
+    const int cg = quant(gm, a.qg, a.rqg);
+    return member_k(a, R, sb, s.cm, cs, cg);
 }
 
-// blockDim = (32, 8): a warp covers 32 consecutive x of one row.
-__global__ void __launch_bounds__(256) screen_kernel(const ScreenArgs a) {
-    const int lane = threadIdx.x;
-    const int x = blockIdx.x * 32 + lane;
-    const int y = a.y_begin + blockIdx.y * 8 + threadIdx.y;
-    if (y >= a.y_end) return;  // warp-uniform
-    const bool in_img = x < a.W;
-    const bool on_grid = in_img && (x % a.stride == 0) && (y % a.stride == 0);
-    const bool interior = on_grid && x >= a.lo && x <= a.W - 1 - a.hi && y >= a.lo && y <= a.H - 1 - a.hi;
-    bool keep = on_grid && !interior;  // screening.py:438-442 border keeps
-    bool surv = false;
-    int stage0 = -1, later = 0;
-    if (interior) {
-        const int cy = y - a.y_origin;  // table-local row (features are frame-invariant)
-        stage0 = ring_member(a, a.ring[0], x, cy);
-        surv = stage0 == 3;
-        for (int r = 1; r < a.n_rings && surv; ++r) {
-            ++later;
-            surv = ring_member(a, a.ring[r], x, cy) == 3;
+__global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) {
+    extern __shared__ unsigned sbits[];
+    __shared__ int q_x[WARPS][QCAP];
+    __shared__ int q_cm[WARPS][QCAP];
+    __shared__ double q_mq[WARPS][QCAP], q_md[WARPS][QCAP];
+    __shared__ long long q_s1q[WARPS][QCAP], q_s1d[WARPS][QCAP];
+    __shared__ unsigned s_mask[WARPS][CHUNKS];
+
+    // stage the rings' membership bitmaps
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
+    for (int r = 0; r < a.n_rings; ++r) {
+        const RingDev& R = a.ring[r];
+        if (R.bm < 0) continue;
+        for (int i = tid; i < R.bwords; i += WARPS * 32) sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x, warp = threadIdx.y;
+    const int y = a.y_begin + blockIdx.y * WARPS + warp;
+    if (y >= a.y_end) return;  // warp-uniform; no block barriers below
+    const int x0 = blockIdx.x * SEG;
+    const int cy = y - a.y_origin;  // table-local row: features are frame-invariant
+    const bool row_grid = (y % a.stride) == 0;
+    const bool row_int = row_grid && y >= a.lo && y <= a.H - 1 - a.hi;
+    const long long* rowp = a.planes + (long long)cy * a.pitch;
+    const RingDev& R0 = a.ring[0];
+    const unsigned lt = (1u << lane) - 1u;
+    const bool inst = a.stage_counts != nullptr;
+
+    int qn = 0;
+    unsigned surv_count = 0;
+    unsigned long long st0 = 0, st1 = 0, st2 = 0, st3 = 0;
+
+    // finish queue entries [qn - cnt, qn), one per lane, and fold them into the mask
+    auto drain = [&](int cnt) {
+        bool keep = false;
+        if (lane < cnt) {
+            const int e = qn - cnt + lane;
+            const int x = q_x[warp][e];
+            Stage1 s;
+            s.cm = q_cm[warp][e];
+            s.mq = q_mq[warp][e];
+            s.md = q_md[warp][e];
+            s.s1q = q_s1q[warp][e];
+            s.s1d = q_s1d[warp][e];
+            const long long* pc = rowp + x;
+            bool grad = false;
+            keep = finish_ring(a, R0, sbits, pc, x, cy, s, grad);
+            st2 += grad;
+            for (int r = 1; r < a.n_rings && keep; ++r) {
+                const RingDev& R = a.ring[r];
+                ++st3;
+                const Stage1 t = stage1(a, R, pc);
+                bool g2 = false;
+                keep = member_m(a, R, sbits, t.cm) && finish_ring(a, R, sbits, pc, x, cy, t, g2);
+            }
+            if (keep) {
+                const int off = x - x0;
+                atomicOr(&s_mask[warp][off >> 5], 1u << (off & 31));
+            }
         }
-        keep = surv;
+        surv_count += __popc(__ballot_sync(FULL, keep));
+        qn -= cnt;
+        __syncwarp();
+    };
+
+#pragma unroll 1
+    for (int c = 0; c < CHUNKS; ++c) {
+        const int x = x0 + c * 32 + lane;
+        const bool on_grid = row_grid && x < a.W && (x % a.stride) == 0;
+        const bool interior = row_int && on_grid && x >= a.lo && x <= a.W - 1 - a.hi;
+        const unsigned border = __ballot_sync(FULL, on_grid && !interior);
+        if (lane == 0) s_mask[warp][c] = border;
+        bool pass = false;
+        Stage1 s;
+        if (interior) {
+            s = stage1(a, R0, rowp + x);
+            pass = member_m(a, R0, sbits, s.cm);
+        }
+        const unsigned pb = __ballot_sync(FULL, pass);
+        if (inst) {
+            st0 += __popc(__ballot_sync(FULL, interior));
+            st1 += __popc(pb);
+        }
+        if (pass) {
+            const int e = qn + __popc(pb & lt);
+            q_x[warp][e] = x;
+            q_cm[warp][e] = s.cm;
+            q_mq[warp][e] = s.mq;
+            q_md[warp][e] = s.md;
+            q_s1q[warp][e] = s.s1q;
+            q_s1d[warp][e] = s.s1d;
+        }
+        qn += __popc(pb);
+        __syncwarp();
+        if (qn >= 32) drain(32);
     }
-    const unsigned word = __ballot_sync(FULL, keep);
-    const unsigned sw = __ballot_sync(FULL, surv);
+    if (qn > 0) drain(qn);
+    __syncwarp();
     const long long row = y - a.y_begin;
-    if (lane == 0) {
-        if (blockIdx.x * 32 < (unsigned)a.W) a.mask[row * a.mask_pitch + blockIdx.x] = word;
-        if (sw) atomicAdd(a.row_counts + row, (unsigned)__popc(sw));
+    if (lane < CHUNKS) {
+        const int w = blockIdx.x * CHUNKS + lane;
+        if (w * 32 < a.W) a.mask[row * a.mask_pitch + w] = s_mask[warp][lane];
     }
-    if (a.stage_counts) {  // instrumentation only (bench.py roofline), uniform branch
-        const unsigned e0 = __ballot_sync(FULL, stage0 >= 0), e1 = __ballot_sync(FULL, stage0 >= 1),
-                       e2 = __ballot_sync(FULL, stage0 >= 2);
-        int lt = later;
+    if (lane == 0 && surv_count) atomicAdd(a.row_counts + row, surv_count);
+    if (inst) {
+        unsigned long long v[4] = {st0, st1, st2, st3};
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) lt += __shfl_down_sync(FULL, lt, d);
-        if (lane == 0) {
-            atomicAdd(a.stage_counts + 0, (unsigned long long)__popc(e0));
-            atomicAdd(a.stage_counts + 1, (unsigned long long)__popc(e1));
-            atomicAdd(a.stage_counts + 2, (unsigned long long)__popc(e2));
-            atomicAdd(a.stage_counts + 3, (unsigned long long)lt);
+        for (int i = 0; i < 4; ++i) {
+            unsigned long long t = (i < 2) ? (lane == 0 ? v[i] : 0ull) : v[i];  // st0/st1 are warp totals
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) t += __shfl_down_sync(FULL, t, d);
+            if (lane == 0 && t) atomicAdd(a.stage_counts + i, t);
         }
     }
 }
@@ -192,6 +308,27 @@ __global__ void fill_grid_kernel(int W, int y_begin, int y_end, int stride, unsi
     if (w == 0) row_counts[row] = 0;
 }
 
+// div_rn vs IEEE division on n operands of a family (mode), divisor b.
+__global__ void selftest_div_kernel(unsigned long long n, unsigned long long seed, double b, int mode,
+                                    unsigned long long* bad) {
+    const double y = __drcp_rn(b);
+    unsigned long long local = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        unsigned long long h = (i + seed) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 27;
+        double a;
+        if (mode == 0) a = (double)(long long)(i + seed);                       // consecutive integers
+        else if (mode == 1) a = (double)(long long)(h >> 21);                   // integers < 2^43
+        else if (mode == 2) a = __longlong_as_double((long long)((h >> 4) | 0x3800000000000000ull));  // wide doubles
+        else a = (double)(long long)(h >> 22) * 0.5 - 1099511627776.0;          // half-integers, both signs
+        if (div_rn(a, b, y) != __ddiv_rn(a, b)) ++local;
+    }
+    if (local) atomicAdd(bad, local);
+}
+
 }  // namespace
 
 int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
@@ -204,29 +341,34 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         set_error("bad table frame");
         return SS_EINVAL;
     }
+    if (W > (1 << 30) || H > (1 << 30)) { set_error("image too large"); return SS_EINVAL; }
     if (y_begin < 0 || y_end > H || y_begin > y_end) { set_error("bad row range"); return SS_EINVAL; }
     if (m < 2 * 4 || stride < 1) { set_error("bad size/stride"); return SS_EINVAL; }
     if (n_rings < 1 || n_rings > SS_MAX_RINGS) { set_error("n_rings out of range"); return SS_EINVAL; }
     if (pitch != plane_pitch(w)) { set_error("plane pitch mismatch"); return SS_EINVAL; }
     if (mask_pitch < (W + 31) / 32) { set_error("mask pitch too small"); return SS_EINVAL; }
     const int lo = (m - 1) / 2, hi = m / 2;
-    // every evaluated centre's patch rows must be inside the table
     const int64_t ylo = std::max<int64_t>(y_begin, lo), yhi = std::min<int64_t>(y_end - 1, H - 1 - hi);
     if (ylo <= yhi && (ylo - lo < y_origin || yhi + hi > y_origin + h - 1)) {
         set_error("table band [%lld, %lld) does not cover rows [%lld, %lld] with margins", (long long)y_origin,
                   (long long)(y_origin + h), (long long)ylo, (long long)yhi);
         return SS_EINVAL;
     }
+    if (!h_blob || h_blob[0] != n_rings) { set_error("key blob does not match n_rings"); return SS_EINVAL; }
+    if ((int64_t)(m / 2 + 2) * pitch + m > (int64_t)INT32_MAX) {
+        set_error("patch offsets exceed 32 bits");
+        return SS_EINVAL;
+    }
+
     ScreenArgs a;
     a.planes = reinterpret_cast<const long long*>(d_planes);
     a.pitch = pitch;
-    a.plane_stride = (h + 1) * pitch;
+    a.ps = (h + 1) * pitch;
     a.W = (int)W;
     a.H = (int)H;
     a.y_origin = (int)y_origin;
     a.y_begin = (int)y_begin;
     a.y_end = (int)y_end;
-    a.m = m;
     a.stride = stride;
     a.lo = lo;
     a.hi = hi;
@@ -234,42 +376,72 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     a.qm = qm;
     a.qs = qs;
     a.qg = qg;
+    a.rqm = 1.0 / qm;
+    a.rqs = 1.0 / qs;
+    a.rqg = 1.0 / qg;
     a.blob = reinterpret_cast<const long long*>(d_blob);
     a.mask = d_mask;
     a.mask_pitch = mask_pitch;
     a.row_counts = d_row_counts;
     a.stage_counts = d_stage_counts;
-    // blob header: [0] n_rings, then per ring (off_m, n_m, off_ms, n_ms, off_k, n_k)
-    if (!h_blob || h_blob[0] != n_rings) { set_error("key blob does not match n_rings"); return SS_EINVAL; }
+    int smem_words = 0;
+    const long long P = pitch;
     for (int r = 0; r < n_rings; ++r) {
         RingDev& R = a.ring[r];
         const int n = ring_n[r], d = ring_d[r];
-        if (n < 1 || d < 0 || n > hi || d > lo) { set_error("ring (%d,%d) does not fit m=%d", n, d, m); return SS_EINVAL; }
+        if (n < 1 || d < 1 || n > hi || d > lo) {
+            set_error("ring (%d,%d) does not fit m=%d", n, d, m);
+            return SS_EINVAL;
+        }
         R.n = n;
         R.d = d;
-        R.cnt_sq = (double)(4LL * n * n);                                        // features.py:323
-        R.w1_sq = (double)(2LL * n * n * n);                                     // features.py:324
-        R.cnt_di = (double)(2LL * d * d + 2LL * d + 1);                          // integral.py:189-191
+        R.sa = (int)((n + 1) * P + (n + 1));
+        R.sb = (int)((n + 1) * P + (1 - n));
+        R.sc = (int)((1 - n) * P + (n + 1));
+        R.sd = (int)((1 - n) * P + (1 - n));
+        R.ea = (int)((d + 1) * P + 1);
+        R.ed = (int)(-(long long)d * P + 1);
+        R.ob = -d;
+        R.oc = d + 1;
+        R.cnt_sq = (double)(4LL * n * n);                                            // features.py:323
+        R.w1_sq = (double)(2LL * n * n * n);                                         // features.py:324
+        R.cnt_di = (double)(2LL * d * d + 2LL * d + 1);                              // integral.py:189-191
         R.w1_di = (double)(2LL * d * d + (long long)d * (d - 1) * (2 * d - 1) / 3);  // features.py:341-343
-        const int64_t* hd = h_blob + 1 + 6 * r;
+        R.rcp_sq = 1.0 / R.cnt_sq;  // host IEEE division: RN(1/b)
+        R.rcp_di = 1.0 / R.cnt_di;
+        R.rw1_sq = 1.0 / R.w1_sq;
+        R.rw1_di = 1.0 / R.w1_di;
+        const int64_t* hd = h_blob + 1 + SS_BLOB_HDR * r;
         R.off_m = (int)hd[0];
         R.n_m = (int)hd[1];
         R.off_ms = (int)hd[2];
         R.n_ms = (int)hd[3];
         R.off_k = (int)hd[4];
         R.n_k = (int)hd[5];
-        // dense 64-bit bitmap of the mean projection when it spans < 64 cells
-        R.m_dense = 0;
-        R.m_lo = 0;
-        R.m_bits = 0;
-        if (R.n_m == 0) {
-            R.m_dense = 1;  // empty set: nothing passes
-        } else {
-            const int64_t lo_c = h_blob[R.off_m], hi_c = h_blob[R.off_m + R.n_m - 1];
-            if (hi_c - lo_c < 64) {
-                R.m_dense = 1;
-                R.m_lo = lo_c;
-                for (int i = 0; i < R.n_m; ++i) R.m_bits |= 1ull << (h_blob[R.off_m + i] - lo_c);
+        R.cm_lo = (int)hd[6];
+        R.cm_n = (int)hd[7];
+        R.cs_lo = (int)hd[8];
+        R.cs_n = (int)hd[9];
+        R.cg_lo = (int)hd[10];
+        R.cg_n = (int)hd[11];
+        R.bm = -1;
+        R.wm = R.wms = 0;
+        R.bsrc = -1;
+        R.bwords = 0;
+        if (R.n_k == 0) {  // empty ring: nothing passes
+            R.bm = smem_words;
+            R.cm_n = 0;
+            R.bwords = 1;
+            smem_words += 1;
+        } else if (hd[12] >= 0) {
+            const int64_t words = hd[13] + hd[14] + hd[15];
+            if (smem_words + words <= SMEM_BITMAP_WORDS) {
+                R.bm = smem_words;
+                R.wm = (int)hd[13];
+                R.wms = (int)hd[14];
+                R.bsrc = (int)(hd[12] * 2);
+                R.bwords = (int)words;
+                smem_words += (int)words;
             }
         }
     }
@@ -277,8 +449,10 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     const int64_t rows = y_end - y_begin;
     if (rows == 0) return SS_OK;
     if (cudaMemsetAsync(d_row_counts, 0, rows * sizeof(uint32_t), s) != cudaSuccess) return check_launch("memset");
-    dim3 grid((unsigned)((W + 31) / 32), (unsigned)((rows + 7) / 8));
-    screen_kernel<<<grid, dim3(32, 8), 0, s>>>(a);
+    const size_t smem = (size_t)std::max(smem_words, 1) * 4;
+    if (smem > 32 * 1024) cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)((W + SEG - 1) / SEG), (unsigned)((rows + WARPS - 1) / WARPS));
+    screen_kernel<<<grid, dim3(32, WARPS), smem, s>>>(a);
     note_launch();
     return check_launch("screen_kernel");
 }
@@ -292,6 +466,13 @@ int fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_
         (int)W, (int)y_begin, (int)y_end, stride, d_mask, mask_pitch, d_row_counts);
     note_launch();
     return check_launch("fill_grid_kernel");
+}
+
+int selftest_div(uint64_t n, uint64_t seed, double b, int mode, unsigned long long* d_bad, void* stream) {
+    if (b <= 0.0 || mode < 0 || mode > 3) { set_error("bad selftest arguments"); return SS_EINVAL; }
+    selftest_div_kernel<<<148 * 16, 256, 0, as_stream(stream)>>>(n, seed, b, mode, d_bad);
+    note_launch();
+    return check_launch("selftest_div_kernel");
 }
 
 }  // namespace ss
@@ -309,5 +490,9 @@ int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,
                  int64_t mask_pitch_words, uint32_t* d_row_counts, void* stream) {
     return ss::fill_grid(W, y_begin, y_end, stride, d_mask, mask_pitch_words, d_row_counts, stream);
+}
+int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, unsigned long long* d_mismatches,
+                    void* stream) {
+    return ss::selftest_div(n, seed, divisor, mode, d_mismatches, stream);
 }
 }

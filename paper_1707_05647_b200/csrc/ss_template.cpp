@@ -8,6 +8,7 @@
 // (image_io.py:216-228) and the patch-side ring features (features.py:
 // 220-224 via :322-370).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -195,33 +196,65 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
         ss::set_error("bad keyset arguments");
         return SS_EINVAL;
     }
-    // header: n_rings, then per ring (off_m, n_m, off_ms, n_ms, off_k, n_k)
-    std::vector<int64_t> blob(1 + 6 * (size_t)n_rings, 0);
+    // Layout (int64 slots): [0] n_rings; header of SS_BLOB_HDR slots per ring at
+    // 1 + SS_BLOB_HDR * r:
+    //   0 off_m  1 n_m  2 off_ms  3 n_ms  4 off_k  5 n_k        sorted arrays
+    //   6 cm_lo  7 cm_n  8 cs_lo  9 cs_n  10 cg_lo  11 cg_n     key bounding box
+    //   12 off_bits (-1: none)  13 words_m  14 words_ms  15 words_full
+    // The bit section packs uint32 words [m | ms | full] two per slot; bit i of
+    // ms is (cm-cm_lo)*cs_n + (cs-cs_lo), of full ((..)*cg_n + (cg-cg_lo)).
+    const int H = SS_BLOB_HDR;
+    std::vector<int64_t> blob(1 + (size_t)H * n_rings, 0);
     blob[0] = n_rings;
     for (int32_t r = 0; r < n_rings; ++r) {
         const int64_t a = h_key_off[r], b = h_key_off[r + 1];
         std::vector<int64_t> km, kms;
+        int64_t lo[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, hi[3] = {-1, -1, -1};
         for (int64_t i = a; i < b; ++i) {
             if (i > a && h_keys[i] <= h_keys[i - 1]) {
                 ss::set_error("ring keys must be sorted and unique");
                 return SS_EINVAL;
             }
             const int64_t ms = h_keys[i] / SS_KEY_BASE, mm = ms / SS_KEY_BASE;
+            const int64_t c3[3] = {mm, ms % SS_KEY_BASE, h_keys[i] % SS_KEY_BASE};
+            for (int c = 0; c < 3; ++c) { lo[c] = std::min(lo[c], c3[c]); hi[c] = std::max(hi[c], c3[c]); }
             if (kms.empty() || kms.back() != ms) kms.push_back(ms);
             if (km.empty() || km.back() != mm) km.push_back(mm);
         }
-        int64_t* hd = &blob[1 + 6 * (size_t)r];
-        hd[0] = (int64_t)blob.size();
-        hd[1] = (int64_t)km.size();
+        auto hd = [&](int i) -> int64_t& { return blob[1 + (size_t)H * r + i]; };
+        hd(0) = (int64_t)blob.size();
+        hd(1) = (int64_t)km.size();
         blob.insert(blob.end(), km.begin(), km.end());
-        hd = &blob[1 + 6 * (size_t)r];
-        hd[2] = (int64_t)blob.size();
-        hd[3] = (int64_t)kms.size();
+        hd(2) = (int64_t)blob.size();
+        hd(3) = (int64_t)kms.size();
         blob.insert(blob.end(), kms.begin(), kms.end());
-        hd = &blob[1 + 6 * (size_t)r];
-        hd[4] = (int64_t)blob.size();
-        hd[5] = b - a;
+        hd(4) = (int64_t)blob.size();
+        hd(5) = b - a;
         blob.insert(blob.end(), h_keys + a, h_keys + b);
+        const int64_t n[3] = {b > a ? hi[0] - lo[0] + 1 : 0, b > a ? hi[1] - lo[1] + 1 : 0,
+                              b > a ? hi[2] - lo[2] + 1 : 0};
+        for (int c = 0; c < 3; ++c) { hd(6 + 2 * c) = b > a ? lo[c] : 0; hd(7 + 2 * c) = n[c]; }
+        hd(12) = -1;
+        const int64_t bm = n[0], bms = n[0] * n[1], bfull = n[0] * n[1] * n[2];
+        const int64_t wm = (bm + 31) / 32, wms = (bms + 31) / 32, wfull = (bfull + 31) / 32;
+        if (b > a && wm + wms + wfull <= SS_BLOB_MAX_BITMAP_WORDS) {
+            std::vector<uint32_t> words((size_t)(wm + wms + wfull), 0u);
+            auto set = [&](int64_t base, int64_t bit) { words[(size_t)(base + bit / 32)] |= 1u << (bit % 32); };
+            for (int64_t i = a; i < b; ++i) {
+                const int64_t ms = h_keys[i] / SS_KEY_BASE, mm = ms / SS_KEY_BASE;
+                const int64_t im = mm - lo[0], is = ms % SS_KEY_BASE - lo[1], ig = h_keys[i] % SS_KEY_BASE - lo[2];
+                set(0, im);
+                set(wm, im * n[1] + is);
+                set(wm + wms, (im * n[1] + is) * n[2] + ig);
+            }
+            if (words.size() % 2) words.push_back(0u);
+            hd(12) = (int64_t)blob.size();
+            hd(13) = wm;
+            hd(14) = wms;
+            hd(15) = wfull;
+            for (size_t i = 0; i < words.size(); i += 2)
+                blob.push_back((int64_t)((uint64_t)words[i] | ((uint64_t)words[i + 1] << 32)));
+        }
     }
     const size_t need = blob.size() * sizeof(int64_t);
     if (h_blob) {

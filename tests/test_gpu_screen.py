@@ -161,7 +161,7 @@ def test_errors_and_edge_cases(cuda):
     with pytest.raises(ValueError):
         screen(scene, scene[:4, :4])
     # template larger than the image: every size is all-border, nothing tested
-    small = scene[:20, :30].copy()
+    small = scene[:10, :14].copy()
     res = screen(small, scene[:32, :32].copy())
     assert res.stats.patches_tested == 0 and len(res.candidates) == 0
     for m in res.ladder:

@@ -94,3 +94,26 @@ def test_overflow_guard_rejected(cuda):
     L = _native.lib()
     with pytest.raises(ValueError, match="too large"):
         _native.check(L.ss_build_tables(1, 300000, 300000, 300000, 16, L.ss_plane_pitch(300000), 0, 0, None))
+
+
+def test_division_routine_matches_ieee(cuda):
+    """The screen divides by per-size constants with a reciprocal and two FMA
+    corrections; it must equal IEEE division for every operand family the
+    features produce (integer sums, half-integer gradient numerators, wide doubles)."""
+    import torch
+
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    bad = torch.zeros(1, dtype=torch.int64, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    divisors = [4.0 * n * n for n in (4, 5, 11, 16, 64, 181, 256)]
+    divisors += [2.0 * d * d + 2 * d + 1 for d in (3, 6, 15, 23, 181, 255)]
+    divisors += [2.0 * n ** 3 for n in (4, 11, 64, 256)]
+    divisors += [2.0 * d * d + d * (d - 1) * (2 * d - 1) // 3 for d in (3, 15, 255)]
+    divisors += [8.0, 3.0, 0.75, 1e-3, 1e6, 6.25, 7.123456789]
+    for i, b in enumerate(divisors):
+        for mode in range(4):
+            _native.check(L.ss_selftest_div(1 << 22, 1000 * i + mode, b, mode, bad.data_ptr(), s))
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0

@@ -58,6 +58,7 @@ def test_keyset_blob_layout():
     from paper_1707_05647_b200 import _native
 
     KB = _native.KEY_BASE
+    HDR = 16
     keys = [np.array([(1 * KB + 2) * KB + 3, (1 * KB + 2) * KB + 4, (5 * KB + 0) * KB + 0], np.int64),
             np.array([], np.int64)]
     allk = np.concatenate(keys)
@@ -68,11 +69,23 @@ def test_keyset_blob_layout():
     blob = np.empty(size.value // 8, np.int64)
     _native.check(L.ss_keyset_blob(allk.ctypes.data, off.ctypes.data, 2, blob.ctypes.data, ctypes.byref(size)))
     assert blob[0] == 2
-    om, nm, oms, nms, ok, nk = blob[1:7]
+    h = blob[1:1 + HDR]
+    om, nm, oms, nms, ok, nk = h[:6]
     assert list(blob[om:om + nm]) == [1, 5]
     assert list(blob[oms:oms + nms]) == [1 * KB + 2, 5 * KB]
     assert list(blob[ok:ok + nk]) == list(keys[0])
-    assert blob[7 + 1] == 0 and blob[7 + 3] == 0 and blob[7 + 5] == 0
+    # bounding box cm in [1,5], cs in [0,2], cg in [0,4]
+    assert list(h[6:12]) == [1, 5, 0, 3, 0, 5]
+    ob, wm, wms, wfull = h[12:16]
+    assert ob > 0 and (wm, wms, wfull) == (1, 1, 3)
+    words = blob[ob:].view(np.uint32)
+    bits = lambda base, i: (int(words[base + i // 32]) >> (i % 32)) & 1
+    assert [bits(0, i) for i in range(5)] == [1, 0, 0, 0, 1]
+    assert bits(wm, 0 * 3 + 2) and bits(wm, 4 * 3 + 0) and not bits(wm, 0 * 3 + 0)
+    assert bits(wm + wms, (0 * 3 + 2) * 5 + 3) and bits(wm + wms, (0 * 3 + 2) * 5 + 4)
+    assert bits(wm + wms, (4 * 3 + 0) * 5 + 0) and not bits(wm + wms, (0 * 3 + 2) * 5 + 2)
+    h2 = blob[1 + HDR:1 + 2 * HDR]
+    assert h2[1] == h2[3] == h2[5] == 0 and h2[12] == -1
     bad = np.array([5, 3], np.int64)
     with pytest.raises(ValueError, match="sorted"):
         _native.check(L.ss_keyset_blob(bad.ctypes.data, np.array([0, 2], np.int64).ctypes.data, 1, None,
