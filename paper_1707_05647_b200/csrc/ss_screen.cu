@@ -119,34 +119,50 @@ __device__ __forceinline__ bool member_k(const ScreenArgs& a, const RingDev& R, 
 
 __device__ __forceinline__ long long ld(const long long* p) { return __ldg(p); }
 
+// The 8 corner elements of one kind for ring R (4 SAT, 2 E, 2 O), loaded
+// together so a single memory round trip covers them.
+struct Corners {
+    long long q[4], e[2], o[2];
+};
+__device__ __forceinline__ void load_corners(const ScreenArgs& a, const RingDev& R, const long long* pc, int kind,
+                                             Corners& c) {
+    const long long* pq = pc + (long long)kind * a.ps;
+    const long long* pe = pc + (long long)(4 + kind) * a.ps;
+    const long long* po = pc + (long long)(8 + kind) * a.ps;
+    c.q[0] = ld(pq + R.sa);
+    c.q[1] = ld(pq + R.sb);
+    c.q[2] = ld(pq + R.sc);
+    c.q[3] = ld(pq + R.sd);
+    c.e[0] = ld(pe + R.ea);
+    c.e[1] = ld(pe + R.ed);
+    c.o[0] = ld(po + R.ob);
+    c.o[1] = ld(po + R.oc);
+}
+__device__ __forceinline__ long long sq_of(const Corners& c) { return c.q[0] - c.q[1] - c.q[2] + c.q[3]; }
+__device__ __forceinline__ long long di_of(const Corners& c) { return c.e[0] - c.o[0] - c.o[1] + c.e[1]; }
+
 struct Stage1 {
     long long s1q, s1d;
     double mq, md;
     int cm;
 };
 
-// Stage 1 (mean cell) of ring R for the centre whose PLAIN-SAT element is pc.
-__device__ __forceinline__ Stage1 stage1(const ScreenArgs& a, const RingDev& R, const long long* pc) {
+// Stage 1 (mean cell) of ring R from its PLAIN corners.
+__device__ __forceinline__ Stage1 stage1_of(const ScreenArgs& a, const RingDev& R, const Corners& c) {
     Stage1 s;
-    const long long* pe = pc + 4 * a.ps;
-    const long long* po = pc + 8 * a.ps;
-    s.s1q = ld(pc + R.sa) - ld(pc + R.sb) - ld(pc + R.sc) + ld(pc + R.sd);
-    s.s1d = ld(pe + R.ea) - ld(po + R.ob) - ld(po + R.oc) + ld(pe + R.ed);
+    s.s1q = sq_of(c);
+    s.s1d = di_of(c);
     s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);                   // features.py:325
     s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);                   // features.py:349
     s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
     return s;
 }
 
-// Stages 2 (std) and 3 (gradient) of ring R given its stage 1.
-__device__ __forceinline__ bool finish_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sb,
-                                           const long long* pc, int cx, int cy, const Stage1& s, bool& grad) {
-    const long long ps = a.ps;
-    const long long* q2 = pc + 3 * ps;
-    const long long* e2 = pc + 7 * ps;
-    const long long* o2 = pc + 11 * ps;
-    const long long s2q = ld(q2 + R.sa) - ld(q2 + R.sb) - ld(q2 + R.sc) + ld(q2 + R.sd);
-    const long long s2d = ld(e2 + R.ea) - ld(o2 + R.ob) - ld(o2 + R.oc) + ld(e2 + R.ed);
+// Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
+__device__ __forceinline__ bool finish_of(const ScreenArgs& a, const RingDev& R, const unsigned* sb, int cx, int cy,
+                                         const Stage1& s, const Corners& c2, const Corners& cx_, const Corners& cy_,
+                                         bool& grad) {
+    const long long s2q = sq_of(c2), s2d = di_of(c2);
     // features.py:326, 350: sqrt(max(s2/count - mean*mean, 0))
     const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
     const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
@@ -154,16 +170,12 @@ __device__ __forceinline__ bool finish_ring(const ScreenArgs& a, const RingDev& 
     const int cs = quant(sd, a.qs, a.rqs);
     if (!member_ms(a, R, sb, s.cm, cs)) return false;
     grad = true;
-    const long long sxq = ld(pc + 1 * ps + R.sa) - ld(pc + 1 * ps + R.sb) - ld(pc + 1 * ps + R.sc) + ld(pc + 1 * ps + R.sd);
-    const long long syq = ld(pc + 2 * ps + R.sa) - ld(pc + 2 * ps + R.sb) - ld(pc + 2 * ps + R.sc) + ld(pc + 2 * ps + R.sd);
-    const long long sxd = ld(pc + 5 * ps + R.ea) - ld(pc + 9 * ps + R.ob) - ld(pc + 9 * ps + R.oc) + ld(pc + 5 * ps + R.ed);
-    const long long syd = ld(pc + 6 * ps + R.ea) - ld(pc + 10 * ps + R.ob) - ld(pc + 10 * ps + R.oc) + ld(pc + 6 * ps + R.ed);
     const double fq = (double)s.s1q, fd = (double)s.s1d;
     // features.py:328-329, 351-352: (s - (c + off) * s1) / w1; product and difference are exact
-    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
-    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gxq = div_rn(__dsub_rn((double)sq_of(cx_), __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gyq = div_rn(__dsub_rn((double)sq_of(cy_), __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gxd = div_rn(__dsub_rn((double)di_of(cx_), __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gyd = div_rn(__dsub_rn((double)di_of(cy_), __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
     const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
     const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
     const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
@@ -173,10 +185,13 @@ __device__ __forceinline__ bool finish_ring(const ScreenArgs& a, const RingDev& 
 
 __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) {
     extern __shared__ unsigned sbits[];
+    // Q1: ring-0 stage-1 passers with their stage-1 state; QN: (x, ring) pairs for rings >= 1
     __shared__ int q_x[WARPS][QCAP];
     __shared__ int q_cm[WARPS][QCAP];
     __shared__ double q_mq[WARPS][QCAP], q_md[WARPS][QCAP];
     __shared__ long long q_s1q[WARPS][QCAP], q_s1d[WARPS][QCAP];
+    __shared__ int qn_x[WARPS][QCAP];
+    __shared__ unsigned char qn_r[WARPS][QCAP];
     __shared__ unsigned s_mask[WARPS][CHUNKS];
 
     // stage the rings' membership bitmaps
@@ -201,16 +216,34 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
     const unsigned lt = (1u << lane) - 1u;
     const bool inst = a.stage_counts != nullptr;
 
-    int qn = 0;
+    int n1 = 0, nn = 0;  // queue lengths
     unsigned surv_count = 0;
     unsigned long long st0 = 0, st1 = 0, st2 = 0, st3 = 0;
 
-    // finish queue entries [qn - cnt, qn), one per lane, and fold them into the mask
-    auto drain = [&](int cnt) {
-        bool keep = false;
+    auto survive = [&](bool keep, int x) {
+        if (keep) {
+            const int off = x - x0;
+            atomicOr(&s_mask[warp][off >> 5], 1u << (off & 31));
+        }
+        surv_count += __popc(__ballot_sync(FULL, keep));
+    };
+    auto push_next = [&](bool push, int x, int r) {
+        const unsigned b = __ballot_sync(FULL, push);
+        if (push) {
+            const int e = nn + __popc(b & lt);
+            qn_x[warp][e] = x;
+            qn_r[warp][e] = (unsigned char)r;
+        }
+        nn += __popc(b);
+        __syncwarp();
+    };
+    // ring-0 stages 2-3 for Q1 entries [n1 - cnt, n1)
+    auto drain1 = [&](int cnt) {
+        bool keep = false, more = false;
+        int x = 0;
         if (lane < cnt) {
-            const int e = qn - cnt + lane;
-            const int x = q_x[warp][e];
+            const int e = n1 - cnt + lane;
+            x = q_x[warp][e];
             Stage1 s;
             s.cm = q_cm[warp][e];
             s.mq = q_mq[warp][e];
@@ -218,29 +251,60 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
             s.s1q = q_s1q[warp][e];
             s.s1d = q_s1d[warp][e];
             const long long* pc = rowp + x;
+            Corners c2, cxk, cyk;
+            load_corners(a, R0, pc, 3, c2);
+            load_corners(a, R0, pc, 1, cxk);
+            load_corners(a, R0, pc, 2, cyk);
             bool grad = false;
-            keep = finish_ring(a, R0, sbits, pc, x, cy, s, grad);
+            const bool pass = finish_of(a, R0, sbits, x, cy, s, c2, cxk, cyk, grad);
             st2 += grad;
-            for (int r = 1; r < a.n_rings && keep; ++r) {
-                const RingDev& R = a.ring[r];
-                ++st3;
-                const Stage1 t = stage1(a, R, pc);
-                bool g2 = false;
-                keep = member_m(a, R, sbits, t.cm) && finish_ring(a, R, sbits, pc, x, cy, t, g2);
-            }
-            if (keep) {
-                const int off = x - x0;
-                atomicOr(&s_mask[warp][off >> 5], 1u << (off & 31));
-            }
+            keep = pass && a.n_rings == 1;
+            more = pass && a.n_rings > 1;
         }
-        surv_count += __popc(__ballot_sync(FULL, keep));
-        qn -= cnt;
+        n1 -= cnt;
         __syncwarp();
+        survive(keep, x);
+        push_next(more, x, 1);
+    };
+    // one full ring evaluation for QN entries [nn - cnt, nn)
+    auto drainN = [&](int cnt) {
+        bool keep = false, more = false;
+        int x = 0, r = 0;
+        if (lane < cnt) {
+            const int e = nn - cnt + lane;
+            x = qn_x[warp][e];
+            r = qn_r[warp][e];
+        }
+        nn -= cnt;
+        __syncwarp();
+        if (lane < cnt) {
+            const RingDev& R = a.ring[r];
+            const long long* pc = rowp + x;
+            Corners c0, c2, cxk, cyk;
+            load_corners(a, R, pc, 0, c0);
+            load_corners(a, R, pc, 3, c2);
+            load_corners(a, R, pc, 1, cxk);
+            load_corners(a, R, pc, 2, cyk);
+            ++st3;
+            const Stage1 t = stage1_of(a, R, c0);
+            bool grad = false;
+            const bool pass = member_m(a, R, sbits, t.cm) && finish_of(a, R, sbits, x, cy, t, c2, cxk, cyk, grad);
+            keep = pass && r + 1 == a.n_rings;
+            more = pass && r + 1 < a.n_rings;
+        }
+        survive(keep, x);
+        push_next(more, x, r + 1);
     };
 
+    // stage 1 of ring 0 over the segment, software-pipelined one chunk ahead
+    // (only centres inside the evaluable interior are loaded: their corners are in bounds)
+    auto in_interior = [&](int xx) { return row_int && xx >= a.lo && xx <= a.W - 1 - a.hi; };
+    Corners cur, nxt;
+    if (in_interior(x0 + lane)) load_corners(a, R0, rowp + x0 + lane, 0, cur);
 #pragma unroll 1
     for (int c = 0; c < CHUNKS; ++c) {
         const int x = x0 + c * 32 + lane;
+        if (c + 1 < CHUNKS && in_interior(x + 32)) load_corners(a, R0, rowp + x + 32, 0, nxt);
         const bool on_grid = row_grid && x < a.W && (x % a.stride) == 0;
         const bool interior = row_int && on_grid && x >= a.lo && x <= a.W - 1 - a.hi;
         const unsigned border = __ballot_sync(FULL, on_grid && !interior);
@@ -248,7 +312,7 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
         bool pass = false;
         Stage1 s;
         if (interior) {
-            s = stage1(a, R0, rowp + x);
+            s = stage1_of(a, R0, cur);
             pass = member_m(a, R0, sbits, s.cm);
         }
         const unsigned pb = __ballot_sync(FULL, pass);
@@ -257,7 +321,7 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
             st1 += __popc(pb);
         }
         if (pass) {
-            const int e = qn + __popc(pb & lt);
+            const int e = n1 + __popc(pb & lt);
             q_x[warp][e] = x;
             q_cm[warp][e] = s.cm;
             q_mq[warp][e] = s.mq;
@@ -265,11 +329,14 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
             q_s1q[warp][e] = s.s1q;
             q_s1d[warp][e] = s.s1d;
         }
-        qn += __popc(pb);
+        n1 += __popc(pb);
         __syncwarp();
-        if (qn >= 32) drain(32);
+        if (n1 >= 32) drain1(32);
+        while (nn >= 32) drainN(32);
+        cur = nxt;
     }
-    if (qn > 0) drain(qn);
+    if (n1 > 0) drain1(n1);
+    while (nn > 0) drainN(nn < 32 ? nn : 32);
     __syncwarp();
     const long long row = y - a.y_begin;
     if (lane < CHUNKS) {
