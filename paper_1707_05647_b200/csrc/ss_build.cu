@@ -31,10 +31,7 @@ namespace {
 constexpr int TPB = 128;  // threads per tile
 constexpr int COLS = 4;   // consecutive columns per thread
 constexpr int TILE = TPB * COLS;
-constexpr int RB = kBandRows;
-constexpr int CW = kChunkCols;
-static_assert(TILE == CW + 2 * RB + 2, "tile geometry");
-constexpr int OFF = RB + 1;  // state index of x is x + OFF
+static_assert(TILE == kTileCols && TPB == kBuildThreads, "tile geometry");
 constexpr unsigned FULL = 0xffffffffu;
 
 struct BuildArgs {
@@ -61,16 +58,21 @@ __device__ __forceinline__ long long* st_ptr(const BuildArgs& a, int64_t b, int 
     return a.state + ((b * 4 + k) * 3 + type) * a.slen;
 }
 
-// row-prefix at group boundary g (sum over x < 64 g) for quantity q
+// row-prefix at group boundary g (sum over x < kGroup * g) for quantity q
 __device__ __forceinline__ long long rowpre_at(const BuildArgs& a, int64_t y, int64_t g, int q) {
     if (g <= 0) return 0;
     if (g > a.G) g = a.G;
     return a.rowpre[(y * (a.G + 1) + g) * 3 + q];
 }
 
-// kMode 0: local end state (pass 1); kMode 1: final planes (pass 3)
-template <int kMode>
+// kMode 0: local end state (pass 1); kMode 1: final planes (pass 3).
+// RB = rows per band; the tile owns CW plane columns plus RB+1 halo columns
+// on each side; state index of x is x + OFF.
+template <int kMode, int RB>
 __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
+    constexpr int CW = kTileCols - 2 * RB - 2;
+    constexpr int OFF = RB + 1;
+    static_assert(CW % kGroup == 0 && (RB + 1) % kGroup == 0, "XL+1 must be group aligned");
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t chunk = blockIdx.x, band = blockIdx.y;
     const int64_t c0 = chunk * CW;             // first owned plane column
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 
     if (kMode == 1 && band == 0) {
         // plane row 0 (y = -1) is zero in all 12 planes
-        const int64_t c = c0 - 64 + (int64_t)t * COLS;
+        const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;
         if (c >= c0 && c < c0 + CW && c < a.pitch) {
             for (int p = 0; p < 12; ++p) {
                 long long* dst = a.planes + p * a.plane_stride + c;
@@ -121,15 +123,33 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     }
 
     const int64_t g0 = (XL + 1) / kGroup;  // P(XL) = rowpre(g0): x < XL+1
-    int buf = 0;
-    for (int64_t y = y0; y < y1; ++y, buf ^= 1) {
-        // ── A: pixels, thread-local scans, warp scans ────────────────────
-        int lv[COLS], lx[COLS], lq[COLS];
+    // next row's pixels and row prefixes are fetched one row ahead
+    int pv[COLS];
+    long long pb[3];
+    auto fetch = [&](int64_t y) {
         const uint8_t* row = a.img + y * a.img_pitch;
 #pragma unroll
         for (int j = 0; j < COLS; ++j) {
             const int64_t x = xb + j;
-            int v = (x >= 0 && x < W) ? (int)__ldg(row + x) : 0;
+            pv[j] = (x >= 0 && x < W) ? (int)__ldg(row + x) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) pb[q] = rowpre_at(a, y, g0, q);
+    };
+    if (y0 < y1) fetch(y0);
+    int buf = 0;
+    for (int64_t y = y0; y < y1; ++y, buf ^= 1) {
+        // ── A: pixels, thread-local scans, warp scans ────────────────────
+        int lv[COLS], lx[COLS], lq[COLS];
+        const long long bv = pb[0], bx = pb[1], bq = pb[2];
+        int cv[COLS];
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) cv[j] = pv[j];
+        if (y + 1 < y1) fetch(y + 1);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            const int64_t x = xb + j;
+            int v = cv[j];
             if (t == 0 && j == 0) v = 0;  // column XL is inside rowpre(g0)
             const int wl = (int)(x - XL);  // local x weight: (x+1) - (XL+1)
             lv[j] = v;
@@ -157,7 +177,6 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 
         // ── B: full row prefixes P for the 4 kinds ───────────────────────
         for (int w = 0; w < warp; ++w) { ev += sTot[buf][w][0]; ex += sTot[buf][w][1]; eq += sTot[buf][w][2]; }
-        const long long bv = rowpre_at(a, y, g0, 0), bx = rowpre_at(a, y, g0, 1), bq = rowpre_at(a, y, g0, 2);
         long long P[4][COLS];
 #pragma unroll
         for (int j = 0; j < COLS; ++j) {
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                 GG[k][j] = Gn[j];
             }
             if (kMode == 1) {
-                const int64_t c = c0 - 64 + (int64_t)t * COLS;  // plane column of j = 0
+                const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;  // plane column of j = 0
                 if (c >= c0 && c < c0 + CW && c < a.pitch) {
                     const int64_t r = y + 1;
                     long long* ps = a.planes + (0 * 4 + k) * a.plane_stride + r * a.pitch + c;
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     }
 }
 
-// Row prefixes at 64-column group boundaries: rowpre[y][g] = sums over x < 64 g
+// Row prefixes at group boundaries: rowpre[y][g] = sums over x < kGroup * g
 // of (v, (x+1) v, v^2), g = 0..G.  One warp per row.
 __global__ void rowpre_kernel(BuildArgs a) {
     const int64_t y = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -292,7 +311,8 @@ __global__ void rowpre_kernel(BuildArgs a) {
 }
 
 // Pass 2a: inclusive band states of the SAT rows (in place).
-__global__ void band_scan_s_kernel(BuildArgs a, int64_t nb) {
+__global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
+    const int OFF = RB + 1;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= 4 * a.W) return;
     const int k = (int)(gid / a.W);
@@ -308,7 +328,8 @@ __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb) {
 // Pass 2b: inclusive FF / GG band states.  FF paths move left by RB per band
 // (clamped to S(W-1) beyond the right edge), GG paths move right (zero at
 // x <= 0).  Each stored element is read and written by exactly one thread.
-__global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb) {
+__global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
+    const int OFF = RB + 1;
     const int64_t W = a.W;
     const int64_t nF = W - 1 + OFF + (nb - 1) * RB, nG = W + RB + (nb - 1) * RB;
     const int64_t per_kind = nF + nG;
@@ -352,11 +373,32 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 static size_t rowpre_bytes(int64_t W, int64_t H) { return align_up((size_t)H * (n_groups(W) + 1) * 3 * 8, 256); }
 static size_t state_bytes(int64_t W, int64_t H) {
-    const int64_t nb = n_bands(H) - 1;
-    return nb > 0 ? align_up((size_t)nb * 12 * state_len(W) * 8, 256) : 0;
+    const int rb = pick_band_rows(W, H);
+    const int64_t nb = n_bands(H, rb) - 1;
+    return nb > 0 ? align_up((size_t)nb * 12 * state_len(W, rb) * 8, 256) : 0;
 }
 
 size_t build_workspace_bytes(int64_t W, int64_t H) { return rowpre_bytes(W, H) + state_bytes(W, H); }
+
+template <int RB>
+static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
+    if (nbands > 1) {
+        band_kernel<0, RB><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
+        note_launch();
+        if (int e = check_launch("band_kernel<local>")) return e;
+        const int64_t nb = nbands - 1, W = a.W;
+        band_scan_s_kernel<<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        note_launch();
+        if (int e = check_launch("band_scan_s_kernel")) return e;
+        const int64_t per_kind = (W - 1 + (RB + 1) + (nb - 1) * RB) + (W + RB + (nb - 1) * RB);
+        band_scan_fg_kernel<<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        note_launch();
+        if (int e = check_launch("band_scan_fg_kernel")) return e;
+    }
+    band_kernel<1, RB><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
+    note_launch();
+    return check_launch("band_kernel<final>");
+}
 
 int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
                  int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream) {
@@ -380,6 +422,7 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         return SS_EINVAL;
     }
     cudaStream_t s = as_stream(stream);
+    const int rb = pick_band_rows(W, H);
     BuildArgs a;
     a.img = d_img;
     a.W = W;
@@ -391,29 +434,18 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     a.G = n_groups(W);
     a.rowpre = reinterpret_cast<long long*>(d_ws);
     a.state = reinterpret_cast<long long*>(static_cast<char*>(d_ws) + rowpre_bytes(W, H));
-    a.slen = state_len(W);
-    a.n_chunks = n_chunks(W);
-    const int64_t nbands = n_bands(H);
+    a.slen = state_len(W, rb);
+    a.n_chunks = n_chunks(W, rb);
+    const int64_t nbands = n_bands(H, rb);
 
     rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
     note_launch();
     if (int e = check_launch("rowpre_kernel")) return e;
-    if (nbands > 1) {
-        band_kernel<0><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
-        note_launch();
-        if (int e = check_launch("band_kernel<local>")) return e;
-        const int64_t nb = nbands - 1;
-        band_scan_s_kernel<<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb);
-        note_launch();
-        if (int e = check_launch("band_scan_s_kernel")) return e;
-        const int64_t per_kind = (W - 1 + OFF + (nb - 1) * RB) + (W + RB + (nb - 1) * RB);
-        band_scan_fg_kernel<<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb);
-        note_launch();
-        if (int e = check_launch("band_scan_fg_kernel")) return e;
+    switch (rb) {
+    case 63: return launch_bands<63>(a, nbands, s);
+    case 31: return launch_bands<31>(a, nbands, s);
+    default: return launch_bands<15>(a, nbands, s);
     }
-    band_kernel<1><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
-    note_launch();
-    return check_launch("band_kernel<final>");
 }
 
 }  // namespace ss

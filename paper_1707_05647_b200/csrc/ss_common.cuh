@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/starscreen_b200.h"
 
@@ -16,20 +17,33 @@ namespace ss {
 void set_error(const char* fmt, ...);
 void note_launch(uint64_t n = 1);
 
-// Build-geometry constants.
-constexpr int kBuildThreads = 512;            // threads per band tile
-constexpr int kBandRows = 63;                 // Rb: rows per band
-constexpr int kChunkCols = 384;               // Cw: plane columns per tile
-constexpr int kGroup = 64;                    // row-prefix granularity
-static_assert(kChunkCols + 2 * kBandRows + 2 <= kBuildThreads, "tile too wide");
-static_assert((kChunkCols % kGroup) == 0 && ((kBandRows + 1) % kGroup) == 0, "XL must be group aligned");
+// Build geometry: a 128-thread tile covers
+// 512 columns = Cw owned plane columns + an Rb+1 halo on each side, and Rb
+// rows.  Rb is picked per image size so small images still fill the GPU.
+constexpr int kBuildThreads = 128;
+constexpr int kTileCols = 512;
+constexpr int kGroup = 16;  // row-prefix granularity (columns)
+inline int chunk_cols(int rb) { return kTileCols - 2 * rb - 2; }
+inline int pick_band_rows(int64_t W, int64_t H) {
+    // test hook: SS_BAND_ROWS=15|31|63 forces a geometry (tests cover all three)
+    if (const char* e = getenv("SS_BAND_ROWS")) {
+        const int v = atoi(e);
+        if (v == 15 || v == 31 || v == 63) return v;
+    }
+    const int cand[3] = {63, 31, 15};
+    for (int rb : cand) {
+        const int64_t tiles = ((H + rb - 1) / rb) * ((W + 1 + chunk_cols(rb) - 1) / chunk_cols(rb));
+        if (tiles >= 148 * 6) return rb;
+    }
+    return 15;
+}
 
 inline int64_t plane_pitch(int64_t W) { return ((W + 1 + 31) / 32) * 32; }
-inline int64_t n_bands(int64_t H) { return (H + kBandRows - 1) / kBandRows; }
-inline int64_t n_chunks(int64_t W) { return (W + 1 + kChunkCols - 1) / kChunkCols; }
+inline int64_t n_bands(int64_t H, int rb) { return (H + rb - 1) / rb; }
+inline int64_t n_chunks(int64_t W, int rb) { return (W + 1 + chunk_cols(rb) - 1) / chunk_cols(rb); }
 inline int64_t n_groups(int64_t W) { return (W + kGroup - 1) / kGroup; }
 // state row length: x in [-1-Rb, W+Rb]
-inline int64_t state_len(int64_t W) { return W + 2 * kBandRows + 2; }
+inline int64_t state_len(int64_t W, int rb) { return W + 2 * rb + 2; }
 
 inline bool overflow_guard_fails(int64_t W, int64_t H) {
     // integral.py:59-63: 255 * max(w,h) * w * h >= 2**62 -> ValueError

@@ -72,11 +72,13 @@ def test_golden_images(cuda):
         check_planes(img, planes, brute_extra=img.size <= 400)
 
 
-@pytest.mark.parametrize("shape", [(63, 383), (64, 384), (126, 385), (127, 767), (200, 1000), (517, 130), (1, 2000),
-                                   (1300, 3), (190, 770)])
-def test_band_and_chunk_boundaries(cuda, shape):
-    """Shapes straddling the 63-row band and 384-column chunk seams."""
-    rng = np.random.default_rng(sum(shape))
+@pytest.mark.parametrize("band_rows", [15, 31, 63])
+@pytest.mark.parametrize("shape", [(15, 479), (16, 480), (31, 447), (63, 383), (64, 384), (126, 385), (127, 767),
+                                   (200, 1000), (517, 130), (1, 2000), (1300, 3), (190, 961)])
+def test_band_and_chunk_boundaries(cuda, shape, band_rows, monkeypatch):
+    """Shapes straddling the band (15/31/63 rows) and chunk (480/448/384 columns) seams."""
+    monkeypatch.setenv("SS_BAND_ROWS", str(band_rows))
+    rng = np.random.default_rng(sum(shape) + band_rows)
     img = rng.integers(0, 256, shape, dtype=np.uint8)
     check_planes(img, device_planes(img, cuda))
 
