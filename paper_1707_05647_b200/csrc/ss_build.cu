@@ -310,6 +310,10 @@ __global__ void rowpre_kernel(BuildArgs a) {
     }
 }
 
+// Pass 2 loads a batch of band states into registers before the dependent
+// running sum, so the serial chain is over adds, not memory round trips.
+constexpr int SCAN_BATCH = 16;
+
 // Pass 2a: inclusive band states of the SAT rows (in place).
 __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
     const int OFF = RB + 1;
@@ -318,10 +322,17 @@ __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
     const int k = (int)(gid / a.W);
     const int64_t x = gid % a.W;
     long long acc = 0;
-    for (int64_t b = 0; b < nb; ++b) {
-        long long* p = st_ptr(a, b, k, 0) + x + OFF;
-        acc += *p;
-        *p = acc;
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
+        long long v[SCAN_BATCH];
+#pragma unroll
+        for (int j = 0; j < SCAN_BATCH; ++j) v[j] = (b0 + j < nb) ? st_ptr(a, b0 + j, k, 0)[x + OFF] : 0;
+#pragma unroll
+        for (int j = 0; j < SCAN_BATCH; ++j) {
+            if (b0 + j < nb) {
+                acc += v[j];
+                st_ptr(a, b0 + j, k, 0)[x + OFF] = acc;
+            }
+        }
     }
 }
 
@@ -337,31 +348,39 @@ __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
     if (gid >= 4 * per_kind) return;
     const int k = (int)(gid / per_kind);
     const int64_t i = gid % per_kind;
+    const bool ff = i < nF;
+    // FF: p0 in [-OFF, W-2 + (nb-1) RB], p = p0 - b RB; GG: p0 in [1-(nb-1)RB, W+RB], p = p0 + b RB
+    const int64_t p0 = ff ? (-OFF + i) : (1 - (nb - 1) * RB + (i - nF));
+    const int64_t step = ff ? -RB : RB;
     long long acc = 0;
-    if (i < nF) {
-        const int64_t p0 = -OFF + i;  // p0 in [-OFF, W-2 + (nb-1) RB]
-        for (int64_t b = 0; b < nb; ++b) {
-            const int64_t p = p0 - b * RB;
-            if (p < -OFF) break;
-            if (p >= W - 1) {
-                acc = st_ptr(a, b, k, 0)[W - 1 + OFF];  // inclusive S(W-1)
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
+        long long v[SCAN_BATCH];
+        int kind[SCAN_BATCH];  // 0 skip/stop, 1 accumulate+store, 2 clamp (FF: acc = S(W-1); GG: acc = 0)
+#pragma unroll
+        for (int j = 0; j < SCAN_BATCH; ++j) {
+            const int64_t b = b0 + j;
+            const int64_t p = p0 + b * step;
+            v[j] = 0;
+            kind[j] = 0;
+            if (b >= nb) continue;
+            if (ff) {
+                if (p < -OFF) continue;
+                if (p >= W - 1) { kind[j] = 2; v[j] = st_ptr(a, b, k, 0)[W - 1 + OFF]; }
+                else { kind[j] = 1; v[j] = st_ptr(a, b, k, 1)[p + OFF]; }
             } else {
-                long long* q = st_ptr(a, b, k, 1) + p + OFF;
-                acc += *q;
-                *q = acc;
+                if (p > W + RB) continue;
+                if (p <= 0) { kind[j] = 2; }
+                else { kind[j] = 1; v[j] = st_ptr(a, b, k, 2)[p + OFF]; }
             }
         }
-    } else {
-        const int64_t p0 = 1 - (nb - 1) * RB + (i - nF);  // p0 in [1-(nb-1)RB, W+RB]
-        for (int64_t b = 0; b < nb; ++b) {
-            const int64_t p = p0 + b * RB;
-            if (p > W + RB) break;
-            if (p <= 0) {
-                acc = 0;
-            } else {
-                long long* q = st_ptr(a, b, k, 2) + p + OFF;
-                acc += *q;
-                *q = acc;
+#pragma unroll
+        for (int j = 0; j < SCAN_BATCH; ++j) {
+            if (kind[j] == 2) {
+                acc = v[j];
+            } else if (kind[j] == 1) {
+                acc += v[j];
+                const int64_t p = p0 + (b0 + j) * step;
+                st_ptr(a, b0 + j, k, ff ? 1 : 2)[p + OFF] = acc;
             }
         }
     }

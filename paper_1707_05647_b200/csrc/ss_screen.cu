@@ -28,15 +28,15 @@
 #include <climits>
 #include <cmath>
 
+#include <cuda.h>
+
 #include "ss_common.cuh"
 
 namespace ss {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int WARPS = 8;   // rows per CTA
-constexpr int CHUNKS = 8;  // 32-centre chunks per warp
-constexpr int SEG = 32 * CHUNKS;
+constexpr int WARPS = 8;   // consumer warps per CTA (one tile row each)
 constexpr int QCAP = 64;
 constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
 
@@ -183,74 +183,172 @@ __device__ __forceinline__ bool finish_of(const ScreenArgs& a, const RingDev& R,
     return member_k(a, R, sb, s.cm, cs, cg);
 }
 
-__global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) {
-    extern __shared__ unsigned sbits[];
-    // Q1: ring-0 stage-1 passers with their stage-1 state; QN: (x, ring) pairs for rings >= 1
-    __shared__ int q_x[WARPS][QCAP];
+// ── TMA / mbarrier helpers (sm_90+ PTX, used on sm_100a) ──────────────────
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
+}
+
+struct TmaMaps {
+    CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) int64
+};
+
+// Tile geometry: TY rows (one per consumer warp) x TX columns; the 8 ring-0
+// PLAIN corner boxes of a tile are staged by TMA into one pipeline stage.
+constexpr int CW_ = WARPS;           // consumer warps
+constexpr int TY = CW_;              // tile rows
+constexpr int TX = 32;               // tile columns (one chunk per warp)
+constexpr int NBOX = 8;
+constexpr int STAGES = 4;
+constexpr int BOX_BYTES = TX * TY * 8;
+constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+
+struct TileMap {
+    int n_tx, n_ty;        // tiles along x, y
+    int strip;             // tiles per column strip (L2 locality for wide images)
+    long long n_tiles;
+};
+
+__device__ __forceinline__ void tile_coords(const TileMap& t, long long idx, int& tx, int& ty) {
+    // strip-major: strips of `strip` tile columns, row-blocks within a strip, x fastest
+    const long long per_strip = (long long)t.strip * t.n_ty;
+    const long long s = idx / per_strip;
+    const int s0 = (int)(s * t.strip);
+    const int width = min(t.strip, t.n_tx - s0);
+    const long long r = idx - s * per_strip;
+    ty = (int)(r / width);
+    tx = s0 + (int)(r % width);
+}
+
+__global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
+                                                                  const TileMap tm) {
+    extern __shared__ __align__(128) unsigned char dsmem[];
+    unsigned char* stage_buf = dsmem;                                // STAGES x STAGE_BYTES
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    // Q1: ring-0 stage-1 passers with their stage-1 state; QN: (x, y, ring) for rings >= 1
+    __shared__ int q_x[WARPS][QCAP], q_y[WARPS][QCAP];
     __shared__ int q_cm[WARPS][QCAP];
     __shared__ double q_mq[WARPS][QCAP], q_md[WARPS][QCAP];
     __shared__ long long q_s1q[WARPS][QCAP], q_s1d[WARPS][QCAP];
-    __shared__ int qn_x[WARPS][QCAP];
+    __shared__ int qn_x[WARPS][QCAP], qn_y[WARPS][QCAP];
     __shared__ unsigned char qn_r[WARPS][QCAP];
-    __shared__ unsigned s_mask[WARPS][CHUNKS];
 
-    // stage the rings' membership bitmaps
-    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
     for (int r = 0; r < a.n_rings; ++r) {
         const RingDev& R = a.ring[r];
         if (R.bm < 0) continue;
-        for (int i = tid; i < R.bwords; i += WARPS * 32) sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
+        for (int i = threadIdx.x; i < R.bwords; i += (WARPS + 1) * 32)
+            sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    const int lane = threadIdx.x, warp = threadIdx.y;
-    const int y = a.y_begin + blockIdx.y * WARPS + warp;
-    if (y >= a.y_end) return;  // warp-uniform; no block barriers below
-    const int x0 = blockIdx.x * SEG;
-    const int cy = y - a.y_origin;  // table-local row: features are frame-invariant
-    const bool row_grid = (y % a.stride) == 0;
-    const bool row_int = row_grid && y >= a.lo && y <= a.H - 1 - a.hi;
-    const long long* rowp = a.planes + (long long)cy * a.pitch;
     const RingDev& R0 = a.ring[0];
+    const int ylo = a.lo, yhi = a.H - 1 - a.hi, xlo = a.lo, xhi = a.W - 1 - a.hi;
+
+    if (warp == WARPS) {
+        // ── producer: one lane streams the tiles' corner boxes ──────────────
+        if (lane == 0) {
+            int it = 0;
+            for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
+                const int s = it % STAGES;
+                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+                int tx, ty;
+                tile_coords(tm, t, tx, ty);
+                const int x0 = tx * TX;
+                const int cy0 = a.y_begin + ty * TY - a.y_origin;  // table-local first row
+                unsigned char* dst = stage_buf + s * STAGE_BYTES;
+                mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+                // plane coordinates are (col = x + 1, row = y + 1) of the corner (include/starscreen_b200.h)
+                tma_load_2d(dst + 0 * BOX_BYTES, &maps.sat, x0 + R0.n + 1, cy0 + R0.n + 1, &full_bar[s]);
+                tma_load_2d(dst + 1 * BOX_BYTES, &maps.sat, x0 - R0.n + 1, cy0 + R0.n + 1, &full_bar[s]);
+                tma_load_2d(dst + 2 * BOX_BYTES, &maps.sat, x0 + R0.n + 1, cy0 - R0.n + 1, &full_bar[s]);
+                tma_load_2d(dst + 3 * BOX_BYTES, &maps.sat, x0 - R0.n + 1, cy0 - R0.n + 1, &full_bar[s]);
+                tma_load_2d(dst + 4 * BOX_BYTES, &maps.e, x0 + 1, cy0 + R0.d + 1, &full_bar[s]);
+                tma_load_2d(dst + 5 * BOX_BYTES, &maps.e, x0 + 1, cy0 - R0.d, &full_bar[s]);
+                tma_load_2d(dst + 6 * BOX_BYTES, &maps.o, x0 - R0.d, cy0, &full_bar[s]);
+                tma_load_2d(dst + 7 * BOX_BYTES, &maps.o, x0 + R0.d + 1, cy0, &full_bar[s]);
+            }
+        }
+        return;
+    }
+
+    // ── consumers: warp w takes row w of each tile ───────────────────────────
     const unsigned lt = (1u << lane) - 1u;
     const bool inst = a.stage_counts != nullptr;
-
-    int n1 = 0, nn = 0;  // queue lengths
-    unsigned surv_count = 0;
+    int n1 = 0, nn = 0;
     unsigned long long st0 = 0, st1 = 0, st2 = 0, st3 = 0;
 
-    auto survive = [&](bool keep, int x) {
+    auto survive = [&](bool keep, int x, int y) {
         if (keep) {
-            const int off = x - x0;
-            atomicOr(&s_mask[warp][off >> 5], 1u << (off & 31));
+            const long long row = y - a.y_begin;
+            atomicOr(a.mask + row * a.mask_pitch + (x >> 5), 1u << (x & 31));
+            atomicAdd(a.row_counts + row, 1u);
         }
-        surv_count += __popc(__ballot_sync(FULL, keep));
     };
-    auto push_next = [&](bool push, int x, int r) {
+    auto push_next = [&](bool push, int x, int y, int r) {
         const unsigned b = __ballot_sync(FULL, push);
         if (push) {
             const int e = nn + __popc(b & lt);
             qn_x[warp][e] = x;
+            qn_y[warp][e] = y;
             qn_r[warp][e] = (unsigned char)r;
         }
         nn += __popc(b);
         __syncwarp();
     };
-    // ring-0 stages 2-3 for Q1 entries [n1 - cnt, n1)
+    // ring-0 stages 2-3 for Q1 entries [n1 - cnt, n1), one per lane
     auto drain1 = [&](int cnt) {
         bool keep = false, more = false;
-        int x = 0;
+        int x = 0, y = 0;
         if (lane < cnt) {
             const int e = n1 - cnt + lane;
             x = q_x[warp][e];
+            y = q_y[warp][e];
             Stage1 s;
             s.cm = q_cm[warp][e];
             s.mq = q_mq[warp][e];
             s.md = q_md[warp][e];
             s.s1q = q_s1q[warp][e];
             s.s1d = q_s1d[warp][e];
-            const long long* pc = rowp + x;
+            const int cy = y - a.y_origin;
+            const long long* pc = a.planes + (long long)cy * a.pitch + x;
             Corners c2, cxk, cyk;
             load_corners(a, R0, pc, 3, c2);
             load_corners(a, R0, pc, 1, cxk);
@@ -263,23 +361,25 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
         }
         n1 -= cnt;
         __syncwarp();
-        survive(keep, x);
-        push_next(more, x, 1);
+        survive(keep, x, y);
+        push_next(more, x, y, 1);
     };
     // one full ring evaluation for QN entries [nn - cnt, nn)
     auto drainN = [&](int cnt) {
         bool keep = false, more = false;
-        int x = 0, r = 0;
+        int x = 0, y = 0, r = 0;
         if (lane < cnt) {
             const int e = nn - cnt + lane;
             x = qn_x[warp][e];
+            y = qn_y[warp][e];
             r = qn_r[warp][e];
         }
         nn -= cnt;
         __syncwarp();
         if (lane < cnt) {
             const RingDev& R = a.ring[r];
-            const long long* pc = rowp + x;
+            const int cy = y - a.y_origin;
+            const long long* pc = a.planes + (long long)cy * a.pitch + x;
             Corners c0, c2, cxk, cyk;
             load_corners(a, R, pc, 0, c0);
             load_corners(a, R, pc, 3, c2);
@@ -292,28 +392,40 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
             keep = pass && r + 1 == a.n_rings;
             more = pass && r + 1 < a.n_rings;
         }
-        survive(keep, x);
-        push_next(more, x, r + 1);
+        survive(keep, x, y);
+        push_next(more, x, y, r + 1);
     };
 
-    // stage 1 of ring 0 over the segment, software-pipelined one chunk ahead
-    // (only centres inside the evaluable interior are loaded: their corners are in bounds)
-    auto in_interior = [&](int xx) { return row_int && xx >= a.lo && xx <= a.W - 1 - a.hi; };
-    Corners cur, nxt;
-    if (in_interior(x0 + lane)) load_corners(a, R0, rowp + x0 + lane, 0, cur);
-#pragma unroll 1
-    for (int c = 0; c < CHUNKS; ++c) {
-        const int x = x0 + c * 32 + lane;
-        if (c + 1 < CHUNKS && in_interior(x + 32)) load_corners(a, R0, rowp + x + 32, 0, nxt);
+    int it = 0;
+    for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        int tx, ty;
+        tile_coords(tm, t, tx, ty);
+        const int y = a.y_begin + ty * TY + warp;
+        const int x = tx * TX + lane;
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * TX + lane;
+        constexpr int BOX = TX * TY;
+        const long long s1q = box[0 * BOX] - box[1 * BOX] - box[2 * BOX] + box[3 * BOX];
+        const long long s1d = box[4 * BOX] - box[6 * BOX] - box[7 * BOX] + box[5 * BOX];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        if (y >= a.y_end) continue;  // warp-uniform (past the last row)
+        const bool row_grid = (y % a.stride) == 0;
         const bool on_grid = row_grid && x < a.W && (x % a.stride) == 0;
-        const bool interior = row_int && on_grid && x >= a.lo && x <= a.W - 1 - a.hi;
+        const bool interior = on_grid && y >= ylo && y <= yhi && x >= xlo && x <= xhi;
         const unsigned border = __ballot_sync(FULL, on_grid && !interior);
-        if (lane == 0) s_mask[warp][c] = border;
+        if (lane == 0 && tx * TX < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + tx] = border;
+        __syncwarp();
         bool pass = false;
-        Stage1 s;
+        Stage1 st;
         if (interior) {
-            s = stage1_of(a, R0, cur);
-            pass = member_m(a, R0, sbits, s.cm);
+            st.s1q = s1q;
+            st.s1d = s1d;
+            st.mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);                   // features.py:325
+            st.md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);                   // features.py:349
+            st.cm = quant(__dmul_rn(__dadd_rn(st.mq, st.md), 0.5), a.qm, a.rqm);  // features.py:365
+            pass = member_m(a, R0, sbits, st.cm);
         }
         const unsigned pb = __ballot_sync(FULL, pass);
         if (inst) {
@@ -323,27 +435,20 @@ __global__ void __launch_bounds__(WARPS * 32) screen_kernel(const ScreenArgs a) 
         if (pass) {
             const int e = n1 + __popc(pb & lt);
             q_x[warp][e] = x;
-            q_cm[warp][e] = s.cm;
-            q_mq[warp][e] = s.mq;
-            q_md[warp][e] = s.md;
-            q_s1q[warp][e] = s.s1q;
-            q_s1d[warp][e] = s.s1d;
+            q_y[warp][e] = y;
+            q_cm[warp][e] = st.cm;
+            q_mq[warp][e] = st.mq;
+            q_md[warp][e] = st.md;
+            q_s1q[warp][e] = st.s1q;
+            q_s1d[warp][e] = st.s1d;
         }
         n1 += __popc(pb);
         __syncwarp();
         if (n1 >= 32) drain1(32);
         while (nn >= 32) drainN(32);
-        cur = nxt;
     }
     if (n1 > 0) drain1(n1);
     while (nn > 0) drainN(nn < 32 ? nn : 32);
-    __syncwarp();
-    const long long row = y - a.y_begin;
-    if (lane < CHUNKS) {
-        const int w = blockIdx.x * CHUNKS + lane;
-        if (w * 32 < a.W) a.mask[row * a.mask_pitch + w] = s_mask[warp][lane];
-    }
-    if (lane == 0 && surv_count) atomicAdd(a.row_counts + row, surv_count);
     if (inst) {
         unsigned long long v[4] = {st0, st1, st2, st3};
 #pragma unroll
@@ -397,6 +502,35 @@ __global__ void selftest_div_kernel(unsigned long long n, unsigned long long see
 }
 
 }  // namespace
+
+// 2-D TMA descriptor of one int64 plane: dims (W+1 columns, h+1 rows), box TX x TY.
+static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, int64_t h, int64_t pitch) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return SS_ECUDA;
+        }
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)TX, (cuuint32_t)TY};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<int64_t*>(plane), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return SS_ECUDA;
+    }
+    return SS_OK;
+}
 
 int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
                 int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings, const int32_t* ring_n,
@@ -516,10 +650,32 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     const int64_t rows = y_end - y_begin;
     if (rows == 0) return SS_OK;
     if (cudaMemsetAsync(d_row_counts, 0, rows * sizeof(uint32_t), s) != cudaSuccess) return check_launch("memset");
-    const size_t smem = (size_t)std::max(smem_words, 1) * 4;
-    if (smem > 32 * 1024) cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((unsigned)((W + SEG - 1) / SEG), (unsigned)((rows + WARPS - 1) / WARPS));
-    screen_kernel<<<grid, dim3(32, WARPS), smem, s>>>(a);
+    // the mask rows are (re)initialised by the kernel; survivors are OR'ed in
+    TmaMaps maps;
+    if (int e = encode_plane_map(&maps.sat, d_planes, W, h, pitch)) return e;
+    if (int e = encode_plane_map(&maps.e, d_planes + 4 * a.ps, W, h, pitch)) return e;
+    if (int e = encode_plane_map(&maps.o, d_planes + 8 * a.ps, W, h, pitch)) return e;
+    TileMap tm;
+    tm.n_tx = (int)((W + TX - 1) / TX);
+    tm.n_ty = (int)((rows + TY - 1) / TY);
+    // column strips keep the rows a tile's corners revisit (2n apart) resident
+    // in L2: (m + rows in flight) x strip width x 24 B (PLAIN SAT/E/O) <~ 48 MB
+    {
+        const int64_t budget = 48ll << 20;
+        const int64_t rows_in_flight = 148LL * 2 * TY;
+        int64_t width = budget / ((int64_t)(m + rows_in_flight) * 24);
+        int strip = (int)std::max<int64_t>(1, width / TX);
+        tm.strip = std::min(strip, tm.n_tx);
+    }
+    tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
+    const size_t smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(smem_words, 1) * 4;
+    cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, screen_kernel, (WARPS + 1) * 32, smem);
+    const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * std::max(per_sm, 1));
+    screen_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, smem, s>>>(a, maps, tm);
     note_launch();
     return check_launch("screen_kernel");
 }
