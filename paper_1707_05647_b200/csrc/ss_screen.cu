@@ -223,13 +223,20 @@ struct TmaMaps {
 
 // Tile geometry: TY rows (one per consumer warp) x TX columns; the 8 ring-0
 // PLAIN corner boxes of a tile are staged by TMA into one pipeline stage.
-constexpr int CW_ = WARPS;           // consumer warps
-constexpr int TY = CW_;              // tile rows
+// Measured on B200 + driver 580: a tile-mode TMA box must start at a 16-byte
+// aligned inner coordinate (an odd int64 column raises "illegal
+// instruction"), so each box starts at the even column at or below the
+// corner and is BW = TX + 2 columns wide; readers skip the parity offset.
+constexpr int TY = WARPS;            // tile rows
 constexpr int TX = 32;               // tile columns (one chunk per warp)
+constexpr int BW = TX + 2;           // staged box width (int64 columns)
 constexpr int NBOX = 8;
 constexpr int STAGES = 4;
-constexpr int BOX_BYTES = TX * TY * 8;
+constexpr int BOX_ELEMS = BW * TY;
+constexpr int BOX_BYTES = BOX_ELEMS * 8;
 constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+
+__device__ __forceinline__ int floor_even(int c) { return c & ~1; }  // two's complement: floor to even
 
 struct TileMap {
     int n_tx, n_ty;        // tiles along x, y
@@ -296,14 +303,15 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
                 unsigned char* dst = stage_buf + s * STAGE_BYTES;
                 mbar_expect_tx(&full_bar[s], STAGE_BYTES);
                 // plane coordinates are (col = x + 1, row = y + 1) of the corner (include/starscreen_b200.h)
-                tma_load_2d(dst + 0 * BOX_BYTES, &maps.sat, x0 + R0.n + 1, cy0 + R0.n + 1, &full_bar[s]);
-                tma_load_2d(dst + 1 * BOX_BYTES, &maps.sat, x0 - R0.n + 1, cy0 + R0.n + 1, &full_bar[s]);
-                tma_load_2d(dst + 2 * BOX_BYTES, &maps.sat, x0 + R0.n + 1, cy0 - R0.n + 1, &full_bar[s]);
-                tma_load_2d(dst + 3 * BOX_BYTES, &maps.sat, x0 - R0.n + 1, cy0 - R0.n + 1, &full_bar[s]);
-                tma_load_2d(dst + 4 * BOX_BYTES, &maps.e, x0 + 1, cy0 + R0.d + 1, &full_bar[s]);
-                tma_load_2d(dst + 5 * BOX_BYTES, &maps.e, x0 + 1, cy0 - R0.d, &full_bar[s]);
-                tma_load_2d(dst + 6 * BOX_BYTES, &maps.o, x0 - R0.d, cy0, &full_bar[s]);
-                tma_load_2d(dst + 7 * BOX_BYTES, &maps.o, x0 + R0.d + 1, cy0, &full_bar[s]);
+                const int n = R0.n, d = R0.d;
+                tma_load_2d(dst + 0 * BOX_BYTES, &maps.sat, floor_even(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 1 * BOX_BYTES, &maps.sat, floor_even(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 2 * BOX_BYTES, &maps.sat, floor_even(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 3 * BOX_BYTES, &maps.sat, floor_even(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 4 * BOX_BYTES, &maps.e, floor_even(x0 + 1), cy0 + d + 1, &full_bar[s]);
+                tma_load_2d(dst + 5 * BOX_BYTES, &maps.e, floor_even(x0 + 1), cy0 - d, &full_bar[s]);
+                tma_load_2d(dst + 6 * BOX_BYTES, &maps.o, floor_even(x0 - d), cy0, &full_bar[s]);
+                tma_load_2d(dst + 7 * BOX_BYTES, &maps.o, floor_even(x0 + d + 1), cy0, &full_bar[s]);
             }
         }
         return;
@@ -404,10 +412,13 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         const int y = a.y_begin + ty * TY + warp;
         const int x = tx * TX + lane;
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
-        const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * TX + lane;
-        constexpr int BOX = TX * TY;
-        const long long s1q = box[0 * BOX] - box[1 * BOX] - box[2 * BOX] + box[3 * BOX];
-        const long long s1d = box[4 * BOX] - box[6 * BOX] - box[7 * BOX] + box[5 * BOX];
+        // x0 is even, so each box's parity offset depends on the ring only
+        const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
+        const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;
+        const long long s1q = box[0 * BOX_ELEMS + pq] - box[1 * BOX_ELEMS + pq] - box[2 * BOX_ELEMS + pq] +
+                              box[3 * BOX_ELEMS + pq];
+        const long long s1d = box[4 * BOX_ELEMS + pe] - box[6 * BOX_ELEMS + po0] - box[7 * BOX_ELEMS + po1] +
+                              box[5 * BOX_ELEMS + pe];
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
         if (y >= a.y_end) continue;  // warp-uniform (past the last row)
@@ -520,7 +531,7 @@ static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, i
     }
     const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
     const cuuint64_t strides[1] = {(cuuint64_t)pitch * 8};
-    const cuuint32_t box[2] = {(cuuint32_t)TX, (cuuint32_t)TY};
+    const cuuint32_t box[2] = {(cuuint32_t)BW, (cuuint32_t)TY};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<int64_t*>(plane), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
