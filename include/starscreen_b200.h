@@ -95,8 +95,9 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
  * d_row_counts.  h_ring_n / h_ring_d: ring_plan(m) (features.py:190-211).
  * d_blob: the ss_keyset_blob() layout copied to the device.  d_stage_counts
  * (nullable, 4 x u64, accumulated) instruments the early-exit cascade:
- * ring-0 evaluations, ring-0 centres reaching the std stage, reaching the
- * gradient stage, and evaluations of rings >= 1.
+ * ring-0 evaluations (every interior centre), ring-0 mean-projection
+ * passes, centres passing every ring's mean test (they read the SQUARED /
+ * X / Y planes), and ring-0 full passes (they go on to rings >= 1).
  */
 int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_pitch, int64_t W, int64_t H,
                    int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,

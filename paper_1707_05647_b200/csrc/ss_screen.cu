@@ -231,10 +231,18 @@ constexpr int TY = WARPS;            // tile rows
 constexpr int TX = 32;               // tile columns (one chunk per warp)
 constexpr int BW = TX + 2;           // staged box width (int64 columns)
 constexpr int NBOX = 8;
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int BOX_ELEMS = BW * TY;
 constexpr int BOX_BYTES = BOX_ELEMS * 8;
 constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+
+// payload of a queued centre: its ring-0 stage-1 state
+struct Entry {
+    int x, y, cm;
+    double mq, md;
+    long long s1q, s1d;
+};
+constexpr int QUEUE_BYTES = WARPS * QCAP * (int)sizeof(Entry);
 
 __device__ __forceinline__ int floor_even(int c) { return c & ~1; }  // two's complement: floor to even
 
@@ -259,13 +267,14 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
                                                                   const TileMap tm) {
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;                                // STAGES x STAGE_BYTES
-    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES + 2 * QUEUE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-    // Q1: ring-0 stage-1 passers with their stage-1 state; QN: (x, y, ring) for rings >= 1
-    __shared__ int q_x[WARPS][QCAP], q_y[WARPS][QCAP];
-    __shared__ int q_cm[WARPS][QCAP];
-    __shared__ double q_mq[WARPS][QCAP], q_md[WARPS][QCAP];
-    __shared__ long long q_s1q[WARPS][QCAP], q_s1d[WARPS][QCAP];
+    // Work queues (per consumer warp), each drained 32 entries at a time:
+    //   QA: ring-0 mean passers (ring-0 stage-1 state) -> mean tests of rings >= 1
+    //   QB: centres whose every ring passed the mean test -> ring-0 std/gradient
+    //   QN: (x, y, ring) -> full evaluation of ring >= 1
+    Entry(*qa)[QCAP] = reinterpret_cast<Entry(*)[QCAP]>(dsmem + STAGES * STAGE_BYTES);
+    Entry(*qb)[QCAP] = reinterpret_cast<Entry(*)[QCAP]>(dsmem + STAGES * STAGE_BYTES + QUEUE_BYTES);
     __shared__ int qn_x[WARPS][QCAP], qn_y[WARPS][QCAP];
     __shared__ unsigned char qn_r[WARPS][QCAP];
 
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
     // ── consumers: warp w takes row w of each tile ───────────────────────────
     const unsigned lt = (1u << lane) - 1u;
     const bool inst = a.stage_counts != nullptr;
-    int n1 = 0, nn = 0;
+    int na = 0, nb = 0, nn = 0;
     unsigned long long st0 = 0, st1 = 0, st2 = 0, st3 = 0;
 
     auto survive = [&](bool keep, int x, int y) {
@@ -330,7 +339,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
             atomicAdd(a.row_counts + row, 1u);
         }
     };
-    auto push_next = [&](bool push, int x, int y, int r) {
+    auto push_n = [&](bool push, int x, int y, int r) {
         const unsigned b = __ballot_sync(FULL, push);
         if (push) {
             const int e = nn + __popc(b & lt);
@@ -341,20 +350,50 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         nn += __popc(b);
         __syncwarp();
     };
-    // ring-0 stages 2-3 for Q1 entries [n1 - cnt, n1), one per lane
-    auto drain1 = [&](int cnt) {
+    // QA: mean tests of rings 1.. (PLAIN corners only, all rings' loads issued together)
+    auto drainA = [&](int cnt) {
+        bool pass = false;
+        Entry en;
+        if (lane < cnt) {
+            en = qa[warp][na - cnt + lane];
+            const long long* pc = a.planes + (long long)(en.y - a.y_origin) * a.pitch + en.x;
+            pass = true;
+            constexpr int BATCH = 2;
+            for (int r0 = 1; r0 < a.n_rings && pass; r0 += BATCH) {
+                Corners c[BATCH];
+#pragma unroll
+                for (int j = 0; j < BATCH; ++j)
+                    if (r0 + j < a.n_rings) load_corners(a, a.ring[r0 + j], pc, 0, c[j]);
+#pragma unroll
+                for (int j = 0; j < BATCH; ++j)
+                    if (r0 + j < a.n_rings && pass) {
+                        const RingDev& R = a.ring[r0 + j];
+                        pass = member_m(a, R, sbits, stage1_of(a, R, c[j]).cm);
+                    }
+            }
+        }
+        na -= cnt;
+        __syncwarp();
+        const unsigned b = __ballot_sync(FULL, pass);
+        if (pass) qb[warp][nb + __popc(b & lt)] = en;
+        nb += __popc(b);
+        st2 += (lane == 0) ? __popc(b) : 0;
+        __syncwarp();
+    };
+    // QB: ring-0 std / gradient stages (SQUARED, X, Y corners in one round trip)
+    auto drainB = [&](int cnt) {
         bool keep = false, more = false;
         int x = 0, y = 0;
         if (lane < cnt) {
-            const int e = n1 - cnt + lane;
-            x = q_x[warp][e];
-            y = q_y[warp][e];
+            const Entry en = qb[warp][nb - cnt + lane];
+            x = en.x;
+            y = en.y;
             Stage1 s;
-            s.cm = q_cm[warp][e];
-            s.mq = q_mq[warp][e];
-            s.md = q_md[warp][e];
-            s.s1q = q_s1q[warp][e];
-            s.s1d = q_s1d[warp][e];
+            s.cm = en.cm;
+            s.mq = en.mq;
+            s.md = en.md;
+            s.s1q = en.s1q;
+            s.s1d = en.s1d;
             const int cy = y - a.y_origin;
             const long long* pc = a.planes + (long long)cy * a.pitch + x;
             Corners c2, cxk, cyk;
@@ -363,16 +402,16 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
             load_corners(a, R0, pc, 2, cyk);
             bool grad = false;
             const bool pass = finish_of(a, R0, sbits, x, cy, s, c2, cxk, cyk, grad);
-            st2 += grad;
             keep = pass && a.n_rings == 1;
             more = pass && a.n_rings > 1;
         }
-        n1 -= cnt;
+        nb -= cnt;
         __syncwarp();
         survive(keep, x, y);
-        push_next(more, x, y, 1);
+        push_n(more, x, y, 1);
+        st3 += (lane == 0) ? __popc(__ballot_sync(FULL, more)) : 0;
     };
-    // one full ring evaluation for QN entries [nn - cnt, nn)
+    // QN: full evaluation of ring r >= 1 (its mean test already passed in QA)
     auto drainN = [&](int cnt) {
         bool keep = false, more = false;
         int x = 0, y = 0, r = 0;
@@ -393,15 +432,23 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
             load_corners(a, R, pc, 3, c2);
             load_corners(a, R, pc, 1, cxk);
             load_corners(a, R, pc, 2, cyk);
-            ++st3;
             const Stage1 t = stage1_of(a, R, c0);
             bool grad = false;
-            const bool pass = member_m(a, R, sbits, t.cm) && finish_of(a, R, sbits, x, cy, t, c2, cxk, cyk, grad);
+            const bool pass = finish_of(a, R, sbits, x, cy, t, c2, cxk, cyk, grad);
             keep = pass && r + 1 == a.n_rings;
             more = pass && r + 1 < a.n_rings;
         }
         survive(keep, x, y);
-        push_next(more, x, y, r + 1);
+        push_n(more, x, y, r + 1);
+    };
+    auto service = [&](bool flush) {
+        // drain deeper queues first so every queue stays below QCAP
+        for (;;) {
+            if (nn >= 32 || (flush && nn > 0)) { drainN(nn < 32 ? nn : 32); continue; }
+            if (nb >= 32 || (flush && nb > 0)) { drainB(nb < 32 ? nb : 32); continue; }
+            if (na >= 32 || (flush && na > 0)) { drainA(na < 32 ? na : 32); continue; }
+            break;
+        }
     };
 
     int it = 0;
@@ -429,42 +476,35 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         if (lane == 0 && tx * TX < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + tx] = border;
         __syncwarp();
         bool pass = false;
-        Stage1 st;
+        Entry en;
         if (interior) {
-            st.s1q = s1q;
-            st.s1d = s1d;
-            st.mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);                   // features.py:325
-            st.md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);                   // features.py:349
-            st.cm = quant(__dmul_rn(__dadd_rn(st.mq, st.md), 0.5), a.qm, a.rqm);  // features.py:365
-            pass = member_m(a, R0, sbits, st.cm);
+            en.x = x;
+            en.y = y;
+            en.s1q = s1q;
+            en.s1d = s1d;
+            en.mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);                   // features.py:325
+            en.md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);                   // features.py:349
+            en.cm = quant(__dmul_rn(__dadd_rn(en.mq, en.md), 0.5), a.qm, a.rqm);  // features.py:365
+            pass = member_m(a, R0, sbits, en.cm);
         }
         const unsigned pb = __ballot_sync(FULL, pass);
-        if (inst) {
+        if (inst && lane == 0) {
             st0 += __popc(__ballot_sync(FULL, interior));
             st1 += __popc(pb);
+        } else if (inst) {
+            __ballot_sync(FULL, interior);
         }
-        if (pass) {
-            const int e = n1 + __popc(pb & lt);
-            q_x[warp][e] = x;
-            q_y[warp][e] = y;
-            q_cm[warp][e] = st.cm;
-            q_mq[warp][e] = st.mq;
-            q_md[warp][e] = st.md;
-            q_s1q[warp][e] = st.s1q;
-            q_s1d[warp][e] = st.s1d;
-        }
-        n1 += __popc(pb);
+        if (pass) qa[warp][na + __popc(pb & lt)] = en;
+        na += __popc(pb);
         __syncwarp();
-        if (n1 >= 32) drain1(32);
-        while (nn >= 32) drainN(32);
+        service(false);
     }
-    if (n1 > 0) drain1(n1);
-    while (nn > 0) drainN(nn < 32 ? nn : 32);
+    service(true);
     if (inst) {
         unsigned long long v[4] = {st0, st1, st2, st3};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            unsigned long long t = (i < 2) ? (lane == 0 ? v[i] : 0ull) : v[i];  // st0/st1 are warp totals
+            unsigned long long t = v[i];
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) t += __shfl_down_sync(FULL, t, d);
             if (lane == 0 && t) atomicAdd(a.stage_counts + i, t);
@@ -679,7 +719,7 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         tm.strip = std::min(strip, tm.n_tx);
     }
     tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
-    const size_t smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(smem_words, 1) * 4;
+    const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * (size_t)QUEUE_BYTES + (size_t)std::max(smem_words, 1) * 4;
     cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
