@@ -408,8 +408,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         nb -= cnt;
         __syncwarp();
         survive(keep, x, y);
+        const unsigned mb = __ballot_sync(FULL, more);
+        st3 += (lane == 0) ? __popc(mb) : 0;
         push_n(more, x, y, 1);
-        st3 += (lane == 0) ? __popc(__ballot_sync(FULL, more)) : 0;
     };
     // QN: full evaluation of ring r >= 1 (its mean test already passed in QA)
     auto drainN = [&](int cnt) {
@@ -488,11 +489,10 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
             pass = member_m(a, R0, sbits, en.cm);
         }
         const unsigned pb = __ballot_sync(FULL, pass);
+        const unsigned ib = __ballot_sync(FULL, interior);
         if (inst && lane == 0) {
-            st0 += __popc(__ballot_sync(FULL, interior));
+            st0 += __popc(ib);
             st1 += __popc(pb);
-        } else if (inst) {
-            __ballot_sync(FULL, interior);
         }
         if (pass) qa[warp][na + __popc(pb & lt)] = en;
         na += __popc(pb);
