@@ -327,11 +327,10 @@ def run_ours(args):
     # ── roofline of the dominant kernel (K3 screen) ──
     peak, peak_src = measured_peak_hbm()
     # algorithmic bytes: every ring-0 evaluation
-    # needs the 3 PLAIN planes (24 B/position); centres that pass every
-    # ring's mean test also need the 9 SQUARED/X/Y planes (72 B); +1/8 B mask
-    # bit.  SURVEY.md 8(d)'s dense figure (all 12 planes, 96 B) is reported
-    # beside it.
-    alg_bytes = 24.0 * stage[0] + 72.0 * stage[2] + positions / 8.0
+    # needs the 3 PLAIN planes (24 B/position); candidates (ring-0 mean
+    # passers) also need the 9 SQUARED/X/Y planes (72 B); +1/8 B mask bit.
+    # SURVEY.md 8(d)'s dense figure (all 12 planes, 96 B) is reported beside it.
+    alg_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
     achieved = alg_bytes / (screen_ms / 1e3) / 1e9
     dense_bytes = 96.125 * positions
     roofline = {
@@ -339,8 +338,8 @@ def run_ours(args):
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
         "peak_source": peak_src,
         "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": alg_bytes / max(positions, 1),
-        "cascade": {"ring0_evals": stage[0], "ring0_mean_pass": stage[1], "all_rings_mean_pass": stage[2],
-                    "ring0_pass": stage[3]},
+        "cascade": {"ring0_evals": stage[0], "ring0_mean_pass": stage[1], "ring0_pass": stage[2],
+                    "survivors": stage[3]},
         "screen_ms_per_step": screen_ms, "screen_share_of_step": screen_ms / (total_ms / args.steps),
         "survey_dense_bytes_per_position": 96.125,
         "survey_dense_equiv_GBps": dense_bytes / (screen_ms / 1e3) / 1e9,

@@ -96,14 +96,17 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
  * d_blob: the ss_keyset_blob() layout copied to the device.  d_stage_counts
  * (nullable, 4 x u64, accumulated) instruments the early-exit cascade:
  * ring-0 evaluations (every interior centre), ring-0 mean-projection
- * passes, centres passing every ring's mean test (they read the SQUARED /
- * X / Y planes), and ring-0 full passes (they go on to rings >= 1).
+ * passes (candidates that read the SQUARED / X / Y planes), ring-0 full
+ * passes, and final survivors.
  */
 int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_pitch, int64_t W, int64_t H,
                    int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,
                    const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
                    double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
-                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* stream);
+                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* d_workspace,
+                   size_t workspace_bytes, void* stream);
+/* Bytes of device workspace ss_screen_size needs for `rows` decided rows. */
+size_t ss_screen_workspace_bytes(int64_t W, int64_t rows);
 
 /*
  * Device self-test of the screen's division routine: counts operands of

@@ -13,17 +13,22 @@
 // i.e. identical to IEEE division (ss_selftest_div checks it against
 // __ddiv_rn on the device; the parity tests check the whole path).
 //
-// Work decomposition: a warp owns a 256-centre segment of one row (8 chunks
-// of 32).  Stage 1 of ring 0 -- the mean cell, from the PLAIN planes only --
-// runs on all lanes.  A centre can only be a member if its mean cell is in
-// the ring's mean projection, so only those centres are pushed into a
-// per-warp shared-memory queue and finished (std stage on the SQUARED
-// planes, gradient stage on the X/Y planes, then rings >= 1) 32 at a time
-// with full lanes.  The decision is unchanged -- the projection tests are
-// implied by full membership -- but the X/Y/SQ planes and most fp64 work are
-// skipped for most centres and lane divergence stays bounded.  Membership
-// tests use dense bitmaps of the key bounding box in shared memory (binary
-// search over the sorted keys when the box is too large).
+// Work decomposition (per ladder size, all on one stream):
+//   K3a stage1_kernel -- persistent CTAs; a producer warp streams the 8 ring-0
+//       PLAIN corner boxes of each 8 x 32 centre tile into shared memory with
+//       TMA (mbarrier pipeline); consumer warps write the border keeps into
+//       the mask, compute the ring-0 mean cell and append the centres whose
+//       mean cell is in the ring's mean projection to a candidate list.
+//   K3b ring_kernel(r) -- one launch per ring, one candidate per thread:
+//       gathers all 32 corners of ring r at once, finishes the cascade (mean,
+//       std, gradient membership) and appends members to the next list; the
+//       last ring ORs survivors into the mask.
+// The projection tests are implied by full membership, so the decision is
+// the reference's; the SQUARED/X/Y planes and most fp64 work are only
+// touched for candidates, and every gather kernel runs with full lanes and
+// full occupancy.  Membership tests use dense bitmaps of the key bounding
+// box in shared memory (binary search over the sorted keys when the box is
+// too large).
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -37,7 +42,6 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WARPS = 8;   // consumer warps per CTA (one tile row each)
-constexpr int QCAP = 64;
 constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
 
 struct RingDev {
@@ -221,34 +225,26 @@ struct TmaMaps {
     CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) int64
 };
 
-// Tile geometry: TY rows (one per consumer warp) x TX columns; the 8 ring-0
-// PLAIN corner boxes of a tile are staged by TMA into one pipeline stage.
-// Measured on B200 + driver 580: a tile-mode TMA box must start at a 16-byte
-// aligned inner coordinate (an odd int64 column raises "illegal
+// Stage-1 tile geometry: TY rows (one per consumer warp) x TX columns; the 8
+// ring-0 PLAIN corner boxes of a tile are staged by TMA into one pipeline
+// stage.  Measured on B200 + driver 580: a tile-mode TMA box must start at a
+// 16-byte aligned inner coordinate (an odd int64 column raises "illegal
 // instruction"), so each box starts at the even column at or below the
 // corner and is BW = TX + 2 columns wide; readers skip the parity offset.
-constexpr int TY = WARPS;            // tile rows
-constexpr int TX = 32;               // tile columns (one chunk per warp)
-constexpr int BW = TX + 2;           // staged box width (int64 columns)
+constexpr int TY = WARPS;   // tile rows
+constexpr int TX = 32;      // tile columns (one chunk per warp)
+constexpr int BW = TX + 2;  // staged box width (int64 columns)
 constexpr int NBOX = 8;
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int BOX_ELEMS = BW * TY;
 constexpr int BOX_BYTES = BOX_ELEMS * 8;
 constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
 
-// payload of a queued centre: its ring-0 stage-1 state
-struct Entry {
-    int x, y, cm;
-    double mq, md;
-    long long s1q, s1d;
-};
-constexpr int QUEUE_BYTES = WARPS * QCAP * (int)sizeof(Entry);
-
 __device__ __forceinline__ int floor_even(int c) { return c & ~1; }  // two's complement: floor to even
 
 struct TileMap {
-    int n_tx, n_ty;        // tiles along x, y
-    int strip;             // tiles per column strip (L2 locality for wide images)
+    int n_tx, n_ty;  // tiles along x, y
+    int strip;       // tiles per column strip (L2 locality for wide images)
     long long n_tiles;
 };
 
@@ -263,29 +259,38 @@ __device__ __forceinline__ void tile_coords(const TileMap& t, long long idx, int
     tx = s0 + (int)(r % width);
 }
 
-__global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
-                                                                  const TileMap tm) {
-    extern __shared__ __align__(128) unsigned char dsmem[];
-    unsigned char* stage_buf = dsmem;                                // STAGES x STAGE_BYTES
-    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES + 2 * QUEUE_BYTES);
-    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-    // Work queues (per consumer warp), each drained 32 entries at a time:
-    //   QA: ring-0 mean passers (ring-0 stage-1 state) -> mean tests of rings >= 1
-    //   QB: centres whose every ring passed the mean test -> ring-0 std/gradient
-    //   QN: (x, y, ring) -> full evaluation of ring >= 1
-    Entry(*qa)[QCAP] = reinterpret_cast<Entry(*)[QCAP]>(dsmem + STAGES * STAGE_BYTES);
-    Entry(*qb)[QCAP] = reinterpret_cast<Entry(*)[QCAP]>(dsmem + STAGES * STAGE_BYTES + QUEUE_BYTES);
-    __shared__ int qn_x[WARPS][QCAP], qn_y[WARPS][QCAP];
-    __shared__ unsigned char qn_r[WARPS][QCAP];
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Copy the rings' membership bitmaps into shared memory (all threads).
+__device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbits, int r_lo, int r_hi) {
     const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
-    for (int r = 0; r < a.n_rings; ++r) {
+    for (int r = r_lo; r < r_hi; ++r) {
         const RingDev& R = a.ring[r];
         if (R.bm < 0) continue;
-        for (int i = threadIdx.x; i < R.bwords; i += (WARPS + 1) * 32)
+        for (int i = threadIdx.x; i < R.bwords; i += blockDim.x)
             sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
     }
+}
+
+// Append `flag` lanes' (x, y) to a device list with one atomic per warp.
+__device__ __forceinline__ void append(bool flag, int x, int y, int2* list, unsigned* count) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned b = __ballot_sync(FULL, flag);
+    if (!b) return;
+    unsigned base = 0;
+    if (lane == (unsigned)(__ffs(b) - 1)) base = atomicAdd(count, (unsigned)__popc(b));
+    base = __shfl_sync(FULL, base, __ffs(b) - 1);
+    if (flag) list[base + __popc(b & ((1u << lane) - 1u))] = make_int2(x, y);
+}
+
+// K3a: every grid centre of the decided rows -- border keeps into the mask,
+// ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
+// passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
+__global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
+                                                                  const TileMap tm, int2* list0, unsigned* count0) {
+    extern __shared__ __align__(128) unsigned char dsmem[];
+    unsigned char* stage_buf = dsmem;
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    stage_bitmaps(a, sbits, 0, 1);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -294,9 +299,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const RingDev& R0 = a.ring[0];
-    const int ylo = a.lo, yhi = a.H - 1 - a.hi, xlo = a.lo, xhi = a.W - 1 - a.hi;
 
     if (warp == WARPS) {
         // ── producer: one lane streams the tiles' corner boxes ──────────────
@@ -327,131 +331,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
     }
 
     // ── consumers: warp w takes row w of each tile ───────────────────────────
-    const unsigned lt = (1u << lane) - 1u;
-    const bool inst = a.stage_counts != nullptr;
-    int na = 0, nb = 0, nn = 0;
-    unsigned long long st0 = 0, st1 = 0, st2 = 0, st3 = 0;
-
-    auto survive = [&](bool keep, int x, int y) {
-        if (keep) {
-            const long long row = y - a.y_begin;
-            atomicOr(a.mask + row * a.mask_pitch + (x >> 5), 1u << (x & 31));
-            atomicAdd(a.row_counts + row, 1u);
-        }
-    };
-    auto push_n = [&](bool push, int x, int y, int r) {
-        const unsigned b = __ballot_sync(FULL, push);
-        if (push) {
-            const int e = nn + __popc(b & lt);
-            qn_x[warp][e] = x;
-            qn_y[warp][e] = y;
-            qn_r[warp][e] = (unsigned char)r;
-        }
-        nn += __popc(b);
-        __syncwarp();
-    };
-    // QA: mean tests of rings 1.. (PLAIN corners only, all rings' loads issued together)
-    auto drainA = [&](int cnt) {
-        bool pass = false;
-        Entry en;
-        if (lane < cnt) {
-            en = qa[warp][na - cnt + lane];
-            const long long* pc = a.planes + (long long)(en.y - a.y_origin) * a.pitch + en.x;
-            pass = true;
-            constexpr int BATCH = 2;
-            for (int r0 = 1; r0 < a.n_rings && pass; r0 += BATCH) {
-                Corners c[BATCH];
-#pragma unroll
-                for (int j = 0; j < BATCH; ++j)
-                    if (r0 + j < a.n_rings) load_corners(a, a.ring[r0 + j], pc, 0, c[j]);
-#pragma unroll
-                for (int j = 0; j < BATCH; ++j)
-                    if (r0 + j < a.n_rings && pass) {
-                        const RingDev& R = a.ring[r0 + j];
-                        pass = member_m(a, R, sbits, stage1_of(a, R, c[j]).cm);
-                    }
-            }
-        }
-        na -= cnt;
-        __syncwarp();
-        const unsigned b = __ballot_sync(FULL, pass);
-        if (pass) qb[warp][nb + __popc(b & lt)] = en;
-        nb += __popc(b);
-        st2 += (lane == 0) ? __popc(b) : 0;
-        __syncwarp();
-    };
-    // QB: ring-0 std / gradient stages (SQUARED, X, Y corners in one round trip)
-    auto drainB = [&](int cnt) {
-        bool keep = false, more = false;
-        int x = 0, y = 0;
-        if (lane < cnt) {
-            const Entry en = qb[warp][nb - cnt + lane];
-            x = en.x;
-            y = en.y;
-            Stage1 s;
-            s.cm = en.cm;
-            s.mq = en.mq;
-            s.md = en.md;
-            s.s1q = en.s1q;
-            s.s1d = en.s1d;
-            const int cy = y - a.y_origin;
-            const long long* pc = a.planes + (long long)cy * a.pitch + x;
-            Corners c2, cxk, cyk;
-            load_corners(a, R0, pc, 3, c2);
-            load_corners(a, R0, pc, 1, cxk);
-            load_corners(a, R0, pc, 2, cyk);
-            bool grad = false;
-            const bool pass = finish_of(a, R0, sbits, x, cy, s, c2, cxk, cyk, grad);
-            keep = pass && a.n_rings == 1;
-            more = pass && a.n_rings > 1;
-        }
-        nb -= cnt;
-        __syncwarp();
-        survive(keep, x, y);
-        const unsigned mb = __ballot_sync(FULL, more);
-        st3 += (lane == 0) ? __popc(mb) : 0;
-        push_n(more, x, y, 1);
-    };
-    // QN: full evaluation of ring r >= 1 (its mean test already passed in QA)
-    auto drainN = [&](int cnt) {
-        bool keep = false, more = false;
-        int x = 0, y = 0, r = 0;
-        if (lane < cnt) {
-            const int e = nn - cnt + lane;
-            x = qn_x[warp][e];
-            y = qn_y[warp][e];
-            r = qn_r[warp][e];
-        }
-        nn -= cnt;
-        __syncwarp();
-        if (lane < cnt) {
-            const RingDev& R = a.ring[r];
-            const int cy = y - a.y_origin;
-            const long long* pc = a.planes + (long long)cy * a.pitch + x;
-            Corners c0, c2, cxk, cyk;
-            load_corners(a, R, pc, 0, c0);
-            load_corners(a, R, pc, 3, c2);
-            load_corners(a, R, pc, 1, cxk);
-            load_corners(a, R, pc, 2, cyk);
-            const Stage1 t = stage1_of(a, R, c0);
-            bool grad = false;
-            const bool pass = finish_of(a, R, sbits, x, cy, t, c2, cxk, cyk, grad);
-            keep = pass && r + 1 == a.n_rings;
-            more = pass && r + 1 < a.n_rings;
-        }
-        survive(keep, x, y);
-        push_n(more, x, y, r + 1);
-    };
-    auto service = [&](bool flush) {
-        // drain deeper queues first so every queue stays below QCAP
-        for (;;) {
-            if (nn >= 32 || (flush && nn > 0)) { drainN(nn < 32 ? nn : 32); continue; }
-            if (nb >= 32 || (flush && nb > 0)) { drainB(nb < 32 ? nb : 32); continue; }
-            if (na >= 32 || (flush && na > 0)) { drainA(na < 32 ? na : 32); continue; }
-            break;
-        }
-    };
-
+    const int ylo = a.lo, yhi = a.H - 1 - a.hi, xlo = a.lo, xhi = a.W - 1 - a.hi;
+    const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;  // box parity offsets (x0 even)
+    unsigned long long n_int = 0, n_pass = 0;
     int it = 0;
     for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
         const int s = it % STAGES;
@@ -460,9 +342,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         const int y = a.y_begin + ty * TY + warp;
         const int x = tx * TX + lane;
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
-        // x0 is even, so each box's parity offset depends on the ring only
         const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
-        const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;
         const long long s1q = box[0 * BOX_ELEMS + pq] - box[1 * BOX_ELEMS + pq] - box[2 * BOX_ELEMS + pq] +
                               box[3 * BOX_ELEMS + pq];
         const long long s1d = box[4 * BOX_ELEMS + pe] - box[6 * BOX_ELEMS + po0] - box[7 * BOX_ELEMS + po1] +
@@ -475,41 +355,71 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 2) screen_kernel(const Scree
         const bool interior = on_grid && y >= ylo && y <= yhi && x >= xlo && x <= xhi;
         const unsigned border = __ballot_sync(FULL, on_grid && !interior);
         if (lane == 0 && tx * TX < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + tx] = border;
-        __syncwarp();
         bool pass = false;
-        Entry en;
         if (interior) {
-            en.x = x;
-            en.y = y;
-            en.s1q = s1q;
-            en.s1d = s1d;
-            en.mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);                   // features.py:325
-            en.md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);                   // features.py:349
-            en.cm = quant(__dmul_rn(__dadd_rn(en.mq, en.md), 0.5), a.qm, a.rqm);  // features.py:365
-            pass = member_m(a, R0, sbits, en.cm);
+            const double mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);  // features.py:325
+            const double md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);  // features.py:349
+            pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm));
         }
-        const unsigned pb = __ballot_sync(FULL, pass);
-        const unsigned ib = __ballot_sync(FULL, interior);
-        if (inst && lane == 0) {
-            st0 += __popc(ib);
-            st1 += __popc(pb);
-        }
-        if (pass) qa[warp][na + __popc(pb & lt)] = en;
-        na += __popc(pb);
-        __syncwarp();
-        service(false);
+        n_int += __popc(__ballot_sync(FULL, interior));
+        n_pass += __popc(__ballot_sync(FULL, pass));
+        append(pass, x, y, list0, count0);
     }
-    service(true);
-    if (inst) {
-        unsigned long long v[4] = {st0, st1, st2, st3};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            unsigned long long t = v[i];
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) t += __shfl_down_sync(FULL, t, d);
-            if (lane == 0 && t) atomicAdd(a.stage_counts + i, t);
+    if (a.stage_counts && lane == 0) {
+        atomicAdd(a.stage_counts + 0, n_int);
+        atomicAdd(a.stage_counts + 1, n_pass);
+    }
+}
+
+// K3b: one ring over a candidate list, one centre per thread (full lanes,
+// full occupancy; all of the ring's corners are gathered in one round trip).
+// Ring 0 recomputes its mean (already passed) and finishes the std and
+// gradient stages; rings >= 1 run the whole cascade.  Members go to `out`,
+// or -- for the last ring -- into the mask and the per-row survivor counts.
+__global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r, const int2* in, const unsigned* in_count,
+                                                   int2* out, unsigned* out_count) {
+    extern __shared__ unsigned sbits[];
+    stage_bitmaps(a, sbits, r, r + 1);
+    __syncthreads();
+    const RingDev& R = a.ring[r];
+    const bool last = (r + 1 == a.n_rings);
+    const unsigned count = *in_count;
+    const unsigned lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    unsigned long long n_pass = 0;
+    for (long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < count;
+         base += warps * 32) {
+        const long long idx = base + lane;
+        bool pass = false;
+        int x = 0, y = 0;
+        if (idx < count) {
+            const int2 e = in[idx];
+            x = e.x;
+            y = e.y;
+            const int cy = y - a.y_origin;
+            const long long* pc = a.planes + (long long)cy * a.pitch + x;
+            Corners c0, c2, cxk, cyk;
+            load_corners(a, R, pc, 0, c0);
+            load_corners(a, R, pc, 3, c2);
+            load_corners(a, R, pc, 1, cxk);
+            load_corners(a, R, pc, 2, cyk);
+            const Stage1 s = stage1_of(a, R, c0);
+            bool grad = false;
+            pass = (r == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, x, cy, s, c2, cxk, cyk, grad);
+        }
+        n_pass += __popc(__ballot_sync(FULL, pass));
+        if (last) {
+            if (pass) {
+                const long long row = y - a.y_begin;
+                atomicOr(a.mask + row * a.mask_pitch + (x >> 5), 1u << (x & 31));
+                atomicAdd(a.row_counts + row, 1u);
+            }
+        } else {
+            append(pass, x, y, out, out_count);
         }
     }
+    if (a.stage_counts && r == 0 && lane == 0 && n_pass) atomicAdd(a.stage_counts + 2, n_pass);
+    if (a.stage_counts && last && lane == 0 && n_pass) atomicAdd(a.stage_counts + 3, n_pass);
 }
 
 __global__ void fill_grid_kernel(int W, int y_begin, int y_end, int stride, unsigned* mask, long long mask_pitch,
@@ -554,6 +464,10 @@ __global__ void selftest_div_kernel(unsigned long long n, unsigned long long see
 
 }  // namespace
 
+size_t screen_workspace_bytes(int64_t W, int64_t rows) {
+    return 256 + (size_t)2 * (size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) * sizeof(int2);
+}
+
 // 2-D TMA descriptor of one int64 plane: dims (W+1 columns, h+1 rows), box TX x TY.
 static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, int64_t h, int64_t pitch) {
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -587,7 +501,7 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
                 int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings, const int32_t* ring_n,
                 const int32_t* ring_d, const int64_t* d_blob, const int64_t* h_blob, double qm, double qs, double qg,
                 uint32_t* d_mask, int64_t mask_pitch, uint32_t* d_row_counts, unsigned long long* d_stage_counts,
-                void* stream) {
+                void* d_ws, size_t ws_bytes, void* stream) {
     if (w != W) { set_error("row-band tables must span the full width (w == W)"); return SS_EINVAL; }
     if (W < 1 || H < 1 || h < 1 || y_origin < 0 || y_origin + h > H) {
         set_error("bad table frame");
@@ -636,7 +550,6 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     a.mask_pitch = mask_pitch;
     a.row_counts = d_row_counts;
     a.stage_counts = d_stage_counts;
-    int smem_words = 0;
     const long long P = pitch;
     for (int r = 0; r < n_rings; ++r) {
         RingDev& R = a.ring[r];
@@ -680,28 +593,41 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         R.wm = R.wms = 0;
         R.bsrc = -1;
         R.bwords = 0;
+        // each kernel stages only its own ring's bitmap, at shared offset 0
         if (R.n_k == 0) {  // empty ring: nothing passes
-            R.bm = smem_words;
+            R.bm = 0;
             R.cm_n = 0;
             R.bwords = 1;
-            smem_words += 1;
         } else if (hd[12] >= 0) {
             const int64_t words = hd[13] + hd[14] + hd[15];
-            if (smem_words + words <= SMEM_BITMAP_WORDS) {
-                R.bm = smem_words;
+            if (words <= SMEM_BITMAP_WORDS) {
+                R.bm = 0;
                 R.wm = (int)hd[13];
                 R.wms = (int)hd[14];
                 R.bsrc = (int)(hd[12] * 2);
                 R.bwords = (int)words;
-                smem_words += (int)words;
             }
         }
     }
     cudaStream_t s = as_stream(stream);
     const int64_t rows = y_end - y_begin;
     if (rows == 0) return SS_OK;
+    const size_t need = screen_workspace_bytes(W, rows);
+    if (!d_ws || ws_bytes < need) {
+        set_error("screen workspace too small: %zu < %zu", ws_bytes, need);
+        return SS_EINVAL;
+    }
+    // workspace: [counters: SS_MAX_RINGS+1 u32, padded] [list A] [list B]
+    unsigned* counts = static_cast<unsigned*>(d_ws);
+    int2* list_a = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + 256);
+    int2* list_b = list_a + (size_t)W * rows;
     if (cudaMemsetAsync(d_row_counts, 0, rows * sizeof(uint32_t), s) != cudaSuccess) return check_launch("memset");
-    // the mask rows are (re)initialised by the kernel; survivors are OR'ed in
+    if (cudaMemsetAsync(counts, 0, 256, s) != cudaSuccess) return check_launch("memset");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+    // K3a: the mask rows are (re)initialised here; survivors are OR'ed in by K3b
     TmaMaps maps;
     if (int e = encode_plane_map(&maps.sat, d_planes, W, h, pitch)) return e;
     if (int e = encode_plane_map(&maps.e, d_planes + 4 * a.ps, W, h, pitch)) return e;
@@ -713,22 +639,35 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     // in L2: (m + rows in flight) x strip width x 24 B (PLAIN SAT/E/O) <~ 48 MB
     {
         const int64_t budget = 48ll << 20;
-        const int64_t rows_in_flight = 148LL * 2 * TY;
-        int64_t width = budget / ((int64_t)(m + rows_in_flight) * 24);
-        int strip = (int)std::max<int64_t>(1, width / TX);
-        tm.strip = std::min(strip, tm.n_tx);
+        const int64_t rows_in_flight = (int64_t)sms * 3 * TY;
+        const int64_t width = budget / ((int64_t)(m + rows_in_flight) * 24);
+        tm.strip = (int)std::min<int64_t>(std::max<int64_t>(1, width / TX), tm.n_tx);
     }
     tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
-    const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * (size_t)QUEUE_BYTES + (size_t)std::max(smem_words, 1) * 4;
-    cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, screen_kernel, (WARPS + 1) * 32, smem);
-    const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * std::max(per_sm, 1));
-    screen_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, smem, s>>>(a, maps, tm);
-    note_launch();
-    return check_launch("screen_kernel");
+    {
+        const size_t smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(a.ring[0].bwords, 1) * 4;
+        cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage1_kernel, (WARPS + 1) * 32, smem);
+        const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * std::max(per_sm, 1));
+        stage1_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, smem, s>>>(a, maps, tm, list_a,
+                                                                                            counts + 0);
+        note_launch();
+        if (int e = check_launch("stage1_kernel")) return e;
+    }
+    // K3b: ring r reads list r (counts[r]) and appends to list r+1 (counts[r+1])
+    for (int r = 0; r < n_rings; ++r) {
+        const int2* in = (r % 2 == 0) ? list_a : list_b;
+        int2* out = (r % 2 == 0) ? list_b : list_a;
+        const size_t smem = (size_t)std::max(a.ring[r].bwords, 1) * 4;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ring_kernel, 256, smem);
+        ring_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), 256, smem, s>>>(a, r, in, counts + r, out, counts + r + 1);
+        note_launch();
+        if (int e = check_launch("ring_kernel")) return e;
+    }
+    return SS_OK;
 }
 
 int fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask, int64_t mask_pitch,
@@ -756,11 +695,13 @@ int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_
                    int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,
                    const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
                    double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
-                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* stream) {
+                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* d_workspace,
+                   size_t workspace_bytes, void* stream) {
     return ss::screen_size(d_planes, w, h, plane_pitch, W, H, y_origin, y_begin, y_end, m, stride, n_rings, h_ring_n,
                            h_ring_d, d_blob, h_blob, q_mean, q_std, q_grad, d_mask, mask_pitch_words, d_row_counts,
-                           d_stage_counts, stream);
+                           d_stage_counts, d_workspace, workspace_bytes, stream);
 }
+size_t ss_screen_workspace_bytes(int64_t W, int64_t rows) { return ss::screen_workspace_bytes(W, rows); }
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,
                  int64_t mask_pitch_words, uint32_t* d_row_counts, void* stream) {
     return ss::fill_grid(W, y_begin, y_end, stride, d_mask, mask_pitch_words, d_row_counts, stream);

@@ -97,6 +97,8 @@ class Engine:
         self.mrows = self.y_end - self.y_begin
         self.compact_ws = torch.empty(max(8, int(self.L.ss_compact_workspace_bytes(self.mrows))), dtype=torch.uint8,
                                       device=self.device)
+        self.screen_ws = torch.empty(int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1))),
+                                     dtype=torch.uint8, device=self.device)
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -173,7 +175,7 @@ class Engine:
             self.planes.data_ptr(), self.W, self.rows, self.pitch, self.W, self.H, self.y_origin, self.y_begin,
             self.y_end, sp.m, cfg.stride, len(sp.plan), sp.ring_n.ctypes.data, sp.ring_d.ctypes.data,
             sp.blob_dev.data_ptr(), sp.blob.ctypes.data, q[0], q[1], q[2], mask.data_ptr(), self.words, rc.data_ptr(),
-            _p(self.stage_counts), s), "screen_size")
+            _p(self.stage_counts), self.screen_ws.data_ptr(), self.screen_ws.numel(), s), "screen_size")
 
     def compact_size(self, k: int, tp: TemplatePlan) -> None:
         sp = tp.sizes[k]
