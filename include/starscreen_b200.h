@@ -45,6 +45,7 @@ extern "C" {
 #define SS_ECUDA 3     /* CUDA launch / runtime  -> RuntimeError */
 
 #define SS_MAX_RINGS 16
+#define SS_MAX_SIZES 64 /* ladder sizes per ss_*_ladder call */
 #define SS_KEY_BASE (1LL << 21) /* screening.py:57 _KEY_BASE */
 #define SS_BLOB_HDR 16             /* int64 header slots per ring in a key blob */
 #define SS_BLOB_MAX_BITMAP_WORDS 8192 /* per-ring membership bitmap cap (32 KiB) */
@@ -138,6 +139,19 @@ int ss_compact(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int6
                int64_t capacity, unsigned long long* d_total, unsigned long long* d_size_count,
                void* d_workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * Whole-ladder form of ss_compact: one call for every size of a ladder.
+ * d_masks holds n_sizes masks size_stride_words apart (rows y_begin..y_end),
+ * d_row_counts n_sizes x rows counts; sizes with m < MIN_PATCH_SIDE are
+ * skipped.  d_size_counts (n_sizes u64) and *d_total receive the counts;
+ * survivors are written in ladder order, then row-major.
+ */
+size_t ss_compact_ladder_workspace_bytes(int64_t rows, int32_t n_sizes);
+int ss_compact_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
+                      int64_t H, int64_t y_begin, int64_t y_end, int32_t n_sizes, const int32_t* h_m, int32_t stride,
+                      const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
+                      unsigned long long* d_size_counts, void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* ── kept region (screening.py:316-330 _footprint_union) ─────────────── */
 /* Workspace for ss_region_accumulate with sizes up to m_max. */
 size_t ss_region_workspace_bytes(int64_t W, int64_t H, int32_t m_max);
@@ -148,6 +162,11 @@ size_t ss_region_workspace_bytes(int64_t W, int64_t H, int32_t m_max);
 int ss_region_accumulate(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int32_t m,
                          int32_t stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes,
                          void* stream);
+/* Whole-ladder form of ss_region_accumulate (full-image masks). */
+size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes);
+int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
+                     int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
+                     size_t workspace_bytes, void* stream);
 /* d_count += number of set bits of the W x H region mask. */
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H,
                 unsigned long long* d_count, void* stream);

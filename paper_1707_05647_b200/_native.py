@@ -44,6 +44,11 @@ _SIGS = {
     "ss_compact_workspace_bytes": (c_sz, [c_i64]),
     "ss_compact": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_i64, c_p, c_p,
                                   c_p, c_sz, c_p]),
+    "ss_compact_ladder_workspace_bytes": (c_sz, [c_i64, c_i32]),
+    "ss_compact_ladder": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_p, c_i32, c_p, c_p,
+                                         c_i64, c_p, c_p, c_p, c_sz, c_p]),
+    "ss_region_ladder_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "ss_region_ladder": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i32, c_p, c_i32, c_p, c_p, c_sz, c_p]),
     "ss_region_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
     "ss_region_accumulate": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
     "ss_popcount": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),

@@ -218,6 +218,188 @@ __global__ void popcount_kernel(const unsigned* bits, long long pitch, long long
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
 }
 
+// ── whole-ladder variants: one launch per kernel for every size ───────────
+
+struct Ladder {
+    int L;
+    int m[SS_MAX_SIZES];
+};
+
+// One CTA per size: relative exclusive scan of the size's row counts.
+__global__ void __launch_bounds__(1024) scan_sizes_kernel(const unsigned* counts, long long rows,
+                                                          unsigned long long* row_off, unsigned long long* size_counts) {
+    __shared__ unsigned long long warp_sums[32];
+    __shared__ unsigned long long carry;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int k = blockIdx.x;
+    const unsigned* c = counts + (long long)k * rows;
+    unsigned long long* off = row_off + (long long)k * rows;
+    if (t == 0) carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < rows; base += 1024) {
+        const long long i = base + t;
+        const unsigned long long v = (i < rows) ? c[i] : 0ull;
+        unsigned long long s = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(FULL, s, d);
+            if (lane >= d) s += o;
+        }
+        if (lane == 31) warp_sums[warp] = s;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = warp_sums[lane];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long o = __shfl_up_sync(FULL, w, d);
+                if (lane >= d) w += o;
+            }
+            warp_sums[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long before = carry + (warp ? warp_sums[warp - 1] : 0ull) + s - v;
+        if (i < rows) off[i] = before;
+        __syncthreads();
+        if (t == 1023) carry = before + v;
+        __syncthreads();
+    }
+    if (t == 0) size_counts[k] = carry;
+}
+
+// grid (row blocks, sizes): one warp per mask row writes its survivors at
+// base(size) + row offset, base = survivors of the earlier ladder sizes.
+__global__ void write_xy_all_kernel(const unsigned* masks, long long mask_pitch, long long size_stride, int W, int H,
+                                    int y_begin, long long rows, int stride, const Ladder lad, const unsigned* counts,
+                                    const unsigned long long* row_off, const unsigned long long* size_counts, int* xy,
+                                    long long capacity, unsigned long long* total) {
+    const int k = blockIdx.y;
+    if (blockIdx.x == 0 && k == 0 && threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int j = 0; j < lad.L; ++j) s += size_counts[j];
+        *total = s;
+    }
+    const int m = lad.m[k];
+    if (m < 8) return;
+    const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows || counts[(long long)k * rows + row] == 0) return;  // warp-uniform
+    unsigned long long base = 0;
+    for (int j = 0; j < k; ++j) base += size_counts[j];
+    const int lo = (m - 1) / 2, hi = m / 2;
+    const int x_lo = lo, x_hi = W - 1 - hi;
+    const unsigned* mrow = masks + (long long)k * size_stride + row * mask_pitch;
+    const long long words = (W + 31) / 32;
+    unsigned long long pos = base + row_off[(long long)k * rows + row];
+    const int y = y_begin + (int)row;
+    for (long long wb = 0; wb < words; wb += 32) {
+        const long long w = wb + lane;
+        unsigned bits = (w < words) ? (mrow[w] & interior_bits(w, x_lo, x_hi)) : 0u;
+        const int c = __popc(bits);
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += o;
+        }
+        unsigned long long p = pos + (unsigned long long)(incl - c);
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (p < (unsigned long long)capacity) {
+                xy[2 * p] = (int)(w * 32 + b);
+                xy[2 * p + 1] = y;
+            }
+            ++p;
+        }
+        pos += (unsigned long long)__shfl_sync(FULL, incl, 31);
+    }
+    (void)stride;
+    (void)H;
+}
+
+// grid (words, sizes): column pass of every size's footprint dilation.
+__global__ void vdilate_all_kernel(const unsigned* masks, long long mask_pitch, long long size_stride, long long words,
+                                   int W, int H, long long P, const Ladder lad, unsigned* V) {
+    extern __shared__ unsigned smem[];
+    const int k = blockIdx.y;
+    const int m = lad.m[k];
+    const long long w = blockIdx.x;
+    unsigned* Vk = V + (long long)k * H * words;
+    const int lo = (m - 1) / 2, hi = m / 2, L = m;
+    const int x_lo = lo, x_hi = W - 1 - hi, y_lo = lo, y_hi = H - 1 - hi;
+    const long long ext = (long long)H + 2 * P;
+    unsigned* A = smem;
+    unsigned* B = smem + ext;
+    const unsigned cm = (m >= 8) ? interior_bits(w, x_lo, x_hi) : 0u;
+    const unsigned* mk = masks + (long long)k * size_stride;
+    int any = 0;
+    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
+        const long long r = i - P;
+        const unsigned v = (cm && r >= y_lo && r <= y_hi) ? (mk[r * mask_pitch + w] & cm) : 0u;
+        A[i] = v;
+        any |= (v != 0u);
+    }
+    if (!__syncthreads_or(any)) {
+        for (long long y = threadIdx.x; y < H; y += blockDim.x) Vk[y * words + w] = 0u;
+        return;
+    }
+    int l = 1;
+    while (2 * l <= L) {
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + l < ext ? A[i + l] : 0u);
+        __syncthreads();
+        unsigned* t = A; A = B; B = t;
+        l *= 2;
+    }
+    if (l < L) {
+        const int s = L - l;
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + s < ext ? A[i + s] : 0u);
+        __syncthreads();
+        unsigned* t = A; A = B; B = t;
+    }
+    for (long long y = threadIdx.x; y < H; y += blockDim.x) Vk[y * words + w] = A[y - hi + P];
+}
+
+// grid (rows, sizes): row pass of every size, OR'ed into the region.
+__global__ void hdilate_all_kernel(const unsigned* V, long long words, long long P, int W, int H, const Ladder lad,
+                                   unsigned* region, long long region_pitch) {
+    extern __shared__ unsigned smem[];
+    const int k = blockIdx.y;
+    const int m = lad.m[k];
+    if (m < 8) return;
+    const int L = m, hi = m / 2;
+    const long long ext = words + 2 * P;
+    unsigned* A = smem;
+    unsigned* B = smem + ext;
+    const int y = blockIdx.x;
+    const unsigned* Vk = V + (long long)k * H * words;
+    int any = 0;
+    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
+        const long long wi = i - P;
+        const unsigned v = (wi >= 0 && wi < words) ? Vk[(long long)y * words + wi] : 0u;
+        A[i] = v;
+        any |= (v != 0u);
+    }
+    if (!__syncthreads_or(any)) return;
+    int l = 1;
+    while (2 * l <= L) {
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, l);
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+        l *= 2;
+    }
+    if (l < L) {
+        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, L - l);
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+    }
+    const unsigned last_mask = (W % 32) ? ((1u << (W % 32)) - 1u) : FULL;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x) {
+        unsigned r = shifted_hi(A, i + P, ext, hi);
+        if (i == words - 1) r &= last_mask;
+        if (r) atomicOr(region + (long long)y * region_pitch + i, r);
+    }
+}
+
 }  // namespace
 
 size_t compact_workspace_bytes(int64_t rows) { return (size_t)std::max<int64_t>(rows, 1) * 8; }
@@ -279,6 +461,89 @@ int region_accumulate(const uint32_t* d_mask, int64_t mask_pitch, int64_t W, int
     return check_launch("hdilate_rows_kernel");
 }
 
+static int fill_ladder(Ladder& lad, int32_t L, const int32_t* h_m) {
+    if (L < 1 || L > SS_MAX_SIZES || !h_m) {
+        set_error("ladder length %d out of range", (int)L);
+        return SS_EINVAL;
+    }
+    lad.L = L;
+    for (int k = 0; k < L; ++k) lad.m[k] = h_m[k];
+    return SS_OK;
+}
+
+size_t compact_ladder_workspace_bytes(int64_t rows, int32_t L) {
+    return (size_t)std::max<int64_t>(rows, 1) * std::max<int32_t>(L, 1) * 8 + 256 + (size_t)SS_MAX_SIZES * 8;
+}
+
+int compact_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H,
+                   int64_t y_begin, int64_t y_end, int32_t L, const int32_t* h_m, int32_t stride,
+                   const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
+                   unsigned long long* d_size_counts, void* d_ws, size_t ws_bytes, void* stream) {
+    Ladder lad;
+    if (int e = fill_ladder(lad, L, h_m)) return e;
+    const int64_t rows = y_end - y_begin;
+    if (rows < 0 || W < 1 || stride < 1) { set_error("bad compact arguments"); return SS_EINVAL; }
+    cudaStream_t s = as_stream(stream);
+    if (rows == 0) {
+        cudaMemsetAsync(d_size_counts, 0, sizeof(unsigned long long) * L, s);
+        cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), s);
+        return SS_OK;
+    }
+    if (ws_bytes < compact_ladder_workspace_bytes(rows, L) || !d_ws) {
+        set_error("compact workspace too small");
+        return SS_EINVAL;
+    }
+    auto* row_off = static_cast<unsigned long long*>(d_ws);
+    scan_sizes_kernel<<<(unsigned)L, 1024, 0, s>>>(d_row_counts, rows, row_off, d_size_counts);
+    note_launch();
+    if (int e = check_launch("scan_sizes_kernel")) return e;
+    write_xy_all_kernel<<<dim3((unsigned)((rows * 32 + 255) / 256), (unsigned)L), 256, 0, s>>>(
+        d_masks, mask_pitch, size_stride, (int)W, (int)H, (int)y_begin, rows, stride, lad, d_row_counts, row_off,
+        d_size_counts, d_xy, capacity, d_total);
+    note_launch();
+    return check_launch("write_xy_all_kernel");
+}
+
+size_t region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t L) {
+    return (size_t)std::max<int32_t>(L, 1) * H * ((W + 31) / 32) * 4;
+}
+
+int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H, int32_t L,
+                  const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
+    Ladder lad;
+    if (int e = fill_ladder(lad, L, h_m)) return e;
+    if (W < 1 || H < 1 || stride < 1) { set_error("bad region arguments"); return SS_EINVAL; }
+    if (ws_bytes < region_ladder_workspace_bytes(W, H, L) || !d_ws) {
+        set_error("region workspace too small");
+        return SS_EINVAL;
+    }
+    int m_max = 1;
+    for (int k = 0; k < L; ++k) m_max = std::max(m_max, (int)h_m[k]);
+    const int64_t words = (W + 31) / 32;
+    unsigned* V = static_cast<unsigned*>(d_ws);
+    cudaStream_t s = as_stream(stream);
+    {
+        const int64_t P = m_max;
+        const size_t smem = (size_t)2 * (H + 2 * P) * 4;
+        if (smem > 227 * 1024) { set_error("image too tall for the region pass"); return SS_EINVAL; }
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(vdilate_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        vdilate_all_kernel<<<dim3((unsigned)words, (unsigned)L), 1024, smem, s>>>(d_masks, mask_pitch, size_stride, words,
+                                                                                (int)W, (int)H, P, lad, V);
+        note_launch();
+        if (int e = check_launch("vdilate_all_kernel")) return e;
+    }
+    const int64_t P = (m_max + 31) / 32 + 1;
+    const int threads = (int)std::min<int64_t>(1024, ((words + 2 * P + 31) / 32) * 32);
+    const size_t smem = (size_t)2 * (words + 2 * P) * 4;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(hdilate_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hdilate_all_kernel<<<dim3((unsigned)H, (unsigned)L), threads, smem, s>>>(V, words, P, (int)W, (int)H, lad, d_region,
+                                                                             mask_pitch);
+    note_launch();
+    return check_launch("hdilate_all_kernel");
+}
+
 int popcount(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, unsigned long long* d_count, void* stream) {
     if (W < 1 || H < 0) { set_error("bad popcount arguments"); return SS_EINVAL; }
     if (H == 0) return SS_OK;
@@ -306,6 +571,26 @@ int ss_region_accumulate(const uint32_t* d_mask, int64_t mask_pitch_words, int64
                          int32_t stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes, void* stream) {
     return ss::region_accumulate(d_mask, mask_pitch_words, W, H, m, stride, d_region, d_workspace, workspace_bytes,
                                  stream);
+}
+size_t ss_compact_ladder_workspace_bytes(int64_t rows, int32_t n_sizes) {
+    return ss::compact_ladder_workspace_bytes(rows, n_sizes);
+}
+int ss_compact_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
+                      int64_t H, int64_t y_begin, int64_t y_end, int32_t n_sizes, const int32_t* h_m, int32_t stride,
+                      const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
+                      unsigned long long* d_size_counts, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::compact_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, y_begin, y_end, n_sizes, h_m, stride,
+                              d_row_counts, d_xy, capacity, d_total, d_size_counts, d_workspace, workspace_bytes,
+                              stream);
+}
+size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes) {
+    return ss::region_ladder_workspace_bytes(W, H, n_sizes);
+}
+int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
+                     int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
+                     size_t workspace_bytes, void* stream) {
+    return ss::region_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, n_sizes, h_m, stride, d_region,
+                             d_workspace, workspace_bytes, stream);
 }
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, unsigned long long* d_count,
                 void* stream) {

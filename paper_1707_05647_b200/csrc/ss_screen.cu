@@ -250,13 +250,15 @@ struct TileMap {
 
 __device__ __forceinline__ void tile_coords(const TileMap& t, long long idx, int& tx, int& ty) {
     // strip-major: strips of `strip` tile columns, row-blocks within a strip, x fastest
-    const long long per_strip = (long long)t.strip * t.n_ty;
-    const long long s = idx / per_strip;
-    const int s0 = (int)(s * t.strip);
-    const int width = min(t.strip, t.n_tx - s0);
-    const long long r = idx - s * per_strip;
-    ty = (int)(r / width);
-    tx = s0 + (int)(r % width);
+    const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty;
+    const unsigned i = (unsigned)idx;
+    const unsigned s = i / per_strip;
+    const int s0 = (int)(s * (unsigned)t.strip);
+    const unsigned width = (unsigned)min(t.strip, t.n_tx - s0);
+    const unsigned r = i - s * per_strip;
+    const unsigned q = r / width;
+    ty = (int)q;
+    tx = s0 + (int)(r - q * width);
 }
 
 // Copy the rings' membership bitmaps into shared memory (all threads).
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    __shared__ int2 tile_xy[STAGES];  // (tx, ty) of the tile in each stage, written by the producer
     stage_bitmaps(a, sbits, 0, 1);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 int tx, ty;
                 tile_coords(tm, t, tx, ty);
+                tile_xy[s] = make_int2(tx, ty);  // published by the mbarrier arrive below
                 const int x0 = tx * TX;
                 const int cy0 = a.y_begin + ty * TY - a.y_origin;  // table-local first row
                 unsigned char* dst = stage_buf + s * STAGE_BYTES;
@@ -335,13 +339,14 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
     const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;  // box parity offsets (x0 even)
     unsigned long long n_int = 0, n_pass = 0;
     int it = 0;
+    const bool unit_stride = a.stride == 1;
     for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
         const int s = it % STAGES;
-        int tx, ty;
-        tile_coords(tm, t, tx, ty);
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        const int2 txy = tile_xy[s];
+        const int tx = txy.x, ty = txy.y;
         const int y = a.y_begin + ty * TY + warp;
         const int x = tx * TX + lane;
-        mbar_wait(&full_bar[s], (it / STAGES) & 1);
         const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
         const long long s1q = box[0 * BOX_ELEMS + pq] - box[1 * BOX_ELEMS + pq] - box[2 * BOX_ELEMS + pq] +
                               box[3 * BOX_ELEMS + pq];
@@ -350,8 +355,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
         if (y >= a.y_end) continue;  // warp-uniform (past the last row)
-        const bool row_grid = (y % a.stride) == 0;
-        const bool on_grid = row_grid && x < a.W && (x % a.stride) == 0;
+        const bool row_grid = unit_stride || (y % a.stride) == 0;
+        const bool on_grid = row_grid && x < a.W && (unit_stride || (x % a.stride) == 0);
         const bool interior = on_grid && y >= ylo && y <= yhi && x >= xlo && x <= xhi;
         const unsigned border = __ballot_sync(FULL, on_grid && !interior);
         if (lane == 0 && tx * TX < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + tx] = border;

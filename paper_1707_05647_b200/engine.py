@@ -95,8 +95,7 @@ class Engine:
                                     device=self.device)
         self.words = (self.W + 31) // 32
         self.mrows = self.y_end - self.y_begin
-        self.compact_ws = torch.empty(max(8, int(self.L.ss_compact_workspace_bytes(self.mrows))), dtype=torch.uint8,
-                                      device=self.device)
+        self.compact_ws = None
         self.screen_ws = torch.empty(int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1))),
                                      dtype=torch.uint8, device=self.device)
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
@@ -114,15 +113,17 @@ class Engine:
 
     # ── buffers ────────────────────────────────────────────────────────────
     def _ensure(self, n_sizes: int, max_m: int, capacity: int, region: bool) -> None:
-        if self.masks is None or self.n_sizes < n_sizes:
+        if self.masks is None or self.n_sizes != n_sizes:
             self.n_sizes = n_sizes
             self.masks = torch.empty((n_sizes, self.mrows, self.words), dtype=torch.int32, device=self.device)
             self.row_counts = torch.empty((n_sizes, max(self.mrows, 1)), dtype=torch.int32, device=self.device)
             self.size_counts = torch.zeros(n_sizes, dtype=torch.int64, device=self.device)
-        if region and (self.region is None or self._region_m < max_m):
-            self._region_m = max_m
+            self.compact_ws = torch.empty(int(self.L.ss_compact_ladder_workspace_bytes(max(self.mrows, 1), n_sizes)),
+                                          dtype=torch.uint8, device=self.device)
+            self.region_ws = None
+        if region and (self.region is None or self.region_ws is None):
             self.region = torch.empty((self.H, self.words), dtype=torch.int32, device=self.device)
-            self.region_ws = torch.empty(int(self.L.ss_region_workspace_bytes(self.W, self.H, max_m)),
+            self.region_ws = torch.empty(int(self.L.ss_region_ladder_workspace_bytes(self.W, self.H, n_sizes)),
                                          dtype=torch.uint8, device=self.device)
         if self.xy is None or self.capacity < capacity:
             self.capacity = max(capacity, 1)
@@ -177,23 +178,27 @@ class Engine:
             sp.blob_dev.data_ptr(), sp.blob.ctypes.data, q[0], q[1], q[2], mask.data_ptr(), self.words, rc.data_ptr(),
             _p(self.stage_counts), self.screen_ws.data_ptr(), self.screen_ws.numel(), s), "screen_size")
 
-    def compact_size(self, k: int, tp: TemplatePlan) -> None:
-        sp = tp.sizes[k]
-        if sp.m < MIN_PATCH_SIDE:
-            return
-        _native.check(self.L.ss_compact(
-            self.masks[k].data_ptr(), self.words, self.W, self.H, self.y_begin, self.y_end, sp.m, tp.config.stride,
-            self.row_counts[k].data_ptr(), self.xy.data_ptr(), self.capacity, self.totals.data_ptr(),
-            self.size_counts[k:].data_ptr(), self.compact_ws.data_ptr(), self.compact_ws.numel(), _stream_handle()),
-            "compact")
+    def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:
+        return np.array([sp.m for sp in tp.sizes], np.int32)
 
-    def region_size(self, k: int, tp: TemplatePlan) -> None:
-        sp = tp.sizes[k]
-        if sp.m < MIN_PATCH_SIDE:
-            return
-        _native.check(self.L.ss_region_accumulate(
-            self.masks[k].data_ptr(), self.words, self.W, self.H, sp.m, tp.config.stride, self.region.data_ptr(),
-            self.region_ws.data_ptr(), self.region_ws.numel(), _stream_handle()), "region")
+    def compact_all(self, tp: TemplatePlan) -> None:
+        """K4 for every size in one pass (ladder order, then row-major)."""
+        ms = self._ladder_array(tp)
+        _native.check(self.L.ss_compact_ladder(
+            self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, self.y_begin, self.y_end,
+            len(ms), ms.ctypes.data, tp.config.stride, self.row_counts.data_ptr(), self.xy.data_ptr(), self.capacity,
+            self.totals.data_ptr(), self.size_counts.data_ptr(), self.compact_ws.data_ptr(), self.compact_ws.numel(),
+            _stream_handle()), "compact")
+
+    def region_all(self, tp: TemplatePlan) -> None:
+        """K5 for every size in one pass, then the region popcount."""
+        ms = self._ladder_array(tp)
+        _native.check(self.L.ss_region_ladder(
+            self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, len(ms), ms.ctypes.data,
+            tp.config.stride, self.region.data_ptr(), self.region_ws.data_ptr(), self.region_ws.numel(),
+            _stream_handle()), "region")
+        _native.check(self.L.ss_popcount(self.region.data_ptr(), self.words, self.W, self.H,
+                                         self.totals[1:].data_ptr(), _stream_handle()), "popcount")
 
     def run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool = True, region: bool = True,
             capacity: Optional[int] = None) -> None:
@@ -203,27 +208,21 @@ class Engine:
         self._ensure(len(tp.sizes), tp.max_m, capacity or self.default_capacity(tp), region)
         if build:
             self.build_tables(img)
-        self.totals.zero_()
-        self.size_counts.zero_()
         if region:
             self.region.zero_()
+            self.totals[1:].zero_()
         for k in range(len(tp.sizes)):
             if self.hooks is not None:
                 self.hooks[0](k)
             self.screen_size(k, tp)
             if self.hooks is not None:
                 self.hooks[1](k)
-            self.compact_size(k, tp)
-            if region:
-                self.region_size(k, tp)
+        self.compact_all(tp)
         if region:
-            _native.check(self.L.ss_popcount(self.region.data_ptr(), self.words, self.W, self.H,
-                                             self.totals[1:].data_ptr(), _stream_handle()), "popcount")
+            self.region_all(tp)
 
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:
         """Grow the survivor buffer and redo K4 only (after an overflow)."""
         self.capacity = capacity
         self.xy = torch.empty((capacity, 2), dtype=torch.int32, device=self.device)
-        self.totals[0].zero_()
-        for k in range(len(tp.sizes)):
-            self.compact_size(k, tp)
+        self.compact_all(tp)
