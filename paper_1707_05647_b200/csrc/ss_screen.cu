@@ -232,10 +232,11 @@ struct TmaMaps {
 // instruction"), so each box starts at the even column at or below the
 // corner and is BW = TX + 2 columns wide; readers skip the parity offset.
 constexpr int TY = WARPS;   // tile rows
-constexpr int TX = 32;      // tile columns (one chunk per warp)
+constexpr int CPW = 2;      // 32-centre chunks per warp per tile
+constexpr int TX = 32 * CPW;  // tile columns
 constexpr int BW = TX + 2;  // staged box width (int64 columns)
 constexpr int NBOX = 8;
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int BOX_ELEMS = BW * TY;
 constexpr int BOX_BYTES = BOX_ELEMS * 8;
 constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ int2 tile_xy[STAGES];  // (tx, ty) of the tile in each stage, written by the producer
+    __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
     stage_bitmaps(a, sbits, 0, 1);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -334,9 +336,12 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
         return;
     }
 
-    // ── consumers: warp w takes row w of each tile ───────────────────────────
+    // ── consumers: warp w takes row w of each tile, CPW chunks of 32 ────────
     const int ylo = a.lo, yhi = a.H - 1 - a.hi, xlo = a.lo, xhi = a.W - 1 - a.hi;
     const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;  // box parity offsets (x0 even)
+    const unsigned lt = (1u << lane) - 1u;
+    int2* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
+    int nbuf = 0;
     unsigned long long n_int = 0, n_pass = 0;
     int it = 0;
     const bool unit_stride = a.stride == 1;
@@ -346,29 +351,55 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
         const int2 txy = tile_xy[s];
         const int tx = txy.x, ty = txy.y;
         const int y = a.y_begin + ty * TY + warp;
-        const int x = tx * TX + lane;
         const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
-        const long long s1q = box[0 * BOX_ELEMS + pq] - box[1 * BOX_ELEMS + pq] - box[2 * BOX_ELEMS + pq] +
-                              box[3 * BOX_ELEMS + pq];
-        const long long s1d = box[4 * BOX_ELEMS + pe] - box[6 * BOX_ELEMS + po0] - box[7 * BOX_ELEMS + po1] +
-                              box[5 * BOX_ELEMS + pe];
+        long long s1q[CPW], s1d[CPW];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const long long* b = box + 32 * c;
+            s1q[c] = b[0 * BOX_ELEMS + pq] - b[1 * BOX_ELEMS + pq] - b[2 * BOX_ELEMS + pq] + b[3 * BOX_ELEMS + pq];
+            s1d[c] = b[4 * BOX_ELEMS + pe] - b[6 * BOX_ELEMS + po0] - b[7 * BOX_ELEMS + po1] + b[5 * BOX_ELEMS + pe];
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
         if (y >= a.y_end) continue;  // warp-uniform (past the last row)
         const bool row_grid = unit_stride || (y % a.stride) == 0;
-        const bool on_grid = row_grid && x < a.W && (unit_stride || (x % a.stride) == 0);
-        const bool interior = on_grid && y >= ylo && y <= yhi && x >= xlo && x <= xhi;
-        const unsigned border = __ballot_sync(FULL, on_grid && !interior);
-        if (lane == 0 && tx * TX < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + tx] = border;
-        bool pass = false;
-        if (interior) {
-            const double mq = div_rn((double)s1q, R0.cnt_sq, R0.rcp_sq);  // features.py:325
-            const double md = div_rn((double)s1d, R0.cnt_di, R0.rcp_di);  // features.py:349
-            pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm));
+        const bool row_int = row_grid && y >= ylo && y <= yhi;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const int x = tx * TX + 32 * c + lane;
+            const bool on_grid = row_grid && x < a.W && (unit_stride || (x % a.stride) == 0);
+            const bool interior = row_int && on_grid && x >= xlo && x <= xhi;
+            const unsigned border = __ballot_sync(FULL, on_grid && !interior);
+            const int word = tx * CPW + c;
+            if (lane == 0 && word * 32 < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + word] = border;
+            bool pass = false;
+            if (interior) {
+                const double mq = div_rn((double)s1q[c], R0.cnt_sq, R0.rcp_sq);  // features.py:325
+                const double md = div_rn((double)s1d[c], R0.cnt_di, R0.rcp_di);  // features.py:349
+                pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm));
+            }
+            const unsigned pb = __ballot_sync(FULL, pass);
+            n_int += __popc(__ballot_sync(FULL, interior));
+            n_pass += __popc(pb);
+            if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, y);
+            nbuf += __popc(pb);
         }
-        n_int += __popc(__ballot_sync(FULL, interior));
-        n_pass += __popc(__ballot_sync(FULL, pass));
-        append(pass, x, y, list0, count0);
+        while (nbuf >= 32) {
+            __syncwarp();
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(count0, 32u);
+            base = __shfl_sync(FULL, base, 0);
+            list0[base + lane] = buf[nbuf - 32 + lane];
+            nbuf -= 32;
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    if (nbuf > 0) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
+        base = __shfl_sync(FULL, base, 0);
+        if (lane < nbuf) list0[base + lane] = buf[lane];
     }
     if (a.stage_counts && lane == 0) {
         atomicAdd(a.stage_counts + 0, n_int);
