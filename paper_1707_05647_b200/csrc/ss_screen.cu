@@ -413,27 +413,33 @@ __global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenAr
 // gradient stages; rings >= 1 run the whole cascade.  Members go to `out`,
 // or -- for the last ring -- into the mask and the per-row survivor counts.
 __global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r, const int2* in, const unsigned* in_count,
-                                                   int2* out, unsigned* out_count) {
+                                                      int2* out, unsigned* out_count) {
     extern __shared__ unsigned sbits[];
+    __shared__ int2 stage_out[8][64];  // per-warp staging of members, flushed 32 at a time
     stage_bitmaps(a, sbits, r, r + 1);
     __syncthreads();
     const RingDev& R = a.ring[r];
     const bool last = (r + 1 == a.n_rings);
     const unsigned count = *in_count;
-    const unsigned lane = threadIdx.x & 31;
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const long long step = (long long)gridDim.x * (blockDim.x >> 5) * 32;
+    int2* buf = stage_out[warp];
+    int nbuf = 0;
     unsigned long long n_pass = 0;
-    for (long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < count;
-         base += warps * 32) {
-        const long long idx = base + lane;
+    long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
+    // the candidate list is read one iteration ahead so the corner gathers
+    // do not wait behind the list load
+    int2 next = (base + lane < count) ? in[base + lane] : make_int2(-1, -1);
+    for (; base < count; base += step) {
+        const int2 e = next;
+        const long long nidx = base + step + lane;
+        next = (nidx < count) ? in[nidx] : make_int2(-1, -1);
+        const bool valid = e.x >= 0;
         bool pass = false;
-        int x = 0, y = 0;
-        if (idx < count) {
-            const int2 e = in[idx];
-            x = e.x;
-            y = e.y;
-            const int cy = y - a.y_origin;
-            const long long* pc = a.planes + (long long)cy * a.pitch + x;
+        if (valid) {
+            const int cy = e.y - a.y_origin;
+            const long long* pc = a.planes + (long long)cy * a.pitch + e.x;
             Corners c0, c2, cxk, cyk;
             load_corners(a, R, pc, 0, c0);
             load_corners(a, R, pc, 3, c2);
@@ -441,18 +447,36 @@ __global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r,
             load_corners(a, R, pc, 2, cyk);
             const Stage1 s = stage1_of(a, R, c0);
             bool grad = false;
-            pass = (r == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, x, cy, s, c2, cxk, cyk, grad);
+            pass = (r == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk, grad);
         }
-        n_pass += __popc(__ballot_sync(FULL, pass));
+        const unsigned pb = __ballot_sync(FULL, pass);
+        n_pass += __popc(pb);
         if (last) {
             if (pass) {
-                const long long row = y - a.y_begin;
-                atomicOr(a.mask + row * a.mask_pitch + (x >> 5), 1u << (x & 31));
+                const long long row = e.y - a.y_begin;
+                atomicOr(a.mask + row * a.mask_pitch + (e.x >> 5), 1u << (e.x & 31));
                 atomicAdd(a.row_counts + row, 1u);
             }
         } else {
-            append(pass, x, y, out, out_count);
+            if (pass) buf[nbuf + __popc(pb & lt)] = e;
+            nbuf += __popc(pb);
+            if (nbuf >= 32) {
+                __syncwarp();
+                unsigned ob = 0;
+                if (lane == 0) ob = atomicAdd(out_count, 32u);
+                ob = __shfl_sync(FULL, ob, 0);
+                out[ob + lane] = buf[nbuf - 32 + lane];
+                nbuf -= 32;
+                __syncwarp();
+            }
         }
+    }
+    __syncwarp();
+    if (!last && nbuf > 0) {
+        unsigned ob = 0;
+        if (lane == 0) ob = atomicAdd(out_count, (unsigned)nbuf);
+        ob = __shfl_sync(FULL, ob, 0);
+        if (lane < (unsigned)nbuf) out[ob + lane] = buf[lane];
     }
     if (a.stage_counts && r == 0 && lane == 0 && n_pass) atomicAdd(a.stage_counts + 2, n_pass);
     if (a.stage_counts && last && lane == 0 && n_pass) atomicAdd(a.stage_counts + 3, n_pass);
