@@ -41,7 +41,7 @@ namespace ss {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int WARPS = 8;   // consumer warps per CTA (one tile row each)
+constexpr int WARPS = 16;  // stage-1 consumer warps per CTA (one tile row each)
 constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
 
 struct RingDev {
@@ -287,7 +287,7 @@ __device__ __forceinline__ void append(bool flag, int x, int y, int2* list, unsi
 // K3a: every grid centre of the decided rows -- border keeps into the mask,
 // ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
 // passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
-__global__ void __launch_bounds__((WARPS + 1) * 32) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
+__global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
                                                                   const TileMap tm, int2* list0, unsigned* count0) {
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
