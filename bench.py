@@ -356,17 +356,19 @@ def run_ours(args):
         for _ in range(max(3, min(args.steps, 10))):
             t0 = time.perf_counter()
             res = screen(case.image, case.template, cfg, device=dev)
+            cand = res.candidates.array()  # the survivor list read back to the host
             times.append(time.perf_counter() - t0)
-        h2d = case.image.nbytes + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None)
-        words = (wl.width + 31) // 32
-        d2h = (len(tp.sizes) * wl.height * words * 4 + wl.height * words * 4 + len(res.candidates) * 8 + 16
-               + len(tp.sizes) * 8)
+        n_inst = sum(math.ceil(m * wl.ladder_ratio) - m + 1 for m in tp.ladder if m >= 8)
+        h2d = (case.image.nbytes + case.template.nbytes + n_inst * 36 * 4
+               + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None))
+        d2h = len(cand) * 8 + 16 + len(tp.sizes) * 8 + n_inst * 16 * 3 * 8
         e2e_t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e = {"value": total_positions / float(e2e_t.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e2e_t.item()),
-               "api": "paper_1707_05647_b200.screen(numpy image, numpy template, cfg) incl. host feature sets"}
+               "api": "paper_1707_05647_b200.screen(numpy image, numpy template, cfg) + candidates read back; "
+                      "template feature sets included; masks stay on the device until accessed"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

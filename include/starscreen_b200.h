@@ -183,6 +183,22 @@ int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int
 int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t k_hi, int32_t n_rings,
                         const int32_t* h_ring_n, const int32_t* h_ring_d, double q_mean, double q_std,
                         double q_grad, int64_t* h_keys, int64_t* h_key_off);
+/*
+ * Host: guard-banded key sets (screening.py:122-155) from precomputed ring
+ * features h_feats[nk][n_rings][3] (mean, std, grad_mag), rescales in k
+ * order.  Same outputs / errors as ss_feature_set_keys.
+ */
+int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, double q_mean, double q_std,
+                          double q_grad, int64_t* h_keys, int64_t* h_key_off);
+/*
+ * Device (f2): ring features of n_inst (m, k) rescale instances of the n x n
+ * template d_template in one launch.  d_desc: n_inst rows of desc_stride
+ * int32 = [m, k, n_rings, 0, n_0, d_0, n_1, d_1, ...] (desc_stride >=
+ * 4 + 2*SS_MAX_RINGS); d_out: n_inst x SS_MAX_RINGS x 3 doubles.  Bit-identical
+ * to ss_template_ring_features.
+ */
+int ss_template_features_device(const uint8_t* d_template, int32_t n, int32_t n_inst, const int32_t* d_desc,
+                                int32_t desc_stride, double* d_out, void* stream);
 /* Ring features (mean, std, grad_mag per ring) of one rescale k (tests). */
 int ss_template_ring_features(const uint8_t* h_template, int32_t n, int32_t k, int32_t m, int32_t n_rings,
                               const int32_t* h_ring_n, const int32_t* h_ring_d, double* h_out);

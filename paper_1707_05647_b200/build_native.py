@@ -25,6 +25,7 @@ SOURCES = {
     "ss_build.cu": [],
     "ss_screen.cu": ["-fmad=false"],
     "ss_post.cu": [],
+    "ss_featureset.cu": ["-fmad=false"],
 }
 
 

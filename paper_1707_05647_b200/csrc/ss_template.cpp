@@ -147,6 +147,16 @@ int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t
         for (int32_t t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
         for (auto& th : pool) th.join();
     }
+    return ss_keys_from_features(feats.data(), nk, n_rings, q_mean, q_std, q_grad, h_keys, h_key_off);
+}
+
+int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, double q_mean, double q_std,
+                          double q_grad, int64_t* h_keys, int64_t* h_key_off) {
+    if (!h_feats || nk < 0 || n_rings < 1 || n_rings > SS_MAX_RINGS) {
+        ss::set_error("bad feature-key arguments");
+        return SS_EINVAL;
+    }
+    const double* feats_ = h_feats;
     // FeatureSet.insert in k order (screening.py:127-145)
     const double qs[3] = {q_mean, q_std, q_grad};
     std::vector<std::vector<int64_t>> rings(n_rings);
@@ -155,7 +165,7 @@ int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t
             int64_t cells[3][3];
             int nc[3];
             for (int ch = 0; ch < 3; ++ch) {
-                const double v = feats[((size_t)i * n_rings + r) * 3 + ch], q = qs[ch], half = q / 2.0;
+                const double v = feats_[((size_t)i * n_rings + r) * 3 + ch], q = qs[ch], half = q / 2.0;
                 int64_t c3[3] = {ss::quantize(v - half, q), ss::quantize(v, q), ss::quantize(v + half, q)};
                 std::sort(c3, c3 + 3);
                 nc[ch] = (int)(std::unique(c3, c3 + 3) - c3);

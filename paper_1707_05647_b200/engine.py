@@ -20,7 +20,7 @@ import torch
 
 from . import _native
 from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, patch_center_margins, ring_plan
-from .featureset import FeatureSet, build_feature_set, keyset_blob
+from .featureset import FeatureSet, build_feature_set, build_feature_sets_device, keyset_blob
 
 
 def _p(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -57,14 +57,21 @@ class TemplatePlan:
 
 
 def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device) -> TemplatePlan:
-    """Template side of screen() (screening.py:497, 511): ladder + per-size key sets."""
+    """Template side of screen() (screening.py:497, 511): ladder + per-size key sets.
+
+    On a CUDA device the rescale features of every size come from one GPU
+    launch (f2, build_feature_sets_device); otherwise from the host C++ path.
+    """
     n = template.shape[1]
     ladder = ladder_sizes(n, cfg)
     tp = TemplatePlan(n, cfg, ladder)
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    evaluated = [m for m in ladder if m >= MIN_PATCH_SIDE]
+    fsets = build_feature_sets_device(template, evaluated, cfg, dev) if dev.type == "cuda" else {}
     for m in ladder:
         sp = SizePlan(m)
         if m >= MIN_PATCH_SIDE:
-            fs = build_feature_set(template, m, cfg)
+            fs = fsets[m] if m in fsets else build_feature_set(template, m, cfg)
             sp.plan = fs.plan
             sp.feature_set = fs
             sp.blob = keyset_blob(fs)

@@ -148,6 +148,63 @@ def build_feature_set(template: np.ndarray, m: int, cfg: ScreeningConfig) -> Fea
     return fs
 
 
+SS_MAX_RINGS = 16
+DESC_STRIDE = 4 + 2 * SS_MAX_RINGS
+
+
+def build_feature_sets_device(template: np.ndarray, ms, cfg: ScreeningConfig, device) -> dict:
+    """build_feature_set for every size in `ms` with the rescale features on the GPU (f2).
+
+    One kernel launch evaluates every (m, k) rescale instance
+    (csrc/ss_featureset.cu); the guard-banded key sets are then built on the
+    host from the returned features, in k order, exactly as build_feature_set
+    (screening.py:222-250) does.
+    """
+    import torch
+
+    tpl = as_gray(template)
+    n = tpl.shape[0]
+    if tpl.shape[0] != tpl.shape[1]:
+        raise ValueError(f"template must be square, got {tpl.shape[1]}x{tpl.shape[0]}")
+    sizes = []
+    rows = []
+    for m in ms:
+        if m < MIN_PATCH_SIDE:
+            raise ValueError(f"patch side {m} below minimum {MIN_PATCH_SIDE}")
+        plan = ring_plan(m, cfg.ring_count)
+        k_hi = math.ceil(m * cfg.ladder_ratio)
+        first = len(rows)
+        for k in range(m, k_hi + 1):
+            d = np.zeros(DESC_STRIDE, np.int32)
+            d[0], d[1], d[2] = m, k, len(plan)
+            for r, (nr, dr) in enumerate(plan):
+                d[4 + 2 * r], d[5 + 2 * r] = nr, dr
+            rows.append(d)
+        sizes.append((m, plan, first, len(rows) - first))
+    out = {}
+    if not rows:
+        return out
+    dev = torch.device(device)
+    d_desc = torch.from_numpy(np.stack(rows)).to(dev)
+    d_tpl = torch.from_numpy(tpl).to(dev)
+    d_out = torch.empty((len(rows), SS_MAX_RINGS, 3), dtype=torch.float64, device=dev)
+    _native.check(_native.lib().ss_template_features_device(
+        d_tpl.data_ptr(), n, len(rows), d_desc.data_ptr(), DESC_STRIDE, d_out.data_ptr(),
+        torch.cuda.current_stream(dev).cuda_stream), "template features")
+    feats_all = d_out.cpu().numpy()
+    qm, qs, qg = cfg.quantizer.factors()
+    for m, plan, first, nk in sizes:
+        feats = np.ascontiguousarray(feats_all[first:first + nk, :len(plan), :])
+        keys = np.empty(len(plan) * 27 * nk, np.int64)
+        off = np.empty(len(plan) + 1, np.int64)
+        _native.check(_native.lib().ss_keys_from_features(_ptr(feats), nk, len(plan), qm, qs, qg, _ptr(keys),
+                                                          _ptr(off)), "feature set")
+        fs = FeatureSet(plan, cfg.quantizer)
+        fs._set_sorted([keys[off[r]:off[r + 1]].copy() for r in range(len(plan))])
+        out[m] = fs
+    return out
+
+
 def keyset_blob(fs: FeatureSet) -> np.ndarray:
     """Device-ready membership blob of one size (keys + mean / (mean,std) projections)."""
     arrays = fs.ring_keys()

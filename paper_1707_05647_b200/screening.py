@@ -4,13 +4,14 @@ Mirrors screening.py:474-539 (same signature, validation order, error
 classes and messages, result fields) with the per-pixel work on the GPU:
 tables (K1/K2), ring features + membership + mask (K3), survivor list (K4)
 and the kept region (K5), all through libstarscreen_b200 (engine.py).  The
-template side (ladder, ring plans, guard-banded key sets) runs on the host
-(featureset.py, native C++).
+template side computes every rescale's ring features in one GPU launch (f2)
+and builds the guard-banded key sets on the host (featureset.py).
 
-Results stay bit-packed until a caller looks: ``size_masks[m]`` and
-``region_mask`` unpack on first access and ``candidates`` is a sequence
-view over the compacted int32 survivor list, so a 16384^2 x 33-size screen
-does not materialise 8.8 GB of bools or 10^7 Python tuples.
+Results stay on the device, bit-packed, until a caller looks: the counts
+(PruneStats) are read back by screen(); ``candidates`` copies the compacted
+int32 survivor list on first use; ``size_masks[m]`` / ``region_mask`` copy
+and unpack one mask on first access -- a 16384^2 x 33-size screen never
+materialises 8.8 GB of bools or 10^7 Python tuples it is not asked for.
 """
 
 from __future__ import annotations
@@ -63,23 +64,39 @@ def unpack_bits(words: np.ndarray, width: int) -> np.ndarray:
     return bits[:, :width].astype(bool)
 
 
-class SizeMasks(Mapping):
-    """Dict[m, bool (H, W)] view over bit-packed per-size keep masks."""
+def _host_words(t) -> np.ndarray:
+    """Bit-packed words as uint32 numpy (from a torch tensor or an array)."""
+    if isinstance(t, torch.Tensor):
+        return t.cpu().numpy().view(np.uint32)
+    return np.asarray(t).view(np.uint32)
 
-    def __init__(self, ladder: Tuple[int, ...], packed: np.ndarray, width: int):
+
+class SizeMasks(Mapping):
+    """Dict[m, bool (H, W)] view over bit-packed per-size keep masks.
+
+    The packed masks may stay on the device; a size is copied to the host on
+    first access to .packed(m) and unpacked on first access to [m].
+    """
+
+    def __init__(self, ladder: Tuple[int, ...], packed, width: int):
         self._ladder = tuple(ladder)
-        self._packed = packed  # (L, H, words) uint32
+        self._packed = packed  # (L, H, words) uint32 array or int32 CUDA tensor
         self._width = width
+        self._host: Dict[int, np.ndarray] = {}
         self._cache: Dict[int, np.ndarray] = {}
 
-    def __getitem__(self, m: int) -> np.ndarray:
-        if m not in self._cache:
-            k = self._ladder.index(m)  # ValueError -> KeyError below
-            self._cache[m] = unpack_bits(self._packed[k], self._width)
-        return self._cache[m]
-
     def packed(self, m: int) -> np.ndarray:
-        return self._packed[self._ladder.index(m)]
+        if m not in self._host:
+            k = self._ladder.index(m)
+            self._host[m] = _host_words(self._packed[k])
+        return self._host[m]
+
+    def __getitem__(self, m: int) -> np.ndarray:
+        if m not in self._ladder:
+            raise KeyError(m)
+        if m not in self._cache:
+            self._cache[m] = unpack_bits(self.packed(m), self._width)
+        return self._cache[m]
 
     def __contains__(self, m) -> bool:
         return m in self._ladder
@@ -90,23 +107,30 @@ class SizeMasks(Mapping):
     def __len__(self) -> int:
         return len(self._ladder)
 
-    def __missing__(self, m):  # pragma: no cover - Mapping protocol
-        raise KeyError(m)
-
 
 class CandidateList(Sequence):
-    """List[(cx, cy, m)] view: ladder order, then row-major (screening.py:280-283)."""
+    """List[(cx, cy, m)] view: ladder order, then row-major (screening.py:280-283).
 
-    def __init__(self, xy: np.ndarray, sizes: np.ndarray):
-        self.xy = xy  # (k, 2) int32
+    Backed by the compacted int32 (cx, cy) survivor list -- copied from the
+    device on first use -- and the per-size counts.
+    """
+
+    def __init__(self, xy, sizes: np.ndarray):
+        self._xy = xy  # (k, 2) int32 array or CUDA tensor
         self.m = sizes  # (k,) int32
 
     @staticmethod
-    def build(xy: np.ndarray, ladder: Tuple[int, ...], counts: List[int]) -> "CandidateList":
+    def build(xy, ladder: Tuple[int, ...], counts: List[int]) -> "CandidateList":
         return CandidateList(xy, np.repeat(np.asarray(ladder, np.int32), counts))
 
+    @property
+    def xy(self) -> np.ndarray:
+        if isinstance(self._xy, torch.Tensor):
+            self._xy = self._xy.cpu().numpy()
+        return self._xy
+
     def __len__(self) -> int:
-        return int(self.xy.shape[0])
+        return int(self.m.shape[0])
 
     def __getitem__(self, i):
         if isinstance(i, slice):
@@ -132,7 +156,7 @@ class CandidateList(Sequence):
 
     def array(self) -> np.ndarray:
         """(k, 3) int32 [cx, cy, m]."""
-        return np.concatenate([self.xy, self.m[:, None]], axis=1)
+        return np.concatenate([self.xy.reshape(-1, 2), self.m[:, None]], axis=1)
 
     def __repr__(self) -> str:
         return f"CandidateList(len={len(self)})"
@@ -153,13 +177,18 @@ class ScreeningResult:
         self._region = None
         self.stats = stats
 
+    def region_packed(self) -> np.ndarray:
+        """Bit-packed region rows (H, ceil(W/32)) uint32."""
+        if self._region_packed is None:
+            return np.zeros((self.height, (self.width + 31) // 32), np.uint32)
+        if isinstance(self._region_packed, torch.Tensor):
+            self._region_packed = _host_words(self._region_packed)
+        return self._region_packed
+
     @property
     def region_mask(self) -> np.ndarray:
         if self._region is None:
-            if self._region_packed is None:
-                self._region = np.zeros((self.height, self.width), dtype=bool)
-            else:
-                self._region = unpack_bits(self._region_packed, self.width)
+            self._region = unpack_bits(self.region_packed(), self.width)
         return self._region
 
     def __repr__(self) -> str:
@@ -211,16 +240,17 @@ def validate(image, template, cfg: ScreeningConfig):
 
 
 def fetch_result(eng: Engine, tp: TemplatePlan, start: float) -> ScreeningResult:
-    """Device -> host: per-size counts, survivor list, packed masks, region."""
+    """Counts to the host; survivor list, masks and region stay on the device
+    (private copies, the engine's buffers are reused) until first accessed."""
     totals = eng.totals.cpu()  # synchronises the stream
     kept = int(totals[0])
     if kept > eng.capacity:
         eng.recompact(tp, kept)
         totals = eng.totals.cpu()
     counts = eng.size_counts[: len(tp.sizes)].cpu().numpy().astype(np.int64)
-    xy = eng.xy[:kept].cpu().numpy()
-    packed = eng.masks[: len(tp.sizes)].cpu().numpy().view(np.uint32)
-    region = eng.region.cpu().numpy().view(np.uint32) if eng.region is not None else None
+    xy = eng.xy[:kept].clone()
+    packed = eng.masks[: len(tp.sizes)].clone()
+    region = eng.region.clone() if eng.region is not None else None
     elapsed = time.perf_counter() - start
     W, H = eng.W, eng.H
     stats = PruneStats(

@@ -95,7 +95,7 @@ def properties(res, img, wl):
         np.add.at(diff, (yb, xa), -1)
         np.add.at(diff, (yb, xb), 1)
         want_reg = diff.cumsum(0).cumsum(1)[:128, :W] > 0
-        got = unpack_bits(res._region_packed[r0:r1], W)
+        got = unpack_bits(res.region_packed()[r0:r1], W)
         assert np.array_equal(got, want_reg), r0
 
 

@@ -119,3 +119,46 @@ def test_division_routine_matches_ieee(cuda):
             _native.check(L.ss_selftest_div(1 << 22, 1000 * i + mode, b, mode, bad.data_ptr(), s))
     torch.cuda.synchronize()
     assert int(bad.item()) == 0
+
+
+def test_template_features_device_bitwise(cuda):
+    """f2: GPU rescale features == host C++ (== reference, test_native_lib) bit for bit."""
+    import torch
+
+    from paper_1707_05647_b200 import Quantizer, ScreeningConfig, build_feature_set, ring_plan
+    from paper_1707_05647_b200.featureset import build_feature_sets_device, template_ring_features
+
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        n = int(rng.integers(8, 96))
+        tpl = rng.integers(0, 256, (n, n), dtype=np.uint8)
+        ratio = float(rng.uniform(1.05, 1.5))
+        cfg = ScreeningConfig(ladder_ratio=ratio, ring_count=int(rng.integers(1, 6)),
+                              quantizer=Quantizer(*rng.uniform(0.5, 10, 3)))
+        ms = sorted({int(rng.integers(8, 3 * n)) for _ in range(3)})
+        dev = build_feature_sets_device(tpl, ms, cfg, cuda)
+        for m in ms:
+            host = build_feature_set(tpl, m, cfg)
+            for a, b in zip(dev[m].ring_keys(), host.ring_keys()):
+                assert np.array_equal(a, b), (trial, m)
+    # raw features, every rescale of a 512 patch (config 4's largest size)
+    n = 128
+    tpl = rng.integers(0, 256, (n, n), dtype=np.uint8)
+    from paper_1707_05647_b200 import _native
+
+    plan = ring_plan(512, 3)
+    rows = []
+    for k in (512, 530, 560):
+        d = np.zeros(36, np.int32)
+        d[0], d[1], d[2] = 512, k, len(plan)
+        for r, (nr, dr) in enumerate(plan):
+            d[4 + 2 * r], d[5 + 2 * r] = nr, dr
+        rows.append(d)
+    out = torch.empty((3, 16, 3), dtype=torch.float64, device=cuda)
+    _native.check(_native.lib().ss_template_features_device(
+        torch.from_numpy(tpl).to(cuda).data_ptr(), n, 3, torch.from_numpy(np.stack(rows)).to(cuda).data_ptr(), 36,
+        out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    got = out.cpu().numpy()
+    for i, k in enumerate((512, 530, 560)):
+        want = template_ring_features(tpl, k, 512, plan)
+        assert np.array_equal(got[i, :3].view(np.int64), want.view(np.int64))
