@@ -23,6 +23,9 @@ from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, p
 from .featureset import FeatureSet, build_feature_set, build_feature_sets_device, keyset_blob
 
 
+N_STREAMS = 4  # concurrent ladder sizes
+
+
 def _p(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
@@ -103,8 +106,12 @@ class Engine:
         self.words = (self.W + 31) // 32
         self.mrows = self.y_end - self.y_begin
         self.compact_ws = None
-        self.screen_ws = torch.empty(int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1))),
-                                     dtype=torch.uint8, device=self.device)
+        # ladder sizes are independent: they run on N_STREAMS side streams
+        # (fork/join around the K3 region), each with its own screen workspace
+        self.n_streams = N_STREAMS
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n_streams)]
+        ws = int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1)))
+        self.screen_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device) for _ in range(self.n_streams)]
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -116,7 +123,7 @@ class Engine:
         self.capacity = 0
         self.xy = None
         self.stage_counts = None  # set to a (4,) int64 device tensor to instrument the cascade
-        self.hooks = None  # optional (before, after) callables around each screen launch
+        self.hooks = None  # optional (before, after) callables(main_stream) around the K3 region
 
     # ── buffers ────────────────────────────────────────────────────────────
     def _ensure(self, n_sizes: int, max_m: int, capacity: int, region: bool) -> None:
@@ -168,7 +175,8 @@ class Engine:
                                              self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
                                              _stream_handle()), "build_tables")
 
-    def screen_size(self, k: int, tp: TemplatePlan) -> None:
+    def screen_size(self, k: int, tp: TemplatePlan, ws: Optional[torch.Tensor] = None) -> None:
+        ws = self.screen_ws[0] if ws is None else ws
         sp = tp.sizes[k]
         cfg = tp.config
         mask = self.masks[k]
@@ -183,7 +191,7 @@ class Engine:
             self.planes.data_ptr(), self.W, self.rows, self.pitch, self.W, self.H, self.y_origin, self.y_begin,
             self.y_end, sp.m, cfg.stride, len(sp.plan), sp.ring_n.ctypes.data, sp.ring_d.ctypes.data,
             sp.blob_dev.data_ptr(), sp.blob.ctypes.data, q[0], q[1], q[2], mask.data_ptr(), self.words, rc.data_ptr(),
-            _p(self.stage_counts), self.screen_ws.data_ptr(), self.screen_ws.numel(), s), "screen_size")
+            _p(self.stage_counts), ws.data_ptr(), ws.numel(), s), "screen_size")
 
     def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:
         return np.array([sp.m for sp in tp.sizes], np.int32)
@@ -218,12 +226,24 @@ class Engine:
         if region:
             self.region.zero_()
             self.totals[1:].zero_()
+        main = torch.cuda.current_stream(self.device)
+        if self.hooks is not None:
+            self.hooks[0](main)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        used = set()
         for k in range(len(tp.sizes)):
-            if self.hooks is not None:
-                self.hooks[0](k)
-            self.screen_size(k, tp)
-            if self.hooks is not None:
-                self.hooks[1](k)
+            j = k % self.n_streams
+            st = self.streams[j]
+            if j not in used:
+                st.wait_event(fork)
+                used.add(j)
+            with torch.cuda.stream(st):
+                self.screen_size(k, tp, self.screen_ws[j])
+        for j in used:
+            main.wait_stream(self.streams[j])
+        if self.hooks is not None:
+            self.hooks[1](main)
         self.compact_all(tp)
         if region:
             self.region_all(tp)
