@@ -23,7 +23,7 @@ from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, p
 from .featureset import FeatureSet, build_feature_set, build_feature_sets_device, keyset_blob
 
 
-N_STREAMS = 4  # concurrent ladder sizes
+N_STREAMS = 1  # concurrent ladder sizes (measured: >1 contends for L2 and is slower)
 
 
 def _p(t: Optional[torch.Tensor]) -> Optional[int]:
