@@ -156,7 +156,11 @@ class CandidateList(Sequence):
 
     def array(self) -> np.ndarray:
         """(k, 3) int32 [cx, cy, m]."""
-        return np.concatenate([self.xy.reshape(-1, 2), self.m[:, None]], axis=1)
+        xy = self.xy.reshape(-1, 2)
+        out = np.empty((xy.shape[0], 3), np.int32)
+        out[:, :2] = xy
+        out[:, 2] = self.m
+        return out
 
     def __repr__(self) -> str:
         return f"CandidateList(len={len(self)})"
