@@ -205,6 +205,20 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def k3_traffic(name):
+    """DRAM bytes (read + write) of the K3 kernels per step, from the committed
+    ncu launch list of this workload (profiles/r1/k3_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "k3_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(name)
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec["dram_bytes_per_step"], rec["source"]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -326,23 +340,26 @@ def run_ours(args):
 
     # ── roofline of the dominant kernel (K3 screen) ──
     peak, peak_src = measured_peak_hbm()
-    # algorithmic bytes: every ring-0 evaluation
-    # needs the 3 PLAIN planes (24 B/position); candidates (ring-0 mean
-    # passers) also need the 9 SQUARED/X/Y planes (72 B); +1/8 B mask bit.
-    # SURVEY.md 8(d)'s dense figure (all 12 planes, 96 B) is reported beside it.
-    alg_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
+    # algorithmic bytes: SURVEY.md 8(d)'s per-unit figure -- 96 B per
+    # position x scale (the 12 int64 planes read once per ladder size for
+    # ring 0) + 1/8 B of mask bit -- times the positions one step screens.
+    # The cascade-aware count (3 PLAIN planes for every ring-0 evaluation, the
+    # other 9 only for mean-projection passers) is reported beside it.
+    alg_bytes = 96.125 * positions
     achieved = alg_bytes / (screen_ms / 1e3) / 1e9
-    dense_bytes = 96.125 * positions
+    cascade_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
+    traffic, traffic_src = k3_traffic(wl.name)
     roofline = {
-        "bound": "hbm", "kernel": "screen_kernel (K3, all ladder sizes of one step)",
-        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        "bound": "hbm", "kernel": "screen (K3: stage1_kernel + ring_kernel, all ladder sizes of one step)",
+        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": peak_src,
-        "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": alg_bytes / max(positions, 1),
+        "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": 96.125,
+        "cascade_alg_bytes_per_step": cascade_bytes,
+        "cascade_achieved_GBps": cascade_bytes / (screen_ms / 1e3) / 1e9,
         "cascade": {"ring0_evals": stage[0], "ring0_mean_pass": stage[1], "ring0_pass": stage[2],
                     "survivors": stage[3]},
         "screen_ms_per_step": screen_ms, "screen_share_of_step": screen_ms / (total_ms / args.steps),
-        "survey_dense_bytes_per_position": 96.125,
-        "survey_dense_equiv_GBps": dense_bytes / (screen_ms / 1e3) / 1e9,
     }
 
     # ── e2e through the public API (host numpy in, host result out) ──

@@ -288,7 +288,8 @@ __device__ __forceinline__ void append(bool flag, int x, int y, int2* list, unsi
 // ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
 // passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
-                                                                  const TileMap tm, int2* list0, unsigned* count0) {
+                                                                  const TileMap tm, int2* list0, unsigned* count0,
+                                                                  unsigned* tile_ctr) {
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
@@ -310,10 +311,20 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     if (warp == WARPS) {
         // ── producer: one lane streams the tiles' corner boxes ──────────────
         if (lane == 0) {
-            int it = 0;
-            for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
+            // Tiles are handed out by a global counter so every CTA works near
+            // the same point of the strip-major order: the L2 working set is
+            // the rows in flight, not the spread of CTAs that drift apart.
+            unsigned t_next = atomicAdd(tile_ctr, 1u);
+            for (int it = 0;; ++it) {
                 const int s = it % STAGES;
+                const long long t = t_next;
+                if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);  // one tile ahead: hides the atomic
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+                if (t >= tm.n_tiles) {
+                    tile_xy[s] = make_int2(-1, -1);
+                    mbar_arrive(&full_bar[s]);
+                    break;
+                }
                 int tx, ty;
                 tile_coords(tm, t, tx, ty);
                 tile_xy[s] = make_int2(tx, ty);  // published by the mbarrier arrive below
@@ -343,12 +354,12 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     int2* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
     int nbuf = 0;
     unsigned long long n_int = 0, n_pass = 0;
-    int it = 0;
     const bool unit_stride = a.stride == 1;
-    for (long long t = blockIdx.x; t < tm.n_tiles; t += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
         const int2 txy = tile_xy[s];
+        if (txy.x < 0) break;  // producer ran out of tiles
         const int tx = txy.x, ty = txy.y;
         const int y = a.y_begin + ty * TY + warp;
         const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
 // gradient stages; rings >= 1 run the whole cascade.  Members go to `out`,
 // or -- for the last ring -- into the mask and the per-row survivor counts.
 __global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r, const int2* in, const unsigned* in_count,
-                                                      int2* out, unsigned* out_count) {
+                                                      int2* out, unsigned* out_count, unsigned* group_ctr) {
     extern __shared__ unsigned sbits[];
     __shared__ int2 stage_out[8][64];  // per-warp staging of members, flushed 32 at a time
     stage_bitmaps(a, sbits, r, r + 1);
@@ -423,18 +434,32 @@ __global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r,
     const unsigned count = *in_count;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const long long step = (long long)gridDim.x * (blockDim.x >> 5) * 32;
     int2* buf = stage_out[warp];
     int nbuf = 0;
     unsigned long long n_pass = 0;
-    long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-    // the candidate list is read one iteration ahead so the corner gathers
-    // do not wait behind the list load
-    int2 next = (base + lane < count) ? in[base + lane] : make_int2(-1, -1);
-    for (; base < count; base += step) {
+    // Warps take groups of RG entries from a global counter, in list order,
+    // so all warps gather from the same neighbourhood of the image (the list
+    // is in tile order) and the planes' rows are reused from L2.  The next
+    // entry (and the next group) is fetched one iteration ahead so the corner
+    // gathers do not wait behind the list load.
+    // The atomic's result stays in lane 0 until the group is needed, so its
+    // round trip overlaps RG / 32 iterations instead of stalling the shuffle.
+    constexpr unsigned RG = 128;
+    unsigned g_raw = 0;
+    if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
+    unsigned cur = __shfl_sync(FULL, g_raw, 0) * RG, k = 0;
+    if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
+    int2 next = (cur + lane < count) ? in[cur + lane] : make_int2(-1, -1);
+    for (bool have = cur < count; have;) {  // warp-uniform: the current slot lies in the list
         const int2 e = next;
-        const long long nidx = base + step + lane;
-        next = (nidx < count) ? in[nidx] : make_int2(-1, -1);
+        if (++k == RG / 32) {
+            k = 0;
+            cur = __shfl_sync(FULL, g_raw, 0) * RG;
+            if (lane == 0 && cur < count) g_raw = atomicAdd(group_ctr, 1u);
+        }
+        const unsigned slot = cur + 32 * k;
+        have = slot < count;
+        next = (have && slot + lane < count) ? in[slot + lane] : make_int2(-1, -1);
         const bool valid = e.x >= 0;
         bool pass = false;
         if (valid) {
@@ -547,9 +572,11 @@ static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, i
     const cuuint64_t strides[1] = {(cuuint64_t)pitch * 8};
     const cuuint32_t box[2] = {(cuuint32_t)BW, (cuuint32_t)TY};
     const cuuint32_t estr[2] = {1, 1};
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<int64_t*>(plane), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
         return SS_ECUDA;
@@ -677,7 +704,8 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         set_error("screen workspace too small: %zu < %zu", ws_bytes, need);
         return SS_EINVAL;
     }
-    // workspace: [counters: SS_MAX_RINGS+1 u32, padded] [list A] [list B]
+    // workspace: [counters: list counts [0, SS_MAX_RINGS], tile counter [32], ring group
+    //             counters [33, 33 + SS_MAX_RINGS); 256 B] [list A] [list B]
     unsigned* counts = static_cast<unsigned*>(d_ws);
     int2* list_a = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + 256);
     int2* list_b = list_a + (size_t)W * rows;
@@ -695,23 +723,36 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     TileMap tm;
     tm.n_tx = (int)((W + TX - 1) / TX);
     tm.n_ty = (int)((rows + TY - 1) / TY);
-    // column strips keep the rows a tile's corners revisit (2n apart) resident
-    // in L2: (m + rows in flight) x strip width x 24 B (PLAIN SAT/E/O) <~ 48 MB
+    // Column strips: a SAT element is used by four centres at the corners of
+    // a 2n x 2n square, so it is read from HBM once only if the rows between
+    // them (vertical reuse) and the columns between them (horizontal reuse)
+    // are still in L2.  The widest strip whose working set -- (m + rows in
+    // flight) x (strip + m) x 24 B of PLAIN SAT/E/O -- fits the budget keeps
+    // both; narrower strips re-read (strip + m) / strip of the columns.
+    const size_t s1_smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(a.ring[0].bwords, 1) * 4;
+    int s1_per_sm = 1;
+    cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, stage1_kernel, (WARPS + 1) * 32, s1_smem);
+    s1_per_sm = std::max(s1_per_sm, 1);
     {
-        const int64_t budget = 48ll << 20;
-        const int64_t rows_in_flight = (int64_t)sms * 3 * TY;
-        const int64_t width = budget / ((int64_t)(m + rows_in_flight) * 24);
-        tm.strip = (int)std::min<int64_t>(std::max<int64_t>(1, width / TX), tm.n_tx);
+        const int64_t budget = 40ll << 20;
+        const int64_t in_flight = (int64_t)sms * s1_per_sm * STAGES;  // tiles being staged or consumed
+        tm.strip = 1;
+        for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
+            const int64_t rows = (in_flight + strip - 1) / strip * TY;
+            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * 24;
+            if (ws <= budget) {
+                tm.strip = strip;
+                break;
+            }
+        }
     }
+    if (const char* e = getenv("SS_STRIP")) tm.strip = std::max(1, std::min(tm.n_tx, atoi(e)));  // experiment hook
     tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
     {
-        const size_t smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(a.ring[0].bwords, 1) * 4;
-        cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage1_kernel, (WARPS + 1) * 32, smem);
-        const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * std::max(per_sm, 1));
-        stage1_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, smem, s>>>(a, maps, tm, list_a,
-                                                                                            counts + 0);
+        const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm);
+        stage1_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, list_a,
+                                                                                            counts + 0, counts + 32);
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;
     }
@@ -723,7 +764,8 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         if (smem > 48 * 1024) cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ring_kernel, 256, smem);
-        ring_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), 256, smem, s>>>(a, r, in, counts + r, out, counts + r + 1);
+        ring_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), 256, smem, s>>>(a, r, in, counts + r, out, counts + r + 1,
+                                                                               counts + 33 + r);
         note_launch();
         if (int e = check_launch("ring_kernel")) return e;
     }
