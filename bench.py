@@ -350,7 +350,7 @@ def run_ours(args):
     cascade_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
     traffic, traffic_src = k3_traffic(wl.name)
     roofline = {
-        "bound": "hbm", "kernel": "screen (K3: stage1_kernel + ring_kernel, all ladder sizes of one step)",
+        "bound": "hbm", "kernel": "screen (K3: stage1_kernel + rings_kernel, all ladder sizes of one step)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": peak_src,

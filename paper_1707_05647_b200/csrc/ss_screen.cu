@@ -19,9 +19,10 @@
 //       TMA (mbarrier pipeline); consumer warps write the border keeps into
 //       the mask, compute the ring-0 mean cell and append the centres whose
 //       mean cell is in the ring's mean projection to a candidate list.
-//   K3b ring_kernel(r) -- one launch per ring, one candidate per thread:
-//       gathers all 32 corners of ring r at once, finishes the cascade (mean,
-//       std, gradient membership) and appends members to the next list; the
+//   K3b rings_kernel -- one launch for all rings, one candidate per thread:
+//       gathers all 32 corners of a ring at once, finishes the cascade (mean,
+//       std, gradient membership); members of ring r wait in per-warp shared
+//       queues for ring r+1 (full 32-lane batches, same L2 neighbourhood); the
 //       last ring ORs survivors into the mask.
 // The projection tests are implied by full membership, so the decision is
 // the reference's; the SQUARED/X/Y planes and most fp64 work are only
@@ -418,93 +419,109 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     }
 }
 
-// K3b: one ring over a candidate list, one centre per thread (full lanes,
-// full occupancy; all of the ring's corners are gathered in one round trip).
-// Ring 0 recomputes its mean (already passed) and finishes the std and
-// gradient stages; rings >= 1 run the whole cascade.  Members go to `out`,
-// or -- for the last ring -- into the mask and the per-row survivor counts.
-__global__ void __launch_bounds__(256, 3) ring_kernel(const ScreenArgs a, int r, const int2* in, const unsigned* in_count,
-                                                      int2* out, unsigned* out_count, unsigned* group_ctr) {
-    extern __shared__ unsigned sbits[];
-    __shared__ int2 stage_out[8][64];  // per-warp staging of members, flushed 32 at a time
-    stage_bitmaps(a, sbits, r, r + 1);
-    __syncthreads();
-    const RingDev& R = a.ring[r];
-    const bool last = (r + 1 == a.n_rings);
-    const unsigned count = *in_count;
+// K3b: every ring of the cascade over the ring-0 candidate list, one launch
+// per size.  Each warp evaluates 32 entries of one ring level at a time with
+// full lanes: a level-0 batch comes from the list, deeper levels from the
+// warp's own shared-memory queues of the previous level's members (deepest
+// full queue first, so each holds < 64).  Ring r >= 1 is therefore evaluated
+// shortly after ring r-1 on centres the warp has just touched -- their planes'
+// rows are still in L2 -- instead of in a later pass over the whole image.
+// Ring 0 recomputes its (passed) mean cell and finishes std and gradient;
+// deeper rings run the whole cascade; last-ring members are OR'ed into the
+// mask and the per-row survivor counts.
+constexpr int RK_WARPS = 8;
+constexpr int QCAP = 64;
+
+__device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
+                                          int2 e) {
+    const int cy = e.y - a.y_origin;
+    const long long* pc = a.planes + (long long)cy * a.pitch + e.x;
+    Corners c0, c2, cxk, cyk;
+    load_corners(a, R, pc, 0, c0);
+    load_corners(a, R, pc, 3, c2);
+    load_corners(a, R, pc, 1, cxk);
+    load_corners(a, R, pc, 2, cyk);
+    const Stage1 s = stage1_of(a, R, c0);
+    bool grad = false;
+    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk, grad);
+}
+
+__global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArgs a, const int2* in,
+                                                                 const unsigned* in_count, unsigned* group_ctr,
+                                                                 int bitmap_words) {
+    extern __shared__ unsigned sbits[];  // [all rings' bitmaps][queues: warp x level x QCAP int2]
+    __shared__ int qcnt[RK_WARPS][SS_MAX_RINGS];
+    stage_bitmaps(a, sbits, 0, a.n_rings);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int levels = a.n_rings;
+    int2* queues = reinterpret_cast<int2*>(sbits + ((bitmap_words + 1) & ~1)) + (size_t)warp * levels * QCAP;
+    if (lane < SS_MAX_RINGS) qcnt[warp][lane] = 0;
+    __syncthreads();
+    const unsigned count = *in_count;
     const unsigned lt = (1u << lane) - 1u;
-    int2* buf = stage_out[warp];
-    int nbuf = 0;
-    unsigned long long n_pass = 0;
-    // Warps take groups of RG entries from a global counter, in list order,
-    // so all warps gather from the same neighbourhood of the image (the list
-    // is in tile order) and the planes' rows are reused from L2.  The next
-    // entry (and the next group) is fetched one iteration ahead so the corner
-    // gathers do not wait behind the list load.
-    // The atomic's result stays in lane 0 until the group is needed, so its
-    // round trip overlaps RG / 32 iterations instead of stalling the shuffle.
+    unsigned long long n_pass0 = 0, n_surv = 0;
+    // level-0 entries come in groups of RG from a global counter, in list
+    // (tile) order; the atomic's result stays in lane 0 until needed and the
+    // next entry is loaded one batch ahead.
     constexpr unsigned RG = 128;
     unsigned g_raw = 0;
     if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
     unsigned cur = __shfl_sync(FULL, g_raw, 0) * RG, k = 0;
     if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
     int2 next = (cur + lane < count) ? in[cur + lane] : make_int2(-1, -1);
-    for (bool have = cur < count; have;) {  // warp-uniform: the current slot lies in the list
-        const int2 e = next;
-        if (++k == RG / 32) {
-            k = 0;
-            cur = __shfl_sync(FULL, g_raw, 0) * RG;
-            if (lane == 0 && cur < count) g_raw = atomicAdd(group_ctr, 1u);
+    bool have_input = cur < count;
+    for (;;) {
+        // pick the batch: deepest queue holding >= 32, else the list, else drain
+        int level = -1;
+        for (int l = levels - 1; l >= 1; --l)
+            if (qcnt[warp][l] >= 32) { level = l; break; }
+        int2 e;
+        if (level < 0 && have_input) {
+            level = 0;
+            e = next;
+            if (++k == RG / 32) {
+                k = 0;
+                cur = __shfl_sync(FULL, g_raw, 0) * RG;
+                if (lane == 0 && cur < count) g_raw = atomicAdd(group_ctr, 1u);
+            }
+            const unsigned slot = cur + 32 * k;
+            have_input = slot < count;
+            next = (have_input && slot + lane < count) ? in[slot + lane] : make_int2(-1, -1);
+        } else {
+            if (level < 0) {
+                for (int l = levels - 1; l >= 1; --l)
+                    if (qcnt[warp][l] > 0) { level = l; break; }
+                if (level < 0) break;  // list and queues empty
+            }
+            const int c = qcnt[warp][level], take = min(c, 32);
+            const int2* q = queues + level * QCAP;
+            e = ((int)lane < take) ? q[c - take + lane] : make_int2(-1, -1);
+            __syncwarp();
+            if (lane == 0) qcnt[warp][level] = c - take;
+            __syncwarp();
         }
-        const unsigned slot = cur + 32 * k;
-        have = slot < count;
-        next = (have && slot + lane < count) ? in[slot + lane] : make_int2(-1, -1);
-        const bool valid = e.x >= 0;
-        bool pass = false;
-        if (valid) {
-            const int cy = e.y - a.y_origin;
-            const long long* pc = a.planes + (long long)cy * a.pitch + e.x;
-            Corners c0, c2, cxk, cyk;
-            load_corners(a, R, pc, 0, c0);
-            load_corners(a, R, pc, 3, c2);
-            load_corners(a, R, pc, 1, cxk);
-            load_corners(a, R, pc, 2, cyk);
-            const Stage1 s = stage1_of(a, R, c0);
-            bool grad = false;
-            pass = (r == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk, grad);
-        }
+        const bool pass = e.x >= 0 && eval_ring(a, a.ring[level], sbits, level, e);
         const unsigned pb = __ballot_sync(FULL, pass);
-        n_pass += __popc(pb);
-        if (last) {
+        if (level == 0) n_pass0 += __popc(pb);
+        if (level + 1 == levels) {
+            n_surv += __popc(pb);
             if (pass) {
                 const long long row = e.y - a.y_begin;
                 atomicOr(a.mask + row * a.mask_pitch + (e.x >> 5), 1u << (e.x & 31));
                 atomicAdd(a.row_counts + row, 1u);
             }
-        } else {
-            if (pass) buf[nbuf + __popc(pb & lt)] = e;
-            nbuf += __popc(pb);
-            if (nbuf >= 32) {
-                __syncwarp();
-                unsigned ob = 0;
-                if (lane == 0) ob = atomicAdd(out_count, 32u);
-                ob = __shfl_sync(FULL, ob, 0);
-                out[ob + lane] = buf[nbuf - 32 + lane];
-                nbuf -= 32;
-                __syncwarp();
-            }
+        } else if (pb) {
+            const int c = qcnt[warp][level + 1];
+            if (pass) queues[(level + 1) * QCAP + c + __popc(pb & lt)] = e;
+            __syncwarp();
+            if (lane == 0) qcnt[warp][level + 1] = c + __popc(pb);
+            __syncwarp();
         }
     }
-    __syncwarp();
-    if (!last && nbuf > 0) {
-        unsigned ob = 0;
-        if (lane == 0) ob = atomicAdd(out_count, (unsigned)nbuf);
-        ob = __shfl_sync(FULL, ob, 0);
-        if (lane < (unsigned)nbuf) out[ob + lane] = buf[lane];
+    if (a.stage_counts && lane == 0) {
+        if (n_pass0) atomicAdd(a.stage_counts + 2, n_pass0);
+        if (n_surv) atomicAdd(a.stage_counts + 3, n_surv);
     }
-    if (a.stage_counts && r == 0 && lane == 0 && n_pass) atomicAdd(a.stage_counts + 2, n_pass);
-    if (a.stage_counts && last && lane == 0 && n_pass) atomicAdd(a.stage_counts + 3, n_pass);
 }
 
 __global__ void fill_grid_kernel(int W, int y_begin, int y_end, int stride, unsigned* mask, long long mask_pitch,
@@ -550,7 +567,7 @@ __global__ void selftest_div_kernel(unsigned long long n, unsigned long long see
 }  // namespace
 
 size_t screen_workspace_bytes(int64_t W, int64_t rows) {
-    return 256 + (size_t)2 * (size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) * sizeof(int2);
+    return 256 + (size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) * sizeof(int2);
 }
 
 // 2-D TMA descriptor of one int64 plane: dims (W+1 columns, h+1 rows), box TX x TY.
@@ -638,6 +655,7 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     a.row_counts = d_row_counts;
     a.stage_counts = d_stage_counts;
     const long long P = pitch;
+    int bm_words = 0;
     for (int r = 0; r < n_rings; ++r) {
         RingDev& R = a.ring[r];
         const int n = ring_n[r], d = ring_d[r];
@@ -680,19 +698,27 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         R.wm = R.wms = 0;
         R.bsrc = -1;
         R.bwords = 0;
-        // each kernel stages only its own ring's bitmap, at shared offset 0
+        // rings' bitmaps are packed into one shared-memory budget in ring
+        // order (ring 0 first: stage1_kernel stages it alone at offset 0);
+        // a ring that does not fit uses binary search over its sorted keys
         if (R.n_k == 0) {  // empty ring: nothing passes
-            R.bm = 0;
-            R.cm_n = 0;
-            R.bwords = 1;
+            if (bm_words + 1 <= SMEM_BITMAP_WORDS) {
+                R.bm = bm_words;
+                R.cm_n = 0;
+                R.bwords = 1;
+                bm_words += 1;
+            } else {
+                R.n_m = 0;  // binary search over nothing: never a member
+            }
         } else if (hd[12] >= 0) {
             const int64_t words = hd[13] + hd[14] + hd[15];
-            if (words <= SMEM_BITMAP_WORDS) {
-                R.bm = 0;
+            if (bm_words + words <= SMEM_BITMAP_WORDS) {
+                R.bm = bm_words;
                 R.wm = (int)hd[13];
                 R.wms = (int)hd[14];
                 R.bsrc = (int)(hd[12] * 2);
                 R.bwords = (int)words;
+                bm_words += (int)words;
             }
         }
     }
@@ -704,11 +730,10 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         set_error("screen workspace too small: %zu < %zu", ws_bytes, need);
         return SS_EINVAL;
     }
-    // workspace: [counters: list counts [0, SS_MAX_RINGS], tile counter [32], ring group
-    //             counters [33, 33 + SS_MAX_RINGS); 256 B] [list A] [list B]
+    // workspace: [counters: list count [0], tile counter [32], list group counter [33];
+    //             256 B] [ring-0 candidate list: W x rows int2]
     unsigned* counts = static_cast<unsigned*>(d_ws);
     int2* list_a = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + 256);
-    int2* list_b = list_a + (size_t)W * rows;
     if (cudaMemsetAsync(d_row_counts, 0, rows * sizeof(uint32_t), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(counts, 0, 256, s) != cudaSuccess) return check_launch("memset");
     int dev = 0, sms = 148;
@@ -756,18 +781,16 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;
     }
-    // K3b: ring r reads list r (counts[r]) and appends to list r+1 (counts[r+1])
-    for (int r = 0; r < n_rings; ++r) {
-        const int2* in = (r % 2 == 0) ? list_a : list_b;
-        int2* out = (r % 2 == 0) ? list_b : list_a;
-        const size_t smem = (size_t)std::max(a.ring[r].bwords, 1) * 4;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // K3b: all rings over list 0 (counts[0]); survivors into the mask
+    {
+        const size_t smem = (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * n_rings * QCAP * sizeof(int2);
+        cudaFuncSetAttribute(rings_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ring_kernel, 256, smem);
-        ring_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), 256, smem, s>>>(a, r, in, counts + r, out, counts + r + 1,
-                                                                               counts + 33 + r);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rings_kernel, RK_WARPS * 32, smem);
+        rings_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, s>>>(a, list_a, counts + 0,
+                                                                                     counts + 33, bm_words);
         note_launch();
-        if (int e = check_launch("ring_kernel")) return e;
+        if (int e = check_launch("rings_kernel")) return e;
     }
     return SS_OK;
 }
