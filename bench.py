@@ -76,7 +76,7 @@ def config_json(wl, ladder, n_gpus, extra=None):
         "quantizer": list(wl.q),
         "parallelism": f"image-parallel x{n_gpus}" if n_gpus > 1 else "single GPU",
         "per_rank_images": 1,
-        "l2": "flushed (256 MiB write) between timed steps; tables are 12 int64 planes "
+        "l2": "flushed (256 MiB write) between timed steps; tables are 12 planes (32-bit cells mod 2^32 where exact, else int64) "
               f"({12 * 8 * (wl.width + 1) * (wl.height + 1) / 1e6:.0f} MB) > 126 MB L2",
     }
     if extra:

@@ -71,6 +71,18 @@ size_t ss_build_workspace_bytes(int64_t W, int64_t H);
  */
 int ss_build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
                     int64_t plane_pitch, void* d_workspace, size_t workspace_bytes, void* stream);
+/* Bytes of the 12-plane block of 32-bit cells (same pitch, in elements). */
+size_t ss_tables32_bytes(int64_t W, int64_t H);
+/*
+ * ss_build_tables writing the int64 planes and/or ("32-bit planes") the same
+ * cells mod 2^32 in one pass; either pointer may be NULL, not both.  The
+ * screen reads the 32-bit planes for every ladder size whose ring sums fit
+ * (ss_screen_fits32) -- half the bytes per corner -- and the int64 planes
+ * otherwise.
+ */
+int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                     uint32_t* d_planes32, int64_t plane_pitch, void* d_workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* ── per-size membership sets (screening.py:100-178 FeatureSet) ──────── */
 /*
@@ -89,7 +101,10 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
 /*
  * Evaluates every grid centre of global rows [y_begin, y_end) for patch side
  * m.  The tables cover a w x h sub-image whose row 0 is global row y_origin
- * (full width: w == W); row-band shards pass their halo'd band.  Writes the
+ * (full width: w == W); row-band shards pass their halo'd band.  d_planes /
+ * d_planes32: the int64 and/or 32-bit planes of ss_build_tables2 (either may
+ * be NULL; the 32-bit ones are used when ss_screen_fits32 holds for the ring
+ * plan, and the int64 ones are then not needed).  Writes the
  * bit-packed keep mask (bit x%32 of word x/32, rows y_begin.. at
  * mask_pitch_words apart; border grid centres set, as the reference keeps
  * them) and, per mask row, the number of evaluated survivors into
@@ -100,12 +115,18 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
  * passes (candidates that read the SQUARED / X / Y planes), ring-0 full
  * passes, and final survivors.
  */
-int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_pitch, int64_t W, int64_t H,
-                   int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,
-                   const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
-                   double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
-                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* d_workspace,
-                   size_t workspace_bytes, void* stream);
+int ss_screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
+                   int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride,
+                   int32_t n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob,
+                   const int64_t* h_blob, double q_mean, double q_std, double q_grad, uint32_t* d_mask,
+                   int64_t mask_pitch_words, uint32_t* d_row_counts, unsigned long long* d_stage_counts,
+                   void* d_workspace, size_t workspace_bytes, void* stream);
+/*
+ * 1 when every region sum of ring_plan (h_ring_n, h_ring_d) is recoverable
+ * from the 32-bit planes: PLAIN / SQUARED sums < 2^32 and centred x / y
+ * moments < 2^31 in magnitude (n <= 128 for 8-bit images); else 0.
+ */
+int ss_screen_fits32(int32_t n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d);
 /* Bytes of device workspace ss_screen_size needs for `rows` decided rows. */
 size_t ss_screen_workspace_bytes(int64_t W, int64_t rows);
 

@@ -35,8 +35,11 @@ _SIGS = {
     "ss_tables_bytes": (c_sz, [c_i64, c_i64]),
     "ss_build_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "ss_build_tables": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_sz, c_p]),
+    "ss_tables32_bytes": (c_sz, [c_i64, c_i64]),
+    "ss_build_tables2": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_i64, c_p, c_sz, c_p]),
+    "ss_screen_fits32": (ctypes.c_int, [c_i32, c_p, c_p]),
     "ss_keyset_blob": (ctypes.c_int, [c_p, c_p, c_i32, c_p, ctypes.POINTER(c_sz)]),
-    "ss_screen_size": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
+    "ss_screen_size": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
                                       c_i32, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),
     "ss_screen_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "ss_selftest_div": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, c_d, c_i32, c_p, c_p]),

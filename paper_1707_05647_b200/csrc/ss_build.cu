@@ -37,7 +37,8 @@ constexpr unsigned FULL = 0xffffffffu;
 struct BuildArgs {
     const uint8_t* img;
     int64_t W, H, img_pitch;
-    long long* planes;  // 12 planes
+    long long* planes;   // 12 int64 planes (nullable)
+    unsigned* planes32;  // 12 planes mod 2^32, same pitch (nullable)
     int64_t pitch, plane_stride;
     const long long* rowpre;  // [H][G+1][3]
     int64_t G;
@@ -52,6 +53,8 @@ __device__ __forceinline__ long long shfl_down64(long long v, int d) {
 __device__ __forceinline__ long long shfl_up64(long long v, int d) {
     return (long long)__shfl_up_sync(FULL, (unsigned long long)v, d);
 }
+
+__device__ __forceinline__ int64_t r_off(const BuildArgs& a, int64_t r) { return r * a.pitch; }
 
 // state pointer: band b, kind k, type (0 S, 1 FF, 2 GG)
 __device__ __forceinline__ long long* st_ptr(const BuildArgs& a, int64_t b, int k, int type) {
@@ -115,9 +118,12 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
         const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;
         if (c >= c0 && c < c0 + CW && c < a.pitch) {
             for (int p = 0; p < 12; ++p) {
-                long long* dst = a.planes + p * a.plane_stride + c;
-                reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(0, 0);
-                reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(0, 0);
+                if (a.planes) {
+                    long long* dst = a.planes + p * a.plane_stride + c;
+                    reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(0, 0);
+                    reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(0, 0);
+                }
+                if (a.planes32) *reinterpret_cast<uint4*>(a.planes32 + p * a.plane_stride + c) = make_uint4(0, 0, 0, 0);
             }
         }
     }
@@ -235,19 +241,28 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
             if (kMode == 1) {
                 const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;  // plane column of j = 0
                 if (c >= c0 && c < c0 + CW && c < a.pitch) {
-                    const int64_t r = y + 1;
-                    long long* ps = a.planes + (0 * 4 + k) * a.plane_stride + r * a.pitch + c;
-                    long long* pe = a.planes + (1 * 4 + k) * a.plane_stride + r * a.pitch + c;
-                    long long* po = a.planes + (2 * 4 + k) * a.plane_stride + r * a.pitch + c;
-                    longlong2* vs = reinterpret_cast<longlong2*>(ps);
-                    longlong2* ve = reinterpret_cast<longlong2*>(pe);
-                    longlong2* vo = reinterpret_cast<longlong2*>(po);
-                    vs[0] = make_longlong2(S[k][0], S[k][1]);
-                    vs[1] = make_longlong2(S[k][2], S[k][3]);
-                    ve[0] = make_longlong2(Fn[0] - Gn[0], Fn[1] - Gn[1]);
-                    ve[1] = make_longlong2(Fn[2] - Gn[2], Fn[3] - Gn[3]);
-                    vo[0] = make_longlong2(Fn[1] - Gn[0], Fn[2] - Gn[1]);
-                    vo[1] = make_longlong2(Fn[3] - Gn[2], fnext - Gn[3]);
+                    const int64_t off = r_off(a, y + 1) + c;
+                    const long long e0 = Fn[0] - Gn[0], e1 = Fn[1] - Gn[1], e2 = Fn[2] - Gn[2], e3 = Fn[3] - Gn[3];
+                    const long long o0 = Fn[1] - Gn[0], o1 = Fn[2] - Gn[1], o2 = Fn[3] - Gn[2], o3 = fnext - Gn[3];
+                    if (a.planes) {
+                        longlong2* vs = reinterpret_cast<longlong2*>(a.planes + (0 * 4 + k) * a.plane_stride + off);
+                        longlong2* ve = reinterpret_cast<longlong2*>(a.planes + (1 * 4 + k) * a.plane_stride + off);
+                        longlong2* vo = reinterpret_cast<longlong2*>(a.planes + (2 * 4 + k) * a.plane_stride + off);
+                        vs[0] = make_longlong2(S[k][0], S[k][1]);
+                        vs[1] = make_longlong2(S[k][2], S[k][3]);
+                        ve[0] = make_longlong2(e0, e1);
+                        ve[1] = make_longlong2(e2, e3);
+                        vo[0] = make_longlong2(o0, o1);
+                        vo[1] = make_longlong2(o2, o3);
+                    }
+                    if (a.planes32) {  // the same cells mod 2^32 (region sums are exact in 32 bits)
+                        *reinterpret_cast<uint4*>(a.planes32 + (0 * 4 + k) * a.plane_stride + off) =
+                            make_uint4((unsigned)S[k][0], (unsigned)S[k][1], (unsigned)S[k][2], (unsigned)S[k][3]);
+                        *reinterpret_cast<uint4*>(a.planes32 + (1 * 4 + k) * a.plane_stride + off) =
+                            make_uint4((unsigned)e0, (unsigned)e1, (unsigned)e2, (unsigned)e3);
+                        *reinterpret_cast<uint4*>(a.planes32 + (2 * 4 + k) * a.plane_stride + off) =
+                            make_uint4((unsigned)o0, (unsigned)o1, (unsigned)o2, (unsigned)o3);
+                    }
                 }
             }
         }
@@ -419,7 +434,7 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
     return check_launch("band_kernel<final>");
 }
 
-int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes, uint32_t* d_planes32,
                  int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream) {
     if (W < 1 || H < 1) { set_error("empty image"); return SS_EINVAL; }
     if (overflow_guard_fails(W, H)) {
@@ -431,7 +446,8 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         set_error("plane_pitch must be ss_plane_pitch(W) = %lld", (long long)plane_pitch(W));
         return SS_EINVAL;
     }
-    if (!d_img || !d_planes || (reinterpret_cast<uintptr_t>(d_planes) & 15)) {
+    if (!d_img || (!d_planes && !d_planes32) || (reinterpret_cast<uintptr_t>(d_planes) & 15) ||
+        (reinterpret_cast<uintptr_t>(d_planes32) & 15)) {
         set_error("null or misaligned device pointer");
         return SS_EINVAL;
     }
@@ -448,6 +464,7 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     a.H = H;
     a.img_pitch = img_pitch;
     a.planes = reinterpret_cast<long long*>(d_planes);
+    a.planes32 = reinterpret_cast<unsigned*>(d_planes32);
     a.pitch = plane_pitch_;
     a.plane_stride = (H + 1) * plane_pitch_;
     a.G = n_groups(W);
@@ -472,9 +489,17 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
 extern "C" {
 int64_t ss_plane_pitch(int64_t W) { return ss::plane_pitch(W); }
 size_t ss_tables_bytes(int64_t W, int64_t H) { return (size_t)12 * (size_t)(H + 1) * ss::plane_pitch(W) * 8; }
+size_t ss_tables32_bytes(int64_t W, int64_t H) { return (size_t)12 * (size_t)(H + 1) * ss::plane_pitch(W) * 4; }
 size_t ss_build_workspace_bytes(int64_t W, int64_t H) { return ss::build_workspace_bytes(W, H); }
 int ss_build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
                     int64_t plane_pitch, void* d_workspace, size_t workspace_bytes, void* stream) {
-    return ss::build_tables(d_img, W, H, img_pitch, d_planes, plane_pitch, d_workspace, workspace_bytes, stream);
+    return ss::build_tables(d_img, W, H, img_pitch, d_planes, nullptr, plane_pitch, d_workspace, workspace_bytes,
+                            stream);
+}
+int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                     uint32_t* d_planes32, int64_t plane_pitch, void* d_workspace, size_t workspace_bytes,
+                     void* stream) {
+    return ss::build_tables(d_img, W, H, img_pitch, d_planes, d_planes32, plane_pitch, d_workspace, workspace_bytes,
+                            stream);
 }
 }

@@ -60,7 +60,7 @@ struct RingDev {
 };
 
 struct ScreenArgs {
-    const long long* planes;
+    const void* planes;   // 12 planes of int64, or of uint32 (cells mod 2^32)
     long long pitch, ps;  // row pitch, plane stride (elements)
     int W, H, y_origin, y_begin, y_end, stride, lo, hi, n_rings;
     double qm, qs, qg, rqm, rqs, rqg;
@@ -122,29 +122,43 @@ __device__ __forceinline__ bool member_k(const ScreenArgs& a, const RingDev& R, 
     return bsearch_eq(a.blob + R.off_k, R.n_k, ((long long)cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
 }
 
-__device__ __forceinline__ long long ld(const long long* p) { return __ldg(p); }
-
-// The 8 corner elements of one kind for ring R (4 SAT, 2 E, 2 O), loaded
-// together so a single memory round trip covers them.
-struct Corners {
-    long long q[4], e[2], o[2];
+// Plane elements: exact int64 cells, or the same cells mod 2^32 (u32).  A
+// region sum is a +-+- combination of four cells; with u32 planes it is
+// computed mod 2^32 and recovered exactly because the host only takes the u32
+// path when every ring's sums are known to fit (fits32()):
+//   PLAIN / SQUARED sums are non-negative and < 2^32;
+//   X / Y sums are (c + 1) * S1 + D with D = sum (x - c) v, |D| < 2^31, so
+//   D = (int32)(sum - (c + 1) * S1 mod 2^32).
+template <typename T> struct Corners {
+    T q[4], e[2], o[2];
 };
-__device__ __forceinline__ void load_corners(const ScreenArgs& a, const RingDev& R, const long long* pc, int kind,
-                                             Corners& c) {
-    const long long* pq = pc + (long long)kind * a.ps;
-    const long long* pe = pc + (long long)(4 + kind) * a.ps;
-    const long long* po = pc + (long long)(8 + kind) * a.ps;
-    c.q[0] = ld(pq + R.sa);
-    c.q[1] = ld(pq + R.sb);
-    c.q[2] = ld(pq + R.sc);
-    c.q[3] = ld(pq + R.sd);
-    c.e[0] = ld(pe + R.ea);
-    c.e[1] = ld(pe + R.ed);
-    c.o[0] = ld(po + R.ob);
-    c.o[1] = ld(po + R.oc);
+template <typename T>
+__device__ __forceinline__ void load_corners(const ScreenArgs& a, const RingDev& R, const T* pc, int kind,
+                                             Corners<T>& c) {
+    const T* pq = pc + (long long)kind * a.ps;
+    const T* pe = pc + (long long)(4 + kind) * a.ps;
+    const T* po = pc + (long long)(8 + kind) * a.ps;
+    c.q[0] = __ldg(pq + R.sa);
+    c.q[1] = __ldg(pq + R.sb);
+    c.q[2] = __ldg(pq + R.sc);
+    c.q[3] = __ldg(pq + R.sd);
+    c.e[0] = __ldg(pe + R.ea);
+    c.e[1] = __ldg(pe + R.ed);
+    c.o[0] = __ldg(po + R.ob);
+    c.o[1] = __ldg(po + R.oc);
 }
-__device__ __forceinline__ long long sq_of(const Corners& c) { return c.q[0] - c.q[1] - c.q[2] + c.q[3]; }
-__device__ __forceinline__ long long di_of(const Corners& c) { return c.e[0] - c.o[0] - c.o[1] + c.e[1]; }
+template <typename T> __device__ __forceinline__ T sq_of(const Corners<T>& c) { return c.q[0] - c.q[1] - c.q[2] + c.q[3]; }
+template <typename T> __device__ __forceinline__ T di_of(const Corners<T>& c) { return c.e[0] - c.o[0] - c.o[1] + c.e[1]; }
+
+// exact non-negative region sum (PLAIN, SQUARED)
+__device__ __forceinline__ long long unsigned_sum(long long v) { return v; }
+__device__ __forceinline__ long long unsigned_sum(unsigned v) { return (long long)v; }
+// exact weighted region sum with weight (c + 1) at the centre column/row c
+__device__ __forceinline__ long long weighted_sum(long long v, long long, long long) { return v; }
+__device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long long s1) {
+    const long long base = c1 * s1;
+    return base + (long long)(int)(v - (unsigned)base);
+}
 
 struct Stage1 {
     long long s1q, s1d;
@@ -153,10 +167,11 @@ struct Stage1 {
 };
 
 // Stage 1 (mean cell) of ring R from its PLAIN corners.
-__device__ __forceinline__ Stage1 stage1_of(const ScreenArgs& a, const RingDev& R, const Corners& c) {
+template <typename T>
+__device__ __forceinline__ Stage1 stage1_of(const ScreenArgs& a, const RingDev& R, const Corners<T>& c) {
     Stage1 s;
-    s.s1q = sq_of(c);
-    s.s1d = di_of(c);
+    s.s1q = unsigned_sum(sq_of(c));
+    s.s1d = unsigned_sum(di_of(c));
     s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);                   // features.py:325
     s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);                   // features.py:349
     s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
@@ -164,23 +179,25 @@ __device__ __forceinline__ Stage1 stage1_of(const ScreenArgs& a, const RingDev& 
 }
 
 // Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
+template <typename T>
 __device__ __forceinline__ bool finish_of(const ScreenArgs& a, const RingDev& R, const unsigned* sb, int cx, int cy,
-                                         const Stage1& s, const Corners& c2, const Corners& cx_, const Corners& cy_,
-                                         bool& grad) {
-    const long long s2q = sq_of(c2), s2d = di_of(c2);
+                                         const Stage1& s, const Corners<T>& c2, const Corners<T>& cx_,
+                                         const Corners<T>& cy_) {
+    const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
     // features.py:326, 350: sqrt(max(s2/count - mean*mean, 0))
     const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
     const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
     const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
     const int cs = quant(sd, a.qs, a.rqs);
     if (!member_ms(a, R, sb, s.cm, cs)) return false;
-    grad = true;
     const double fq = (double)s.s1q, fd = (double)s.s1d;
+    const long long sxq = weighted_sum(sq_of(cx_), cx + 1, s.s1q), syq = weighted_sum(sq_of(cy_), cy + 1, s.s1q);
+    const long long sxd = weighted_sum(di_of(cx_), cx + 1, s.s1d), syd = weighted_sum(di_of(cy_), cy + 1, s.s1d);
     // features.py:328-329, 351-352: (s - (c + off) * s1) / w1; product and difference are exact
-    const double gxq = div_rn(__dsub_rn((double)sq_of(cx_), __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gyq = div_rn(__dsub_rn((double)sq_of(cy_), __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gxd = div_rn(__dsub_rn((double)di_of(cx_), __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
-    const double gyd = div_rn(__dsub_rn((double)di_of(cy_), __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
     const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
     const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
     const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
@@ -223,26 +240,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 struct TmaMaps {
-    CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) int64
+    CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) of T
 };
 
 // Stage-1 tile geometry: TY rows (one per consumer warp) x TX columns; the 8
 // ring-0 PLAIN corner boxes of a tile are staged by TMA into one pipeline
 // stage.  Measured on B200 + driver 580: a tile-mode TMA box must start at a
 // 16-byte aligned inner coordinate (an odd int64 column raises "illegal
-// instruction"), so each box starts at the even column at or below the
-// corner and is BW = TX + 2 columns wide; readers skip the parity offset.
-constexpr int TY = WARPS;   // tile rows
-constexpr int CPW = 2;      // 32-centre chunks per warp per tile
+// instruction"), so each box starts at the ALIGN-column boundary at or below
+// the corner and is BW = TX + ALIGN columns wide; readers skip the offset.
+constexpr int TY = WARPS;     // tile rows
+constexpr int CPW = 2;        // 32-centre chunks per warp per tile
 constexpr int TX = 32 * CPW;  // tile columns
-constexpr int BW = TX + 2;  // staged box width (int64 columns)
 constexpr int NBOX = 8;
 constexpr int STAGES = 3;
-constexpr int BOX_ELEMS = BW * TY;
-constexpr int BOX_BYTES = BOX_ELEMS * 8;
-constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
-
-__device__ __forceinline__ int floor_even(int c) { return c & ~1; }  // two's complement: floor to even
+template <typename T> struct Geo {
+    static constexpr int ALIGN = 16 / (int)sizeof(T);
+    static constexpr int BW = TX + ALIGN;  // staged box width (elements)
+    static constexpr int BOX_ELEMS = BW * TY;
+    static constexpr int BOX_BYTES = BOX_ELEMS * (int)sizeof(T);
+    static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+    __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }  // two's complement
+    __device__ static int rem(int c) { return c & (ALIGN - 1); }
+};
 
 struct TileMap {
     int n_tx, n_ty;  // tiles along x, y
@@ -288,12 +308,14 @@ __device__ __forceinline__ void append(bool flag, int x, int y, int2* list, unsi
 // K3a: every grid centre of the decided rows -- border keeps into the mask,
 // ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
 // passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
+template <typename T>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
                                                                   const TileMap tm, int2* list0, unsigned* count0,
                                                                   unsigned* tile_ctr) {
+    using G = Geo<T>;
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
-    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * STAGE_BYTES);
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ int2 tile_xy[STAGES];  // (tx, ty) of the tile in each stage, written by the producer
     __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
@@ -331,18 +353,18 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
                 tile_xy[s] = make_int2(tx, ty);  // published by the mbarrier arrive below
                 const int x0 = tx * TX;
                 const int cy0 = a.y_begin + ty * TY - a.y_origin;  // table-local first row
-                unsigned char* dst = stage_buf + s * STAGE_BYTES;
-                mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+                unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
+                mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
                 // plane coordinates are (col = x + 1, row = y + 1) of the corner (include/starscreen_b200.h)
                 const int n = R0.n, d = R0.d;
-                tma_load_2d(dst + 0 * BOX_BYTES, &maps.sat, floor_even(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
-                tma_load_2d(dst + 1 * BOX_BYTES, &maps.sat, floor_even(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
-                tma_load_2d(dst + 2 * BOX_BYTES, &maps.sat, floor_even(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
-                tma_load_2d(dst + 3 * BOX_BYTES, &maps.sat, floor_even(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
-                tma_load_2d(dst + 4 * BOX_BYTES, &maps.e, floor_even(x0 + 1), cy0 + d + 1, &full_bar[s]);
-                tma_load_2d(dst + 5 * BOX_BYTES, &maps.e, floor_even(x0 + 1), cy0 - d, &full_bar[s]);
-                tma_load_2d(dst + 6 * BOX_BYTES, &maps.o, floor_even(x0 - d), cy0, &full_bar[s]);
-                tma_load_2d(dst + 7 * BOX_BYTES, &maps.o, floor_even(x0 + d + 1), cy0, &full_bar[s]);
+                tma_load_2d(dst + 0 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 1 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 2 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 3 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 4 * G::BOX_BYTES, &maps.e, G::floor_al(x0 + 1), cy0 + d + 1, &full_bar[s]);
+                tma_load_2d(dst + 5 * G::BOX_BYTES, &maps.e, G::floor_al(x0 + 1), cy0 - d, &full_bar[s]);
+                tma_load_2d(dst + 6 * G::BOX_BYTES, &maps.o, G::floor_al(x0 - d), cy0, &full_bar[s]);
+                tma_load_2d(dst + 7 * G::BOX_BYTES, &maps.o, G::floor_al(x0 + d + 1), cy0, &full_bar[s]);
             }
         }
         return;
@@ -350,7 +372,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
 
     // ── consumers: warp w takes row w of each tile, CPW chunks of 32 ────────
     const int ylo = a.lo, yhi = a.H - 1 - a.hi, xlo = a.lo, xhi = a.W - 1 - a.hi;
-    const int pq = (R0.n + 1) & 1, pe = 1, po0 = R0.d & 1, po1 = (R0.d + 1) & 1;  // box parity offsets (x0 even)
+    // offsets of the corner column inside each box (x0 is a multiple of ALIGN)
+    const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d), po1 = G::rem(R0.d + 1);
     const unsigned lt = (1u << lane) - 1u;
     int2* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
     int nbuf = 0;
@@ -363,13 +386,14 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
         if (txy.x < 0) break;  // producer ran out of tiles
         const int tx = txy.x, ty = txy.y;
         const int y = a.y_begin + ty * TY + warp;
-        const long long* box = reinterpret_cast<const long long*>(stage_buf + s * STAGE_BYTES) + warp * BW + lane;
+        const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
         long long s1q[CPW], s1d[CPW];
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
-            const long long* b = box + 32 * c;
-            s1q[c] = b[0 * BOX_ELEMS + pq] - b[1 * BOX_ELEMS + pq] - b[2 * BOX_ELEMS + pq] + b[3 * BOX_ELEMS + pq];
-            s1d[c] = b[4 * BOX_ELEMS + pe] - b[6 * BOX_ELEMS + po0] - b[7 * BOX_ELEMS + po1] + b[5 * BOX_ELEMS + pe];
+            const T* b = box + 32 * c;
+            constexpr int E = G::BOX_ELEMS;
+            s1q[c] = unsigned_sum((T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]));
+            s1d[c] = unsigned_sum((T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -432,20 +456,21 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
 constexpr int RK_WARPS = 8;
 constexpr int QCAP = 64;
 
+template <typename T>
 __device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
                                           int2 e) {
     const int cy = e.y - a.y_origin;
-    const long long* pc = a.planes + (long long)cy * a.pitch + e.x;
-    Corners c0, c2, cxk, cyk;
+    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + e.x;
+    Corners<T> c0, c2, cxk, cyk;
     load_corners(a, R, pc, 0, c0);
     load_corners(a, R, pc, 3, c2);
     load_corners(a, R, pc, 1, cxk);
     load_corners(a, R, pc, 2, cyk);
     const Stage1 s = stage1_of(a, R, c0);
-    bool grad = false;
-    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk, grad);
+    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk);
 }
 
+template <typename T>
 __global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArgs a, const int2* in,
                                                                  const unsigned* in_count, unsigned* group_ctr,
                                                                  int bitmap_words) {
@@ -500,7 +525,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArg
             if (lane == 0) qcnt[warp][level] = c - take;
             __syncwarp();
         }
-        const bool pass = e.x >= 0 && eval_ring(a, a.ring[level], sbits, level, e);
+        const bool pass = e.x >= 0 && eval_ring<T>(a, a.ring[level], sbits, level, e);
         const unsigned pb = __ballot_sync(FULL, pass);
         if (level == 0) n_pass0 += __popc(pb);
         if (level + 1 == levels) {
@@ -570,8 +595,10 @@ size_t screen_workspace_bytes(int64_t W, int64_t rows) {
     return 256 + (size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) * sizeof(int2);
 }
 
-// 2-D TMA descriptor of one int64 plane: dims (W+1 columns, h+1 rows), box TX x TY.
-static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, int64_t h, int64_t pitch) {
+// 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
+// h+1 rows), box BW x TY.
+static int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes, int box_w, int64_t W, int64_t h,
+                            int64_t pitch) {
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -586,12 +613,13 @@ static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, i
         encode = reinterpret_cast<EncodeFn>(fn);
     }
     const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
-    const cuuint64_t strides[1] = {(cuuint64_t)pitch * 8};
-    const cuuint32_t box[2] = {(cuuint32_t)BW, (cuuint32_t)TY};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch * (cuuint64_t)elem_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)TY};
     const cuuint32_t estr[2] = {1, 1};
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<int64_t*>(plane), dims, strides, box,
+    const CUresult r = encode(map, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_INT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                              const_cast<void*>(plane), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -601,7 +629,22 @@ static int encode_plane_map(CUtensorMap* map, const int64_t* plane, int64_t W, i
     return SS_OK;
 }
 
-int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
+// True when every region sum of ring (n, d) is recoverable from planes mod
+// 2^32 (see weighted_sum): PLAIN/SQUARED sums of the square (4n^2 pixels)
+// and the diamond (2d^2+2d+1 pixels) are < 2^32, and the centred first
+// moments |sum (x - c) v| of both are < 2^31.
+bool ring_fits32(int64_t n, int64_t d) {
+    const int64_t lim_u = (int64_t)1 << 32, lim_s = (int64_t)1 << 31;
+    if (65025 * 4 * n * n >= lim_u) return false;
+    if (65025 * (2 * d * d + 2 * d + 1) >= lim_u) return false;
+    if (255 * 2 * n * n * n >= lim_s) return false;  // sum |x - c| over the square <= 2 n^3
+    int64_t mom = 0;                                 // sum |dx| over the diamond
+    for (int64_t k = 1; k <= d; ++k) mom += 2 * k * (2 * (d - k) + 1);
+    return 255 * mom < lim_s;
+}
+
+int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t pitch, int64_t W,
+                int64_t H, int64_t y_origin,
                 int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings, const int32_t* ring_n,
                 const int32_t* ring_d, const int64_t* d_blob, const int64_t* h_blob, double qm, double qs, double qg,
                 uint32_t* d_mask, int64_t mask_pitch, uint32_t* d_row_counts, unsigned long long* d_stage_counts,
@@ -631,7 +674,6 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     }
 
     ScreenArgs a;
-    a.planes = reinterpret_cast<const long long*>(d_planes);
     a.pitch = pitch;
     a.ps = (h + 1) * pitch;
     a.W = (int)W;
@@ -722,6 +764,14 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
             }
         }
     }
+    bool use32 = d_planes32 != nullptr;
+    for (int r = 0; r < n_rings && use32; ++r) use32 = ring_fits32(ring_n[r], ring_d[r]);
+    if (!use32 && !d_planes) {
+        set_error("size m=%d needs the int64 planes (ring sums exceed 32 bits)", m);
+        return SS_EINVAL;
+    }
+    a.planes = use32 ? static_cast<const void*>(d_planes32) : static_cast<const void*>(d_planes);
+    const int eb = use32 ? 4 : 8;
     cudaStream_t s = as_stream(stream);
     const int64_t rows = y_end - y_begin;
     if (rows == 0) return SS_OK;
@@ -742,9 +792,14 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
 
     // K3a: the mask rows are (re)initialised here; survivors are OR'ed in by K3b
     TmaMaps maps;
-    if (int e = encode_plane_map(&maps.sat, d_planes, W, h, pitch)) return e;
-    if (int e = encode_plane_map(&maps.e, d_planes + 4 * a.ps, W, h, pitch)) return e;
-    if (int e = encode_plane_map(&maps.o, d_planes + 8 * a.ps, W, h, pitch)) return e;
+    {
+        const char* base = static_cast<const char*>(a.planes);
+        const int bw = use32 ? Geo<unsigned>::BW : Geo<long long>::BW;
+        const size_t pb = (size_t)a.ps * eb;
+        if (int e = encode_plane_map(&maps.sat, base, eb, bw, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.e, base + 4 * pb, eb, bw, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.o, base + 8 * pb, eb, bw, W, h, pitch)) return e;
+    }
     TileMap tm;
     tm.n_tx = (int)((W + TX - 1) / TX);
     tm.n_ty = (int)((rows + TY - 1) / TY);
@@ -752,12 +807,14 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     // a 2n x 2n square, so it is read from HBM once only if the rows between
     // them (vertical reuse) and the columns between them (horizontal reuse)
     // are still in L2.  The widest strip whose working set -- (m + rows in
-    // flight) x (strip + m) x 24 B of PLAIN SAT/E/O -- fits the budget keeps
+    // flight) x (strip + m) x 3 planes of PLAIN SAT/E/O -- fits the budget keeps
     // both; narrower strips re-read (strip + m) / strip of the columns.
-    const size_t s1_smem = (size_t)STAGES * STAGE_BYTES + (size_t)std::max(a.ring[0].bwords, 1) * 4;
+    auto s1 = use32 ? stage1_kernel<unsigned> : stage1_kernel<long long>;
+    const size_t s1_smem = (size_t)STAGES * (use32 ? Geo<unsigned>::STAGE_BYTES : Geo<long long>::STAGE_BYTES) +
+                           (size_t)std::max(a.ring[0].bwords, 1) * 4;
     int s1_per_sm = 1;
-    cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, stage1_kernel, (WARPS + 1) * 32, s1_smem);
+    cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem);
     s1_per_sm = std::max(s1_per_sm, 1);
     {
         const int64_t budget = 40ll << 20;
@@ -765,7 +822,7 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
         tm.strip = 1;
         for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
             const int64_t rows = (in_flight + strip - 1) / strip * TY;
-            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * 24;
+            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * 3 * eb;
             if (ws <= budget) {
                 tm.strip = strip;
                 break;
@@ -776,19 +833,20 @@ int screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t pitch, in
     tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
     {
         const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm);
-        stage1_kernel<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, list_a,
-                                                                                            counts + 0, counts + 32);
+        s1<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, list_a, counts + 0,
+                                                                                 counts + 32);
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;
     }
     // K3b: all rings over list 0 (counts[0]); survivors into the mask
     {
         const size_t smem = (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * n_rings * QCAP * sizeof(int2);
-        cudaFuncSetAttribute(rings_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
+        auto rk = use32 ? rings_kernel<unsigned> : rings_kernel<long long>;
+        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rings_kernel, RK_WARPS * 32, smem);
-        rings_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, s>>>(a, list_a, counts + 0,
-                                                                                     counts + 33, bm_words);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, RK_WARPS * 32, smem);
+        rk<<<(unsigned)(sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, s>>>(a, list_a, counts + 0, counts + 33,
+                                                                           bm_words);
         note_launch();
         if (int e = check_launch("rings_kernel")) return e;
     }
@@ -816,15 +874,21 @@ int selftest_div(uint64_t n, uint64_t seed, double b, int mode, unsigned long lo
 }  // namespace ss
 
 extern "C" {
-int ss_screen_size(const int64_t* d_planes, int64_t w, int64_t h, int64_t plane_pitch, int64_t W, int64_t H,
-                   int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings,
-                   const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob, const int64_t* h_blob,
-                   double q_mean, double q_std, double q_grad, uint32_t* d_mask, int64_t mask_pitch_words,
-                   uint32_t* d_row_counts, unsigned long long* d_stage_counts, void* d_workspace,
-                   size_t workspace_bytes, void* stream) {
-    return ss::screen_size(d_planes, w, h, plane_pitch, W, H, y_origin, y_begin, y_end, m, stride, n_rings, h_ring_n,
-                           h_ring_d, d_blob, h_blob, q_mean, q_std, q_grad, d_mask, mask_pitch_words, d_row_counts,
-                           d_stage_counts, d_workspace, workspace_bytes, stream);
+int ss_screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
+                   int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t m, int32_t stride,
+                   int32_t n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d, const int64_t* d_blob,
+                   const int64_t* h_blob, double q_mean, double q_std, double q_grad, uint32_t* d_mask,
+                   int64_t mask_pitch_words, uint32_t* d_row_counts, unsigned long long* d_stage_counts,
+                   void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::screen_size(d_planes, d_planes32, w, h, plane_pitch, W, H, y_origin, y_begin, y_end, m, stride, n_rings,
+                           h_ring_n, h_ring_d, d_blob, h_blob, q_mean, q_std, q_grad, d_mask, mask_pitch_words,
+                           d_row_counts, d_stage_counts, d_workspace, workspace_bytes, stream);
+}
+int ss_screen_fits32(int32_t n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d) {
+    if (n_rings < 1 || !h_ring_n || !h_ring_d) return 0;
+    for (int r = 0; r < n_rings; ++r)
+        if (!ss::ring_fits32(h_ring_n[r], h_ring_d[r])) return 0;
+    return 1;
 }
 size_t ss_screen_workspace_bytes(int64_t W, int64_t rows) { return ss::screen_workspace_bytes(W, rows); }
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,

@@ -43,6 +43,7 @@ class SizePlan:
     blob_dev: Optional[torch.Tensor] = None
     ring_n: Optional[np.ndarray] = None
     ring_d: Optional[np.ndarray] = None
+    fits32: bool = True  # ring sums recoverable from the 32-bit planes (ss_screen_fits32)
 
 
 @dataclass
@@ -81,6 +82,8 @@ def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device) -> Temp
             sp.blob_dev = torch.from_numpy(sp.blob).to(device)
             sp.ring_n = np.array([p[0] for p in fs.plan], np.int32)
             sp.ring_d = np.array([p[1] for p in fs.plan], np.int32)
+            sp.fits32 = bool(_native.lib().ss_screen_fits32(len(fs.plan), sp.ring_n.ctypes.data,
+                                                            sp.ring_d.ctypes.data))
         tp.sizes.append(sp)
     return tp
 
@@ -99,8 +102,12 @@ class Engine:
             band = (0, self.H, 0, self.H)
         self.y_origin, self.rows, self.y_begin, self.y_end = (int(v) for v in band)
         self.pitch = int(self.L.ss_plane_pitch(self.W))
-        tb = int(self.L.ss_tables_bytes(self.W, self.rows))
-        self.planes = torch.empty(tb // 8, dtype=torch.int64, device=self.device)
+        # 32-bit planes (cells mod 2^32) serve every size whose ring sums fit
+        # (ss_screen_fits32); the int64 planes are allocated and built only
+        # for templates with a larger size (see run())
+        tb32 = int(self.L.ss_tables32_bytes(self.W, self.rows))
+        self.planes32 = torch.empty(tb32 // 4, dtype=torch.int32, device=self.device)
+        self.planes = None
         self.build_ws = torch.empty(max(1, int(self.L.ss_build_workspace_bytes(self.W, self.rows))), dtype=torch.uint8,
                                     device=self.device)
         self.words = (self.W + 31) // 32
@@ -123,6 +130,7 @@ class Engine:
         self.capacity = 0
         self.xy = None
         self.stage_counts = None  # set to a (4,) int64 device tensor to instrument the cascade
+        self.force_int64 = False  # test hook: screen every size from the int64 planes
         self.hooks = None  # optional (before, after) callables(main_stream) around the K3 region
 
     # ── buffers ────────────────────────────────────────────────────────────
@@ -167,13 +175,27 @@ class Engine:
         return total
 
     # ── the hot path ───────────────────────────────────────────────────────
-    def build_tables(self, img: torch.Tensor) -> None:
-        """K1/K2 on the current stream.  img: (rows, W) uint8 on the device."""
+    def needs_int64(self, tp: TemplatePlan) -> bool:
+        """True when some size's ring sums exceed the 32-bit planes."""
+        if self.force_int64:
+            return True
+        for sp in tp.sizes:
+            if sp.plan and not sp.fits32:
+                return True
+        return False
+
+    def build_tables(self, img: torch.Tensor, int64: bool = False) -> None:
+        """K1/K2 on the current stream.  img: (rows, W) uint8 on the device.
+        Writes the 32-bit planes, and the int64 planes too when `int64`."""
         assert img.dtype == torch.uint8 and img.is_cuda and img.shape == (self.rows, self.W)
         img = img.contiguous()
-        _native.check(self.L.ss_build_tables(img.data_ptr(), self.W, self.rows, self.W, self.planes.data_ptr(),
-                                             self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
-                                             _stream_handle()), "build_tables")
+        if int64 and self.planes is None:
+            tb = int(self.L.ss_tables_bytes(self.W, self.rows))
+            self.planes = torch.empty(tb // 8, dtype=torch.int64, device=self.device)
+        _native.check(self.L.ss_build_tables2(img.data_ptr(), self.W, self.rows, self.W,
+                                              _p(self.planes) if int64 else None, self.planes32.data_ptr(),
+                                              self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
+                                              _stream_handle()), "build_tables")
 
     def screen_size(self, k: int, tp: TemplatePlan, ws: Optional[torch.Tensor] = None) -> None:
         ws = self.screen_ws[0] if ws is None else ws
@@ -188,7 +210,8 @@ class Engine:
             return
         q = cfg.quantizer.factors()
         _native.check(self.L.ss_screen_size(
-            self.planes.data_ptr(), self.W, self.rows, self.pitch, self.W, self.H, self.y_origin, self.y_begin,
+            _p(self.planes) if (self.force_int64 or not sp.fits32) else None,
+            None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch, self.W, self.H, self.y_origin, self.y_begin,
             self.y_end, sp.m, cfg.stride, len(sp.plan), sp.ring_n.ctypes.data, sp.ring_d.ctypes.data,
             sp.blob_dev.data_ptr(), sp.blob.ctypes.data, q[0], q[1], q[2], mask.data_ptr(), self.words, rc.data_ptr(),
             _p(self.stage_counts), ws.data_ptr(), ws.numel(), s), "screen_size")
@@ -222,7 +245,7 @@ class Engine:
         region = region and full
         self._ensure(len(tp.sizes), tp.max_m, capacity or self.default_capacity(tp), region)
         if build:
-            self.build_tables(img)
+            self.build_tables(img, int64=self.needs_int64(tp))
         if region:
             self.region.zero_()
             self.totals[1:].zero_()

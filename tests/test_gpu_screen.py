@@ -175,3 +175,41 @@ def test_errors_and_edge_cases(cuda):
     assert np.array_equal(a.region_mask, b.region_mask)
     # very fine quantizer: sparse (binary-search) membership path, still bit-exact
     compare_with_oracle(scene, tpl, {"quantizer": (1e-3, 1e-3, 1e-3)})
+
+
+def test_int64_and_32bit_planes_agree(cuda):
+    """The int64-plane screen (forced) and the 32-bit-plane screen give the same result."""
+    import workloads as WL
+    from paper_1707_05647_b200 import screen
+    from paper_1707_05647_b200.screening import get_engine
+
+    wl = WL.CONFIGS[0]
+    c = WL.make_cases(wl)[0]
+    kw = {"alpha": 0.6, "beta": 1.6, "ladder_ratio": 1.2, "quantizer": (6.0, 5.0, 7.0)}
+    a = screen(c.image, c.template, pcfg(kw))
+    eng = get_engine(c.image.shape[1], c.image.shape[0])
+    eng.force_int64 = True
+    try:
+        b = screen(c.image, c.template, pcfg(kw))
+    finally:
+        eng.force_int64 = False
+    assert a.candidates == b.candidates
+    for m in a.ladder:
+        assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
+    assert np.array_equal(a.region_packed(), b.region_packed())
+
+
+@pytest.mark.parametrize("side", [256, 258])
+def test_32bit_boundary_sizes(cuda, side):
+    """m = 256 (ring-0 n = 128: 32-bit planes) and m = 258 (n = 129: int64 planes) vs the oracle."""
+    from paper_1707_05647_b200 import _native
+    import workloads as WL
+
+    n0 = side // 2
+    plan = O.ring_plan(side, 3)
+    rn = np.array([p[0] for p in plan], np.int32)
+    rd = np.array([p[1] for p in plan], np.int32)
+    assert bool(_native.lib().ss_screen_fits32(len(plan), rn.ctypes.data, rd.ctypes.data)) == (n0 <= 128)
+    img = WL.make_image(640, 560, seed=41, sigma=4.0, noise=3.0)
+    case = WL.make_template(img, 43, side, (1.0, 1.0), std_threshold=10.0)
+    compare_with_oracle(img, case.template, {"alpha": 1.0, "beta": 1.0, "quantizer": (4.0, 4.0, 4.0)})

@@ -22,9 +22,12 @@ def device_planes(img, cuda):
 
     h, w = img.shape
     eng = Engine(w, h, cuda)
-    eng.build_tables(torch.from_numpy(np.ascontiguousarray(img)).to(cuda))
+    eng.build_tables(torch.from_numpy(np.ascontiguousarray(img)).to(cuda), int64=True)
     torch.cuda.synchronize()
     p = eng.planes.view(12, h + 1, eng.pitch).cpu().numpy()
+    # the 32-bit planes written by the same pass are the cells mod 2^32
+    p32 = eng.planes32.view(12, h + 1, eng.pitch).cpu().numpy().view(np.uint32)
+    assert np.array_equal(p32[:, :, : w + 1], p[:, :, : w + 1].astype(np.uint32)), "32-bit planes != int64 mod 2^32"
     return p[:, :, : w + 1]
 
 
@@ -155,9 +158,12 @@ def test_template_features_device_bitwise(cuda):
             d[4 + 2 * r], d[5 + 2 * r] = nr, dr
         rows.append(d)
     out = torch.empty((3, 16, 3), dtype=torch.float64, device=cuda)
+    # keep the device copies referenced until the kernel has run (a temporary's
+    # memory goes back to the caching allocator as soon as data_ptr() returns)
+    d_tpl = torch.from_numpy(tpl).to(cuda)
+    d_desc = torch.from_numpy(np.stack(rows)).to(cuda)
     _native.check(_native.lib().ss_template_features_device(
-        torch.from_numpy(tpl).to(cuda).data_ptr(), n, 3, torch.from_numpy(np.stack(rows)).to(cuda).data_ptr(), 36,
-        out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        d_tpl.data_ptr(), n, 3, d_desc.data_ptr(), 36, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     got = out.cpu().numpy()
     for i, k in enumerate((512, 530, 560)):
         want = template_ring_features(tpl, k, 512, plan)
