@@ -340,13 +340,18 @@ def run_ours(args):
 
     # ── roofline of the dominant kernel (K3 screen) ──
     peak, peak_src = measured_peak_hbm()
-    # algorithmic bytes: SURVEY.md 8(d)'s per-unit figure -- 96 B per
-    # position x scale (the 12 int64 planes read once per ladder size for
-    # ring 0) + 1/8 B of mask bit -- times the positions one step screens.
-    # The cascade-aware count (3 PLAIN planes for every ring-0 evaluation, the
-    # other 9 only for mean-projection passers) is reported beside it.
-    alg_bytes = 96.125 * positions
+    # algorithmic bytes: SURVEY.md 8(d)'s per-unit figure -- the 12 planes
+    # read once per ladder size for ring 0, + 1/8 B of mask bit per position
+    # -- with this layout's cell width: 12 x 4 B for sizes screened from the
+    # 32-bit planes, 12 x 8 B (SURVEY's 96 B) for sizes that need int64.
+    # SURVEY's literal 96 B figure and the cascade-aware count (3 PLAIN planes
+    # for every ring-0 evaluation, the other 9 only for mean-projection
+    # passers) are reported beside it.
+    per_size = eng.tested_per_size(tp)
+    alg_bytes = sum(cnt * (12 * (4 if sp.fits32 else 8) + 0.125) for sp, cnt in zip(tp.sizes, per_size))
     achieved = alg_bytes / (screen_ms / 1e3) / 1e9
+    cell_bytes = 12 * 8.0 * sum(cnt for sp, cnt in zip(tp.sizes, per_size) if not sp.fits32) / max(positions, 1) + \
+        12 * 4.0 * sum(cnt for sp, cnt in zip(tp.sizes, per_size) if sp.fits32) / max(positions, 1)
     cascade_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
     traffic, traffic_src = k3_traffic(wl.name)
     roofline = {
@@ -354,7 +359,10 @@ def run_ours(args):
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": peak_src,
-        "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": 96.125,
+        "alg_bytes_per_step": alg_bytes, "alg_bytes_per_position": alg_bytes / max(positions, 1),
+        "plane_bytes_per_position": cell_bytes,
+        "survey_96B_bytes_per_step": 96.125 * positions,
+        "survey_96B_equiv_GBps": 96.125 * positions / (screen_ms / 1e3) / 1e9,
         "cascade_alg_bytes_per_step": cascade_bytes,
         "cascade_achieved_GBps": cascade_bytes / (screen_ms / 1e3) / 1e9,
         "cascade": {"ring0_evals": stage[0], "ring0_mean_pass": stage[1], "ring0_pass": stage[2],

@@ -45,14 +45,23 @@ def _host_cc() -> list:
 
 
 def build(verbose: bool = False) -> str:
+    """Compile every source and link.  Experiment hooks (not used by the
+    product build): SS_EXTRA_NVCC adds flags (e.g. -DRINGS_GROUP=64),
+    SS_ONLY=a.cu,b.cu recompiles only those sources and reuses the others'
+    objects from build/."""
     nvcc = _nvcc()
+    extra_all = os.environ.get("SS_EXTRA_NVCC", "").split()
+    only = set(filter(None, os.environ.get("SS_ONLY", "").split(",")))
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
     for src, extra in SOURCES.items():
         obj = os.path.join(objdir, src + ".o")
-        cmd = [nvcc, *_host_cc(), *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        if only and src not in only and os.path.exists(obj):
+            objs.append(obj)
+            continue
+        cmd = [nvcc, *_host_cc(), *ARCH, *COMMON, *extra, *extra_all, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -253,8 +253,8 @@ constexpr int TY = WARPS;     // tile rows
 constexpr int CPW = 2;        // 32-centre chunks per warp per tile
 constexpr int TX = 32 * CPW;  // tile columns
 constexpr int NBOX = 8;
-constexpr int STAGES = 3;
 template <typename T> struct Geo {
+    static constexpr int STAGES = sizeof(T) == 4 ? 4 : 3;  // pipeline depth (u32: 35 KB, int64: 68 KB a stage)
     static constexpr int ALIGN = 16 / (int)sizeof(T);
     static constexpr int BW = TX + ALIGN;  // staged box width (elements)
     static constexpr int BOX_ELEMS = BW * TY;
@@ -283,13 +283,16 @@ __device__ __forceinline__ void tile_coords(const TileMap& t, long long idx, int
     tx = s0 + (int)(r - q * width);
 }
 
-// Copy the rings' membership bitmaps into shared memory (all threads).
-__device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbits, int r_lo, int r_hi) {
+// Copy the rings' membership bitmaps into shared memory (all threads);
+// m_only: just the mean-projection words (all stage 1 tests).
+__device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbits, int r_lo, int r_hi,
+                                              bool m_only = false) {
     const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
     for (int r = r_lo; r < r_hi; ++r) {
         const RingDev& R = a.ring[r];
         if (R.bm < 0) continue;
-        for (int i = threadIdx.x; i < R.bwords; i += blockDim.x)
+        const int words = m_only ? max(R.wm, 1) : R.bwords;
+        for (int i = threadIdx.x; i < words; i += blockDim.x)
             sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
     }
 }
@@ -313,13 +316,14 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
                                                                   const TileMap tm, int2* list0, unsigned* count0,
                                                                   unsigned* tile_ctr) {
     using G = Geo<T>;
+    constexpr int STAGES = G::STAGES;
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ int2 tile_xy[STAGES];  // (tx, ty) of the tile in each stage, written by the producer
     __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
-    stage_bitmaps(a, sbits, 0, 1);
+    stage_bitmaps(a, sbits, 0, 1, true);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -377,6 +381,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     const unsigned lt = (1u << lane) - 1u;
     int2* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
     int nbuf = 0;
+    unsigned res = 0;       // lane 0: base of the next reserved block of 32 list slots
+    bool have_res = false;  // warp-uniform
     unsigned long long n_int = 0, n_pass = 0;
     const bool unit_stride = a.stride == 1;
     for (int it = 0;; ++it) {
@@ -420,18 +426,26 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, y);
             nbuf += __popc(pb);
         }
+        // Full blocks of 32 go to list slots reserved one block ahead (the
+        // reservation's atomic round trip overlaps the next tiles); the
+        // warp's last reservation is padded with (-1, -1), which the rings
+        // kernel skips.
         while (nbuf >= 32) {
             __syncwarp();
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(count0, 32u);
-            base = __shfl_sync(FULL, base, 0);
+            if (!have_res && lane == 0) res = atomicAdd(count0, 32u);
+            const unsigned base = __shfl_sync(FULL, res, 0);
+            if (lane == 0) res = atomicAdd(count0, 32u);
+            have_res = true;
             list0[base + lane] = buf[nbuf - 32 + lane];
             nbuf -= 32;
             __syncwarp();
         }
     }
     __syncwarp();
-    if (nbuf > 0) {
+    if (have_res) {
+        const unsigned base = __shfl_sync(FULL, res, 0);
+        list0[base + lane] = lane < nbuf ? buf[lane] : make_int2(-1, -1);
+    } else if (nbuf > 0) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
         base = __shfl_sync(FULL, base, 0);
@@ -455,6 +469,12 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
 // mask and the per-row survivor counts.
 constexpr int RK_WARPS = 8;
 constexpr int QCAP = 64;
+#ifndef RINGS_GROUP
+#define RINGS_GROUP 128  // list entries a warp takes per grab: in flight = warps x RINGS_GROUP
+#endif
+#ifndef RINGS_COUNTERS
+#define RINGS_COUNTERS 8  // group counters (workspace words 33 ..)
+#endif
 
 template <typename T>
 __device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
@@ -488,11 +508,15 @@ __global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArg
     // level-0 entries come in groups of RG from a global counter, in list
     // (tile) order; the atomic's result stays in lane 0 until needed and the
     // next entry is loaded one batch ahead.
-    constexpr unsigned RG = 128;
+    // NCTR counters hand out interleaved groups (counter j: groups j, j+NCTR,
+    // ...) so no single address serialises the grabs.
+    constexpr unsigned RG = RINGS_GROUP, NCTR = RINGS_COUNTERS;
+    const unsigned j = (blockIdx.x * RK_WARPS + warp) % NCTR;
+    unsigned* ctr = group_ctr + j;
     unsigned g_raw = 0;
-    if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
-    unsigned cur = __shfl_sync(FULL, g_raw, 0) * RG, k = 0;
-    if (lane == 0) g_raw = atomicAdd(group_ctr, 1u);
+    if (lane == 0) g_raw = atomicAdd(ctr, 1u);
+    unsigned cur = (__shfl_sync(FULL, g_raw, 0) * NCTR + j) * RG, k = 0;
+    if (lane == 0) g_raw = atomicAdd(ctr, 1u);
     int2 next = (cur + lane < count) ? in[cur + lane] : make_int2(-1, -1);
     bool have_input = cur < count;
     for (;;) {
@@ -506,8 +530,8 @@ __global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArg
             e = next;
             if (++k == RG / 32) {
                 k = 0;
-                cur = __shfl_sync(FULL, g_raw, 0) * RG;
-                if (lane == 0 && cur < count) g_raw = atomicAdd(group_ctr, 1u);
+                cur = (__shfl_sync(FULL, g_raw, 0) * NCTR + j) * RG;
+                if (lane == 0 && cur < count) g_raw = atomicAdd(ctr, 1u);
             }
             const unsigned slot = cur + 32 * k;
             have_input = slot < count;
@@ -591,8 +615,12 @@ __global__ void selftest_div_kernel(unsigned long long n, unsigned long long see
 
 }  // namespace
 
+// list slots beyond one per centre: padding of the stage-1 warps' last
+// reserved blocks (<= 32 per consumer warp in flight)
+constexpr size_t LIST_SLACK = (size_t)1 << 20;
+
 size_t screen_workspace_bytes(int64_t W, int64_t rows) {
-    return 256 + (size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) * sizeof(int2);
+    return 256 + ((size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) + LIST_SLACK) * sizeof(int2);
 }
 
 // 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
@@ -780,7 +808,7 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
         set_error("screen workspace too small: %zu < %zu", ws_bytes, need);
         return SS_EINVAL;
     }
-    // workspace: [counters: list count [0], tile counter [32], list group counter [33];
+    // workspace: [counters: list count [0], tile counter [32], list group counters [33, 33 + 8);
     //             256 B] [ring-0 candidate list: W x rows int2]
     unsigned* counts = static_cast<unsigned*>(d_ws);
     int2* list_a = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + 256);
@@ -810,19 +838,22 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     // flight) x (strip + m) x 3 planes of PLAIN SAT/E/O -- fits the budget keeps
     // both; narrower strips re-read (strip + m) / strip of the columns.
     auto s1 = use32 ? stage1_kernel<unsigned> : stage1_kernel<long long>;
-    const size_t s1_smem = (size_t)STAGES * (use32 ? Geo<unsigned>::STAGE_BYTES : Geo<long long>::STAGE_BYTES) +
-                           (size_t)std::max(a.ring[0].bwords, 1) * 4;
+    const size_t s1_smem = use32 ? (size_t)Geo<unsigned>::STAGES * Geo<unsigned>::STAGE_BYTES
+                                 : (size_t)Geo<long long>::STAGES * Geo<long long>::STAGE_BYTES;
+    const size_t s1_smem_all = s1_smem + (size_t)std::max(a.ring[0].wm, 1) * 4;
     int s1_per_sm = 1;
     cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem_all);
     s1_per_sm = std::max(s1_per_sm, 1);
     {
-        const int64_t budget = 40ll << 20;
-        const int64_t in_flight = (int64_t)sms * s1_per_sm * STAGES;  // tiles being staged or consumed
+        int64_t budget = 40ll << 20, planes = 3;
+        if (const char* e = getenv("SS_STRIP_BUDGET_MB")) budget = (int64_t)atoi(e) << 20;  // experiment hooks
+        if (const char* e = getenv("SS_STRIP_PLANES")) planes = atoi(e);
+        const int64_t in_flight = (int64_t)sms * s1_per_sm * (use32 ? Geo<unsigned>::STAGES : Geo<long long>::STAGES);
         tm.strip = 1;
         for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
             const int64_t rows = (in_flight + strip - 1) / strip * TY;
-            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * 3 * eb;
+            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * planes * eb;
             if (ws <= budget) {
                 tm.strip = strip;
                 break;
@@ -833,7 +864,7 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
     {
         const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm);
-        s1<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, list_a, counts + 0,
+        s1<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem_all, s>>>(a, maps, tm, list_a, counts + 0,
                                                                                  counts + 32);
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;

@@ -23,7 +23,23 @@ from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, p
 from .featureset import FeatureSet, build_feature_set, build_feature_sets_device, keyset_blob
 
 
-N_STREAMS = 1  # concurrent ladder sizes (measured: >1 contends for L2 and is slower)
+import os
+
+# Ladder sizes run on up to N_STREAMS side streams (fork/join around K3):
+# for images whose 32-bit tables fit in a few GB, three sizes in flight fill
+# the launch tails and overlap one size's compute-bound stage 1 with
+# another's memory-bound rings (measured: config 1 -19%, config 2 -12%);
+# for larger images two sizes' working sets thrash L2 (config 4 +27%), so
+# they run one at a time.  SS_STREAMS overrides (experiments).
+N_STREAMS = 3
+STREAMS_MAX_TABLE_BYTES = 4 << 30
+
+
+def streams_for(table_bytes: int) -> int:
+    env = os.environ.get("SS_STREAMS")
+    if env:
+        return max(1, int(env))
+    return N_STREAMS if table_bytes <= STREAMS_MAX_TABLE_BYTES else 1
 
 
 def _p(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -115,7 +131,7 @@ class Engine:
         self.compact_ws = None
         # ladder sizes are independent: they run on N_STREAMS side streams
         # (fork/join around the K3 region), each with its own screen workspace
-        self.n_streams = N_STREAMS
+        self.n_streams = streams_for(tb32)
         self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n_streams)]
         ws = int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1)))
         self.screen_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device) for _ in range(self.n_streams)]
@@ -159,9 +175,13 @@ class Engine:
 
     def tested(self, tp: TemplatePlan) -> int:
         """patches_tested of the decided rows (screening.py:446, 513)."""
-        total = 0
+        return sum(self.tested_per_size(tp))
+
+    def tested_per_size(self, tp: TemplatePlan) -> List[int]:
+        out = []
         for sp in tp.sizes:
             if sp.m < MIN_PATCH_SIDE:
+                out.append(0)
                 continue
             lo, hi = patch_center_margins(sp.m)
             nx = grid_count(self.W, lo, hi, tp.config.stride)
@@ -171,8 +191,8 @@ class Engine:
                 s = tp.config.stride
                 first = ((ylo + s - 1) // s) * s
                 ny = 0 if first > yhi else (yhi - first) // s + 1
-            total += nx * ny
-        return total
+            out.append(nx * ny)
+        return out
 
     # ── the hot path ───────────────────────────────────────────────────────
     def needs_int64(self, tp: TemplatePlan) -> bool:
