@@ -386,7 +386,7 @@ def run_ours(args):
         n_inst = sum(math.ceil(m * wl.ladder_ratio) - m + 1 for m in tp.ladder if m >= 8)
         h2d = (case.image.nbytes + case.template.nbytes + n_inst * 36 * 4
                + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None))
-        d2h = len(cand) * 8 + 16 + len(tp.sizes) * 8 + n_inst * 16 * 3 * 8
+        d2h = len(cand) * 12 + 16 + n_inst * 16 * 3 * 8
         e2e_t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

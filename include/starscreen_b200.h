@@ -165,13 +165,16 @@ int ss_compact(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int6
  * d_masks holds n_sizes masks size_stride_words apart (rows y_begin..y_end),
  * d_row_counts n_sizes x rows counts; sizes with m < MIN_PATCH_SIDE are
  * skipped.  d_size_counts (n_sizes u64) and *d_total receive the counts;
- * survivors are written in ladder order, then row-major.
+ * survivors are written in ladder order, then row-major, as int32 rows of
+ * xy_columns = 2 (cx, cy) or 3 (cx, cy, m) -- the candidates list
+ * (screening.py:280-283) in one buffer.
  */
 size_t ss_compact_ladder_workspace_bytes(int64_t rows, int32_t n_sizes);
 int ss_compact_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
                       int64_t H, int64_t y_begin, int64_t y_end, int32_t n_sizes, const int32_t* h_m, int32_t stride,
-                      const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
-                      unsigned long long* d_size_counts, void* d_workspace, size_t workspace_bytes, void* stream);
+                      const uint32_t* d_row_counts, int32_t* d_xy, int32_t xy_columns, int64_t capacity,
+                      unsigned long long* d_total, unsigned long long* d_size_counts, void* d_workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* ── kept region (screening.py:316-330 _footprint_union) ─────────────── */
 /* Workspace for ss_region_accumulate with sizes up to m_max. */

@@ -49,7 +49,7 @@ _SIGS = {
                                   c_p, c_sz, c_p]),
     "ss_compact_ladder_workspace_bytes": (c_sz, [c_i64, c_i32]),
     "ss_compact_ladder": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_p, c_i32, c_p, c_p,
-                                         c_i64, c_p, c_p, c_p, c_sz, c_p]),
+                                         c_i32, c_i64, c_p, c_p, c_p, c_sz, c_p]),
     "ss_region_ladder_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
     "ss_region_ladder": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i32, c_p, c_i32, c_p, c_p, c_sz, c_p]),
     "ss_region_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(1024) scan_sizes_kernel(const unsigned* counts
 __global__ void write_xy_all_kernel(const unsigned* masks, long long mask_pitch, long long size_stride, int W, int H,
                                     int y_begin, long long rows, int stride, const Ladder lad, const unsigned* counts,
                                     const unsigned long long* row_off, const unsigned long long* size_counts, int* xy,
-                                    long long capacity, unsigned long long* total) {
+                                    int cols, long long capacity, unsigned long long* total) {
     const int k = blockIdx.y;
     if (blockIdx.x == 0 && k == 0 && threadIdx.x == 0) {
         unsigned long long s = 0;
@@ -306,8 +306,10 @@ __global__ void write_xy_all_kernel(const unsigned* masks, long long mask_pitch,
             const int b = __ffs(bits) - 1;
             bits &= bits - 1;
             if (p < (unsigned long long)capacity) {
-                xy[2 * p] = (int)(w * 32 + b);
-                xy[2 * p + 1] = y;
+                int* o = xy + (long long)cols * (long long)p;
+                o[0] = (int)(w * 32 + b);
+                o[1] = y;
+                if (cols == 3) o[2] = m;
             }
             ++p;
         }
@@ -477,12 +479,14 @@ size_t compact_ladder_workspace_bytes(int64_t rows, int32_t L) {
 
 int compact_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H,
                    int64_t y_begin, int64_t y_end, int32_t L, const int32_t* h_m, int32_t stride,
-                   const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
-                   unsigned long long* d_size_counts, void* d_ws, size_t ws_bytes, void* stream) {
+                   const uint32_t* d_row_counts, int32_t* d_xy, int32_t cols, int64_t capacity,
+                   unsigned long long* d_total, unsigned long long* d_size_counts, void* d_ws, size_t ws_bytes,
+                   void* stream) {
     Ladder lad;
     if (int e = fill_ladder(lad, L, h_m)) return e;
     const int64_t rows = y_end - y_begin;
     if (rows < 0 || W < 1 || stride < 1) { set_error("bad compact arguments"); return SS_EINVAL; }
+    if (cols != 2 && cols != 3) { set_error("xy_columns must be 2 or 3"); return SS_EINVAL; }
     cudaStream_t s = as_stream(stream);
     if (rows == 0) {
         cudaMemsetAsync(d_size_counts, 0, sizeof(unsigned long long) * L, s);
@@ -499,7 +503,7 @@ int compact_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_str
     if (int e = check_launch("scan_sizes_kernel")) return e;
     write_xy_all_kernel<<<dim3((unsigned)((rows * 32 + 255) / 256), (unsigned)L), 256, 0, s>>>(
         d_masks, mask_pitch, size_stride, (int)W, (int)H, (int)y_begin, rows, stride, lad, d_row_counts, row_off,
-        d_size_counts, d_xy, capacity, d_total);
+        d_size_counts, d_xy, cols, capacity, d_total);
     note_launch();
     return check_launch("write_xy_all_kernel");
 }
@@ -577,11 +581,12 @@ size_t ss_compact_ladder_workspace_bytes(int64_t rows, int32_t n_sizes) {
 }
 int ss_compact_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
                       int64_t H, int64_t y_begin, int64_t y_end, int32_t n_sizes, const int32_t* h_m, int32_t stride,
-                      const uint32_t* d_row_counts, int32_t* d_xy, int64_t capacity, unsigned long long* d_total,
-                      unsigned long long* d_size_counts, void* d_workspace, size_t workspace_bytes, void* stream) {
+                      const uint32_t* d_row_counts, int32_t* d_xy, int32_t xy_columns, int64_t capacity,
+                      unsigned long long* d_total, unsigned long long* d_size_counts, void* d_workspace,
+                      size_t workspace_bytes, void* stream) {
     return ss::compact_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, y_begin, y_end, n_sizes, h_m, stride,
-                              d_row_counts, d_xy, capacity, d_total, d_size_counts, d_workspace, workspace_bytes,
-                              stream);
+                              d_row_counts, d_xy, xy_columns, capacity, d_total, d_size_counts, d_workspace,
+                              workspace_bytes, stream);
 }
 size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes) {
     return ss::region_ladder_workspace_bytes(W, H, n_sizes);

@@ -165,7 +165,7 @@ class Engine:
                                          dtype=torch.uint8, device=self.device)
         if self.xy is None or self.capacity < capacity:
             self.capacity = max(capacity, 1)
-            self.xy = torch.empty((self.capacity, 2), dtype=torch.int32, device=self.device)
+            self.xy = torch.empty((self.capacity, 3), dtype=torch.int32, device=self.device)
 
     def default_capacity(self, tp: TemplatePlan) -> int:
         # Start at 2% of the decided positions (measured survivor rates are
@@ -244,7 +244,7 @@ class Engine:
         ms = self._ladder_array(tp)
         _native.check(self.L.ss_compact_ladder(
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, self.y_begin, self.y_end,
-            len(ms), ms.ctypes.data, tp.config.stride, self.row_counts.data_ptr(), self.xy.data_ptr(), self.capacity,
+            len(ms), ms.ctypes.data, tp.config.stride, self.row_counts.data_ptr(), self.xy.data_ptr(), 3, self.capacity,
             self.totals.data_ptr(), self.size_counts.data_ptr(), self.compact_ws.data_ptr(), self.compact_ws.numel(),
             _stream_handle()), "compact")
 
@@ -294,5 +294,5 @@ class Engine:
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:
         """Grow the survivor buffer and redo K4 only (after an overflow)."""
         self.capacity = capacity
-        self.xy = torch.empty((capacity, 2), dtype=torch.int32, device=self.device)
+        self.xy = torch.empty((capacity, 3), dtype=torch.int32, device=self.device)
         self.compact_all(tp)

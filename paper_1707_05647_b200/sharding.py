@@ -159,7 +159,7 @@ def screen_band_device(image: np.ndarray, tp, band: Band, device) -> BandResult:
     if kept > eng.capacity:
         eng.recompact(tp, kept)
     counts = eng.size_counts[: len(tp.sizes)].cpu().numpy().astype(np.int64)
-    xy = eng.xy[:kept].cpu().numpy()
+    xy = eng.xy[:kept, :2].cpu().numpy()
     masks = eng.masks[: len(tp.sizes)].cpu().numpy().view(np.uint32)
     return BandResult(band, counts, xy, masks, eng.tested(tp))
 
