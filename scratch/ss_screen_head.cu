@@ -51,7 +51,6 @@ struct RingDev {
     int ea, ed;          // E corners: [+d+1][+1], [-d][+1]
     int ob, oc;          // O corners: [0][-d], [0][+d+1]
     double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
-    float fa, fb;  // RN32(1 / (2 cnt qm)) of the square / diamond: fp32 estimate of the mean cell
     int cm_lo, cm_n, cs_lo, cs_n, cg_lo, cg_n;
     int bm;        // shared-memory word offset of [m | ms | full] bits; -1: binary search
     int wm, wms;   // words of the m and ms bitmaps
@@ -64,7 +63,6 @@ struct ScreenArgs {
     const void* planes;   // 12 planes of int64, or of uint32 (cells mod 2^32)
     long long pitch, ps;  // row pitch, plane stride (elements)
     int W, H, y_origin, y_begin, y_end, stride, lo, hi, n_rings;
-    int sums_in_list;  // ring-0 PLAIN sums fit 32 bits: list entries carry them (rings skip 8 gathers)
     double qm, qs, qg, rqm, rqs, rqg;
     const long long* blob;
     unsigned* mask;
@@ -162,53 +160,21 @@ __device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long
     return base + (long long)(int)(v - (unsigned)base);
 }
 
-// RN conversion of an exact non-negative region sum to fp32 (rel. error <= 2^-24)
-__device__ __forceinline__ float to_f32(long long v) { return __ll2float_rn(v); }
-__device__ __forceinline__ float to_f32(unsigned v) { return __uint2float_rn(v); }
-
-// Mean cell floor(t), t = ((s1q/cq + s1d/cd) * 0.5) / qm + 0.5 (features.py:325, 349, 365;
-// screening.py:86-87), from exact non-negative PLAIN sums.  The fp32 estimate tf is
-// within 4e-7 (tf + 1) of the fp64 t (six roundings of 2^-24 on non-negative terms), so
-// when [tf - dl, tf + dl] holds no integer, floor(t) = floor(tf) exactly; only centres
-// whose mean lies within ~4e-6 of a cell boundary take the fp64 op sequence.
-template <typename S>
-__device__ __forceinline__ int mean_cell(const ScreenArgs& a, const RingDev& R, S s1q, S s1d) {
-    const float tf = fmaf(to_f32(s1q), R.fa, fmaf(to_f32(s1d), R.fb, 0.5f));
-    const float dl = fmaf(tf, 4e-6f, 4e-6f);
-    int cm = (int)floorf(tf - dl);
-    if (cm != (int)floorf(tf + dl)) {
-        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
-        const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);  // features.py:349
-        cm = quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm);
-    }
-    return cm;
-}
-
-#ifndef RINGS_FAST_CM
-#define RINGS_FAST_CM 0  // the rings need the fp64 means anyway; the exact cell is a short chain on top
-#endif
-#ifndef STAGE1_FAST_CM
-#define STAGE1_FAST_CM 1
-#endif
-
 struct Stage1 {
     long long s1q, s1d;
     double mq, md;
     int cm;
 };
 
-// Stage 1 of ring R from its exact PLAIN sums: means and mean cell.
-__device__ __forceinline__ Stage1 stage1_from(const ScreenArgs& a, const RingDev& R, long long s1q, long long s1d) {
+// Stage 1 (mean cell) of ring R from its PLAIN corners.
+template <typename T>
+__device__ __forceinline__ Stage1 stage1_of(const ScreenArgs& a, const RingDev& R, const Corners<T>& c) {
     Stage1 s;
-    s.s1q = s1q;
-    s.s1d = s1d;
-    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
-    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);  // features.py:349
-#if RINGS_FAST_CM
-    s.cm = mean_cell(a, R, s1q, s1d);  // features.py:365
-#else
+    s.s1q = unsigned_sum(sq_of(c));
+    s.s1d = unsigned_sum(di_of(c));
+    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);                   // features.py:325
+    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);                   // features.py:349
     s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
-#endif
     return s;
 }
 
@@ -287,27 +253,6 @@ constexpr int TY = WARPS;     // tile rows
 constexpr int CPW = 2;        // 32-centre chunks per warp per tile
 constexpr int TX = 32 * CPW;  // tile columns
 constexpr int NBOX = 8;
-constexpr int TILE_POS = TX * TY;  // centres per tile
-// Candidate lists, two modes picked per size on the host (see screen_size):
-// * small sizes: one list, entries (x, y);
-// * large sizes (>= LARGE_TILES tiles): `parts` sub-lists -- stage-1 CTA b
-//   serves partition b % parts (tiles p, p + parts, ...) and appends to its
-//   own sub-list and counter, so no single counter serialises a long grid --
-//   and entries (x, y, s1q, s1d) that carry the ring-0 PLAIN sums (the rings
-//   kernel skips those 8 gathers).
-// Either way the lists follow the strip-major tile order.
-constexpr int MAX_PARTS = 8;
-constexpr unsigned GROUP_CTRS = 8;  // rings group counters per partition
-constexpr int CTR_STRIDE = 32;  // words between counters (one 128-B line each)
-template <typename E> __device__ __forceinline__ E make_entry(int x, int y, unsigned sq, unsigned sd);
-template <> __device__ __forceinline__ int4 make_entry<int4>(int x, int y, unsigned sq, unsigned sd) {
-    return make_int4(x, y, (int)sq, (int)sd);
-}
-template <> __device__ __forceinline__ int2 make_entry<int2>(int x, int y, unsigned, unsigned) {
-    return make_int2(x, y);
-}
-__device__ __forceinline__ int4 widen(int4 e) { return e; }
-__device__ __forceinline__ int4 widen(int2 e) { return make_int4(e.x, e.y, 0, 0); }
 template <typename T> struct Geo {
     static constexpr int STAGES = sizeof(T) == 4 ? 4 : 3;  // pipeline depth (u32: 35 KB, int64: 68 KB a stage)
     static constexpr int ALIGN = 16 / (int)sizeof(T);
@@ -352,13 +297,24 @@ __device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbi
     }
 }
 
+// Append `flag` lanes' (x, y) to a device list with one atomic per warp.
+__device__ __forceinline__ void append(bool flag, int x, int y, int2* list, unsigned* count) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned b = __ballot_sync(FULL, flag);
+    if (!b) return;
+    unsigned base = 0;
+    if (lane == (unsigned)(__ffs(b) - 1)) base = atomicAdd(count, (unsigned)__popc(b));
+    base = __shfl_sync(FULL, base, __ffs(b) - 1);
+    if (flag) list[base + __popc(b & ((1u << lane) - 1u))] = make_int2(x, y);
+}
+
 // K3a: every grid centre of the decided rows -- border keeps into the mask,
 // ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
 // passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
-template <typename T, typename Entry>
+template <typename T>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
-                                                                  const TileMap tm, int parts, Entry* list_base, long long part_cap,
-                                                                  unsigned* list_ctr, unsigned* tile_ctr_base) {
+                                                                  const TileMap tm, int2* list0, unsigned* count0,
+                                                                  unsigned* tile_ctr) {
     using G = Geo<T>;
     constexpr int STAGES = G::STAGES;
     extern __shared__ __align__(128) unsigned char dsmem[];
@@ -366,7 +322,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ int2 tile_xy[STAGES];  // (tx, ty) of the tile in each stage, written by the producer
-    __shared__ Entry cand_buf[WARPS][32 * (CPW + 1)];
+    __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
     stage_bitmaps(a, sbits, 0, 1, true);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -378,7 +334,6 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const RingDev& R0 = a.ring[0];
-    const int part = (int)(blockIdx.x % parts);
 
     if (warp == WARPS) {
         // ── producer: one lane streams the tiles' corner boxes ──────────────
@@ -386,11 +341,10 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             // Tiles are handed out by a global counter so every CTA works near
             // the same point of the strip-major order: the L2 working set is
             // the rows in flight, not the spread of CTAs that drift apart.
-            unsigned* tile_ctr = tile_ctr_base + part * CTR_STRIDE;
             unsigned t_next = atomicAdd(tile_ctr, 1u);
             for (int it = 0;; ++it) {
                 const int s = it % STAGES;
-                const long long t = (long long)t_next * parts + part;
+                const long long t = t_next;
                 if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);  // one tile ahead: hides the atomic
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 if (t >= tm.n_tiles) {
@@ -425,9 +379,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     // offsets of the corner column inside each box (x0 is a multiple of ALIGN)
     const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d), po1 = G::rem(R0.d + 1);
     const unsigned lt = (1u << lane) - 1u;
-    Entry* list0 = list_base + part * part_cap;
-    unsigned* count0 = list_ctr + part * CTR_STRIDE;
-    Entry* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
+    int2* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
     int nbuf = 0;
     unsigned res = 0;       // lane 0: base of the next reserved block of 32 list slots
     bool have_res = false;  // warp-uniform
@@ -441,13 +393,13 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
         const int tx = txy.x, ty = txy.y;
         const int y = a.y_begin + ty * TY + warp;
         const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
-        T s1q[CPW], s1d[CPW];  // exact PLAIN region sums (u32 planes: sums < 2^32, see weighted_sum)
+        long long s1q[CPW], s1d[CPW];
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
             const T* b = box + 32 * c;
             constexpr int E = G::BOX_ELEMS;
-            s1q[c] = (T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]);
-            s1d[c] = (T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]);
+            s1q[c] = unsigned_sum((T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]));
+            s1d[c] = unsigned_sum((T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -463,24 +415,20 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             const int word = tx * CPW + c;
             if (lane == 0 && word * 32 < a.W) a.mask[(long long)(y - a.y_begin) * a.mask_pitch + word] = border;
             bool pass = false;
-#if STAGE1_FAST_CM
-            if (interior) pass = member_m(a, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
-#else
             if (interior) {
                 const double mq = div_rn((double)s1q[c], R0.cnt_sq, R0.rcp_sq);  // features.py:325
                 const double md = div_rn((double)s1d[c], R0.cnt_di, R0.rcp_di);  // features.py:349
                 pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm));
             }
-#endif
             const unsigned pb = __ballot_sync(FULL, pass);
             n_int += __popc(__ballot_sync(FULL, interior));
             n_pass += __popc(pb);
-            if (pass) buf[nbuf + __popc(pb & lt)] = make_entry<Entry>(x, y, (unsigned)s1q[c], (unsigned)s1d[c]);
+            if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, y);
             nbuf += __popc(pb);
         }
         // Full blocks of 32 go to list slots reserved one block ahead (the
         // reservation's atomic round trip overlaps the next tiles); the
-        // warp's last reservation is padded with x = -1, which the rings
+        // warp's last reservation is padded with (-1, -1), which the rings
         // kernel skips.
         while (nbuf >= 32) {
             __syncwarp();
@@ -496,7 +444,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     __syncwarp();
     if (have_res) {
         const unsigned base = __shfl_sync(FULL, res, 0);
-        list0[base + lane] = lane < nbuf ? buf[lane] : make_entry<Entry>(-1, -1, 0, 0);
+        list0[base + lane] = lane < nbuf ? buf[lane] : make_int2(-1, -1);
     } else if (nbuf > 0) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
@@ -521,45 +469,31 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
 // mask and the per-row survivor counts.
 constexpr int RK_WARPS = 8;
 constexpr int QCAP = 64;
-#ifndef RINGS_MINB
-#define RINGS_MINB 3  // resident CTAs per SM the register budget is sized for
-#endif
-
-// Ring `level` at centre e = (x, y, s1q, s1d): level 0 entries come from the
-// stage-1 list and passed the mean test (with a.sums_in_list they carry the
-// ring-0 PLAIN sums, so those 8 gathers are skipped); deeper levels start
-// with the mean test.
-template <typename T, bool SUMS>
-__device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
-                                          int4 e) {
-    const int cy = e.y - a.y_origin;
-    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + e.x;
-    Corners<T> c2, cxk, cyk;
-    long long s1q, s1d;
-    if (SUMS && level == 0 && a.sums_in_list) {
-        s1q = (unsigned)e.z;
-        s1d = (unsigned)e.w;
-    } else {
-        Corners<T> c0;
-        load_corners(a, R, pc, 0, c0);
-        s1q = unsigned_sum(sq_of(c0));
-        s1d = unsigned_sum(di_of(c0));
-    }
-    load_corners(a, R, pc, 3, c2);
-    load_corners(a, R, pc, 1, cxk);
-    load_corners(a, R, pc, 2, cyk);
-    const Stage1 s = stage1_from(a, R, s1q, s1d);
-    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk);
-}
-
 #ifndef RINGS_GROUP
 #define RINGS_GROUP 128  // list entries a warp takes per grab: in flight = warps x RINGS_GROUP
 #endif
+#ifndef RINGS_COUNTERS
+#define RINGS_COUNTERS 8  // group counters (workspace words 33 ..)
+#endif
 
-template <typename T, typename Entry>
-__global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const ScreenArgs a, int parts, const Entry* list_base,
-                                                                 long long part_cap, const unsigned* list_ctr,
-                                                                 unsigned* group_ctr, int bitmap_words) {
+template <typename T>
+__device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
+                                          int2 e) {
+    const int cy = e.y - a.y_origin;
+    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + e.x;
+    Corners<T> c0, c2, cxk, cyk;
+    load_corners(a, R, pc, 0, c0);
+    load_corners(a, R, pc, 3, c2);
+    load_corners(a, R, pc, 1, cxk);
+    load_corners(a, R, pc, 2, cyk);
+    const Stage1 s = stage1_of(a, R, c0);
+    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RK_WARPS * 32, 3) rings_kernel(const ScreenArgs a, const int2* in,
+                                                                 const unsigned* in_count, unsigned* group_ctr,
+                                                                 int bitmap_words) {
     extern __shared__ unsigned sbits[];  // [all rings' bitmaps][queues: warp x level x QCAP int2]
     __shared__ int qcnt[RK_WARPS][SS_MAX_RINGS];
     stage_bitmaps(a, sbits, 0, a.n_rings);
@@ -568,66 +502,40 @@ __global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const 
     int2* queues = reinterpret_cast<int2*>(sbits + ((bitmap_words + 1) & ~1)) + (size_t)warp * levels * QCAP;
     if (lane < SS_MAX_RINGS) qcnt[warp][lane] = 0;
     __syncthreads();
+    const unsigned count = *in_count;
     const unsigned lt = (1u << lane) - 1u;
     unsigned long long n_pass0 = 0, n_surv = 0;
-    // Level-0 entries come in groups of RG list entries, in list (tile) order:
-    // warp w starts on partition w % parts and moves on to the next
-    // partition when its own is used up.  Each partition's groups are handed
-    // out by GROUP_CTRS interleaved counters (counter c: groups c, c +
-    // GROUP_CTRS, ...) so no single address serialises the grabs.  The next
-    // group's number waits in lane 0 (one atomic ahead) and the next batch is
-    // loaded one batch ahead.
-    constexpr unsigned RG = RINGS_GROUP;
-    const unsigned wid = blockIdx.x * RK_WARPS + warp;
-    int q = (int)(wid % parts), visited = 1;
-    const unsigned gc = (wid / parts) % GROUP_CTRS;
-    unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
-    const Entry* in = list_base + q * part_cap;
+    // level-0 entries come in groups of RG from a global counter, in list
+    // (tile) order; the atomic's result stays in lane 0 until needed and the
+    // next entry is loaded one batch ahead.
+    // NCTR counters hand out interleaved groups (counter j: groups j, j+NCTR,
+    // ...) so no single address serialises the grabs.
+    constexpr unsigned RG = RINGS_GROUP, NCTR = RINGS_COUNTERS;
+    const unsigned j = (blockIdx.x * RK_WARPS + warp) % NCTR;
+    unsigned* ctr = group_ctr + j;
     unsigned g_raw = 0;
-    if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
-    unsigned cur = 0, k = 0;
-    bool have_input = true;
-    // next group of the current partition (a group number at or past the end
-    // means the partition is used up: later ones are too, so the prefetched
-    // number can be dropped)
-    auto grab = [&]() {
-        for (;;) {
-            cur = (__shfl_sync(FULL, g_raw, 0) * GROUP_CTRS + gc) * RG;
-            if (cur < cnt_q) {
-                if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
-                return;
-            }
-            if (visited == parts) {
-                have_input = false;
-                return;
-            }
-            ++visited;
-            q = q + 1 == parts ? 0 : q + 1;
-            cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
-            in = list_base + q * part_cap;
-            if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
-        }
-    };
-    auto fetch = [&]() -> int4 {  // this lane's entry of batch k of the current group
-        const unsigned slot = cur + 32 * k + lane;
-        return (have_input && slot < cnt_q) ? widen(in[slot]) : make_int4(-1, -1, 0, 0);
-    };
-    grab();
-    int4 next = fetch();
+    if (lane == 0) g_raw = atomicAdd(ctr, 1u);
+    unsigned cur = (__shfl_sync(FULL, g_raw, 0) * NCTR + j) * RG, k = 0;
+    if (lane == 0) g_raw = atomicAdd(ctr, 1u);
+    int2 next = (cur + lane < count) ? in[cur + lane] : make_int2(-1, -1);
+    bool have_input = cur < count;
     for (;;) {
         // pick the batch: deepest queue holding >= 32, else the list, else drain
         int level = -1;
         for (int l = levels - 1; l >= 1; --l)
             if (qcnt[warp][l] >= 32) { level = l; break; }
-        int4 e;
+        int2 e;
         if (level < 0 && have_input) {
             level = 0;
             e = next;
-            if (++k == RG / 32 || cur + 32 * k >= cnt_q) {
+            if (++k == RG / 32) {
                 k = 0;
-                grab();
+                cur = (__shfl_sync(FULL, g_raw, 0) * NCTR + j) * RG;
+                if (lane == 0 && cur < count) g_raw = atomicAdd(ctr, 1u);
             }
-            next = fetch();
+            const unsigned slot = cur + 32 * k;
+            have_input = slot < count;
+            next = (have_input && slot + lane < count) ? in[slot + lane] : make_int2(-1, -1);
         } else {
             if (level < 0) {
                 for (int l = levels - 1; l >= 1; --l)
@@ -636,13 +544,12 @@ __global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const 
             }
             const int c = qcnt[warp][level], take = min(c, 32);
             const int2* q = queues + level * QCAP;
-            const int2 qe = ((int)lane < take) ? q[c - take + lane] : make_int2(-1, -1);
-            e = make_int4(qe.x, qe.y, 0, 0);
+            e = ((int)lane < take) ? q[c - take + lane] : make_int2(-1, -1);
             __syncwarp();
             if (lane == 0) qcnt[warp][level] = c - take;
             __syncwarp();
         }
-        const bool pass = e.x >= 0 && eval_ring<T, sizeof(Entry) == sizeof(int4)>(a, a.ring[level], sbits, level, e);
+        const bool pass = e.x >= 0 && eval_ring<T>(a, a.ring[level], sbits, level, e);
         const unsigned pb = __ballot_sync(FULL, pass);
         if (level == 0) n_pass0 += __popc(pb);
         if (level + 1 == levels) {
@@ -654,7 +561,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const 
             }
         } else if (pb) {
             const int c = qcnt[warp][level + 1];
-            if (pass) queues[(level + 1) * QCAP + c + __popc(pb & lt)] = make_int2(e.x, e.y);
+            if (pass) queues[(level + 1) * QCAP + c + __popc(pb & lt)] = e;
             __syncwarp();
             if (lane == 0) qcnt[warp][level + 1] = c + __popc(pb);
             __syncwarp();
@@ -708,32 +615,12 @@ __global__ void selftest_div_kernel(unsigned long long n, unsigned long long see
 
 }  // namespace
 
-// Workspace: [counters: 3 x MAX_PARTS lines] [`parts` candidate sub-lists of
-// part_cap entries].  A partition serves ceil(tiles / parts) tiles (<=
-// TILE_POS passers each) plus the padding of its warps' last reserved blocks
-// (< 32 per stage-1 consumer warp; at most 2 CTAs per SM).
-constexpr size_t CTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
-constexpr long long LARGE_TILES = 32768;  // sizes with at least this many tiles use the large-list mode
-static long long n_tiles_of(int64_t W, int64_t rows) {
-    return ((std::max<int64_t>(W, 1) + TX - 1) / TX) * ((std::max<int64_t>(rows, 1) + TY - 1) / TY);
-}
-static long long part_cap_of(int64_t W, int64_t rows, int sms, int parts) {
-    const long long ctas = (2LL * sms + parts - 1) / parts;
-    return (n_tiles_of(W, rows) + parts - 1) / parts * TILE_POS + ctas * WARPS * 32;
-}
-static size_t list_bytes(int64_t W, int64_t rows, int sms, bool large) {
-    return large ? (size_t)MAX_PARTS * part_cap_of(W, rows, sms, MAX_PARTS) * sizeof(int4)
-                 : (size_t)part_cap_of(W, rows, sms, 1) * sizeof(int2);
-}
-static int device_sms() {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
-}
+// list slots beyond one per centre: padding of the stage-1 warps' last
+// reserved blocks (<= 32 per consumer warp in flight)
+constexpr size_t LIST_SLACK = (size_t)1 << 20;
+
 size_t screen_workspace_bytes(int64_t W, int64_t rows) {
-    const int sms = device_sms();
-    return CTR_BYTES + std::max(list_bytes(W, rows, sms, false), list_bytes(W, rows, sms, true));
+    return 256 + ((size_t)std::max<int64_t>(W, 1) * (size_t)std::max<int64_t>(rows, 1) + LIST_SLACK) * sizeof(int2);
 }
 
 // 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
@@ -784,78 +671,6 @@ bool ring_fits32(int64_t n, int64_t d) {
     return 255 * mom < lim_s;
 }
 
-struct K3Launch {
-    ScreenArgs a;
-    TmaMaps maps;
-    TileMap tm;
-    int m, eb, sms, bm_words;
-    void* list;
-    unsigned *list_ctr, *tile_ctr, *group_ctr;
-    cudaStream_t s;
-};
-
-// K3a stage1_kernel then K3b rings_kernel of one size, with planes of T and
-// list entries of E in `parts` sub-lists.
-template <typename T, typename E>
-static int launch_k3(K3Launch& L, int parts) {
-    using G = Geo<T>;
-    const ScreenArgs& a = L.a;
-    TileMap& tm = L.tm;
-    const long long part_cap = part_cap_of(a.W, a.y_end - a.y_begin, L.sms, parts);
-    E* list = static_cast<E*>(L.list);
-    // K3a: the mask rows are (re)initialised here; survivors are OR'ed in by K3b
-    auto s1 = stage1_kernel<T, E>;
-    const size_t s1_smem_all = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(a.ring[0].wm, 1) * 4;
-    int s1_per_sm = 1;
-    cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem_all);
-    s1_per_sm = std::min(std::max(s1_per_sm, 1), 2);  // part_cap_of budgets <= 2 CTAs per SM
-    // Column strips: a SAT element is used by four centres at the corners of
-    // a 2n x 2n square, so it is read from HBM once only if the rows between
-    // them (vertical reuse) and the columns between them (horizontal reuse)
-    // are still in L2.  The widest strip whose working set -- (m + rows in
-    // flight) x (strip + m) x 3 planes of PLAIN SAT/E/O -- fits the budget keeps
-    // both; narrower strips re-read (strip + m) / strip of the columns.
-    {
-        int64_t budget = 40ll << 20, planes = 3;
-        if (const char* e = getenv("SS_STRIP_BUDGET_MB")) budget = (int64_t)atoi(e) << 20;  // experiment hooks
-        if (const char* e = getenv("SS_STRIP_PLANES")) planes = atoi(e);
-        const int64_t in_flight = (int64_t)L.sms * s1_per_sm * G::STAGES;
-        tm.strip = 1;
-        for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
-            const int64_t rows = (in_flight + strip - 1) / strip * TY;
-            const int64_t ws = (L.m + 2 + rows) * ((int64_t)strip * TX + L.m + 2) * planes * L.eb;
-            if (ws <= budget) {
-                tm.strip = strip;
-                break;
-            }
-        }
-    }
-    if (const char* e = getenv("SS_STRIP")) tm.strip = std::max(1, std::min(tm.n_tx, atoi(e)));  // experiment hook
-    {
-        // every partition needs a CTA (CTAs without tiles exit at once)
-        const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)L.sms * s1_per_sm),
-                                                   parts);
-        s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem_all, L.s>>>(a, L.maps, tm, parts, list, part_cap, L.list_ctr,
-                                                                  L.tile_ctr);
-        note_launch();
-        if (int e = check_launch("stage1_kernel")) return e;
-    }
-    // K3b: all rings over the stage-1 sub-lists; survivors into the mask
-    {
-        const size_t smem = (size_t)((L.bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.n_rings * QCAP * sizeof(int2);
-        auto rk = rings_kernel<T, E>;
-        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, RK_WARPS * 32, smem);
-        rk<<<(unsigned)(L.sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, L.s>>>(a, parts, list, part_cap, L.list_ctr,
-                                                                                L.group_ctr, L.bm_words);
-        note_launch();
-        if (int e = check_launch("rings_kernel")) return e;
-    }
-    return SS_OK;
-}
-
 int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t pitch, int64_t W,
                 int64_t H, int64_t y_origin,
                 int64_t y_begin, int64_t y_end, int32_t m, int32_t stride, int32_t n_rings, const int32_t* ring_n,
@@ -898,11 +713,6 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     a.lo = lo;
     a.hi = hi;
     a.n_rings = n_rings;
-    {
-        // ring-0 PLAIN sums (square 4n^2, diamond 2d^2+2d+1 pixels of <= 255) below 2^32
-        const int64_t n0 = ring_n[0], d0 = ring_d[0];
-        a.sums_in_list = (255 * 4 * n0 * n0 < ((int64_t)1 << 32)) && (255 * (2 * d0 * d0 + 2 * d0 + 1) < ((int64_t)1 << 32));
-    }
     a.qm = qm;
     a.qs = qs;
     a.qg = qg;
@@ -941,8 +751,6 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
         R.rcp_di = 1.0 / R.cnt_di;
         R.rw1_sq = 1.0 / R.w1_sq;
         R.rw1_di = 1.0 / R.w1_di;
-        R.fa = (float)(1.0 / (2.0 * R.cnt_sq * qm));
-        R.fb = (float)(1.0 / (2.0 * R.cnt_di * qm));
         const int64_t* hd = h_blob + 1 + SS_BLOB_HDR * r;
         R.off_m = (int)hd[0];
         R.n_m = (int)hd[1];
@@ -1000,17 +808,18 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
         set_error("screen workspace too small: %zu < %zu", ws_bytes, need);
         return SS_EINVAL;
     }
-    // workspace counters (one 128-B line each): stage-1 tile counters, list
-    // counters, rings group counters -- MAX_PARTS of each
-    unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
-    unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
-    unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
-    const int sms = device_sms();
-    void* list_a = static_cast<char*>(d_ws) + CTR_BYTES;
+    // workspace: [counters: list count [0], tile counter [32], list group counters [33, 33 + 8);
+    //             256 B] [ring-0 candidate list: W x rows int2]
+    unsigned* counts = static_cast<unsigned*>(d_ws);
+    int2* list_a = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + 256);
     if (cudaMemsetAsync(d_row_counts, 0, rows * sizeof(uint32_t), s) != cudaSuccess) return check_launch("memset");
-    if (cudaMemsetAsync(tile_ctr, 0, CTR_BYTES, s) != cudaSuccess) return check_launch("memset");
+    if (cudaMemsetAsync(counts, 0, 256, s) != cudaSuccess) return check_launch("memset");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 
-    TmaMaps maps;  // PLAIN SAT / E / O planes for the stage-1 TMA boxes
+    // K3a: the mask rows are (re)initialised here; survivors are OR'ed in by K3b
+    TmaMaps maps;
     {
         const char* base = static_cast<const char*>(a.planes);
         const int bw = use32 ? Geo<unsigned>::BW : Geo<long long>::BW;
@@ -1022,17 +831,57 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     TileMap tm;
     tm.n_tx = (int)((W + TX - 1) / TX);
     tm.n_ty = (int)((rows + TY - 1) / TY);
-    tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
-    tm.strip = 1;
-    bool large = tm.n_tiles >= LARGE_TILES;
-    if (const char* e = getenv("SS_LIST_MODE")) large = atoi(e) != 0;  // experiment hook
-    K3Launch L{a, maps, tm, m, eb, sms, bm_words, list_a, list_ctr, tile_ctr, group_ctr, s};
-    if (large) {
-        L.a.sums_in_list = a.sums_in_list;
-        return use32 ? launch_k3<unsigned, int4>(L, MAX_PARTS) : launch_k3<long long, int4>(L, MAX_PARTS);
+    // Column strips: a SAT element is used by four centres at the corners of
+    // a 2n x 2n square, so it is read from HBM once only if the rows between
+    // them (vertical reuse) and the columns between them (horizontal reuse)
+    // are still in L2.  The widest strip whose working set -- (m + rows in
+    // flight) x (strip + m) x 3 planes of PLAIN SAT/E/O -- fits the budget keeps
+    // both; narrower strips re-read (strip + m) / strip of the columns.
+    auto s1 = use32 ? stage1_kernel<unsigned> : stage1_kernel<long long>;
+    const size_t s1_smem = use32 ? (size_t)Geo<unsigned>::STAGES * Geo<unsigned>::STAGE_BYTES
+                                 : (size_t)Geo<long long>::STAGES * Geo<long long>::STAGE_BYTES;
+    const size_t s1_smem_all = s1_smem + (size_t)std::max(a.ring[0].wm, 1) * 4;
+    int s1_per_sm = 1;
+    cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem_all);
+    s1_per_sm = std::max(s1_per_sm, 1);
+    {
+        int64_t budget = 40ll << 20, planes = 3;
+        if (const char* e = getenv("SS_STRIP_BUDGET_MB")) budget = (int64_t)atoi(e) << 20;  // experiment hooks
+        if (const char* e = getenv("SS_STRIP_PLANES")) planes = atoi(e);
+        const int64_t in_flight = (int64_t)sms * s1_per_sm * (use32 ? Geo<unsigned>::STAGES : Geo<long long>::STAGES);
+        tm.strip = 1;
+        for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
+            const int64_t rows = (in_flight + strip - 1) / strip * TY;
+            const int64_t ws = (m + 2 + rows) * ((int64_t)strip * TX + m + 2) * planes * eb;
+            if (ws <= budget) {
+                tm.strip = strip;
+                break;
+            }
+        }
     }
-    L.a.sums_in_list = 0;
-    return use32 ? launch_k3<unsigned, int2>(L, 1) : launch_k3<long long, int2>(L, 1);
+    if (const char* e = getenv("SS_STRIP")) tm.strip = std::max(1, std::min(tm.n_tx, atoi(e)));  // experiment hook
+    tm.n_tiles = (long long)tm.n_tx * tm.n_ty;
+    {
+        const long long grid = std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm);
+        s1<<<(unsigned)std::max<long long>(grid, 1), (WARPS + 1) * 32, s1_smem_all, s>>>(a, maps, tm, list_a, counts + 0,
+                                                                                 counts + 32);
+        note_launch();
+        if (int e = check_launch("stage1_kernel")) return e;
+    }
+    // K3b: all rings over list 0 (counts[0]); survivors into the mask
+    {
+        const size_t smem = (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * n_rings * QCAP * sizeof(int2);
+        auto rk = use32 ? rings_kernel<unsigned> : rings_kernel<long long>;
+        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, RK_WARPS * 32, smem);
+        rk<<<(unsigned)(sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, s>>>(a, list_a, counts + 0, counts + 33,
+                                                                           bm_words);
+        note_launch();
+        if (int e = check_launch("rings_kernel")) return e;
+    }
+    return SS_OK;
 }
 
 int fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask, int64_t mask_pitch,

@@ -213,3 +213,23 @@ def test_32bit_boundary_sizes(cuda, side):
     img = WL.make_image(640, 560, seed=41, sigma=4.0, noise=3.0)
     case = WL.make_template(img, 43, side, (1.0, 1.0), std_threshold=10.0)
     compare_with_oracle(img, case.template, {"alpha": 1.0, "beta": 1.0, "quantizer": (4.0, 4.0, 4.0)})
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_list_modes_vs_oracle(cuda, monkeypatch, mode):
+    """Both candidate-list modes of K3 (one (x, y) list; partitioned sub-lists
+    carrying the ring-0 sums) on the same inputs, 32-bit and int64 planes."""
+    import workloads as WL
+    from paper_1707_05647_b200.screening import get_engine
+
+    monkeypatch.setenv("SS_LIST_MODE", mode)
+    img = WL.make_image(700, 380, seed=61, sigma=2.5, noise=2.0)
+    case = WL.make_template(img, 62, 40, (0.8, 1.3), std_threshold=10.0)
+    kw = {"alpha": 0.5, "beta": 1.8, "ladder_ratio": 1.25, "quantizer": (6.0, 6.0, 6.0)}
+    compare_with_oracle(img, case.template, kw)
+    eng = get_engine(img.shape[1], img.shape[0])
+    eng.force_int64 = True
+    try:
+        compare_with_oracle(img, case.template, kw)
+    finally:
+        eng.force_int64 = False
