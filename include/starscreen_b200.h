@@ -139,6 +139,27 @@ size_t ss_screen_workspace_bytes(int64_t W, int64_t rows);
 int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, unsigned long long* d_mismatches,
                     void* stream);
 
+/*
+ * The whole ladder loop of screen() (screening.py:502-520) in one call: for
+ * every size k (ladder order) ss_screen_size, or ss_fill_grid when m < 8
+ * (screening.py:505-510), enqueued on streams[1 + k % (n_streams - 1)] with
+ * an event fork from / join to streams[0] (all sizes on streams[0] when
+ * n_streams == 1).  Per size k: h_m[k], h_n_rings[k], ring plan at
+ * h_ring_n / h_ring_d + k * SS_MAX_RINGS, key blob at d_blobs / h_blobs +
+ * h_blob_off[k] (ss_ladder_keysets), mask at d_masks + k *
+ * size_stride_words, row counts at d_row_counts + k * row_counts_stride.
+ * d_workspaces[i] (ss_screen_workspace_bytes each) belongs to streams[i].
+ * flags bit 0: screen every size from the int64 planes (test hook).
+ */
+int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
+                     int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride,
+                     int32_t n_sizes, const int32_t* h_m, const int32_t* h_n_rings, const int32_t* h_ring_n,
+                     const int32_t* h_ring_d, const int64_t* d_blobs, const int64_t* h_blobs,
+                     const int64_t* h_blob_off, double q_mean, double q_std, double q_grad, uint32_t* d_masks,
+                     int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
+                     int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags, int32_t n_streams,
+                     void* const* streams, void* const* d_workspaces, size_t workspace_bytes);
+
 /* screening.py:505-510: sizes below MIN_PATCH_SIDE keep every grid centre. */
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,
                  int64_t mask_pitch_words, uint32_t* d_row_counts, void* stream);
@@ -214,6 +235,20 @@ int ss_feature_set_keys(const uint8_t* h_template, int32_t n, int32_t m, int32_t
  */
 int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, double q_mean, double q_std,
                           double q_grad, int64_t* h_keys, int64_t* h_key_off);
+/*
+ * Host: ss_keys_from_features + ss_keyset_blob for every size of a ladder in
+ * one call.  h_feats: the instances of all sizes in ladder order, rings
+ * feat_ring_stride apart (the ss_template_features_device layout, stride
+ * SS_MAX_RINGS); size k has h_nk[k] instances and h_n_rings[k] rings.
+ * Outputs: keys (size k's rings at h_key_off, n_rings[k] + 1 offsets per
+ * size, relative to the size's first key), blobs (size k at
+ * h_blob_off[k], n_sizes + 1 offsets in int64 slots).  keys_cap / blobs_cap
+ * are the buffers' slots; too small -> SS_EINVAL.
+ */
+int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n_sizes, const int32_t* h_nk,
+                      const int32_t* h_n_rings, double q_mean, double q_std, double q_grad, int64_t* h_keys,
+                      int64_t keys_cap, int64_t* h_key_off, int64_t* h_blobs, int64_t blobs_cap,
+                      int64_t* h_blob_off);
 /*
  * Device (f2): ring features of n_inst (m, k) rescale instances of the n x n
  * template d_template in one launch.  d_desc: n_inst rows of desc_stride

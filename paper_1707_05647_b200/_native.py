@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libstarscreen_b200.so")
 
 SS_OK, SS_EINVAL, SS_ECAPACITY, SS_ECUDA = 0, 1, 2, 3
 SS_MAX_RINGS = 16
+SS_BLOB_MAX_BITMAP_WORDS = 8192
 KEY_BASE = 1 << 21
 
 _lib = None
@@ -44,6 +45,11 @@ _SIGS = {
     "ss_screen_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "ss_selftest_div": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, c_d, c_i32, c_p, c_p]),
     "ss_fill_grid": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i32, c_p, c_i64, c_p, c_p]),
+    "ss_screen_ladder": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
+                                        c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_i64, c_p, c_i64,
+                                        c_p, c_i32, c_i32, c_p, c_p, c_sz]),
+    "ss_ladder_keysets": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_i64,
+                                         c_p]),
     "ss_compact_workspace_bytes": (c_sz, [c_i64]),
     "ss_compact": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_i64, c_p, c_p,
                                   c_p, c_sz, c_p]),

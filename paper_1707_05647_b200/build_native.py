@@ -26,6 +26,7 @@ SOURCES = {
     "ss_screen.cu": ["-fmad=false"],
     "ss_post.cu": [],
     "ss_featureset.cu": ["-fmad=false"],
+    "ss_ladder.cpp": [],
 }
 
 

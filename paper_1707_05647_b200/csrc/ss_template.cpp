@@ -278,4 +278,52 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
     return SS_OK;
 }
 
+
+int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n_sizes, const int32_t* h_nk,
+                      const int32_t* h_n_rings, double q_mean, double q_std, double q_grad, int64_t* h_keys,
+                      int64_t keys_cap, int64_t* h_key_off, int64_t* h_blobs, int64_t blobs_cap,
+                      int64_t* h_blob_off) {
+    if (!h_feats || n_sizes < 0 || n_sizes > SS_MAX_SIZES || !h_nk || !h_n_rings || !h_keys || !h_key_off ||
+        !h_blobs || !h_blob_off || feat_ring_stride < 1 || feat_ring_stride > SS_MAX_RINGS) {
+        ss::set_error("bad ladder keyset arguments");
+        return SS_EINVAL;
+    }
+    int64_t key_pos = 0, blob_pos = 0, off_pos = 0, inst = 0;
+    h_blob_off[0] = 0;
+    std::vector<double> feats;
+    for (int32_t k = 0; k < n_sizes; ++k) {
+        const int32_t nk = h_nk[k], nr = h_n_rings[k];
+        if (nk < 0 || nr < 1 || nr > feat_ring_stride) {
+            ss::set_error("bad ladder keyset size %d", k);
+            return SS_EINVAL;
+        }
+        // this size's features, rings packed (ss_keys_from_features layout)
+        feats.resize((size_t)nk * nr * 3);
+        for (int32_t i = 0; i < nk; ++i)
+            std::memcpy(&feats[(size_t)i * nr * 3], h_feats + (size_t)(inst + i) * feat_ring_stride * 3,
+                        sizeof(double) * 3 * (size_t)nr);
+        inst += nk;
+        if (key_pos + (int64_t)nr * 27 * nk > keys_cap) {
+            ss::set_error("ladder keyset key buffer too small");
+            return SS_EINVAL;
+        }
+        int64_t* off = h_key_off + off_pos;  // nr + 1 offsets relative to this size's first key
+        if (int e = ss_keys_from_features(feats.data(), nk, nr, q_mean, q_std, q_grad, h_keys + key_pos, off))
+            return e;
+        size_t bytes = 0;
+        if (int e = ss_keyset_blob(h_keys + key_pos, off, nr, nullptr, &bytes)) return e;
+        const int64_t slots = (int64_t)(bytes / sizeof(int64_t));
+        if (blob_pos + slots > blobs_cap) {
+            ss::set_error("ladder keyset blob buffer too small");
+            return SS_EINVAL;
+        }
+        if (int e = ss_keyset_blob(h_keys + key_pos, off, nr, h_blobs + blob_pos, &bytes)) return e;
+        key_pos += off[nr];
+        off_pos += nr + 1;
+        blob_pos += slots;
+        h_blob_off[k + 1] = blob_pos;
+    }
+    return SS_OK;
+}
+
 }  // extern "C"

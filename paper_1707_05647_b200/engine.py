@@ -12,6 +12,7 @@ a CUDA graph.  Row-band shards use the same engine with a band frame
 from __future__ import annotations
 
 import ctypes
+import functools
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -19,8 +20,9 @@ import numpy as np
 import torch
 
 from . import _native
+from ._native import SS_BLOB_MAX_BITMAP_WORDS, SS_MAX_RINGS
 from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, patch_center_margins, ring_plan
-from .featureset import FeatureSet, build_feature_set, build_feature_sets_device, keyset_blob
+from .featureset import FeatureSet, build_feature_set, instance_descriptors, keyset_blob, template_features_device
 
 
 import os
@@ -54,53 +56,174 @@ def _stream_handle() -> int:
 class SizePlan:
     m: int
     plan: Tuple[Tuple[int, int], ...] = ()
-    feature_set: Optional[FeatureSet] = None
-    blob: Optional[np.ndarray] = None  # host copy (kernel parameters are read from it)
-    blob_dev: Optional[torch.Tensor] = None
+    keys: Optional[List[np.ndarray]] = None  # per-ring sorted keys (FeatureSet.ring_keys())
+    blob: Optional[np.ndarray] = None  # host key blob (kernel parameters are read from it)
     ring_n: Optional[np.ndarray] = None
     ring_d: Optional[np.ndarray] = None
     fits32: bool = True  # ring sums recoverable from the 32-bit planes (ss_screen_fits32)
+    quantizer: Optional[object] = None
+    _fs: Optional[FeatureSet] = None
+
+    @property
+    def feature_set(self) -> Optional[FeatureSet]:
+        """The reference's FeatureSet for this size (built on first access)."""
+        if self._fs is None and self.keys is not None:
+            fs = FeatureSet(self.plan, self.quantizer)
+            fs._set_sorted(self.keys)
+            self._fs = fs
+        return self._fs
 
 
 @dataclass
 class TemplatePlan:
-    """Everything the device needs about one template and config."""
+    """Everything the device needs about one template and config: per size the
+    ring plan and key blob, and the whole ladder as flat arrays for
+    ss_screen_ladder (one call per screen)."""
 
     template_side: int
     config: ScreeningConfig
     ladder: Tuple[int, ...]
     sizes: List[SizePlan] = field(default_factory=list)
+    m_arr: Optional[np.ndarray] = None  # (L,) int32
+    n_rings: Optional[np.ndarray] = None  # (L,) int32, 0 for m < MIN_PATCH_SIDE
+    ring_n: Optional[np.ndarray] = None  # (L, SS_MAX_RINGS) int32
+    ring_d: Optional[np.ndarray] = None
+    blobs: Optional[np.ndarray] = None  # all sizes' key blobs, int64
+    blob_off: Optional[np.ndarray] = None  # (L + 1,) int64 slot offsets
+    blobs_dev: Optional[torch.Tensor] = None
+    geometry: Optional["LadderGeometry"] = None
 
     @property
     def max_m(self) -> int:
         return max(self.ladder) if self.ladder else 1
 
 
-def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device) -> TemplatePlan:
-    """Template side of screen() (screening.py:497, 511): ladder + per-size key sets.
+@dataclass(frozen=True)
+class LadderGeometry:
+    """Config-derived constants of one (template side, config): ladder, ring
+    plans, the flat per-size arrays ss_screen_ladder reads and the f2
+    instance descriptors.  Pure functions of (n, alpha, beta, ladder_ratio,
+    ring_count), computed once and shared (read-only) by every TemplatePlan."""
 
-    On a CUDA device the rescale features of every size come from one GPU
-    launch (f2, build_feature_sets_device); otherwise from the host C++ path.
-    """
-    n = template.shape[1]
+    ladder: Tuple[int, ...]
+    plans: Tuple[Tuple[Tuple[int, int], ...], ...]
+    m_arr: np.ndarray
+    n_rings: np.ndarray
+    ring_n: np.ndarray
+    ring_d: np.ndarray
+    fits32: Tuple[bool, ...]
+    evaluated: Tuple[int, ...]
+    desc: np.ndarray  # (n_inst, DESC_STRIDE) int32 rescale instances of the evaluated sizes
+    nk: np.ndarray  # (len(evaluated),) int32 instances per evaluated size
+
+
+@functools.lru_cache(maxsize=64)
+def ladder_geometry(n: int, alpha: float, beta: float, ladder_ratio: float, ring_count: int) -> LadderGeometry:
+    cfg = ScreeningConfig(alpha=alpha, beta=beta, ladder_ratio=ladder_ratio, ring_count=ring_count)
     ladder = ladder_sizes(n, cfg)
-    tp = TemplatePlan(n, cfg, ladder)
-    dev = torch.device(device) if device is not None else torch.device("cpu")
-    evaluated = [m for m in ladder if m >= MIN_PATCH_SIDE]
-    fsets = build_feature_sets_device(template, evaluated, cfg, dev) if dev.type == "cuda" else {}
-    for m in ladder:
-        sp = SizePlan(m)
-        if m >= MIN_PATCH_SIDE:
-            fs = fsets[m] if m in fsets else build_feature_set(template, m, cfg)
-            sp.plan = fs.plan
-            sp.feature_set = fs
-            sp.blob = keyset_blob(fs)
-            sp.blob_dev = torch.from_numpy(sp.blob).to(device)
-            sp.ring_n = np.array([p[0] for p in fs.plan], np.int32)
-            sp.ring_d = np.array([p[1] for p in fs.plan], np.int32)
-            sp.fits32 = bool(_native.lib().ss_screen_fits32(len(fs.plan), sp.ring_n.ctypes.data,
-                                                            sp.ring_d.ctypes.data))
+    L = len(ladder)
+    plans = tuple(ring_plan(m, ring_count) if m >= MIN_PATCH_SIDE else () for m in ladder)
+    m_arr = np.array(ladder, np.int32)
+    n_rings = np.array([len(p) for p in plans], np.int32)
+    ring_n = np.zeros((max(L, 1), SS_MAX_RINGS), np.int32)
+    ring_d = np.zeros((max(L, 1), SS_MAX_RINGS), np.int32)
+    fits = []
+    lib = _native.lib()
+    for k, plan in enumerate(plans):
+        for r, (nr, dr) in enumerate(plan):
+            ring_n[k, r], ring_d[k, r] = nr, dr
+        fits.append(bool(plan) and bool(lib.ss_screen_fits32(len(plan), ring_n[k].ctypes.data, ring_d[k].ctypes.data)))
+    evaluated = tuple(m for m in ladder if m >= MIN_PATCH_SIDE)
+    desc, nk = instance_descriptors(evaluated, ring_count, ladder_ratio)
+    for a in (m_arr, n_rings, ring_n, ring_d, nk):
+        a.setflags(write=False)
+    return LadderGeometry(ladder, plans, m_arr, n_rings, ring_n, ring_d, tuple(fits), evaluated, desc, nk)
+
+
+def plan_ladder(n: int, cfg: ScreeningConfig) -> TemplatePlan:
+    """The template-independent part of prepare_template: ladder, ring plans,
+    flat arrays (ladder_sizes screening.py:202-219, ring_plan
+    features.py:190-211)."""
+    geo = ladder_geometry(n, cfg.alpha, cfg.beta, cfg.ladder_ratio, cfg.ring_count)
+    tp = TemplatePlan(n, cfg, geo.ladder)
+    tp.geometry = geo
+    tp.m_arr, tp.n_rings, tp.ring_n, tp.ring_d = geo.m_arr, geo.n_rings, geo.ring_n, geo.ring_d
+    for k, m in enumerate(geo.ladder):
+        plan = geo.plans[k]
+        sp = SizePlan(m, plan, quantizer=cfg.quantizer, fits32=geo.fits32[k] if plan else True)
+        if plan:
+            sp.ring_n = geo.ring_n[k, : len(plan)]
+            sp.ring_d = geo.ring_d[k, : len(plan)]
         tp.sizes.append(sp)
+    return tp
+
+
+def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """The template-dependent part of prepare_template (build_feature_set,
+    screening.py:222-250, for every size).
+
+    On a CUDA device: the rescale features of every size from one GPU launch
+    on `stream` (f2; only that stream is synchronised), the key sets and
+    device blobs of every size from one host call (ss_ladder_keysets), and
+    one upload of the blobs on the current stream.  Otherwise each size goes
+    through the host C++ build_feature_set.
+    """
+    cfg = tp.config
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    L = len(tp.sizes)
+    geo = getattr(tp, "geometry", None)
+    if dev.type == "cuda" and geo is not None and geo.evaluated:
+        feats = template_features_device(template, geo.desc, dev, stream)
+        nk = geo.nk
+        n_r = tp.n_rings[tp.n_rings > 0]
+        keys_cap = int(27 * (nk.astype(np.int64) * n_r).sum())
+        blobs_cap = int(sum(1 + 16 * int(r) + int(r) * (81 * int(k) + SS_BLOB_MAX_BITMAP_WORDS // 2 + 2)
+                            for k, r in zip(nk, n_r)))
+        keys = np.empty(max(keys_cap, 1), np.int64)
+        key_off = np.empty(int(n_r.sum()) + len(n_r), np.int64)
+        blobs = np.empty(max(blobs_cap, 1), np.int64)
+        boff = np.empty(len(n_r) + 1, np.int64)
+        q = cfg.quantizer.factors()
+        _native.check(_native.lib().ss_ladder_keysets(
+            feats.ctypes.data, SS_MAX_RINGS, len(n_r), nk.ctypes.data, n_r.ctypes.data, q[0], q[1], q[2],
+            keys.ctypes.data, keys.size, key_off.ctypes.data, blobs.ctypes.data, blobs.size, boff.ctypes.data),
+            "feature sets")
+        tp.blobs = blobs[: int(boff[-1])]
+        tp.blob_off = np.zeros(L + 1, np.int64)
+        i = ko = kp = 0
+        for k, sp in enumerate(tp.sizes):
+            if sp.plan:
+                r = len(sp.plan)
+                off = key_off[ko: ko + r + 1]
+                sp.keys = [keys[kp + off[j]: kp + off[j + 1]] for j in range(r)]
+                kp += int(off[r])
+                ko += r + 1
+                sp.blob = tp.blobs[int(boff[i]): int(boff[i + 1])]
+                i += 1
+            tp.blob_off[k + 1] = boff[i]
+    else:
+        parts = []
+        tp.blob_off = np.zeros(L + 1, np.int64)
+        for k, sp in enumerate(tp.sizes):
+            if sp.plan:
+                fs = build_feature_set(template, sp.m, cfg)
+                sp._fs = fs
+                sp.keys = fs.ring_keys()
+                sp.blob = keyset_blob(fs)
+                parts.append(sp.blob)
+            tp.blob_off[k + 1] = tp.blob_off[k] + (len(sp.blob) if sp.plan else 0)
+        tp.blobs = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+    if not tp.blobs.size:
+        tp.blobs = np.zeros(1, np.int64)
+    if dev.type == "cuda":
+        tp.blobs_dev = torch.from_numpy(tp.blobs).pin_memory().to(dev, non_blocking=True)
+
+
+def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device,
+                     stream: Optional[torch.cuda.Stream] = None) -> TemplatePlan:
+    """Template side of screen() (screening.py:497, 511): ladder + per-size key sets."""
+    tp = plan_ladder(template.shape[1], cfg)
+    fill_keysets(tp, template, device, stream)
     return tp
 
 
@@ -133,8 +256,10 @@ class Engine:
         # (fork/join around the K3 region), each with its own screen workspace
         self.n_streams = streams_for(tb32)
         self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n_streams)]
+        self.template_stream = torch.cuda.Stream(self.device)  # f2 features, overlapping the table build
         ws = int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1)))
         self.screen_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device) for _ in range(self.n_streams)]
+        self.screen_ws_main = self.screen_ws[0]  # used only when there are no side streams
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -217,24 +342,24 @@ class Engine:
                                               self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
                                               _stream_handle()), "build_tables")
 
-    def screen_size(self, k: int, tp: TemplatePlan, ws: Optional[torch.Tensor] = None) -> None:
-        ws = self.screen_ws[0] if ws is None else ws
-        sp = tp.sizes[k]
+    def screen_ladder(self, tp: TemplatePlan, main: Optional[torch.cuda.Stream] = None) -> None:
+        """K3 for every ladder size in one ss_screen_ladder call (sizes spread
+        over the side streams, event fork/join around them)."""
+        main = main or torch.cuda.current_stream(self.device)
         cfg = tp.config
-        mask = self.masks[k]
-        rc = self.row_counts[k]
-        s = _stream_handle()
-        if sp.m < MIN_PATCH_SIDE:
-            _native.check(self.L.ss_fill_grid(self.W, self.y_begin, self.y_end, cfg.stride, mask.data_ptr(),
-                                              self.words, rc.data_ptr(), s), "fill_grid")
-            return
         q = cfg.quantizer.factors()
-        _native.check(self.L.ss_screen_size(
-            _p(self.planes) if (self.force_int64 or not sp.fits32) else None,
-            None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch, self.W, self.H, self.y_origin, self.y_begin,
-            self.y_end, sp.m, cfg.stride, len(sp.plan), sp.ring_n.ctypes.data, sp.ring_d.ctypes.data,
-            sp.blob_dev.data_ptr(), sp.blob.ctypes.data, q[0], q[1], q[2], mask.data_ptr(), self.words, rc.data_ptr(),
-            _p(self.stage_counts), ws.data_ptr(), ws.numel(), s), "screen_size")
+        L = len(tp.sizes)
+        handles = (ctypes.c_void_p * (1 + self.n_streams))(main.cuda_stream, *[st.cuda_stream for st in self.streams])
+        wss = (ctypes.c_void_p * (1 + self.n_streams))(self.screen_ws_main.data_ptr(),
+                                                        *[w.data_ptr() for w in self.screen_ws])
+        _native.check(self.L.ss_screen_ladder(
+            _p(self.planes), None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch,
+            self.W, self.H, self.y_origin, self.y_begin, self.y_end, cfg.stride, L, tp.m_arr.ctypes.data,
+            tp.n_rings.ctypes.data, tp.ring_n.ctypes.data, tp.ring_d.ctypes.data, tp.blobs_dev.data_ptr(),
+            tp.blobs.ctypes.data, tp.blob_off.ctypes.data, q[0], q[1], q[2], self.masks.data_ptr(), self.words,
+            self.mrows * self.words, self.row_counts.data_ptr(), self.row_counts.shape[1], _p(self.stage_counts),
+            1 if self.force_int64 else 0, 1 + self.n_streams, handles, wss, self.screen_ws[0].numel()),
+            "screen")
 
     def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:
         return np.array([sp.m for sp in tp.sizes], np.int32)
@@ -272,19 +397,7 @@ class Engine:
         main = torch.cuda.current_stream(self.device)
         if self.hooks is not None:
             self.hooks[0](main)
-        fork = torch.cuda.Event()
-        fork.record(main)
-        used = set()
-        for k in range(len(tp.sizes)):
-            j = k % self.n_streams
-            st = self.streams[j]
-            if j not in used:
-                st.wait_event(fork)
-                used.add(j)
-            with torch.cuda.stream(st):
-                self.screen_size(k, tp, self.screen_ws[j])
-        for j in used:
-            main.wait_stream(self.streams[j])
+        self.screen_ladder(tp, main)
         if self.hooks is not None:
             self.hooks[1](main)
         self.compact_all(tp)

@@ -152,49 +152,74 @@ SS_MAX_RINGS = 16
 DESC_STRIDE = 4 + 2 * SS_MAX_RINGS
 
 
-def build_feature_sets_device(template: np.ndarray, ms, cfg: ScreeningConfig, device) -> dict:
-    """build_feature_set for every size in `ms` with the rescale features on the GPU (f2).
+def instance_descriptors(ms, ring_count: int, ladder_ratio: float):
+    """Rescale instances (m, k = m .. ceil(m * ratio), screening.py:236-238) of
+    every size in `ms` as the f2 kernel's descriptor rows
+    [m, k, n_rings, 0, n_0, d_0, ...]; returns (desc (n_inst, DESC_STRIDE)
+    int32, nk (len(ms),) int32 instances per size)."""
+    rows, nk = [], []
+    for m in ms:
+        if m < MIN_PATCH_SIDE:
+            raise ValueError(f"patch side {m} below minimum {MIN_PATCH_SIDE}")
+        plan = ring_plan(m, ring_count)
+        k_hi = math.ceil(m * ladder_ratio)
+        d = np.zeros((k_hi - m + 1, DESC_STRIDE), np.int32)
+        d[:, 0] = m
+        d[:, 1] = np.arange(m, k_hi + 1)
+        d[:, 2] = len(plan)
+        for r, (nr, dr) in enumerate(plan):
+            d[:, 4 + 2 * r], d[:, 5 + 2 * r] = nr, dr
+        rows.append(d)
+        nk.append(k_hi - m + 1)
+    desc = np.concatenate(rows) if rows else np.zeros((0, DESC_STRIDE), np.int32)
+    return np.ascontiguousarray(desc), np.array(nk, np.int32)
 
-    One kernel launch evaluates every (m, k) rescale instance
-    (csrc/ss_featureset.cu); the guard-banded key sets are then built on the
-    host from the returned features, in k order, exactly as build_feature_set
-    (screening.py:222-250) does.
-    """
+
+def template_features_device(template: np.ndarray, desc: np.ndarray, device, stream=None) -> np.ndarray:
+    """Ring features of the rescale instances `desc` (instance_descriptors) of
+    the template, from one GPU launch (f2, csrc/ss_featureset.cu) on `stream`
+    (default: the current stream), which is synchronised.  Returns
+    (n_inst, SS_MAX_RINGS, 3) float64 on the host."""
     import torch
 
     tpl = as_gray(template)
     n = tpl.shape[0]
     if tpl.shape[0] != tpl.shape[1]:
         raise ValueError(f"template must be square, got {tpl.shape[1]}x{tpl.shape[0]}")
-    sizes = []
-    rows = []
-    for m in ms:
-        if m < MIN_PATCH_SIDE:
-            raise ValueError(f"patch side {m} below minimum {MIN_PATCH_SIDE}")
-        plan = ring_plan(m, cfg.ring_count)
-        k_hi = math.ceil(m * cfg.ladder_ratio)
-        first = len(rows)
-        for k in range(m, k_hi + 1):
-            d = np.zeros(DESC_STRIDE, np.int32)
-            d[0], d[1], d[2] = m, k, len(plan)
-            for r, (nr, dr) in enumerate(plan):
-                d[4 + 2 * r], d[5 + 2 * r] = nr, dr
-            rows.append(d)
-        sizes.append((m, plan, first, len(rows) - first))
-    out = {}
-    if not rows:
-        return out
+    if desc.shape[0] == 0:
+        return np.zeros((0, SS_MAX_RINGS, 3))
     dev = torch.device(device)
-    d_desc = torch.from_numpy(np.stack(rows)).to(dev)
-    d_tpl = torch.from_numpy(tpl).to(dev)
-    d_out = torch.empty((len(rows), SS_MAX_RINGS, 3), dtype=torch.float64, device=dev)
-    _native.check(_native.lib().ss_template_features_device(
-        d_tpl.data_ptr(), n, len(rows), d_desc.data_ptr(), DESC_STRIDE, d_out.data_ptr(),
-        torch.cuda.current_stream(dev).cuda_stream), "template features")
-    feats_all = d_out.cpu().numpy()
+    stream = stream or torch.cuda.current_stream(dev)
+    with torch.cuda.stream(stream):
+        d_desc = torch.from_numpy(desc).pin_memory().to(dev, non_blocking=True)
+        d_tpl = torch.from_numpy(tpl).pin_memory().to(dev, non_blocking=True)
+        d_out = torch.empty((desc.shape[0], SS_MAX_RINGS, 3), dtype=torch.float64, device=dev)
+        _native.check(_native.lib().ss_template_features_device(
+            d_tpl.data_ptr(), n, desc.shape[0], d_desc.data_ptr(), DESC_STRIDE, d_out.data_ptr(), stream.cuda_stream),
+            "template features")
+        host = torch.empty(d_out.shape, dtype=torch.float64, pin_memory=True)
+        host.copy_(d_out, non_blocking=True)
+    stream.synchronize()
+    return host.numpy()
+
+
+def build_feature_sets_device(template: np.ndarray, ms, cfg: ScreeningConfig, device) -> dict:
+    """build_feature_set for every size in `ms` with the rescale features on the GPU (f2).
+
+    The guard-banded key sets are built on the host from the returned
+    features, in k order, exactly as build_feature_set (screening.py:222-250)
+    does.
+    """
+    desc, nks = instance_descriptors(ms, cfg.ring_count, cfg.ladder_ratio)
+    feats_all = template_features_device(template, desc, device)
+    out = {}
     qm, qs, qg = cfg.quantizer.factors()
-    for m, plan, first, nk in sizes:
+    first = 0
+    for m, nk in zip(ms, nks):
+        nk = int(nk)
+        plan = ring_plan(m, cfg.ring_count)
         feats = np.ascontiguousarray(feats_all[first:first + nk, :len(plan), :])
+        first += nk
         keys = np.empty(len(plan) * 27 * nk, np.int64)
         off = np.empty(len(plan) + 1, np.int64)
         _native.check(_native.lib().ss_keys_from_features(_ptr(feats), nk, len(plan), qm, qs, qg, _ptr(keys),

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from .config import MIN_PATCH_SIDE, ScreeningConfig
-from .engine import Engine, TemplatePlan, prepare_template
+from .engine import Engine, TemplatePlan, fill_keysets, plan_ladder, prepare_template
 from .image import as_gray, std_dev
 
 
@@ -86,7 +86,7 @@ def upload_image(img: np.ndarray, device) -> torch.Tensor:
     dev = torch.device(device)
     src = torch.from_numpy(np.ascontiguousarray(img))
     if src.numel() < 2 * _UPLOAD_CHUNK:
-        return src.to(dev)
+        return src.pin_memory().to(dev, non_blocking=True)
     out = torch.empty(src.shape, dtype=torch.uint8, device=dev)
     flat_src, flat_dst = src.view(-1), out.view(-1)
     stream = torch.cuda.current_stream(dev)
@@ -328,7 +328,12 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     h, w = img.shape
     start = time.perf_counter()
     eng = get_engine(w, h, device)
-    tp = prepare_template(tpl, cfg, eng.device)
+    # The image side starts first (upload + K1/K2 on the current stream);
+    # the template side (f2 features on the engine's template stream, host
+    # key sets) overlaps it.
+    tp = plan_ladder(tpl.shape[1], cfg)
     img_dev = upload_image(img, eng.device)
-    eng.run(img_dev, tp)
+    eng.build_tables(img_dev, int64=eng.needs_int64(tp))
+    fill_keysets(tp, tpl, eng.device, eng.template_stream)
+    eng.run(img_dev, tp, build=False)
     return fetch_result(eng, tp, start)
