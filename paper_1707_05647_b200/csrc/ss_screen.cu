@@ -284,7 +284,13 @@ struct TmaMaps {
 // instruction"), so each box starts at the ALIGN-column boundary at or below
 // the corner and is BW = TX + ALIGN columns wide; readers skip the offset.
 constexpr int TY = WARPS;     // tile rows
-constexpr int CPW = 2;        // 32-centre chunks per warp per tile
+#ifndef S1_CPW
+#define S1_CPW 2
+#endif
+#ifndef S1_STAGES32
+#define S1_STAGES32 4
+#endif
+constexpr int CPW = S1_CPW;   // 32-centre chunks per warp per tile
 constexpr int TX = 32 * CPW;  // tile columns
 constexpr int NBOX = 8;
 constexpr int TILE_POS = TX * TY;  // centres per tile
@@ -309,7 +315,7 @@ template <> __device__ __forceinline__ int2 make_entry<int2>(int x, int y, unsig
 __device__ __forceinline__ int4 widen(int4 e) { return e; }
 __device__ __forceinline__ int4 widen(int2 e) { return make_int4(e.x, e.y, 0, 0); }
 template <typename T> struct Geo {
-    static constexpr int STAGES = sizeof(T) == 4 ? 4 : 3;  // pipeline depth (u32: 35 KB, int64: 68 KB a stage)
+    static constexpr int STAGES = sizeof(T) == 4 ? S1_STAGES32 : 3;  // pipeline depth (u32: 35 KB, int64: 68 KB a stage)
     static constexpr int ALIGN = 16 / (int)sizeof(T);
     static constexpr int BW = TX + ALIGN;  // staged box width (elements)
     static constexpr int BOX_ELEMS = BW * TY;
