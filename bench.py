@@ -57,6 +57,9 @@ def dist_env():
     return rank, world, local
 
 
+POOL_ENGINES = 4  # engines of the pool that screens a batch's images concurrently
+
+
 def workload_config(cfg_idx):
     import workloads as WL
 
@@ -75,7 +78,6 @@ def config_json(wl, ladder, n_gpus, extra=None):
         "ladder_ratio": wl.ladder_ratio,
         "quantizer": list(wl.q),
         "parallelism": f"image-parallel x{n_gpus}" if n_gpus > 1 else "single GPU",
-        "per_rank_images": 1,
         "l2": "flushed (256 MiB write) between timed steps; tables are 12 planes (32-bit cells mod 2^32 where exact, else int64) "
               f"({12 * 8 * (wl.width + 1) * (wl.height + 1) / 1e6:.0f} MB) > 126 MB L2",
     }
@@ -205,9 +207,10 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def k3_traffic(name):
-    """DRAM bytes (read + write) of the K3 kernels per step, from the committed
-    ncu launch list of this workload (profiles/r1/k3_traffic.json), or None."""
+def k3_traffic(name, images=1):
+    """DRAM bytes (read + write) of the K3 kernels per step of `images`
+    images, from the committed ncu launch list of this workload
+    (profiles/r1/k3_traffic.json, recorded over rec["images"] images), or None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "k3_traffic.json")
     try:
         with open(path) as f:
@@ -216,7 +219,7 @@ def k3_traffic(name):
         return None, None
     if not rec:
         return None, None
-    return rec["dram_bytes_per_step"], rec["source"]
+    return rec["dram_bytes_per_step"] / rec.get("images", 1) * images, rec["source"]
 
 
 def run_ours(args):
@@ -224,8 +227,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import workloads as WL
-    from paper_1707_05647_b200 import _native, screen
-    from paper_1707_05647_b200.engine import Engine, prepare_template
+    from paper_1707_05647_b200 import _native, screen, screen_batch
+    from paper_1707_05647_b200.engine import EnginePool, prepare_template
 
     rank, world, local = dist_env()
     if world > 1:
@@ -235,39 +238,52 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     wl = workload_config(args.config)
     cfg = WL.screening_config(wl)
-    case = WL.make_cases(wl, images=1, first_image=rank)[0]
-    img_dev = torch.from_numpy(case.image).to(dev)
-    tp = prepare_template(case.template, cfg, dev)
-    eng = Engine(wl.width, wl.height, dev)
+    # Single-image configs: every rank screens its own image (weak scaling).
+    # Batch configs (config 3: 64 images): a step is the whole batch, images
+    # dealt to ranks round-robin (strong scaling), each rank's share screened
+    # by an engine pool whose engines overlap on the GPU.
+    batch = wl.images > 1
+    idx = [i for i in range(wl.images) if i % world == rank] if batch else [rank]
+    cases = [WL.make_cases(wl, images=1, first_image=i)[0] for i in idx]
+    case = cases[0]
+    imgs_dev = [torch.from_numpy(c.image).to(dev) for c in cases]
+    tps = [prepare_template(c.template, cfg, dev) for c in cases]
+    tp = tps[0]
+    pool = EnginePool(wl.width, wl.height, dev, n=min(POOL_ENGINES, len(cases)))
+    eng = pool.engines[0]
     stream = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
     # ── instrumented pass (not timed): cascade stage counts for the roofline ──
-    eng.stage_counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    for e in pool.engines:
+        e.stage_counts = counts
     with torch.cuda.stream(stream):
-        eng.run(img_dev, tp)
+        pool.run(imgs_dev, tps)
     torch.cuda.synchronize()
-    stage = eng.stage_counts.cpu().tolist()
-    eng.stage_counts = None
-    positions = eng.tested(tp)
-    survivors = int(eng.totals[0].item())
+    stage = counts.cpu().tolist()
+    for e in pool.engines:
+        e.stage_counts = None
+    positions = sum(eng.tested(t) for t in tps)
+    survivors = int(stage[3])
+    capacity = max(max(1, survivors // len(cases)) * 4, 1 << 16)
 
     # per-launch events around every screen kernel (dominant kernel)
     ev_pairs = []
 
-    def before(k):
+    def before(st):  # st: the stream the engine enqueues K3 on
         e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
+        e.record(st)
         ev_pairs.append([e, None])
 
-    def after(k):
+    def after(st):
         e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
+        e.record(st)
         ev_pairs[-1][1] = e
 
     def step():
-        eng.run(img_dev, tp, capacity=max(survivors, 1) * 2)
+        pool.run(imgs_dev, tps, capacity=capacity)
 
     graph = None
     with torch.cuda.stream(stream):
@@ -314,16 +330,17 @@ def run_ours(args):
         launches = n_launch_graph * args.steps
     total_ms = sum(step_ms)
 
-    # per-kernel timing of the screen launches (dominant kernel), same stream
+    # per-kernel timing of the screen launches (dominant kernel): one engine,
+    # one image at a time (a batch's engines overlap, so their K3 intervals
+    # would not add up), scaled to the step's images
     eng.hooks = (before, after)
     with torch.cuda.stream(stream):
         for i in range(3):
             flush.fill_(i)
-            step()
+            eng.run(imgs_dev[0], tps[0], capacity=capacity)
     torch.cuda.synchronize()
     eng.hooks = None
-    screen_ms = sum(a.elapsed_time(b) for a, b in ev_pairs) / 3.0  # per step, all sizes
-    n_sizes = sum(1 for sp in tp.sizes if sp.plan)
+    screen_ms = sum(a.elapsed_time(b) for a, b in ev_pairs) / 3.0 * len(cases)  # per step, all sizes and images
 
     # max over ranks
     t = torch.tensor([total_ms, float(positions), float(survivors)], dtype=torch.float64, device=dev)
@@ -347,13 +364,13 @@ def run_ours(args):
     # SURVEY's literal 96 B figure and the cascade-aware count (3 PLAIN planes
     # for every ring-0 evaluation, the other 9 only for mean-projection
     # passers) are reported beside it.
-    per_size = eng.tested_per_size(tp)
+    per_size = [c * len(cases) for c in eng.tested_per_size(tp)]  # the batch's images share the ladder
     alg_bytes = sum(cnt * (12 * (4 if sp.fits32 else 8) + 0.125) for sp, cnt in zip(tp.sizes, per_size))
     achieved = alg_bytes / (screen_ms / 1e3) / 1e9
     cell_bytes = 12 * 8.0 * sum(cnt for sp, cnt in zip(tp.sizes, per_size) if not sp.fits32) / max(positions, 1) + \
         12 * 4.0 * sum(cnt for sp, cnt in zip(tp.sizes, per_size) if sp.fits32) / max(positions, 1)
     cascade_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
-    traffic, traffic_src = k3_traffic(wl.name)
+    traffic, traffic_src = k3_traffic(wl.name, len(cases))
     roofline = {
         "bound": "hbm", "kernel": "screen (K3: stage1_kernel + rings_kernel, all ladder sizes of one step)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -369,24 +386,35 @@ def run_ours(args):
                     "survivors": stage[3]},
         "screen_ms_per_step": screen_ms, "screen_share_of_step": screen_ms / (total_ms / args.steps),
     }
+    if batch:
+        roofline["screen_ms_note"] = ("batch: one image's K3 time (one engine, nothing overlapping) x the step's "
+                                      "images; in the step the pool's engines overlap")
 
     # ── e2e through the public API (host numpy in, host result out) ──
     e2e = None
     if not args.no_e2e:
         torch.cuda.synchronize()
+        images = [c.image for c in cases]
+        templates = [c.template for c in cases]
+
+        def call():
+            if batch:
+                res = screen_batch(images, templates, cfg, device=dev, engines=POOL_ENGINES)
+            else:
+                res = [screen(case.image, case.template, cfg, device=dev)]
+            return sum(len(r.candidates.array()) for r in res)  # the survivor lists read back to the host
+
         for _ in range(3):
-            screen(case.image, case.template, cfg, device=dev).candidates.array()
+            call()
         times = []
-        h2d = d2h = 0
-        for _ in range(max(5, min(args.steps, 20))):
+        for _ in range(max(5, min(args.steps, 20)) if not batch else 5):
             t0 = time.perf_counter()
-            res = screen(case.image, case.template, cfg, device=dev)
-            cand = res.candidates.array()  # the survivor list read back to the host
+            n_cand = call()
             times.append(time.perf_counter() - t0)
         n_inst = sum(math.ceil(m * wl.ladder_ratio) - m + 1 for m in tp.ladder if m >= 8)
-        h2d = (case.image.nbytes + case.template.nbytes + n_inst * 36 * 4
-               + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None))
-        d2h = len(cand) * 12 + 16 + n_inst * 16 * 3 * 8
+        h2d = len(cases) * (case.image.nbytes + case.template.nbytes + n_inst * 36 * 4
+                            + sum(sp.blob.nbytes for sp in tp.sizes if sp.blob is not None))
+        d2h = n_cand * 12 + len(cases) * (16 + n_inst * 16 * 3 * 8)
         e2e_t = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -394,8 +422,10 @@ def run_ours(args):
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e2e_t.item()),
                "ms_min_median_max": [1e3 * min(times), 1e3 * statistics.median(times), 1e3 * max(times)],
                "calls": len(times),
-               "api": "paper_1707_05647_b200.screen(numpy image, numpy template, cfg) + candidates read back; "
-                      "template feature sets included; masks stay on the device until accessed"}
+               "api": ("paper_1707_05647_b200.screen_batch(64 numpy images, templates, cfg)" if batch else
+                       "paper_1707_05647_b200.screen(numpy image, numpy template, cfg)")
+                      + " + candidates read back; template feature sets included; masks stay on the device until "
+                        "accessed"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -406,10 +436,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "scaling": "strong" if batch else "weak", "vs_baseline": None, "dtype": "int64+f64",
             "data": "synthetic (seeded noise + shapes, SURVEY.md 8(d); template per reference protocol)",
             "config": config_json(wl, tp.ladder, world, {
                 "positions_per_step_per_gpu": positions, "survivors_per_step": survivors,
+                "per_rank_images": len(cases), "engines": len(pool),
                 "cuda_graph": bool(graph is not None)}),
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -28,6 +28,7 @@ from .screening import (
     SizeMasks,
     prune_stats,
     screen,
+    screen_batch,
 )
 
 __all__ = [
@@ -54,4 +55,5 @@ __all__ = [
     "SizeMasks",
     "prune_stats",
     "screen",
+    "screen_batch",
 ]

@@ -409,3 +409,37 @@ class Engine:
         self.capacity = capacity
         self.xy = torch.empty((capacity, 3), dtype=torch.int32, device=self.device)
         self.compact_all(tp)
+
+
+class EnginePool:
+    """Several engines of one image shape, each on its own stream, for
+    batches of independent images (config 3: 64 x 1920x1080).  Image i goes
+    to engine i % n; the engines' work overlaps on the GPU, filling the SMs
+    that one small image's ladder leaves idle.  ``run`` forks from and joins
+    back to the current stream (CUDA-graph capturable); an engine reused for
+    a later image overwrites its buffers, so callers that need every image's
+    results fetch them between uses (screening.screen_batch)."""
+
+    def __init__(self, width: int, height: int, device=None, n: int = 4):
+        if n < 1:
+            raise ValueError("an engine pool needs at least one engine")
+        self.engines = [Engine(width, height, device) for _ in range(n)]
+        self.device = self.engines[0].device
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(n)]
+
+    def __len__(self) -> int:
+        return len(self.engines)
+
+    def run(self, imgs: Sequence[torch.Tensor], tps: Sequence[TemplatePlan], **kw) -> None:
+        main = torch.cuda.current_stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        used = min(len(self.engines), len(imgs))
+        for j in range(used):
+            self.streams[j].wait_event(fork)
+        for i, (img, tp) in enumerate(zip(imgs, tps)):
+            j = i % len(self.engines)
+            with torch.cuda.stream(self.streams[j]):
+                self.engines[j].run(img, tp, **kw)
+        for j in range(used):
+            main.wait_stream(self.streams[j])

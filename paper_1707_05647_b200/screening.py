@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from .config import MIN_PATCH_SIDE, ScreeningConfig
-from .engine import Engine, TemplatePlan, fill_keysets, plan_ladder, prepare_template
+from .engine import Engine, EnginePool, TemplatePlan, fill_keysets, plan_ladder, prepare_template
 from .image import as_gray, std_dev
 
 
@@ -337,3 +337,69 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     fill_keysets(tp, tpl, eng.device, eng.template_stream)
     eng.run(img_dev, tp, build=False)
     return fetch_result(eng, tp, start)
+
+
+_pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
+
+
+def get_pool(width: int, height: int, device=None, n: int = 4) -> EnginePool:
+    """One cached engine pool per (W, H, device, n); the most recent shape only."""
+    dev = torch.device(device if device is not None else "cuda")
+    key = (width, height, str(dev), n)
+    with _engine_lock:
+        pool = _pool_cache.get(key)
+        if pool is None:
+            _pool_cache.clear()
+            pool = EnginePool(width, height, dev, n)
+            _pool_cache[key] = pool
+        return pool
+
+
+def screen_batch(images: Sequence[np.ndarray], templates: Sequence[np.ndarray],
+                 cfg: Optional[ScreeningConfig] = None, device=None, engines: int = 4) -> List[ScreeningResult]:
+    """screen(images[i], templates[i], cfg) for a batch of same-shape images
+    (the benchmark loop of synth_bench.py:400-410 over independent cases).
+
+    Image i runs on engine i % engines of a pool, each engine on its own
+    stream: while the GPU screens image i, the host prepares image i + 1's
+    template side and image i - engines' results are read back.  Results are
+    identical to calling screen() per image; wall_time_s of each result is
+    measured from the start of its own preparation to its read-back.
+    """
+    cfg = cfg or ScreeningConfig()
+    if len(images) != len(templates):
+        raise ValueError(f"{len(images)} images but {len(templates)} templates")
+    if not len(images):
+        return []
+    checked = [validate(img, tpl, cfg) for img, tpl in zip(images, templates)]
+    h, w = checked[0][0].shape
+    if any(img.shape != (h, w) for img, _ in checked):
+        raise ValueError("screen_batch needs images of one shape")
+    pool = get_pool(w, h, device, max(1, min(engines, len(images))))
+    n = len(pool)
+    results: List[Optional[ScreeningResult]] = [None] * len(images)
+    pending: List[Optional[Tuple[int, TemplatePlan, float]]] = [None] * n
+
+    def collect(j: int) -> None:
+        if pending[j] is None:
+            return
+        i, tp, start = pending[j]
+        with torch.cuda.stream(pool.streams[j]):
+            results[i] = fetch_result(pool.engines[j], tp, start)
+        pending[j] = None
+
+    for i, (img, tpl) in enumerate(checked):
+        j = i % n
+        collect(j)  # the engine's previous image leaves before its buffers are reused
+        eng = pool.engines[j]
+        start = time.perf_counter()
+        with torch.cuda.stream(pool.streams[j]):
+            tp = plan_ladder(tpl.shape[1], cfg)
+            img_dev = upload_image(img, eng.device)
+            eng.build_tables(img_dev, int64=eng.needs_int64(tp))
+            fill_keysets(tp, tpl, eng.device, eng.template_stream)
+            eng.run(img_dev, tp, build=False)
+        pending[j] = (i, tp, start)
+    for j in range(n):
+        collect(j)
+    return results  # type: ignore[return-value]

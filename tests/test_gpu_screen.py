@@ -233,3 +233,28 @@ def test_list_modes_vs_oracle(cuda, monkeypatch, mode):
         compare_with_oracle(img, case.template, kw)
     finally:
         eng.force_int64 = False
+
+
+def test_screen_batch_matches_screen(cuda):
+    """screen_batch (engine pool, overlapped streams, engine reuse) == screen() per image."""
+    import workloads as WL
+    from paper_1707_05647_b200 import screen, screen_batch
+
+    imgs, tpls = [], []
+    for i in range(7):
+        img = WL.make_image(400, 300, seed=300 + i, sigma=2.5, noise=1.0)
+        case = WL.make_template(img, 400 + i, 32, (0.8, 1.2), std_threshold=10.0)
+        imgs.append(img)
+        tpls.append(case.template)
+    cfg = pcfg({"alpha": 0.7, "beta": 1.4, "quantizer": (6.0, 6.0, 6.0)})
+    batch = screen_batch(imgs, tpls, cfg, engines=3)
+    assert len(batch) == len(imgs)
+    for img, tpl, b in zip(imgs, tpls, batch):
+        a = screen(img, tpl, cfg)
+        assert a.candidates == b.candidates
+        assert a.stats.patches_tested == b.stats.patches_tested
+        assert a.stats.region_pixels_kept == b.stats.region_pixels_kept
+        for m in a.ladder:
+            assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
+    with pytest.raises(ValueError):
+        screen_batch(imgs[:2], tpls[:1], cfg)
