@@ -57,7 +57,7 @@ def dist_env():
     return rank, world, local
 
 
-POOL_ENGINES = 4  # engines of the pool that screens a batch's images concurrently
+POOL_ENGINES = int(os.environ.get("SS_POOL_ENGINES", "4"))  # engines screening a batch's images concurrently
 
 
 def workload_config(cfg_idx):

@@ -303,6 +303,10 @@ constexpr int TILE_POS = TX * TY;  // centres per tile
 //   kernel skips those 8 gathers).
 // Either way the lists follow the strip-major tile order.
 constexpr int MAX_PARTS = 8;
+// List slots a stage-1 warp reserves per atomic (a multiple of 32): fewer
+// atomics on the list counter vs. the padding of each warp's last blocks
+// (measured: 64 for the single list, 128 for the partitioned lists).
+constexpr int RESERVE_SMALL = 64, RESERVE_LARGE = 128, RESERVE_MAX = 128;
 constexpr unsigned GROUP_CTRS = 8;  // rings group counters per partition
 constexpr int CTR_STRIDE = 32;  // words between counters (one 128-B line each)
 template <typename E> __device__ __forceinline__ E make_entry(int x, int y, unsigned sq, unsigned sd);
@@ -363,7 +367,7 @@ __device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbi
 // passers appended to list0.  Persistent CTAs: warp WARPS is the producer.
 template <typename T, typename Entry>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const ScreenArgs a, const __grid_constant__ TmaMaps maps,
-                                                                  const TileMap tm, int parts, Entry* list_base, long long part_cap,
+                                                                  const TileMap tm, int parts, int reserve, Entry* list_base, long long part_cap,
                                                                   unsigned* list_ctr, unsigned* tile_ctr_base) {
     using G = Geo<T>;
     constexpr int STAGES = G::STAGES;
@@ -435,8 +439,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
     unsigned* count0 = list_ctr + part * CTR_STRIDE;
     Entry* buf = cand_buf[warp];  // passers are staged per warp and flushed 32 at a time
     int nbuf = 0;
-    unsigned res = 0;       // lane 0: base of the next reserved block of 32 list slots
+    unsigned res = 0;       // lane 0: base of the next reserved block of `reserve` list slots
     bool have_res = false;  // warp-uniform
+    unsigned res_base = 0, res_left = 0;  // warp-uniform: the block being filled
     unsigned long long n_int = 0, n_pass = 0;
     const bool unit_stride = a.stride == 1;
     for (int it = 0;; ++it) {
@@ -484,25 +489,38 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             if (pass) buf[nbuf + __popc(pb & lt)] = make_entry<Entry>(x, y, (unsigned)s1q[c], (unsigned)s1d[c]);
             nbuf += __popc(pb);
         }
-        // Full blocks of 32 go to list slots reserved one block ahead (the
-        // reservation's atomic round trip overlaps the next tiles); the
-        // warp's last reservation is padded with x = -1, which the rings
-        // kernel skips.
+        // Full batches of 32 go to list slots reserved `reserve` at a time,
+        // one reservation ahead (the atomic's round trip overlaps the next
+        // tiles); the rest of the warp's last reservations is padded with
+        // x = -1, which the rings kernel skips.
         while (nbuf >= 32) {
             __syncwarp();
-            if (!have_res && lane == 0) res = atomicAdd(count0, 32u);
-            const unsigned base = __shfl_sync(FULL, res, 0);
-            if (lane == 0) res = atomicAdd(count0, 32u);
-            have_res = true;
-            list0[base + lane] = buf[nbuf - 32 + lane];
+            if (res_left == 0) {
+                if (!have_res && lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                res_base = __shfl_sync(FULL, res, 0);
+                res_left = reserve;
+                if (lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                have_res = true;
+            }
+            list0[res_base + lane] = buf[nbuf - 32 + lane];
+            res_base += 32;
+            res_left -= 32;
             nbuf -= 32;
             __syncwarp();
         }
     }
     __syncwarp();
     if (have_res) {
-        const unsigned base = __shfl_sync(FULL, res, 0);
-        list0[base + lane] = lane < nbuf ? buf[lane] : make_entry<Entry>(-1, -1, 0, 0);
+        // finish the current block, then the one reserved ahead
+        unsigned base = res_base, left = res_left;
+        if (left == 0) {
+            base = __shfl_sync(FULL, res, 0);
+            left = reserve;
+        } else {
+            const unsigned ahead = __shfl_sync(FULL, res, 0);
+            for (unsigned i = lane; i < (unsigned)reserve; i += 32) list0[ahead + i] = make_entry<Entry>(-1, -1, 0, 0);
+        }
+        for (unsigned i = lane; i < left; i += 32) list0[base + i] = i < (unsigned)nbuf ? buf[i] : make_entry<Entry>(-1, -1, 0, 0);
     } else if (nbuf > 0) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
@@ -725,7 +743,7 @@ static long long n_tiles_of(int64_t W, int64_t rows) {
 }
 static long long part_cap_of(int64_t W, int64_t rows, int sms, int parts) {
     const long long ctas = (2LL * sms + parts - 1) / parts;
-    return (n_tiles_of(W, rows) + parts - 1) / parts * TILE_POS + ctas * WARPS * 32;
+    return (n_tiles_of(W, rows) + parts - 1) / parts * TILE_POS + ctas * WARPS * 2 * RESERVE_MAX;
 }
 static size_t list_bytes(int64_t W, int64_t rows, int sms, bool large) {
     return large ? (size_t)MAX_PARTS * part_cap_of(W, rows, sms, MAX_PARTS) * sizeof(int4)
@@ -842,7 +860,8 @@ static int launch_k3(K3Launch& L, int parts) {
         // every partition needs a CTA (CTAs without tiles exit at once)
         const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)L.sms * s1_per_sm),
                                                    parts);
-        s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem_all, L.s>>>(a, L.maps, tm, parts, list, part_cap, L.list_ctr,
+        s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem_all, L.s>>>(a, L.maps, tm, parts,
+                                                                  parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list, part_cap, L.list_ctr,
                                                                   L.tile_ctr);
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;
