@@ -303,11 +303,14 @@ constexpr int TILE_POS = TX * TY;  // centres per tile
 //   kernel skips those 8 gathers).
 // Either way the lists follow the strip-major tile order.
 constexpr int MAX_PARTS = 8;
+constexpr int TILE_CTRS = MAX_PARTS;  // stage-1 tile counters (partition p's CTAs use counter p)
 // List slots a stage-1 warp reserves per atomic (a multiple of 32): fewer
 // atomics on the list counter vs. the padding of each warp's last blocks
 // (measured: 64 for the single list, 128 for the partitioned lists).
 constexpr int RESERVE_SMALL = 64, RESERVE_LARGE = 128, RESERVE_MAX = 128;
-constexpr unsigned GROUP_CTRS = 8;  // rings group counters per partition
+#ifndef GROUP_CTRS
+#define GROUP_CTRS 8u  // rings group counters per partition
+#endif
 constexpr int CTR_STRIDE = 32;  // words between counters (one 128-B line each)
 template <typename E> __device__ __forceinline__ E make_entry(int x, int y, unsigned sq, unsigned sd);
 template <> __device__ __forceinline__ int4 make_entry<int4>(int x, int y, unsigned sq, unsigned sd) {
@@ -396,11 +399,15 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             // Tiles are handed out by a global counter so every CTA works near
             // the same point of the strip-major order: the L2 working set is
             // the rows in flight, not the spread of CTAs that drift apart.
-            unsigned* tile_ctr = tile_ctr_base + part * CTR_STRIDE;
+            // TILE_CTRS interleaved tile counters (counter c: tiles c, c +
+            // TILE_CTRS, ...): one address for the whole grid serialised the
+            // producers.  With partitioned lists, counter == partition.
+            const int tc = (int)(blockIdx.x % TILE_CTRS);
+            unsigned* tile_ctr = tile_ctr_base + tc * CTR_STRIDE;
             unsigned t_next = atomicAdd(tile_ctr, 1u);
             for (int it = 0;; ++it) {
                 const int s = it % STAGES;
-                const long long t = (long long)t_next * parts + part;
+                const long long t = (long long)t_next * TILE_CTRS + tc;
                 if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);  // one tile ahead: hides the atomic
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 if (t >= tm.n_tiles) {
@@ -857,9 +864,9 @@ static int launch_k3(K3Launch& L, int parts) {
     }
     if (const char* e = getenv("SS_STRIP")) tm.strip = std::max(1, std::min(tm.n_tx, atoi(e)));  // experiment hook
     {
-        // every partition needs a CTA (CTAs without tiles exit at once)
+        // every tile counter / partition needs a CTA (CTAs without tiles exit at once)
         const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)L.sms * s1_per_sm),
-                                                   parts);
+                                                   (long long)TILE_CTRS);
         s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem_all, L.s>>>(a, L.maps, tm, parts,
                                                                   parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list, part_cap, L.list_ctr,
                                                                   L.tile_ctr);
