@@ -212,6 +212,14 @@ size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes);
 int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
                      int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
                      size_t workspace_bytes, void* stream);
+/*
+ * f4 (cli.py:97-98 _mask_to_pgm): a bit-packed W x H mask (size mask or
+ * region) as one byte per pixel, 255 = kept, 0 = not -- the raster of the
+ * PGM files `starscreen screen --out-mask / --out-size-masks` writes
+ * (image_io.py:108-128 save_pgm).  d_out: H rows of W bytes.
+ */
+int ss_bits_to_bytes(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, uint8_t* d_out,
+                     void* stream);
 /* d_count += number of set bits of the W x H region mask. */
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H,
                 unsigned long long* d_count, void* stream);

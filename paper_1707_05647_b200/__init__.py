@@ -20,6 +20,7 @@ from .config import (
 )
 from .featureset import FeatureSet, RingBand, RingFeatureVector, build_feature_set
 from .image import as_gray, std_dev
+from .pgm import PgmError, load_pgm, save_pgm, save_screen_outputs, screen_stats_payload, write_json_atomic
 from .screening import (
     CandidateList,
     FlatTemplateError,
@@ -48,6 +49,12 @@ __all__ = [
     "build_feature_set",
     "as_gray",
     "std_dev",
+    "PgmError",
+    "load_pgm",
+    "save_pgm",
+    "save_screen_outputs",
+    "screen_stats_payload",
+    "write_json_atomic",
     "CandidateList",
     "FlatTemplateError",
     "PruneStats",

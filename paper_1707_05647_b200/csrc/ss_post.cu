@@ -402,6 +402,28 @@ __global__ void hdilate_all_kernel(const unsigned* V, long long words, long long
     }
 }
 
+// f4: bit-packed mask rows -> one byte per pixel, 255 kept / 0 not
+// (cli.py:97-98 _mask_to_pgm), the PGM raster.  A thread per output 16 B:
+// one 16-bit slice of a mask word, coalesced stores.
+__global__ void bits_to_bytes_kernel(const unsigned* bits, long long pitch, int W, long long H, uint8_t* out) {
+    const long long per_row = (W + 15) / 16;
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= per_row * H) return;
+    const long long y = gid / per_row, c = gid % per_row;
+    const unsigned wv = bits[y * pitch + (c >> 1)] >> ((c & 1) * 16);
+    uint8_t v[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) v[b] = ((wv >> b) & 1u) ? 255 : 0;
+    uint8_t* o = out + y * (long long)W + c * 16;
+    const long long rem = (long long)W - c * 16;
+    const int n = rem < 16 ? (int)rem : 16;
+    if (n == 16 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+        *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(v);
+    } else {
+        for (int b = 0; b < n; ++b) o[b] = v[b];
+    }
+}
+
 }  // namespace
 
 size_t compact_workspace_bytes(int64_t rows) { return (size_t)std::max<int64_t>(rows, 1) * 8; }
@@ -548,6 +570,17 @@ int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stri
     return check_launch("hdilate_all_kernel");
 }
 
+int bits_to_bytes(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, uint8_t* d_out, void* stream) {
+    if (W < 1 || H < 1 || pitch < (W + 31) / 32 || !d_bits || !d_out) {
+        set_error("bad bits_to_bytes arguments");
+        return SS_EINVAL;
+    }
+    const long long n = (W + 15) / 16 * H;
+    bits_to_bytes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_bits, pitch, (int)W, H, d_out);
+    note_launch();
+    return check_launch("bits_to_bytes_kernel");
+}
+
 int popcount(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, unsigned long long* d_count, void* stream) {
     if (W < 1 || H < 0) { set_error("bad popcount arguments"); return SS_EINVAL; }
     if (H == 0) return SS_OK;
@@ -600,5 +633,9 @@ int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t 
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, unsigned long long* d_count,
                 void* stream) {
     return ss::popcount(d_bits, mask_pitch_words, W, H, d_count, stream);
+}
+int ss_bits_to_bytes(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, uint8_t* d_out,
+                     void* stream) {
+    return ss::bits_to_bytes(d_bits, mask_pitch_words, W, H, d_out, stream);
 }
 }

@@ -216,7 +216,9 @@ class CandidateList(Sequence):
 class ScreeningResult:
     """screening.py:276-298: everything the second stage needs from the screen."""
 
-    def __init__(self, width, height, template_side, config, ladder, candidates, size_masks, region_packed, stats):
+    def __init__(self, width, height, template_side, config, ladder, candidates, size_masks, region_packed, stats,
+                 size_counts=None):
+        self._size_counts = None if size_counts is None else [int(c) for c in size_counts]
         self.width = width
         self.height = height
         self.template_side = template_side
@@ -241,6 +243,32 @@ class ScreeningResult:
         if self._region is None:
             self._region = unpack_bits(self.region_packed(), self.width)
         return self._region
+
+    def candidates_per_size(self) -> List[int]:
+        """Survivors per ladder size, in ladder order (cli.py:104-106)."""
+        if self._size_counts is None:
+            ms = self.candidates.m if len(self.candidates) else np.zeros(0, np.int32)
+            self._size_counts = [int(np.count_nonzero(ms == m)) for m in self.ladder]
+        return list(self._size_counts)
+
+    def region_pgm(self) -> np.ndarray:
+        """The kept region as a 0/255 uint8 raster (cli.py:97-98, 159-160), built on the device."""
+        from .pgm import packed_to_pgm
+
+        src = self._region_packed
+        if src is None:
+            return np.zeros((self.height, self.width), np.uint8)
+        return packed_to_pgm(src, self.width)
+
+    def size_mask_pgm(self, m: int) -> np.ndarray:
+        """One size's centre mask as a 0/255 uint8 raster (cli.py:161-163), built on the device."""
+        from .pgm import packed_to_pgm
+
+        if m not in self.ladder:
+            raise KeyError(m)
+        packed = self.size_masks._packed
+        k = self.ladder.index(m)
+        return packed_to_pgm(packed[k] if isinstance(packed, torch.Tensor) else np.asarray(packed)[k], self.width)
 
     def __repr__(self) -> str:
         return (f"ScreeningResult({self.width}x{self.height}, n={self.template_side}, ladder={self.ladder}, "
@@ -298,6 +326,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float) -> ScreeningResult
     if kept > eng.capacity:
         eng.recompact(tp, kept)
         totals = eng.totals.cpu()
+    size_counts = eng.size_counts[: len(tp.sizes)].cpu().tolist()
     rows = eng.xy[:kept].clone()
     packed = eng.masks[: len(tp.sizes)].clone()
     region = eng.region.clone() if eng.region is not None else None
@@ -312,7 +341,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float) -> ScreeningResult
     )
     cands = CandidateList(rows, kept)
     return ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, SizeMasks(tp.ladder, packed, W),
-                           region, stats)
+                           region, stats, size_counts)
 
 
 def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfig] = None,

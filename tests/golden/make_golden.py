@@ -206,11 +206,59 @@ def frozen_fixture():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def io_fixture():
+    """f4 wire formats, written by the reference's own functions: the stats
+    JSON of `starscreen screen` (cli.py:101-134, write_json_atomic
+    synth_bench.py:314-326; screen_time zeroed -- the only run-dependent
+    field), the region / size-mask PGM files (cli.py:97-98, save_pgm
+    image_io.py:108-128), and load_pgm on the header variants the reference
+    tests parse (pkg/tests/test_image_io.py:61-109)."""
+    import dataclasses
+    import tempfile
+
+    from starscreen import cli as C
+    from starscreen import image_io as IO
+    from starscreen.synth_bench import write_json_atomic
+
+    out = {}
+    cases = {name: (img, tpl, kw) for name, img, tpl, kw in screen_cases()}
+    names = ["t4_default", "t21_odd", "t22_tall"]
+    with tempfile.TemporaryDirectory() as d:
+        for name in names:
+            img, tpl, kw = cases[name]
+            res = S.screen(img, tpl, _cfg(kw))
+            res = dataclasses.replace(res, stats=dataclasses.replace(res.stats, wall_time_s=0.0))
+            payload = C._screen_stats_payload("scene.pgm", "template.pgm", res)
+            write_json_atomic(os.path.join(d, "stats.json"), payload)
+            out[f"{name}/stats_json"] = np.frombuffer(open(os.path.join(d, "stats.json"), "rb").read(), np.uint8)
+            IO.save_pgm(os.path.join(d, "region.pgm"), C._mask_to_pgm(res.region_mask))
+            out[f"{name}/region_pgm"] = np.frombuffer(open(os.path.join(d, "region.pgm"), "rb").read(), np.uint8)
+            for m in (res.ladder[0], res.ladder[-1]):
+                IO.save_pgm(os.path.join(d, "m.pgm"), C._mask_to_pgm(res.size_masks[m]))
+                out[f"{name}/mask_pgm_{m}"] = np.frombuffer(open(os.path.join(d, "m.pgm"), "rb").read(), np.uint8)
+        blobs = [b"P5 # magic\n# a comment line\n  3\t2 # dims\n255\n" + bytes(range(6)),
+                 b"P5\n2 1\n15\n" + bytes([3, 15]),
+                 b"P5\n7 3\n255\n" + bytes(range(21)),
+                 b"P2\n2 2\n255\n" + b"\x00" * 4, b"P5\n2 2\n300\n" + b"\x00" * 4, b"P5\n2 2\n0\n" + b"\x00" * 4,
+                 b"P5\n0 2\n255\n", b"P5\n2 2\n255\n\x00\x00", b"P5\n2\n", b"P5\nab 2\n255\n" + b"\x00" * 4,
+                 b"P6 junk"]
+        for i, blob in enumerate(blobs):
+            path = os.path.join(d, "in.pgm")
+            open(path, "wb").write(blob)
+            out[f"pgm_in{i}"] = np.frombuffer(blob, np.uint8)
+            try:
+                out[f"pgm_out{i}"] = IO.load_pgm(path)
+            except IO.PgmError as e:
+                out[f"pgm_err{i}"] = np.array(str(e))
+        out["pgm_n"] = np.array(len(blobs))
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
+
+
+FIXTURES = {"tables": tables_fixture, "features": features_fixture, "featuresets": featuresets_fixture,
+            "screens": screens_fixture, "report": report_fixture, "frozen": frozen_fixture, "io": io_fixture}
+
 if __name__ == "__main__":
-    tables_fixture()
-    features_fixture()
-    featuresets_fixture()
-    screens_fixture()
-    report_fixture()
-    frozen_fixture()
+    for name in (sys.argv[1:] or list(FIXTURES)):
+        FIXTURES[name]()
     print("golden fixtures written to", HERE)
