@@ -20,6 +20,7 @@ from .config import (
 )
 from .featureset import FeatureSet, RingBand, RingFeatureVector, build_feature_set
 from .image import as_gray, std_dev
+from .second_stage import MatchResult, match_candidates
 from .pgm import PgmError, load_pgm, save_pgm, save_screen_outputs, screen_stats_payload, write_json_atomic
 from .screening import (
     CandidateList,
@@ -63,4 +64,6 @@ __all__ = [
     "prune_stats",
     "screen",
     "screen_batch",
+    "MatchResult",
+    "match_candidates",
 ]

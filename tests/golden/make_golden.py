@@ -255,8 +255,42 @@ def io_fixture():
     np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
 
 
+def match_fixture():
+    """f3: the reference's match_candidates (second_stage.py:168-204) on the
+    reference's own screens -- golden screen cases and report.json scenes."""
+    from starscreen import second_stage as M
+
+    out = {}
+    names = []
+    cases = {name: (img, tpl, kw) for name, img, tpl, kw in screen_cases()}
+    jobs = [("t4_default", 10.0), ("t5_q", 10.0), ("t21_odd", 30.0), ("t14_stride3", 45.0), ("t13_single", 10.0),
+            ("t6_big_m", 10.0), ("t22_tall", 20.0)]
+    for name, step in jobs:
+        img, tpl, kw = cases[name]
+        res = S.screen(img, tpl, _cfg(kw))
+        r = M.match_candidates(img, tpl, res, angle_step=step)
+        key = f"{name}@{step:g}"
+        names.append(key)
+        out[f"{key}/step"] = np.array(step)
+        out[f"{key}/result"] = np.array([r.cx, r.cy, r.scale, r.angle, r.score], np.float64)
+    for img_idx, case_idx in ((0, 0), (3, 1), (5, 0), (2, 1)):
+        scene = make_textured_scene(320, 240, seed=600 + img_idx)
+        tpl, _ = make_case(scene, _case_seed(1, img_idx, case_idx))
+        res = S.screen(scene, tpl)
+        r = M.match_candidates(scene, tpl, res)
+        key = f"scene{img_idx}_case{case_idx}"
+        names.append(key)
+        out[f"{key}/image"] = scene
+        out[f"{key}/template"] = tpl
+        out[f"{key}/step"] = np.array(10.0)
+        out[f"{key}/result"] = np.array([r.cx, r.cy, r.scale, r.angle, r.score], np.float64)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "match.npz"), **out)
+
+
 FIXTURES = {"tables": tables_fixture, "features": features_fixture, "featuresets": featuresets_fixture,
-            "screens": screens_fixture, "report": report_fixture, "frozen": frozen_fixture, "io": io_fixture}
+            "screens": screens_fixture, "report": report_fixture, "frozen": frozen_fixture, "io": io_fixture,
+            "match": match_fixture}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(FIXTURES)):
