@@ -271,41 +271,42 @@ int ss_template_ring_features(const uint8_t* h_template, int32_t n, int32_t k, i
                               const int32_t* h_ring_n, const int32_t* h_ring_d, double* h_out);
 
 /* ── second stage (f3, second_stage.py:106-204 match_candidates) ───── */
+/* Row pitch (bytes) of the A planes of ss_match_planes for an image W wide. */
+int64_t ss_match_plane_pitch(int64_t W);
 /*
- * Probe operands of ladder size m for n_angles rotations of the n x n
- * template: resize_bilinear to m x m (image_io.py:164-178) then
- * _rotate_with_mask per angle (image_io.py:181-203) with the rotation's
- * cos / sin in d_cos / d_sin (computed on the host exactly as NumPy does).
- * Outputs int8 GEMM operands of value - 128: d_b1 (k_pad x n1, row-major):
- * column a = masked probe, column n_angles + a = support; d_b2 (k_pad x n2):
- * column a = support; padding = value 0.  d_stats[a] = (support pixels,
- * sum of the masked probe, sum of its squares).  d_base: m*m bytes scratch.
- * k_pad >= m*m, n1 >= 2*n_angles, n2 >= n_angles.
+ * The three u8 A planes of the NCC dot products (H rows of `pitch` bytes
+ * each, zero right of column W, at 0, H*pitch, 2*H*pitch of d_planes): the
+ * image, and the high / low bytes of its squares.
+ */
+int ss_match_planes(const uint8_t* d_img, int64_t W, int64_t H, uint8_t* d_planes, int64_t pitch, void* stream);
+/* Bytes of the probe fragments of ss_match_probes for size m, n_angles angles. */
+size_t ss_match_probe_bytes(int32_t m, int32_t n_angles);
+/*
+ * Probes of ladder size m for n_angles rotations of the n x n template:
+ * resize_bilinear to m x m (image_io.py:164-178), then _rotate_with_mask per
+ * angle (image_io.py:181-203) with the rotation's cos / sin in d_cos / d_sin
+ * (computed on the host exactly as NumPy does).  Writes the masked probes
+ * and supports as u8 tensor-core B fragments (groups of 40 angles) into
+ * d_bfrag (ss_match_probe_bytes), and d_stats[a] = (support pixels, sum of
+ * the masked probe, sum of its squares).  d_base: m*m bytes scratch.
  */
 int ss_match_probes(const uint8_t* d_template, int32_t n, int32_t m, int32_t n_angles, const double* d_cos,
-                    const double* d_sin, int8_t* d_b1, int32_t n1, int8_t* d_b2, int32_t n2, int32_t k_pad,
-                    long long* d_stats, uint8_t* d_base, void* stream);
+                    const double* d_sin, uint8_t* d_bfrag, long long* d_stats, uint8_t* d_base, void* stream);
+/* Partial-result rows ss_match_fused needs for `count` candidates (x 40 each). */
+int64_t ss_match_parts(int64_t count);
 /*
- * The m x m windows of candidates first .. first+count-1 of d_rows (rows of
- * row_cols int32, (cx, cy, ...)), the sliding_window_view gather of
- * second_stage.py:131-141, as int8 operands (count_pad x k_pad, rows past
- * count are zero windows): d_a1 = w - 128, d_a2 = (w^2 >> 8) - 128,
- * d_a3 = (w^2 & 255) - 128; d_rsum: per row the exact sums of w, w^2 >> 8,
- * w^2 & 255.
+ * For angle group `group` (angles 40*group ..) of the probes d_bfrag and the
+ * candidates first .. first+count-1 of d_rows (rows of row_cols int32,
+ * (cx, cy, ...), all of size m): the masked NCC scores of
+ * second_stage.py:136-152 (exact integer dot products, float64 in NumPy's op
+ * order) and, per angle, the best score and its candidate index (relative to
+ * `first`; the first candidate on equal scores, as np.argmax) into
+ * d_best_score / d_best_idx[angle].  d_part_*: ss_match_parts(count) x 40.
  */
-int ss_match_gather(const uint8_t* d_img, int64_t W, int64_t H, const int32_t* d_rows, int32_t row_cols,
-                    int64_t first, int64_t count, int64_t count_pad, int32_t m, int32_t k_pad, int8_t* d_a1,
-                    int8_t* d_a2, int8_t* d_a3, long long* d_rsum, void* stream);
-/*
- * From the int32 GEMMs d_c1 = a1 @ b1 (count x n1), d_c2 = a2 @ b2,
- * d_c3 = a3 @ b2 (count x n2): the exact dot products (offsets removed),
- * the float64 scores of second_stage.py:142-152 in NumPy's op order, and per
- * angle the best score and its candidate (base + row; the first candidate on
- * equal scores, as np.argmax) into d_best_score / d_best_idx.
- */
-int ss_match_scores(const int32_t* d_c1, int32_t n1, const int32_t* d_c2, const int32_t* d_c3, int32_t n2,
-                    const long long* d_rsum, const long long* d_stats, int64_t count, int32_t n_angles, int32_t k_pad,
-                    int64_t base, double* d_best_score, long long* d_best_idx, void* stream);
+int ss_match_fused(const uint8_t* d_planes, int64_t W, int64_t H, int64_t pitch, const int32_t* d_rows,
+                   int32_t row_cols, int64_t first, int64_t count, int32_t m, const uint8_t* d_bfrag, int32_t n_angles,
+                   int32_t group, const long long* d_stats, double* d_part_score, long long* d_part_idx,
+                   double* d_best_score, long long* d_best_idx, void* stream);
 
 #ifdef __cplusplus
 }

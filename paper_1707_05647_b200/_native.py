@@ -62,12 +62,13 @@ _SIGS = {
     "ss_region_accumulate": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
     "ss_popcount": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),
     "ss_bits_to_bytes": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),
-    "ss_match_probes": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_p, c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p,
-                                       c_p]),
-    "ss_match_gather": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_i32, c_i64, c_i64, c_i64, c_i32, c_i32, c_p, c_p,
-                                       c_p, c_p, c_p]),
-    "ss_match_scores": (ctypes.c_int, [c_p, c_i32, c_p, c_p, c_i32, c_p, c_p, c_i64, c_i32, c_i32, c_i64, c_p, c_p,
-                                       c_p]),
+    "ss_match_plane_pitch": (c_i64, [c_i64]),
+    "ss_match_planes": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_i64, c_p]),
+    "ss_match_probe_bytes": (c_sz, [c_i32, c_i32]),
+    "ss_match_probes": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "ss_match_parts": (c_i64, [c_i64]),
+    "ss_match_fused": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_i32, c_i64, c_i64, c_i32, c_p, c_i32, c_i32,
+                                      c_p, c_p, c_p, c_p, c_p, c_p]),
     "ss_feature_set_keys": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_p]),
     "ss_keys_from_features": (ctypes.c_int, [c_p, c_i32, c_i32, c_d, c_d, c_d, c_p, c_p]),
     "ss_template_features_device": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_i32, c_p, c_p]),

@@ -12,13 +12,12 @@ Per ladder size (ascending, as the reference iterates ``sorted(by_size)``):
   every angle with its support mask (image_io.py:164-203), on the device;
   the rotation's cos / sin come from NumPy, as in the reference, so the
   probes are bit-identical;
-* ``ss_match_gather`` lays the candidates' windows out as int8 GEMM operands;
-* the dot products ``W @ [P | M]`` and ``(W * W) @ M`` (second_stage.py:
-  136-150) run as int8 tensor-core GEMMs (``torch._int_mm``, cuBLASLt) on
-  value-128 offset operands -- exact integers, like the reference's float64
-  products of integer data;
-* ``ss_match_scores`` undoes the offsets and replays the reference's float64
-  score sequence op for op, reducing to the best candidate per angle.
+* ``ss_match_fused`` gathers the candidates' windows straight from the
+  image into u8 tensor-core fragments and computes ``W @ [P | M]`` and
+  ``(W * W) @ M`` (second_stage.py:136-150; W^2 as its high and low bytes)
+  with u8 x u8 -> s32 MMAs -- exact integers, like the reference's float64
+  products of integer data -- then replays the reference's float64 score
+  sequence op for op and reduces to the best candidate per angle.
 
 There is no CPU fallback.
 """
@@ -35,7 +34,7 @@ import torch
 from . import _native
 from .image import as_gray
 
-_CHUNK_BYTES = 768 << 20  # A-operand bytes per chunk of candidates (3 int8 matrices)
+_GROUP = 40  # angles per fused launch (csrc/ss_match.cu MAX_GROUP_ANGLES)
 
 
 @dataclass(frozen=True)
@@ -73,64 +72,29 @@ def _rotation_cos_sin(angles: Sequence[float]) -> Tuple[np.ndarray, np.ndarray]:
     return c, s
 
 
-class _SizeProbes:
-    """Probe operands of one ladder size (second_stage.py:124-135)."""
-
-    def __init__(self, tpl_dev: torch.Tensor, n: int, m: int, cs_dev, sn_dev, na: int, stream):
-        self.m = m
-        self.k_pad = _round_up(m * m, 16)
-        self.n1 = _round_up(2 * na, 8)
-        self.n2 = _round_up(na, 8)
-        dev = tpl_dev.device
-        self.b1 = torch.empty((self.k_pad, self.n1), dtype=torch.int8, device=dev)
-        self.b2 = torch.empty((self.k_pad, self.n2), dtype=torch.int8, device=dev)
-        self.stats = torch.empty((na, 3), dtype=torch.int64, device=dev)
-        base = torch.empty(m * m, dtype=torch.uint8, device=dev)
-        _native.check(_native.lib().ss_match_probes(
-            tpl_dev.data_ptr(), n, m, na, cs_dev.data_ptr(), sn_dev.data_ptr(), self.b1.data_ptr(), self.n1,
-            self.b2.data_ptr(), self.n2, self.k_pad, self.stats.data_ptr(), base.data_ptr(), stream), "match probes")
-
-
-def _best_of_size(img_dev: torch.Tensor, rows: torch.Tensor, first: int, count: int, probes: _SizeProbes, na: int,
-                  stream) -> Tuple[np.ndarray, np.ndarray]:
+def _best_per_angle(planes: torch.Tensor, W: int, H: int, pitch: int, tpl_dev: torch.Tensor, n: int,
+                    rows: torch.Tensor, first: int, count: int, m: int, cs_dev: torch.Tensor, sn_dev: torch.Tensor,
+                    na: int, stream) -> Tuple[np.ndarray, np.ndarray]:
     """Per angle, the best (score, candidate index within the size) over the
-    size's `count` candidates starting at row `first` of `rows`."""
-    H, W = img_dev.shape
-    dev = img_dev.device
+    size's `count` candidates starting at row `first` of `rows`
+    (second_stage.py:106-165)."""
     L = _native.lib()
-    per_cand = 3 * probes.k_pad
-    chunk = max(32, min(_round_up(count, 32), (_CHUNK_BYTES // per_cand) // 32 * 32))
-    scores, idxs = [], []
-    a1 = torch.empty((chunk, probes.k_pad), dtype=torch.int8, device=dev)
-    a2 = torch.empty_like(a1)
-    a3 = torch.empty_like(a1)
-    rsum = torch.empty((chunk, 3), dtype=torch.int64, device=dev)
-    for s in range(0, count, chunk):
-        e = min(count, s + chunk)
-        n_pad = max(32, _round_up(e - s, 32))
-        _native.check(L.ss_match_gather(img_dev.data_ptr(), W, H, rows.data_ptr(), rows.shape[1], first + s, e - s,
-                                        n_pad, probes.m, probes.k_pad, a1.data_ptr(), a2.data_ptr(), a3.data_ptr(),
-                                        rsum.data_ptr(), stream), "match gather")
-        c1 = torch._int_mm(a1[:n_pad], probes.b1)
-        c2 = torch._int_mm(a2[:n_pad], probes.b2)
-        c3 = torch._int_mm(a3[:n_pad], probes.b2)
-        bs = torch.empty(na, dtype=torch.float64, device=dev)
-        bi = torch.empty(na, dtype=torch.int64, device=dev)
-        _native.check(L.ss_match_scores(c1.data_ptr(), probes.n1, c2.data_ptr(), c3.data_ptr(), probes.n2,
-                                        rsum.data_ptr(), probes.stats.data_ptr(), e - s, na, probes.k_pad, s,
-                                        bs.data_ptr(), bi.data_ptr(), stream), "match scores")
-        scores.append(bs)
-        idxs.append(bi)
-    sc = torch.stack(scores).cpu().numpy()
-    ix = torch.stack(idxs).cpu().numpy()
-    # chunks in candidate order: per angle the highest score, first candidate on ties
-    best_s = sc[0].copy()
-    best_i = ix[0].copy()
-    for k in range(1, sc.shape[0]):
-        upd = sc[k] > best_s
-        best_s[upd] = sc[k][upd]
-        best_i[upd] = ix[k][upd]
-    return best_s, best_i
+    dev = planes.device
+    bfrag = torch.empty(int(L.ss_match_probe_bytes(m, na)), dtype=torch.uint8, device=dev)
+    stats = torch.empty((na, 3), dtype=torch.int64, device=dev)
+    base = torch.empty(m * m, dtype=torch.uint8, device=dev)
+    _native.check(L.ss_match_probes(tpl_dev.data_ptr(), n, m, na, cs_dev.data_ptr(), sn_dev.data_ptr(),
+                                    bfrag.data_ptr(), stats.data_ptr(), base.data_ptr(), stream), "match probes")
+    parts = int(L.ss_match_parts(count))
+    part_s = torch.empty((parts, _GROUP), dtype=torch.float64, device=dev)
+    part_i = torch.empty((parts, _GROUP), dtype=torch.int64, device=dev)
+    best_s = torch.empty(na, dtype=torch.float64, device=dev)
+    best_i = torch.empty(na, dtype=torch.int64, device=dev)
+    for g in range((na + _GROUP - 1) // _GROUP):
+        _native.check(L.ss_match_fused(planes.data_ptr(), W, H, pitch, rows.data_ptr(), rows.shape[1], first, count,
+                                       m, bfrag.data_ptr(), na, g, stats.data_ptr(), part_s.data_ptr(),
+                                       part_i.data_ptr(), best_s.data_ptr(), best_i.data_ptr(), stream), "match")
+    return best_s.cpu().numpy(), best_i.cpu().numpy()
 
 
 def match_candidates(image: np.ndarray, template: np.ndarray, screened, angle_step: float = 10.0,
@@ -158,15 +122,18 @@ def match_candidates(image: np.ndarray, template: np.ndarray, screened, angle_st
     cs, sn = _rotation_cos_sin(angles)
     cs_dev = torch.from_numpy(cs).to(dev)
     sn_dev = torch.from_numpy(sn).to(dev)
+    H, W = img.shape
     img_dev = torch.from_numpy(img).to(dev)
     tpl_dev = torch.from_numpy(tpl).to(dev)
+    pitch = int(_native.lib().ss_match_plane_pitch(W))
+    planes = torch.empty(3 * H * pitch, dtype=torch.uint8, device=dev)
+    _native.check(_native.lib().ss_match_planes(img_dev.data_ptr(), W, H, planes.data_ptr(), pitch, sh), "match planes")
     best: Optional[MatchResult] = None
     for k in sorted(range(len(screened.ladder)), key=lambda k: screened.ladder[k]):
         m, count, first = screened.ladder[k], int(counts[k]), int(starts[k])
         if count == 0:
             continue
-        probes = _SizeProbes(tpl_dev, n, m, cs_dev, sn_dev, na, sh)
-        top, idx = _best_of_size(img_dev, rows, first, count, probes, na, sh)
+        top, idx = _best_per_angle(planes, W, H, pitch, tpl_dev, n, rows, first, count, m, cs_dev, sn_dev, na, sh)
         # second_stage.py:153-162: angles in order, exact ties to the smallest (angle, candidate)
         best_score, best_angle, best_cand = -math.inf, 0, 0
         for a in range(na):

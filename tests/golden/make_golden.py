@@ -264,7 +264,7 @@ def match_fixture():
     names = []
     cases = {name: (img, tpl, kw) for name, img, tpl, kw in screen_cases()}
     jobs = [("t4_default", 10.0), ("t5_q", 10.0), ("t21_odd", 30.0), ("t14_stride3", 45.0), ("t13_single", 10.0),
-            ("t6_big_m", 10.0), ("t22_tall", 20.0)]
+            ("t6_big_m", 10.0), ("t22_tall", 20.0), ("t6_big_m", 5.0), ("t21_odd", 4.0)]
     for name, step in jobs:
         img, tpl, kw = cases[name]
         res = S.screen(img, tpl, _cfg(kw))
