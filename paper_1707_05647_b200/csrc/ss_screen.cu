@@ -31,8 +31,13 @@
 // box in shared memory (binary search over the sorted keys when the box is
 // too large).
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include <cuda.h>
 
@@ -757,10 +762,43 @@ static size_t list_bytes(int64_t W, int64_t rows, int sms, bool large) {
                  : (size_t)part_cap_of(W, rows, sms, 1) * sizeof(int2);
 }
 static int device_sms() {
-    int dev = 0, sms = 148;
+    static std::atomic<int> cached[64] = {};
+    int dev = 0;
     cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cached[dev].load(std::memory_order_relaxed) > 0) return cached[dev].load();
+    int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cached[dev].store(sms);
     return sms;
+}
+
+// Resident CTAs per SM of kernel `fn` at `smem` dynamic bytes.  The first use
+// of a kernel on a device raises its dynamic shared-memory limit to the
+// maximum; results are cached per (kernel, block, smem, device) -- these
+// queries cost more host time than a launch, and a ladder makes 2 per size.
+static int occupancy(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+    static std::set<std::pair<const void*, int>> raised;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(fn, threads, smem, dev);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (raised.insert({fn, dev}).second) {
+        // the opt-in limit covers static + dynamic shared memory
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fn);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    per_sm = std::max(per_sm, 1);
+    cache[key] = per_sm;
+    return per_sm;
 }
 size_t screen_workspace_bytes(int64_t W, int64_t rows) {
     const int sms = device_sms();
@@ -837,10 +875,8 @@ static int launch_k3(K3Launch& L, int parts) {
     // K3a: the mask rows are (re)initialised here; survivors are OR'ed in by K3b
     auto s1 = stage1_kernel<T, E>;
     const size_t s1_smem_all = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(a.ring[0].wm, 1) * 4;
-    int s1_per_sm = 1;
-    cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s1_per_sm, s1, (WARPS + 1) * 32, s1_smem_all);
-    s1_per_sm = std::min(std::max(s1_per_sm, 1), 2);  // part_cap_of budgets <= 2 CTAs per SM
+    const int s1_per_sm = std::min(occupancy(reinterpret_cast<const void*>(s1), (WARPS + 1) * 32, s1_smem_all),
+                                   2);  // part_cap_of budgets <= 2 CTAs per SM
     // Column strips: a SAT element is used by four centres at the corners of
     // a 2n x 2n square, so it is read from HBM once only if the rows between
     // them (vertical reuse) and the columns between them (horizontal reuse)
@@ -877,9 +913,7 @@ static int launch_k3(K3Launch& L, int parts) {
     {
         const size_t smem = (size_t)((L.bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.n_rings * QCAP * sizeof(int2);
         auto rk = rings_kernel<T, E>;
-        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, RK_WARPS * 32, smem);
+        const int per_sm = occupancy(reinterpret_cast<const void*>(rk), RK_WARPS * 32, smem);
         rk<<<(unsigned)(L.sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, L.s>>>(a, parts, list, part_cap, L.list_ctr,
                                                                                 L.group_ctr, L.bm_words);
         note_launch();

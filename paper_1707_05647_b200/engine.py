@@ -22,7 +22,8 @@ import torch
 from . import _native
 from ._native import SS_BLOB_MAX_BITMAP_WORDS, SS_MAX_RINGS
 from .config import MIN_PATCH_SIDE, ScreeningConfig, grid_count, ladder_sizes, patch_center_margins, ring_plan
-from .featureset import FeatureSet, build_feature_set, instance_descriptors, keyset_blob, template_features_device
+from .featureset import (FeatureSet, build_feature_set, instance_descriptors, keyset_blob, launch_template_features,
+                         wait_template_features)
 
 
 import os
@@ -158,7 +159,18 @@ def plan_ladder(n: int, cfg: ScreeningConfig) -> TemplatePlan:
     return tp
 
 
-def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None) -> None:
+def launch_features(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None):
+    """Start fill_keysets' GPU part early (f2 rescale features, async on
+    `stream`); pass the handle to fill_keysets.  None off the GPU path."""
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    geo = getattr(tp, "geometry", None)
+    if dev.type != "cuda" or geo is None or not geo.evaluated:
+        return None
+    return launch_template_features(template, geo.desc, dev, stream)
+
+
+def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None,
+                 pending=None) -> None:
     """The template-dependent part of prepare_template (build_feature_set,
     screening.py:222-250, for every size).
 
@@ -173,7 +185,9 @@ def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optiona
     L = len(tp.sizes)
     geo = getattr(tp, "geometry", None)
     if dev.type == "cuda" and geo is not None and geo.evaluated:
-        feats = template_features_device(template, geo.desc, dev, stream)
+        if pending is None:
+            pending = launch_template_features(template, geo.desc, dev, stream)
+        feats = wait_template_features(pending)
         nk = geo.nk
         n_r = tp.n_rings[tp.n_rings > 0]
         keys_cap = int(27 * (nk.astype(np.int64) * n_r).sum())

@@ -175,11 +175,12 @@ def instance_descriptors(ms, ring_count: int, ladder_ratio: float):
     return np.ascontiguousarray(desc), np.array(nk, np.int32)
 
 
-def template_features_device(template: np.ndarray, desc: np.ndarray, device, stream=None) -> np.ndarray:
-    """Ring features of the rescale instances `desc` (instance_descriptors) of
-    the template, from one GPU launch (f2, csrc/ss_featureset.cu) on `stream`
-    (default: the current stream), which is synchronised.  Returns
-    (n_inst, SS_MAX_RINGS, 3) float64 on the host."""
+def launch_template_features(template: np.ndarray, desc: np.ndarray, device, stream=None):
+    """Enqueue the ring features of the rescale instances `desc`
+    (instance_descriptors) of the template: one GPU launch (f2,
+    csrc/ss_featureset.cu) on `stream` (default: the current stream) and the
+    copy of the result into pinned host memory.  Returns a handle for
+    wait_template_features."""
     import torch
 
     tpl = as_gray(template)
@@ -187,7 +188,7 @@ def template_features_device(template: np.ndarray, desc: np.ndarray, device, str
     if tpl.shape[0] != tpl.shape[1]:
         raise ValueError(f"template must be square, got {tpl.shape[1]}x{tpl.shape[0]}")
     if desc.shape[0] == 0:
-        return np.zeros((0, SS_MAX_RINGS, 3))
+        return None
     dev = torch.device(device)
     stream = stream or torch.cuda.current_stream(dev)
     with torch.cuda.stream(stream):
@@ -199,8 +200,24 @@ def template_features_device(template: np.ndarray, desc: np.ndarray, device, str
             "template features")
         host = torch.empty(d_out.shape, dtype=torch.float64, pin_memory=True)
         host.copy_(d_out, non_blocking=True)
-    stream.synchronize()
+        done = torch.cuda.Event()
+        done.record(stream)
+    return host, done
+
+
+def wait_template_features(handle) -> np.ndarray:
+    """(n_inst, SS_MAX_RINGS, 3) float64 host features of a launch_template_features handle."""
+    if handle is None:
+        return np.zeros((0, SS_MAX_RINGS, 3))
+    host, done = handle
+    done.synchronize()
     return host.numpy()
+
+
+def template_features_device(template: np.ndarray, desc: np.ndarray, device, stream=None) -> np.ndarray:
+    """Ring features of the rescale instances `desc` (instance_descriptors) of
+    the template from one GPU launch (f2); (n_inst, SS_MAX_RINGS, 3) float64."""
+    return wait_template_features(launch_template_features(template, desc, device, stream))
 
 
 def build_feature_sets_device(template: np.ndarray, ms, cfg: ScreeningConfig, device) -> dict:

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from .config import MIN_PATCH_SIDE, ScreeningConfig
-from .engine import Engine, EnginePool, TemplatePlan, fill_keysets, plan_ladder, prepare_template
+from .engine import Engine, EnginePool, TemplatePlan, fill_keysets, launch_features, plan_ladder, prepare_template
 from .image import as_gray, std_dev
 
 
@@ -357,13 +357,14 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     h, w = img.shape
     start = time.perf_counter()
     eng = get_engine(w, h, device)
-    # The image side starts first (upload + K1/K2 on the current stream);
-    # the template side (f2 features on the engine's template stream, host
-    # key sets) overlaps it.
+    # The template's f2 features start first (engine's template stream), the
+    # image side (upload + K1/K2 on the current stream) overlaps them, then
+    # the host builds the key sets.
     tp = plan_ladder(tpl.shape[1], cfg)
+    pending = launch_features(tp, tpl, eng.device, eng.template_stream)
     img_dev = upload_image(img, eng.device)
     eng.build_tables(img_dev, int64=eng.needs_int64(tp))
-    fill_keysets(tp, tpl, eng.device, eng.template_stream)
+    fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
     eng.run(img_dev, tp, build=False)
     return fetch_result(eng, tp, start)
 
@@ -424,9 +425,10 @@ def screen_batch(images: Sequence[np.ndarray], templates: Sequence[np.ndarray],
         start = time.perf_counter()
         with torch.cuda.stream(pool.streams[j]):
             tp = plan_ladder(tpl.shape[1], cfg)
+            feats = launch_features(tp, tpl, eng.device, eng.template_stream)
             img_dev = upload_image(img, eng.device)
             eng.build_tables(img_dev, int64=eng.needs_int64(tp))
-            fill_keysets(tp, tpl, eng.device, eng.template_stream)
+            fill_keysets(tp, tpl, eng.device, eng.template_stream, feats)
             eng.run(img_dev, tp, build=False)
         pending[j] = (i, tp, start)
     for j in range(n):
