@@ -60,6 +60,22 @@ def dist_env():
 POOL_ENGINES = int(os.environ.get("SS_POOL_ENGINES", "4"))  # engines screening a batch's images concurrently
 
 
+BAND_CONFIGS = (2, 4)  # BASELINE.json: one large image, row bands with halo across GPUs
+
+
+class BandRunner:
+    """One rank's row band (engine with a band frame) behind EnginePool's interface."""
+
+    def __init__(self, engine):
+        self.engines = [engine]
+
+    def __len__(self):
+        return 1
+
+    def run(self, imgs, tps, **kw):
+        self.engines[0].run(imgs[0], tps[0], region=False, **kw)
+
+
 def workload_config(cfg_idx):
     import workloads as WL
 
@@ -228,7 +244,8 @@ def run_ours(args):
 
     import workloads as WL
     from paper_1707_05647_b200 import _native, screen, screen_batch
-    from paper_1707_05647_b200.engine import EnginePool, prepare_template
+    from paper_1707_05647_b200.engine import Engine, EnginePool, prepare_template
+    from paper_1707_05647_b200.sharding import plan_bands, screen_sharded
 
     rank, world, local = dist_env()
     if world > 1:
@@ -242,14 +259,27 @@ def run_ours(args):
     # Batch configs (config 3: 64 images): a step is the whole batch, images
     # dealt to ranks round-robin (strong scaling), each rank's share screened
     # by an engine pool whose engines overlap on the GPU.
+    # Row-band configs (2 and 4) on N > 1 GPUs: one image, rank r decides row
+    # band r over tables of its halo'd band (sharding.py; strong scaling);
+    # the kept region needs the neighbours' survivors, so it is not part of
+    # a band's step (screen_sharded computes it after the gather, in e2e).
     batch = wl.images > 1
-    idx = [i for i in range(wl.images) if i % world == rank] if batch else [rank]
+    banded = wl.index in BAND_CONFIGS and (world > 1 or os.environ.get("SS_BENCH_BANDS") == "1")
+    if banded and not dist.is_initialized():  # SS_BENCH_BANDS=1 on one GPU: the band path with a group of 1
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+                                device_id=dev)
+    idx = [i for i in range(wl.images) if i % world == rank] if batch else [0 if banded else rank]
     cases = [WL.make_cases(wl, images=1, first_image=i)[0] for i in idx]
     case = cases[0]
-    imgs_dev = [torch.from_numpy(c.image).to(dev) for c in cases]
     tps = [prepare_template(c.template, cfg, dev) for c in cases]
     tp = tps[0]
-    pool = EnginePool(wl.width, wl.height, dev, n=min(POOL_ENGINES, len(cases)))
+    band = plan_bands(wl.height, world, tp.ladder)[rank] if banded else None
+    if banded:
+        imgs_dev = [torch.from_numpy(np.ascontiguousarray(case.image[band.y_origin:band.y_origin + band.rows])).to(dev)]
+        pool = BandRunner(Engine(wl.width, wl.height, dev, band=(band.y_origin, band.rows, band.y_begin, band.y_end)))
+    else:
+        imgs_dev = [torch.from_numpy(c.image).to(dev) for c in cases]
+        pool = EnginePool(wl.width, wl.height, dev, n=min(POOL_ENGINES, len(cases)))
     eng = pool.engines[0]
     stream = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -400,6 +430,8 @@ def run_ours(args):
         def call():
             if batch:
                 res = screen_batch(images, templates, cfg, device=dev, engines=POOL_ENGINES)
+            elif banded:
+                res = [screen_sharded(case.image, case.template, cfg, device=dev)]
             else:
                 res = [screen(case.image, case.template, cfg, device=dev)]
             return sum(len(r.candidates.array()) for r in res)  # the survivor lists read back to the host
@@ -423,6 +455,8 @@ def run_ours(args):
                "ms_min_median_max": [1e3 * min(times), 1e3 * statistics.median(times), 1e3 * max(times)],
                "calls": len(times),
                "api": ("paper_1707_05647_b200.screen_batch(64 numpy images, templates, cfg)" if batch else
+                       "paper_1707_05647_b200.sharding.screen_sharded(numpy image, numpy template, cfg) over "
+                       f"{world} ranks" if banded else
                        "paper_1707_05647_b200.screen(numpy image, numpy template, cfg)")
                       + " + candidates read back; template feature sets included; masks stay on the device until "
                         "accessed"}
@@ -436,11 +470,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if batch else "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "scaling": "strong" if (batch or banded) else "weak", "vs_baseline": None, "dtype": "int64+f64",
             "data": "synthetic (seeded noise + shapes, SURVEY.md 8(d); template per reference protocol)",
             "config": config_json(wl, tp.ladder, world, {
                 "positions_per_step_per_gpu": positions, "survivors_per_step": survivors,
                 "per_rank_images": len(cases), "engines": len(pool),
+                "row_band": None if band is None else {"y_begin": band.y_begin, "y_end": band.y_end,
+                                                       "table_rows": band.rows},
                 "cuda_graph": bool(graph is not None)}),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -450,7 +486,7 @@ def run_ours(args):
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         }
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

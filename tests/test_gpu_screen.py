@@ -258,3 +258,27 @@ def test_screen_batch_matches_screen(cuda):
             assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
     with pytest.raises(ValueError):
         screen_batch(imgs[:2], tpls[:1], cfg)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_bands_on_device_assemble_to_full_screen(cuda, world):
+    """The multi-GPU data path (sharding.py: halo'd row bands, tables local to
+    the band, border status in global rows) run band by band on one GPU:
+    assembled, it equals the single-image screen."""
+    import workloads as WL
+    from paper_1707_05647_b200 import screen
+    from paper_1707_05647_b200.engine import prepare_template
+    from paper_1707_05647_b200.sharding import assemble, plan_bands, screen_band_device
+
+    img = WL.make_image(500, 431, seed=71, sigma=2.5, noise=2.0)
+    case = WL.make_template(img, 72, 40, (0.8, 1.3), std_threshold=10.0)
+    cfg = pcfg({"alpha": 0.5, "beta": 1.8, "ladder_ratio": 1.25, "quantizer": (6.0, 6.0, 6.0)})
+    full = screen(img, case.template, cfg)
+    tp = prepare_template(case.template, cfg, cuda)
+    parts = [screen_band_device(img, tp, b, cuda) for b in plan_bands(img.shape[0], world, tp.ladder)]
+    masks, xy, counts, tested = assemble(parts, img.shape[1], img.shape[0], tp.ladder)
+    assert tested == full.stats.patches_tested
+    assert np.array_equal(xy, full.candidates.array()[:, :2])
+    assert list(counts) == full.candidates_per_size()
+    for k, m in enumerate(full.ladder):
+        assert np.array_equal(masks[k], full.size_masks.packed(m)), m
