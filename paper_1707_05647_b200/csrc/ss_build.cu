@@ -53,12 +53,15 @@ __device__ __forceinline__ long long shfl_down64(long long v, int d) {
 __device__ __forceinline__ long long shfl_up64(long long v, int d) {
     return (long long)__shfl_up_sync(FULL, (unsigned long long)v, d);
 }
+__device__ __forceinline__ unsigned shfl_down64(unsigned v, int d) { return __shfl_down_sync(FULL, v, d); }
+__device__ __forceinline__ unsigned shfl_up64(unsigned v, int d) { return __shfl_up_sync(FULL, v, d); }
 
 __device__ __forceinline__ int64_t r_off(const BuildArgs& a, int64_t r) { return r * a.pitch; }
 
 // state pointer: band b, kind k, type (0 S, 1 FF, 2 GG)
-__device__ __forceinline__ long long* st_ptr(const BuildArgs& a, int64_t b, int k, int type) {
-    return a.state + ((b * 4 + k) * 3 + type) * a.slen;
+template <typename V>
+__device__ __forceinline__ V* st_ptr(const BuildArgs& a, int64_t b, int k, int type) {
+    return reinterpret_cast<V*>(a.state) + ((b * 4 + k) * 3 + type) * a.slen;
 }
 
 // row-prefix at group boundary g (sum over x < kGroup * g) for quantity q
@@ -71,7 +74,12 @@ __device__ __forceinline__ long long rowpre_at(const BuildArgs& a, int64_t y, in
 // kMode 0: local end state (pass 1); kMode 1: final planes (pass 3).
 // RB = rows per band; the tile owns CW plane columns plus RB+1 halo columns
 // on each side; state index of x is x + OFF.
-template <int kMode, int RB>
+// V: the recurrences' element type -- long long (exact int64 cells; writes
+// the int64 planes and, if requested, their low 32 bits) or unsigned (cells
+// mod 2^32: every operation is + - x, so the low 32 bits of the exact cells
+// follow from 32-bit arithmetic; writes the 32-bit planes only, with half the
+// registers, shuffles and band-state traffic).
+template <int kMode, int RB, typename V>
 __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     constexpr int CW = kTileCols - 2 * RB - 2;
     constexpr int OFF = RB + 1;
@@ -86,18 +94,18 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     const int64_t W = a.W;
 
     __shared__ int sTot[2][TPB / 32][4];              // warp totals of (v, xw, sq)
-    __shared__ long long sEdgeFF[2][TPB / 32][4][2];  // lane-0 FF_old[0..1] per kind
-    __shared__ long long sEdgeQ[2][TPB / 32][4];      // lane-31 GG_old[3]+P[3]
-    __shared__ long long sEdgeP[2][TPB / 32][4];      // lane-0 P[0]
+    __shared__ V sEdgeFF[2][TPB / 32][4][2];  // lane-0 FF_old[0..1] per kind
+    __shared__ V sEdgeQ[2][TPB / 32][4];      // lane-31 GG_old[3]+P[3]
+    __shared__ V sEdgeP[2][TPB / 32][4];      // lane-0 P[0]
 
-    long long S[4][COLS], FF[4][COLS], GG[4][COLS];
+    V S[4][COLS], FF[4][COLS], GG[4][COLS];
     // carry: state at row y0-1
     if (kMode == 1 && band > 0) {
         for (int k = 0; k < 4; ++k) {
-            const long long* pS = st_ptr(a, band - 1, k, 0);
-            const long long* pF = st_ptr(a, band - 1, k, 1);
-            const long long* pG = st_ptr(a, band - 1, k, 2);
-            const long long swk = pS[W - 1 + OFF];
+            const V* pS = st_ptr<V>(a, band - 1, k, 0);
+            const V* pF = st_ptr<V>(a, band - 1, k, 1);
+            const V* pG = st_ptr<V>(a, band - 1, k, 2);
+            const V swk = pS[W - 1 + OFF];
 #pragma unroll
             for (int j = 0; j < COLS; ++j) {
                 const int64_t x = xb + j;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
         const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;
         if (c >= c0 && c < c0 + CW && c < a.pitch) {
             for (int p = 0; p < 12; ++p) {
-                if (a.planes) {
+                if (sizeof(V) == 8 && a.planes) {
                     long long* dst = a.planes + p * a.plane_stride + c;
                     reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(0, 0);
                     reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(0, 0);
@@ -183,16 +191,16 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 
         // ── B: full row prefixes P for the 4 kinds ───────────────────────
         for (int w = 0; w < warp; ++w) { ev += sTot[buf][w][0]; ex += sTot[buf][w][1]; eq += sTot[buf][w][2]; }
-        long long P[4][COLS];
+        V P[4][COLS];
 #pragma unroll
         for (int j = 0; j < COLS; ++j) {
-            const long long cv = (long long)(ev + lv[j]);
-            P[0][j] = bv + cv;
-            P[1][j] = bx + (long long)(ex + lx[j]) + (XL + 1) * cv;  // (i+1) = (i-XL) + (XL+1)
-            P[2][j] = (y + 1) * P[0][j];
-            P[3][j] = bq + (long long)(eq + lq[j]);
+            const V cv = (V)(ev + lv[j]);
+            P[0][j] = (V)bv + cv;
+            P[1][j] = (V)bx + (V)(ex + lx[j]) + (V)(XL + 1) * cv;  // (i+1) = (i-XL) + (XL+1)
+            P[2][j] = (V)(y + 1) * P[0][j];
+            P[3][j] = (V)bq + (V)(eq + lq[j]);
         }
-        long long Q[4];
+        V Q[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) Q[k] = GG[k][COLS - 1] + P[k][COLS - 1];
         if (lane == 31) {
@@ -209,9 +217,9 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             // FF_new(x) = FF_old(x+1) + P(x)
-            long long nf0 = shfl_down64(FF[k][0], 1);
-            long long nf1 = shfl_down64(FF[k][1], 1);
-            long long np0 = shfl_down64(P[k][0], 1);
+            V nf0 = shfl_down64(FF[k][0], 1);
+            V nf1 = shfl_down64(FF[k][1], 1);
+            V np0 = shfl_down64(P[k][0], 1);
             if (lane == 31) {
                 if (warp + 1 < TPB / 32) {
                     nf0 = sEdgeFF[buf][warp + 1][k][0];
@@ -222,16 +230,16 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                 }
             }
             // GG_new(x) = GG_old(x-1) + P(x-1)
-            long long pq = shfl_up64(Q[k], 1);
+            V pq = shfl_up64(Q[k], 1);
             if (lane == 0) pq = (warp > 0) ? sEdgeQ[buf][warp - 1][k] : 0;
-            long long Fn[COLS], Gn[COLS];
+            V Fn[COLS], Gn[COLS];
 #pragma unroll
             for (int j = 0; j < COLS - 1; ++j) Fn[j] = FF[k][j + 1] + P[k][j];
             Fn[COLS - 1] = nf0 + P[k][COLS - 1];
             Gn[0] = pq;
 #pragma unroll
             for (int j = 1; j < COLS; ++j) Gn[j] = GG[k][j - 1] + P[k][j - 1];
-            const long long fnext = nf1 + np0;  // FF_new of the next thread's column 0
+            const V fnext = nf1 + np0;  // FF_new of the next thread's column 0
 #pragma unroll
             for (int j = 0; j < COLS; ++j) {
                 S[k][j] += P[k][j];
@@ -242,18 +250,18 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                 const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;  // plane column of j = 0
                 if (c >= c0 && c < c0 + CW && c < a.pitch) {
                     const int64_t off = r_off(a, y + 1) + c;
-                    const long long e0 = Fn[0] - Gn[0], e1 = Fn[1] - Gn[1], e2 = Fn[2] - Gn[2], e3 = Fn[3] - Gn[3];
-                    const long long o0 = Fn[1] - Gn[0], o1 = Fn[2] - Gn[1], o2 = Fn[3] - Gn[2], o3 = fnext - Gn[3];
-                    if (a.planes) {
+                    const V e0 = Fn[0] - Gn[0], e1 = Fn[1] - Gn[1], e2 = Fn[2] - Gn[2], e3 = Fn[3] - Gn[3];
+                    const V o0 = Fn[1] - Gn[0], o1 = Fn[2] - Gn[1], o2 = Fn[3] - Gn[2], o3 = fnext - Gn[3];
+                    if (sizeof(V) == 8 && a.planes) {
                         longlong2* vs = reinterpret_cast<longlong2*>(a.planes + (0 * 4 + k) * a.plane_stride + off);
                         longlong2* ve = reinterpret_cast<longlong2*>(a.planes + (1 * 4 + k) * a.plane_stride + off);
                         longlong2* vo = reinterpret_cast<longlong2*>(a.planes + (2 * 4 + k) * a.plane_stride + off);
-                        vs[0] = make_longlong2(S[k][0], S[k][1]);
-                        vs[1] = make_longlong2(S[k][2], S[k][3]);
-                        ve[0] = make_longlong2(e0, e1);
-                        ve[1] = make_longlong2(e2, e3);
-                        vo[0] = make_longlong2(o0, o1);
-                        vo[1] = make_longlong2(o2, o3);
+                        vs[0] = make_longlong2((long long)S[k][0], (long long)S[k][1]);
+                        vs[1] = make_longlong2((long long)S[k][2], (long long)S[k][3]);
+                        ve[0] = make_longlong2((long long)e0, (long long)e1);
+                        ve[1] = make_longlong2((long long)e2, (long long)e3);
+                        vo[0] = make_longlong2((long long)o0, (long long)o1);
+                        vo[1] = make_longlong2((long long)o2, (long long)o3);
                     }
                     if (a.planes32) {  // the same cells mod 2^32 (region sums are exact in 32 bits)
                         *reinterpret_cast<uint4*>(a.planes32 + (0 * 4 + k) * a.plane_stride + off) =
@@ -279,9 +287,9 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
             if (!owned) continue;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (x >= 0 && x <= W - 1) st_ptr(a, band, k, 0)[x + OFF] = S[k][j];
-                if (x >= -OFF && x <= W - 2) st_ptr(a, band, k, 1)[x + OFF] = FF[k][j];
-                if (x >= 1 && x <= W + RB) st_ptr(a, band, k, 2)[x + OFF] = GG[k][j];
+                if (x >= 0 && x <= W - 1) st_ptr<V>(a, band, k, 0)[x + OFF] = S[k][j];
+                if (x >= -OFF && x <= W - 2) st_ptr<V>(a, band, k, 1)[x + OFF] = FF[k][j];
+                if (x >= 1 && x <= W + RB) st_ptr<V>(a, band, k, 2)[x + OFF] = GG[k][j];
             }
         }
     }
@@ -330,22 +338,23 @@ __global__ void rowpre_kernel(BuildArgs a) {
 constexpr int SCAN_BATCH = 16;
 
 // Pass 2a: inclusive band states of the SAT rows (in place).
+template <typename V>
 __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
     const int OFF = RB + 1;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= 4 * a.W) return;
     const int k = (int)(gid / a.W);
     const int64_t x = gid % a.W;
-    long long acc = 0;
+    V acc = 0;
     for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
-        long long v[SCAN_BATCH];
+        V v[SCAN_BATCH];
 #pragma unroll
-        for (int j = 0; j < SCAN_BATCH; ++j) v[j] = (b0 + j < nb) ? st_ptr(a, b0 + j, k, 0)[x + OFF] : 0;
+        for (int j = 0; j < SCAN_BATCH; ++j) v[j] = (b0 + j < nb) ? st_ptr<V>(a, b0 + j, k, 0)[x + OFF] : 0;
 #pragma unroll
         for (int j = 0; j < SCAN_BATCH; ++j) {
             if (b0 + j < nb) {
                 acc += v[j];
-                st_ptr(a, b0 + j, k, 0)[x + OFF] = acc;
+                st_ptr<V>(a, b0 + j, k, 0)[x + OFF] = acc;
             }
         }
     }
@@ -354,6 +363,7 @@ __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
 // Pass 2b: inclusive FF / GG band states.  FF paths move left by RB per band
 // (clamped to S(W-1) beyond the right edge), GG paths move right (zero at
 // x <= 0).  Each stored element is read and written by exactly one thread.
+template <typename V>
 __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
     const int OFF = RB + 1;
     const int64_t W = a.W;
@@ -367,9 +377,9 @@ __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
     // FF: p0 in [-OFF, W-2 + (nb-1) RB], p = p0 - b RB; GG: p0 in [1-(nb-1)RB, W+RB], p = p0 + b RB
     const int64_t p0 = ff ? (-OFF + i) : (1 - (nb - 1) * RB + (i - nF));
     const int64_t step = ff ? -RB : RB;
-    long long acc = 0;
+    V acc = 0;
     for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
-        long long v[SCAN_BATCH];
+        V v[SCAN_BATCH];
         int kind[SCAN_BATCH];  // 0 skip/stop, 1 accumulate+store, 2 clamp (FF: acc = S(W-1); GG: acc = 0)
 #pragma unroll
         for (int j = 0; j < SCAN_BATCH; ++j) {
@@ -380,12 +390,12 @@ __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
             if (b >= nb) continue;
             if (ff) {
                 if (p < -OFF) continue;
-                if (p >= W - 1) { kind[j] = 2; v[j] = st_ptr(a, b, k, 0)[W - 1 + OFF]; }
-                else { kind[j] = 1; v[j] = st_ptr(a, b, k, 1)[p + OFF]; }
+                if (p >= W - 1) { kind[j] = 2; v[j] = st_ptr<V>(a, b, k, 0)[W - 1 + OFF]; }
+                else { kind[j] = 1; v[j] = st_ptr<V>(a, b, k, 1)[p + OFF]; }
             } else {
                 if (p > W + RB) continue;
                 if (p <= 0) { kind[j] = 2; }
-                else { kind[j] = 1; v[j] = st_ptr(a, b, k, 2)[p + OFF]; }
+                else { kind[j] = 1; v[j] = st_ptr<V>(a, b, k, 2)[p + OFF]; }
             }
         }
 #pragma unroll
@@ -395,7 +405,7 @@ __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
             } else if (kind[j] == 1) {
                 acc += v[j];
                 const int64_t p = p0 + (b0 + j) * step;
-                st_ptr(a, b0 + j, k, ff ? 1 : 2)[p + OFF] = acc;
+                st_ptr<V>(a, b0 + j, k, ff ? 1 : 2)[p + OFF] = acc;
             }
         }
     }
@@ -414,22 +424,22 @@ static size_t state_bytes(int64_t W, int64_t H) {
 
 size_t build_workspace_bytes(int64_t W, int64_t H) { return rowpre_bytes(W, H) + state_bytes(W, H); }
 
-template <int RB>
+template <int RB, typename V>
 static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
     if (nbands > 1) {
-        band_kernel<0, RB><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
+        band_kernel<0, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
         note_launch();
         if (int e = check_launch("band_kernel<local>")) return e;
         const int64_t nb = nbands - 1, W = a.W;
-        band_scan_s_kernel<<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        band_scan_s_kernel<V><<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb, RB);
         note_launch();
         if (int e = check_launch("band_scan_s_kernel")) return e;
         const int64_t per_kind = (W - 1 + (RB + 1) + (nb - 1) * RB) + (W + RB + (nb - 1) * RB);
-        band_scan_fg_kernel<<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        band_scan_fg_kernel<V><<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb, RB);
         note_launch();
         if (int e = check_launch("band_scan_fg_kernel")) return e;
     }
-    band_kernel<1, RB><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
+    band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
     note_launch();
     return check_launch("band_kernel<final>");
 }
@@ -477,10 +487,18 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
     note_launch();
     if (int e = check_launch("rowpre_kernel")) return e;
+    // exact int64 recurrences when the int64 planes are wanted, else mod 2^32
+    if (d_planes) {
+        switch (rb) {
+        case 63: return launch_bands<63, long long>(a, nbands, s);
+        case 31: return launch_bands<31, long long>(a, nbands, s);
+        default: return launch_bands<15, long long>(a, nbands, s);
+        }
+    }
     switch (rb) {
-    case 63: return launch_bands<63>(a, nbands, s);
-    case 31: return launch_bands<31>(a, nbands, s);
-    default: return launch_bands<15>(a, nbands, s);
+    case 63: return launch_bands<63, unsigned>(a, nbands, s);
+    case 31: return launch_bands<31, unsigned>(a, nbands, s);
+    default: return launch_bands<15, unsigned>(a, nbands, s);
     }
 }
 
