@@ -23,6 +23,8 @@
 //   pass 3  every tile recomputes its rows with the true carry and streams
 //           the 12 planes out with 16-byte stores.
 // All sums are exact int64 (integral.py:114,134,139).
+#include <algorithm>
+
 #include "ss_common.cuh"
 
 namespace ss {
@@ -417,9 +419,13 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 static size_t rowpre_bytes(int64_t W, int64_t H) { return align_up((size_t)H * (n_groups(W) + 1) * 3 * 8, 256); }
 static size_t state_bytes(int64_t W, int64_t H) {
-    const int rb = pick_band_rows(W, H);
-    const int64_t nb = n_bands(H, rb) - 1;
-    return nb > 0 ? align_up((size_t)nb * 12 * state_len(W, rb) * 8, 256) : 0;
+    size_t need = 0;
+    for (bool wide : {true, false}) {  // either build geometry
+        const int rb = pick_band_rows(W, H, wide);
+        const int64_t nb = n_bands(H, rb) - 1;
+        if (nb > 0) need = std::max(need, align_up((size_t)nb * 12 * state_len(W, rb) * 8, 256));
+    }
+    return need;
 }
 
 size_t build_workspace_bytes(int64_t W, int64_t H) { return rowpre_bytes(W, H) + state_bytes(W, H); }
@@ -467,7 +473,7 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         return SS_EINVAL;
     }
     cudaStream_t s = as_stream(stream);
-    const int rb = pick_band_rows(W, H);
+    const int rb = pick_band_rows(W, H, d_planes != nullptr);
     BuildArgs a;
     a.img = d_img;
     a.W = W;

@@ -24,7 +24,11 @@ constexpr int kBuildThreads = 128;
 constexpr int kTileCols = 512;
 constexpr int kGroup = 16;  // row-prefix granularity (columns)
 inline int chunk_cols(int rb) { return kTileCols - 2 * rb - 2; }
-inline int pick_band_rows(int64_t W, int64_t H) {
+// wide: the exact int64 build (3 resident CTAs per SM) wants >= 6 tiles per
+// SM; the 32-bit build (4 resident, and its band scan is the serial part)
+// does better with taller bands down to 2 tiles per SM (measured: config 1
+// 31-row bands 0.974 vs 1.003 ms per step).
+inline int pick_band_rows(int64_t W, int64_t H, bool wide = true) {
     // test hook: SS_BAND_ROWS=15|31|63 forces a geometry (tests cover all three)
     if (const char* e = getenv("SS_BAND_ROWS")) {
         const int v = atoi(e);
@@ -33,7 +37,7 @@ inline int pick_band_rows(int64_t W, int64_t H) {
     const int cand[3] = {63, 31, 15};
     for (int rb : cand) {
         const int64_t tiles = ((H + rb - 1) / rb) * ((W + 1 + chunk_cols(rb) - 1) / chunk_cols(rb));
-        if (tiles >= 148 * 6) return rb;
+        if (tiles >= 148 * (wide ? 6 : 2)) return rb;
     }
     return 15;
 }
