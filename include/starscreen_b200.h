@@ -150,6 +150,13 @@ int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, uns
  * size_stride_words, row counts at d_row_counts + k * row_counts_stride.
  * d_workspaces[i] (ss_screen_workspace_bytes each) belongs to streams[i].
  * flags bit 0: screen every size from the int64 planes (test hook).
+ * flags bit 1: fused ladder -- the sizes that share a plane width are
+ * screened in lock-step (ss_ladder_screen.cu: two launches per row band, each
+ * plane row read from HBM about once per band instead of once per size), all
+ * on streams[0] with d_workspaces[0], whose workspace_bytes should be
+ * ss_ladder_workspace_bytes(W, y_end - y_begin, n_sizes) (a smaller one
+ * means more row bands, or per-size screening when it cannot hold one).
+ * Same results as the per-size path.
  */
 int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
                      int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride,
@@ -159,6 +166,11 @@ int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_
                      int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
                      int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags, int32_t n_streams,
                      void* const* streams, void* const* d_workspaces, size_t workspace_bytes);
+
+/* Workspace bytes for the fused ladder (flags bit 1) of n_sizes sizes over
+ * `rows` decided rows: one row band of at most 4 GiB of candidate list, and
+ * at least ss_screen_workspace_bytes (the per-size fallback shares it). */
+size_t ss_ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes);
 
 /* screening.py:505-510: sizes below MIN_PATCH_SIDE keep every grid centre. */
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,

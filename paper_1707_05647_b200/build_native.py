@@ -27,6 +27,7 @@ SOURCES = {
     "ss_post.cu": [],
     "ss_featureset.cu": ["-fmad=false"],
     "ss_ladder.cpp": [],
+    "ss_ladder_screen.cu": ["-fmad=false"],
     "ss_match.cu": ["-fmad=false"],
 }
 

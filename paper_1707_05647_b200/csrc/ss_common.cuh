@@ -55,6 +55,9 @@ inline bool overflow_guard_fails(int64_t W, int64_t H) {
     return b >= ((__int128)1 << 62);
 }
 
+// internal status: the fused ladder declined a group (nothing enqueued; screen per size)
+constexpr int SS_DECLINED = -1000;
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int check_launch(const char* what) {

@@ -8,6 +8,16 @@
 
 #include "ss_common.cuh"
 
+namespace ss {
+int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
+                        int64_t y_begin, int64_t y_end, int32_t stride, int n, const int* ks, const int32_t* h_m,
+                        const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
+                        const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
+                        double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
+                        uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
+                        size_t ws_bytes, cudaStream_t s);
+}  // namespace ss
+
 extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
                                 int64_t plane_pitch, int64_t W, int64_t H, int64_t y_origin, int64_t y_begin,
                                 int64_t y_end, int32_t stride, int32_t n_sizes, const int32_t* h_m,
@@ -24,6 +34,59 @@ extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_plane
         return SS_EINVAL;
     }
     const bool int64_only = (flags & 1) != 0;
+    if (flags & 2) {
+        if (w != W) {
+            ss::set_error("row-band tables must span the full width (w == W)");
+            return SS_EINVAL;
+        }
+        // fused ladder (ss_ladder_screen.cu): all sizes of one plane width in
+        // lock-step on streams[0]; m < 8 sizes keep their grid; a group the
+        // fused path declines is screened size by size on the same stream
+        void* st = streams[0];
+        std::vector<int> g32, g64;
+        for (int32_t k = 0; k < n_sizes; ++k) {
+            if (h_m[k] < 8 || h_n_rings[k] == 0) {
+                uint32_t* mask = d_masks + (size_t)k * (size_t)size_stride_words;
+                uint32_t* rc = d_row_counts + (size_t)k * (size_t)row_counts_stride;
+                if (int e = ss_fill_grid(W, y_begin, y_end, stride, mask, mask_pitch_words, rc, st)) return e;
+                continue;
+            }
+            const bool fits = !int64_only && d_planes32 &&
+                              ss_screen_fits32(h_n_rings[k], h_ring_n + (size_t)k * SS_MAX_RINGS,
+                                               h_ring_d + (size_t)k * SS_MAX_RINGS);
+            (fits ? g32 : g64).push_back(k);
+        }
+        for (int g = 0; g < 2; ++g) {
+            const std::vector<int>& ks = g == 0 ? g32 : g64;
+            if (ks.empty()) continue;
+            const void* planes = g == 0 ? static_cast<const void*>(d_planes32) : static_cast<const void*>(d_planes);
+            if (!planes) {
+                ss::set_error("ladder needs the int64 planes (ring sums exceed 32 bits)");
+                return SS_EINVAL;
+            }
+            int e = ss::screen_ladder_fused(planes, g == 0 ? 4 : 8, h, plane_pitch, W, H, y_origin, y_begin, y_end,
+                                            stride, (int)ks.size(), ks.data(), h_m, h_n_rings, h_ring_n, h_ring_d,
+                                            d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad, d_masks,
+                                            mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,
+                                            d_stage_counts, d_workspaces[0], workspace_bytes, ss::as_stream(st));
+            if (e == ss::SS_DECLINED) {
+                for (int k : ks) {
+                    const int32_t* rn = h_ring_n + (size_t)k * SS_MAX_RINGS;
+                    const int32_t* rd = h_ring_d + (size_t)k * SS_MAX_RINGS;
+                    e = ss_screen_size(g == 0 ? nullptr : d_planes, g == 0 ? d_planes32 : nullptr, w, h, plane_pitch,
+                                       W, H, y_origin, y_begin, y_end, h_m[k], stride, h_n_rings[k], rn, rd,
+                                       d_blobs + h_blob_off[k], h_blobs + h_blob_off[k], q_mean, q_std, q_grad,
+                                       d_masks + (size_t)k * (size_t)size_stride_words, mask_pitch_words,
+                                       d_row_counts + (size_t)k * (size_t)row_counts_stride, d_stage_counts,
+                                       d_workspaces[0], workspace_bytes, st);
+                    if (e) return e;
+                }
+            } else if (e) {
+                return e;
+            }
+        }
+        return SS_OK;
+    }
     cudaStream_t main = ss::as_stream(streams[0]);
     const int n_side = n_streams - 1;
     std::vector<cudaEvent_t> events;

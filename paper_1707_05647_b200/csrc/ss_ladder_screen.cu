@@ -1,0 +1,611 @@
+// ss_ladder_screen.cu -- K3 for a whole ladder in lock-step (fused sizes).
+//
+// The per-size screen (ss_screen.cu) reads every plane once per ladder size:
+// a 9-size ladder streams the 12 planes from HBM nine times, in 18 launches.
+// Here all sizes that share a plane width advance through the image
+// together, in two launches per row band:
+//   * ladder_stage1_kernel -- the stage-1 tile space is (strip, tile row,
+//     size, tile column): every size's tiles of one 16-row block are handed
+//     out back to back, so the ring-0 PLAIN corner boxes of all sizes come
+//     from the same rows while they sit in L2;
+//   * ladder_rings_kernel -- consumes the single candidate list in that
+//     order; each entry carries its size (y | size << TAG_SHIFT), each lane
+//     reads its size's ring parameters from shared memory, and deeper rings
+//     go through the same per-warp queues as in the per-size kernel.
+// A plane row is therefore fetched from HBM about once per row band instead
+// of once per size.  The decisions are the per-size kernels' (same device
+// helpers, same fp64 op order): only the order of work changes.
+//
+// Replaces, for all sizes of screen()'s ladder loop at once (screening.py:
+// 502-520), the per-size _scan_size (screening.py:418-471).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ss_screen_dev.cuh"
+
+namespace ss {
+namespace {
+
+constexpr int FMAX_SIZES = SS_MAX_SIZES;
+constexpr int FMAX_RINGS = 104;  // rings over all fused sizes (kernel parameters <= 32 KB)
+constexpr int TAG_SHIFT = 24;    // list entry .y = row | size << TAG_SHIFT
+constexpr int YMASK = (1 << TAG_SHIFT) - 1;
+constexpr int S1_BITS_WORDS = 4096;  // stage-1 mean-projection bits of all sizes
+
+struct SizeDev {
+    unsigned* mask;        // this size's mask; row 0 is global row mask_y0
+    unsigned* row_counts;  // per mask row
+    int lo, hi, n_rings, ring0;
+    int bm1, wm1, bsrc1;  // stage-1 mean bits: smem word offset (-1: binary search), words, blob u32 index
+    int pad;
+};
+
+struct FusedArgs {
+    const void* planes;  // 12 planes of T
+    long long pitch, ps;
+    int W, H, y_origin, y_begin, y_end, stride;  // [y_begin, y_end): rows decided by this pass
+    int mask_y0;
+    int n_sizes, n_rings, max_levels, bm_words, bm1_words;
+    double qm, qs, qg, rqm, rqs, rqg;
+    const long long* blob;  // all sizes' key blobs (offsets in RingDev rebased)
+    long long mask_pitch;
+    unsigned long long* stage_counts;
+    SizeDev size[FMAX_SIZES];
+    RingDev ring[FMAX_RINGS];
+};
+static_assert(sizeof(FusedArgs) <= 32000, "fused ladder parameters exceed the kernel parameter limit");
+static_assert(sizeof(RingDev) % 4 == 0, "RingDev is copied to shared memory by words");
+
+struct TileMapF {
+    int n_tx, n_ty, strip, n_sizes;
+    long long n_tiles;  // n_tx * n_ty * n_sizes
+};
+
+// strip-major; inside a strip: tile row, then size, then tile column
+__device__ __forceinline__ void tile_coords_f(const TileMapF& t, long long idx, int& tx, int& ty, int& s) {
+    const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty * (unsigned)t.n_sizes;
+    const unsigned i = (unsigned)idx;
+    const unsigned st = i / per_strip;
+    const int s0 = (int)(st * (unsigned)t.strip);
+    const unsigned width = (unsigned)min(t.strip, t.n_tx - s0);
+    const unsigned r = i - st * per_strip;
+    const unsigned span = width * (unsigned)t.n_sizes;
+    const unsigned q = r / span;
+    const unsigned rem = r - q * span;
+    const unsigned sz = rem / width;
+    ty = (int)q;
+    s = (int)sz;
+    tx = s0 + (int)(rem - sz * width);
+}
+
+__device__ __forceinline__ bool member_m1(const FusedArgs& a, const SizeDev& S, const RingDev& R, const unsigned* sb,
+                                          int cm) {
+    if (S.bm1 >= 0) {
+        const unsigned i = (unsigned)(cm - R.cm_lo);
+        return i < (unsigned)R.cm_n && bit(sb + S.bm1, (int)i);
+    }
+    return bsearch_eq(a.blob + R.off_m, R.n_m, cm);
+}
+
+// Stage 1 of every fused size: border keeps into the masks, ring-0 mean cell
+// from TMA-staged PLAIN corner boxes, mean-projection passers appended to the
+// candidate list tagged with their size.  Persistent CTAs; warp WARPS is the
+// producer.  Same pipeline as stage1_kernel (ss_screen.cu).
+template <typename T>
+__global__ void __launch_bounds__((WARPS + 1) * 32, 1)
+    ladder_stage1_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ TmaMaps maps, const TileMapF tm,
+                         int parts, int reserve, int2* list_base, long long part_cap, unsigned* list_ctr,
+                         unsigned* tile_ctr_base) {
+    using G = Geo<T>;
+    constexpr int STAGES = G::STAGES;
+    extern __shared__ __align__(128) unsigned char dsmem[];
+    unsigned char* stage_buf = dsmem;
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    __shared__ int4 tile_info[STAGES];  // (tx, ty, size) of the tile in each stage
+    __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
+    {
+        const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
+        for (int s = 0; s < a.n_sizes; ++s) {
+            const SizeDev& S = a.size[s];
+            if (S.bm1 < 0) continue;
+            for (int i = threadIdx.x; i < S.wm1; i += blockDim.x)
+                sbits[S.bm1 + i] = S.bsrc1 >= 0 ? __ldg(blob32 + S.bsrc1 + i) : 0u;
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = (int)(blockIdx.x % parts);
+
+    if (warp == WARPS) {
+        if (lane == 0) {
+            const int tc = (int)(blockIdx.x % TILE_CTRS);
+            unsigned* tile_ctr = tile_ctr_base + tc * CTR_STRIDE;
+            unsigned t_next = atomicAdd(tile_ctr, 1u);
+            for (int it = 0;; ++it) {
+                const int s = it % STAGES;
+                const long long t = (long long)t_next * TILE_CTRS + tc;
+                if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);
+                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+                if (t >= tm.n_tiles) {
+                    tile_info[s] = make_int4(-1, -1, -1, 0);
+                    mbar_arrive(&full_bar[s]);
+                    break;
+                }
+                int tx, ty, sz;
+                tile_coords_f(tm, t, tx, ty, sz);
+                tile_info[s] = make_int4(tx, ty, sz, 0);
+                const RingDev& R0 = a.ring[a.size[sz].ring0];
+                const int x0 = tx * TX;
+                const int cy0 = a.y_begin + ty * TY - a.y_origin;
+                unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
+                mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
+                const int n = R0.n, d = R0.d;
+                tma_load_2d(dst + 0 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 1 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 2 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 3 * G::BOX_BYTES, &maps.sat, G::floor_al(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 4 * G::BOX_BYTES, &maps.e, G::floor_al(x0 + 1), cy0 + d + 1, &full_bar[s]);
+                tma_load_2d(dst + 5 * G::BOX_BYTES, &maps.e, G::floor_al(x0 + 1), cy0 - d, &full_bar[s]);
+                tma_load_2d(dst + 6 * G::BOX_BYTES, &maps.o, G::floor_al(x0 - d), cy0, &full_bar[s]);
+                tma_load_2d(dst + 7 * G::BOX_BYTES, &maps.o, G::floor_al(x0 + d + 1), cy0, &full_bar[s]);
+            }
+        }
+        return;
+    }
+
+    const unsigned lt = (1u << lane) - 1u;
+    int2* list0 = list_base + part * part_cap;
+    unsigned* count0 = list_ctr + part * CTR_STRIDE;
+    int2* buf = cand_buf[warp];
+    int nbuf = 0;
+    unsigned res = 0;
+    bool have_res = false;
+    unsigned res_base = 0, res_left = 0;
+    unsigned long long n_int = 0, n_pass = 0;
+    const bool unit_stride = a.stride == 1;
+    for (int it = 0;; ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        const int4 ti = tile_info[s];
+        if (ti.x < 0) break;
+        const int tx = ti.x, ty = ti.y, sz = ti.z;
+        const SizeDev& S = a.size[sz];
+        const RingDev& R0 = a.ring[S.ring0];
+        const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d), po1 = G::rem(R0.d + 1);
+        const int y = a.y_begin + ty * TY + warp;
+        const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
+        T s1q[CPW], s1d[CPW];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const T* b = box + 32 * c;
+            constexpr int E = G::BOX_ELEMS;
+            s1q[c] = (T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]);
+            s1d[c] = (T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        if (y >= a.y_end) continue;
+        const int ylo = S.lo, yhi = a.H - 1 - S.hi, xlo = S.lo, xhi = a.W - 1 - S.hi;
+        const bool row_grid = unit_stride || (y % a.stride) == 0;
+        const bool row_int = row_grid && y >= ylo && y <= yhi;
+        unsigned* mrow = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
+        const int tag = y | (sz << TAG_SHIFT);
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const int x = tx * TX + 32 * c + lane;
+            const bool on_grid = row_grid && x < a.W && (unit_stride || (x % a.stride) == 0);
+            const bool interior = row_int && on_grid && x >= xlo && x <= xhi;
+            const unsigned border = __ballot_sync(FULL, on_grid && !interior);
+            const int word = tx * CPW + c;
+            if (lane == 0 && word * 32 < a.W) mrow[word] = border;
+            bool pass = false;
+            if (interior) pass = member_m1(a, S, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
+            const unsigned pb = __ballot_sync(FULL, pass);
+            n_int += __popc(__ballot_sync(FULL, interior));
+            n_pass += __popc(pb);
+            if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, tag);
+            nbuf += __popc(pb);
+        }
+        while (nbuf >= 32) {
+            __syncwarp();
+            if (res_left == 0) {
+                if (!have_res && lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                res_base = __shfl_sync(FULL, res, 0);
+                res_left = reserve;
+                if (lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                have_res = true;
+            }
+            list0[res_base + lane] = buf[nbuf - 32 + lane];
+            res_base += 32;
+            res_left -= 32;
+            nbuf -= 32;
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    if (have_res) {
+        unsigned base = res_base, left = res_left;
+        if (left == 0) {
+            base = __shfl_sync(FULL, res, 0);
+            left = reserve;
+        } else {
+            const unsigned ahead = __shfl_sync(FULL, res, 0);
+            for (unsigned i = lane; i < (unsigned)reserve; i += 32) list0[ahead + i] = make_int2(-1, -1);
+        }
+        for (unsigned i = lane; i < left; i += 32) list0[base + i] = i < (unsigned)nbuf ? buf[i] : make_int2(-1, -1);
+    } else if (nbuf > 0) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
+        base = __shfl_sync(FULL, base, 0);
+        if (lane < nbuf) list0[base + lane] = buf[lane];
+    }
+    if (a.stage_counts && lane == 0) {
+        atomicAdd(a.stage_counts + 0, n_int);
+        atomicAdd(a.stage_counts + 1, n_pass);
+    }
+}
+
+struct SizeSm {
+    unsigned* mask;
+    unsigned* row_counts;
+    int ring0, n_rings;
+};
+
+// Ring `level` of ring parameters R at table-local centre (x, cy).
+template <typename T>
+__device__ __forceinline__ bool eval_ring_f(const FusedArgs& a, const RingDev& R, const unsigned* sbits, int level,
+                                            int x, int cy) {
+    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + x;
+    Corners<T> c0, c2, cxk, cyk;
+    load_corners(a, R, pc, 0, c0);
+    load_corners(a, R, pc, 3, c2);
+    load_corners(a, R, pc, 1, cxk);
+    load_corners(a, R, pc, 2, cyk);
+    const Stage1 s = stage1_from(a, R, unsigned_sum(sq_of(c0)), unsigned_sum(di_of(c0)));
+    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, x, cy, s, c2, cxk, cyk);
+}
+
+// Every ring of every fused size over the stage-1 list (see rings_kernel in
+// ss_screen.cu for the batching / queue scheme); lanes of one batch may
+// belong to different sizes: each reads its size's ring from shared memory.
+template <typename T>
+__global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB)
+    ladder_rings_kernel(const __grid_constant__ FusedArgs a, int parts, const int2* list_base, long long part_cap,
+                        const unsigned* list_ctr, unsigned* group_ctr) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    RingDev* sring = reinterpret_cast<RingDev*>(rsm);
+    SizeSm* ssize = reinterpret_cast<SizeSm*>(rsm + (size_t)a.n_rings * sizeof(RingDev));
+    unsigned* sbits = reinterpret_cast<unsigned*>(ssize + a.n_sizes);
+    __shared__ int qcnt[RK_WARPS][SS_MAX_RINGS];
+    {
+        const int* src = reinterpret_cast<const int*>(a.ring);
+        int* dst = reinterpret_cast<int*>(sring);
+        const int words = a.n_rings * (int)(sizeof(RingDev) / 4);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+        for (int s = threadIdx.x; s < a.n_sizes; s += blockDim.x)
+            ssize[s] = SizeSm{a.size[s].mask, a.size[s].row_counts, a.size[s].ring0, a.size[s].n_rings};
+        const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
+        for (int r = 0; r < a.n_rings; ++r) {
+            const RingDev& R = a.ring[r];
+            if (R.bm < 0) continue;
+            for (int i = threadIdx.x; i < R.bwords; i += blockDim.x)
+                sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
+        }
+    }
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int levels = a.max_levels;
+    int2* queues = reinterpret_cast<int2*>(sbits + ((a.bm_words + 1) & ~1)) + (size_t)warp * levels * QCAP;
+    if (lane < SS_MAX_RINGS) qcnt[warp][lane] = 0;
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned long long n_pass0 = 0, n_surv = 0;
+    constexpr unsigned RG = RINGS_GROUP;
+    const unsigned wid = blockIdx.x * RK_WARPS + warp;
+    int q = (int)(wid % parts), visited = 1;
+    const unsigned gc = (wid / parts) % GROUP_CTRS;
+    unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
+    const int2* in = list_base + q * part_cap;
+    unsigned g_raw = 0;
+    if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+    unsigned cur = 0, k = 0;
+    bool have_input = true;
+    auto grab = [&]() {
+        for (;;) {
+            cur = (__shfl_sync(FULL, g_raw, 0) * GROUP_CTRS + gc) * RG;
+            if (cur < cnt_q) {
+                if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+                return;
+            }
+            if (visited == parts) {
+                have_input = false;
+                return;
+            }
+            ++visited;
+            q = q + 1 == parts ? 0 : q + 1;
+            cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
+            in = list_base + q * part_cap;
+            if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+        }
+    };
+    auto fetch = [&]() -> int2 {
+        const unsigned slot = cur + 32 * k + lane;
+        return (have_input && slot < cnt_q) ? in[slot] : make_int2(-1, -1);
+    };
+    grab();
+    int2 next = fetch();
+    for (;;) {
+        int level = -1;
+        for (int l = levels - 1; l >= 1; --l)
+            if (qcnt[warp][l] >= 32) { level = l; break; }
+        int2 e;
+        if (level < 0 && have_input) {
+            level = 0;
+            e = next;
+            if (++k == RG / 32 || cur + 32 * k >= cnt_q) {
+                k = 0;
+                grab();
+            }
+            next = fetch();
+        } else {
+            if (level < 0) {
+                for (int l = levels - 1; l >= 1; --l)
+                    if (qcnt[warp][l] > 0) { level = l; break; }
+                if (level < 0) break;
+            }
+            const int c = qcnt[warp][level], take = min(c, 32);
+            const int2* qq = queues + level * QCAP;
+            e = ((int)lane < take) ? qq[c - take + lane] : make_int2(-1, -1);
+            __syncwarp();
+            if (lane == 0) qcnt[warp][level] = c - take;
+            __syncwarp();
+        }
+        const bool valid = e.x >= 0;
+        const int sz = valid ? (e.y >> TAG_SHIFT) : 0, y = e.y & YMASK;
+        const SizeSm S = ssize[sz];
+        const bool pass = valid && eval_ring_f<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin);
+        const bool last = level + 1 == S.n_rings;
+        const unsigned pb = __ballot_sync(FULL, pass);
+        if (level == 0) n_pass0 += __popc(pb);
+        const unsigned sb = __ballot_sync(FULL, pass && last);
+        n_surv += __popc(sb);
+        if (pass && last) {
+            const long long row = y - a.mask_y0;
+            atomicOr(S.mask + row * a.mask_pitch + (e.x >> 5), 1u << (e.x & 31));
+            atomicAdd(S.row_counts + row, 1u);
+        }
+        const unsigned qb = pb & ~sb;
+        if (qb) {
+            const int c = qcnt[warp][level + 1];
+            if (pass && !last) queues[(level + 1) * QCAP + c + __popc(qb & lt)] = e;
+            __syncwarp();
+            if (lane == 0) qcnt[warp][level + 1] = c + __popc(qb);
+            __syncwarp();
+        }
+    }
+    if (a.stage_counts && lane == 0) {
+        if (n_pass0) atomicAdd(a.stage_counts + 2, n_pass0);
+        if (n_surv) atomicAdd(a.stage_counts + 3, n_surv);
+    }
+}
+
+constexpr size_t FCTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
+constexpr long long FUSED_LARGE_TILES = 32768;  // partitioned lists from this many tiles per pass
+constexpr size_t FUSED_WS_CAP = (size_t)4 << 30;  // ss_ladder_workspace_bytes: row bands beyond this
+
+long long tiles_of(int64_t W, int64_t rows) {
+    return ((std::max<int64_t>(W, 1) + TX - 1) / TX) * ((std::max<int64_t>(rows, 1) + TY - 1) / TY);
+}
+int parts_for(int64_t W, int64_t rows, int n_sizes) {
+    return tiles_of(W, rows) * n_sizes >= FUSED_LARGE_TILES ? MAX_PARTS : 1;
+}
+long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int parts) {
+    const long long ctas = (2LL * sms + parts - 1) / parts;
+    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * TILE_POS + ctas * WARPS * 2 * RESERVE_MAX;
+}
+size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms) {
+    const int parts = parts_for(W, rows, n_sizes);
+    return FCTR_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * sizeof(int2);
+}
+
+}  // namespace
+
+size_t screen_workspace_bytes(int64_t W, int64_t rows);  // ss_screen.cu
+
+// Workspace of the fused ladder for `n_sizes` sizes: one row band up to
+// FUSED_WS_CAP (taller images run in several bands), and never less than the
+// per-size screen needs (the fallback shares it).
+size_t ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
+    const int sms = device_sms();
+    const int64_t S = std::max<int32_t>(n_sizes, 1);
+    int64_t band = std::max<int64_t>(rows, 1);
+    while (band > 4 * TY && fused_ws_bytes(W, band, (int)S, sms) > FUSED_WS_CAP) band = (band / 2 + TY - 1) / TY * TY;
+    return std::max(fused_ws_bytes(W, band, (int)S, sms), screen_workspace_bytes(W, std::max<int64_t>(rows, 1)));
+}
+
+// K3 for the sizes ks[0..n) of a ladder, all screened from planes of one
+// width (eb = 4: 32-bit cells, 8: int64), in row bands of as many rows as the
+// workspace holds.  Returns SS_DECLINED (nothing enqueued) when the sizes do
+// not fit the fused parameter block or the workspace is too small for a
+// useful band; the caller then screens them one by one.
+int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
+                        int64_t y_begin, int64_t y_end, int32_t stride, int n, const int* ks, const int32_t* h_m,
+                        const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
+                        const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
+                        double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
+                        uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
+                        size_t ws_bytes, cudaStream_t s) {
+    if (n < 1 || n > FMAX_SIZES || H >= (1LL << TAG_SHIFT) || W > (1 << 30) || stride < 1) return SS_DECLINED;
+    if (pitch != plane_pitch(W)) { set_error("plane pitch mismatch"); return SS_EINVAL; }
+    if (mask_pitch < (W + 31) / 32) { set_error("mask pitch too small"); return SS_EINVAL; }
+    if (y_begin < 0 || y_end > H || y_begin > y_end || y_origin < 0 || y_origin + h > H) {
+        set_error("bad row range");
+        return SS_EINVAL;
+    }
+    const int64_t rows = y_end - y_begin;
+    if (rows == 0) return SS_OK;
+    std::vector<unsigned char> hostbuf(sizeof(FusedArgs), 0);
+    FusedArgs& a = *reinterpret_cast<FusedArgs*>(hostbuf.data());
+    a.planes = planes;
+    a.pitch = pitch;
+    a.ps = (h + 1) * pitch;
+    a.W = (int)W;
+    a.H = (int)H;
+    a.y_origin = (int)y_origin;
+    a.stride = stride;
+    a.mask_y0 = (int)y_begin;
+    a.n_sizes = n;
+    a.qm = qm;
+    a.qs = qs;
+    a.qg = qg;
+    a.rqm = 1.0 / qm;
+    a.rqs = 1.0 / qs;
+    a.rqg = 1.0 / qg;
+    a.blob = reinterpret_cast<const long long*>(d_blobs);
+    a.mask_pitch = mask_pitch;
+    a.stage_counts = d_stage_counts;
+    int n_rings = 0, bm_words = 0, bm1 = 0, max_m = 0;
+    for (int j = 0; j < n; ++j) {
+        const int k = ks[j], m = h_m[k], nr = h_n_rings[k];
+        const int64_t* hb = h_blobs + h_blob_off[k];
+        if (m < 8 || nr < 1 || nr > SS_MAX_RINGS || hb[0] != nr) {
+            set_error("bad fused ladder size %d (m=%d)", k, m);
+            return SS_EINVAL;
+        }
+        if (n_rings + nr > FMAX_RINGS) return SS_DECLINED;
+        const int lo = (m - 1) / 2, hi = m / 2;
+        const int64_t ylo = std::max<int64_t>(y_begin, lo), yhi = std::min<int64_t>(y_end - 1, H - 1 - hi);
+        if (ylo <= yhi && (ylo - lo < y_origin || yhi + hi > y_origin + h - 1)) {
+            set_error("table band [%lld, %lld) does not cover rows [%lld, %lld] with margins", (long long)y_origin,
+                      (long long)(y_origin + h), (long long)ylo, (long long)yhi);
+            return SS_EINVAL;
+        }
+        if ((int64_t)(m / 2 + 2) * pitch + m > (int64_t)INT32_MAX) {
+            set_error("patch offsets exceed 32 bits");
+            return SS_EINVAL;
+        }
+        SizeDev& S = a.size[j];
+        S.mask = d_masks + (size_t)k * (size_t)size_stride;
+        S.row_counts = d_row_counts + (size_t)k * (size_t)rc_stride;
+        S.lo = lo;
+        S.hi = hi;
+        S.n_rings = nr;
+        S.ring0 = n_rings;
+        for (int r = 0; r < nr; ++r)
+            if (int e = fill_ring(a.ring[n_rings + r], h_ring_n[(size_t)k * SS_MAX_RINGS + r],
+                                  h_ring_d[(size_t)k * SS_MAX_RINGS + r], m, pitch, qm, hb + 1 + SS_BLOB_HDR * r,
+                                  h_blob_off[k], bm_words, SMEM_BITMAP_WORDS))
+                return e;
+        // stage 1's copy of ring 0's mean-projection bits
+        const int64_t* hd = hb + 1;
+        S.bm1 = -1;
+        S.wm1 = 0;
+        S.bsrc1 = -1;
+        if (hd[5] == 0) {  // empty ring 0: cm_n == 0, nothing passes
+            if (bm1 + 1 <= S1_BITS_WORDS) { S.bm1 = bm1; S.wm1 = 1; bm1 += 1; }
+        } else if (hd[12] >= 0 && bm1 + hd[13] <= S1_BITS_WORDS) {
+            S.bm1 = bm1;
+            S.wm1 = (int)hd[13];
+            S.bsrc1 = (int)((hd[12] + h_blob_off[k]) * 2);
+            bm1 += (int)hd[13];
+        }
+        a.max_levels = std::max(a.max_levels, nr);
+        max_m = std::max(max_m, m);
+        n_rings += nr;
+    }
+    a.n_rings = n_rings;
+    a.bm_words = bm_words;
+    a.bm1_words = bm1;
+
+    const int sms = device_sms();
+    // row bands: as many rows per pass as the workspace holds
+    int64_t band = rows;
+    while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + TY - 1) / TY * TY;
+    if (!d_ws || fused_ws_bytes(W, band, n, sms) > ws_bytes) return SS_DECLINED;
+
+    for (int j = 0; j < n; ++j)
+        if (cudaMemsetAsync(a.size[j].row_counts, 0, (size_t)rows * sizeof(uint32_t), s) != cudaSuccess)
+            return check_launch("memset");
+    TmaMaps maps;
+    {
+        const char* base = static_cast<const char*>(planes);
+        const int bw = eb == 4 ? Geo<unsigned>::BW : Geo<long long>::BW;
+        const size_t pb = (size_t)a.ps * eb;
+        if (int e = encode_plane_map(&maps.sat, base, eb, bw, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.e, base + 4 * pb, eb, bw, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.o, base + 8 * pb, eb, bw, W, h, pitch)) return e;
+    }
+    unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
+    unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
+    unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
+    int2* list = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + FCTR_BYTES);
+
+    auto launch = [&](auto tag) -> int {
+        using T = decltype(tag);
+        using G = Geo<T>;
+        auto s1 = ladder_stage1_kernel<T>;
+        auto rk = ladder_rings_kernel<T>;
+        const size_t s1_smem = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(bm1, 1) * 4;
+        const int s1_per_sm = std::min(occupancy(reinterpret_cast<const void*>(s1), (WARPS + 1) * 32, s1_smem), 2);
+        const size_t rk_smem = (size_t)n_rings * sizeof(RingDev) + (size_t)n * sizeof(SizeSm) +
+                               (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.max_levels * QCAP * sizeof(int2);
+        const int rk_per_sm = std::max(occupancy(reinterpret_cast<const void*>(rk), RK_WARPS * 32, rk_smem), 1);
+        for (int64_t yb = y_begin; yb < y_end; yb += band) {
+            const int64_t ye = std::min<int64_t>(y_end, yb + band), brows = ye - yb;
+            a.y_begin = (int)yb;
+            a.y_end = (int)ye;
+            TileMapF tm;
+            tm.n_tx = (int)((W + TX - 1) / TX);
+            tm.n_ty = (int)((brows + TY - 1) / TY);
+            tm.n_sizes = n;
+            tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n;
+            // column strips: the widest whose working set -- (max_m + rows in
+            // flight) x (strip + max_m) columns of all 12 planes -- fits the L2
+            // budget (the rings that follow touch every plane of those rows)
+            {
+                int64_t budget = 48ll << 20;
+                if (const char* e = getenv("SS_FUSED_STRIP_BUDGET_MB")) budget = (int64_t)atoi(e) << 20;
+                const int64_t in_flight = (int64_t)sms * s1_per_sm * G::STAGES;
+                tm.strip = 1;
+                for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
+                    const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * TY;
+                    const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * TX + max_m + 2) * 12 * eb;
+                    if (ws <= budget) {
+                        tm.strip = strip;
+                        break;
+                    }
+                }
+            }
+            const int parts = parts_for(W, brows, n);
+            const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
+            if (cudaMemsetAsync(d_ws, 0, FCTR_BYTES, s) != cudaSuccess) return check_launch("memset");
+            const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm),
+                                                       (long long)TILE_CTRS);
+            s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, parts,
+                                                                 parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list,
+                                                                 part_cap, list_ctr, tile_ctr);
+            note_launch();
+            if (int e = check_launch("ladder_stage1_kernel")) return e;
+            rk<<<(unsigned)(sms * rk_per_sm), RK_WARPS * 32, rk_smem, s>>>(a, parts, list, part_cap, list_ctr,
+                                                                          group_ctr);
+            note_launch();
+            if (int e = check_launch("ladder_rings_kernel")) return e;
+        }
+        return SS_OK;
+    };
+    return eb == 4 ? launch((unsigned)0) : launch((long long)0);
+}
+
+}  // namespace ss
+
+extern "C" size_t ss_ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
+    return ss::ladder_workspace_bytes(W, rows, n_sizes);
+}

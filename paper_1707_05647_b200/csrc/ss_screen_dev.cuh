@@ -1,0 +1,504 @@
+// ss_screen_dev.cuh -- device helpers shared by the per-size screen
+// (ss_screen.cu) and the fused ladder screen (ss_ladder_screen.cu): ring
+// parameters, the exact fp64 feature / quantize / membership sequence
+// (SURVEY.md App. A), TMA + mbarrier wrappers, stage-1 tile geometry.
+// Internal: included only by translation units compiled with -fmad=false.
+#pragma once
+#include <cuda.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
+
+#include "ss_common.cuh"
+
+namespace ss {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARPS = 16;  // stage-1 consumer warps per CTA (one tile row each)
+constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
+
+struct RingDev {
+    int n, d;
+    int sa, sb, sc, sd;  // SAT corners rel. to [cy][cx]: [+n+1][+n+1] [+n+1][-n+1] [-n+1][+n+1] [-n+1][-n+1]
+    int ea, ed;          // E corners: [+d+1][+1], [-d][+1]
+    int ob, oc;          // O corners: [0][-d], [0][+d+1]
+    double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
+    float fa, fb;  // RN32(1 / (2 cnt qm)) of the square / diamond: fp32 estimate of the mean cell
+    int cm_lo, cm_n, cs_lo, cs_n, cg_lo, cg_n;
+    int bm;        // shared-memory word offset of [m | ms | full] bits; -1: binary search
+    int wm, wms;   // words of the m and ms bitmaps
+    int bsrc;      // uint32 index of the bit section in the device blob (-1: zero fill)
+    int bwords;    // words to stage
+    int off_m, n_m, off_ms, n_ms, off_k, n_k;
+};
+
+struct ScreenArgs {
+    const void* planes;   // 12 planes of int64, or of uint32 (cells mod 2^32)
+    long long pitch, ps;  // row pitch, plane stride (elements)
+    int W, H, y_origin, y_begin, y_end, stride, lo, hi, n_rings;
+    int sums_in_list;  // ring-0 PLAIN sums fit 32 bits: list entries carry them (rings skip 8 gathers)
+    double qm, qs, qg, rqm, rqs, rqg;
+    const long long* blob;
+    unsigned* mask;
+    long long mask_pitch;
+    unsigned* row_counts;
+    unsigned long long* stage_counts;
+    RingDev ring[SS_MAX_RINGS];
+};
+
+// Correctly rounded a / b given y = RN(1 / b) (Markstein): the first FMA pair
+// brings q within one ulp of a/b, the second rounds it exactly.
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+    double q = __dmul_rn(a, y);
+    double r = __fma_rn(-b, q, a);
+    q = __fma_rn(r, y, q);
+    r = __fma_rn(-b, q, a);
+    return __fma_rn(r, y, q);
+}
+
+// screening.py:86-87 floor(f / q + 0.5)
+__device__ __forceinline__ int quant(double f, double q, double rq) {
+    return (int)floor(__dadd_rn(div_rn(f, q, rq), 0.5));
+}
+
+__device__ __forceinline__ bool bsearch_eq(const long long* __restrict__ a, int n, long long key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && __ldg(a + lo) == key;
+}
+
+__device__ __forceinline__ bool bit(const unsigned* s, int idx) { return (s[idx >> 5] >> (idx & 31)) & 1u; }
+
+template <class A>
+__device__ __forceinline__ bool member_m(const A& a, const RingDev& R, const unsigned* sb, int cm) {
+    if (R.bm >= 0) {
+        const unsigned i = (unsigned)(cm - R.cm_lo);
+        return i < (unsigned)R.cm_n && bit(sb + R.bm, (int)i);
+    }
+    return bsearch_eq(a.blob + R.off_m, R.n_m, cm);
+}
+template <class A>
+__device__ __forceinline__ bool member_ms(const A& a, const RingDev& R, const unsigned* sb, int cm, int cs) {
+    if (R.bm >= 0) {
+        const unsigned j = (unsigned)(cs - R.cs_lo);
+        return j < (unsigned)R.cs_n && bit(sb + R.bm + R.wm, (cm - R.cm_lo) * R.cs_n + (int)j);
+    }
+    return bsearch_eq(a.blob + R.off_ms, R.n_ms, (long long)cm * SS_KEY_BASE + cs);
+}
+template <class A>
+__device__ __forceinline__ bool member_k(const A& a, const RingDev& R, const unsigned* sb, int cm, int cs,
+                                         int cg) {
+    if (R.bm >= 0) {
+        const unsigned k = (unsigned)(cg - R.cg_lo);
+        return k < (unsigned)R.cg_n &&
+               bit(sb + R.bm + R.wm + R.wms, ((cm - R.cm_lo) * R.cs_n + (cs - R.cs_lo)) * R.cg_n + (int)k);
+    }
+    return bsearch_eq(a.blob + R.off_k, R.n_k, ((long long)cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
+}
+
+// Plane elements: exact int64 cells, or the same cells mod 2^32 (u32).  A
+// region sum is a +-+- combination of four cells; with u32 planes it is
+// computed mod 2^32 and recovered exactly because the host only takes the u32
+// path when every ring's sums are known to fit (fits32()):
+//   PLAIN / SQUARED sums are non-negative and < 2^32;
+//   X / Y sums are (c + 1) * S1 + D with D = sum (x - c) v, |D| < 2^31, so
+//   D = (int32)(sum - (c + 1) * S1 mod 2^32).
+template <typename T> struct Corners {
+    T q[4], e[2], o[2];
+};
+template <typename T, class A>
+__device__ __forceinline__ void load_corners(const A& a, const RingDev& R, const T* pc, int kind,
+                                             Corners<T>& c) {
+    const T* pq = pc + (long long)kind * a.ps;
+    const T* pe = pc + (long long)(4 + kind) * a.ps;
+    const T* po = pc + (long long)(8 + kind) * a.ps;
+    c.q[0] = __ldg(pq + R.sa);
+    c.q[1] = __ldg(pq + R.sb);
+    c.q[2] = __ldg(pq + R.sc);
+    c.q[3] = __ldg(pq + R.sd);
+    c.e[0] = __ldg(pe + R.ea);
+    c.e[1] = __ldg(pe + R.ed);
+    c.o[0] = __ldg(po + R.ob);
+    c.o[1] = __ldg(po + R.oc);
+}
+template <typename T> __device__ __forceinline__ T sq_of(const Corners<T>& c) { return c.q[0] - c.q[1] - c.q[2] + c.q[3]; }
+template <typename T> __device__ __forceinline__ T di_of(const Corners<T>& c) { return c.e[0] - c.o[0] - c.o[1] + c.e[1]; }
+
+// exact non-negative region sum (PLAIN, SQUARED)
+__device__ __forceinline__ long long unsigned_sum(long long v) { return v; }
+__device__ __forceinline__ long long unsigned_sum(unsigned v) { return (long long)v; }
+// exact weighted region sum with weight (c + 1) at the centre column/row c
+__device__ __forceinline__ long long weighted_sum(long long v, long long, long long) { return v; }
+__device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long long s1) {
+    const long long base = c1 * s1;
+    return base + (long long)(int)(v - (unsigned)base);
+}
+
+// RN conversion of an exact non-negative region sum to fp32 (rel. error <= 2^-24)
+__device__ __forceinline__ float to_f32(long long v) { return __ll2float_rn(v); }
+__device__ __forceinline__ float to_f32(unsigned v) { return __uint2float_rn(v); }
+
+// Mean cell floor(t), t = ((s1q/cq + s1d/cd) * 0.5) / qm + 0.5 (features.py:325, 349, 365;
+// screening.py:86-87), from exact non-negative PLAIN sums.  The fp32 estimate tf is
+// within 4e-7 (tf + 1) of the fp64 t (six roundings of 2^-24 on non-negative terms), so
+// when [tf - dl, tf + dl] holds no integer, floor(t) = floor(tf) exactly; only centres
+// whose mean lies within ~4e-6 of a cell boundary take the fp64 op sequence.
+template <typename S, class A>
+__device__ __forceinline__ int mean_cell(const A& a, const RingDev& R, S s1q, S s1d) {
+    const float tf = fmaf(to_f32(s1q), R.fa, fmaf(to_f32(s1d), R.fb, 0.5f));
+    const float dl = fmaf(tf, 4e-6f, 4e-6f);
+    int cm = (int)floorf(tf - dl);
+    if (cm != (int)floorf(tf + dl)) {
+        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
+        const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);  // features.py:349
+        cm = quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm);
+    }
+    return cm;
+}
+
+#ifndef RINGS_FAST_CM
+#define RINGS_FAST_CM 0  // the rings need the fp64 means anyway; the exact cell is a short chain on top
+#endif
+#ifndef STAGE1_FAST_CM
+#define STAGE1_FAST_CM 1
+#endif
+
+struct Stage1 {
+    long long s1q, s1d;
+    double mq, md;
+    int cm;
+};
+
+// Stage 1 of ring R from its exact PLAIN sums: means and mean cell.
+template <class A>
+__device__ __forceinline__ Stage1 stage1_from(const A& a, const RingDev& R, long long s1q, long long s1d) {
+    Stage1 s;
+    s.s1q = s1q;
+    s.s1d = s1d;
+    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
+    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);  // features.py:349
+#if RINGS_FAST_CM
+    s.cm = mean_cell(a, R, s1q, s1d);  // features.py:365
+#else
+    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
+#endif
+    return s;
+}
+
+// Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
+template <typename T, class A>
+__device__ __forceinline__ bool finish_of(const A& a, const RingDev& R, const unsigned* sb, int cx, int cy,
+                                         const Stage1& s, const Corners<T>& c2, const Corners<T>& cx_,
+                                         const Corners<T>& cy_) {
+    const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
+    // features.py:326, 350: sqrt(max(s2/count - mean*mean, 0))
+    const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
+    const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
+    const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
+    const int cs = quant(sd, a.qs, a.rqs);
+    if (!member_ms(a, R, sb, s.cm, cs)) return false;
+    const double fq = (double)s.s1q, fd = (double)s.s1d;
+    const long long sxq = weighted_sum(sq_of(cx_), cx + 1, s.s1q), syq = weighted_sum(sq_of(cy_), cy + 1, s.s1q);
+    const long long sxd = weighted_sum(di_of(cx_), cx + 1, s.s1d), syd = weighted_sum(di_of(cy_), cy + 1, s.s1d);
+    // features.py:328-329, 351-352: (s - (c + off) * s1) / w1; product and difference are exact
+    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
+    const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
+    const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
+    const int cg = quant(gm, a.qg, a.rqg);
+    return member_k(a, R, sb, s.cm, cs, cg);
+}
+
+// Host: the device parameters of ring (n, d) of patch side m (features.py:
+// 94-142 constants, corner offsets at row pitch P, the key blob header hd of
+// ss_keyset_blob with its offsets rebased by blob_base slots) and its
+// membership bitmap's place in the shared-memory budget (rings are packed in
+// the order they are filled; a ring that does not fit uses binary search).
+inline int fill_ring(RingDev& R, int n, int d, int m, long long P, double qm, const int64_t* hd, long long blob_base,
+                     int& bm_words, int budget) {
+    const int lo = (m - 1) / 2, hi = m / 2;
+    if (n < 1 || d < 1 || n > hi || d > lo) {
+        set_error("ring (%d,%d) does not fit m=%d", n, d, m);
+        return SS_EINVAL;
+    }
+    R.n = n;
+    R.d = d;
+    R.sa = (int)((n + 1) * P + (n + 1));
+    R.sb = (int)((n + 1) * P + (1 - n));
+    R.sc = (int)((1 - n) * P + (n + 1));
+    R.sd = (int)((1 - n) * P + (1 - n));
+    R.ea = (int)((d + 1) * P + 1);
+    R.ed = (int)(-(long long)d * P + 1);
+    R.ob = -d;
+    R.oc = d + 1;
+    R.cnt_sq = (double)(4LL * n * n);                                            // features.py:323
+    R.w1_sq = (double)(2LL * n * n * n);                                         // features.py:324
+    R.cnt_di = (double)(2LL * d * d + 2LL * d + 1);                              // integral.py:189-191
+    R.w1_di = (double)(2LL * d * d + (long long)d * (d - 1) * (2 * d - 1) / 3);  // features.py:341-343
+    R.rcp_sq = 1.0 / R.cnt_sq;  // host IEEE division: RN(1/b)
+    R.rcp_di = 1.0 / R.cnt_di;
+    R.rw1_sq = 1.0 / R.w1_sq;
+    R.rw1_di = 1.0 / R.w1_di;
+    R.fa = (float)(1.0 / (2.0 * R.cnt_sq * qm));
+    R.fb = (float)(1.0 / (2.0 * R.cnt_di * qm));
+    R.off_m = (int)(hd[0] + blob_base);
+    R.n_m = (int)hd[1];
+    R.off_ms = (int)(hd[2] + blob_base);
+    R.n_ms = (int)hd[3];
+    R.off_k = (int)(hd[4] + blob_base);
+    R.n_k = (int)hd[5];
+    R.cm_lo = (int)hd[6];
+    R.cm_n = (int)hd[7];
+    R.cs_lo = (int)hd[8];
+    R.cs_n = (int)hd[9];
+    R.cg_lo = (int)hd[10];
+    R.cg_n = (int)hd[11];
+    R.bm = -1;
+    R.wm = R.wms = 0;
+    R.bsrc = -1;
+    R.bwords = 0;
+    if (R.n_k == 0) {  // empty ring: nothing passes
+        if (bm_words + 1 <= budget) {
+            R.bm = bm_words;
+            R.cm_n = 0;
+            R.bwords = 1;
+            bm_words += 1;
+        } else {
+            R.n_m = 0;  // binary search over nothing: never a member
+        }
+    } else if (hd[12] >= 0) {
+        const int64_t words = hd[13] + hd[14] + hd[15];
+        if (bm_words + words <= budget) {
+            R.bm = bm_words;
+            R.wm = (int)hd[13];
+            R.wms = (int)hd[14];
+            R.bsrc = (int)((hd[12] + blob_base) * 2);
+            R.bwords = (int)words;
+            bm_words += (int)words;
+        }
+    }
+    return SS_OK;
+}
+
+// ── TMA / mbarrier helpers (sm_90+ PTX, used on sm_100a) ──────────────────
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
+}
+
+struct TmaMaps {
+    CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) of T
+};
+
+// Stage-1 tile geometry: TY rows (one per consumer warp) x TX columns; the 8
+// ring-0 PLAIN corner boxes of a tile are staged by TMA into one pipeline
+// stage.  Measured on B200 + driver 580: a tile-mode TMA box must start at a
+// 16-byte aligned inner coordinate (an odd int64 column raises "illegal
+// instruction"), so each box starts at the ALIGN-column boundary at or below
+// the corner and is BW = TX + ALIGN columns wide; readers skip the offset.
+constexpr int TY = WARPS;     // tile rows
+#ifndef S1_CPW
+#define S1_CPW 2
+#endif
+#ifndef S1_STAGES32
+#define S1_STAGES32 4
+#endif
+constexpr int CPW = S1_CPW;   // 32-centre chunks per warp per tile
+constexpr int TX = 32 * CPW;  // tile columns
+constexpr int NBOX = 8;
+constexpr int TILE_POS = TX * TY;  // centres per tile
+// Candidate lists, two modes picked per size on the host (see screen_size):
+// * small sizes: one list, entries (x, y);
+// * large sizes (>= LARGE_TILES tiles): `parts` sub-lists -- stage-1 CTA b
+//   serves partition b % parts (tiles p, p + parts, ...) and appends to its
+//   own sub-list and counter, so no single counter serialises a long grid --
+//   and entries (x, y, s1q, s1d) that carry the ring-0 PLAIN sums (the rings
+//   kernel skips those 8 gathers).
+// Either way the lists follow the strip-major tile order.
+constexpr int MAX_PARTS = 8;
+constexpr int TILE_CTRS = MAX_PARTS;  // stage-1 tile counters (partition p's CTAs use counter p)
+// List slots a stage-1 warp reserves per atomic (a multiple of 32): fewer
+// atomics on the list counter vs. the padding of each warp's last blocks
+// (measured: 64 for the single list, 128 for the partitioned lists).
+constexpr int RESERVE_SMALL = 64, RESERVE_LARGE = 128, RESERVE_MAX = 128;
+#ifndef GROUP_CTRS
+#define GROUP_CTRS 8u  // rings group counters per partition
+#endif
+constexpr int CTR_STRIDE = 32;  // words between counters (one 128-B line each)
+template <typename E> __device__ __forceinline__ E make_entry(int x, int y, unsigned sq, unsigned sd);
+template <> __device__ __forceinline__ int4 make_entry<int4>(int x, int y, unsigned sq, unsigned sd) {
+    return make_int4(x, y, (int)sq, (int)sd);
+}
+template <> __device__ __forceinline__ int2 make_entry<int2>(int x, int y, unsigned, unsigned) {
+    return make_int2(x, y);
+}
+__device__ __forceinline__ int4 widen(int4 e) { return e; }
+__device__ __forceinline__ int4 widen(int2 e) { return make_int4(e.x, e.y, 0, 0); }
+template <typename T> struct Geo {
+    static constexpr int STAGES = sizeof(T) == 4 ? S1_STAGES32 : 3;  // pipeline depth (u32: 35 KB, int64: 68 KB a stage)
+    static constexpr int ALIGN = 16 / (int)sizeof(T);
+    static constexpr int BW = TX + ALIGN;  // staged box width (elements)
+    static constexpr int BOX_ELEMS = BW * TY;
+    static constexpr int BOX_BYTES = BOX_ELEMS * (int)sizeof(T);
+    static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+    __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }  // two's complement
+    __device__ static int rem(int c) { return c & (ALIGN - 1); }
+};
+
+struct TileMap {
+    int n_tx, n_ty;  // tiles along x, y
+    int strip;       // tiles per column strip (L2 locality for wide images)
+    long long n_tiles;
+};
+
+__device__ __forceinline__ void tile_coords(const TileMap& t, long long idx, int& tx, int& ty) {
+    // strip-major: strips of `strip` tile columns, row-blocks within a strip, x fastest
+    const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty;
+    const unsigned i = (unsigned)idx;
+    const unsigned s = i / per_strip;
+    const int s0 = (int)(s * (unsigned)t.strip);
+    const unsigned width = (unsigned)min(t.strip, t.n_tx - s0);
+    const unsigned r = i - s * per_strip;
+    const unsigned q = r / width;
+    ty = (int)q;
+    tx = s0 + (int)(r - q * width);
+}
+
+// Copy the rings' membership bitmaps into shared memory (all threads);
+// m_only: just the mean-projection words (all stage 1 tests).
+__device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbits, int r_lo, int r_hi,
+                                              bool m_only = false) {
+    const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
+    for (int r = r_lo; r < r_hi; ++r) {
+        const RingDev& R = a.ring[r];
+        if (R.bm < 0) continue;
+        const int words = m_only ? max(R.wm, 1) : R.bwords;
+        for (int i = threadIdx.x; i < words; i += blockDim.x)
+            sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
+    }
+}
+
+constexpr int RK_WARPS = 8;
+constexpr int QCAP = 64;
+#ifndef RINGS_MINB
+#define RINGS_MINB 3  // resident CTAs per SM the register budget is sized for
+#endif
+
+#ifndef RINGS_GROUP
+#define RINGS_GROUP 128  // list entries a warp takes per grab: in flight = warps x RINGS_GROUP
+#endif
+
+inline int device_sms() {
+    static std::atomic<int> cached[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cached[dev].load(std::memory_order_relaxed) > 0) return cached[dev].load();
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cached[dev].store(sms);
+    return sms;
+}
+
+// Resident CTAs per SM of kernel `fn` at `smem` dynamic bytes.  The first use
+// of a kernel on a device raises its dynamic shared-memory limit to the
+// maximum; results are cached per (kernel, block, smem, device) -- these
+// queries cost more host time than a launch, and a ladder makes 2 per size.
+inline int occupancy(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+    static std::set<std::pair<const void*, int>> raised;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(fn, threads, smem, dev);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (raised.insert({fn, dev}).second) {
+        // the opt-in limit covers static + dynamic shared memory
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fn);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    per_sm = std::max(per_sm, 1);
+    cache[key] = per_sm;
+    return per_sm;
+}
+// 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
+// h+1 rows), box BW x TY.
+inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes, int box_w, int64_t W, int64_t h,
+                            int64_t pitch) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return SS_ECUDA;
+        }
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch * (cuuint64_t)elem_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)TY};
+    const cuuint32_t estr[2] = {1, 1};
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook
+    const CUresult r = encode(map, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_INT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                              const_cast<void*>(plane), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return SS_ECUDA;
+    }
+    return SS_OK;
+}
+
+
+}  // namespace
+}  // namespace ss

@@ -38,6 +38,14 @@ N_STREAMS = 3
 STREAMS_MAX_TABLE_BYTES = 4 << 30
 
 
+# Fused ladder (ss_ladder_screen.cu): every size sharing a plane width is
+# screened in lock-step, two launches per row band, so each plane row is read
+# from HBM about once per band instead of once per size.  SS_FUSED=0 selects
+# the per-size kernels on side streams (experiments, tests).
+def fused_enabled() -> bool:
+    return os.environ.get("SS_FUSED", "1") != "0"
+
+
 def streams_for(table_bytes: int) -> int:
     env = os.environ.get("SS_STREAMS")
     if env:
@@ -271,9 +279,8 @@ class Engine:
         self.n_streams = streams_for(tb32)
         self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n_streams)]
         self.template_stream = torch.cuda.Stream(self.device)  # f2 features, overlapping the table build
-        ws = int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1)))
-        self.screen_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device) for _ in range(self.n_streams)]
-        self.screen_ws_main = self.screen_ws[0]  # used only when there are no side streams
+        self.screen_ws = None  # per-size workspaces, one per side stream (allocated when the per-size path runs)
+        self.ladder_ws = None  # fused ladder workspace (allocated for the first ladder that needs it)
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -363,16 +370,33 @@ class Engine:
         cfg = tp.config
         q = cfg.quantizer.factors()
         L = len(tp.sizes)
-        handles = (ctypes.c_void_p * (1 + self.n_streams))(main.cuda_stream, *[st.cuda_stream for st in self.streams])
-        wss = (ctypes.c_void_p * (1 + self.n_streams))(self.screen_ws_main.data_ptr(),
-                                                        *[w.data_ptr() for w in self.screen_ws])
+        flags = 1 if self.force_int64 else 0
+        if fused_enabled():
+            need = int(self.L.ss_ladder_workspace_bytes(self.W, max(self.mrows, 1), max(L, 1)))
+            if self.ladder_ws is None or self.ladder_ws.numel() < need:
+                self.ladder_ws = None
+                self.ladder_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            flags |= 2
+            handles = (ctypes.c_void_p * 1)(main.cuda_stream)
+            wss = (ctypes.c_void_p * 1)(self.ladder_ws.data_ptr())
+            n_streams, ws_bytes = 1, self.ladder_ws.numel()
+        else:
+            if self.screen_ws is None:
+                ws = int(self.L.ss_screen_workspace_bytes(self.W, max(self.mrows, 1)))
+                self.screen_ws = [torch.empty(ws, dtype=torch.uint8, device=self.device)
+                                  for _ in range(self.n_streams)]
+            handles = (ctypes.c_void_p * (1 + self.n_streams))(main.cuda_stream,
+                                                                *[st.cuda_stream for st in self.streams])
+            wss = (ctypes.c_void_p * (1 + self.n_streams))(self.screen_ws[0].data_ptr(),
+                                                            *[w.data_ptr() for w in self.screen_ws])
+            n_streams, ws_bytes = 1 + self.n_streams, self.screen_ws[0].numel()
         _native.check(self.L.ss_screen_ladder(
             _p(self.planes), None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch,
             self.W, self.H, self.y_origin, self.y_begin, self.y_end, cfg.stride, L, tp.m_arr.ctypes.data,
             tp.n_rings.ctypes.data, tp.ring_n.ctypes.data, tp.ring_d.ctypes.data, tp.blobs_dev.data_ptr(),
             tp.blobs.ctypes.data, tp.blob_off.ctypes.data, q[0], q[1], q[2], self.masks.data_ptr(), self.words,
             self.mrows * self.words, self.row_counts.data_ptr(), self.row_counts.shape[1], _p(self.stage_counts),
-            1 if self.force_int64 else 0, 1 + self.n_streams, handles, wss, self.screen_ws[0].numel()),
+            flags, n_streams, handles, wss, ws_bytes),
             "screen")
 
     def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:
