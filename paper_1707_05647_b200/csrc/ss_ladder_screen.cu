@@ -88,7 +88,8 @@ __device__ __forceinline__ bool member_m1(const FusedArgs& a, const SizeDev& S, 
     return bsearch_eq(a.blob + R.off_m, R.n_m, cm);
 }
 
-// Stage 1 of every fused size: border keeps into the masks, ring-0 mean cell
+// Stage 1 of every fused size (interior centres; ladder_border_kernel wrote the
+// border keeps): ring-0 mean cell
 // from TMA-staged PLAIN corner boxes, mean-projection passers appended to the
 // candidate list tagged with their size.  Persistent CTAs; warp WARPS is the
 // producer.  Same pipeline as stage1_kernel (ss_screen.cu).
@@ -193,25 +194,23 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
-        if (y >= a.y_end) continue;
-        const int ylo = S.lo, yhi = a.H - 1 - S.hi, xlo = S.lo, xhi = a.W - 1 - S.hi;
-        const bool row_grid = unit_stride || (y % a.stride) == 0;
-        const bool row_int = row_grid && y >= ylo && y <= yhi;
-        unsigned* mrow = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
+        // border keeps are already in the masks (ladder_border_kernel); only
+        // interior centres of interior grid rows are evaluated here
+        if (y >= a.y_end || y < S.lo || y > a.H - 1 - S.hi || (!unit_stride && (y % a.stride) != 0)) continue;
+        const int xlo = S.lo, xhi = a.W - 1 - S.hi;
         const int tag = y | (sz << TAG_SHIFT);
+        const int xt = tx * TX;
+        const bool full = unit_stride && xt >= xlo && xt + TX - 1 <= xhi;  // warp-uniform: no per-lane tests
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
-            const int x = tx * TX + 32 * c + lane;
-            const bool on_grid = row_grid && x < a.W && (unit_stride || (x % a.stride) == 0);
-            const bool interior = row_int && on_grid && x >= xlo && x <= xhi;
-            const unsigned border = __ballot_sync(FULL, on_grid && !interior);
-            const int word = tx * CPW + c;
-            if (lane == 0 && word * 32 < a.W) mrow[word] = border;
-            bool pass = false;
-            if (interior) pass = member_m1(a, S, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
+            const int x = xt + 32 * c + lane;
+            const bool interior = full || (x >= xlo && x <= xhi && (unit_stride || (x % a.stride) == 0));
+            const bool pass = interior && member_m1(a, S, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
             const unsigned pb = __ballot_sync(FULL, pass);
-            n_int += __popc(__ballot_sync(FULL, interior));
-            n_pass += __popc(pb);
+            if (a.stage_counts) {
+                n_int += __popc(__ballot_sync(FULL, interior));
+                n_pass += __popc(pb);
+            }
             if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, tag);
             nbuf += __popc(pb);
         }
@@ -254,6 +253,39 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     }
 }
 
+// Border keeps of every fused size (screening.py:438-442): rows [y_begin,
+// y_end) of each mask get the grid centres outside the size's interior; the
+// interior bits start at 0 and the rings kernel ORs its survivors in.
+__global__ void ladder_border_kernel(const __grid_constant__ FusedArgs a) {
+    const int words = (a.W + 31) >> 5;
+    const SizeDev& S = a.size[blockIdx.z];
+    const int xlo = S.lo, xhi = a.W - 1 - S.hi;
+    for (int y = a.y_begin + blockIdx.y; y < a.y_end; y += gridDim.y) {
+        unsigned* row = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
+        const bool row_grid = a.stride == 1 || y % a.stride == 0;
+        const bool row_int = row_grid && y >= S.lo && y <= a.H - 1 - S.hi;
+        for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+            const int x0 = w * 32;
+            unsigned grid = 0;
+            if (row_grid) {
+                const int nb = min(32, a.W - x0);
+                if (a.stride == 1) {
+                    grid = nb == 32 ? FULL : (1u << nb) - 1u;
+                } else {
+                    for (int b = 0; b < nb; ++b)
+                        if ((x0 + b) % a.stride == 0) grid |= 1u << b;
+                }
+            }
+            unsigned inter = 0;
+            if (row_int) {
+                const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
+                if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
+            }
+            row[w] = grid & ~inter;
+        }
+    }
+}
+
 struct SizeSm {
     unsigned* mask;
     unsigned* row_counts;
@@ -264,12 +296,12 @@ struct SizeSm {
 template <typename T>
 __device__ __forceinline__ bool eval_ring_f(const FusedArgs& a, const RingDev& R, const unsigned* sbits, int level,
                                             int x, int cy) {
-    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + x;
+    const PlanePtrs<T> pc = plane_ptrs<T>(a, cy, x);
     Corners<T> c0, c2, cxk, cyk;
-    load_corners(a, R, pc, 0, c0);
-    load_corners(a, R, pc, 3, c2);
-    load_corners(a, R, pc, 1, cxk);
-    load_corners(a, R, pc, 2, cyk);
+    load_corners(pc, R, 0, c0);
+    load_corners(pc, R, 3, c2);
+    load_corners(pc, R, 1, cxk);
+    load_corners(pc, R, 2, cyk);
     const Stage1 s = stage1_from(a, R, unsigned_sum(sq_of(c0)), unsigned_sum(di_of(c0)));
     return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, x, cy, s, c2, cxk, cyk);
 }
@@ -457,6 +489,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     a.planes = planes;
     a.pitch = pitch;
     a.ps = (h + 1) * pitch;
+    if (3 * a.ps >= (long long)INT32_MAX) return SS_DECLINED;  // PlanePtrs: 32-bit kind offsets
     a.W = (int)W;
     a.H = (int)H;
     a.y_origin = (int)y_origin;
@@ -587,6 +620,13 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
             if (cudaMemsetAsync(d_ws, 0, FCTR_BYTES, s) != cudaSuccess) return check_launch("memset");
+            {
+                const int words = (int)((W + 31) / 32);
+                const dim3 bg((unsigned)((words + 127) / 128), (unsigned)std::min<int64_t>(brows, 65535), (unsigned)n);
+                ladder_border_kernel<<<bg, 128, 0, s>>>(a);
+                note_launch();
+                if (int e = check_launch("ladder_border_kernel")) return e;
+            }
             const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm),
                                                        (long long)TILE_CTRS);
             s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, parts,

@@ -241,7 +241,7 @@ template <typename T, bool SUMS>
 __device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R, const unsigned* sbits, int level,
                                           int4 e) {
     const int cy = e.y - a.y_origin;
-    const T* pc = static_cast<const T*>(a.planes) + (long long)cy * a.pitch + e.x;
+    const PlanePtrs<T> pc = plane_ptrs<T>(a, cy, e.x);
     Corners<T> c2, cxk, cyk;
     long long s1q, s1d;
     if (SUMS && level == 0 && a.sums_in_list) {
@@ -249,13 +249,13 @@ __device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R,
         s1d = (unsigned)e.w;
     } else {
         Corners<T> c0;
-        load_corners(a, R, pc, 0, c0);
+        load_corners(pc, R, 0, c0);
         s1q = unsigned_sum(sq_of(c0));
         s1d = unsigned_sum(di_of(c0));
     }
-    load_corners(a, R, pc, 3, c2);
-    load_corners(a, R, pc, 1, cxk);
-    load_corners(a, R, pc, 2, cyk);
+    load_corners(pc, R, 3, c2);
+    load_corners(pc, R, 1, cxk);
+    load_corners(pc, R, 2, cyk);
     const Stage1 s = stage1_from(a, R, s1q, s1d);
     return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, e.x, cy, s, c2, cxk, cyk);
 }
@@ -550,6 +550,10 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     ScreenArgs a;
     a.pitch = pitch;
     a.ps = (h + 1) * pitch;
+    if (3 * a.ps >= (long long)INT32_MAX) {  // kinds of one plane type are 32-bit offsets apart (PlanePtrs)
+        set_error("table too large: 3 planes exceed 2^31 elements");
+        return SS_EINVAL;
+    }
     a.W = (int)W;
     a.H = (int)H;
     a.y_origin = (int)y_origin;

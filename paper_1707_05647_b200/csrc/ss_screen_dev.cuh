@@ -113,12 +113,24 @@ __device__ __forceinline__ bool member_k(const A& a, const RingDev& R, const uns
 template <typename T> struct Corners {
     T q[4], e[2], o[2];
 };
+// Per-centre plane pointers: the SAT / E / O planes of kind PLAIN at the
+// centre, kinds `ks` elements apart (3 ks < 2^31, checked on the host), so
+// every corner address is one 32-bit offset on a 64-bit pointer (IMAD.WIDE).
+template <typename T> struct PlanePtrs {
+    const T *q, *e, *o;
+    int ks;
+};
 template <typename T, class A>
-__device__ __forceinline__ void load_corners(const A& a, const RingDev& R, const T* pc, int kind,
-                                             Corners<T>& c) {
-    const T* pq = pc + (long long)kind * a.ps;
-    const T* pe = pc + (long long)(4 + kind) * a.ps;
-    const T* po = pc + (long long)(8 + kind) * a.ps;
+__device__ __forceinline__ PlanePtrs<T> plane_ptrs(const A& a, int cy, int x) {
+    const T* p = static_cast<const T*>(a.planes) + ((long long)cy * a.pitch + x);
+    return PlanePtrs<T>{p, p + 4 * a.ps, p + 8 * a.ps, (int)a.ps};
+}
+template <typename T>
+__device__ __forceinline__ void load_corners(const PlanePtrs<T>& P, const RingDev& R, int kind, Corners<T>& c) {
+    const int ko = kind * P.ks;
+    const T* pq = P.q + ko;
+    const T* pe = P.e + ko;
+    const T* po = P.o + ko;
     c.q[0] = __ldg(pq + R.sa);
     c.q[1] = __ldg(pq + R.sb);
     c.q[2] = __ldg(pq + R.sc);
