@@ -62,6 +62,23 @@ struct TileMapF {
     long long n_tiles;  // n_tx * n_ty * n_sizes
 };
 
+// Fused stage-1 tile geometry: 16 rows x 32*CPW columns; 32-bit planes take
+// 128-column tiles (four independent centres per lane: the chains overlap),
+// int64 planes 64 (three pipeline stages must fit shared memory).
+template <typename T> struct GeoF {
+    static constexpr int CPW = sizeof(T) == 4 ? 4 : 2;
+    static constexpr int TX = 32 * CPW;
+    static constexpr int STAGES = 3;
+    static constexpr int ALIGN = 16 / (int)sizeof(T);
+    static constexpr int BW = TX + ALIGN;
+    static constexpr int BOX_ELEMS = BW * TY;
+    static constexpr int BOX_BYTES = BOX_ELEMS * (int)sizeof(T);
+    static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+    __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }
+    __device__ static int rem(int c) { return c & (ALIGN - 1); }
+};
+constexpr int TXMAX = 128;  // widest fused tile (workspace sizing)
+
 // strip-major; inside a strip: tile row, then size, then tile column
 __device__ __forceinline__ void tile_coords_f(const TileMapF& t, long long idx, int& tx, int& ty, int& s) {
     const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty * (unsigned)t.n_sizes;
@@ -79,15 +96,6 @@ __device__ __forceinline__ void tile_coords_f(const TileMapF& t, long long idx, 
     tx = s0 + (int)(rem - sz * width);
 }
 
-__device__ __forceinline__ bool member_m1(const FusedArgs& a, const SizeDev& S, const RingDev& R, const unsigned* sb,
-                                          int cm) {
-    if (S.bm1 >= 0) {
-        const unsigned i = (unsigned)(cm - R.cm_lo);
-        return i < (unsigned)R.cm_n && bit(sb + S.bm1, (int)i);
-    }
-    return bsearch_eq(a.blob + R.off_m, R.n_m, cm);
-}
-
 // Stage 1 of every fused size (interior centres; ladder_border_kernel wrote the
 // border keeps): ring-0 mean cell
 // from TMA-staged PLAIN corner boxes, mean-projection passers appended to the
@@ -98,8 +106,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     ladder_stage1_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ TmaMaps maps, const TileMapF tm,
                          int parts, int reserve, int2* list_base, long long part_cap, unsigned* list_ctr,
                          unsigned* tile_ctr_base) {
-    using G = Geo<T>;
-    constexpr int STAGES = G::STAGES;
+    using G = GeoF<T>;
+    constexpr int STAGES = G::STAGES, CPW = G::CPW;
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                 tile_coords_f(tm, t, tx, ty, sz);
                 tile_info[s] = make_int4(tx, ty, sz, 0);
                 const RingDev& R0 = a.ring[a.size[sz].ring0];
-                const int x0 = tx * TX;
+                const int x0 = tx * G::TX;
                 const int cy0 = a.y_begin + ty * TY - a.y_origin;
                 unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
                 mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
@@ -181,38 +189,67 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         const int tx = ti.x, ty = ti.y, sz = ti.z;
         const SizeDev& S = a.size[sz];
         const RingDev& R0 = a.ring[S.ring0];
-        const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d), po1 = G::rem(R0.d + 1);
         const int y = a.y_begin + ty * TY + warp;
-        const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
-        T s1q[CPW], s1d[CPW];
+        // border keeps are already in the masks (ladder_border_kernel); only
+        // interior centres of interior grid rows are evaluated here
+        const bool row_int = y < a.y_end && y >= S.lo && y <= a.H - 1 - S.hi && (unit_stride || (y % a.stride) == 0);
+        T s1q[CPW], s1d[CPW];  // exact PLAIN region sums
+        if (row_int) {
+            const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d),
+                      po1 = G::rem(R0.d + 1);
+            const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
 #pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-            const T* b = box + 32 * c;
-            constexpr int E = G::BOX_ELEMS;
-            s1q[c] = (T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]);
-            s1d[c] = (T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]);
+            for (int c = 0; c < CPW; ++c) {
+                const T* b = box + 32 * c;
+                constexpr int E = G::BOX_ELEMS;
+                s1q[c] = (T)(b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql]);
+                s1d[c] = (T)(b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe]);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
-        // border keeps are already in the masks (ladder_border_kernel); only
-        // interior centres of interior grid rows are evaluated here
-        if (y >= a.y_end || y < S.lo || y > a.H - 1 - S.hi || (!unit_stride && (y % a.stride) != 0)) continue;
+        if (!row_int) continue;
+        // mean cells of all chunks (fp32 estimate, exact unless within ~4e-6
+        // of a cell boundary: see mean_cell), then the rare exact fallback
+        int cm[CPW];
+        unsigned amb = 0;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const float tf = fmaf(to_f32(s1q[c]), R0.fa, fmaf(to_f32(s1d[c]), R0.fb, 0.5f));
+            const float dl = fmaf(tf, 4e-6f, 4e-6f);
+            cm[c] = (int)floorf(tf - dl);
+            amb |= (unsigned)(cm[c] != (int)floorf(tf + dl)) << c;
+        }
+        if (__any_sync(FULL, amb != 0)) {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c)
+                if ((amb >> c) & 1u) cm[c] = mean_cell_exact(a, R0, s1q[c], s1d[c]);
+        }
         const int xlo = S.lo, xhi = a.W - 1 - S.hi;
         const int tag = y | (sz << TAG_SHIFT);
-        const int xt = tx * TX;
-        const bool full = unit_stride && xt >= xlo && xt + TX - 1 <= xhi;  // warp-uniform: no per-lane tests
+        const int xt = tx * G::TX;
+        const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;  // warp-uniform: no per-lane tests
+        bool pass[CPW];
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
             const int x = xt + 32 * c + lane;
             const bool interior = full || (x >= xlo && x <= xhi && (unit_stride || (x % a.stride) == 0));
-            const bool pass = interior && member_m1(a, S, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
-            const unsigned pb = __ballot_sync(FULL, pass);
-            if (a.stage_counts) {
-                n_int += __popc(__ballot_sync(FULL, interior));
-                n_pass += __popc(pb);
+            bool member;
+            if (S.bm1 >= 0) {
+                const unsigned i = (unsigned)(cm[c] - R0.cm_lo);
+                member = i < (unsigned)R0.cm_n && bit(sbits + S.bm1, (int)i);
+            } else {
+                member = interior && bsearch_eq(a.blob + R0.off_m, R0.n_m, cm[c]);
             }
-            if (pass) buf[nbuf + __popc(pb & lt)] = make_int2(x, tag);
+            pass[c] = interior && member;
+            if (a.stage_counts) n_int += __popc(__ballot_sync(FULL, interior));
+        }
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const unsigned pb = __ballot_sync(FULL, pass[c]);
+            if (pass[c]) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
             nbuf += __popc(pb);
+            n_pass += __popc(pb);
         }
         while (nbuf >= 32) {
             __syncwarp();
@@ -433,15 +470,16 @@ constexpr size_t FCTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
 constexpr long long FUSED_LARGE_TILES = 32768;  // partitioned lists from this many tiles per pass
 constexpr size_t FUSED_WS_CAP = (size_t)4 << 30;  // ss_ladder_workspace_bytes: row bands beyond this
 
+// capacity in tiles of TXMAX x TY centres (covers either fused tile width)
 long long tiles_of(int64_t W, int64_t rows) {
-    return ((std::max<int64_t>(W, 1) + TX - 1) / TX) * ((std::max<int64_t>(rows, 1) + TY - 1) / TY);
+    return ((std::max<int64_t>(W, 1) + TXMAX - 1) / TXMAX) * ((std::max<int64_t>(rows, 1) + TY - 1) / TY);
 }
 int parts_for(int64_t W, int64_t rows, int n_sizes) {
     return tiles_of(W, rows) * n_sizes >= FUSED_LARGE_TILES ? MAX_PARTS : 1;
 }
 long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int parts) {
     const long long ctas = (2LL * sms + parts - 1) / parts;
-    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * TILE_POS + ctas * WARPS * 2 * RESERVE_MAX;
+    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * (TXMAX * TY) + ctas * WARPS * 2 * RESERVE_MAX;
 }
 size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms) {
     const int parts = parts_for(W, rows, n_sizes);
@@ -570,7 +608,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     TmaMaps maps;
     {
         const char* base = static_cast<const char*>(planes);
-        const int bw = eb == 4 ? Geo<unsigned>::BW : Geo<long long>::BW;
+        const int bw = eb == 4 ? GeoF<unsigned>::BW : GeoF<long long>::BW;
         const size_t pb = (size_t)a.ps * eb;
         if (int e = encode_plane_map(&maps.sat, base, eb, bw, W, h, pitch)) return e;
         if (int e = encode_plane_map(&maps.e, base + 4 * pb, eb, bw, W, h, pitch)) return e;
@@ -583,7 +621,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
 
     auto launch = [&](auto tag) -> int {
         using T = decltype(tag);
-        using G = Geo<T>;
+        using G = GeoF<T>;
         auto s1 = ladder_stage1_kernel<T>;
         auto rk = ladder_rings_kernel<T>;
         const size_t s1_smem = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(bm1, 1) * 4;
@@ -596,7 +634,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
             a.y_begin = (int)yb;
             a.y_end = (int)ye;
             TileMapF tm;
-            tm.n_tx = (int)((W + TX - 1) / TX);
+            tm.n_tx = (int)((W + G::TX - 1) / G::TX);
             tm.n_ty = (int)((brows + TY - 1) / TY);
             tm.n_sizes = n;
             tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n;
@@ -610,7 +648,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
                 tm.strip = 1;
                 for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
                     const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * TY;
-                    const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * TX + max_m + 2) * 12 * eb;
+                    const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * G::TX + max_m + 2) * 12 * eb;
                     if (ws <= budget) {
                         tm.strip = strip;
                         break;

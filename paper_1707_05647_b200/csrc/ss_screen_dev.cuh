@@ -162,6 +162,13 @@ __device__ __forceinline__ float to_f32(unsigned v) { return __uint2float_rn(v);
 // within 4e-7 (tf + 1) of the fp64 t (six roundings of 2^-24 on non-negative terms), so
 // when [tf - dl, tf + dl] holds no integer, floor(t) = floor(tf) exactly; only centres
 // whose mean lies within ~4e-6 of a cell boundary take the fp64 op sequence.
+// The fp64 mean cell of ring R (features.py:325, 349, 365; screening.py:86-87).
+template <typename S, class A>
+__device__ __forceinline__ int mean_cell_exact(const A& a, const RingDev& R, S s1q, S s1d) {
+    const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);
+    const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
+    return quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm);
+}
 template <typename S, class A>
 __device__ __forceinline__ int mean_cell(const A& a, const RingDev& R, S s1q, S s1d) {
     const float tf = fmaf(to_f32(s1q), R.fa, fmaf(to_f32(s1d), R.fb, 0.5f));
