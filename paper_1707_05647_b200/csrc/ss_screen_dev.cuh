@@ -125,20 +125,33 @@ __device__ __forceinline__ PlanePtrs<T> plane_ptrs(const A& a, int cy, int x) {
     const T* p = static_cast<const T*>(a.planes) + ((long long)cy * a.pitch + x);
     return PlanePtrs<T>{p, p + 4 * a.ps, p + 8 * a.ps, (int)a.ps};
 }
+// One read-only load at a 32-bit element offset from a 64-bit pointer:
+// address = p + sext(off) * sizeof(T) in one mad.wide (IMAD.WIDE); left to
+// itself the compiler re-associates these into 64-bit index arithmetic and
+// spends 3-4 integer instructions per corner.
+__device__ __forceinline__ unsigned ldg_at(const unsigned* p, int off) {
+    unsigned v;
+    asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 4, %1;\n\tld.global.nc.u32 %0, [ad];\n\t}"
+        : "=r"(v) : "l"(p), "r"(off));
+    return v;
+}
+__device__ __forceinline__ long long ldg_at(const long long* p, int off) {
+    long long v;
+    asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %1;\n\tld.global.nc.s64 %0, [ad];\n\t}"
+        : "=l"(v) : "l"(p), "r"(off));
+    return v;
+}
 template <typename T>
 __device__ __forceinline__ void load_corners(const PlanePtrs<T>& P, const RingDev& R, int kind, Corners<T>& c) {
     const int ko = kind * P.ks;
-    const T* pq = P.q + ko;
-    const T* pe = P.e + ko;
-    const T* po = P.o + ko;
-    c.q[0] = __ldg(pq + R.sa);
-    c.q[1] = __ldg(pq + R.sb);
-    c.q[2] = __ldg(pq + R.sc);
-    c.q[3] = __ldg(pq + R.sd);
-    c.e[0] = __ldg(pe + R.ea);
-    c.e[1] = __ldg(pe + R.ed);
-    c.o[0] = __ldg(po + R.ob);
-    c.o[1] = __ldg(po + R.oc);
+    c.q[0] = ldg_at(P.q, ko + R.sa);
+    c.q[1] = ldg_at(P.q, ko + R.sb);
+    c.q[2] = ldg_at(P.q, ko + R.sc);
+    c.q[3] = ldg_at(P.q, ko + R.sd);
+    c.e[0] = ldg_at(P.e, ko + R.ea);
+    c.e[1] = ldg_at(P.e, ko + R.ed);
+    c.o[0] = ldg_at(P.o, ko + R.ob);
+    c.o[1] = ldg_at(P.o, ko + R.oc);
 }
 template <typename T> __device__ __forceinline__ T sq_of(const Corners<T>& c) { return c.q[0] - c.q[1] - c.q[2] + c.q[3]; }
 template <typename T> __device__ __forceinline__ T di_of(const Corners<T>& c) { return c.e[0] - c.o[0] - c.o[1] + c.e[1]; }
