@@ -48,6 +48,7 @@ struct FusedArgs {
     int mask_y0;
     int n_sizes, n_rings, max_levels, bm_words, bm1_words;
     double qm, qs, qg, rqm, rqs, rqg;
+    int qpow2;  // see ScreenArgs
     const long long* blob;  // all sizes' key blobs (offsets in RingDev rebased)
     long long mask_pitch;
     unsigned long long* stage_counts;
@@ -540,6 +541,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     a.rqm = 1.0 / qm;
     a.rqs = 1.0 / qs;
     a.rqg = 1.0 / qg;
+    a.qpow2 = quant_pow2_bits(qm, qs, qg);
     a.blob = reinterpret_cast<const long long*>(d_blobs);
     a.mask_pitch = mask_pitch;
     a.stage_counts = d_stage_counts;

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             if (interior) {
                 const double mq = div_rn((double)s1q[c], R0.cnt_sq, R0.rcp_sq);  // features.py:325
                 const double md = div_rn((double)s1d[c], R0.cnt_di, R0.rcp_di);  // features.py:349
-                pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm));
+                pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm, a.qpow2 & 1));
             }
 #endif
             const unsigned pb = __ballot_sync(FULL, pass);
@@ -574,6 +574,7 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     a.rqm = 1.0 / qm;
     a.rqs = 1.0 / qs;
     a.rqg = 1.0 / qg;
+    a.qpow2 = quant_pow2_bits(qm, qs, qg);
     a.blob = reinterpret_cast<const long long*>(d_blob);
     a.mask = d_mask;
     a.mask_pitch = mask_pitch;

@@ -7,6 +7,7 @@
 #include <cuda.h>
 
 #include <atomic>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <set>
@@ -42,6 +43,7 @@ struct ScreenArgs {
     int W, H, y_origin, y_begin, y_end, stride, lo, hi, n_rings;
     int sums_in_list;  // ring-0 PLAIN sums fit 32 bits: list entries carry them (rings skip 8 gathers)
     double qm, qs, qg, rqm, rqs, rqg;
+    int qpow2;  // bit c: quantizer step c (mean, std, grad) is a power of two
     const long long* blob;
     unsigned* mask;
     long long mask_pitch;
@@ -61,8 +63,9 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
 }
 
 // screening.py:86-87 floor(f / q + 0.5)
-__device__ __forceinline__ int quant(double f, double q, double rq) {
-    return (int)floor(__dadd_rn(div_rn(f, q, rq), 0.5));
+// With q a power of two (pow2, uniform), f / q is exact and equals f * rq.
+__device__ __forceinline__ int quant(double f, double q, double rq, bool pow2) {
+    return (int)floor(__dadd_rn(pow2 ? __dmul_rn(f, rq) : div_rn(f, q, rq), 0.5));
 }
 
 __device__ __forceinline__ bool bsearch_eq(const long long* __restrict__ a, int n, long long key) {
@@ -180,7 +183,7 @@ template <typename S, class A>
 __device__ __forceinline__ int mean_cell_exact(const A& a, const RingDev& R, S s1q, S s1d) {
     const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);
     const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
-    return quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm);
+    return quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm, a.qpow2 & 1);
 }
 template <typename S, class A>
 __device__ __forceinline__ int mean_cell(const A& a, const RingDev& R, S s1q, S s1d) {
@@ -190,7 +193,7 @@ __device__ __forceinline__ int mean_cell(const A& a, const RingDev& R, S s1q, S 
     if (cm != (int)floorf(tf + dl)) {
         const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
         const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);  // features.py:349
-        cm = quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm);
+        cm = quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm, a.qpow2 & 1);
     }
     return cm;
 }
@@ -219,7 +222,7 @@ __device__ __forceinline__ Stage1 stage1_from(const A& a, const RingDev& R, long
 #if RINGS_FAST_CM
     s.cm = mean_cell(a, R, s1q, s1d);  // features.py:365
 #else
-    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm);  // features.py:365
+    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm, a.qpow2 & 1);  // features.py:365
 #endif
     return s;
 }
@@ -234,7 +237,7 @@ __device__ __forceinline__ bool finish_of(const A& a, const RingDev& R, const un
     const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
     const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
     const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
-    const int cs = quant(sd, a.qs, a.rqs);
+    const int cs = quant(sd, a.qs, a.rqs, (a.qpow2 >> 1) & 1);
     if (!member_ms(a, R, sb, s.cm, cs)) return false;
     const double fq = (double)s.s1q, fd = (double)s.s1d;
     const long long sxq = weighted_sum(sq_of(cx_), cx + 1, s.s1q), syq = weighted_sum(sq_of(cy_), cy + 1, s.s1q);
@@ -247,8 +250,18 @@ __device__ __forceinline__ bool finish_of(const A& a, const RingDev& R, const un
     const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
     const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
     const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    const int cg = quant(gm, a.qg, a.rqg);
+    const int cg = quant(gm, a.qg, a.rqg, (a.qpow2 >> 2) & 1);
     return member_k(a, R, sb, s.cm, cs, cg);
+}
+
+// Host: bit c set when quantizer step c (mean, std, grad) is a power of two
+// (then f / q == f * (1 / q) exactly and quant skips the division).
+inline int quant_pow2_bits(double qm, double qs, double qg) {
+    auto p2 = [](double q) {
+        int e = 0;
+        return q > 0.0 && std::frexp(q, &e) == 0.5;
+    };
+    return (p2(qm) ? 1 : 0) | (p2(qs) ? 2 : 0) | (p2(qg) ? 4 : 0);
 }
 
 // Host: the device parameters of ring (n, d) of patch side m (features.py:
