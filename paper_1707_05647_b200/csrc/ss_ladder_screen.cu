@@ -49,6 +49,7 @@ struct FusedArgs {
     int n_sizes, n_rings, max_levels, bm_words, bm1_words;
     double qm, qs, qg, rqm, rqs, rqg;
     int qpow2;  // see ScreenArgs
+    float rqs_f, rqg_f, band_s;
     const long long* blob;  // all sizes' key blobs (offsets in RingDev rebased)
     long long mask_pitch;
     unsigned long long* stage_counts;
@@ -330,20 +331,6 @@ struct SizeSm {
     int ring0, n_rings;
 };
 
-// Ring `level` of ring parameters R at table-local centre (x, cy).
-template <typename T>
-__device__ __forceinline__ bool eval_ring_f(const FusedArgs& a, const RingDev& R, const unsigned* sbits, int level,
-                                            int x, int cy) {
-    const PlanePtrs<T> pc = plane_ptrs<T>(a, cy, x);
-    Corners<T> c0, c2, cxk, cyk;
-    load_corners(pc, R, 0, c0);
-    load_corners(pc, R, 3, c2);
-    load_corners(pc, R, 1, cxk);
-    load_corners(pc, R, 2, cyk);
-    const Stage1 s = stage1_from(a, R, unsigned_sum(sq_of(c0)), unsigned_sum(di_of(c0)));
-    return (level == 0 || member_m(a, R, sbits, s.cm)) && finish_of(a, R, sbits, x, cy, s, c2, cxk, cyk);
-}
-
 // Every ring of every fused size over the stage-1 list (see rings_kernel in
 // ss_screen.cu for the batching / queue scheme); lanes of one batch may
 // belong to different sizes: each reads its size's ring from shared memory.
@@ -441,7 +428,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB)
         const bool valid = e.x >= 0;
         const int sz = valid ? (e.y >> TAG_SHIFT) : 0, y = e.y & YMASK;
         const SizeSm S = ssize[sz];
-        const bool pass = valid && eval_ring_f<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin);
+        const bool pass = valid && eval_ring_fast<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin);
         const bool last = level + 1 == S.n_rings;
         const unsigned pb = __ballot_sync(FULL, pass);
         if (level == 0) n_pass0 += __popc(pb);
@@ -542,6 +529,9 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     a.rqs = 1.0 / qs;
     a.rqg = 1.0 / qg;
     a.qpow2 = quant_pow2_bits(qm, qs, qg);
+    a.rqs_f = (float)(1.0 / qs);
+    a.rqg_f = (float)(1.0 / qg);
+    a.band_s = (float)(1e-5 / qs);
     a.blob = reinterpret_cast<const long long*>(d_blobs);
     a.mask_pitch = mask_pitch;
     a.stage_counts = d_stage_counts;

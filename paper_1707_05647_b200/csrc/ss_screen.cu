@@ -575,6 +575,9 @@ int screen_size(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, 
     a.rqs = 1.0 / qs;
     a.rqg = 1.0 / qg;
     a.qpow2 = quant_pow2_bits(qm, qs, qg);
+    a.rqs_f = (float)(1.0 / qs);
+    a.rqg_f = (float)(1.0 / qg);
+    a.band_s = (float)(1e-5 / qs);
     a.blob = reinterpret_cast<const long long*>(d_blob);
     a.mask = d_mask;
     a.mask_pitch = mask_pitch;

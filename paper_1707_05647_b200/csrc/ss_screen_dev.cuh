@@ -29,6 +29,8 @@ struct RingDev {
     int ob, oc;          // O corners: [0][-d], [0][+d+1]
     double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
     float fa, fb;  // RN32(1 / (2 cnt qm)) of the square / diamond: fp32 estimate of the mean cell
+    int icq, icd;  // pixel counts 4n^2, 2d^2+2d+1 (exact integer variances)
+    float rcq, rcd, rw2q, rw1d;  // RN32 of 1/icq, 1/icd, 1/(2 w1_sq), 1/w1_di (fp32 estimates of std / gradient)
     int cm_lo, cm_n, cs_lo, cs_n, cg_lo, cg_n;
     int bm;        // shared-memory word offset of [m | ms | full] bits; -1: binary search
     int wm, wms;   // words of the m and ms bitmaps
@@ -44,6 +46,7 @@ struct ScreenArgs {
     int sums_in_list;  // ring-0 PLAIN sums fit 32 bits: list entries carry them (rings skip 8 gathers)
     double qm, qs, qg, rqm, rqs, rqg;
     int qpow2;  // bit c: quantizer step c (mean, std, grad) is a power of two
+    float rqs_f, rqg_f, band_s;  // RN32(1/qs), RN32(1/qg), 1e-5 / qs (eval_ring_fast)
     const long long* blob;
     unsigned* mask;
     long long mask_pitch;
@@ -228,30 +231,120 @@ __device__ __forceinline__ Stage1 stage1_from(const A& a, const RingDev& R, long
 }
 
 // Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
+// The fp64 std cell (features.py:326, 350, 366; screening.py:86-87):
+// sqrt(max(s2/count - mean*mean, 0)) of both parts, averaged, quantized.
+template <class A>
+__device__ __forceinline__ int std_cell_exact(const A& a, const RingDev& R, double mq, double md, long long s2q,
+                                              long long s2d) {
+    const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(mq, mq));
+    const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(md, md));
+    const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
+    return quant(sd, a.qs, a.rqs, (a.qpow2 >> 1) & 1);
+}
+// The fp64 gradient-magnitude cell (features.py:328-329, 351-352, 367-371)
+// from the exact first moments sx*, sy* (weights x+1 / y+1) and PLAIN sums:
+// (s - (c + off) * s1) / w1 -- product and difference exact -- averaged,
+// hypot as sqrt(gx*gx + gy*gy), quantized.
+template <class A>
+__device__ __forceinline__ int grad_cell_exact(const A& a, const RingDev& R, int cx, int cy, long long s1q,
+                                               long long s1d, long long sxq, long long syq, long long sxd,
+                                               long long syd) {
+    const double fq = (double)s1q, fd = (double)s1d;
+    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
+    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
+    const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);
+    const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
+    const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
+    return quant(gm, a.qg, a.rqg, (a.qpow2 >> 2) & 1);
+}
+
+// Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
 template <typename T, class A>
 __device__ __forceinline__ bool finish_of(const A& a, const RingDev& R, const unsigned* sb, int cx, int cy,
                                          const Stage1& s, const Corners<T>& c2, const Corners<T>& cx_,
                                          const Corners<T>& cy_) {
     const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
-    // features.py:326, 350: sqrt(max(s2/count - mean*mean, 0))
-    const double vq = __dsub_rn(div_rn((double)s2q, R.cnt_sq, R.rcp_sq), __dmul_rn(s.mq, s.mq));
-    const double vd = __dsub_rn(div_rn((double)s2d, R.cnt_di, R.rcp_di), __dmul_rn(s.md, s.md));
-    const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
-    const int cs = quant(sd, a.qs, a.rqs, (a.qpow2 >> 1) & 1);
+    const int cs = std_cell_exact(a, R, s.mq, s.md, s2q, s2d);
     if (!member_ms(a, R, sb, s.cm, cs)) return false;
-    const double fq = (double)s.s1q, fd = (double)s.s1d;
     const long long sxq = weighted_sum(sq_of(cx_), cx + 1, s.s1q), syq = weighted_sum(sq_of(cy_), cy + 1, s.s1q);
     const long long sxd = weighted_sum(di_of(cx_), cx + 1, s.s1d), syd = weighted_sum(di_of(cy_), cy + 1, s.s1d);
-    // features.py:328-329, 351-352: (s - (c + off) * s1) / w1; product and difference are exact
-    const double gxq = div_rn(__dsub_rn((double)sxq, __dmul_rn(__dadd_rn((double)cx, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gyq = div_rn(__dsub_rn((double)syq, __dmul_rn(__dadd_rn((double)cy, 1.5), fq)), R.w1_sq, R.rw1_sq);
-    const double gxd = div_rn(__dsub_rn((double)sxd, __dmul_rn(__dadd_rn((double)cx, 1.0), fd)), R.w1_di, R.rw1_di);
-    const double gyd = div_rn(__dsub_rn((double)syd, __dmul_rn(__dadd_rn((double)cy, 1.0), fd)), R.w1_di, R.rw1_di);
-    const double gx = __dmul_rn(__dadd_rn(gxq, gxd), 0.5);  // features.py:367-369
-    const double gy = __dmul_rn(__dadd_rn(gyq, gyd), 0.5);
-    const double gm = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    const int cg = quant(gm, a.qg, a.rqg, (a.qpow2 >> 2) & 1);
+    const int cg = grad_cell_exact(a, R, cx, cy, s.s1q, s.s1d, sxq, syq, sxd, syd);
     return member_k(a, R, sb, s.cm, cs, cg);
+}
+
+// Centred first moment D = sum (x - c) v of a region from its weighted sum
+// (weights c + 1 at the centre column / row c) and PLAIN sum s1, exact:
+// 32-bit planes hold the weighted sum mod 2^32 and |D| < 2^31 (fits32).
+__device__ __forceinline__ long long centred(unsigned v, int c1, long long s1) {
+    return (long long)(int)(v - (unsigned)c1 * (unsigned)s1);
+}
+__device__ __forceinline__ long long centred(long long v, int c1, long long s1) { return v - (long long)c1 * s1; }
+
+// A cell floor(t) from an fp32 estimate tf with |tf - t| <= band: exact
+// unless [tf - band, tf + band] straddles an integer (returns false then).
+__device__ __forceinline__ bool cell_of(float tf, float band, int& cell) {
+    cell = (int)floorf(tf - band);
+    return cell == (int)floorf(tf + band);
+}
+
+// Ring R at table-local centre (cx, cy), decided from fp32 estimates of the
+// three cells built on exact integer region sums -- the variances
+// s2*count - s1^2 and the centred moments are exact integers, so each
+// estimate is within a few 2^-24 relative (plus, for the std, the fp64
+// reference's own cancellation error near zero variance) of the value the
+// reference's fp64 sequence produces -- and the fp64 sequence itself only
+// for a lane whose estimate lies within that error band of a cell boundary.
+// Same decisions as stage1_from + finish_of (the parity tests compare the
+// fused path, which uses this, with the oracle); the error bands:
+//   mean: mean_cell (4e-6 (t + 1));
+//   std:  |sqrt(V)/c| in fp32 <= 2.7e-7 rel, t <= 4.5e-7 (t + 1); fp64
+//         var error <= 4 * 2^-53 * 65025 => std error <= 5.4e-6 absolute;
+//         band 1e-6 (t + 1) + 1e-5 / qs;
+//   grad: |gx_f - gx| <= 2.5e-7 (|gxq| + |gxd|) (likewise y), hypot is
+//         1-Lipschitz, + 2.5e-7 rel; band 2x that plus 4e-7 (t + 1).
+template <typename T, class A>
+__device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, const unsigned* sb, int level, int cx,
+                                               int cy) {
+    const PlanePtrs<T> P = plane_ptrs<T>(a, cy, cx);
+    Corners<T> c0, c2, ckx, cky;
+    load_corners(P, R, 0, c0);
+    load_corners(P, R, 3, c2);
+    load_corners(P, R, 1, ckx);
+    load_corners(P, R, 2, cky);
+    const long long s1q = unsigned_sum(sq_of(c0)), s1d = unsigned_sum(di_of(c0));
+    const int cm = mean_cell(a, R, s1q, s1d);  // features.py:365 (level 0 entries passed this test in stage 1)
+    if (level > 0 && !member_m(a, R, sb, cm)) return false;
+    // std: exact integer variances V = s2 * count - s1^2 (>= 0)
+    const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
+    const long long vq = s2q * R.icq - s1q * s1q, vd = s2d * R.icd - s1d * s1d;
+    const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(__fsqrt_rn(__ll2float_rn(vq)), R.rcq),
+                                          __fmul_rn(__fsqrt_rn(__ll2float_rn(vd)), R.rcd)),
+                                0.5f);
+    const float ts = __fmaf_rn(sdf, a.rqs_f, 0.5f);
+    int cs;
+    if (!cell_of(ts, __fmaf_rn(ts, 1e-6f, 1e-6f) + a.band_s, cs)) {
+        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq), md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
+        cs = std_cell_exact(a, R, mq, md, s2q, s2d);
+    }
+    if (!member_ms(a, R, sb, cm, cs)) return false;
+    // gradient: exact centred moments; square offset c + 1.5 => numerator 2D - s1 over 2 w1
+    const long long dxq = centred(sq_of(ckx), cx + 1, s1q), dyq = centred(sq_of(cky), cy + 1, s1q);
+    const long long dxd = centred(di_of(ckx), cx + 1, s1d), dyd = centred(di_of(cky), cy + 1, s1d);
+    const float gxq = __fmul_rn(__ll2float_rn(2 * dxq - s1q), R.rw2q), gyq = __fmul_rn(__ll2float_rn(2 * dyq - s1q), R.rw2q);
+    const float gxd = __fmul_rn(__ll2float_rn(dxd), R.rw1d), gyd = __fmul_rn(__ll2float_rn(dyd), R.rw1d);
+    const float gx = __fmul_rn(__fadd_rn(gxq, gxd), 0.5f), gy = __fmul_rn(__fadd_rn(gyq, gyd), 0.5f);
+    const float gm = __fsqrt_rn(__fmaf_rn(gx, gx, __fmul_rn(gy, gy)));
+    const float tg = __fmaf_rn(gm, a.rqg_f, 0.5f);
+    const float sum = __fadd_rn(__fadd_rn(fabsf(gxq), fabsf(gxd)), __fadd_rn(fabsf(gyq), fabsf(gyd)));
+    const float bg = __fmaf_rn(__fmul_rn(__fadd_rn(sum, gm), 6e-7f), a.rqg_f, __fmaf_rn(tg, 4e-7f, 4e-7f));
+    int cg;
+    if (!cell_of(tg, bg, cg)) {
+        cg = grad_cell_exact(a, R, cx, cy, s1q, s1d, (long long)(cx + 1) * s1q + dxq, (long long)(cy + 1) * s1q + dyq,
+                             (long long)(cx + 1) * s1d + dxd, (long long)(cy + 1) * s1d + dyd);
+    }
+    return member_k(a, R, sb, cm, cs, cg);
 }
 
 // Host: bit c set when quantizer step c (mean, std, grad) is a power of two
@@ -296,6 +389,12 @@ inline int fill_ring(RingDev& R, int n, int d, int m, long long P, double qm, co
     R.rw1_di = 1.0 / R.w1_di;
     R.fa = (float)(1.0 / (2.0 * R.cnt_sq * qm));
     R.fb = (float)(1.0 / (2.0 * R.cnt_di * qm));
+    R.icq = (int)(4LL * n * n);
+    R.icd = (int)(2LL * d * d + 2LL * d + 1);
+    R.rcq = (float)(1.0 / R.cnt_sq);
+    R.rcd = (float)(1.0 / R.cnt_di);
+    R.rw2q = (float)(1.0 / (2.0 * R.w1_sq));
+    R.rw1d = (float)(1.0 / R.w1_di);
     R.off_m = (int)(hd[0] + blob_base);
     R.n_m = (int)hd[1];
     R.off_ms = (int)(hd[2] + blob_base);
