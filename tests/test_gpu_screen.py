@@ -282,3 +282,53 @@ def test_row_bands_on_device_assemble_to_full_screen(cuda, world):
     assert list(counts) == full.candidates_per_size()
     for k, m in enumerate(full.ladder):
         assert np.array_equal(masks[k], full.size_masks.packed(m)), m
+
+
+def _boundary_image(seed):
+    """Flat blocks at mean-cell boundaries (v = 8k + 4), exact ramps,
+    checkerboards and stripes: many centres whose mean / std / gradient sit
+    exactly on or within rounding of a quantizer boundary."""
+    rng = np.random.default_rng(seed)
+    H, W = 300, 360
+    img = np.zeros((H, W), np.uint8)
+    for by in range(0, H, 60):
+        for bx in range(0, W, 60):
+            img[by:by + 60, bx:bx + 60] = 8 * int(rng.integers(0, 32)) + 4
+    yy, xx = np.mgrid[0:60, 0:60]
+    img[0:60, 0:60] = (xx * 4) % 256
+    img[60:120, 120:180] = (yy * 2 + xx * 2) % 256
+    img[120:180, 240:300] = ((xx + yy) % 2) * 255
+    img[180:240, 0:60] = 4 + 8 * ((xx // 8) % 2)
+    img[240:300, 300:360] = 12 + 16 * ((yy // 4) % 2)
+    return img
+
+
+@pytest.mark.parametrize("q", [(8.0, 8.0, 8.0), (2.0, 0.5, 0.25), (3.0, 1e-3, 0.7), (16.0, 4.0, 1e-3)])
+def test_boundary_heavy_image_vs_oracle(cuda, q):
+    """The fused rings decide cells from fp32 estimates and defer to the fp64
+    sequence only near a boundary: on an image built to put features on
+    boundaries the masks must still equal the oracle's bit for bit."""
+    img = _boundary_image(5)
+    tpl = np.ascontiguousarray(img[30:70, 30:70])
+    compare_with_oracle(img, tpl, {"alpha": 0.6, "beta": 1.6, "ladder_ratio": 1.2, "quantizer": q})
+
+
+@pytest.mark.parametrize("q", [(8.0, 8.0, 8.0), (5.0, 3.0, 2.5)])
+def test_fused_ladder_equals_per_size_path(cuda, monkeypatch, q):
+    """The fused ladder (lock-step sizes, fp32-estimated cells) and the
+    per-size kernels (fp64 sequence everywhere) on the same inputs."""
+    import workloads as WL
+    from paper_1707_05647_b200 import screen
+
+    img = WL.make_image(900, 700, seed=81, sigma=3.0, noise=2.0)
+    case = WL.make_template(img, 82, 48, (0.7, 1.4), std_threshold=10.0)
+    cfg = pcfg({"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.15, "quantizer": q})
+    monkeypatch.setenv("SS_FUSED", "1")
+    a = screen(img, case.template, cfg)
+    monkeypatch.setenv("SS_FUSED", "0")
+    b = screen(img, case.template, cfg)
+    assert a.candidates == b.candidates
+    assert (a.stats.patches_tested, a.stats.patches_kept, a.stats.region_pixels_kept) == (
+        b.stats.patches_tested, b.stats.patches_kept, b.stats.region_pixels_kept)
+    for m in a.ladder:
+        assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
