@@ -181,7 +181,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     unsigned res = 0;
     bool have_res = false;
     unsigned res_base = 0, res_left = 0;
-    unsigned long long n_int = 0, n_pass = 0;
+    unsigned n_int = 0, n_pass = 0;  // per warp: < 2^32
     const bool unit_stride = a.stride == 1;
     for (int it = 0;; ++it) {
         const int s = it % STAGES;
@@ -231,25 +231,36 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         const int tag = y | (sz << TAG_SHIFT);
         const int xt = tx * G::TX;
         const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;  // warp-uniform: no per-lane tests
-        bool pass[CPW];
+        unsigned pm = 0;  // bit c: chunk c's centre passes
+        if (S.bm1 >= 0) {
+            const int cm_lo = R0.cm_lo;
+            const unsigned cm_n = (unsigned)R0.cm_n;
+            const unsigned* bits = sbits + S.bm1;
 #pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-            const int x = xt + 32 * c + lane;
-            const bool interior = full || (x >= xlo && x <= xhi && (unit_stride || (x % a.stride) == 0));
-            bool member;
-            if (S.bm1 >= 0) {
-                const unsigned i = (unsigned)(cm[c] - R0.cm_lo);
-                member = i < (unsigned)R0.cm_n && bit(sbits + S.bm1, (int)i);
-            } else {
-                member = interior && bsearch_eq(a.blob + R0.off_m, R0.n_m, cm[c]);
+            for (int c = 0; c < CPW; ++c) {
+                const unsigned i = (unsigned)(cm[c] - cm_lo);
+                pm |= (unsigned)(i < cm_n && bit(bits, (int)i)) << c;
             }
-            pass[c] = interior && member;
-            if (a.stage_counts) n_int += __popc(__ballot_sync(FULL, interior));
+        } else {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) pm |= (unsigned)bsearch_eq(a.blob + R0.off_m, R0.n_m, cm[c]) << c;
+        }
+        if (!full) {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const int x = xt + 32 * c + lane;
+                const bool interior = x >= xlo && x <= xhi && (unit_stride || (x % a.stride) == 0);
+                if (!interior) pm &= ~(1u << c);
+                if (a.stage_counts) n_int += __popc(__ballot_sync(FULL, interior));
+            }
+        } else if (a.stage_counts) {
+            n_int += 32 * CPW;
         }
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
-            const unsigned pb = __ballot_sync(FULL, pass[c]);
-            if (pass[c]) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
+            const bool p = (pm >> c) & 1u;
+            const unsigned pb = __ballot_sync(FULL, p);
+            if (p) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
             nbuf += __popc(pb);
             n_pass += __popc(pb);
         }
@@ -287,8 +298,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         if (lane < nbuf) list0[base + lane] = buf[lane];
     }
     if (a.stage_counts && lane == 0) {
-        atomicAdd(a.stage_counts + 0, n_int);
-        atomicAdd(a.stage_counts + 1, n_pass);
+        atomicAdd(a.stage_counts + 0, (unsigned long long)n_int);
+        atomicAdd(a.stage_counts + 1, (unsigned long long)n_pass);
     }
 }
 
