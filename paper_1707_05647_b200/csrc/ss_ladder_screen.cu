@@ -645,7 +645,7 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
             // flight) x (strip + max_m) columns of all 12 planes -- fits the L2
             // budget (the rings that follow touch every plane of those rows)
             {
-                int64_t budget = 48ll << 20;
+                int64_t budget = 96ll << 20;  // measured: 96 MB beats 48 MB on configs 2 and 4, equal on 1 and 3
                 if (const char* e = getenv("SS_FUSED_STRIP_BUDGET_MB")) budget = (int64_t)atoi(e) << 20;
                 const int64_t in_flight = (int64_t)sms * s1_per_sm * G::STAGES;
                 tm.strip = 1;
