@@ -319,87 +319,114 @@ __global__ void write_xy_all_kernel(const unsigned* masks, long long mask_pitch,
     (void)H;
 }
 
-// grid (words, sizes): column pass of every size's footprint dilation.
-__global__ void vdilate_all_kernel(const unsigned* masks, long long mask_pitch, long long size_stride, long long words,
-                                   int W, int H, long long P, const Ladder lad, unsigned* V) {
-    extern __shared__ unsigned smem[];
-    const int k = blockIdx.y;
+// K5 (ladder form), pass 1 -- row dilation of every size: H_k(y) bit x =
+// OR of size k's evaluated survivors (interior bits of its mask) in columns
+// [x - hi, x + lo], i.e. the footprint columns (screening.py:316-330).  One
+// warp per (size, row): the row sits in shared memory, F_L(x) = OR S[x,
+// x+L-1] by shift-OR doubling (ping-pong buffers, __syncwarp between steps),
+// then H(x) = F_L(x - hi).  Rows outside the size's interior are zero.
+constexpr int RP_WARPS = 8;
+__global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsigned* masks, long long mask_pitch,
+                                                                    long long size_stride, int W, int H,
+                                                                    long long words, long long P,
+                                                                    const Ladder lad, unsigned* Hb) {
+    extern __shared__ unsigned rsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long task = (long long)blockIdx.x * RP_WARPS + warp;
+    if (task >= (long long)lad.L * H) return;
+    const int k = (int)(task / H), y = (int)(task % H);
     const int m = lad.m[k];
-    const long long w = blockIdx.x;
-    unsigned* Vk = V + (long long)k * H * words;
-    const int lo = (m - 1) / 2, hi = m / 2, L = m;
-    const int x_lo = lo, x_hi = W - 1 - hi, y_lo = lo, y_hi = H - 1 - hi;
-    const long long ext = (long long)H + 2 * P;
-    unsigned* A = smem;
-    unsigned* B = smem + ext;
-    const unsigned cm = (m >= 8) ? interior_bits(w, x_lo, x_hi) : 0u;
-    const unsigned* mk = masks + (long long)k * size_stride;
-    int any = 0;
-    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
-        const long long r = i - P;
-        const unsigned v = (cm && r >= y_lo && r <= y_hi) ? (mk[r * mask_pitch + w] & cm) : 0u;
+    const int lo = (m - 1) / 2, hi = m / 2;
+    unsigned* out = Hb + ((long long)k * H + y) * words;
+    const unsigned* mrow = masks + (long long)k * size_stride + (long long)y * mask_pitch;
+    // F is needed at x - hi >= -hi: the row sits at word offset P of a
+    // left-padded buffer (padding = 0 = no survivors)
+    const long long ext = words + P;
+    unsigned* A = rsm + (size_t)warp * 2 * ext;
+    unsigned* B = A + ext;
+    const bool live = m >= 8 && y >= lo && y <= H - 1 - hi;
+    unsigned any = 0;
+    for (long long i = lane; i < ext; i += 32) {
+        const long long wi = i - P;
+        const unsigned v = (live && wi >= 0) ? (mrow[wi] & interior_bits(wi, lo, W - 1 - hi)) : 0u;
         A[i] = v;
-        any |= (v != 0u);
+        any |= v;
     }
-    if (!__syncthreads_or(any)) {
-        for (long long y = threadIdx.x; y < H; y += blockDim.x) Vk[y * words + w] = 0u;
+    if (!__any_sync(FULL, any != 0u)) {
+        for (long long i = lane; i < words; i += 32) out[i] = 0u;
         return;
     }
+    __syncwarp();
+    const int L = m;
     int l = 1;
     while (2 * l <= L) {
-        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + l < ext ? A[i + l] : 0u);
-        __syncthreads();
+        for (long long i = lane; i < ext; i += 32) B[i] = A[i] | shifted_lo(A, i, ext, l);
+        __syncwarp();
         unsigned* t = A; A = B; B = t;
         l *= 2;
     }
     if (l < L) {
-        const int s = L - l;
-        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | (i + s < ext ? A[i + s] : 0u);
-        __syncthreads();
+        for (long long i = lane; i < ext; i += 32) B[i] = A[i] | shifted_lo(A, i, ext, L - l);
+        __syncwarp();
         unsigned* t = A; A = B; B = t;
-    }
-    for (long long y = threadIdx.x; y < H; y += blockDim.x) Vk[y * words + w] = A[y - hi + P];
-}
-
-// grid (rows, sizes): row pass of every size, OR'ed into the region.
-__global__ void hdilate_all_kernel(const unsigned* V, long long words, long long P, int W, int H, const Ladder lad,
-                                   unsigned* region, long long region_pitch) {
-    extern __shared__ unsigned smem[];
-    const int k = blockIdx.y;
-    const int m = lad.m[k];
-    if (m < 8) return;
-    const int L = m, hi = m / 2;
-    const long long ext = words + 2 * P;
-    unsigned* A = smem;
-    unsigned* B = smem + ext;
-    const int y = blockIdx.x;
-    const unsigned* Vk = V + (long long)k * H * words;
-    int any = 0;
-    for (long long i = threadIdx.x; i < ext; i += blockDim.x) {
-        const long long wi = i - P;
-        const unsigned v = (wi >= 0 && wi < words) ? Vk[(long long)y * words + wi] : 0u;
-        A[i] = v;
-        any |= (v != 0u);
-    }
-    if (!__syncthreads_or(any)) return;
-    int l = 1;
-    while (2 * l <= L) {
-        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, l);
-        __syncthreads();
-        unsigned* tmp = A; A = B; B = tmp;
-        l *= 2;
-    }
-    if (l < L) {
-        for (long long i = threadIdx.x; i < ext; i += blockDim.x) B[i] = A[i] | shifted_lo(A, i, ext, L - l);
-        __syncthreads();
-        unsigned* tmp = A; A = B; B = tmp;
     }
     const unsigned last_mask = (W % 32) ? ((1u << (W % 32)) - 1u) : FULL;
-    for (long long i = threadIdx.x; i < words; i += blockDim.x) {
+    for (long long i = lane; i < words; i += 32) {
         unsigned r = shifted_hi(A, i + P, ext, hi);
         if (i == words - 1) r &= last_mask;
-        if (r) atomicOr(region + (long long)y * region_pitch + i, r);
+        out[i] = r;
     }
+}
+
+// K5 pass 2 -- column dilation of H_k over rows [y - hi, y + lo], OR'ed into
+// the region.  One thread per (size, chunk of C rows, word column): the C
+// windows [r0 + c - hi, r0 + c - hi + L - 1] all contain row b = r0 - hi +
+// L - 1 when L >= C, so each is a suffix-OR of rows [.., b] (computed
+// backwards) | a prefix-OR of rows [b + 1, ..] (forwards): L + C - 1 loads
+// for C outputs (van Herk / Gil-Werman).  Sizes with L < C take every window
+// directly.
+template <int C>
+__global__ void region_cols_kernel(const unsigned* Hb, int H, long long words, long long chunks, const Ladder lad,
+                                   unsigned* region, long long region_pitch) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (long long)lad.L * chunks * words) return;
+    const long long w = gid % words, t = gid / words;
+    const long long ch = t % chunks;
+    const int k = (int)(t / chunks);
+    const int m = lad.m[k];
+    if (m < 8) return;
+    const int lo = (m - 1) / 2, hi = m / 2, L = m;
+    const unsigned* col = Hb + (long long)k * H * words + w;
+    auto ld = [&](int j) -> unsigned { return (j >= 0 && j < H) ? __ldg(col + (long long)j * words) : 0u; };
+    const int r0 = (int)(ch * C);
+    unsigned out[C];
+    if (L >= C) {
+        const int a0 = r0 - hi, b = a0 + L - 1;
+        unsigned s = 0;
+#pragma unroll 4
+        for (int j = b; j >= a0 + C; --j) s |= ld(j);
+#pragma unroll
+        for (int c = C - 1; c >= 0; --c) {
+            s |= ld(a0 + c);
+            out[c] = s;
+        }
+        unsigned p = 0;
+#pragma unroll
+        for (int c = 1; c < C; ++c) {
+            p |= ld(b + c);
+            out[c] |= p;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            unsigned v = 0;
+            for (int j = r0 + c - hi; j <= r0 + c + lo; ++j) v |= ld(j);
+            out[c] = v;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+        if (out[c] && r0 + c < H) atomicOr(region + (long long)(r0 + c) * region_pitch + w, out[c]);
 }
 
 // f4: bit-packed mask rows -> one byte per pixel, 255 kept / 0 not
@@ -546,28 +573,35 @@ int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stri
     int m_max = 1;
     for (int k = 0; k < L; ++k) m_max = std::max(m_max, (int)h_m[k]);
     const int64_t words = (W + 31) / 32;
-    unsigned* V = static_cast<unsigned*>(d_ws);
+    unsigned* Hb = static_cast<unsigned*>(d_ws);
     cudaStream_t s = as_stream(stream);
     {
-        const int64_t P = m_max;
-        const size_t smem = (size_t)2 * (H + 2 * P) * 4;
-        if (smem > 227 * 1024) { set_error("image too tall for the region pass"); return SS_EINVAL; }
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(vdilate_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        vdilate_all_kernel<<<dim3((unsigned)words, (unsigned)L), 1024, smem, s>>>(d_masks, mask_pitch, size_stride, words,
-                                                                                (int)W, (int)H, P, lad, V);
+        const int64_t P = m_max / 32 + 2;  // left padding (words) >= ceil(hi / 32)
+        const size_t smem = (size_t)RP_WARPS * 2 * (words + P) * 4;
+        if (smem > 227 * 1024) { set_error("image too wide for the region pass"); return SS_EINVAL; }
+        static std::atomic<size_t> raised{0};
+        if (smem > 48 * 1024 && smem > raised.load()) {
+            cudaFuncSetAttribute(region_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            raised.store(smem);
+        }
+        const long long tasks = (long long)L * H;
+        region_rows_kernel<<<(unsigned)((tasks + RP_WARPS - 1) / RP_WARPS), RP_WARPS * 32, smem, s>>>(
+            d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb);
         note_launch();
-        if (int e = check_launch("vdilate_all_kernel")) return e;
+        if (int e = check_launch("region_rows_kernel")) return e;
     }
-    const int64_t P = (m_max + 31) / 32 + 1;
-    const int threads = (int)std::min<int64_t>(1024, ((words + 2 * P + 31) / 32) * 32);
-    const size_t smem = (size_t)2 * (words + 2 * P) * 4;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(hdilate_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    hdilate_all_kernel<<<dim3((unsigned)H, (unsigned)L), threads, smem, s>>>(V, words, P, (int)W, (int)H, lad, d_region,
-                                                                             mask_pitch);
+    // taller footprints take longer row chunks (loads per output (L + C - 1) / C)
+    const bool tall = m_max >= 128;
+    const int C = tall ? 32 : 16;
+    const long long chunks = (H + C - 1) / C;
+    const long long threads = (long long)L * chunks * words;
+    const unsigned grid = (unsigned)((threads + 127) / 128);
+    if (tall)
+        region_cols_kernel<32><<<grid, 128, 0, s>>>(Hb, (int)H, words, chunks, lad, d_region, mask_pitch);
+    else
+        region_cols_kernel<16><<<grid, 128, 0, s>>>(Hb, (int)H, words, chunks, lad, d_region, mask_pitch);
     note_launch();
-    return check_launch("hdilate_all_kernel");
+    return check_launch("region_cols_kernel");
 }
 
 int bits_to_bytes(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, uint8_t* d_out, void* stream) {
