@@ -306,12 +306,15 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
 // Border keeps of every fused size (screening.py:438-442): rows [y_begin,
 // y_end) of each mask get the grid centres outside the size's interior; the
 // interior bits start at 0 and the rings kernel ORs its survivors in.
-__global__ void ladder_border_kernel(const __grid_constant__ FusedArgs a) {
+__global__ void ladder_border_kernel(const __grid_constant__ FusedArgs a, unsigned* ctrs, int ctr_words) {
     const int words = (a.W + 31) >> 5;
     const SizeDev& S = a.size[blockIdx.z];
     const int xlo = S.lo, xhi = a.W - 1 - S.hi;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)  // the band's tile / list / group counters
+        for (int i = threadIdx.x; i < ctr_words; i += blockDim.x) ctrs[i] = 0u;
     for (int y = a.y_begin + blockIdx.y; y < a.y_end; y += gridDim.y) {
         unsigned* row = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
+        if (blockIdx.x == 0 && threadIdx.x == 0) S.row_counts[y - a.mask_y0] = 0u;
         const bool row_grid = a.stride == 1 || y % a.stride == 0;
         const bool row_int = row_grid && y >= S.lo && y <= a.H - 1 - S.hi;
         for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
@@ -485,6 +488,36 @@ size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms) {
     return FCTR_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * sizeof(int2);
 }
 
+// The three PLAIN-plane TMA descriptors (SAT / E / O) of a plane buffer,
+// cached per (buffer, geometry): an engine screens from the same planes every
+// call, and encoding costs host time on the critical path of screen().
+int plane_maps_cached(TmaMaps& maps, const void* planes, int eb, int bw, int64_t W, int64_t h, int64_t pitch,
+                      long long ps) {
+    using Key = std::tuple<const void*, int, int, int64_t, int64_t, int64_t, int>;
+    static std::mutex mu;
+    static std::map<Key, TmaMaps> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{planes, eb, bw, W, h, pitch, dev};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const auto it = cache.find(key);
+        if (it != cache.end()) {
+            maps = it->second;
+            return SS_OK;
+        }
+    }
+    const char* base = static_cast<const char*>(planes);
+    const size_t pb = (size_t)ps * eb;
+    if (int e = encode_plane_map(&maps.sat, base, eb, bw, W, h, pitch)) return e;
+    if (int e = encode_plane_map(&maps.e, base + 4 * pb, eb, bw, W, h, pitch)) return e;
+    if (int e = encode_plane_map(&maps.o, base + 8 * pb, eb, bw, W, h, pitch)) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 256) cache.clear();  // buffers come and go with engines; bound the cache
+    cache[key] = maps;
+    return SS_OK;
+}
+
 }  // namespace
 
 size_t screen_workspace_bytes(int64_t W, int64_t rows);  // ss_screen.cu
@@ -605,18 +638,11 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + TY - 1) / TY * TY;
     if (!d_ws || fused_ws_bytes(W, band, n, sms) > ws_bytes) return SS_DECLINED;
 
-    for (int j = 0; j < n; ++j)
-        if (cudaMemsetAsync(a.size[j].row_counts, 0, (size_t)rows * sizeof(uint32_t), s) != cudaSuccess)
-            return check_launch("memset");
+    // (row counts and workspace counters are zeroed by ladder_border_kernel)
     TmaMaps maps;
-    {
-        const char* base = static_cast<const char*>(planes);
-        const int bw = eb == 4 ? GeoF<unsigned>::BW : GeoF<long long>::BW;
-        const size_t pb = (size_t)a.ps * eb;
-        if (int e = encode_plane_map(&maps.sat, base, eb, bw, W, h, pitch)) return e;
-        if (int e = encode_plane_map(&maps.e, base + 4 * pb, eb, bw, W, h, pitch)) return e;
-        if (int e = encode_plane_map(&maps.o, base + 8 * pb, eb, bw, W, h, pitch)) return e;
-    }
+    if (int e = plane_maps_cached(maps, planes, eb, eb == 4 ? GeoF<unsigned>::BW : GeoF<long long>::BW, W, h, pitch,
+                                  a.ps))
+        return e;
     unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
     unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
     unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
@@ -660,11 +686,10 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
             }
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
-            if (cudaMemsetAsync(d_ws, 0, FCTR_BYTES, s) != cudaSuccess) return check_launch("memset");
             {
                 const int words = (int)((W + 31) / 32);
                 const dim3 bg((unsigned)((words + 127) / 128), (unsigned)std::min<int64_t>(brows, 65535), (unsigned)n);
-                ladder_border_kernel<<<bg, 128, 0, s>>>(a);
+                ladder_border_kernel<<<bg, 128, 0, s>>>(a, static_cast<unsigned*>(d_ws), (int)(FCTR_BYTES / 4));
                 note_launch();
                 if (int e = check_launch("ladder_border_kernel")) return e;
             }

@@ -238,7 +238,8 @@ def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optiona
     if not tp.blobs.size:
         tp.blobs = np.zeros(1, np.int64)
     if dev.type == "cuda":
-        tp.blobs_dev = torch.from_numpy(tp.blobs).pin_memory().to(dev, non_blocking=True)
+        # a few KB-MB: a pageable copy costs less host time than pinning a fresh buffer
+        tp.blobs_dev = torch.from_numpy(tp.blobs).to(dev, non_blocking=True)
 
 
 def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device,

@@ -175,6 +175,25 @@ def instance_descriptors(ms, ring_count: int, ladder_ratio: float):
     return np.ascontiguousarray(desc), np.array(nk, np.int32)
 
 
+_desc_cache: dict = {}
+
+
+def _device_desc(desc: np.ndarray, dev):
+    """Device copy of a (read-only, geometry-cached) descriptor array, kept
+    per (array, device): the descriptors of a ladder geometry never change."""
+    key = (id(desc), str(dev))
+    hit = _desc_cache.get(key)
+    if hit is not None and hit[0] is desc:
+        return hit[1]
+    if len(_desc_cache) > 64:
+        _desc_cache.clear()
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(desc)).to(dev)  # synchronous: complete before any stream uses it
+    _desc_cache[key] = (desc, t)
+    return t
+
+
 def launch_template_features(template: np.ndarray, desc: np.ndarray, device, stream=None):
     """Enqueue the ring features of the rescale instances `desc`
     (instance_descriptors) of the template: one GPU launch (f2,
@@ -192,8 +211,8 @@ def launch_template_features(template: np.ndarray, desc: np.ndarray, device, str
     dev = torch.device(device)
     stream = stream or torch.cuda.current_stream(dev)
     with torch.cuda.stream(stream):
-        d_desc = torch.from_numpy(desc).pin_memory().to(dev, non_blocking=True)
-        d_tpl = torch.from_numpy(tpl).pin_memory().to(dev, non_blocking=True)
+        d_desc = _device_desc(desc, dev)
+        d_tpl = torch.from_numpy(tpl).to(dev, non_blocking=True)  # a few KB: the pageable copy is cheaper than pinning
         d_out = torch.empty((desc.shape[0], SS_MAX_RINGS, 3), dtype=torch.float64, device=dev)
         _native.check(_native.lib().ss_template_features_device(
             d_tpl.data_ptr(), n, desc.shape[0], d_desc.data_ptr(), DESC_STRIDE, d_out.data_ptr(), stream.cuda_stream),
