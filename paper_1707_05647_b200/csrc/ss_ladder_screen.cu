@@ -349,7 +349,7 @@ struct SizeSm {
 // ss_screen.cu for the batching / queue scheme); lanes of one batch may
 // belong to different sizes: each reads its size's ring from shared memory.
 template <typename T>
-__global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB)
+__global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     ladder_rings_kernel(const __grid_constant__ FusedArgs a, int parts, const int2* list_base, long long part_cap,
                         const unsigned* list_ctr, unsigned* group_ctr) {
     extern __shared__ __align__(16) unsigned char rsm[];

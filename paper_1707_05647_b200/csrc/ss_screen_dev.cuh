@@ -4,6 +4,13 @@
 // (SURVEY.md App. A), TMA + mbarrier wrappers, stage-1 tile geometry.
 // Internal: included only by translation units compiled with -fmad=false.
 #pragma once
+
+#ifndef EVAL_TWO_PHASE
+#define EVAL_TWO_PHASE 1  // eval_ring_fast: X / Y corners loaded after the std test (63 registers: 4 CTAs / SM)
+#endif
+#ifndef FUSED_RINGS_MINB
+#define FUSED_RINGS_MINB 4  // measured: config 1 K3 -3.4%, config 4 -12% vs one-phase loads at 3 CTAs / SM
+#endif
 #include <cuda.h>
 
 #include <atomic>
@@ -311,8 +318,10 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
     Corners<T> c0, c2, ckx, cky;
     load_corners(P, R, 0, c0);
     load_corners(P, R, 3, c2);
+#if !EVAL_TWO_PHASE
     load_corners(P, R, 1, ckx);
     load_corners(P, R, 2, cky);
+#endif
     const long long s1q = unsigned_sum(sq_of(c0)), s1d = unsigned_sum(di_of(c0));
     const int cm = mean_cell(a, R, s1q, s1d);  // features.py:365 (level 0 entries passed this test in stage 1)
     if (level > 0 && !member_m(a, R, sb, cm)) return false;
@@ -329,6 +338,10 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
         cs = std_cell_exact(a, R, mq, md, s2q, s2d);
     }
     if (!member_ms(a, R, sb, cm, cs)) return false;
+#if EVAL_TWO_PHASE
+    load_corners(P, R, 1, ckx);  // X / Y planes only for (mean, std) members
+    load_corners(P, R, 2, cky);
+#endif
     // gradient: exact centred moments; square offset c + 1.5 => numerator 2D - s1 over 2 w1
     const long long dxq = centred(sq_of(ckx), cx + 1, s1q), dyq = centred(sq_of(cky), cy + 1, s1q);
     const long long dxd = centred(di_of(ckx), cx + 1, s1d), dyd = centred(di_of(cky), cy + 1, s1d);
