@@ -401,8 +401,13 @@ def run_ours(args):
         12 * 4.0 * sum(cnt for sp, cnt in zip(tp.sizes, per_size) if sp.fits32) / max(positions, 1)
     cascade_bytes = 24.0 * stage[0] + 72.0 * stage[1] + positions / 8.0
     traffic, traffic_src = k3_traffic(wl.name, len(cases))
+    # the 12 planes read exactly once per step (32-bit cells, + int64 cells when a size needs them)
+    plane_once = len(cases) * (int(eng.L.ss_tables32_bytes(eng.W, eng.rows)) +
+                               (int(eng.L.ss_tables_bytes(eng.W, eng.rows)) if eng.needs_int64(tp) else 0))
     roofline = {
-        "bound": "hbm", "kernel": "screen (K3: stage1_kernel + rings_kernel, all ladder sizes of one step)",
+        "bound": "hbm",
+        "kernel": ("screen (K3: fused ladder -- ladder_border + ladder_stage1 + ladder_rings kernels -- or, with "
+                   "SS_FUSED=0, stage1_kernel + rings_kernel per size; all ladder sizes of one step)"),
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": peak_src,
@@ -415,6 +420,12 @@ def run_ours(args):
         "cascade": {"ring0_evals": stage[0], "ring0_mean_pass": stage[1], "ring0_pass": stage[2],
                     "survivors": stage[3]},
         "screen_ms_per_step": screen_ms, "screen_share_of_step": screen_ms / (total_ms / args.steps),
+        "frac_note": ("achieved = SURVEY 8(d)'s algorithmic bytes (every plane read once per ladder size) / K3 time; "
+                      "the fused ladder reads each plane about once per row band for all sizes, so frac can exceed 1; "
+                      "dram_GBps / dram_frac are the measured K3 DRAM traffic over the same time"),
+        "plane_once_bytes_per_step": plane_once,
+        "dram_GBps": (traffic / (screen_ms / 1e3) / 1e9) if traffic else None,
+        "dram_frac": (traffic / (screen_ms / 1e3) / 1e9 / peak) if traffic else None,
     }
     if batch:
         roofline["screen_ms_note"] = ("batch: one image's K3 time (one engine, nothing overlapping) x the step's "
