@@ -42,6 +42,21 @@ def test_layout_queries():
     assert L.ss_version() == 1
 
 
+def test_ladder_workspace_query():
+    """The fused ladder's workspace: at least the per-size screen's (the
+    fallback shares it), grows with the sizes screened in lock-step, and is
+    capped (taller images run in row bands)."""
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    for W, H in ((512, 512), (2048, 2048), (1920, 1080)):
+        one = L.ss_ladder_workspace_bytes(W, H, 1)
+        assert one >= L.ss_screen_workspace_bytes(W, H)
+        assert L.ss_ladder_workspace_bytes(W, H, 9) > one
+    big = L.ss_ladder_workspace_bytes(16384, 16384, 33)
+    assert big <= max(5 << 30, L.ss_screen_workspace_bytes(16384, 16384))
+
+
 def test_argument_errors_map_to_value_error():
     from paper_1707_05647_b200 import _native
 
