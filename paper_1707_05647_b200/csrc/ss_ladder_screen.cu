@@ -81,6 +81,17 @@ template <typename T> struct GeoF {
 };
 constexpr int TXMAX = 128;  // widest fused tile (workspace sizing)
 
+// A stage-1 tile and the constants of its size, written by the producer next
+// to the tile's boxes (the consumers read 4 x 16 B instead of indexing the
+// parameter block per tile).
+struct __align__(16) TileConst {
+    int tx, ty, sz, ylo;
+    int yhi, xlo, xhi, bm1;
+    int qr, ql, po0, po1;  // corner columns inside the staged boxes
+    float fa, fb;
+    int cm_lo, cm_n;
+};
+
 // strip-major; inside a strip: tile row, then size, then tile column
 __device__ __forceinline__ void tile_coords_f(const TileMapF& t, long long idx, int& tx, int& ty, int& s) {
     const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty * (unsigned)t.n_sizes;
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-    __shared__ int4 tile_info[STAGES];  // (tx, ty, size) of the tile in each stage
+    __shared__ TileConst tile_info[STAGES];  // the tile in each stage and its size's constants
     __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
@@ -147,14 +158,33 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                 if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 if (t >= tm.n_tiles) {
-                    tile_info[s] = make_int4(-1, -1, -1, 0);
+                    tile_info[s].tx = -1;
                     mbar_arrive(&full_bar[s]);
                     break;
                 }
                 int tx, ty, sz;
                 tile_coords_f(tm, t, tx, ty, sz);
-                tile_info[s] = make_int4(tx, ty, sz, 0);
-                const RingDev& R0 = a.ring[a.size[sz].ring0];
+                const SizeDev& S = a.size[sz];
+                const RingDev& R0 = a.ring[S.ring0];
+                {  // published to the consumers by the mbarrier arrive (complete_tx) below
+                    TileConst& tcst = tile_info[s];
+                    tcst.tx = tx;
+                    tcst.ty = ty;
+                    tcst.sz = sz;
+                    tcst.ylo = S.lo;
+                    tcst.yhi = a.H - 1 - S.hi;
+                    tcst.xlo = S.lo;
+                    tcst.xhi = a.W - 1 - S.hi;
+                    tcst.bm1 = S.bm1;
+                    tcst.qr = G::rem(R0.n + 1);
+                    tcst.ql = G::rem(1 - R0.n);
+                    tcst.po0 = G::rem(-R0.d);
+                    tcst.po1 = G::rem(R0.d + 1);
+                    tcst.fa = R0.fa;
+                    tcst.fb = R0.fb;
+                    tcst.cm_lo = R0.cm_lo;
+                    tcst.cm_n = R0.cm_n;
+                }
                 const int x0 = tx * G::TX;
                 const int cy0 = a.y_begin + ty * TY - a.y_origin;
                 unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
@@ -186,19 +216,16 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
-        const int4 ti = tile_info[s];
-        if (ti.x < 0) break;
-        const int tx = ti.x, ty = ti.y, sz = ti.z;
-        const SizeDev& S = a.size[sz];
-        const RingDev& R0 = a.ring[S.ring0];
+        const TileConst tc = tile_info[s];
+        if (tc.tx < 0) break;
+        const int tx = tc.tx, ty = tc.ty, sz = tc.sz;
         const int y = a.y_begin + ty * TY + warp;
         // border keeps are already in the masks (ladder_border_kernel); only
         // interior centres of interior grid rows are evaluated here
-        const bool row_int = y < a.y_end && y >= S.lo && y <= a.H - 1 - S.hi && (unit_stride || (y % a.stride) == 0);
+        const bool row_int = y < a.y_end && y >= tc.ylo && y <= tc.yhi && (unit_stride || (y % a.stride) == 0);
         T s1q[CPW], s1d[CPW];  // exact PLAIN region sums
         if (row_int) {
-            const int qr = G::rem(R0.n + 1), ql = G::rem(1 - R0.n), pe = 1, po0 = G::rem(-R0.d),
-                      po1 = G::rem(R0.d + 1);
+            const int qr = tc.qr, ql = tc.ql, pe = 1, po0 = tc.po0, po1 = tc.po1;
             const T* box = reinterpret_cast<const T*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
 #pragma unroll
             for (int c = 0; c < CPW; ++c) {
@@ -217,31 +244,33 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         unsigned amb = 0;
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
-            const float tf = fmaf(to_f32(s1q[c]), R0.fa, fmaf(to_f32(s1d[c]), R0.fb, 0.5f));
+            const float tf = fmaf(to_f32(s1q[c]), tc.fa, fmaf(to_f32(s1d[c]), tc.fb, 0.5f));
             const float dl = fmaf(tf, 4e-6f, 4e-6f);
             cm[c] = (int)floorf(tf - dl);
             amb |= (unsigned)(cm[c] != (int)floorf(tf + dl)) << c;
         }
         if (__any_sync(FULL, amb != 0)) {
+            const RingDev& R0 = a.ring[a.size[sz].ring0];
 #pragma unroll
             for (int c = 0; c < CPW; ++c)
                 if ((amb >> c) & 1u) cm[c] = mean_cell_exact(a, R0, s1q[c], s1d[c]);
         }
-        const int xlo = S.lo, xhi = a.W - 1 - S.hi;
+        const int xlo = tc.xlo, xhi = tc.xhi;
         const int tag = y | (sz << TAG_SHIFT);
         const int xt = tx * G::TX;
         const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;  // warp-uniform: no per-lane tests
         unsigned pm = 0;  // bit c: chunk c's centre passes
-        if (S.bm1 >= 0) {
-            const int cm_lo = R0.cm_lo;
-            const unsigned cm_n = (unsigned)R0.cm_n;
-            const unsigned* bits = sbits + S.bm1;
+        if (tc.bm1 >= 0) {
+            const int cm_lo = tc.cm_lo;
+            const unsigned cm_n = (unsigned)tc.cm_n;
+            const unsigned* bits = sbits + tc.bm1;
 #pragma unroll
             for (int c = 0; c < CPW; ++c) {
                 const unsigned i = (unsigned)(cm[c] - cm_lo);
                 pm |= (unsigned)(i < cm_n && bit(bits, (int)i)) << c;
             }
         } else {
+            const RingDev& R0 = a.ring[a.size[sz].ring0];
 #pragma unroll
             for (int c = 0; c < CPW; ++c) pm |= (unsigned)bsearch_eq(a.blob + R0.off_m, R0.n_m, cm[c]) << c;
         }
@@ -443,6 +472,21 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         const int sz = valid ? (e.y >> TAG_SHIFT) : 0, y = e.y & YMASK;
         const SizeSm S = ssize[sz];
         const bool pass = valid && eval_ring_fast<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin);
+#if RINGS_STATS
+        if (valid && pass) atomicAdd(a.stage_counts + 7 + 4 * level, 1ull);
+        if (valid && level == 0) {  // would the means of all deeper rings pass?
+            bool all = true;
+            const PlanePtrs<T> P = plane_ptrs<T>(a, y - a.y_origin, e.x);
+            for (int l = 1; l < S.n_rings && all; ++l) {
+                const RingDev& Rl = sring[S.ring0 + l];
+                Corners<T> c0;
+                load_corners(P, Rl, 0, c0);
+                all = member_m(a, Rl, sbits, mean_cell(a, Rl, unsigned_sum(sq_of(c0)), unsigned_sum(di_of(c0))));
+            }
+            if (all) atomicAdd(a.stage_counts + 20, 1ull);
+            if (all && pass) atomicAdd(a.stage_counts + 21, 1ull);
+        }
+#endif
         const bool last = level + 1 == S.n_rings;
         const unsigned pb = __ballot_sync(FULL, pass);
         if (level == 0) n_pass0 += __popc(pb);

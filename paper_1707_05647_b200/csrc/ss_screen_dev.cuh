@@ -324,7 +324,13 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
 #endif
     const long long s1q = unsigned_sum(sq_of(c0)), s1d = unsigned_sum(di_of(c0));
     const int cm = mean_cell(a, R, s1q, s1d);  // features.py:365 (level 0 entries passed this test in stage 1)
+#if RINGS_STATS
+    atomicAdd(a.stage_counts + 4 + 4 * level, 1ull);
+#endif
     if (level > 0 && !member_m(a, R, sb, cm)) return false;
+#if RINGS_STATS
+    atomicAdd(a.stage_counts + 5 + 4 * level, 1ull);
+#endif
     // std: exact integer variances V = s2 * count - s1^2 (>= 0)
     const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
     const long long vq = s2q * R.icq - s1q * s1q, vd = s2d * R.icd - s1d * s1d;
@@ -338,6 +344,9 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
         cs = std_cell_exact(a, R, mq, md, s2q, s2d);
     }
     if (!member_ms(a, R, sb, cm, cs)) return false;
+#if RINGS_STATS
+    atomicAdd(a.stage_counts + 6 + 4 * level, 1ull);
+#endif
 #if EVAL_TWO_PHASE
     load_corners(P, R, 1, ckx);  // X / Y planes only for (mean, std) members
     load_corners(P, R, 2, cky);
