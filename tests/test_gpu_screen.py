@@ -332,3 +332,15 @@ def test_fused_ladder_equals_per_size_path(cuda, monkeypatch, q):
         b.stats.patches_tested, b.stats.patches_kept, b.stats.region_pixels_kept)
     for m in a.ladder:
         assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
+
+
+def test_fused_ladder_declines_to_per_size_path(cuda):
+    """A ladder whose rings exceed the fused parameter block (37 sizes, 111
+    rings > 104) is screened size by size on the same stream: still equal to
+    the oracle."""
+    import workloads as WL
+
+    img = WL.make_image(320, 280, seed=91, sigma=2.5, noise=2.0)
+    case = WL.make_template(img, 92, 48, (0.8, 1.3), std_threshold=10.0)
+    compare_with_oracle(img, case.template, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.04,
+                                             "quantizer": (8.0, 8.0, 8.0)})
