@@ -138,6 +138,15 @@ size_t ss_screen_workspace_bytes(int64_t W, int64_t rows);
  */
 int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, unsigned long long* d_mismatches,
                     void* stream);
+/*
+ * Device self-test of the fused screen's fp32-estimated cells: n random
+ * region-sum tuples an 8-bit image can produce for ring (ring_n, ring_d),
+ * 3 in 4 aimed within ~1e-6 of a std / gradient cell boundary; adds the std
+ * and gradient cells that differ from the fp64 reference sequence to
+ * d_counts[0] and d_counts[1].
+ */
+int ss_selftest_cells(uint64_t n, uint64_t seed, int32_t ring_n, int32_t ring_d, double q_mean, double q_std,
+                      double q_grad, unsigned long long* d_counts, void* stream);
 
 /*
  * The whole ladder loop of screen() (screening.py:502-520) in one call: for

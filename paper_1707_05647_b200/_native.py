@@ -45,6 +45,7 @@ _SIGS = {
     "ss_screen_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "ss_ladder_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
     "ss_selftest_div": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, c_d, c_i32, c_p, c_p]),
+    "ss_selftest_cells": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, c_i32, c_i32, c_d, c_d, c_d, c_p, c_p]),
     "ss_fill_grid": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i32, c_p, c_i64, c_p, c_p]),
     "ss_screen_ladder": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
                                         c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_i64, c_p, c_i64,

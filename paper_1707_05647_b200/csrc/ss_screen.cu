@@ -38,6 +38,7 @@
 #include <mutex>
 #include <set>
 #include <tuple>
+#include <vector>
 
 #include <cuda.h>
 
@@ -389,6 +390,70 @@ __global__ void fill_grid_kernel(int W, int y_begin, int y_end, int stride, unsi
     if (w == 0) row_counts[row] = 0;
 }
 
+// The fused rings' fp32-estimate cells (std_cell_fast, grad_cell_fast) vs
+// the fp64 reference sequence (std_cell_exact, grad_cell_exact) on random
+// region sums an 8-bit image can produce (0 <= s1 <= 255 count, s1^2 / count
+// <= s2 <= 255 s1), most of them aimed at a std / gradient cell boundary:
+// counts[0] std mismatches, counts[1] gradient mismatches.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long h) {
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 27;
+    h *= 0x94D049BB133111EBull;
+    return h ^ (h >> 31);
+}
+__global__ void selftest_cells_kernel(unsigned long long n, unsigned long long seed, const ScreenArgs a,
+                                      unsigned long long* counts) {
+    const RingDev& R = a.ring[0];
+    unsigned long long bad_s = 0, bad_g = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        unsigned long long h = mix64((i + 1) * 0x9E3779B97F4A7C15ull + seed);
+        auto uni = [&]() {  // uniform in [0, 1)
+            h = mix64(h + 0x9E3779B97F4A7C15ull);
+            return (double)(h >> 11) * 0x1.0p-53;
+        };
+        const bool aim = (i & 3) != 0;  // 3 in 4 samples aimed at a boundary
+        // means and a std split around a target
+        const double mq = 255.0 * uni(), md = fmin(255.0, fmax(0.0, mq + 40.0 * (uni() - 0.5)));
+        double sq_t = 60.0 * uni(), sd_t = 60.0 * uni();
+        if (aim) {  // (sq + sd) / 2 near qs (k - 1/2), k = 1..8
+            const double target = a.qs * (double)(1 + (int)(8.0 * uni()) - 0.5) * (1.0 + 1e-6 * (uni() - 0.5));
+            const double split = uni();
+            sq_t = 2.0 * target * split;
+            sd_t = 2.0 * target * (1.0 - split);
+        }
+        auto sums = [&](int cnt, double mean, double sdev, long long& s1, long long& s2) {
+            s1 = llrint(mean * cnt);
+            s1 = s1 < 0 ? 0 : (s1 > 255LL * cnt ? 255LL * cnt : s1);
+            long long lo = (s1 * s1 + cnt - 1) / cnt, hi = 255 * s1;
+            long long v = llrint((double)cnt * ((double)s1 / cnt * ((double)s1 / cnt) + sdev * sdev));
+            s2 = v < lo ? lo : (v > hi ? hi : v);
+        };
+        long long s1q, s2q, s1d, s2d;
+        sums(R.icq, mq, sq_t, s1q, s2q);
+        sums(R.icd, md, sd_t, s1d, s2d);
+        if (std_cell_fast(a, R, s1q, s1d, s2q, s2d) !=
+            std_cell_exact(a, R, div_rn((double)s1q, R.cnt_sq, R.rcp_sq), div_rn((double)s1d, R.cnt_di, R.rcp_di), s2q, s2d))
+            ++bad_s;
+        // gradient: components of a target magnitude split between square and diamond
+        double gm_t = 200.0 * uni();
+        if (aim) gm_t = a.qg * (double)(1 + (int)(8.0 * uni()) - 0.5) * (1.0 + 1e-6 * (uni() - 0.5));
+        const double th = 6.283185307179586 * uni(), dx = 30.0 * (uni() - 0.5), dy = 30.0 * (uni() - 0.5);
+        const double gx = gm_t * cos(th), gy = gm_t * sin(th);
+        const int cx = (int)(16384.0 * uni()), cy = (int)(16384.0 * uni());
+        const long long dxq = llrint(((gx + dx) * 2.0 * R.w1_sq + (double)s1q) * 0.5);
+        const long long dyq = llrint(((gy + dy) * 2.0 * R.w1_sq + (double)s1q) * 0.5);
+        const long long dxd = llrint((gx - dx) * R.w1_di), dyd = llrint((gy - dy) * R.w1_di);
+        if (grad_cell_fast(a, R, cx, cy, s1q, s1d, dxq, dyq, dxd, dyd) !=
+            grad_cell_exact(a, R, cx, cy, s1q, s1d, (long long)(cx + 1) * s1q + dxq, (long long)(cy + 1) * s1q + dyq,
+                            (long long)(cx + 1) * s1d + dxd, (long long)(cy + 1) * s1d + dyd))
+            ++bad_g;
+    }
+    if (bad_s) atomicAdd(counts + 0, bad_s);
+    if (bad_g) atomicAdd(counts + 1, bad_g);
+}
+
 // div_rn vs IEEE division on n operands of a family (mode), divisor b.
 __global__ void selftest_div_kernel(unsigned long long n, unsigned long long seed, double b, int mode,
                                     unsigned long long* bad) {
@@ -651,6 +716,35 @@ int fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_
     return check_launch("fill_grid_kernel");
 }
 
+int selftest_cells(uint64_t n, uint64_t seed, int32_t ring_n, int32_t ring_d, double qm, double qs, double qg,
+                   unsigned long long* d_counts, void* stream) {
+    if (ring_n < 1 || ring_d < 1 || ring_n > 1024 || ring_d > 1448 || !(qm > 0) || !(qs > 0) || !(qg > 0) || !d_counts) {
+        set_error("bad selftest arguments");
+        return SS_EINVAL;
+    }
+    std::vector<unsigned char> buf(sizeof(ScreenArgs), 0);
+    ScreenArgs& a = *reinterpret_cast<ScreenArgs*>(buf.data());
+    a.qm = qm;
+    a.qs = qs;
+    a.qg = qg;
+    a.rqm = 1.0 / qm;
+    a.rqs = 1.0 / qs;
+    a.rqg = 1.0 / qg;
+    a.qpow2 = quant_pow2_bits(qm, qs, qg);
+    a.rqs_f = (float)(1.0 / qs);
+    a.rqg_f = (float)(1.0 / qg);
+    a.band_s = (float)(1e-5 / qs);
+    // ring constants only (no key blob): a one-ring header with no keys
+    int64_t hd[SS_BLOB_HDR] = {};
+    hd[12] = -1;
+    int bm_words = 0;
+    const int m = 2 * std::max<int>(ring_n, ring_d + 1) + 2;
+    if (int e = fill_ring(a.ring[0], ring_n, ring_d, m, 1 << 20, qm, hd, 0, bm_words, 0)) return e;
+    selftest_cells_kernel<<<148 * 8, 256, 0, as_stream(stream)>>>(n, seed, a, d_counts);
+    note_launch();
+    return check_launch("selftest_cells_kernel");
+}
+
 int selftest_div(uint64_t n, uint64_t seed, double b, int mode, unsigned long long* d_bad, void* stream) {
     if (b <= 0.0 || mode < 0 || mode > 3) { set_error("bad selftest arguments"); return SS_EINVAL; }
     selftest_div_kernel<<<148 * 16, 256, 0, as_stream(stream)>>>(n, seed, b, mode, d_bad);
@@ -681,6 +775,10 @@ size_t ss_screen_workspace_bytes(int64_t W, int64_t rows) { return ss::screen_wo
 int ss_fill_grid(int64_t W, int64_t y_begin, int64_t y_end, int32_t stride, uint32_t* d_mask,
                  int64_t mask_pitch_words, uint32_t* d_row_counts, void* stream) {
     return ss::fill_grid(W, y_begin, y_end, stride, d_mask, mask_pitch_words, d_row_counts, stream);
+}
+int ss_selftest_cells(uint64_t n, uint64_t seed, int32_t ring_n, int32_t ring_d, double q_mean, double q_std,
+                      double q_grad, unsigned long long* d_counts, void* stream) {
+    return ss::selftest_cells(n, seed, ring_n, ring_d, q_mean, q_std, q_grad, d_counts, stream);
 }
 int ss_selftest_div(uint64_t n, uint64_t seed, double divisor, int32_t mode, unsigned long long* d_mismatches,
                     void* stream) {

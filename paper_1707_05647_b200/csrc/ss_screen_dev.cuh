@@ -291,9 +291,52 @@ __device__ __forceinline__ long long centred(long long v, int c1, long long s1) 
 
 // A cell floor(t) from an fp32 estimate tf with |tf - t| <= band: exact
 // unless [tf - band, tf + band] straddles an integer (returns false then).
+#ifndef CELL_BAND_SCALE
+#define CELL_BAND_SCALE 1.0f  // test hook: 0 disables the fp64 fallback (the self-test must then fail)
+#endif
 __device__ __forceinline__ bool cell_of(float tf, float band, int& cell) {
+    band *= CELL_BAND_SCALE;
     cell = (int)floorf(tf - band);
     return cell == (int)floorf(tf + band);
+}
+
+// std cell from the exact integer variances V = s2 * count - s1^2 (>= 0):
+// fp32 estimate, the fp64 reference sequence only within its error band of a
+// boundary (bounds: eval_ring_fast).
+template <class A>
+__device__ __forceinline__ int std_cell_fast(const A& a, const RingDev& R, long long s1q, long long s1d, long long s2q,
+                                             long long s2d) {
+    const long long vq = s2q * R.icq - s1q * s1q, vd = s2d * R.icd - s1d * s1d;
+    const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(__fsqrt_rn(__ll2float_rn(vq)), R.rcq),
+                                          __fmul_rn(__fsqrt_rn(__ll2float_rn(vd)), R.rcd)),
+                                0.5f);
+    const float ts = __fmaf_rn(sdf, a.rqs_f, 0.5f);
+    int cs;
+    if (!cell_of(ts, __fmaf_rn(ts, 1e-6f, 1e-6f) + a.band_s, cs)) {
+        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq), md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
+        cs = std_cell_exact(a, R, mq, md, s2q, s2d);
+    }
+    return cs;
+}
+// gradient-magnitude cell from the exact centred moments D (square offset
+// c + 1.5 => numerator 2D - s1 over 2 w1; diamond offset c + 1 => D / w1).
+template <class A>
+__device__ __forceinline__ int grad_cell_fast(const A& a, const RingDev& R, int cx, int cy, long long s1q,
+                                              long long s1d, long long dxq, long long dyq, long long dxd,
+                                              long long dyd) {
+    const float gxq = __fmul_rn(__ll2float_rn(2 * dxq - s1q), R.rw2q), gyq = __fmul_rn(__ll2float_rn(2 * dyq - s1q), R.rw2q);
+    const float gxd = __fmul_rn(__ll2float_rn(dxd), R.rw1d), gyd = __fmul_rn(__ll2float_rn(dyd), R.rw1d);
+    const float gx = __fmul_rn(__fadd_rn(gxq, gxd), 0.5f), gy = __fmul_rn(__fadd_rn(gyq, gyd), 0.5f);
+    const float gm = __fsqrt_rn(__fmaf_rn(gx, gx, __fmul_rn(gy, gy)));
+    const float tg = __fmaf_rn(gm, a.rqg_f, 0.5f);
+    const float sum = __fadd_rn(__fadd_rn(fabsf(gxq), fabsf(gxd)), __fadd_rn(fabsf(gyq), fabsf(gyd)));
+    const float bg = __fmaf_rn(__fmul_rn(__fadd_rn(sum, gm), 6e-7f), a.rqg_f, __fmaf_rn(tg, 4e-7f, 4e-7f));
+    int cg;
+    if (!cell_of(tg, bg, cg)) {
+        cg = grad_cell_exact(a, R, cx, cy, s1q, s1d, (long long)(cx + 1) * s1q + dxq, (long long)(cy + 1) * s1q + dyq,
+                             (long long)(cx + 1) * s1d + dxd, (long long)(cy + 1) * s1d + dyd);
+    }
+    return cg;
 }
 
 // Ring R at table-local centre (cx, cy), decided from fp32 estimates of the
@@ -331,18 +374,8 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 5 + 4 * level, 1ull);
 #endif
-    // std: exact integer variances V = s2 * count - s1^2 (>= 0)
     const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
-    const long long vq = s2q * R.icq - s1q * s1q, vd = s2d * R.icd - s1d * s1d;
-    const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(__fsqrt_rn(__ll2float_rn(vq)), R.rcq),
-                                          __fmul_rn(__fsqrt_rn(__ll2float_rn(vd)), R.rcd)),
-                                0.5f);
-    const float ts = __fmaf_rn(sdf, a.rqs_f, 0.5f);
-    int cs;
-    if (!cell_of(ts, __fmaf_rn(ts, 1e-6f, 1e-6f) + a.band_s, cs)) {
-        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq), md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
-        cs = std_cell_exact(a, R, mq, md, s2q, s2d);
-    }
+    const int cs = std_cell_fast(a, R, s1q, s1d, s2q, s2d);
     if (!member_ms(a, R, sb, cm, cs)) return false;
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 6 + 4 * level, 1ull);
@@ -351,21 +384,10 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
     load_corners(P, R, 1, ckx);  // X / Y planes only for (mean, std) members
     load_corners(P, R, 2, cky);
 #endif
-    // gradient: exact centred moments; square offset c + 1.5 => numerator 2D - s1 over 2 w1
+    // gradient from the exact centred moments
     const long long dxq = centred(sq_of(ckx), cx + 1, s1q), dyq = centred(sq_of(cky), cy + 1, s1q);
     const long long dxd = centred(di_of(ckx), cx + 1, s1d), dyd = centred(di_of(cky), cy + 1, s1d);
-    const float gxq = __fmul_rn(__ll2float_rn(2 * dxq - s1q), R.rw2q), gyq = __fmul_rn(__ll2float_rn(2 * dyq - s1q), R.rw2q);
-    const float gxd = __fmul_rn(__ll2float_rn(dxd), R.rw1d), gyd = __fmul_rn(__ll2float_rn(dyd), R.rw1d);
-    const float gx = __fmul_rn(__fadd_rn(gxq, gxd), 0.5f), gy = __fmul_rn(__fadd_rn(gyq, gyd), 0.5f);
-    const float gm = __fsqrt_rn(__fmaf_rn(gx, gx, __fmul_rn(gy, gy)));
-    const float tg = __fmaf_rn(gm, a.rqg_f, 0.5f);
-    const float sum = __fadd_rn(__fadd_rn(fabsf(gxq), fabsf(gxd)), __fadd_rn(fabsf(gyq), fabsf(gyd)));
-    const float bg = __fmaf_rn(__fmul_rn(__fadd_rn(sum, gm), 6e-7f), a.rqg_f, __fmaf_rn(tg, 4e-7f, 4e-7f));
-    int cg;
-    if (!cell_of(tg, bg, cg)) {
-        cg = grad_cell_exact(a, R, cx, cy, s1q, s1d, (long long)(cx + 1) * s1q + dxq, (long long)(cy + 1) * s1q + dyq,
-                             (long long)(cx + 1) * s1d + dxd, (long long)(cy + 1) * s1d + dyd);
-    }
+    const int cg = grad_cell_fast(a, R, cx, cy, s1q, s1d, dxq, dyq, dxd, dyd);
     return member_k(a, R, sb, cm, cs, cg);
 }
 

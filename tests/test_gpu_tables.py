@@ -124,6 +124,27 @@ def test_division_routine_matches_ieee(cuda):
     assert int(bad.item()) == 0
 
 
+@pytest.mark.parametrize("q", [(8.0, 8.0, 8.0), (6.0, 6.0, 6.0), (3.0, 0.7, 2.5), (8.0, 1e-3, 1e-3), (2.0, 0.25, 1e6)])
+def test_fp32_estimated_cells_match_fp64(cuda, q):
+    """The fused rings decide std / gradient cells from fp32 estimates and fall
+    back to the fp64 sequence near a boundary: on 2^22 random region sums
+    per ring (3 in 4 aimed within ~1e-6 of a boundary) the cells must equal
+    the fp64 reference sequence's, for small to int64-sized rings."""
+    import torch
+
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    rings = [(4, 5), (8, 11), (11, 15), (16, 15), (32, 45), (45, 63), (64, 63), (91, 128), (128, 181), (181, 255),
+             (256, 255)]
+    for i, (n, d) in enumerate(rings):
+        _native.check(L.ss_selftest_cells(1 << 22, 7919 * i + 1, n, d, q[0], q[1], q[2], counts.data_ptr(), s))
+    torch.cuda.synchronize()
+    assert counts.tolist() == [0, 0]
+
+
 def test_template_features_device_bitwise(cuda):
     """f2: GPU rescale features == host C++ (== reference, test_native_lib) bit for bit."""
     import torch
