@@ -8,6 +8,7 @@
 // (image_io.py:216-228) and the patch-side ring features (features.py:
 // 220-224 via :322-370).
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -159,22 +160,61 @@ int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, do
     const double* feats_ = h_feats;
     // FeatureSet.insert in k order (screening.py:127-145)
     const double qs[3] = {q_mean, q_std, q_grad};
-    std::vector<std::vector<int64_t>> rings(n_rings);
+    // Per ring: the guard-banded keys of every instance (27 per instance,
+    // heavily repeated across neighbouring rescales) deduplicated on insert
+    // in a small open-addressing table, then the unique keys sorted -- the
+    // set semantics of FeatureSet (screening.py:122-155).
+    struct KeySet {
+        std::vector<int64_t> slots, uniq;
+        size_t mask = 0;
+        void init(size_t expect) {
+            size_t cap = 64;
+            while (cap < 2 * expect) cap <<= 1;
+            slots.assign(cap, -1);
+            mask = cap - 1;
+            uniq.clear();
+        }
+        void add(int64_t k) {  // keys are >= 0; -1 marks an empty slot
+            size_t i = (size_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 20) & mask;
+            while (slots[i] != -1) {
+                if (slots[i] == k) return;
+                i = (i + 1) & mask;
+            }
+            slots[i] = k;
+            uniq.push_back(k);
+            if (2 * uniq.size() > slots.size()) rehash();
+        }
+        void rehash() {
+            std::vector<int64_t> keep = uniq;
+            init(2 * keep.size());
+            for (int64_t k : keep) add(k);
+        }
+    };
+    std::vector<KeySet> rings(n_rings);
+    for (auto& r : rings) r.init(256);
+    // an instance whose guard cells equal an earlier instance's (same ring)
+    // adds the same 27 keys: skip it
+    std::vector<std::vector<std::array<int64_t, 9>>> seen(n_rings);
     for (int32_t i = 0; i < nk; ++i) {
         for (int32_t r = 0; r < n_rings; ++r) {
-            int64_t cells[3][3];
+            std::array<int64_t, 9> g;
             int nc[3];
             for (int ch = 0; ch < 3; ++ch) {
                 const double v = feats_[((size_t)i * n_rings + r) * 3 + ch], q = qs[ch], half = q / 2.0;
                 int64_t c3[3] = {ss::quantize(v - half, q), ss::quantize(v, q), ss::quantize(v + half, q)};
                 std::sort(c3, c3 + 3);
                 nc[ch] = (int)(std::unique(c3, c3 + 3) - c3);
-                for (int j = 0; j < nc[ch]; ++j) cells[ch][j] = c3[j];
+                for (int j = 0; j < 3; ++j) g[(size_t)ch * 3 + j] = j < nc[ch] ? c3[j] : -1;
             }
+            bool dup = false;
+            for (const auto& t : seen[r])
+                if (t == g) { dup = true; break; }
+            if (dup) continue;
+            seen[r].push_back(g);
             for (int a = 0; a < nc[0]; ++a)
                 for (int b = 0; b < nc[1]; ++b)
-                    for (int g = 0; g < nc[2]; ++g) {
-                        const int64_t cm = cells[0][a], cs = cells[1][b], cg = cells[2][g];
+                    for (int c = 0; c < nc[2]; ++c) {
+                        const int64_t cm = g[a], cs = g[3 + b], cg = g[6 + c];
                         if (cm >= SS_KEY_BASE || cs >= SS_KEY_BASE || cg >= SS_KEY_BASE) {
                             ss::set_error("quantized cell exceeds key capacity, quantizer too fine");
                             return SS_ECAPACITY;
@@ -183,16 +223,15 @@ int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, do
                             ss::set_error("negative quantized cell; features must be non-negative");
                             return SS_ECAPACITY;
                         }
-                        rings[r].push_back((cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
+                        rings[r].add((cm * SS_KEY_BASE + cs) * SS_KEY_BASE + cg);
                     }
         }
     }
     int64_t pos = 0;
     h_key_off[0] = 0;
     for (int32_t r = 0; r < n_rings; ++r) {
-        auto& v = rings[r];
+        auto& v = rings[r].uniq;
         std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
         std::memcpy(h_keys + pos, v.data(), v.size() * sizeof(int64_t));
         pos += (int64_t)v.size();
         h_key_off[r + 1] = pos;
@@ -200,12 +239,38 @@ int ss_keys_from_features(const double* h_feats, int32_t nk, int32_t n_rings, do
     return SS_OK;
 }
 
+}  // extern "C"
+namespace ss {
+// The ss_keyset_blob layout built into `blob` (reused storage).
+static int build_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings,
+                             std::vector<int64_t>& blob);
+}  // namespace ss
+extern "C" {
+
 int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings, int64_t* h_blob,
                    size_t* blob_bytes) {
     if (!h_key_off || n_rings < 1 || n_rings > SS_MAX_RINGS || !blob_bytes) {
         ss::set_error("bad keyset arguments");
         return SS_EINVAL;
     }
+    std::vector<int64_t> blob;
+    if (int e = ss::build_keyset_blob(h_keys, h_key_off, n_rings, blob)) return e;
+    const size_t need = blob.size() * sizeof(int64_t);
+    if (h_blob) {
+        if (*blob_bytes < need) {
+            ss::set_error("key blob buffer too small: %zu < %zu", *blob_bytes, need);
+            return SS_EINVAL;
+        }
+        std::memcpy(h_blob, blob.data(), need);
+    }
+    *blob_bytes = need;
+    return SS_OK;
+}
+
+}  // extern "C"
+namespace ss {
+static int build_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_rings,
+                             std::vector<int64_t>& blob) {
     // Layout (int64 slots): [0] n_rings; header of SS_BLOB_HDR slots per ring at
     // 1 + SS_BLOB_HDR * r:
     //   0 off_m  1 n_m  2 off_ms  3 n_ms  4 off_k  5 n_k        sorted arrays
@@ -214,7 +279,7 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
     // The bit section packs uint32 words [m | ms | full] two per slot; bit i of
     // ms is (cm-cm_lo)*cs_n + (cs-cs_lo), of full ((..)*cg_n + (cg-cg_lo)).
     const int H = SS_BLOB_HDR;
-    std::vector<int64_t> blob(1 + (size_t)H * n_rings, 0);
+    blob.assign(1 + (size_t)H * n_rings, 0);
     blob[0] = n_rings;
     for (int32_t r = 0; r < n_rings; ++r) {
         const int64_t a = h_key_off[r], b = h_key_off[r + 1];
@@ -266,17 +331,10 @@ int ss_keyset_blob(const int64_t* h_keys, const int64_t* h_key_off, int32_t n_ri
                 blob.push_back((int64_t)((uint64_t)words[i] | ((uint64_t)words[i + 1] << 32)));
         }
     }
-    const size_t need = blob.size() * sizeof(int64_t);
-    if (h_blob) {
-        if (*blob_bytes < need) {
-            ss::set_error("key blob buffer too small: %zu < %zu", *blob_bytes, need);
-            return SS_EINVAL;
-        }
-        std::memcpy(h_blob, blob.data(), need);
-    }
-    *blob_bytes = need;
     return SS_OK;
 }
+}  // namespace ss
+extern "C" {
 
 
 int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n_sizes, const int32_t* h_nk,
@@ -291,6 +349,7 @@ int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n
     int64_t key_pos = 0, blob_pos = 0, off_pos = 0, inst = 0;
     h_blob_off[0] = 0;
     std::vector<double> feats;
+    std::vector<int64_t> blob;
     for (int32_t k = 0; k < n_sizes; ++k) {
         const int32_t nk = h_nk[k], nr = h_n_rings[k];
         if (nk < 0 || nr < 1 || nr > feat_ring_stride) {
@@ -310,14 +369,13 @@ int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n
         int64_t* off = h_key_off + off_pos;  // nr + 1 offsets relative to this size's first key
         if (int e = ss_keys_from_features(feats.data(), nk, nr, q_mean, q_std, q_grad, h_keys + key_pos, off))
             return e;
-        size_t bytes = 0;
-        if (int e = ss_keyset_blob(h_keys + key_pos, off, nr, nullptr, &bytes)) return e;
-        const int64_t slots = (int64_t)(bytes / sizeof(int64_t));
+        if (int e = ss::build_keyset_blob(h_keys + key_pos, off, nr, blob)) return e;
+        const int64_t slots = (int64_t)blob.size();
         if (blob_pos + slots > blobs_cap) {
             ss::set_error("ladder keyset blob buffer too small");
             return SS_EINVAL;
         }
-        if (int e = ss_keyset_blob(h_keys + key_pos, off, nr, h_blobs + blob_pos, &bytes)) return e;
+        std::memcpy(h_blobs + blob_pos, blob.data(), (size_t)slots * sizeof(int64_t));
         key_pos += off[nr];
         off_pos += nr + 1;
         blob_pos += slots;
