@@ -287,6 +287,15 @@ int ss_ladder_keysets(const double* h_feats, int32_t feat_ring_stride, int32_t n
  */
 int ss_template_features_device(const uint8_t* d_template, int32_t n, int32_t n_inst, const int32_t* d_desc,
                                 int32_t desc_stride, double* d_out, void* stream);
+/*
+ * ss_template_features_device as one asynchronous round trip: copies the
+ * n x n host template into d_template, runs the features, copies them into
+ * h_out (pinned, n_inst x SS_MAX_RINGS x 3 doubles) and records `event`
+ * (nullable) on `stream`.
+ */
+int ss_template_features_async(const uint8_t* h_template, int32_t n, int32_t n_inst, const int32_t* d_desc,
+                               int32_t desc_stride, uint8_t* d_template, double* d_out, double* h_out, void* stream,
+                               void* event);
 /* Ring features (mean, std, grad_mag per ring) of one rescale k (tests). */
 int ss_template_ring_features(const uint8_t* h_template, int32_t n, int32_t k, int32_t m, int32_t n_rings,
                               const int32_t* h_ring_n, const int32_t* h_ring_d, double* h_out);

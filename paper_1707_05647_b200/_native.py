@@ -74,6 +74,7 @@ _SIGS = {
     "ss_feature_set_keys": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_p]),
     "ss_keys_from_features": (ctypes.c_int, [c_p, c_i32, c_i32, c_d, c_d, c_d, c_p, c_p]),
     "ss_template_features_device": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_i32, c_p, c_p]),
+    "ss_template_features_async": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_i32, c_p, c_p, c_p, c_p, c_p]),
     "ss_template_ring_features": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_p]),
 }
 

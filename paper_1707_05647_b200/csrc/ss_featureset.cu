@@ -119,3 +119,25 @@ extern "C" int ss_template_features_device(const uint8_t* d_template, int32_t n,
     ss::note_launch();
     return ss::check_launch("template_features_kernel");
 }
+
+// The whole f2 round trip in one host call: template bytes (host) to the
+// device, the features of every instance, the result into pinned host memory
+// and an event recorded after it -- no host synchronisation.
+extern "C" int ss_template_features_async(const uint8_t* h_template, int32_t n, int32_t n_inst, const int32_t* d_desc,
+                                          int32_t desc_stride, uint8_t* d_template, double* d_out, double* h_out,
+                                          void* stream, void* event) {
+    if (!h_template || !d_template || !h_out || n < 1) {
+        ss::set_error("bad template feature arguments");
+        return SS_EINVAL;
+    }
+    cudaStream_t s = ss::as_stream(stream);
+    if (cudaMemcpyAsync(d_template, h_template, (size_t)n * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return ss::check_launch("template upload");
+    if (int e = ss_template_features_device(d_template, n, n_inst, d_desc, desc_stride, d_out, stream)) return e;
+    const size_t bytes = (size_t)n_inst * SS_MAX_RINGS * 3 * sizeof(double);
+    if (bytes && cudaMemcpyAsync(h_out, d_out, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return ss::check_launch("feature readback");
+    if (event && cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), s) != cudaSuccess)
+        return ss::check_launch("event record");
+    return SS_OK;
+}

@@ -210,18 +210,39 @@ def launch_template_features(template: np.ndarray, desc: np.ndarray, device, str
         return None
     dev = torch.device(device)
     stream = stream or torch.cuda.current_stream(dev)
-    with torch.cuda.stream(stream):
-        d_desc = _device_desc(desc, dev)
-        d_tpl = torch.from_numpy(tpl).to(dev, non_blocking=True)  # a few KB: the pageable copy is cheaper than pinning
-        d_out = torch.empty((desc.shape[0], SS_MAX_RINGS, 3), dtype=torch.float64, device=dev)
-        _native.check(_native.lib().ss_template_features_device(
-            d_tpl.data_ptr(), n, desc.shape[0], d_desc.data_ptr(), DESC_STRIDE, d_out.data_ptr(), stream.cuda_stream),
-            "template features")
-        host = torch.empty(d_out.shape, dtype=torch.float64, pin_memory=True)
-        host.copy_(d_out, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(stream)
-    return host, done
+    d_desc = _device_desc(desc, dev)
+    st = _staging(dev, stream, n * n, desc.shape[0])
+    _native.check(_native.lib().ss_template_features_async(
+        tpl.ctypes.data, n, desc.shape[0], d_desc.data_ptr(), DESC_STRIDE, st["tpl"].data_ptr(), st["out"].data_ptr(),
+        st["host"].data_ptr(), stream.cuda_stream, st["event"].cuda_event), "template features")
+    return st["host"][: desc.shape[0]], st["event"]
+
+
+_staging_cache: dict = {}
+
+
+def _staging(dev, stream, tpl_bytes: int, n_inst: int) -> dict:
+    """Per-stream buffers of the f2 round trip (device template and features,
+    pinned host features, an event), grown on demand.  A stream's previous
+    round trip has been consumed (wait_template_features) before the next
+    one is enqueued on it (engine order)."""
+    import torch
+
+    key = (str(dev), stream.cuda_stream)
+    st = _staging_cache.get(key)
+    if st is None or st["tpl"].numel() < tpl_bytes or st["out"].shape[0] < n_inst:
+        tb = max(tpl_bytes, 128 * 128, st["tpl"].numel() if st else 0)
+        ni = max(n_inst, 64, st["out"].shape[0] if st else 0)
+        event = torch.cuda.Event()
+        event.record(stream)  # creates the handle
+        st = {"tpl": torch.empty(tb, dtype=torch.uint8, device=dev),
+              "out": torch.empty((ni, SS_MAX_RINGS, 3), dtype=torch.float64, device=dev),
+              "host": torch.empty((ni, SS_MAX_RINGS, 3), dtype=torch.float64, pin_memory=True),
+              "event": event}
+        if len(_staging_cache) > 32:
+            _staging_cache.clear()
+        _staging_cache[key] = st
+    return st
 
 
 def wait_template_features(handle) -> np.ndarray:
