@@ -228,7 +228,8 @@ size_t ss_region_workspace_bytes(int64_t W, int64_t H, int32_t m_max);
 int ss_region_accumulate(const uint32_t* d_mask, int64_t mask_pitch_words, int64_t W, int64_t H, int32_t m,
                          int32_t stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes,
                          void* stream);
-/* Whole-ladder form of ss_region_accumulate (full-image masks). */
+/* Whole-ladder form of ss_region_accumulate (full-image masks); writes d_region
+ * (the union of every size's footprints; prior contents are replaced). */
 size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes);
 int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
                      int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
@@ -241,7 +242,7 @@ int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t 
  */
 int ss_bits_to_bytes(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, uint8_t* d_out,
                      void* stream);
-/* d_count += number of set bits of the W x H region mask. */
+/* *d_count = number of set bits of the W x H region mask. */
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H,
                 unsigned long long* d_count, void* stream);
 

@@ -329,12 +329,15 @@ constexpr int RP_WARPS = 8;
 __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsigned* masks, long long mask_pitch,
                                                                     long long size_stride, int W, int H,
                                                                     long long words, long long P,
-                                                                    const Ladder lad, unsigned* Hb) {
+                                                                    const Ladder lad, unsigned* Hb,
+                                                                    unsigned* region, long long region_pitch) {
     extern __shared__ unsigned rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long task = (long long)blockIdx.x * RP_WARPS + warp;
     if (task >= (long long)lad.L * H) return;
     const int k = (int)(task / H), y = (int)(task % H);
+    if (k == 0)  // the region is written (not accumulated): the column pass ORs into cleared rows
+        for (long long i = lane; i < words; i += 32) region[(long long)y * region_pitch + i] = 0u;
     const int m = lad.m[k];
     const int lo = (m - 1) / 2, hi = m / 2;
     unsigned* out = Hb + ((long long)k * H + y) * words;
@@ -586,7 +589,7 @@ int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stri
         }
         const long long tasks = (long long)L * H;
         region_rows_kernel<<<(unsigned)((tasks + RP_WARPS - 1) / RP_WARPS), RP_WARPS * 32, smem, s>>>(
-            d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb);
+            d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb, d_region, mask_pitch);
         note_launch();
         if (int e = check_launch("region_rows_kernel")) return e;
     }
@@ -621,6 +624,8 @@ int popcount(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, unsign
     const int64_t words = (W + 31) / 32;
     const int64_t n = words * H;
     const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), as_stream(stream)) != cudaSuccess)
+        return check_launch("memset");
     popcount_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_bits, pitch, words, (int)W, H, d_count);
     note_launch();
     return check_launch("popcount_kernel");

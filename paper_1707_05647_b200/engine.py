@@ -405,7 +405,7 @@ class Engine:
 
     def compact_all(self, tp: TemplatePlan) -> None:
         """K4 for every size in one pass (ladder order, then row-major)."""
-        ms = self._ladder_array(tp)
+        ms = tp.m_arr if tp.m_arr is not None else self._ladder_array(tp)
         _native.check(self.L.ss_compact_ladder(
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, self.y_begin, self.y_end,
             len(ms), ms.ctypes.data, tp.config.stride, self.row_counts.data_ptr(), self.xy.data_ptr(), 3, self.capacity,
@@ -414,7 +414,7 @@ class Engine:
 
     def region_all(self, tp: TemplatePlan) -> None:
         """K5 for every size in one pass, then the region popcount."""
-        ms = self._ladder_array(tp)
+        ms = tp.m_arr if tp.m_arr is not None else self._ladder_array(tp)
         _native.check(self.L.ss_region_ladder(
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, len(ms), ms.ctypes.data,
             tp.config.stride, self.region.data_ptr(), self.region_ws.data_ptr(), self.region_ws.numel(),
@@ -430,9 +430,6 @@ class Engine:
         self._ensure(len(tp.sizes), tp.max_m, capacity or self.default_capacity(tp), region)
         if build:
             self.build_tables(img, int64=self.needs_int64(tp))
-        if region:
-            self.region.zero_()
-            self.totals[1:].zero_()
         main = torch.cuda.current_stream(self.device)
         if self.hooks is not None:
             self.hooks[0](main)
