@@ -9,8 +9,9 @@
 #include "ss_common.cuh"
 
 namespace ss {
-int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
-                        int64_t y_begin, int64_t y_end, int32_t stride, int n, const int* ks, const int32_t* h_m,
+int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int64_t h, int64_t pitch, int64_t W,
+                        int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride, int n,
+                        const int* ks, const int32_t* h_m,
                         const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
                         const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
@@ -64,7 +65,8 @@ extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_plane
                 ss::set_error("ladder needs the int64 planes (ring sums exceed 32 bits)");
                 return SS_EINVAL;
             }
-            int e = ss::screen_ladder_fused(planes, g == 0 ? 4 : 8, h, plane_pitch, W, H, y_origin, y_begin, y_end,
+            int e = ss::screen_ladder_fused(planes, g == 0 ? 4 : 8, g == 0 ? nullptr : d_planes32, h, plane_pitch, W, H,
+                                            y_origin, y_begin, y_end,
                                             stride, (int)ks.size(), ks.data(), h_m, h_n_rings, h_ring_n, h_ring_d,
                                             d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad, d_masks,
                                             mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,

@@ -582,8 +582,9 @@ size_t ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
 // workspace holds.  Returns SS_DECLINED (nothing enqueued) when the sizes do
 // not fit the fused parameter block or the workspace is too small for a
 // useful band; the caller then screens them one by one.
-int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, int64_t W, int64_t H, int64_t y_origin,
-                        int64_t y_begin, int64_t y_end, int32_t stride, int n, const int* ks, const int32_t* h_m,
+int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int64_t h, int64_t pitch, int64_t W,
+                        int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride, int n,
+                        const int* ks, const int32_t* h_m,
                         const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
                         const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
@@ -682,20 +683,33 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
     while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + TY - 1) / TY * TY;
     if (!d_ws || fused_ws_bytes(W, band, n, sms) > ws_bytes) return SS_DECLINED;
 
+    // Stage 1 reads only the ring-0 PLAIN sums: when they fit 32 bits for
+    // every size (255 x pixels < 2^32, n <= 2048), an int64 group's stage 1
+    // runs on the 32-bit PLAIN planes (half the TMA bytes, 128-column tiles)
+    // and only its rings read the int64 planes.
+    bool s1_u32 = eb == 4;
+    if (eb == 8 && planes32_s1) {
+        s1_u32 = true;
+        for (int j = 0; j < n && s1_u32; ++j) {
+            const RingDev& R0 = a.ring[a.size[j].ring0];
+            s1_u32 = 255LL * 4 * R0.n * R0.n < (1LL << 32) && 255LL * (2LL * R0.d * R0.d + 2LL * R0.d + 1) < (1LL << 32);
+        }
+    }
     // (row counts and workspace counters are zeroed by ladder_border_kernel)
     TmaMaps maps;
-    if (int e = plane_maps_cached(maps, planes, eb, eb == 4 ? GeoF<unsigned>::BW : GeoF<long long>::BW, W, h, pitch,
-                                  a.ps))
+    if (int e = s1_u32 ? plane_maps_cached(maps, eb == 4 ? planes : planes32_s1, 4, GeoF<unsigned>::BW, W, h, pitch, a.ps)
+                       : plane_maps_cached(maps, planes, 8, GeoF<long long>::BW, W, h, pitch, a.ps))
         return e;
     unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
     unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
     unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
     int2* list = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + FCTR_BYTES);
 
-    auto launch = [&](auto tag) -> int {
-        using T = decltype(tag);
-        using G = GeoF<T>;
-        auto s1 = ladder_stage1_kernel<T>;
+    auto launch = [&](auto tag, auto tag1) -> int {
+        using T = decltype(tag);    // the rings' planes
+        using T1 = decltype(tag1);  // stage 1's PLAIN planes
+        using G = GeoF<T1>;
+        auto s1 = ladder_stage1_kernel<T1>;
         auto rk = ladder_rings_kernel<T>;
         const size_t s1_smem = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(bm1, 1) * 4;
         const int s1_per_sm = std::min(occupancy(reinterpret_cast<const void*>(s1), (WARPS + 1) * 32, s1_smem), 2);
@@ -751,7 +765,8 @@ int screen_ladder_fused(const void* planes, int eb, int64_t h, int64_t pitch, in
         }
         return SS_OK;
     };
-    return eb == 4 ? launch((unsigned)0) : launch((long long)0);
+    if (eb == 4) return launch((unsigned)0, (unsigned)0);
+    return s1_u32 ? launch((long long)0, (unsigned)0) : launch((long long)0, (long long)0);
 }
 
 }  // namespace ss
