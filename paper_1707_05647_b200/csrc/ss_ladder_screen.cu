@@ -151,11 +151,11 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         if (lane == 0) {
             const int tc = (int)(blockIdx.x % TILE_CTRS);
             unsigned* tile_ctr = tile_ctr_base + tc * CTR_STRIDE;
-            unsigned t_next = atomicAdd(tile_ctr, 1u);
+            unsigned t_next = atom_add_ahead(tile_ctr, 1u);
             for (int it = 0;; ++it) {
                 const int s = it % STAGES;
                 const long long t = (long long)t_next * TILE_CTRS + tc;
-                if (t < tm.n_tiles) t_next = atomicAdd(tile_ctr, 1u);
+                if (t < tm.n_tiles) t_next = atom_add_ahead(tile_ctr, 1u);
                 mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 if (t >= tm.n_tiles) {
                     tile_info[s].tx = -1;
@@ -296,10 +296,10 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         while (nbuf >= 32) {
             __syncwarp();
             if (res_left == 0) {
-                if (!have_res && lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
                 res_base = __shfl_sync(FULL, res, 0);
                 res_left = reserve;
-                if (lane == 0) res = atomicAdd(count0, (unsigned)reserve);
+                if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
                 have_res = true;
             }
             list0[res_base + lane] = buf[nbuf - 32 + lane];
@@ -415,14 +415,14 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
     const int2* in = list_base + q * part_cap;
     unsigned g_raw = 0;
-    if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+    if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
     unsigned cur = 0, k = 0;
     bool have_input = true;
     auto grab = [&]() {
         for (;;) {
             cur = (__shfl_sync(FULL, g_raw, 0) * GROUP_CTRS + gc) * RG;
             if (cur < cnt_q) {
-                if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+                if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
                 return;
             }
             if (visited == parts) {
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
             q = q + 1 == parts ? 0 : q + 1;
             cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
             in = list_base + q * part_cap;
-            if (lane == 0) g_raw = atomicAdd(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
+            if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
         }
     };
     auto fetch = [&]() -> int2 {

@@ -478,6 +478,16 @@ inline int fill_ring(RingDev& R, int n, int d, int m, long long P, double qm, co
     return SS_OK;
 }
 
+// atomicAdd from one lane whose result is consumed later (a reservation taken
+// one step ahead): the builtin is warp-aggregated by the compiler, whose
+// broadcast of the returned value waits for the atomic right away and
+// defeats the look-ahead; the plain PTX atom leaves the latency hidden.
+__device__ __forceinline__ unsigned atom_add_ahead(unsigned* p, unsigned v) {
+    unsigned r;
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+
 // ── TMA / mbarrier helpers (sm_90+ PTX, used on sm_100a) ──────────────────
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
