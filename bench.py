@@ -187,7 +187,32 @@ def cpu_baseline(wl, case, nthreads, max_seconds=30.0):
     dt = time.perf_counter() - t0
     return {"value": res.patches_tested / dt, "unit": UNIT, "cores": nthreads, "kind": "port",
             "sample": sample + f" (oracle/oracle.c, {res.patches_tested} positions in {dt:.2f} s)",
-            "positions": res.patches_tested, "seconds": dt}
+            "positions": res.patches_tested, "seconds": dt, "result": res, "image": img}
+
+
+def parity_vs_oracle(cpu, case, wl, dev):
+    """The public screen() on the image the CPU baseline screened, against the
+    oracle's result: per-size mask bits that differ (the north star's
+    threshold-band count; 0 expected: the fp64 path is bit-exact), candidate
+    list and stats equality."""
+    from paper_1707_05647_b200 import screen
+    import workloads as WL
+
+    ref, img = cpu["result"], cpu["image"]
+    got = screen(img, case.template, WL.screening_config(wl), device=dev)
+    diff = {}
+    for m in ref.ladder:
+        want = np.packbits(ref.size_masks[m], axis=1, bitorder="little")
+        have = got.size_masks.packed(m).view(np.uint8)[:, : want.shape[1]]
+        n = int(np.unpackbits(np.bitwise_xor(want, have)).sum())
+        if n:
+            diff[int(m)] = n
+    cand = np.array(ref.candidates, np.int32).reshape(-1, 3)
+    return {"image": f"{img.shape[1]}x{img.shape[0]}", "sizes": len(ref.ladder),
+            "mask_bit_disagreements": sum(diff.values()), "per_size": diff,
+            "candidates_identical": bool(np.array_equal(got.candidates.array(), cand)),
+            "stats_identical": (got.stats.patches_tested, got.stats.patches_kept, got.stats.region_pixels_kept) ==
+                               (ref.patches_tested, len(ref.candidates), int(ref.region_mask.sum()))}
 
 
 def run_reference(args):
@@ -473,9 +498,11 @@ def run_ours(args):
                         "accessed"}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl, case, os.cpu_count() or 1)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        full = cpu_baseline(wl, case, os.cpu_count() or 1)
+        parity = parity_vs_oracle(full, case, wl, dev)
+        cpu = {k: full[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
         line = {
@@ -491,6 +518,7 @@ def run_ours(args):
                 "cuda_graph": bool(graph is not None)}),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity_vs_oracle": parity,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
