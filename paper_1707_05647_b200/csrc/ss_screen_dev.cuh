@@ -29,21 +29,23 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int WARPS = 16;  // stage-1 consumer warps per CTA (one tile row each)
 constexpr int SMEM_BITMAP_WORDS = 12 * 1024;  // 48 KiB of membership bitmaps per CTA
 
-struct RingDev {
-    int n, d;
+// Fields grouped in 16-byte blocks in the order the fused rings read them
+// (per-lane loads from shared memory become LDS.128).
+struct __align__(16) RingDev {
     int sa, sb, sc, sd;  // SAT corners rel. to [cy][cx]: [+n+1][+n+1] [+n+1][-n+1] [-n+1][+n+1] [-n+1][-n+1]
     int ea, ed;          // E corners: [+d+1][+1], [-d][+1]
     int ob, oc;          // O corners: [0][-d], [0][+d+1]
-    double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
     float fa, fb;  // RN32(1 / (2 cnt qm)) of the square / diamond: fp32 estimate of the mean cell
     int icq, icd;  // pixel counts 4n^2, 2d^2+2d+1 (exact integer variances)
     float rcq, rcd, rw2q, rw1d;  // RN32 of 1/icq, 1/icd, 1/(2 w1_sq), 1/w1_di (fp32 estimates of std / gradient)
-    int cm_lo, cm_n, cs_lo, cs_n, cg_lo, cg_n;
-    int bm;        // shared-memory word offset of [m | ms | full] bits; -1: binary search
-    int wm, wms;   // words of the m and ms bitmaps
-    int bsrc;      // uint32 index of the bit section in the device blob (-1: zero fill)
-    int bwords;    // words to stage
+    int cm_lo, cm_n, cs_lo, cs_n;
+    int cg_lo, cg_n, bm, wm;  // bm: shared-memory word offset of [m | ms | full] bits (-1: binary search)
+    int wms;     // words of the m / ms bitmaps: wm (above), wms
+    int bsrc;    // uint32 index of the bit section in the device blob (-1: zero fill)
+    int bwords;  // words to stage
+    int n, d;
     int off_m, n_m, off_ms, n_ms, off_k, n_k;
+    double cnt_sq, rcp_sq, cnt_di, rcp_di, w1_sq, rw1_sq, w1_di, rw1_di;
 };
 
 struct ScreenArgs {
