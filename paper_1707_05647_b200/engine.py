@@ -282,6 +282,7 @@ class Engine:
         self.template_stream = torch.cuda.Stream(self.device)  # f2 features, overlapping the table build
         self.screen_ws = None  # per-size workspaces, one per side stream (allocated when the per-size path runs)
         self.ladder_ws = None  # fused ladder workspace (allocated for the first ladder that needs it)
+        self.region_stream = None  # K5 beside K4
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -436,9 +437,18 @@ class Engine:
         self.screen_ladder(tp, main)
         if self.hooks is not None:
             self.hooks[1](main)
+        if region:
+            # K5 reads only the masks: it runs beside K4 on a side stream
+            # (both are small latency-bound passes), joined back before return
+            if self.region_stream is None:
+                self.region_stream = torch.cuda.Stream(self.device)
+            rs = self.region_stream
+            rs.wait_stream(main)
+            with torch.cuda.stream(rs):
+                self.region_all(tp)
         self.compact_all(tp)
         if region:
-            self.region_all(tp)
+            main.wait_stream(rs)
 
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:
         """Grow the survivor buffer and redo K4 only (after an overflow)."""
