@@ -406,8 +406,8 @@ __global__ void region_cols_kernel(const unsigned* Hb, int H, long long words, l
     if (L >= C) {
         const int a0 = r0 - hi, b = a0 + L - 1;
         unsigned s = 0;
-#pragma unroll 4
-        for (int j = b; j >= a0 + C; --j) s |= ld(j);
+#pragma unroll 16
+        for (int j = b; j >= a0 + C; --j) s |= ld(j);  // independent loads: 16 in flight
 #pragma unroll
         for (int c = C - 1; c >= 0; --c) {
             s |= ld(a0 + c);
