@@ -375,6 +375,9 @@ class Engine:
         flags = 1 if self.force_int64 else 0
         if fused_enabled():
             need = int(self.L.ss_ladder_workspace_bytes(self.W, max(self.mrows, 1), max(L, 1)))
+            cap = os.environ.get("SS_LADDER_WS_BYTES")  # test hook: a smaller workspace forces row bands
+            if cap:
+                need = int(cap)
             if self.ladder_ws is None or self.ladder_ws.numel() < need:
                 self.ladder_ws = None
                 self.ladder_ws = torch.empty(need, dtype=torch.uint8, device=self.device)

@@ -344,3 +344,22 @@ def test_fused_ladder_declines_to_per_size_path(cuda):
     case = WL.make_template(img, 92, 48, (0.8, 1.3), std_threshold=10.0)
     compare_with_oracle(img, case.template, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.04,
                                              "quantizer": (8.0, 8.0, 8.0)})
+
+
+@pytest.mark.parametrize("cap_mb", [20, 40])
+def test_fused_ladder_row_bands_vs_oracle(cuda, monkeypatch, cap_mb):
+    """A workspace too small for the whole candidate list makes the fused
+    ladder screen the image in several row bands (tables, masks and counts
+    shared, lists per band): still equal to the oracle."""
+    import workloads as WL
+    from paper_1707_05647_b200.screening import _engine_cache
+
+    monkeypatch.setenv("SS_LADDER_WS_BYTES", str(cap_mb << 20))
+    _engine_cache.clear()
+    try:
+        img = WL.make_image(900, 640, seed=101, sigma=2.5, noise=2.0)
+        case = WL.make_template(img, 102, 48, (0.8, 1.3), std_threshold=10.0)
+        compare_with_oracle(img, case.template, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.2,
+                                                 "quantizer": (8.0, 8.0, 8.0)})
+    finally:
+        _engine_cache.clear()
