@@ -516,7 +516,10 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
 }
 
 constexpr size_t FCTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
-constexpr long long FUSED_LARGE_TILES = 32768;  // partitioned lists from this many tiles per pass
+#ifndef FUSED_LARGE_TILES_MACRO
+#define FUSED_LARGE_TILES_MACRO 32768
+#endif
+constexpr long long FUSED_LARGE_TILES = FUSED_LARGE_TILES_MACRO;  // partitioned lists from this many tiles per pass
 constexpr size_t FUSED_WS_CAP = (size_t)4 << 30;  // ss_ladder_workspace_bytes: row bands beyond this
 
 // capacity in tiles of TXMAX x TY centres (covers either fused tile width)

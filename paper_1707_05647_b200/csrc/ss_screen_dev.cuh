@@ -617,7 +617,10 @@ __device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbi
 }
 
 constexpr int RK_WARPS = 8;
-constexpr int QCAP = 64;
+#ifndef QCAP_MACRO
+#define QCAP_MACRO 64
+#endif
+constexpr int QCAP = QCAP_MACRO;
 #ifndef RINGS_MINB
 #define RINGS_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
