@@ -67,10 +67,16 @@ struct TileMapF {
 // Fused stage-1 tile geometry: 16 rows x 32*CPW columns; 32-bit planes take
 // 128-column tiles (four independent centres per lane: the chains overlap),
 // int64 planes 64 (three pipeline stages must fit shared memory).
+#ifndef FUSED_CPW32
+#define FUSED_CPW32 6  // 32-bit tiles: 32-column chunks per lane (measured: 6 x 2 stages beats 5 x 2, 4 x 3, 3 x 4, 2 x 5)
+#endif
+#ifndef FUSED_STAGES32
+#define FUSED_STAGES32 2
+#endif
 template <typename T> struct GeoF {
-    static constexpr int CPW = sizeof(T) == 4 ? 4 : 2;
+    static constexpr int CPW = sizeof(T) == 4 ? FUSED_CPW32 : 2;
     static constexpr int TX = 32 * CPW;
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = sizeof(T) == 4 ? FUSED_STAGES32 : 3;
     static constexpr int ALIGN = 16 / (int)sizeof(T);
     static constexpr int BW = TX + ALIGN;
     static constexpr int BOX_ELEMS = BW * TY;
@@ -79,7 +85,7 @@ template <typename T> struct GeoF {
     __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }
     __device__ static int rem(int c) { return c & (ALIGN - 1); }
 };
-constexpr int TXMAX = 128;  // widest fused tile (workspace sizing)
+constexpr int TXMAX = 32 * (FUSED_CPW32 > 2 ? FUSED_CPW32 : 2);  // widest fused tile (workspace sizing)
 
 // A stage-1 tile and the constants of its size, written by the producer next
 // to the tile's boxes (the consumers read 4 x 16 B instead of indexing the
