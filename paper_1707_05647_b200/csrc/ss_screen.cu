@@ -48,6 +48,8 @@
 namespace ss {
 namespace {
 
+constexpr int RK_WARPS_PS = 8;  // per-size rings kernel: warps per CTA (RINGS_MINB CTAs per SM)
+
 
 // K3a: every grid centre of the decided rows -- border keeps into the mask,
 // ring-0 mean cell from TMA-staged PLAIN corner boxes, mean-projection
@@ -262,11 +264,11 @@ __device__ __forceinline__ bool eval_ring(const ScreenArgs& a, const RingDev& R,
 }
 
 template <typename T, typename Entry>
-__global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const ScreenArgs a, int parts, const Entry* list_base,
+__global__ void __launch_bounds__(RK_WARPS_PS * 32, RINGS_MINB) rings_kernel(const ScreenArgs a, int parts, const Entry* list_base,
                                                                  long long part_cap, const unsigned* list_ctr,
                                                                  unsigned* group_ctr, int bitmap_words) {
     extern __shared__ unsigned sbits[];  // [all rings' bitmaps][queues: warp x level x QCAP int2]
-    __shared__ int qcnt[RK_WARPS][SS_MAX_RINGS];
+    __shared__ int qcnt[RK_WARPS_PS][SS_MAX_RINGS];
     stage_bitmaps(a, sbits, 0, a.n_rings);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int levels = a.n_rings;
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, RINGS_MINB) rings_kernel(const 
     // group's number waits in lane 0 (one atomic ahead) and the next batch is
     // loaded one batch ahead.
     constexpr unsigned RG = RINGS_GROUP;
-    const unsigned wid = blockIdx.x * RK_WARPS + warp;
+    const unsigned wid = blockIdx.x * RK_WARPS_PS + warp;
     int q = (int)(wid % parts), visited = 1;
     const unsigned gc = (wid / parts) % GROUP_CTRS;
     unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
@@ -571,10 +573,10 @@ static int launch_k3(K3Launch& L, int parts) {
     }
     // K3b: all rings over the stage-1 sub-lists; survivors into the mask
     {
-        const size_t smem = (size_t)((L.bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.n_rings * QCAP * sizeof(int2);
+        const size_t smem = (size_t)((L.bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS_PS * a.n_rings * QCAP * sizeof(int2);
         auto rk = rings_kernel<T, E>;
-        const int per_sm = occupancy(reinterpret_cast<const void*>(rk), RK_WARPS * 32, smem);
-        rk<<<(unsigned)(L.sms * std::max(per_sm, 1)), RK_WARPS * 32, smem, L.s>>>(a, parts, list, part_cap, L.list_ctr,
+        const int per_sm = occupancy(reinterpret_cast<const void*>(rk), RK_WARPS_PS * 32, smem);
+        rk<<<(unsigned)(L.sms * std::max(per_sm, 1)), RK_WARPS_PS * 32, smem, L.s>>>(a, parts, list, part_cap, L.list_ctr,
                                                                                 L.group_ctr, L.bm_words);
         note_launch();
         if (int e = check_launch("rings_kernel")) return e;

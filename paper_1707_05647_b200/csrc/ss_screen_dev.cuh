@@ -9,7 +9,7 @@
 #define EVAL_TWO_PHASE 1  // eval_ring_fast: X / Y corners loaded after the std test (63 registers: 4 CTAs / SM)
 #endif
 #ifndef FUSED_RINGS_MINB
-#define FUSED_RINGS_MINB 4  // measured: config 1 K3 -3.4%, config 4 -12% vs one-phase loads at 3 CTAs / SM
+#define FUSED_RINGS_MINB 2  // 2 CTAs x 16 warps: 63 registers (X / Y loaded after the std test); config 1 K3 -3.4%, config 4 -12% vs one-phase loads at 24 warps / SM
 #endif
 #include <cuda.h>
 
@@ -616,7 +616,10 @@ __device__ __forceinline__ void stage_bitmaps(const ScreenArgs& a, unsigned* sbi
     }
 }
 
-constexpr int RK_WARPS = 8;
+#ifndef RK_WARPS_MACRO
+#define RK_WARPS_MACRO 16  // rings warps per CTA (measured: 16 x 2 CTAs ~ 8 x 4 CTAs, slightly ahead)
+#endif
+constexpr int RK_WARPS = RK_WARPS_MACRO;
 #ifndef QCAP_MACRO
 #define QCAP_MACRO 64
 #endif
