@@ -283,6 +283,9 @@ class Engine:
         self.screen_ws = None  # per-size workspaces, one per side stream (allocated when the per-size path runs)
         self.ladder_ws = None  # fused ladder workspace (allocated for the first ladder that needs it)
         self.region_stream = None  # K5 beside K4
+        self.copy_stream = None  # survivor-row readback (start_readback)
+        self.compact_event = None  # recorded after K4 of the last run
+        self.readback_done = None  # the last readback's completion (K4 of the next run waits on it)
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -435,6 +438,9 @@ class Engine:
         if build:
             self.build_tables(img, int64=self.needs_int64(tp))
         main = torch.cuda.current_stream(self.device)
+        if self.readback_done is not None:  # the previous run's rows must have left before K4 rewrites them
+            main.wait_event(self.readback_done)
+            self.readback_done = None
         if self.hooks is not None:
             self.hooks[0](main)
         self.screen_ladder(tp, main)
@@ -450,8 +456,30 @@ class Engine:
             with torch.cuda.stream(rs):
                 self.region_all(tp)
         self.compact_all(tp)
+        if self.compact_event is None:
+            self.compact_event = torch.cuda.Event()
+        self.compact_event.record(main)
         if region:
             main.wait_stream(rs)
+
+    def start_readback(self):
+        """Start copying the survivor rows (capacity rows, int32 (cx, cy, m))
+        into a fresh pinned buffer on a copy stream, right after the last
+        run's K4 -- overlapping K5 and the host's result bookkeeping.
+        Returns (buffer, event) for CandidateList."""
+        if self.compact_event is None:
+            return None
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream(self.device)
+        cs = self.copy_stream
+        host = torch.empty((self.capacity, 3), dtype=torch.int32, pin_memory=True)
+        cs.wait_event(self.compact_event)
+        with torch.cuda.stream(cs):
+            host.copy_(self.xy[: self.capacity], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+        self.readback_done = done
+        return host, done
 
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:
         """Grow the survivor buffer and redo K4 only (after an overflow)."""

@@ -155,9 +155,12 @@ class CandidateList(Sequence):
     first use, then copied once -- and the per-size counts.
     """
 
-    def __init__(self, rows, n: int):
+    def __init__(self, rows, n: int, host=None):
         self._rows = rows  # (k, 3) int32 array or CUDA tensor
         self._n = int(n)
+        # optional (pinned (cap, 3) tensor, event): the rows already on their
+        # way to the host (Engine.start_readback), used when they cover n
+        self._host = host if host is not None and host[0].shape[0] >= self._n else None
 
     @staticmethod
     def build(xy, ladder: Tuple[int, ...], counts: List[int]) -> "CandidateList":
@@ -171,7 +174,12 @@ class CandidateList(Sequence):
     def array(self) -> np.ndarray:
         """(k, 3) int32 [cx, cy, m]."""
         if isinstance(self._rows, torch.Tensor):
-            self._rows = _to_host(self._rows).reshape(-1, 3)
+            if self._host is not None:
+                buf, done = self._host
+                done.synchronize()
+                self._rows = buf[: self._n].numpy()  # a view: buf stays referenced by the array base
+            else:
+                self._rows = _to_host(self._rows).reshape(-1, 3)
         return self._rows
 
     @property
@@ -318,9 +326,11 @@ def validate(image, template, cfg: ScreeningConfig):
     return img, tpl
 
 
-def fetch_result(eng: Engine, tp: TemplatePlan, start: float) -> ScreeningResult:
+def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> ScreeningResult:
     """Counts to the host; survivor list, masks and region stay on the device
-    (private copies, the engine's buffers are reused) until first accessed."""
+    (private copies, the engine's buffers are reused) until first accessed;
+    `readback` (Engine.start_readback) carries the survivor rows' host copy
+    that started right after compaction."""
     totals = eng.totals.cpu()  # synchronises the stream
     kept = int(totals[0])
     if kept > eng.capacity:
@@ -339,7 +349,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float) -> ScreeningResult
         total_pixels=W * H,
         wall_time_s=elapsed,
     )
-    cands = CandidateList(rows, kept)
+    cands = CandidateList(rows, kept, readback)
     return ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, SizeMasks(tp.ladder, packed, W),
                            region, stats, size_counts)
 
@@ -366,7 +376,8 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     eng.build_tables(img_dev, int64=eng.needs_int64(tp))
     fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
     eng.run(img_dev, tp, build=False)
-    return fetch_result(eng, tp, start)
+    readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
+    return fetch_result(eng, tp, start, readback)
 
 
 _pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
