@@ -286,6 +286,7 @@ class Engine:
         self.copy_stream = None  # survivor-row readback (start_readback)
         self.compact_event = None  # recorded after K4 of the last run
         self.readback_done = None  # the last readback's completion (K4 of the next run waits on it)
+        self.last_kept = None  # survivors of the last fetched screen (sizes the next readback)
         self.totals = torch.zeros(2, dtype=torch.int64, device=self.device)  # [0] survivors, [1] region pixels
         self.n_sizes = 0
         self.masks = None
@@ -463,19 +464,21 @@ class Engine:
             main.wait_stream(rs)
 
     def start_readback(self):
-        """Start copying the survivor rows (capacity rows, int32 (cx, cy, m))
-        into a fresh pinned buffer on a copy stream, right after the last
-        run's K4 -- overlapping K5 and the host's result bookkeeping.
-        Returns (buffer, event) for CandidateList."""
-        if self.compact_event is None:
-            return None
+        """Start copying the survivor rows (int32 (cx, cy, m); as many as the
+        last screen kept plus a margin) into a fresh pinned buffer on a copy
+        stream, right after the last run's K4 -- overlapping K5 and the host's
+        result bookkeeping.  Returns (buffer, event) for CandidateList (which
+        falls back to its own copy when the survivors outnumber the buffer)."""
+        if self.compact_event is None or self.last_kept is None:
+            return None  # no estimate of the survivor count yet
+        rows = min(self.capacity, int(self.last_kept * 1.25) + 4096)  # last screen's count + margin
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(self.device)
         cs = self.copy_stream
-        host = torch.empty((self.capacity, 3), dtype=torch.int32, pin_memory=True)
+        host = torch.empty((rows, 3), dtype=torch.int32, pin_memory=True)
         cs.wait_event(self.compact_event)
         with torch.cuda.stream(cs):
-            host.copy_(self.xy[: self.capacity], non_blocking=True)
+            host.copy_(self.xy[:rows], non_blocking=True)
             done = torch.cuda.Event()
             done.record(cs)
         self.readback_done = done

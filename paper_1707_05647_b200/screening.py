@@ -337,6 +337,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> 
         eng.recompact(tp, kept)
         totals = eng.totals.cpu()
     size_counts = eng.size_counts[: len(tp.sizes)].cpu().tolist()
+    eng.last_kept = kept
     rows = eng.xy[:kept].clone()
     packed = eng.masks[: len(tp.sizes)].clone()
     region = eng.region.clone() if eng.region is not None else None
