@@ -394,7 +394,6 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     RingDev* sring = reinterpret_cast<RingDev*>(rsm);
     SizeSm* ssize = reinterpret_cast<SizeSm*>(rsm + (size_t)a.n_rings * sizeof(RingDev));
     unsigned* sbits = reinterpret_cast<unsigned*>(ssize + a.n_sizes);
-    __shared__ int qcnt[RK_WARPS][SS_MAX_RINGS];
     {
         const int* src = reinterpret_cast<const int*>(a.ring);
         int* dst = reinterpret_cast<int*>(sring);
@@ -413,7 +412,9 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int levels = a.max_levels;
     int2* queues = reinterpret_cast<int2*>(sbits + ((a.bm_words + 1) & ~1)) + (size_t)warp * levels * QCAP;
-    if (lane < SS_MAX_RINGS) qcnt[warp][lane] = 0;
+    // per-level queue fill counts, 8 bits each, warp-uniform in a register (levels <= 8)
+    unsigned long long qc = 0;
+    auto qget = [&](int l) { return (int)((qc >> (8 * l)) & 255ull); };
     __syncthreads();
     const unsigned lt = (1u << lane) - 1u;
     unsigned long long n_pass0 = 0, n_surv = 0;
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     for (;;) {
         int level = -1;
         for (int l = levels - 1; l >= 1; --l)
-            if (qcnt[warp][l] >= 32) { level = l; break; }
+            if (qget(l) >= 32) { level = l; break; }
         int2 e;
         if (level < 0 && have_input) {
             level = 0;
@@ -467,15 +468,14 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         } else {
             if (level < 0) {
                 for (int l = levels - 1; l >= 1; --l)
-                    if (qcnt[warp][l] > 0) { level = l; break; }
+                    if (qget(l) > 0) { level = l; break; }
                 if (level < 0) break;
             }
-            const int c = qcnt[warp][level], take = min(c, 32);
+            const int c = qget(level), take = min(c, 32);
             const int2* qq = queues + level * QCAP;
             e = ((int)lane < take) ? qq[c - take + lane] : make_int2(-1, -1);
-            __syncwarp();
-            if (lane == 0) qcnt[warp][level] = c - take;
-            __syncwarp();
+            qc -= (unsigned long long)take << (8 * level);
+            __syncwarp();  // the slots just read may be refilled by the next push
         }
         const bool valid = e.x >= 0;
         const int sz = valid ? (e.y >> TAG_SHIFT) : 0, y = e.y & YMASK;
@@ -508,11 +508,10 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         }
         const unsigned qb = pb & ~sb;
         if (qb) {
-            const int c = qcnt[warp][level + 1];
+            const int c = qget(level + 1);
             if (pass && !last) queues[(level + 1) * QCAP + c + __popc(qb & lt)] = e;
-            __syncwarp();
-            if (lane == 0) qcnt[warp][level + 1] = c + __popc(qb);
-            __syncwarp();
+            qc += (unsigned long long)__popc(qb) << (8 * (level + 1));
+            __syncwarp();  // the entries are visible to the lanes that pop them
         }
     }
     if (a.stage_counts && lane == 0) {
@@ -685,6 +684,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         max_m = std::max(max_m, m);
         n_rings += nr;
     }
+    if (a.max_levels > 8) return SS_DECLINED;  // the rings' queue counts are 8 x 8 bits
     a.n_rings = n_rings;
     a.bm_words = bm_words;
     a.bm1_words = bm1;
