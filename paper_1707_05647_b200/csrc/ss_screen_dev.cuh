@@ -558,7 +558,14 @@ constexpr int TILE_CTRS = MAX_PARTS;  // stage-1 tile counters (partition p's CT
 // List slots a stage-1 warp reserves per atomic (a multiple of 32): fewer
 // atomics on the list counter vs. the padding of each warp's last blocks
 // (measured: 64 for the single list, 128 for the partitioned lists).
-constexpr int RESERVE_SMALL = 64, RESERVE_LARGE = 128, RESERVE_MAX = 128;
+#ifndef RESERVE_SMALL_MACRO
+#define RESERVE_SMALL_MACRO 64
+#endif
+#ifndef RESERVE_LARGE_MACRO
+#define RESERVE_LARGE_MACRO 128
+#endif
+constexpr int RESERVE_SMALL = RESERVE_SMALL_MACRO, RESERVE_LARGE = RESERVE_LARGE_MACRO,
+              RESERVE_MAX = RESERVE_SMALL > RESERVE_LARGE ? RESERVE_SMALL : RESERVE_LARGE;
 #ifndef GROUP_CTRS
 #define GROUP_CTRS 8u  // rings group counters per partition
 #endif
