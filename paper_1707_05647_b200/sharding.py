@@ -146,12 +146,27 @@ def assemble(parts: List[BandResult], width: int, height: int, ladder: Sequence[
     return masks, np.ascontiguousarray(xy, dtype=np.int32).reshape(-1, 2), counts, tested
 
 
-def screen_band_device(image: np.ndarray, tp, band: Band, device) -> BandResult:
-    """This rank's band on its GPU (libstarscreen through engine.Engine)."""
+_band_engines: dict = {}
+
+
+def band_engine(W: int, H: int, band: Band, device):
+    """One cached engine per (shape, band, device) -- the most recent only:
+    an engine's tables and workspaces are allocated once, not per call."""
     from .engine import Engine
 
+    key = (W, H, band.y_origin, band.rows, band.y_begin, band.y_end, str(torch.device(device)))
+    eng = _band_engines.get(key)
+    if eng is None:
+        _band_engines.clear()
+        eng = Engine(W, H, device, band=(band.y_origin, band.rows, band.y_begin, band.y_end))
+        _band_engines[key] = eng
+    return eng
+
+
+def screen_band_device(image: np.ndarray, tp, band: Band, device) -> BandResult:
+    """This rank's band on its GPU (libstarscreen through engine.Engine)."""
     H, W = image.shape
-    eng = Engine(W, H, device, band=(band.y_origin, band.rows, band.y_begin, band.y_end))
+    eng = band_engine(W, H, band, device)
     sub = torch.from_numpy(np.ascontiguousarray(image[band.y_origin:band.y_origin + band.rows])).to(eng.device)
     eng.run(sub, tp, region=False)
     totals = eng.totals.cpu()
