@@ -70,9 +70,9 @@ class BandResult:
     """One rank's share: survivors in global coordinates, packed mask rows."""
 
     band: Band
-    counts: np.ndarray  # (L,) int64 survivors per ladder size
-    xy: np.ndarray  # (k, 2) int32, ladder order then row-major
-    masks: np.ndarray  # (L, y_end - y_begin, words) uint32
+    counts: "torch.Tensor"  # (L,) int64 survivors per ladder size
+    rows: "torch.Tensor"  # (k, 3) int32 (cx, cy, m), ladder order then row-major
+    masks: "torch.Tensor"  # (L, y_end - y_begin, words) int32 (bit-packed rows)
     tested: int
 
 
@@ -98,24 +98,21 @@ def _all_gather_padded(t: torch.Tensor, group=None) -> List[torch.Tensor]:
 
 
 def gather_band_results(local: BandResult, group=None) -> List[BandResult]:
-    """All ranks' BandResults, in rank order (every rank receives all)."""
+    """All ranks' BandResults, in rank order (every rank receives all); the
+    tensors stay on the collective's device (NCCL: the GPU)."""
     world = dist.get_world_size(group)
     dev = _coll_device(group)
-    counts = torch.from_numpy(local.counts.astype(np.int64)).to(dev)
+    counts = torch.as_tensor(local.counts, dtype=torch.int64).to(dev)
     allc = [torch.zeros_like(counts) for _ in range(world)]
     dist.all_gather(allc, counts, group=group)
-    xys = _all_gather_padded(torch.from_numpy(np.ascontiguousarray(local.xy, dtype=np.int32)), group)
-    m = np.ascontiguousarray(local.masks).view(np.int32)
-    ms = _all_gather_padded(torch.from_numpy(np.moveaxis(m, 1, 0).copy()), group)  # rows first
+    rows = _all_gather_padded(torch.as_tensor(local.rows, dtype=torch.int32).reshape(-1, 3), group)
+    m = torch.as_tensor(local.masks).view(torch.int32)
+    ms = _all_gather_padded(m.permute(1, 0, 2).contiguous(), group)  # rows first
     tested = torch.tensor([local.tested], dtype=torch.int64, device=dev)
     allt = [torch.zeros_like(tested) for _ in range(world)]
     dist.all_gather(allt, tested, group=group)
     bands = plan_bands_from(local.band, world, group)
-    out = []
-    for r in range(world):
-        out.append(BandResult(bands[r], allc[r].cpu().numpy(), xys[r].cpu().numpy(),
-                              np.moveaxis(ms[r].cpu().numpy(), 0, 1).view(np.uint32), int(allt[r].item())))
-    return out
+    return [BandResult(bands[r], allc[r], rows[r], ms[r].permute(1, 0, 2), int(allt[r].item())) for r in range(world)]
 
 
 def plan_bands_from(band: Band, world: int, group=None) -> List[Band]:
@@ -127,23 +124,24 @@ def plan_bands_from(band: Band, world: int, group=None) -> List[Band]:
 
 
 def assemble(parts: List[BandResult], width: int, height: int, ladder: Sequence[int]):
-    """Concatenate band results into full-image arrays (ladder order, row-major)."""
+    """Concatenate band results into full-image tensors on the parts' device
+    (ladder order, then row-major): masks (L, H, words) int32, rows (K, 3)
+    int32, counts (L,) int64 (host), tested."""
     L = len(ladder)
     words = (width + 31) // 32
-    masks = np.zeros((L, height, words), np.uint32)
-    xy_parts = [[] for _ in range(L)]
+    dev = parts[0].rows.device if parts else torch.device("cpu")
+    masks = torch.zeros((L, height, words), dtype=torch.int32, device=dev)
+    per_size = [[] for _ in range(L)]
     for p in sorted(parts, key=lambda p: p.band.y_begin):
         masks[:, p.band.y_begin:p.band.y_end] = p.masks
-        start = 0
-        for k in range(L):
-            c = int(p.counts[k])
-            xy_parts[k].append(p.xy[start:start + c])
-            start += c
-    counts = np.array([sum(len(a) for a in xy_parts[k]) for k in range(L)], np.int64)
-    xy = np.concatenate([np.concatenate(xy_parts[k]) if xy_parts[k] else np.zeros((0, 2), np.int32)
-                         for k in range(L)]) if L else np.zeros((0, 2), np.int32)
+        cnts = [int(c) for c in p.counts.tolist()]
+        for k, chunk in enumerate(torch.split(p.rows, cnts)):
+            per_size[k].append(chunk)
+    counts = np.array([sum(int(c.shape[0]) for c in per_size[k]) for k in range(L)], np.int64)
+    empty = torch.zeros((0, 3), dtype=torch.int32, device=dev)
+    rows = torch.cat([torch.cat(per_size[k]) if per_size[k] else empty for k in range(L)]) if L else empty
     tested = sum(p.tested for p in parts)
-    return masks, np.ascontiguousarray(xy, dtype=np.int32).reshape(-1, 2), counts, tested
+    return masks, rows, counts, tested
 
 
 _band_engines: dict = {}
@@ -173,32 +171,31 @@ def screen_band_device(image: np.ndarray, tp, band: Band, device) -> BandResult:
     kept = int(totals[0])
     if kept > eng.capacity:
         eng.recompact(tp, kept)
-    counts = eng.size_counts[: len(tp.sizes)].cpu().numpy().astype(np.int64)
-    xy = eng.xy[:kept, :2].cpu().numpy()
-    masks = eng.masks[: len(tp.sizes)].cpu().numpy().view(np.uint32)
-    return BandResult(band, counts, xy, masks, eng.tested(tp))
+    counts = eng.size_counts[: len(tp.sizes)].clone()
+    rows = eng.xy[:kept].clone()  # (cx, cy, m) on the device
+    masks = eng.masks[: len(tp.sizes)].clone()
+    return BandResult(band, counts, rows, masks, eng.tested(tp))
 
 
-def region_from_masks(masks: np.ndarray, width: int, height: int, ladder: Sequence[int], stride: int, device):
-    """Kept region (K5) on the device from the gathered full survivor masks."""
+def region_from_masks(masks, width: int, height: int, ladder: Sequence[int], stride: int, device):
+    """Kept region (K5, ladder form) on the device from the gathered full
+    survivor masks ((L, H, words) int32 tensor); returns (packed region
+    tensor on the device, kept pixels)."""
     from . import _native
 
     L = _native.lib()
     dev = torch.device(device)
     words = (width + 31) // 32
-    m_max = max(ladder) if ladder else 1
-    region = torch.zeros((height, words), dtype=torch.int32, device=dev)
-    ws = torch.empty(int(L.ss_region_workspace_bytes(width, height, m_max)), dtype=torch.uint8, device=dev)
+    mk = torch.as_tensor(masks).to(dev).view(torch.int32).contiguous()
+    ms = np.asarray(ladder, np.int32)
+    region = torch.empty((height, words), dtype=torch.int32, device=dev)
+    ws = torch.empty(int(L.ss_region_ladder_workspace_bytes(width, height, len(ms))), dtype=torch.uint8, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     s = torch.cuda.current_stream(dev).cuda_stream
-    for k, m in enumerate(ladder):
-        if m < MIN_PATCH_SIDE:
-            continue
-        mk = torch.from_numpy(np.ascontiguousarray(masks[k]).view(np.int32)).to(dev)
-        _native.check(L.ss_region_accumulate(mk.data_ptr(), words, width, height, m, stride, region.data_ptr(),
-                                             ws.data_ptr(), ws.numel(), s), "region")
+    _native.check(L.ss_region_ladder(mk.data_ptr(), words, height * words, width, height, len(ms), ms.ctypes.data,
+                                     stride, region.data_ptr(), ws.data_ptr(), ws.numel(), s), "region")
     _native.check(L.ss_popcount(region.data_ptr(), words, width, height, cnt.data_ptr(), s), "popcount")
-    return region.cpu().numpy().view(np.uint32), int(cnt.item())
+    return region, int(cnt.item())
 
 
 def screen_sharded(image: np.ndarray, template: np.ndarray, cfg=None, group=None, device=None,
@@ -225,8 +222,11 @@ def screen_sharded(image: np.ndarray, template: np.ndarray, cfg=None, group=None
     band = plan_bands(H, world, tp.ladder)[rank]
     local = (band_fn or screen_band_device)(img, tp, band, dev)
     parts = gather_band_results(local, group)
-    masks, xy, counts, tested = assemble(parts, W, H, tp.ladder)
-    region, kept_px = (region_fn or region_from_masks)(masks, W, H, tp.ladder, cfg.stride, dev)
+    masks, rows, counts, tested = assemble(parts, W, H, tp.ladder)
+    if region_fn is None:
+        region, kept_px = region_from_masks(masks, W, H, tp.ladder, cfg.stride, dev)
+    else:  # host stand-in (tests)
+        region, kept_px = region_fn(masks.cpu().numpy().view(np.uint32), W, H, tp.ladder, cfg.stride, dev)
     stats = PruneStats(tested, int(counts.sum()), kept_px, W * H, time.perf_counter() - start)
-    return ScreeningResult(W, H, tp.template_side, cfg, tp.ladder, CandidateList.build(xy, tp.ladder, counts.tolist()),
-                           SizeMasks(tp.ladder, masks, W), region, stats)
+    return ScreeningResult(W, H, tp.template_side, cfg, tp.ladder, CandidateList(rows, int(rows.shape[0])),
+                           SizeMasks(tp.ladder, masks, W), region, stats, counts.tolist())

@@ -276,12 +276,12 @@ def test_row_bands_on_device_assemble_to_full_screen(cuda, world):
     full = screen(img, case.template, cfg)
     tp = prepare_template(case.template, cfg, cuda)
     parts = [screen_band_device(img, tp, b, cuda) for b in plan_bands(img.shape[0], world, tp.ladder)]
-    masks, xy, counts, tested = assemble(parts, img.shape[1], img.shape[0], tp.ladder)
+    masks, rows, counts, tested = assemble(parts, img.shape[1], img.shape[0], tp.ladder)
     assert tested == full.stats.patches_tested
-    assert np.array_equal(xy, full.candidates.array()[:, :2])
+    assert np.array_equal(rows.cpu().numpy(), full.candidates.array())
     assert list(counts) == full.candidates_per_size()
     for k, m in enumerate(full.ladder):
-        assert np.array_equal(masks[k], full.size_masks.packed(m)), m
+        assert np.array_equal(masks[k].cpu().numpy().view(np.uint32), full.size_masks.packed(m).view(np.uint32)), m
 
 
 def _boundary_image(seed):

@@ -13,6 +13,7 @@ import os
 import socket
 
 import numpy as np
+import torch
 import pytest
 import torch.multiprocessing as mp
 
@@ -74,7 +75,7 @@ def oracle_band(img, tp, band, dev):
                         break
                 if ok:
                     masks[k, y - band.y_begin, x] = True
-                    xy.append((x, y))
+                    xy.append((x, y, m))
                     c += 1
         counts.append(c)
     words = (W + 31) // 32
@@ -82,8 +83,9 @@ def oracle_band(img, tp, band, dev):
     if rows:
         b = np.packbits(masks.astype(np.uint8), axis=2, bitorder="little")
         packed[:, :, : b.shape[2]] = b
-    return BandResult(band, np.array(counts, np.int64), np.array(xy, np.int32).reshape(-1, 2),
-                      packed.view(np.uint32), tested)
+    return BandResult(band, torch.tensor(counts, dtype=torch.int64),
+                      torch.from_numpy(np.array(xy, np.int32).reshape(-1, 3)),
+                      torch.from_numpy(packed.view(np.int32).copy()), tested)
 
 
 def oracle_region(masks, W, H, ladder, stride, dev):
