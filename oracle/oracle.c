@@ -100,7 +100,7 @@ static inline int64_t or_diamond_sum(const int64_t* t, int64_t W, int64_t H, int
            rsat_h(t, W, H, u + r, v + r + 1) + rsat_h(t, W, H, u - r - 1, v + r + 1);
 }
 
-/* features.py:322-330 _square_stats_from_sums: exact NumPy op order. */
+/* features.py:94-102 _square_stats_from_sums: exact NumPy op order. */
 static void or_square_stats(int64_t s1, int64_t sx, int64_t sy, int64_t s2, int64_t cx, int64_t cy,
                             int64_t n, double out[4]) {
     const double count = (double)(4 * n * n);
@@ -113,11 +113,11 @@ static void or_square_stats(int64_t s1, int64_t sx, int64_t sy, int64_t s2, int6
     out[3] = ((double)sy - ((double)cy + 1.5) * (double)s1) / w1;
 }
 
-/* features.py:341-343 _ball_l1_mass; integral.py:189-191 diamond_pixel_count. */
+/* features.py:113-115 _ball_l1_mass; integral.py:189-191 diamond_pixel_count. */
 static inline int64_t or_ball_l1_mass(int64_t r) { return 2 * r * r + r * (r - 1) * (2 * r - 1) / 3; }
 static inline int64_t or_diamond_count(int64_t r) { return 2 * r * r + 2 * r + 1; }
 
-/* features.py:346-353 _diamond_stats_from_sums. */
+/* features.py:118-125 _diamond_stats_from_sums. */
 static void or_diamond_stats(int64_t s1, int64_t sx, int64_t sy, int64_t s2, int64_t cx, int64_t cy,
                              int64_t r, double out[4]) {
     const double count = (double)or_diamond_count(r);
@@ -130,7 +130,7 @@ static void or_diamond_stats(int64_t s1, int64_t sx, int64_t sy, int64_t s2, int
     out[3] = ((double)sy - ((double)cy + 1.0) * (double)s1) / w1;
 }
 
-/* features.py:364-370 _octagon_from_parts. */
+/* features.py:136-142 _octagon_from_parts. */
 static void or_octagon_from_parts(const double sq[4], const double di[4], double out[3]) {
     const double gx = (sq[2] + di[2]) * 0.5;
     const double gy = (sq[3] + di[3]) * 0.5;
@@ -139,7 +139,7 @@ static void or_octagon_from_parts(const double sq[4], const double di[4], double
     out[2] = sqrt(gx * gx + gy * gy);
 }
 
-/* features.py:379-382 _octagon_maps for one center. */
+/* features.py:151-154 _octagon_maps for one center. */
 static void or_octagon(const or_tables* t, int64_t cx, int64_t cy, int64_t n, int64_t d, double out[3]) {
     double sq[4], di[4];
     or_square_stats(or_square_sum(t->sat[K_PLAIN], t->W, cx, cy, n),
@@ -204,7 +204,7 @@ int64_t or_scan_size(const int64_t* const* sats, const int64_t* const* rsats, in
     or_tables t;
     for (int k = 0; k < 4; ++k) { t.sat[k] = sats[k]; t.rsat[k] = rsats[k]; }
     t.W = W; t.H = H;
-    /* features.py:442-445 patch_center_margins */
+    /* features.py:214-217 patch_center_margins */
     const int64_t lo = (m - 1) / 2, hi = m / 2;
     memset(mask, 0, (size_t)W * (size_t)H);
     int64_t nix = 0, niy = 0;

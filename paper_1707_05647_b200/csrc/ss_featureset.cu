@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(TPB) template_features_kernel(const uint8_t* _
                 S[q] = t;
             }
             const long long n64 = nr, d64 = dr;
-            // features.py:322-330 (square) / :346-353 (diamond) / :364-370 (octagon)
+            // features.py:94-102 (square) / :346-353 (diamond) / :364-370 (octagon)
             const double cq = (double)(4 * n64 * n64), wq = (double)(2 * n64 * n64 * n64);
             const double mq = __ddiv_rn((double)S[0], cq);
             const double vq = __dsub_rn(__ddiv_rn((double)S[3], cq), __dmul_rn(mq, mq));

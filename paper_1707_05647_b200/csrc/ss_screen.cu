@@ -2,7 +2,7 @@
 //
 // Replaces _scan_size (screening.py:418-471) for one ladder size: the ring
 // features of _ring_maps_rect / _octagon_maps (screening.py:380-415,
-// features.py:322-382), _quantize_arr (screening.py:86-87), _pack_cells
+// features.py:94-154), _quantize_arr (screening.py:86-87), _pack_cells
 // (:90-97), _member_mask (:173-178) and the nonzero / mask bookkeeping.
 //
 // Bit-exactness: compiled with -fmad=false; every fp64 op is one IEEE-
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) stage1_kernel(const Scree
             if (interior) pass = member_m(a, R0, sbits, mean_cell(a, R0, s1q[c], s1d[c]));
 #else
             if (interior) {
-                const double mq = div_rn((double)s1q[c], R0.cnt_sq, R0.rcp_sq);  // features.py:325
-                const double md = div_rn((double)s1d[c], R0.cnt_di, R0.rcp_di);  // features.py:349
+                const double mq = div_rn((double)s1q[c], R0.cnt_sq, R0.rcp_sq);  // features.py:97
+                const double md = div_rn((double)s1d[c], R0.cnt_di, R0.rcp_di);  // features.py:121
                 pass = member_m(a, R0, sbits, quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm, a.qpow2 & 1));
             }
 #endif

@@ -185,12 +185,12 @@ __device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long
 __device__ __forceinline__ float to_f32(long long v) { return __ll2float_rn(v); }
 __device__ __forceinline__ float to_f32(unsigned v) { return __uint2float_rn(v); }
 
-// Mean cell floor(t), t = ((s1q/cq + s1d/cd) * 0.5) / qm + 0.5 (features.py:325, 349, 365;
+// Mean cell floor(t), t = ((s1q/cq + s1d/cd) * 0.5) / qm + 0.5 (features.py:97, 349, 365;
 // screening.py:86-87), from exact non-negative PLAIN sums.  The fp32 estimate tf is
 // within 4e-7 (tf + 1) of the fp64 t (six roundings of 2^-24 on non-negative terms), so
 // when [tf - dl, tf + dl] holds no integer, floor(t) = floor(tf) exactly; only centres
 // whose mean lies within ~4e-6 of a cell boundary take the fp64 op sequence.
-// The fp64 mean cell of ring R (features.py:325, 349, 365; screening.py:86-87).
+// The fp64 mean cell of ring R (features.py:97, 349, 365; screening.py:86-87).
 template <typename S, class A>
 __device__ __forceinline__ int mean_cell_exact(const A& a, const RingDev& R, S s1q, S s1d) {
     const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);
@@ -203,8 +203,8 @@ __device__ __forceinline__ int mean_cell(const A& a, const RingDev& R, S s1q, S 
     const float dl = fmaf(tf, 4e-6f, 4e-6f);
     int cm = (int)floorf(tf - dl);
     if (cm != (int)floorf(tf + dl)) {
-        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
-        const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);  // features.py:349
+        const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq);  // features.py:97
+        const double md = div_rn((double)s1d, R.cnt_di, R.rcp_di);  // features.py:121
         cm = quant(__dmul_rn(__dadd_rn(mq, md), 0.5), a.qm, a.rqm, a.qpow2 & 1);
     }
     return cm;
@@ -229,18 +229,18 @@ __device__ __forceinline__ Stage1 stage1_from(const A& a, const RingDev& R, long
     Stage1 s;
     s.s1q = s1q;
     s.s1d = s1d;
-    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);  // features.py:325
-    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);  // features.py:349
+    s.mq = div_rn((double)s.s1q, R.cnt_sq, R.rcp_sq);  // features.py:97
+    s.md = div_rn((double)s.s1d, R.cnt_di, R.rcp_di);  // features.py:121
 #if RINGS_FAST_CM
-    s.cm = mean_cell(a, R, s1q, s1d);  // features.py:365
+    s.cm = mean_cell(a, R, s1q, s1d);  // features.py:137
 #else
-    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm, a.qpow2 & 1);  // features.py:365
+    s.cm = quant(__dmul_rn(__dadd_rn(s.mq, s.md), 0.5), a.qm, a.rqm, a.qpow2 & 1);  // features.py:137
 #endif
     return s;
 }
 
 // Stages 2 (std) and 3 (gradient) of ring R from its SQUARED, X and Y corners.
-// The fp64 std cell (features.py:326, 350, 366; screening.py:86-87):
+// The fp64 std cell (features.py:98, 350, 366; screening.py:86-87):
 // sqrt(max(s2/count - mean*mean, 0)) of both parts, averaged, quantized.
 template <class A>
 __device__ __forceinline__ int std_cell_exact(const A& a, const RingDev& R, double mq, double md, long long s2q,
@@ -250,7 +250,7 @@ __device__ __forceinline__ int std_cell_exact(const A& a, const RingDev& R, doub
     const double sd = __dmul_rn(__dadd_rn(__dsqrt_rn(vq > 0.0 ? vq : 0.0), __dsqrt_rn(vd > 0.0 ? vd : 0.0)), 0.5);
     return quant(sd, a.qs, a.rqs, (a.qpow2 >> 1) & 1);
 }
-// The fp64 gradient-magnitude cell (features.py:328-329, 351-352, 367-371)
+// The fp64 gradient-magnitude cell (features.py:100-101, 351-352, 367-371)
 // from the exact first moments sx*, sy* (weights x+1 / y+1) and PLAIN sums:
 // (s - (c + off) * s1) / w1 -- product and difference exact -- averaged,
 // hypot as sqrt(gx*gx + gy*gy), quantized.
@@ -368,7 +368,7 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
     load_corners(P, R, 2, cky);
 #endif
     const long long s1q = unsigned_sum(sq_of(c0)), s1d = unsigned_sum(di_of(c0));
-    const int cm = mean_cell(a, R, s1q, s1d);  // features.py:365 (level 0 entries passed this test in stage 1)
+    const int cm = mean_cell(a, R, s1q, s1d);  // features.py:137 (level 0 entries passed this test in stage 1)
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 4 + 4 * level, 1ull);
 #endif
@@ -425,10 +425,10 @@ inline int fill_ring(RingDev& R, int n, int d, int m, long long P, double qm, co
     R.ed = (int)(-(long long)d * P + 1);
     R.ob = -d;
     R.oc = d + 1;
-    R.cnt_sq = (double)(4LL * n * n);                                            // features.py:323
-    R.w1_sq = (double)(2LL * n * n * n);                                         // features.py:324
+    R.cnt_sq = (double)(4LL * n * n);                                            // features.py:95
+    R.w1_sq = (double)(2LL * n * n * n);                                         // features.py:96
     R.cnt_di = (double)(2LL * d * d + 2LL * d + 1);                              // integral.py:189-191
-    R.w1_di = (double)(2LL * d * d + (long long)d * (d - 1) * (2 * d - 1) / 3);  // features.py:341-343
+    R.w1_di = (double)(2LL * d * d + (long long)d * (d - 1) * (2 * d - 1) / 3);  // features.py:113-115
     R.rcp_sq = 1.0 / R.cnt_sq;  // host IEEE division: RN(1/b)
     R.rcp_di = 1.0 / R.cnt_di;
     R.rw1_sq = 1.0 / R.w1_sq;

@@ -52,7 +52,7 @@ struct Sums {
     int64_t s1 = 0, sx = 0, sy = 0, s2 = 0;
 };
 
-// features.py:322-370 on exact integer sums of the m x m patch z, centre c.
+// features.py:94-142 on exact integer sums of the m x m patch z, centre c.
 void ring_features(const uint8_t* z, int64_t m, int32_t n_rings, const int32_t* rn, const int32_t* rd, double* out) {
     const int64_t c = (m - 1) / 2;
     for (int32_t r = 0; r < n_rings; ++r) {

@@ -23,7 +23,7 @@ from .image import as_gray
 
 @dataclass(frozen=True)
 class RingBand:
-    """features.py:298-304."""
+    """features.py:70-76."""
 
     half_size: int
     radius: int
@@ -34,7 +34,7 @@ class RingBand:
 
 @dataclass(frozen=True)
 class RingFeatureVector:
-    """features.py:307-319: per-ring triples, outermost ring first."""
+    """features.py:79-91: per-ring triples, outermost ring first."""
 
     rings: Tuple[RingBand, ...]
 

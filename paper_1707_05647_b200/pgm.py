@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import json
 import os
+import re
 import tempfile
 from pathlib import Path
 from typing import Dict, Optional, Tuple, Union
@@ -33,50 +34,40 @@ class PgmError(ValueError):
     """Raised for malformed or unsupported PGM input (image_io.py:21-22)."""
 
 
-def _read_header_token(data: bytes, pos: int) -> Tuple[bytes, int]:
-    """image_io.py:43-60: skip whitespace and '#' comments, return (token, next position)."""
-    n = len(data)
-    while pos < n:
-        c = data[pos:pos + 1]
-        if c == b"#":
-            while pos < n and data[pos:pos + 1] not in (b"\n", b"\r"):
-                pos += 1
-        elif c.isspace():
-            pos += 1
-        else:
-            break
-    start = pos
-    while pos < n and not data[pos:pos + 1].isspace():
-        pos += 1
-    if start == pos:
-        raise PgmError("truncated PGM header")
-    return data[start:pos], pos
+# One header field: any run of whitespace and '#' comments (to end of line),
+# then the field itself (a maximal run of non-whitespace bytes).
+_FIELD = re.compile(rb"(?:[ \t\n\r\v\f]|#[^\n\r]*)*([^ \t\n\r\v\f]*)")
 
 
 def load_pgm(path: PathLike) -> np.ndarray:
-    """Load a binary (P5) PGM file as a (height, width) uint8 array (image_io.py:63-105)."""
+    """Binary P5 PGM -> (height, width) uint8 array; same acceptance rules and
+    PgmError cases as image_io.py:63-105 (header fields separated by
+    whitespace / comments, maxval 1..255, one whitespace byte before the
+    raster, trailing bytes ignored)."""
     data = Path(path).read_bytes()
-    if data[:2] != b"P5":
+    if not data.startswith(b"P5"):
         raise PgmError(f"unsupported PNM magic {data[:2]!r}, only binary P5 is handled")
-    pos = 2
-    fields = []
-    for _ in range(3):
-        tok, pos = _read_header_token(data, pos)
+    fields, pos = [], 2
+    while len(fields) < 3:
+        m = _FIELD.match(data, pos)
+        tok, pos = m.group(1), m.end()
+        if not tok:
+            raise PgmError("truncated PGM header")
         if not tok.isdigit():
             raise PgmError(f"malformed PGM header field {tok!r}")
         fields.append(int(tok))
     width, height, maxval = fields
-    if width <= 0 or height <= 0:
+    if min(width, height) <= 0:
         raise PgmError(f"bad PGM dimensions {width}x{height}")
     if maxval > MAX_LEVEL:
         raise PgmError(f"maxval {maxval} above 255 is not supported")
     if maxval <= 0:
         raise PgmError(f"bad PGM maxval {maxval}")
-    pos += 1  # single whitespace byte after maxval
-    raster = data[pos:pos + width * height]
-    if len(raster) < width * height:
+    body = memoryview(data)[pos + 1:]
+    need = width * height
+    if len(body) < need:
         raise PgmError("truncated PGM raster")
-    return np.frombuffer(raster, dtype=np.uint8).reshape(height, width).copy()
+    return np.array(body[:need], dtype=np.uint8).reshape(height, width)
 
 
 def _write_atomic(path: PathLike, parts, mode: str = "wb", suffix: str = ".tmp") -> None:

@@ -1,6 +1,6 @@
 """Summarise an ncu --csv launch list (gpu__time_duration / dram bytes) per kernel.
 
-usage: python tools_launches.py launches.csv [runs] [--k3 CONFIG_NAME]
+usage: python tools/launches.py launches.csv [runs] [--k3 CONFIG_NAME]
 Times are converted to microseconds and bytes to GB regardless of the unit ncu
 printed; `runs` divides the totals into per-run figures.  With --k3 the DRAM
 bytes per run of the K3 kernels (stage1_kernel + ring_kernel) are recorded in

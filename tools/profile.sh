@@ -1,5 +1,5 @@
 #!/bin/bash
-# Usage (on the GPU box): bash scripts_profile.sh <tag> [kernel-regex] [skip] [count]
+# Usage (on the GPU box): bash tools/profile.sh <tag> [kernel-regex] [skip] [count]
 # 1) plain bench run (must exit 0), 2) ncu launch list, 3) ncu --set full on the chosen kernel.
 set -u
 TAG=${1:-r1}
