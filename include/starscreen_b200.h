@@ -235,6 +235,17 @@ int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t 
                      int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
                      size_t workspace_bytes, void* stream);
 /*
+ * K5 over a window of `rows` mask rows (per size, same layout) whose row 0 is
+ * global row y0 of an H-row image: interior status (which survivors count,
+ * screening.py:316-330) is decided in global rows, footprints are clipped to
+ * the window.  A row band plus its neighbours' halo rows (hi_max above,
+ * lo_max below) yields the band's region rows exactly (sharding.py).
+ * Workspace: ss_region_ladder_workspace_bytes(W, rows, n_sizes).
+ */
+int ss_region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
+                          int64_t rows, int64_t y0, int64_t H, int32_t n_sizes, const int32_t* h_m, int32_t stride,
+                          uint32_t* d_region, void* d_workspace, size_t workspace_bytes, void* stream);
+/*
  * f4 (cli.py:97-98 _mask_to_pgm): a bit-packed W x H mask (size mask or
  * region) as one byte per pixel, 255 = kept, 0 = not -- the raster of the
  * PGM files `starscreen screen --out-mask / --out-size-masks` writes

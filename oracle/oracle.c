@@ -188,10 +188,22 @@ static int or_member(const int64_t* keys, int64_t nkeys, int64_t key) {
     return keys[lo] == key;
 }
 
+/* SURVEY.md 8(d) parity protocol: t = f/q + 1/2 lies within the 1e-6
+ * relative band of a quantisation boundary, |t - round(t)| <= 1e-6 max(|t|, 1)
+ * (exact boundaries included).  Only the checker uses this; it does not
+ * change any decision. */
+static inline int or_in_band(double f, double q) {
+    const double t = f / q + 0.5;
+    const double at = fabs(t);
+    return fabs(t - nearbyint(t)) <= 1e-6 * (at > 1.0 ? at : 1.0);
+}
+
 /*
  * screening.py:418-471 _scan_size over one ladder size.
  *   mask: H*W bytes, set to 1 for kept grid centers (border keeps included)
  *   kept_xy: capacity 2*cap int32 (cx,cy) pairs, row-major order
+ *   band: optional H*W bytes, 1 at interior centres that are band positions
+ *         (or_in_band), else 0
  * Returns the number of evaluated survivors (or -1 if cap too small,
  * -2 on a pack-capacity error, the reference's ValueError).
  * *tested receives ix.size * iy.size.
@@ -200,13 +212,14 @@ int64_t or_scan_size(const int64_t* const* sats, const int64_t* const* rsats, in
                      int64_t m, int64_t stride, int64_t n_rings, const int32_t* ring_n,
                      const int32_t* ring_d, const int64_t* keys, const int64_t* key_off,
                      double qm, double qs, double qg, uint8_t* mask, int32_t* kept_xy,
-                     int64_t cap, int64_t* tested, int nthreads) {
+                     int64_t cap, int64_t* tested, int nthreads, uint8_t* band) {
     or_tables t;
     for (int k = 0; k < 4; ++k) { t.sat[k] = sats[k]; t.rsat[k] = rsats[k]; }
     t.W = W; t.H = H;
     /* features.py:214-217 patch_center_margins */
     const int64_t lo = (m - 1) / 2, hi = m / 2;
     memset(mask, 0, (size_t)W * (size_t)H);
+    if (band) memset(band, 0, (size_t)W * (size_t)H);
     int64_t nix = 0, niy = 0;
     for (int64_t y = 0; y < H; y += stride) {
         const int in_y = (y >= lo) && (y <= H - 1 - hi);
@@ -233,6 +246,9 @@ int64_t or_scan_size(const int64_t* const* sats, const int64_t* const* rsats, in
             for (int64_t r = 0; r < n_rings && ok; ++r) {
                 double f[3];
                 or_octagon(&t, x, y, ring_n[r], ring_d[r], f);
+                /* band positions: any channel of any ring the reference evaluates here */
+                if (band && (or_in_band(f[0], qm) || or_in_band(f[1], qs) || or_in_band(f[2], qg)))
+                    band[y * W + x] = 1;
                 const int64_t key = or_pack(or_quantize(f[0], qm), or_quantize(f[1], qs), or_quantize(f[2], qg));
                 if (key < 0) { err = 1; ok = 0; break; }
                 ok = or_member(keys + key_off[r], key_off[r + 1] - key_off[r], key);

@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
                                                                     long long size_stride, int W, int H,
                                                                     long long words, long long P,
                                                                     const Ladder lad, unsigned* Hb,
-                                                                    unsigned* region, long long region_pitch) {
+                                                                    unsigned* region, long long region_pitch,
+                                                                    int y0, int Hg) {
     extern __shared__ unsigned rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long task = (long long)blockIdx.x * RP_WARPS + warp;
@@ -347,7 +348,8 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
     const long long ext = words + P;
     unsigned* A = rsm + (size_t)warp * 2 * ext;
     unsigned* B = A + ext;
-    const bool live = m >= 8 && y >= lo && y <= H - 1 - hi;
+    const int gy = y0 + y;  // global row: interior status is decided in image coordinates
+    const bool live = m >= 8 && gy >= lo && gy <= Hg - 1 - hi;
     unsigned any = 0;
     for (long long i = lane; i < ext; i += 32) {
         const long long wi = i - P;
@@ -564,11 +566,16 @@ size_t region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t L) {
     return (size_t)std::max<int32_t>(L, 1) * H * ((W + 31) / 32) * 4;
 }
 
-int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H, int32_t L,
-                  const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
+// K5 over a window of H mask rows whose row 0 is global row y0 of an Hg-row
+// image (a row band plus the neighbours' halo rows, sharding.py): interior
+// status in global rows; footprints clipped to the window, which holds every
+// survivor that covers the rows the caller keeps.
+int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H,
+                       int64_t y0, int64_t Hg, int32_t L, const int32_t* h_m, int32_t stride, uint32_t* d_region,
+                       void* d_ws, size_t ws_bytes, void* stream) {
     Ladder lad;
     if (int e = fill_ladder(lad, L, h_m)) return e;
-    if (W < 1 || H < 1 || stride < 1) { set_error("bad region arguments"); return SS_EINVAL; }
+    if (W < 1 || H < 1 || stride < 1 || y0 < 0 || y0 + H > Hg) { set_error("bad region arguments"); return SS_EINVAL; }
     if (ws_bytes < region_ladder_workspace_bytes(W, H, L) || !d_ws) {
         set_error("region workspace too small");
         return SS_EINVAL;
@@ -589,7 +596,8 @@ int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stri
         }
         const long long tasks = (long long)L * H;
         region_rows_kernel<<<(unsigned)((tasks + RP_WARPS - 1) / RP_WARPS), RP_WARPS * 32, smem, s>>>(
-            d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb, d_region, mask_pitch);
+            d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb, d_region, mask_pitch, (int)y0,
+            (int)Hg);
         note_launch();
         if (int e = check_launch("region_rows_kernel")) return e;
     }
@@ -605,6 +613,12 @@ int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stri
         region_cols_kernel<16><<<grid, 128, 0, s>>>(Hb, (int)H, words, chunks, lad, d_region, mask_pitch);
     note_launch();
     return check_launch("region_cols_kernel");
+}
+
+int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H, int32_t L,
+                  const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
+    return region_ladder_rows(d_masks, mask_pitch, size_stride, W, H, 0, H, L, h_m, stride, d_region, d_ws, ws_bytes,
+                              stream);
 }
 
 int bits_to_bytes(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, uint8_t* d_out, void* stream) {
@@ -668,6 +682,12 @@ int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t 
                      size_t workspace_bytes, void* stream) {
     return ss::region_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, n_sizes, h_m, stride, d_region,
                              d_workspace, workspace_bytes, stream);
+}
+int ss_region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
+                          int64_t rows, int64_t y0, int64_t H, int32_t n_sizes, const int32_t* h_m, int32_t stride,
+                          uint32_t* d_region, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::region_ladder_rows(d_masks, mask_pitch_words, size_stride_words, W, rows, y0, H, n_sizes, h_m, stride,
+                                  d_region, d_workspace, workspace_bytes, stream);
 }
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, unsigned long long* d_count,
                 void* stream) {

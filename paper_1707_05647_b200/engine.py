@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -57,8 +58,8 @@ def _p(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
-def _stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 @dataclass
@@ -300,6 +301,8 @@ class Engine:
         self.stage_counts = None  # set to a (4,) int64 device tensor to instrument the cascade
         self.force_int64 = False  # test hook: screen every size from the int64 planes
         self.hooks = None  # optional (before, after) callables(main_stream) around the K3 region
+        # one screen at a time per engine: its tables, masks and result buffers are shared state
+        self.lock = threading.RLock()
 
     # ── buffers ────────────────────────────────────────────────────────────
     def _ensure(self, n_sizes: int, max_m: int, capacity: int, region: bool) -> None:
@@ -359,6 +362,10 @@ class Engine:
     def build_tables(self, img: torch.Tensor, int64: bool = False) -> None:
         """K1/K2 on the current stream.  img: (rows, W) uint8 on the device.
         Writes the 32-bit planes, and the int64 planes too when `int64`."""
+        with torch.cuda.device(self.device):
+            self._build_tables(img, int64)
+
+    def _build_tables(self, img: torch.Tensor, int64: bool) -> None:
         assert img.dtype == torch.uint8 and img.is_cuda and img.shape == (self.rows, self.W)
         img = img.contiguous()
         if int64 and self.planes is None:
@@ -367,7 +374,7 @@ class Engine:
         _native.check(self.L.ss_build_tables2(img.data_ptr(), self.W, self.rows, self.W,
                                               _p(self.planes) if int64 else None, self.planes32.data_ptr(),
                                               self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
-                                              _stream_handle()), "build_tables")
+                                              _stream_handle(self.device)), "build_tables")
 
     def screen_ladder(self, tp: TemplatePlan, main: Optional[torch.cuda.Stream] = None) -> None:
         """K3 for every ladder size in one ss_screen_ladder call (sizes spread
@@ -418,7 +425,7 @@ class Engine:
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, self.y_begin, self.y_end,
             len(ms), ms.ctypes.data, tp.config.stride, self.row_counts.data_ptr(), self.xy.data_ptr(), 3, self.capacity,
             self.totals.data_ptr(), self.size_counts.data_ptr(), self.compact_ws.data_ptr(), self.compact_ws.numel(),
-            _stream_handle()), "compact")
+            _stream_handle(self.device)), "compact")
 
     def region_all(self, tp: TemplatePlan) -> None:
         """K5 for every size in one pass, then the region popcount."""
@@ -426,18 +433,24 @@ class Engine:
         _native.check(self.L.ss_region_ladder(
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, len(ms), ms.ctypes.data,
             tp.config.stride, self.region.data_ptr(), self.region_ws.data_ptr(), self.region_ws.numel(),
-            _stream_handle()), "region")
+            _stream_handle(self.device)), "region")
         _native.check(self.L.ss_popcount(self.region.data_ptr(), self.words, self.W, self.H,
-                                         self.totals[1:].data_ptr(), _stream_handle()), "popcount")
+                                         self.totals[1:].data_ptr(), _stream_handle(self.device)), "popcount")
 
     def run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool = True, region: bool = True,
             capacity: Optional[int] = None) -> None:
-        """Enqueue the whole screen of one image (no host sync)."""
+        """Enqueue the whole screen of one image (no host sync) on this
+        engine's device (its current stream)."""
+        with torch.cuda.device(self.device):
+            self._run(img, tp, build=build, region=region, capacity=capacity)
+
+    def _run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool, region: bool,
+             capacity: Optional[int]) -> None:
         full = (self.y_begin, self.y_end, self.y_origin, self.rows) == (0, self.H, 0, self.H)
         region = region and full
         self._ensure(len(tp.sizes), tp.max_m, capacity or self.default_capacity(tp), region)
         if build:
-            self.build_tables(img, int64=self.needs_int64(tp))
+            self._build_tables(img, self.needs_int64(tp))
         main = torch.cuda.current_stream(self.device)
         if self.readback_done is not None:  # the previous run's rows must have left before K4 rewrites them
             main.wait_event(self.readback_done)
@@ -486,9 +499,10 @@ class Engine:
 
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:
         """Grow the survivor buffer and redo K4 only (after an overflow)."""
-        self.capacity = capacity
-        self.xy = torch.empty((capacity, 3), dtype=torch.int32, device=self.device)
-        self.compact_all(tp)
+        with torch.cuda.device(self.device):
+            self.capacity = capacity
+            self.xy = torch.empty((capacity, 3), dtype=torch.int32, device=self.device)
+            self.compact_all(tp)
 
 
 class EnginePool:
@@ -505,12 +519,17 @@ class EnginePool:
             raise ValueError("an engine pool needs at least one engine")
         self.engines = [Engine(width, height, device) for _ in range(n)]
         self.device = self.engines[0].device
+        self.lock = threading.RLock()  # one batch at a time per pool
         self.streams = [torch.cuda.Stream(self.device) for _ in range(n)]
 
     def __len__(self) -> int:
         return len(self.engines)
 
     def run(self, imgs: Sequence[torch.Tensor], tps: Sequence[TemplatePlan], **kw) -> None:
+        with torch.cuda.device(self.device):
+            self._run(imgs, tps, **kw)
+
+    def _run(self, imgs: Sequence[torch.Tensor], tps: Sequence[TemplatePlan], **kw) -> None:
         main = torch.cuda.current_stream(self.device)
         fork = torch.cuda.Event()
         fork.record(main)

@@ -125,6 +125,16 @@ class SizeMasks(Mapping):
         self._host: Dict[int, np.ndarray] = {}
         self._cache: Dict[int, np.ndarray] = {}
 
+    def packed_all(self) -> np.ndarray:
+        """(L, H, ceil(W/32)) uint32: every size's bit-packed rows in ladder
+        order, copied to the host in one transfer."""
+        if len(self._host) < len(self._ladder):
+            allw = _host_words(self._packed)
+            for k, m in enumerate(self._ladder):
+                self._host[m] = allw[k]
+            return allw
+        return np.stack([self._host[m] for m in self._ladder])
+
     def packed(self, m: int) -> np.ndarray:
         if m not in self._host:
             k = self._ladder.index(m)
@@ -146,6 +156,15 @@ class SizeMasks(Mapping):
 
     def __len__(self) -> int:
         return len(self._ladder)
+
+
+class BandSizeMasks(SizeMasks):
+    """SizeMasks of a row-band sharded screen (sharding.py): each rank holds
+    the rows [y_begin, y_end) it decided; .packed(m) / [m] are those rows."""
+
+    def __init__(self, ladder: Tuple[int, ...], packed, width: int, rows: Tuple[int, int]):
+        super().__init__(ladder, packed, width)
+        self.rows = (int(rows[0]), int(rows[1]))
 
 
 class CandidateList(Sequence):
@@ -225,8 +244,10 @@ class ScreeningResult:
     """screening.py:276-298: everything the second stage needs from the screen."""
 
     def __init__(self, width, height, template_side, config, ladder, candidates, size_masks, region_packed, stats,
-                 size_counts=None):
+                 size_counts=None, region_rows=None):
         self._size_counts = None if size_counts is None else [int(c) for c in size_counts]
+        # row-band sharded results hold the region rows [y0, y1) of their band only
+        self.region_rows = (0, height) if region_rows is None else (int(region_rows[0]), int(region_rows[1]))
         self.width = width
         self.height = height
         self.template_side = template_side
@@ -241,7 +262,7 @@ class ScreeningResult:
     def region_packed(self) -> np.ndarray:
         """Bit-packed region rows (H, ceil(W/32)) uint32."""
         if self._region_packed is None:
-            return np.zeros((self.height, (self.width + 31) // 32), np.uint32)
+            return np.zeros((self.region_rows[1] - self.region_rows[0], (self.width + 31) // 32), np.uint32)
         if isinstance(self._region_packed, torch.Tensor):
             self._region_packed = _host_words(self._region_packed)
         return self._region_packed
@@ -265,7 +286,7 @@ class ScreeningResult:
 
         src = self._region_packed
         if src is None:
-            return np.zeros((self.height, self.width), np.uint8)
+            return np.zeros((self.region_rows[1] - self.region_rows[0], self.width), np.uint8)
         return packed_to_pgm(src, self.width)
 
     def size_mask_pgm(self, m: int) -> np.ndarray:
@@ -331,6 +352,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> 
     (private copies, the engine's buffers are reused) until first accessed;
     `readback` (Engine.start_readback) carries the survivor rows' host copy
     that started right after compaction."""
+    cur = torch.cuda.current_stream(eng.device)
     totals = eng.totals.cpu()  # synchronises the stream
     kept = int(totals[0])
     if kept > eng.capacity:
@@ -341,6 +363,12 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> 
     rows = eng.xy[:kept].clone()
     packed = eng.masks[: len(tp.sizes)].clone()
     region = eng.region.clone() if eng.region is not None else None
+    # the copies are ordered on this stream; a caller reading them on another
+    # stream must wait for it (screen_batch), and their memory must not be
+    # reused before those streams are done with it
+    for t in (rows, packed, region):
+        if t is not None:
+            t.record_stream(cur)
     elapsed = time.perf_counter() - start
     W, H = eng.W, eng.H
     stats = PruneStats(
@@ -370,15 +398,17 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     eng = get_engine(w, h, device)
     # The template's f2 features start first (engine's template stream), the
     # image side (upload + K1/K2 on the current stream) overlaps them, then
-    # the host builds the key sets.
-    tp = plan_ladder(tpl.shape[1], cfg)
-    pending = launch_features(tp, tpl, eng.device, eng.template_stream)
-    img_dev = upload_image(img, eng.device)
-    eng.build_tables(img_dev, int64=eng.needs_int64(tp))
-    fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
-    eng.run(img_dev, tp, build=False)
-    readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
-    return fetch_result(eng, tp, start, readback)
+    # the host builds the key sets.  The engine is held for the whole call
+    # (concurrent screen() calls of one shape take turns).
+    with eng.lock, torch.cuda.device(eng.device):
+        tp = plan_ladder(tpl.shape[1], cfg)
+        pending = launch_features(tp, tpl, eng.device, eng.template_stream)
+        img_dev = upload_image(img, eng.device)
+        eng.build_tables(img_dev, int64=eng.needs_int64(tp))
+        fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
+        eng.run(img_dev, tp, build=False)
+        readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
+        return fetch_result(eng, tp, start, readback)
 
 
 _pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
@@ -418,9 +448,16 @@ def screen_batch(images: Sequence[np.ndarray], templates: Sequence[np.ndarray],
     if any(img.shape != (h, w) for img, _ in checked):
         raise ValueError("screen_batch needs images of one shape")
     pool = get_pool(w, h, device, max(1, min(engines, len(images))))
+    with pool.lock, torch.cuda.device(pool.device):
+        return _screen_batch(pool, checked, cfg)
+
+
+def _screen_batch(pool: EnginePool, checked, cfg: ScreeningConfig) -> List[ScreeningResult]:
     n = len(pool)
-    results: List[Optional[ScreeningResult]] = [None] * len(images)
+    results: List[Optional[ScreeningResult]] = [None] * len(checked)
     pending: List[Optional[Tuple[int, TemplatePlan, float]]] = [None] * n
+
+    caller = torch.cuda.current_stream(pool.device)
 
     def collect(j: int) -> None:
         if pending[j] is None:
@@ -428,6 +465,9 @@ def screen_batch(images: Sequence[np.ndarray], templates: Sequence[np.ndarray],
         i, tp, start = pending[j]
         with torch.cuda.stream(pool.streams[j]):
             results[i] = fetch_result(pool.engines[j], tp, start)
+        # the result's device copies were made on stream j: the caller's stream
+        # (which reads them) waits for them
+        caller.wait_stream(pool.streams[j])
         pending[j] = None
 
     for i, (img, tpl) in enumerate(checked):

@@ -109,6 +109,11 @@ def match_candidates(image: np.ndarray, template: np.ndarray, screened, angle_st
     if not torch.cuda.is_available():
         raise RuntimeError("match_candidates needs a CUDA device (no CPU fallback)")
     dev = torch.device(device if device is not None else "cuda")
+    with torch.cuda.device(dev):  # launches go to `dev`'s streams whatever device is current
+        return _match(img, tpl, screened, angles, dev)
+
+
+def _match(img, tpl, screened, angles, dev) -> MatchResult:
     n = tpl.shape[0]
     na = len(angles)
     stream = torch.cuda.current_stream(dev)

@@ -1,30 +1,42 @@
-"""Multi-GPU screening: row bands of one image, or images of a batch.
+"""Multi-GPU screening: row bands of one image (configs 2 and 4).
 
-SURVEY.md 8(e): the work shards with no exchange before the final gather.
+SURVEY.md 8(e): the work shards with no exchange inside the hot path.
 
-* Row bands (configs 2 and 4): rank r decides rows [y_begin, y_end) and
-  builds its tables over the halo'd band [y_begin - lo_max, y_end + hi_max)
-  (lo_max / hi_max = the largest ladder size's centre margins,
-  features.py:214-217).  Tables are local to the band -- no prefix carry
-  crosses GPUs, because only region differences are used and the weighted
-  numerators are frame-invariant -- and border status
-  is decided in global coordinates (ss_screen_size's y_origin / y_begin /
-  y_end).  Duplicated work is only the halo part of the table build.
-* Images of a batch (config 3): image i goes to rank i % world.
+* Rank r decides rows [y_begin, y_end) and builds its tables over the halo'd
+  band [y_begin - lo_max, y_end + hi_max) (lo_max / hi_max = the largest
+  ladder size's centre margins, features.py:214-217).  Tables are local to
+  the band -- no prefix carry crosses GPUs, because only region differences
+  are used and the weighted numerators are frame-invariant (SURVEY.md
+  App. B.1) -- and border status is decided in global coordinates
+  (y_origin / y_begin / y_end of ss_screen_ladder).  Duplicated work is the
+  halo part of the table build only.
+* Kept region (screening.py:316-330): a region row p is covered by survivors
+  in rows [p - hi_max, p + lo_max], so a band's region rows need hi_max mask
+  rows of the band above and lo_max of the band below.  They come from a
+  neighbour halo exchange (NCCL send / recv, every size's rows, ~17 MB per
+  neighbour at config 4), and K5 runs over the band plus halo in global
+  coordinates (ss_region_ladder_rows).  The full masks are never gathered.
+* The only other collective is the final gather: an all-gather of per-size
+  survivor counts (+ the band's kept-region pixels) and of the compacted
+  (cx, cy, m) survivor rows, padded to a fixed row capacity, so the step has
+  no host synchronisation (NCCL has no gather primitive).  The rows are then
+  placed in ladder order, rank order within a size (= global row-major
+  order) on the device (``assemble_rows``): the gathered list equals the
+  single-GPU one.
 
-The only collective is the final gather: an all-gather of per-size survivor
-counts, then of the compacted (cx, cy) lists and packed mask rows, padded to
-the largest rank (NCCL has no gather primitive).  Concatenating bands in rank
-order keeps global row-major order, so the gathered candidate list equals the
-single-GPU one.  The kept region is computed after the gather from the full
-survivor masks (it needs neighbour bands' survivors within the margins).
+Bytes over NVLink at config 4, N = 8 (measured survivor count 22.45 M):
+counts 8 x 34 x 8 B; rows 8 x ~2.8 M x 12 B ~ 270 MB received per rank with
+the capacity at the largest band's count + 25%; halo 2 x 33 x 256 x 512 x 4 B
+~ 34 MB per rank.
 
-Host-side planning and assembly are plain functions so they can be tested
-with the gloo backend on CPU (tests/test_sharding_cpu.py).
+The collective and host logic is plain torch, so the gloo tests on CPU
+exercise it with oracle stand-ins for the band screen and the region
+(tests/test_sharding_cpu.py).
 """
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence, Tuple
 
@@ -53,27 +65,29 @@ def ladder_margins(ladder: Sequence[int]) -> Tuple[int, int]:
 
 
 def plan_bands(height: int, world: int, ladder: Sequence[int]) -> List[Band]:
-    """Balanced row bands with the halo the largest ladder size needs."""
+    """Balanced row bands with the halo the largest ladder size needs.
+    Raises ValueError when a band would be thinner than the halo (its
+    neighbours' region rows would need rows of bands further away)."""
     lo, hi = ladder_margins(ladder)
     out = []
     for r in range(world):
         yb = r * height // world
         ye = (r + 1) * height // world
+        if world > 1 and ye - yb < max(lo, hi):
+            raise ValueError(f"{world} row bands of a {height}-row image are thinner than the halo ({max(lo, hi)})")
         y0 = max(0, yb - lo)
         y1 = min(height, ye + hi)
         out.append(Band(r, yb, ye, y0, max(y1 - y0, 1)))
     return out
 
 
-@dataclass
-class BandResult:
-    """One rank's share: survivors in global coordinates, packed mask rows."""
-
-    band: Band
-    counts: "torch.Tensor"  # (L,) int64 survivors per ladder size
-    rows: "torch.Tensor"  # (k, 3) int32 (cx, cy, m), ladder order then row-major
-    masks: "torch.Tensor"  # (L, y_end - y_begin, words) int32 (bit-packed rows)
-    tested: int
+def halo_counts(bands: Sequence[Band], r: int, height: int, ladder: Sequence[int]) -> Tuple[int, int]:
+    """(rows above, rows below) of mask halo band r needs for its region rows."""
+    lo, hi = ladder_margins(ladder)
+    b = bands[r]
+    top = b.y_begin - max(0, b.y_begin - hi) if r > 0 else 0
+    bot = min(height, b.y_end + lo) - b.y_end if r + 1 < len(bands) else 0
+    return top, bot
 
 
 def _coll_device(group=None) -> torch.device:
@@ -81,67 +95,67 @@ def _coll_device(group=None) -> torch.device:
     return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
 
 
-def _all_gather_padded(t: torch.Tensor, group=None) -> List[torch.Tensor]:
-    """All-gather tensors whose first dimension differs per rank."""
-    dev = _coll_device(group)
+def _peer(group, r: int) -> int:
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+def exchange_halo(masks: torch.Tensor, bands: Sequence[Band], height: int, ladder: Sequence[int],
+                  group=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Neighbour exchange of packed mask rows (every size): returns (rows from
+    the band above, rows from the band below), each (L, k, words)."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    L, _, words = masks.shape
+    top_n, bot_n = halo_counts(bands, rank, height, ladder)
+    top = torch.empty((L, top_n, words), dtype=masks.dtype, device=masks.device)
+    bot = torch.empty((L, bot_n, words), dtype=masks.dtype, device=masks.device)
+    ops = []
+    if rank > 0:
+        send_n = halo_counts(bands, rank - 1, height, ladder)[1]  # the band above needs my first rows
+        ops.append(dist.P2POp(dist.isend, masks[:, :send_n].contiguous(), _peer(group, rank - 1), group))
+        ops.append(dist.P2POp(dist.irecv, top, _peer(group, rank - 1), group))
+    if rank + 1 < world:
+        send_n = halo_counts(bands, rank + 1, height, ladder)[0]  # the band below needs my last rows
+        ops.append(dist.P2POp(dist.isend, masks[:, masks.shape[1] - send_n:].contiguous(), _peer(group, rank + 1),
+                              group))
+        ops.append(dist.P2POp(dist.irecv, bot, _peer(group, rank + 1), group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return top, bot
+
+
+def all_gather_stacked(t: torch.Tensor, group=None) -> torch.Tensor:
+    """(world, *t.shape): every rank's equally shaped tensor, rank order."""
     world = dist.get_world_size(group)
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    ns = [int(v.item()) for v in ns]
-    mx = max(ns) if ns else 0
-    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-    pad[: t.shape[0]] = t.to(dev)
-    outs = [torch.zeros_like(pad) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    return [o[:k] for o, k in zip(outs, ns)]
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t.contiguous(), group=group)
+    return torch.stack(outs)
 
 
-def gather_band_results(local: BandResult, group=None) -> List[BandResult]:
-    """All ranks' BandResults, in rank order (every rank receives all); the
-    tensors stay on the collective's device (NCCL: the GPU)."""
-    world = dist.get_world_size(group)
-    dev = _coll_device(group)
-    counts = torch.as_tensor(local.counts, dtype=torch.int64).to(dev)
-    allc = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(allc, counts, group=group)
-    rows = _all_gather_padded(torch.as_tensor(local.rows, dtype=torch.int32).reshape(-1, 3), group)
-    m = torch.as_tensor(local.masks).view(torch.int32)
-    ms = _all_gather_padded(m.permute(1, 0, 2).contiguous(), group)  # rows first
-    tested = torch.tensor([local.tested], dtype=torch.int64, device=dev)
-    allt = [torch.zeros_like(tested) for _ in range(world)]
-    dist.all_gather(allt, tested, group=group)
-    bands = plan_bands_from(local.band, world, group)
-    return [BandResult(bands[r], allc[r], rows[r], ms[r].permute(1, 0, 2), int(allt[r].item())) for r in range(world)]
-
-
-def plan_bands_from(band: Band, world: int, group=None) -> List[Band]:
-    dev = _coll_device(group)
-    t = torch.tensor([band.rank, band.y_begin, band.y_end, band.y_origin, band.rows], dtype=torch.int64, device=dev)
-    allb = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(allb, t, group=group)
-    return [Band(*[int(v) for v in b.cpu().tolist()]) for b in allb]
-
-
-def assemble(parts: List[BandResult], width: int, height: int, ladder: Sequence[int]):
-    """Concatenate band results into full-image tensors on the parts' device
-    (ladder order, then row-major): masks (L, H, words) int32, rows (K, 3)
-    int32, counts (L,) int64 (host), tested."""
-    L = len(ladder)
-    words = (width + 31) // 32
-    dev = parts[0].rows.device if parts else torch.device("cpu")
-    masks = torch.zeros((L, height, words), dtype=torch.int32, device=dev)
-    per_size = [[] for _ in range(L)]
-    for p in sorted(parts, key=lambda p: p.band.y_begin):
-        masks[:, p.band.y_begin:p.band.y_end] = p.masks
-        cnts = [int(c) for c in p.counts.tolist()]
-        for k, chunk in enumerate(torch.split(p.rows, cnts)):
-            per_size[k].append(chunk)
-    counts = np.array([sum(int(c.shape[0]) for c in per_size[k]) for k in range(L)], np.int64)
-    empty = torch.zeros((0, 3), dtype=torch.int32, device=dev)
-    rows = torch.cat([torch.cat(per_size[k]) if per_size[k] else empty for k in range(L)]) if L else empty
-    tested = sum(p.tested for p in parts)
-    return masks, rows, counts, tested
+def assemble_rows(rows_g: torch.Tensor, counts_g: torch.Tensor) -> torch.Tensor:
+    """Gathered survivor rows -> the single-GPU candidate order, on the device
+    without a host sync.  rows_g: (world, cap, 3) int32, each rank's rows in
+    ladder order then row-major (its first sum(counts_g[r]) rows valid);
+    counts_g: (world, L) int64.  Returns (world * cap, 3): ladder order, rank
+    order within a size (bands are row-ordered), the total = counts_g.sum()
+    rows first."""
+    world, cap, _ = rows_g.shape
+    dev = rows_g.device
+    cum = counts_g.cumsum(1)  # (world, L) end of size k in rank r's rows
+    start = cum - counts_g
+    tot_k = counts_g.sum(0)
+    base_k = tot_k.cumsum(0) - tot_k  # start of size k in the output
+    rank_off = counts_g.cumsum(0) - counts_g  # rank r's offset inside size k
+    i = torch.arange(cap, device=dev, dtype=torch.int64).expand(world, cap).contiguous()
+    k = torch.searchsorted(cum, i, right=True)  # size of row i of rank r (L: past the valid rows)
+    L = counts_g.shape[1]
+    valid = k < L
+    kk = k.clamp(max=max(L - 1, 0))
+    dest = (base_k[kk] + rank_off.gather(1, kk) + i - start.gather(1, kk))
+    dest = torch.where(valid, dest, torch.full_like(dest, world * cap))  # invalid rows -> a spare slot
+    out = torch.zeros((world * cap + 1, 3), dtype=rows_g.dtype, device=dev)
+    out.index_copy_(0, dest.reshape(-1), rows_g.reshape(-1, 3))
+    return out[: world * cap]
 
 
 _band_engines: dict = {}
@@ -161,72 +175,198 @@ def band_engine(W: int, H: int, band: Band, device):
     return eng
 
 
-def screen_band_device(image: np.ndarray, tp, band: Band, device) -> BandResult:
-    """This rank's band on its GPU (libstarscreen through engine.Engine)."""
-    H, W = image.shape
-    eng = band_engine(W, H, band, device)
-    sub = torch.from_numpy(np.ascontiguousarray(image[band.y_origin:band.y_origin + band.rows])).to(eng.device)
-    eng.run(sub, tp, region=False)
-    totals = eng.totals.cpu()
-    kept = int(totals[0])
-    if kept > eng.capacity:
-        eng.recompact(tp, kept)
-    counts = eng.size_counts[: len(tp.sizes)].clone()
-    rows = eng.xy[:kept].clone()  # (cx, cy, m) on the device
-    masks = eng.masks[: len(tp.sizes)].clone()
-    return BandResult(band, counts, rows, masks, eng.tested(tp))
-
-
-def region_from_masks(masks, width: int, height: int, ladder: Sequence[int], stride: int, device):
-    """Kept region (K5, ladder form) on the device from the gathered full
-    survivor masks ((L, H, words) int32 tensor); returns (packed region
-    tensor on the device, kept pixels)."""
+def region_rows_device(stack: torch.Tensor, W: int, y0: int, H: int, ladder: Sequence[int], stride: int,
+                       ws: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """K5 over a window of mask rows (global row y0 first) on the device:
+    packed region rows (rows, words) int32 (ss_region_ladder_rows)."""
     from . import _native
 
     L = _native.lib()
-    dev = torch.device(device)
-    words = (width + 31) // 32
-    mk = torch.as_tensor(masks).to(dev).view(torch.int32).contiguous()
+    Ls, rows, words = stack.shape
     ms = np.asarray(ladder, np.int32)
-    region = torch.empty((height, words), dtype=torch.int32, device=dev)
-    ws = torch.empty(int(L.ss_region_ladder_workspace_bytes(width, height, len(ms))), dtype=torch.uint8, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    s = torch.cuda.current_stream(dev).cuda_stream
-    _native.check(L.ss_region_ladder(mk.data_ptr(), words, height * words, width, height, len(ms), ms.ctypes.data,
-                                     stride, region.data_ptr(), ws.data_ptr(), ws.numel(), s), "region")
-    _native.check(L.ss_popcount(region.data_ptr(), words, width, height, cnt.data_ptr(), s), "popcount")
-    return region, int(cnt.item())
+    need = int(L.ss_region_ladder_workspace_bytes(W, rows, Ls))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=stack.device)
+    region = torch.empty((rows, words), dtype=torch.int32, device=stack.device)
+    s = torch.cuda.current_stream(stack.device).cuda_stream
+    _native.check(L.ss_region_ladder_rows(stack.data_ptr(), words, rows * words, W, rows, y0, H, Ls, ms.ctypes.data,
+                                          stride, region.data_ptr(), ws.data_ptr(), ws.numel(), s), "region")
+    return region
+
+
+def popcount_device(region: torch.Tensor, W: int, out: torch.Tensor) -> None:
+    """out[0] = set bits of the packed (rows, words) region (ss_popcount)."""
+    from . import _native
+
+    rows, words = region.shape
+    s = torch.cuda.current_stream(region.device).cuda_stream
+    _native.check(_native.lib().ss_popcount(region.data_ptr(), words, W, rows, out.data_ptr(), s), "popcount")
+
+
+class ShardedScreener:
+    """One rank's share of a row-band sharded screen, enqueued without host
+    synchronisation: band tables + K3 + K4 (engine.Engine with a band frame),
+    the halo exchange, the band's region rows (K5) and popcount, the
+    all-gather of counts and of the survivor rows padded to ``gather_rows``,
+    and the device-side assembly of the gathered rows.  ``result()`` syncs
+    once and builds the ScreeningResult."""
+
+    def __init__(self, width: int, height: int, tp, device=None, group=None):
+        self.W, self.H = int(width), int(height)
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.ladder = tuple(tp.ladder)
+        self.bands = plan_bands(self.H, self.world, self.ladder)
+        self.band = self.bands[self.rank]
+        self.top, self.bot = halo_counts(self.bands, self.rank, self.H, self.ladder)
+        self.engine = band_engine(self.W, self.H, self.band, self.device)
+        self.gather_rows = 1 << 16
+        self.region_ws = None
+        self.px = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.counts_g = self.rows_g = self.rows_out = self.region = None
+
+    def upload_band(self, image: np.ndarray) -> torch.Tensor:
+        b = self.band
+        return torch.from_numpy(np.ascontiguousarray(image[b.y_origin:b.y_origin + b.rows])).to(self.device)
+
+    def set_capacity(self, rows: int) -> None:
+        """Survivor rows per rank: the engine's compaction capacity and the
+        padded row count of the all-gather."""
+        self.gather_rows = max(int(rows), 1)
+
+    def step(self, img: torch.Tensor, tp, capacity: Optional[int] = None) -> None:
+        eng = self.engine
+        L = len(tp.sizes)
+        with torch.cuda.device(self.device):
+            eng.run(img, tp, region=False, capacity=max(capacity or 0, self.gather_rows))
+            masks = eng.masks[:L]
+            top, bot = exchange_halo(masks, self.bands, self.H, self.ladder, self.group)
+            stack = torch.cat([top, masks, bot], 1) if (self.top or self.bot) else masks
+            if self.region_ws is None:
+                rws = int(eng.L.ss_region_ladder_workspace_bytes(self.W, stack.shape[1], L))
+                self.region_ws = torch.empty(rws, dtype=torch.uint8, device=self.device)
+            reg = region_rows_device(stack, self.W, self.band.y_begin - self.top, self.H, self.ladder,
+                                     tp.config.stride, self.region_ws)
+            self.region = reg[self.top: self.top + (self.band.y_end - self.band.y_begin)]
+            popcount_device(self.region, self.W, self.px)
+            local = torch.cat([eng.size_counts[:L], self.px])
+            self.counts_g = all_gather_stacked(local, self.group)  # (world, L + 1)
+            self.rows_g = all_gather_stacked(eng.xy[: self.gather_rows], self.group)
+            self.rows_out = assemble_rows(self.rows_g, self.counts_g[:, :L])
+            self.masks = masks
+
+    def result(self, tp, start: float):
+        """Host sync, overflow handling (every rank sees the same gathered
+        counts, so all re-gather together), ScreeningResult."""
+        from .screening import BandSizeMasks, CandidateList, PruneStats, ScreeningResult
+
+        L = len(tp.sizes)
+        cg = self.counts_g.cpu()
+        per_rank = cg[:, :L].sum(1)
+        need = int(per_rank.max()) if self.world else 0
+        if need > self.gather_rows:  # a rank kept more rows than the gather carried: redo K4 + the row gather
+            eng = self.engine
+            if need > eng.capacity:
+                eng.recompact(tp, need)
+            self.gather_rows = need
+            with torch.cuda.device(self.device):
+                self.rows_g = all_gather_stacked(eng.xy[:need], self.group)
+                self.rows_out = assemble_rows(self.rows_g, self.counts_g[:, :L].to(self.rows_g.device))
+        counts = cg[:, :L].sum(0).numpy().astype(np.int64)
+        total = int(counts.sum())
+        tested = sum(band_tested(self.W, self.H, b, tp) for b in self.bands)
+        stats = PruneStats(tested, total, int(cg[:, L].sum()), self.W * self.H, time.perf_counter() - start)
+        rows = self.rows_out[:total].clone()
+        masks = BandSizeMasks(tp.ladder, self.masks.clone(), self.W, (self.band.y_begin, self.band.y_end))
+        return ScreeningResult(self.W, self.H, tp.template_side, tp.config, tp.ladder, CandidateList(rows, total),
+                               masks, self.region.clone(), stats, counts.tolist(),
+                               region_rows=(self.band.y_begin, self.band.y_end))
+
+
+def band_tested(W: int, H: int, band: Band, tp) -> int:
+    """patches_tested of a band's decided rows (screening.py:446, 513)."""
+    from .config import grid_count
+
+    s = tp.config.stride
+    out = 0
+    for m in tp.ladder:
+        if m < MIN_PATCH_SIDE:
+            continue
+        lo, hi = patch_center_margins(m)
+        nx = grid_count(W, lo, hi, s)
+        ylo, yhi = max(band.y_begin, lo), min(band.y_end - 1, H - 1 - hi)
+        if yhi >= ylo:
+            first = ((ylo + s - 1) // s) * s
+            out += nx * (0 if first > yhi else (yhi - first) // s + 1)
+    return out
+
+
+@dataclass
+class BandResult:
+    """A band screen's output (the stand-in interface of the CPU tests):
+    per-size counts (L,) int64, survivor rows (k, 3) int32 in global
+    coordinates (ladder order, row-major), packed mask rows (L, rows, words)."""
+
+    band: Band
+    counts: torch.Tensor
+    rows: torch.Tensor
+    masks: torch.Tensor
 
 
 def screen_sharded(image: np.ndarray, template: np.ndarray, cfg=None, group=None, device=None,
                    band_fn: Optional[Callable] = None, region_fn: Optional[Callable] = None):
-    """Row-band sharded screen() over the ranks of `group`; every rank gets the result.
+    """Row-band sharded screen() over the ranks of `group`.
 
-    band_fn / region_fn default to the GPU implementations (tests substitute a
-    CPU stand-in to exercise the planning, gather and assembly logic on gloo).
+    Every rank receives the whole candidate list and the whole PruneStats;
+    ``size_masks`` and the region hold the rank's own band rows
+    (``result.region_rows``) -- the masks are not gathered.
+
+    band_fn(image, tp, band, device) -> BandResult and region_fn(stack, W, y0,
+    H, ladder, stride) -> packed region rows replace the GPU band screen and
+    K5 (tests run the collective logic on gloo with CPU stand-ins).
     """
-    import time
-
     from .config import ScreeningConfig
     from .engine import prepare_template
-    from .screening import CandidateList, PruneStats, ScreeningResult, SizeMasks, validate
+    from .screening import BandSizeMasks, CandidateList, PruneStats, ScreeningResult, validate
 
     cfg = cfg or ScreeningConfig()
     img, tpl = validate(image, template, cfg)
     H, W = img.shape
     start = time.perf_counter()
+    if band_fn is None:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(dev):
+            tp = prepare_template(tpl, cfg, dev)
+            sh = ShardedScreener(W, H, tp, dev, group)
+            eng = sh.engine
+            sh.set_capacity(max(eng.last_kept or 0, 1 << 16))
+            sh.step(sh.upload_band(img), tp)
+            return sh.result(tp, start)
+    # CPU stand-ins (tests): the same halo / gather / assembly logic
+    tp = prepare_template(tpl, cfg, torch.device("cpu"))
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
-                                             if torch.cuda.is_available() else None)
-    tp = prepare_template(tpl, cfg, dev if band_fn is None else torch.device("cpu"))
-    band = plan_bands(H, world, tp.ladder)[rank]
-    local = (band_fn or screen_band_device)(img, tp, band, dev)
-    parts = gather_band_results(local, group)
-    masks, rows, counts, tested = assemble(parts, W, H, tp.ladder)
-    if region_fn is None:
-        region, kept_px = region_from_masks(masks, W, H, tp.ladder, cfg.stride, dev)
-    else:  # host stand-in (tests)
-        region, kept_px = region_fn(masks.cpu().numpy().view(np.uint32), W, H, tp.ladder, cfg.stride, dev)
-    stats = PruneStats(tested, int(counts.sum()), kept_px, W * H, time.perf_counter() - start)
-    return ScreeningResult(W, H, tp.template_side, cfg, tp.ladder, CandidateList(rows, int(rows.shape[0])),
-                           SizeMasks(tp.ladder, masks, W), region, stats, counts.tolist())
+    bands = plan_bands(H, world, tp.ladder)
+    band = bands[rank]
+    local = band_fn(img, tp, band, device)
+    masks = torch.as_tensor(local.masks).view(torch.int32)
+    top, bot = exchange_halo(masks, bands, H, tp.ladder, group)
+    t_n = top.shape[1]
+    stack = torch.cat([top, masks, bot], 1)
+    reg = torch.as_tensor(region_fn(stack, W, band.y_begin - t_n, H, tp.ladder, cfg.stride)).view(torch.int32)
+    region = reg[t_n: t_n + band.y_end - band.y_begin]
+    px = int(np.unpackbits(region.numpy().view(np.uint8), bitorder="little").sum())
+    L = len(tp.sizes)
+    local_c = torch.cat([torch.as_tensor(local.counts, dtype=torch.int64), torch.tensor([px], dtype=torch.int64)])
+    counts_g = all_gather_stacked(local_c, group)
+    cap = int(all_gather_stacked(torch.tensor([local.rows.shape[0]], dtype=torch.int64), group).max())
+    padded = torch.zeros((max(cap, 1), 3), dtype=torch.int32)
+    padded[: local.rows.shape[0]] = torch.as_tensor(local.rows, dtype=torch.int32).reshape(-1, 3)
+    rows = assemble_rows(all_gather_stacked(padded, group), counts_g[:, :L])
+    counts = counts_g[:, :L].sum(0).numpy().astype(np.int64)
+    total = int(counts.sum())
+    tested = sum(band_tested(W, H, b, tp) for b in bands)
+    stats = PruneStats(tested, total, int(counts_g[:, L].sum()), W * H, time.perf_counter() - start)
+    return ScreeningResult(W, H, tp.template_side, cfg, tp.ladder, CandidateList(rows[:total], total),
+                           BandSizeMasks(tp.ladder, masks, W, (band.y_begin, band.y_end)), region, stats,
+                           counts.tolist(), region_rows=(band.y_begin, band.y_end))

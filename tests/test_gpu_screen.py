@@ -262,26 +262,50 @@ def test_screen_batch_matches_screen(cuda):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_row_bands_on_device_assemble_to_full_screen(cuda, world):
-    """The multi-GPU data path (sharding.py: halo'd row bands, tables local to
-    the band, border status in global rows) run band by band on one GPU:
-    assembled, it equals the single-image screen."""
+    """The multi-GPU data path (sharding.py) run band by band on one GPU: band
+    tables + screens (halo'd bands, border status in global rows), the mask
+    halo rows the neighbour exchange would deliver, K5 over band + halo
+    (ss_region_ladder_rows) and the device assembly of the padded survivor
+    rows equal the single-image screen's masks, region and candidates."""
+    import torch
+
     import workloads as WL
     from paper_1707_05647_b200 import screen
     from paper_1707_05647_b200.engine import prepare_template
-    from paper_1707_05647_b200.sharding import assemble, plan_bands, screen_band_device
+    from paper_1707_05647_b200.screening import unpack_bits
+    from paper_1707_05647_b200.sharding import (assemble_rows, band_engine, halo_counts, plan_bands,
+                                                region_rows_device)
 
     img = WL.make_image(500, 431, seed=71, sigma=2.5, noise=2.0)
     case = WL.make_template(img, 72, 40, (0.8, 1.3), std_threshold=10.0)
     cfg = pcfg({"alpha": 0.5, "beta": 1.8, "ladder_ratio": 1.25, "quantizer": (6.0, 6.0, 6.0)})
     full = screen(img, case.template, cfg)
+    H, W = img.shape
     tp = prepare_template(case.template, cfg, cuda)
-    parts = [screen_band_device(img, tp, b, cuda) for b in plan_bands(img.shape[0], world, tp.ladder)]
-    masks, rows, counts, tested = assemble(parts, img.shape[1], img.shape[0], tp.ladder)
-    assert tested == full.stats.patches_tested
-    assert np.array_equal(rows.cpu().numpy(), full.candidates.array())
-    assert list(counts) == full.candidates_per_size()
-    for k, m in enumerate(full.ladder):
-        assert np.array_equal(masks[k].cpu().numpy().view(np.uint32), full.size_masks.packed(m).view(np.uint32)), m
+    L = len(tp.sizes)
+    bands = plan_bands(H, world, tp.ladder)
+    masks, counts, rows = [], [], []
+    for b in bands:
+        eng = band_engine(W, H, b, cuda)
+        sub = torch.from_numpy(np.ascontiguousarray(img[b.y_origin:b.y_origin + b.rows])).to(cuda)
+        eng.run(sub, tp, region=False, capacity=1 << 16)
+        masks.append(eng.masks[:L].clone())
+        counts.append(eng.size_counts[:L].clone())
+        rows.append(eng.xy[: 1 << 16].clone())
+    for r, b in enumerate(bands):
+        assert np.array_equal(masks[r].cpu().numpy().view(np.uint32),
+                              full.size_masks.packed_all()[:, b.y_begin:b.y_end])
+        top, bot = halo_counts(bands, r, H, tp.ladder)
+        parts = ([masks[r - 1][:, masks[r - 1].shape[1] - top:]] if top else []) + [masks[r]] + \
+                ([masks[r + 1][:, :bot]] if bot else [])
+        stack = torch.cat(parts, 1)
+        reg = region_rows_device(stack, W, b.y_begin - top, H, tp.ladder, cfg.stride)
+        got = unpack_bits(reg[top: top + b.y_end - b.y_begin].cpu().numpy().view(np.uint32), W)
+        assert np.array_equal(got, full.region_mask[b.y_begin:b.y_end]), r
+    out = assemble_rows(torch.stack(rows), torch.stack(counts))
+    n = full.stats.patches_kept
+    assert int(torch.stack(counts).sum()) == n
+    assert np.array_equal(out[:n].cpu().numpy(), full.candidates.array())
 
 
 def _boundary_image(seed):

@@ -3,8 +3,10 @@
 usage: python tools/launches.py launches.csv [runs] [--k3 CONFIG_NAME]
 Times are converted to microseconds and bytes to GB regardless of the unit ncu
 printed; `runs` divides the totals into per-run figures.  With --k3 the DRAM
-bytes per run of the K3 kernels (stage1_kernel + ring_kernel) are recorded in
-profiles/r1/k3_traffic.json under CONFIG_NAME (bench.py's roofline.traffic).
+bytes and warp instructions (smsp__inst_executed.sum) per run of the K3
+kernels (border + stage 1 + rings) are recorded in
+profiles/<round>/k3_traffic.json under CONFIG_NAME (bench.py's roofline
+traffic / dram / issue entries).
 """
 import json
 import os
@@ -24,6 +26,7 @@ def main(path, runs=1):
     t = defaultdict(float)
     b = defaultdict(float)
     n = defaultdict(int)
+    inst = defaultdict(float)
     for r in rows[1:]:
         if len(r) < len(hdr):
             continue
@@ -34,6 +37,8 @@ def main(path, runs=1):
             n[name] += 1
         elif metric.startswith("dram__bytes"):
             b[name] += val * SCALE_B[unit]
+        elif metric == "smsp__inst_executed.sum":
+            inst[name] += val
     tot = sum(t.values())
     print(f"{'kernel':40s} {'launch':>7s} {'ms/run':>9s} {'share':>6s} {'GB/run':>8s} {'GB/s':>7s}")
     for k in sorted(t, key=lambda k: -t[k]):
@@ -41,16 +46,21 @@ def main(path, runs=1):
         gb = b[k] / runs
         print(f"{k[:40]:40s} {n[k] // runs:7d} {ms:9.3f} {t[k] / tot:6.1%} {gb:8.2f} {gb / (ms / 1e3) if ms else 0:7.0f}")
     print(f"total ms/run {tot / 1e3 / runs:.3f}")
-    return t, b
+    return t, b, inst
 
 
-def record_k3(path, runs, name):
-    t, b = main(path, runs)
+def record_k3(path, runs, name, rnd="r2"):
+    t, b, inst = main(path, runs)
     k3 = [k for k in t if "stage1_kernel" in k or "ring_kernel" in k or "rings_kernel" in k or "border_kernel" in k]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     rec = {"dram_bytes_per_step": sum(b[k] for k in k3) * 1e9 / runs,
            "k3_ms_per_step_under_ncu": sum(t[k] for k in k3) / 1e3 / runs,
-           "source": os.path.relpath(path, os.path.dirname(os.path.abspath(__file__)))}
-    out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "k3_traffic.json")
+           "source": os.path.relpath(os.path.abspath(path), root)}
+    if inst:
+        rec["inst_per_step"] = sum(inst[k] for k in k3) / runs
+        rec["inst_stage1_per_step"] = sum(inst[k] for k in k3 if "stage1" in k) / runs
+        rec["inst_rings_per_step"] = sum(inst[k] for k in k3 if "ring" in k) / runs
+    out = os.path.join(root, "profiles", rnd, "k3_traffic.json")
     data = json.load(open(out)) if os.path.exists(out) else {}
     data[name] = rec
     with open(out, "w") as f:

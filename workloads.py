@@ -11,9 +11,14 @@ public dataset; SURVEY.md section 8(d) fixes the generator:
 4. optional additive N(0, sigma_n) noise;
 5. round half up, clip to 0..255, uint8.
 
-Config 4 ("4x smoothing scale", sigma = 12 on 16384^2) draws its noise field
-at 1/4 resolution, smooths it with sigma/4 and upsamples it x4 bilinearly:
-same correlation length, a fraction of the host time.
+Config 4 ("4x smoothing scale") is sigma = 12 on the full-resolution
+16384^2 noise.  Images of >= 4096^2 pixels are smoothed on the GPU when one is
+present (``_smooth_device``: a separable 97-tap Gaussian, truncate 4 sigma like
+scipy, reflect padding, fp32 shifted-slice accumulation in a fixed order, so
+the result is deterministic); smaller images (and GPU-less hosts) use
+``scipy.ndimage.gaussian_filter``.  The two differ in the last fp32 bits, so
+an image's bytes depend on where it was made; every parity check screens the
+same bytes on both sides, in one process.
 
 Templates follow the reference protocol (synth_bench.py:99-161
 extract_rotated_square / make_case): angle ~ U[0, 360), scale per config,
@@ -63,7 +68,7 @@ CONFIGS = {
     1: Workload(1, 2048, 2048, 1, 3.0, 0.0, 64, (1.25, 1.25), 0.5, 2.0, 4.0 ** (1.0 / 7.0)),
     2: Workload(2, 4096, 4096, 1, 3.0, 8.0, 96, (0.5, 2.0), 0.4, 2.5, 6.25 ** (1.0 / 15.0)),
     3: Workload(3, 1920, 1080, 64, 3.0, 0.0, 48, (0.7, 1.5), 0.6, 1.6, (8.0 / 3.0) ** (1.0 / 7.0)),
-    4: Workload(4, 16384, 16384, 1, 12.0, 0.0, 128, (0.25, 4.0), 0.25, 4.0, 16.0 ** (1.0 / 31.0), zoom=4),
+    4: Workload(4, 16384, 16384, 1, 12.0, 0.0, 128, (0.25, 4.0), 0.25, 4.0, 16.0 ** (1.0 / 31.0)),
 }
 
 
@@ -71,6 +76,37 @@ def _smooth(field: np.ndarray, sigma: float) -> np.ndarray:
     from scipy.ndimage import gaussian_filter
 
     return gaussian_filter(field, sigma, mode="reflect")
+
+
+DEVICE_SMOOTH_PIXELS = 4096 * 4096  # images at least this large are smoothed on the GPU when one exists
+
+
+def _smooth_device(field: np.ndarray, sigma: float):
+    """Separable Gaussian (truncate 4 sigma, reflect padding) on the GPU; returns
+    the smoothed field as a CUDA float32 tensor.  None without a GPU."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return None
+    if not torch.cuda.is_available():
+        return None
+    r = int(4.0 * sigma + 0.5)
+    x = np.arange(-r, r + 1, dtype=np.float64)
+    w = np.exp(-0.5 * (x / sigma) ** 2)
+    w /= w.sum()
+    src = torch.from_numpy(field).cuda()
+    h, wd = src.shape
+    # columns: pad left/right, accumulate the 2r+1 shifted slices
+    pad = torch.nn.functional.pad(src[None, None], (r, r, 0, 0), mode="reflect")[0, 0]
+    tmp = torch.zeros_like(src)
+    for k in range(2 * r + 1):
+        tmp.add_(pad[:, k:k + wd], alpha=float(w[k]))
+    del pad
+    pad = torch.nn.functional.pad(tmp[None, None], (0, 0, r, r), mode="reflect")[0, 0]
+    out = tmp.zero_()
+    for k in range(2 * r + 1):
+        out.add_(pad[k:k + h, :], alpha=float(w[k]))
+    return out
 
 
 def _upsample_bilinear(a: np.ndarray, zoom: int, H: int, W: int) -> np.ndarray:
@@ -97,17 +133,32 @@ def make_image(width: int, height: int, seed: int, sigma: float = 3.0, noise: fl
                n_shapes: int = 20, zoom: int = 1) -> np.ndarray:
     """SURVEY.md 8(d) scene generator (deterministic for a seed)."""
     rng = np.random.default_rng(seed)
+    g = None
     if zoom > 1:
         small = rng.standard_normal((math.ceil(height / zoom), math.ceil(width / zoom))).astype(np.float32)
         small = _smooth(small, sigma / zoom)
         f = _upsample_bilinear(small, zoom, height, width)
+    elif width * height >= DEVICE_SMOOTH_PIXELS:
+        f = rng.standard_normal((height, width), dtype=np.float32)
+        g = _smooth_device(f, sigma)
+        if g is None:
+            f = _smooth(f, sigma)
     else:
         f = _smooth(rng.standard_normal((height, width)).astype(np.float32), sigma)
-    mu = float(f.mean(dtype=np.float64))
-    sd = float(f.std(dtype=np.float64))
-    f -= mu
-    f *= np.float32(40.0 / max(sd, 1e-12))
-    f += np.float32(128.0)
+    if g is not None:  # affine map on the device (fp64 statistics), then back to the host
+        import torch
+
+        mu = float(g.mean(dtype=torch.float64))
+        sd = float(torch.sqrt(((g.double() - mu) ** 2).mean()))
+        g.sub_(mu).mul_(float(np.float32(40.0 / max(sd, 1e-12)))).add_(128.0)
+        f = g.cpu().numpy()
+        del g
+    else:
+        mu = float(f.mean(dtype=np.float64))
+        sd = float(f.std(dtype=np.float64))
+        f -= mu
+        f *= np.float32(40.0 / max(sd, 1e-12))
+        f += np.float32(128.0)
     for _ in range(n_shapes):
         cx = rng.uniform(0, width)
         cy = rng.uniform(0, height)
