@@ -288,9 +288,128 @@ def match_fixture():
     np.savez_compressed(os.path.join(HERE, "match.npz"), **out)
 
 
+def _digest(res):
+    """sha256 over the reference result's candidates, packed size masks (ladder
+    order) and packed region -- compact pin for the 100 criterion-4 screens."""
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(np.array(res.candidates, np.int32).reshape(-1, 3).tobytes())
+    for m in res.ladder:
+        h.update(packbits(res.size_masks[m]).tobytes())
+    h.update(packbits(res.region_mask).tobytes())
+    return h.hexdigest()
+
+
+def _paste(scene, tpl, cx, cy):
+    """pkg/tests/test_screening.py:_paste -- tpl's window centre lands on (cx, cy)."""
+    out = scene.copy()
+    m = tpl.shape[0]
+    lo, _ = F.patch_center_margins(m)
+    out[cy - lo:cy - lo + m, cx - lo:cx - lo + m] = tpl
+    return out
+
+
+def reftests_fixture():
+    """The reference's own hot-path screen tests, as input/output fixtures:
+    pkg/tests/test_screening.py:265-397 (TestScreen: structure, never-miss
+    exact crops, pasted templates at the borders, ordering, masks/region
+    consistency, border keeps, tiny ladder, tested-count formula, scan ==
+    exhaustive scalar membership, stride subset, determinism) and
+    pkg/tests/test_acceptance.py:205-234 (criterion 4: 100 exact-crop screens,
+    10 scenes x 10 crops) and :270-282 (criterion 6 scene).  Every screen is
+    run through the REFERENCE; its full result (or, for the 100 criterion-4
+    screens, a sha256 digest of it) is stored with the inputs."""
+    out = {}
+    full = []  # (key, image, template, cfg kwargs): full results stored
+
+    def add(key, img, tpl, kw=None):
+        kw = kw or {}
+        res = S.screen(img, tpl, _cfg(kw))
+        full.append(key)
+        out[f"{key}/image"] = img
+        out[f"{key}/template"] = tpl
+        out[f"{key}/cfg"] = np.array(json.dumps(kw))
+        out[f"{key}/ladder"] = np.array(res.ladder, np.int32)
+        out[f"{key}/candidates"] = np.array(res.candidates, np.int32).reshape(-1, 3)
+        for m in res.ladder:
+            out[f"{key}/mask_{m}"] = packbits(res.size_masks[m])
+        out[f"{key}/region"] = packbits(res.region_mask)
+        st = res.stats
+        out[f"{key}/stats"] = np.array([st.patches_tested, st.patches_kept, st.region_pixels_kept, st.total_pixels],
+                                       np.int64)
+        return res
+
+    s = make_textured_scene(96, 72, seed=4)  # test_result_structure
+    add("structure", s, s[20:52, 30:62].copy())
+    # test_never_misses_exact_crop: 10 crops, rng 34
+    s = make_textured_scene(160, 120, seed=5)
+    rng = np.random.default_rng(34)
+    lo, hi = F.patch_center_margins(32)
+    crops = []
+    for i in range(10):
+        cx = int(rng.integers(lo, 160 - hi))
+        cy = int(rng.integers(lo, 120 - hi))
+        add(f"crop{i}", s, s[cy - lo:cy - lo + 32, cx - lo:cx - lo + 32].copy())
+        crops.append((cx, cy))
+    out["crop_xy"] = np.array(crops, np.int32)
+    # test_pasted_template_found_at_borders
+    s = make_textured_scene(100, 100, seed=6)
+    tpl = make_textured_scene(32, 32, seed=7)
+    pasted = [(lo, lo), (99 - hi, lo), (lo, 99 - hi), (99 - hi, 99 - hi)]
+    for i, (cx, cy) in enumerate(pasted):
+        add(f"paste{i}", _paste(s, tpl, cx, cy), tpl)
+    out["paste_xy"] = np.array(pasted, np.int32)
+    s = make_textured_scene(128, 96, seed=8)  # test_candidate_ordering
+    add("ordering", s, s[30:62, 40:72].copy())
+    s = make_textured_scene(96, 80, seed=9)  # test_masks_and_region_consistent
+    add("region", s, s[24:56, 24:56].copy())
+    s = make_textured_scene(90, 70, seed=10)  # test_border_centers_kept_in_size_masks_only
+    add("border", s, s[20:52, 20:52].copy())
+    s = make_textured_scene(64, 64, seed=11)  # test_tiny_ladder_sizes_keep_everything
+    add("tiny", s, s[28:36, 28:36].copy())
+    s = make_textured_scene(96, 80, seed=12)  # test_tested_count_matches_grid
+    add("tested", s, s[24:56, 24:56].copy())
+    # test_scan_equals_exhaustive_membership: the scalar path's survivor set
+    s = make_textured_scene(72, 56, seed=13)
+    tpl = s[12:44, 20:52].copy()
+    kw = {"alpha": 1.0, "beta": 1.0}
+    add("exhaustive", s, tpl, kw)
+    fs = S.build_feature_set(tpl, 32, _cfg(kw))
+    t = I.build_tables(s)
+    want = [(cx, cy) for cy in range(lo, 56 - hi) for cx in range(lo, 72 - hi)
+            if fs.contains(F.ring_features(t, cx, cy, 32))]
+    out["exhaustive_want"] = np.array(want, np.int32).reshape(-1, 2)
+    s = make_textured_scene(96, 80, seed=14)  # test_stride
+    add("stride1", s, s[24:56, 24:56].copy(), {"stride": 1})
+    add("stride3", s, s[24:56, 24:56].copy(), {"stride": 3})
+    s = make_textured_scene(100, 90, seed=15)  # test_determinism
+    add("determinism", s, s[30:62, 30:62].copy())
+    s = make_textured_scene(640, 480, seed=99)  # test_criterion_6_screen_speed
+    tpl, _ = make_case(s, seed=1, scale_range=(1.0, 1.0))
+    add("speed640", s, tpl)
+    # criterion 4 (test_acceptance.py:205-234): 100 screens, digests only
+    c4 = []
+    for si in range(10):
+        scene = make_textured_scene(160, 120, seed=7000 + si)
+        out[f"c4_scene{si}"] = scene
+        rng = np.random.default_rng(np.random.SeedSequence([7100, si]))
+        for c in range(10):
+            cx = int(rng.integers(15, 144))
+            cy = int(rng.integers(15, 104))
+            res = S.screen(scene, scene[cy - 15:cy + 17, cx - 15:cx + 17])
+            kept = (cx, cy, 32) in set(res.candidates)
+            c4.append((si, cx, cy, int(kept), len(res.candidates), res.stats.patches_tested,
+                       res.stats.region_pixels_kept))
+            out[f"c4_digest{len(c4) - 1}"] = np.array(_digest(res))
+    out["c4_cases"] = np.array(c4, np.int64)
+    out["full"] = np.array(full)
+    np.savez_compressed(os.path.join(HERE, "reftests.npz"), **out)
+
+
 FIXTURES = {"tables": tables_fixture, "features": features_fixture, "featuresets": featuresets_fixture,
             "screens": screens_fixture, "report": report_fixture, "frozen": frozen_fixture, "io": io_fixture,
-            "match": match_fixture}
+            "match": match_fixture, "reftests": reftests_fixture}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(FIXTURES)):
