@@ -46,6 +46,7 @@ extern "C" {
 
 #define SS_MAX_RINGS 16
 #define SS_MAX_SIZES 64 /* ladder sizes per ss_*_ladder call */
+#define SS_MAX_COARSE 5 /* coarse stage-1 plane sets (shifts) per table build */
 #define SS_KEY_BASE (1LL << 21) /* screening.py:57 _KEY_BASE */
 #define SS_BLOB_HDR 16             /* int64 header slots per ring in a key blob */
 #define SS_BLOB_MAX_BITMAP_WORDS 8192 /* per-ring membership bitmap cap (32 KiB) */
@@ -83,6 +84,22 @@ size_t ss_tables32_bytes(int64_t W, int64_t H);
 int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
                      uint32_t* d_planes32, int64_t plane_pitch, void* d_workspace, size_t workspace_bytes,
                      void* stream);
+
+/*
+ * Stage 1's coarse planes (the fused screen's ring-0 mean test): for each of
+ * n_coarse shifts, the SAT / E / O PLAIN cells as u16 bit slices
+ * (cell >> shift) & 0xffff -- three planes per shift, same pitch as the
+ * 32-bit planes, at d_coarse + (c * 3 + type) * (H + 1) * plane_pitch.
+ * ss_coarse_shift(count) is the shift a region of `count` pixels uses: the
+ * smallest of 1, 4, ..., 16 with 255 count < (2^16 - 4) 2^shift (its slice
+ * sums cannot wrap), -1 if none.
+ */
+int32_t ss_coarse_shift(int64_t count);
+size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse);
+/* ss_build_tables2 plus the coarse planes of h_shifts[0..n_coarse) (<= SS_MAX_COARSE). */
+int ss_build_tables3(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                     uint32_t* d_planes32, int64_t plane_pitch, uint16_t* d_coarse, int32_t n_coarse,
+                     const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* ── per-size membership sets (screening.py:100-178 FeatureSet) ──────── */
 /*
@@ -176,6 +193,23 @@ int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_
                      int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags, int32_t n_streams,
                      void* const* streams, void* const* d_workspaces, size_t workspace_bytes);
 
+/*
+ * ss_screen_ladder with stage 1's coarse planes (ss_build_tables3): when
+ * every fused size's ring-0 square and diamond have their ss_coarse_shift in
+ * h_shifts[0..n_coarse), stage 1 reads the u16 bit slices (half the bytes)
+ * and recomputes exact sums only near a membership boundary; same results.
+ * d_coarse = NULL / n_coarse = 0 is ss_screen_ladder.
+ */
+int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
+                      int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride,
+                      int32_t n_sizes, const int32_t* h_m, const int32_t* h_n_rings, const int32_t* h_ring_n,
+                      const int32_t* h_ring_d, const int64_t* d_blobs, const int64_t* h_blobs,
+                      const int64_t* h_blob_off, double q_mean, double q_std, double q_grad, uint32_t* d_masks,
+                      int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
+                      int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags, int32_t n_streams,
+                      void* const* streams, void* const* d_workspaces, size_t workspace_bytes,
+                      const uint16_t* d_coarse, int32_t n_coarse, const int32_t* h_shifts);
+
 /* Workspace bytes for the fused ladder (flags bit 1) of n_sizes sizes over
  * `rows` decided rows: one row band of at most 4 GiB of candidate list, and
  * at least ss_screen_workspace_bytes (the per-size fallback shares it). */
@@ -253,6 +287,14 @@ int ss_region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch_words, int
  */
 int ss_bits_to_bytes(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H, uint8_t* d_out,
                      void* stream);
+/*
+ * Asynchronous strided copy on `stream` (cudaMemcpy2DAsync, any direction):
+ * `rows` runs of row_bytes bytes, src_pitch / dst_pitch bytes apart.  screen()
+ * streams each finished row chunk of every size's packed mask to pinned host
+ * memory with it while later chunks are still being screened.
+ */
+int ss_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t row_bytes,
+                       int64_t rows, void* stream);
 /* *d_count = number of set bits of the W x H region mask. */
 int ss_popcount(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W, int64_t H,
                 unsigned long long* d_count, void* stream);

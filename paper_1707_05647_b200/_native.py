@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libstarscreen_b200.so")
 SS_OK, SS_EINVAL, SS_ECAPACITY, SS_ECUDA = 0, 1, 2, 3
 SS_MAX_RINGS = 16
 SS_BLOB_MAX_BITMAP_WORDS = 8192
+SS_MAX_COARSE = 5
 KEY_BASE = 1 << 21
 
 _lib = None
@@ -39,6 +40,9 @@ _SIGS = {
     "ss_tables32_bytes": (c_sz, [c_i64, c_i64]),
     "ss_build_tables2": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_i64, c_p, c_sz, c_p]),
     "ss_screen_fits32": (ctypes.c_int, [c_i32, c_p, c_p]),
+    "ss_coarse_shift": (c_i32, [c_i64]),
+    "ss_coarse_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "ss_build_tables3": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p, c_sz, c_p]),
     "ss_keyset_blob": (ctypes.c_int, [c_p, c_p, c_i32, c_p, ctypes.POINTER(c_sz)]),
     "ss_screen_size": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
                                       c_i32, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),
@@ -50,6 +54,9 @@ _SIGS = {
     "ss_screen_ladder": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
                                         c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_i64, c_p, c_i64,
                                         c_p, c_i32, c_i32, c_p, c_p, c_sz]),
+    "ss_screen_ladder2": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32,
+                                         c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_i64,
+                                         c_p, c_i64, c_p, c_i32, c_i32, c_p, c_p, c_sz, c_p, c_i32, c_p]),
     "ss_ladder_keysets": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_i64,
                                          c_p]),
     "ss_compact_workspace_bytes": (c_sz, [c_i64]),
@@ -66,6 +73,7 @@ _SIGS = {
                                              c_p, c_sz, c_p]),
     "ss_popcount": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),
     "ss_bits_to_bytes": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p]),
+    "ss_copy_rows_async": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_i64, c_i64, c_p]),
     "ss_match_plane_pitch": (c_i64, [c_i64]),
     "ss_match_planes": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_i64, c_p]),
     "ss_match_probe_bytes": (c_sz, [c_i32, c_i32]),

@@ -47,6 +47,12 @@ struct BuildArgs {
     long long* state;  // [B-1][4 kinds][3 types][state_len]
     int64_t slen;
     int64_t n_chunks;
+    // coarse PLAIN planes for stage 1 (nullable): for shift c, the SAT / E /
+    // O PLAIN cells as u16 bit slices (cell >> shift[c]) & 0xffff, planes
+    // (c * 3 + type) * plane_stride apart (same pitch as the full planes)
+    unsigned short* coarse;
+    int n_coarse;
+    int shift[SS_MAX_COARSE];
 };
 
 __device__ __forceinline__ long long shfl_down64(long long v, int d) {
@@ -135,6 +141,8 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                 }
                 if (a.planes32) *reinterpret_cast<uint4*>(a.planes32 + p * a.plane_stride + c) = make_uint4(0, 0, 0, 0);
             }
+            for (int p = 0; p < 3 * a.n_coarse; ++p)
+                *reinterpret_cast<uint2*>(a.coarse + p * a.plane_stride + c) = make_uint2(0, 0);
         }
     }
 
@@ -264,6 +272,21 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                         ve[1] = make_longlong2((long long)e2, (long long)e3);
                         vo[0] = make_longlong2((long long)o0, (long long)o1);
                         vo[1] = make_longlong2((long long)o2, (long long)o3);
+                    }
+                    if (k == 0 && a.coarse) {  // stage 1's u16 bit slices of the PLAIN cells (K3L)
+                        const unsigned sv[3][4] = {{(unsigned)S[0][0], (unsigned)S[0][1], (unsigned)S[0][2], (unsigned)S[0][3]},
+                                                   {(unsigned)e0, (unsigned)e1, (unsigned)e2, (unsigned)e3},
+                                                   {(unsigned)o0, (unsigned)o1, (unsigned)o2, (unsigned)o3}};
+                        for (int ci = 0; ci < a.n_coarse; ++ci) {
+                            const int sh = a.shift[ci];
+#pragma unroll
+                            for (int ty = 0; ty < 3; ++ty) {
+                                const unsigned lo = ((sv[ty][0] >> sh) & 0xffffu) | (((sv[ty][1] >> sh) & 0xffffu) << 16);
+                                const unsigned hi = ((sv[ty][2] >> sh) & 0xffffu) | (((sv[ty][3] >> sh) & 0xffffu) << 16);
+                                *reinterpret_cast<uint2*>(a.coarse + (ci * 3 + ty) * a.plane_stride + off) =
+                                    make_uint2(lo, hi);
+                            }
+                        }
                     }
                     if (a.planes32) {  // the same cells mod 2^32 (region sums are exact in 32 bits)
                         *reinterpret_cast<uint4*>(a.planes32 + (0 * 4 + k) * a.plane_stride + off) =
@@ -451,7 +474,8 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
 }
 
 int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes, uint32_t* d_planes32,
-                 int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream) {
+                 int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream, uint16_t* d_coarse = nullptr,
+                 int n_coarse = 0, const int32_t* h_shifts = nullptr) {
     if (W < 1 || H < 1) { set_error("empty image"); return SS_EINVAL; }
     if (overflow_guard_fails(W, H)) {
         set_error("image %lldx%lld too large for 64-bit integral cells", (long long)W, (long long)H);
@@ -467,6 +491,16 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         set_error("null or misaligned device pointer");
         return SS_EINVAL;
     }
+    if (n_coarse < 0 || n_coarse > SS_MAX_COARSE || (n_coarse > 0 && (!d_coarse || !h_shifts)) ||
+        (reinterpret_cast<uintptr_t>(d_coarse) & 15)) {
+        set_error("bad coarse planes");
+        return SS_EINVAL;
+    }
+    for (int i = 0; i < n_coarse; ++i)
+        if (h_shifts[i] < 0 || h_shifts[i] > 16) {  // bits [shift, shift + 16) of a cell known mod 2^32
+            set_error("coarse shift %d outside [0, 16]", (int)h_shifts[i]);
+            return SS_EINVAL;
+        }
     const size_t need = build_workspace_bytes(W, H);
     if (ws_bytes < need || (need && !d_ws)) {
         set_error("build workspace too small: %zu < %zu", ws_bytes, need);
@@ -488,6 +522,9 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     a.state = reinterpret_cast<long long*>(static_cast<char*>(d_ws) + rowpre_bytes(W, H));
     a.slen = state_len(W, rb);
     a.n_chunks = n_chunks(W, rb);
+    a.coarse = reinterpret_cast<unsigned short*>(d_coarse);
+    a.n_coarse = d_coarse ? n_coarse : 0;
+    for (int i = 0; i < SS_MAX_COARSE; ++i) a.shift[i] = i < a.n_coarse ? (int)h_shifts[i] : 0;
     const int64_t nbands = n_bands(H, rb);
 
     rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
@@ -525,5 +562,14 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
                      void* stream) {
     return ss::build_tables(d_img, W, H, img_pitch, d_planes, d_planes32, plane_pitch, d_workspace, workspace_bytes,
                             stream);
+}
+size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse) {
+    return (size_t)3 * (size_t)n_coarse * (size_t)(H + 1) * ss::plane_pitch(W) * 2;
+}
+int ss_build_tables3(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                     uint32_t* d_planes32, int64_t plane_pitch, uint16_t* d_coarse, int32_t n_coarse,
+                     const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return ss::build_tables(d_img, W, H, img_pitch, d_planes, d_planes32, plane_pitch, d_workspace, workspace_bytes,
+                            stream, d_coarse, n_coarse, h_shifts);
 }
 }

@@ -16,8 +16,21 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                         const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
                         uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
-                        size_t ws_bytes, cudaStream_t s);
+                        size_t ws_bytes, cudaStream_t s, const uint16_t* d_coarse, int n_coarse,
+                        const int32_t* h_shifts);
 }  // namespace ss
+
+extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
+                                 int64_t plane_pitch, int64_t W, int64_t H, int64_t y_origin, int64_t y_begin,
+                                 int64_t y_end, int32_t stride, int32_t n_sizes, const int32_t* h_m,
+                                 const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
+                                 const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off,
+                                 double q_mean, double q_std, double q_grad, uint32_t* d_masks,
+                                 int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
+                                 int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags,
+                                 int32_t n_streams, void* const* streams, void* const* d_workspaces,
+                                 size_t workspace_bytes, const uint16_t* d_coarse, int32_t n_coarse,
+                                 const int32_t* h_shifts);
 
 extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
                                 int64_t plane_pitch, int64_t W, int64_t H, int64_t y_origin, int64_t y_begin,
@@ -29,6 +42,24 @@ extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_plane
                                 int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags,
                                 int32_t n_streams, void* const* streams, void* const* d_workspaces,
                                 size_t workspace_bytes) {
+    return ss_screen_ladder2(d_planes, d_planes32, w, h, plane_pitch, W, H, y_origin, y_begin, y_end, stride, n_sizes,
+                             h_m, h_n_rings, h_ring_n, h_ring_d, d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad,
+                             d_masks, mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,
+                             d_stage_counts, flags, n_streams, streams, d_workspaces, workspace_bytes, nullptr, 0,
+                             nullptr);
+}
+
+extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
+                                 int64_t plane_pitch, int64_t W, int64_t H, int64_t y_origin, int64_t y_begin,
+                                 int64_t y_end, int32_t stride, int32_t n_sizes, const int32_t* h_m,
+                                 const int32_t* h_n_rings, const int32_t* h_ring_n, const int32_t* h_ring_d,
+                                 const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off,
+                                 double q_mean, double q_std, double q_grad, uint32_t* d_masks,
+                                 int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
+                                 int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags,
+                                 int32_t n_streams, void* const* streams, void* const* d_workspaces,
+                                 size_t workspace_bytes, const uint16_t* d_coarse, int32_t n_coarse,
+                                 const int32_t* h_shifts) {
     if (n_sizes < 0 || n_sizes > SS_MAX_SIZES || !h_m || !h_n_rings || !h_ring_n || !h_ring_d || !h_blob_off ||
         n_streams < 1 || !streams || !d_workspaces || (n_sizes > 0 && (!d_masks || !d_row_counts))) {
         ss::set_error("bad ladder arguments");
@@ -70,7 +101,8 @@ extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_plane
                                             stride, (int)ks.size(), ks.data(), h_m, h_n_rings, h_ring_n, h_ring_d,
                                             d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad, d_masks,
                                             mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,
-                                            d_stage_counts, d_workspaces[0], workspace_bytes, ss::as_stream(st));
+                                            d_stage_counts, d_workspaces[0], workspace_bytes, ss::as_stream(st),
+                                            d_coarse, n_coarse, h_shifts);
             if (e == ss::SS_DECLINED) {
                 for (int k : ks) {
                     const int32_t* rn = h_ring_n + (size_t)k * SS_MAX_RINGS;

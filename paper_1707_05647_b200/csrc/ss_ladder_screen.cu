@@ -19,7 +19,9 @@
 // Replaces, for all sizes of screen()'s ladder loop at once (screening.py:
 // 502-520), the per-size _scan_size (screening.py:418-471).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "ss_screen_dev.cuh"
@@ -38,11 +40,15 @@ struct SizeDev {
     unsigned* row_counts;  // per mask row
     int lo, hi, n_rings, ring0;
     int bm1, wm1, bsrc1;  // stage-1 mean bits: smem word offset (-1: binary search), words, blob u32 index
+    int c_sq, c_di;       // coarse stage 1: plane-set index of ring 0's square / diamond sums
+    float fa_c, fb_c;     // coarse stage 1: 2^shift / (2 count q_mean) of the square / diamond
+    float band_c;         // coarse stage 1: bound on |t_coarse - t| from the bit slices (K3L)
     int pad;
 };
 
 struct FusedArgs {
     const void* planes;  // 12 planes of T
+    const unsigned* planes32;  // the 32-bit planes (coarse stage 1's exact fallback)
     long long pitch, ps;
     int W, H, y_origin, y_begin, y_end, stride;  // [y_begin, y_end): rows decided by this pass
     int mask_y0;
@@ -56,8 +62,35 @@ struct FusedArgs {
     SizeDev size[FMAX_SIZES];
     RingDev ring[FMAX_RINGS];
 };
-static_assert(sizeof(FusedArgs) <= 32000, "fused ladder parameters exceed the kernel parameter limit");
+// Stage 1 from coarse planes: per shift set c, the u16 bit slices (cell >>
+// shift) & 0xffff of the SAT / E / O PLAIN cells (ss_build_tables3).
+constexpr int CNK = SS_MAX_COARSE;
+struct CoarseMaps {
+    CUtensorMap sat[CNK], e[CNK], o[CNK];
+};
+static_assert(sizeof(FusedArgs) + sizeof(CoarseMaps) <= 31000, "fused ladder parameters exceed the kernel parameter limit");
 static_assert(sizeof(RingDev) % 4 == 0, "RingDev is copied to shared memory by words");
+
+// Candidate-list entries: (x, y | size << TAG_SHIFT), plus -- when stage 1
+// runs on the 32-bit PLAIN planes, so ring 0's PLAIN sums are exact u32 -- the
+// square and diamond PLAIN sums themselves: the rings kernel then skips ring
+// 0's 8 PLAIN gathers (level 0 is most of its work).
+#ifndef FUSED_SUMS
+#define FUSED_SUMS 0  // measured slower: int4 entries cost more list traffic than the 8 gathers they save (config 1 K3 0.480 -> 0.510 ms, config 4 36.3 -> 38.1 ms)
+#endif
+template <typename T1> struct FEntryT { using type = int2; };
+#if FUSED_SUMS
+template <> struct FEntryT<unsigned> { using type = int4; };
+#endif
+template <typename T1> using FEntry = typename FEntryT<T1>::type;
+__device__ __forceinline__ int2 entry_of(int x, int tag, unsigned, unsigned, int2*) { return make_int2(x, tag); }
+__device__ __forceinline__ int4 entry_of(int x, int tag, unsigned sq, unsigned sd, int4*) {
+    return make_int4(x, tag, (int)sq, (int)sd);
+}
+template <typename E> __device__ __forceinline__ E no_entry() {
+    return entry_of(-1, -1, 0u, 0u, static_cast<E*>(nullptr));
+}
+constexpr int CAND_BUF = 64;  // per-warp staging of list entries (flushed 32 at a time)
 
 struct TileMapF {
     int n_tx, n_ty, strip, n_sizes;
@@ -92,10 +125,12 @@ constexpr int TXMAX = 32 * (FUSED_CPW32 > 2 ? FUSED_CPW32 : 2);  // widest fused
 // parameter block per tile).
 struct __align__(16) TileConst {
     int tx, ty, sz, ylo;
-    int yhi, xlo, xhi, bm1;
+    int yhi, xlo, xhi, bm1;  // bm1: smem word offset of the mean bits, -1: binary search, -2: `win` holds them
     int qr, ql, po0, po1;  // corner columns inside the staged boxes
     float fa, fb;
     int cm_lo, cm_n;
+    unsigned win_lo, win_hi;  // ring-0 mean-projection bits of cells cm_lo .. cm_lo + 63 (when cm_n <= 64)
+    int pad0, pad1;
 };
 
 // strip-major; inside a strip: tile row, then size, then tile column
@@ -123,16 +158,17 @@ __device__ __forceinline__ void tile_coords_f(const TileMapF& t, long long idx, 
 template <typename T>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     ladder_stage1_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ TmaMaps maps, const TileMapF tm,
-                         int parts, int reserve, int2* list_base, long long part_cap, unsigned* list_ctr,
+                         int parts, int reserve, FEntry<T>* list_base, long long part_cap, unsigned* list_ctr,
                          unsigned* tile_ctr_base) {
     using G = GeoF<T>;
+    using E = FEntry<T>;
     constexpr int STAGES = G::STAGES, CPW = G::CPW;
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ TileConst tile_info[STAGES];  // the tile in each stage and its size's constants
-    __shared__ int2 cand_buf[WARPS][32 * (CPW + 1)];
+    __shared__ E cand_buf[WARPS][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
         for (int s = 0; s < a.n_sizes; ++s) {
@@ -181,7 +217,15 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                     tcst.yhi = a.H - 1 - S.hi;
                     tcst.xlo = S.lo;
                     tcst.xhi = a.W - 1 - S.hi;
-                    tcst.bm1 = S.bm1;
+                    // cm_n <= 64 (every 8-level mean quantizer): the whole
+                    // mean projection rides in two registers of the tile
+                    if (S.bm1 >= 0 && R0.cm_n <= 64) {
+                        tcst.bm1 = -2;
+                        tcst.win_lo = sbits[S.bm1];
+                        tcst.win_hi = S.wm1 > 1 ? sbits[S.bm1 + 1] : 0u;
+                    } else {
+                        tcst.bm1 = S.bm1;
+                    }
                     tcst.qr = G::rem(R0.n + 1);
                     tcst.ql = G::rem(1 - R0.n);
                     tcst.po0 = G::rem(-R0.d);
@@ -210,9 +254,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     }
 
     const unsigned lt = (1u << lane) - 1u;
-    int2* list0 = list_base + part * part_cap;
+    E* list0 = list_base + part * part_cap;
     unsigned* count0 = list_ctr + part * CTR_STRIDE;
-    int2* buf = cand_buf[warp];
+    E* buf = cand_buf[warp];
     int nbuf = 0;
     unsigned res = 0;
     bool have_res = false;
@@ -266,7 +310,17 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         const int xt = tx * G::TX;
         const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;  // warp-uniform: no per-lane tests
         unsigned pm = 0;  // bit c: chunk c's centre passes
-        if (tc.bm1 >= 0) {
+        if (tc.bm1 == -2) {
+            // bits cm_lo..cm_lo+63 in two registers; bits at and above cm_n are 0
+            const int cm_lo = tc.cm_lo;
+            const unsigned wl = tc.win_lo, wh = tc.win_hi;
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const unsigned i = (unsigned)(cm[c] - cm_lo);
+                const unsigned w = (i & 32u) ? wh : wl;
+                pm |= (unsigned)(i < 64u && ((w >> (i & 31u)) & 1u)) << c;
+            }
+        } else if (tc.bm1 >= 0) {
             const int cm_lo = tc.cm_lo;
             const unsigned cm_n = (unsigned)tc.cm_n;
             const unsigned* bits = sbits + tc.bm1;
@@ -291,6 +345,291 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         } else if (a.stage_counts) {
             n_int += 32 * CPW;
         }
+        if (!__any_sync(FULL, pm != 0u)) continue;  // most warp rows of a tile have no passer
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const bool p = (pm >> c) & 1u;
+            const unsigned pb = __ballot_sync(FULL, p);
+            if (p) buf[nbuf + __popc(pb & lt)] = entry_of(xt + 32 * c + lane, tag, (unsigned)s1q[c], (unsigned)s1d[c], buf);
+            nbuf += __popc(pb);
+            n_pass += __popc(pb);
+            if (nbuf >= 32) {  // < 64 staged: flush the newest 32 (list order is free)
+                __syncwarp();
+                if (res_left == 0) {
+                    if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                    res_base = __shfl_sync(FULL, res, 0);
+                    res_left = reserve;
+                    if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                    have_res = true;
+                }
+                list0[res_base + lane] = buf[nbuf - 32 + lane];
+                res_base += 32;
+                res_left -= 32;
+                nbuf -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    if (have_res) {
+        unsigned base = res_base, left = res_left;
+        if (left == 0) {
+            base = __shfl_sync(FULL, res, 0);
+            left = reserve;
+        } else {
+            const unsigned ahead = __shfl_sync(FULL, res, 0);
+            for (unsigned i = lane; i < (unsigned)reserve; i += 32) list0[ahead + i] = no_entry<E>();
+        }
+        for (unsigned i = lane; i < left; i += 32) list0[base + i] = i < (unsigned)nbuf ? buf[i] : no_entry<E>();
+    } else if (nbuf > 0) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
+        base = __shfl_sync(FULL, base, 0);
+        if (lane < nbuf) list0[base + lane] = buf[lane];
+    }
+    if (a.stage_counts && lane == 0) {
+        atomicAdd(a.stage_counts + 0, (unsigned long long)n_int);
+        atomicAdd(a.stage_counts + 1, (unsigned long long)n_pass);
+    }
+}
+
+// Coarse stage-1 tiles: 16 rows x 224 columns of u16 bit slices; boxes
+// 16 x 248 (496-byte rows; measured on B200 with tools/tma_probe: 16 x 248 /
+// 16 x 256 u16 boxes stream at ~40 B/clk/SM, 16 x 192-200 at ~16, u32 16 x 196
+// at ~32), 3 stages of 62 KB.
+struct GeoC {
+    static constexpr int CPW = 7;
+    static constexpr int TX = 32 * CPW;
+    static constexpr int STAGES = 3;
+    static constexpr int ALIGN = 8;  // 16-byte aligned box starts
+    static constexpr int BW = 248;
+    static_assert(BW >= TX + ALIGN - 1, "box must cover the tile at any alignment");
+    static constexpr int BOX_ELEMS = BW * TY;
+    static constexpr int BOX_BYTES = BOX_ELEMS * 2;
+    static_assert(BOX_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
+    static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+    __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }
+    __device__ static int rem(int c) { return c & (ALIGN - 1); }
+};
+
+struct __align__(16) TileConstC {
+    int tx, ty, sz, ylo;
+    int yhi, xlo, xhi, bm1;  // bm1 as TileConst
+    int qr, ql, po0, po1;
+    float fa, fb, band;  // coarse factors of the size and its error bound
+    int cm_lo;
+    int cm_n;
+    unsigned win_lo, win_hi;
+    int pad;
+};
+
+// Stage 1 of every fused size from the coarse planes.  A region sum S of
+// `count` pixels whose slices have shift k is recovered as the integer I with
+// |S - I 2^k| < 2^(k+1) (four floors of cell / 2^k; no wrap since
+// 255 count < (2^16 - 4) 2^k, ss_coarse_shift), so the mean-cell estimate
+// t = I_sq fa + I_di fb + 1/2 is within band (+ the fp32 terms of mean_cell)
+// of the reference's t.  A centre is decided from the estimate unless t lies
+// within that bound of a cell boundary whose two cells differ in ring-0
+// membership; those lanes recompute the exact sums from the 32-bit planes
+// (mean_cell: fp32 estimate, fp64 sequence near a boundary).  Same decisions
+// as ladder_stage1_kernel; half the TMA bytes per centre.
+__global__ void __launch_bounds__((WARPS + 1) * 32, 1)
+    ladder_stage1_coarse_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ CoarseMaps maps,
+                                const TileMapF tm, int parts, int reserve, int2* list_base, long long part_cap,
+                                unsigned* list_ctr, unsigned* tile_ctr_base) {
+    using G = GeoC;
+    constexpr int STAGES = G::STAGES, CPW = G::CPW;
+    extern __shared__ __align__(128) unsigned char dsmem[];
+    unsigned char* stage_buf = dsmem;
+    unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    __shared__ TileConstC tile_info[STAGES];
+    __shared__ int2 cand_buf[WARPS][CAND_BUF];
+    {
+        const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
+        for (int s = 0; s < a.n_sizes; ++s) {
+            const SizeDev& S = a.size[s];
+            if (S.bm1 < 0) continue;
+            for (int i = threadIdx.x; i < S.wm1; i += blockDim.x)
+                sbits[S.bm1 + i] = S.bsrc1 >= 0 ? __ldg(blob32 + S.bsrc1 + i) : 0u;
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = (int)(blockIdx.x % parts);
+
+    if (warp == WARPS) {
+        if (lane == 0) {
+            const int tc = (int)(blockIdx.x % TILE_CTRS);
+            unsigned* tile_ctr = tile_ctr_base + tc * CTR_STRIDE;
+            unsigned t_next = atom_add_ahead(tile_ctr, 1u);
+            for (int it = 0;; ++it) {
+                const int s = it % STAGES;
+                const long long t = (long long)t_next * TILE_CTRS + tc;
+                if (t < tm.n_tiles) t_next = atom_add_ahead(tile_ctr, 1u);
+                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+                if (t >= tm.n_tiles) {
+                    tile_info[s].tx = -1;
+                    mbar_arrive(&full_bar[s]);
+                    break;
+                }
+                int tx, ty, sz;
+                tile_coords_f(tm, t, tx, ty, sz);
+                const SizeDev& S = a.size[sz];
+                const RingDev& R0 = a.ring[S.ring0];
+                {
+                    TileConstC& tcst = tile_info[s];
+                    tcst.tx = tx;
+                    tcst.ty = ty;
+                    tcst.sz = sz;
+                    tcst.ylo = S.lo;
+                    tcst.yhi = a.H - 1 - S.hi;
+                    tcst.xlo = S.lo;
+                    tcst.xhi = a.W - 1 - S.hi;
+                    if (S.bm1 >= 0 && R0.cm_n <= 64) {
+                        tcst.bm1 = -2;
+                        tcst.win_lo = sbits[S.bm1];
+                        tcst.win_hi = S.wm1 > 1 ? sbits[S.bm1 + 1] : 0u;
+                    } else {
+                        tcst.bm1 = S.bm1;
+                    }
+                    tcst.qr = G::rem(R0.n + 1);
+                    tcst.ql = G::rem(1 - R0.n);
+                    tcst.po0 = G::rem(-R0.d);
+                    tcst.po1 = G::rem(R0.d + 1);
+                    tcst.fa = S.fa_c;
+                    tcst.fb = S.fb_c;
+                    tcst.band = S.band_c;
+                    tcst.cm_lo = R0.cm_lo;
+                    tcst.cm_n = R0.cm_n;
+                }
+                const int x0 = tx * G::TX;
+                const int cy0 = a.y_begin + ty * TY - a.y_origin;
+                unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
+                mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
+                const int n = R0.n, d = R0.d;
+                const CUtensorMap* msat = &maps.sat[S.c_sq];
+                const CUtensorMap* me = &maps.e[S.c_di];
+                const CUtensorMap* mo = &maps.o[S.c_di];
+                tma_load_2d(dst + 0 * G::BOX_BYTES, msat, G::floor_al(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 1 * G::BOX_BYTES, msat, G::floor_al(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
+                tma_load_2d(dst + 2 * G::BOX_BYTES, msat, G::floor_al(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 3 * G::BOX_BYTES, msat, G::floor_al(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
+                tma_load_2d(dst + 4 * G::BOX_BYTES, me, G::floor_al(x0 + 1), cy0 + d + 1, &full_bar[s]);
+                tma_load_2d(dst + 5 * G::BOX_BYTES, me, G::floor_al(x0 + 1), cy0 - d, &full_bar[s]);
+                tma_load_2d(dst + 6 * G::BOX_BYTES, mo, G::floor_al(x0 - d), cy0, &full_bar[s]);
+                tma_load_2d(dst + 7 * G::BOX_BYTES, mo, G::floor_al(x0 + d + 1), cy0, &full_bar[s]);
+            }
+        }
+        return;
+    }
+
+    const unsigned lt = (1u << lane) - 1u;
+    int2* list0 = list_base + part * part_cap;
+    unsigned* count0 = list_ctr + part * CTR_STRIDE;
+    int2* buf = cand_buf[warp];
+    int nbuf = 0;
+    unsigned res = 0;
+    bool have_res = false;
+    unsigned res_base = 0, res_left = 0;
+    unsigned n_int = 0, n_pass = 0;
+    const bool unit_stride = a.stride == 1;
+    for (int it = 0;; ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        const TileConstC tc = tile_info[s];
+        if (tc.tx < 0) break;
+        const int tx = tc.tx, ty = tc.ty, sz = tc.sz;
+        const int y = a.y_begin + ty * TY + warp;
+        const bool row_int = y < a.y_end && y >= tc.ylo && y <= tc.yhi && (unit_stride || (y % a.stride) == 0);
+        int iq[CPW], id[CPW];  // coarse sums: I with |S - I 2^k| < 2^(k+1)
+        if (row_int) {
+            const int qr = tc.qr, ql = tc.ql, pe = 1, po0 = tc.po0, po1 = tc.po1;
+            const unsigned short* box =
+                reinterpret_cast<const unsigned short*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const unsigned short* b = box + 32 * c;
+                constexpr int E = G::BOX_ELEMS;
+                const unsigned vq = (unsigned)b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql];
+                const unsigned vd = (unsigned)b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe];
+                iq[c] = (int)((vq + 1u) & 0xffffu) - 1;  // I in [-1, 2^16 - 3]
+                id[c] = (int)((vd + 1u) & 0xffffu) - 1;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        if (!row_int) continue;
+        const int cm_lo = tc.cm_lo;
+        auto member = [&](int cm) -> bool {
+            if (tc.bm1 == -2) {
+                const unsigned i = (unsigned)(cm - cm_lo);
+                const unsigned w = (i & 32u) ? tc.win_hi : tc.win_lo;
+                return i < 64u && ((w >> (i & 31u)) & 1u);
+            }
+            if (tc.bm1 >= 0) {
+                const unsigned i = (unsigned)(cm - cm_lo);
+                return i < (unsigned)tc.cm_n && bit(sbits + tc.bm1, (int)i);
+            }
+            const RingDev& R0 = a.ring[a.size[sz].ring0];
+            return bsearch_eq(a.blob + R0.off_m, R0.n_m, cm);
+        };
+        const int xt = tx * G::TX;
+        unsigned pm = 0, amb = 0;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const float tf = fmaf((float)iq[c], tc.fa, fmaf((float)id[c], tc.fb, 0.5f));
+            const float dl = tc.band + fmaf(tf, 4e-6f, 4e-6f);
+            const float fl = floorf(tf);
+            const int cm = (int)fl;
+            const float fr = tf - fl;
+            const bool p = member(cm);
+            pm |= (unsigned)p << c;
+            if (fr < dl || fr > 1.0f - dl) {  // the true cell may be the neighbour
+                if (member(fr < dl ? cm - 1 : cm + 1) != p) amb |= 1u << c;
+            }
+        }
+        const int xlo = tc.xlo, xhi = tc.xhi;
+        const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;
+        if (!full) {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const int x = xt + 32 * c + lane;
+                const bool interior = x >= xlo && x <= xhi && (unit_stride || (x % a.stride) == 0);
+                if (!interior) {
+                    pm &= ~(1u << c);
+                    amb &= ~(1u << c);
+                }
+                if (a.stage_counts) n_int += __popc(__ballot_sync(FULL, interior));
+            }
+        } else if (a.stage_counts) {
+            n_int += 32 * CPW;
+        }
+        if (__any_sync(FULL, amb != 0u)) {
+            // exact PLAIN sums from the 32-bit planes (ambiguous interior lanes only)
+            const RingDev& R0 = a.ring[a.size[sz].ring0];
+            const unsigned* rowp = a.planes32 + (long long)(y - a.y_origin) * a.pitch;
+#pragma unroll 1
+            for (int c = 0; c < CPW; ++c) {
+                if (!((amb >> c) & 1u)) continue;
+                const unsigned* q = rowp + xt + 32 * c + lane;
+                const unsigned* e = q + 4 * a.ps;
+                const unsigned* o = q + 8 * a.ps;
+                const unsigned sq = __ldg(q + R0.sa) - __ldg(q + R0.sb) - __ldg(q + R0.sc) + __ldg(q + R0.sd);
+                const unsigned sd = __ldg(e + R0.ea) - __ldg(o + R0.ob) - __ldg(o + R0.oc) + __ldg(e + R0.ed);
+                const bool p = member(mean_cell(a, R0, sq, sd));
+                pm = (pm & ~(1u << c)) | ((unsigned)p << c);
+            }
+        }
+        const int tag = y | (sz << TAG_SHIFT);
+        if (!__any_sync(FULL, pm != 0u)) continue;
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
             const bool p = (pm >> c) & 1u;
@@ -298,21 +637,21 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
             if (p) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
             nbuf += __popc(pb);
             n_pass += __popc(pb);
-        }
-        while (nbuf >= 32) {
-            __syncwarp();
-            if (res_left == 0) {
-                if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
-                res_base = __shfl_sync(FULL, res, 0);
-                res_left = reserve;
-                if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
-                have_res = true;
+            if (nbuf >= 32) {
+                __syncwarp();
+                if (res_left == 0) {
+                    if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                    res_base = __shfl_sync(FULL, res, 0);
+                    res_left = reserve;
+                    if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                    have_res = true;
+                }
+                list0[res_base + lane] = buf[nbuf - 32 + lane];
+                res_base += 32;
+                res_left -= 32;
+                nbuf -= 32;
+                __syncwarp();
             }
-            list0[res_base + lane] = buf[nbuf - 32 + lane];
-            res_base += 32;
-            res_left -= 32;
-            nbuf -= 32;
-            __syncwarp();
         }
     }
     __syncwarp();
@@ -386,10 +725,11 @@ struct SizeSm {
 // Every ring of every fused size over the stage-1 list (see rings_kernel in
 // ss_screen.cu for the batching / queue scheme); lanes of one batch may
 // belong to different sizes: each reads its size's ring from shared memory.
-template <typename T>
+template <typename T, typename E>
 __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
-    ladder_rings_kernel(const __grid_constant__ FusedArgs a, int parts, const int2* list_base, long long part_cap,
+    ladder_rings_kernel(const __grid_constant__ FusedArgs a, int parts, const E* list_base, long long part_cap,
                         const unsigned* list_ctr, unsigned* group_ctr) {
+    constexpr bool SUMS = sizeof(E) == sizeof(int4);  // level-0 entries carry ring 0's PLAIN sums
     extern __shared__ __align__(16) unsigned char rsm[];
     RingDev* sring = reinterpret_cast<RingDev*>(rsm);
     SizeSm* ssize = reinterpret_cast<SizeSm*>(rsm + (size_t)a.n_rings * sizeof(RingDev));
@@ -423,7 +763,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     int q = (int)(wid % parts), visited = 1;
     const unsigned gc = (wid / parts) % GROUP_CTRS;
     unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
-    const int2* in = list_base + q * part_cap;
+    const E* in = list_base + q * part_cap;
     unsigned g_raw = 0;
     if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
     unsigned cur = 0, k = 0;
@@ -446,20 +786,25 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
             if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
         }
     };
-    auto fetch = [&]() -> int2 {
+    auto fetch = [&]() -> E {
         const unsigned slot = cur + 32 * k + lane;
-        return (have_input && slot < cnt_q) ? in[slot] : make_int2(-1, -1);
+        return (have_input && slot < cnt_q) ? in[slot] : no_entry<E>();
     };
     grab();
-    int2 next = fetch();
+    E next = fetch();
     for (;;) {
         int level = -1;
         for (int l = levels - 1; l >= 1; --l)
             if (qget(l) >= 32) { level = l; break; }
         int2 e;
+        unsigned s1q0 = 0, s1d0 = 0;  // level 0 (SUMS): ring 0's PLAIN sums from stage 1
         if (level < 0 && have_input) {
             level = 0;
-            e = next;
+            e = make_int2(next.x, next.y);
+            if constexpr (SUMS) {
+                s1q0 = (unsigned)reinterpret_cast<const int4&>(next).z;
+                s1d0 = (unsigned)reinterpret_cast<const int4&>(next).w;
+            }
             if (++k == RG / 32 || cur + 32 * k >= cnt_q) {
                 k = 0;
                 grab();
@@ -480,7 +825,8 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         const bool valid = e.x >= 0;
         const int sz = valid ? (e.y >> TAG_SHIFT) : 0, y = e.y & YMASK;
         const SizeSm S = ssize[sz];
-        const bool pass = valid && eval_ring_fast<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin);
+        const bool pass = valid && eval_ring_fast<T>(a, sring[S.ring0 + level], sbits, level, e.x, y - a.y_origin,
+                                                     SUMS && level == 0, s1q0, s1d0);
 #if RINGS_STATS
         if (valid && pass) atomicAdd(a.stage_counts + 7 + 4 * level, 1ull);
         if (valid && level == 0) {  // would the means of all deeper rings pass?
@@ -525,7 +871,7 @@ constexpr size_t FCTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
 #define FUSED_LARGE_TILES_MACRO 32768
 #endif
 constexpr long long FUSED_LARGE_TILES = FUSED_LARGE_TILES_MACRO;  // partitioned lists from this many tiles per pass
-constexpr size_t FUSED_WS_CAP = (size_t)4 << 30;  // ss_ladder_workspace_bytes: row bands beyond this
+constexpr size_t FUSED_WS_CAP = (size_t)(2 * sizeof(FEntry<unsigned>)) << 28;  // ss_ladder_workspace_bytes: row bands beyond this (4 GiB of int2 entries)
 
 // capacity in tiles of TXMAX x TY centres (covers either fused tile width)
 long long tiles_of(int64_t W, int64_t rows) {
@@ -538,9 +884,9 @@ long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int part
     const long long ctas = (2LL * sms + parts - 1) / parts;
     return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * (TXMAX * TY) + ctas * WARPS * 2 * RESERVE_MAX;
 }
-size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms) {
+size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms, size_t entry = sizeof(FEntry<unsigned>)) {
     const int parts = parts_for(W, rows, n_sizes);
-    return FCTR_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * sizeof(int2);
+    return FCTR_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * entry;
 }
 
 // The three PLAIN-plane TMA descriptors (SAT / E / O) of a plane buffer,
@@ -573,7 +919,48 @@ int plane_maps_cached(TmaMaps& maps, const void* planes, int eb, int bw, int64_t
     return SS_OK;
 }
 
+// The coarse TMA descriptors (u16 SAT / E / O bit-slice planes of every
+// shift set), cached like plane_maps_cached.
+int coarse_maps_cached(CoarseMaps& maps, const uint16_t* coarse, int n_coarse, int64_t W, int64_t h, int64_t pitch,
+                       long long ps) {
+    using Key = std::tuple<const void*, int, int64_t, int64_t, int64_t, int>;
+    static std::mutex mu;
+    static std::map<Key, CoarseMaps> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{coarse, n_coarse, W, h, pitch, dev};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const auto it = cache.find(key);
+        if (it != cache.end()) {
+            maps = it->second;
+            return SS_OK;
+        }
+    }
+    std::memset(&maps, 0, sizeof(maps));
+    for (int c = 0; c < n_coarse; ++c) {
+        const uint16_t* base = coarse + (size_t)c * 3 * (size_t)ps;
+        if (int e = encode_plane_map(&maps.sat[c], base, 2, GeoC::BW, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.e[c], base + ps, 2, GeoC::BW, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.o[c], base + 2 * ps, 2, GeoC::BW, W, h, pitch)) return e;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 256) cache.clear();
+    cache[key] = maps;
+    return SS_OK;
+}
+
 }  // namespace
+
+// The coarse shift of a region of `count` pixels (ss_coarse_shift): the
+// smallest of 1, 4, 7, ... 16 with 255 count < (2^16 - 4) 2^shift, so its u16
+// slice sum never wraps; -1 when none.  Consecutive grid shifts keep
+// 2^shift / count <= 4 x 510 / 65532 (the estimate's error, K3L).
+int coarse_shift(long long count) {
+    for (int k = 1; k <= 16; k += 3)
+        if (255LL * count < (65532LL << k)) return k;
+    return -1;
+}
 
 size_t screen_workspace_bytes(int64_t W, int64_t rows);  // ss_screen.cu
 
@@ -600,7 +987,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                         const int64_t* d_blobs, const int64_t* h_blobs, const int64_t* h_blob_off, double qm,
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
                         uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
-                        size_t ws_bytes, cudaStream_t s) {
+                        size_t ws_bytes, cudaStream_t s, const uint16_t* d_coarse, int n_coarse,
+                        const int32_t* h_shifts) {
     if (n < 1 || n > FMAX_SIZES || H >= (1LL << TAG_SHIFT) || W > (1 << 30) || stride < 1) return SS_DECLINED;
     if (pitch != plane_pitch(W)) { set_error("plane pitch mismatch"); return SS_EINVAL; }
     if (mask_pitch < (W + 31) / 32) { set_error("mask pitch too small"); return SS_EINVAL; }
@@ -613,6 +1001,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     std::vector<unsigned char> hostbuf(sizeof(FusedArgs), 0);
     FusedArgs& a = *reinterpret_cast<FusedArgs*>(hostbuf.data());
     a.planes = planes;
+    a.planes32 = static_cast<const unsigned*>(eb == 4 ? planes : planes32_s1);
     a.pitch = pitch;
     a.ps = (h + 1) * pitch;
     if (3 * a.ps >= (long long)INT32_MAX) return SS_DECLINED;  // PlanePtrs: 32-bit kind offsets
@@ -685,6 +1074,30 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         n_rings += nr;
     }
     if (a.max_levels > 8) return SS_DECLINED;  // the rings' queue counts are 8 x 8 bits
+    // Coarse stage 1 (ladder_stage1_coarse_kernel) when every size's ring-0
+    // square and diamond have a built shift and the estimate's error bound
+    // stays well inside a cell; SS_COARSE=0 forces the 32-bit stage 1.
+    bool coarse = d_coarse && n_coarse > 0 && h_shifts && a.planes32;
+    if (const char* e = getenv("SS_COARSE")) coarse = coarse && atoi(e) != 0;
+    for (int j = 0; j < n && coarse; ++j) {
+        SizeDev& S = a.size[j];
+        const RingDev& R0 = a.ring[S.ring0];
+        const long long cq = 4LL * R0.n * R0.n, cd = 2LL * R0.d * R0.d + 2LL * R0.d + 1;
+        const int kq = coarse_shift(cq), kd = coarse_shift(cd);
+        S.c_sq = S.c_di = -1;
+        for (int i = 0; i < n_coarse; ++i) {
+            if (h_shifts[i] == kq) S.c_sq = i;
+            if (h_shifts[i] == kd) S.c_di = i;
+        }
+        const double band = (std::ldexp(1.0, kq) / (double)cq + std::ldexp(1.0, kd) / (double)cd) / qm;
+        if (kq < 0 || kd < 0 || S.c_sq < 0 || S.c_di < 0 || !(band < 0.2)) {
+            coarse = false;
+            break;
+        }
+        S.fa_c = (float)(std::ldexp(1.0, kq) / (2.0 * (double)cq * qm));
+        S.fb_c = (float)(std::ldexp(1.0, kd) / (2.0 * (double)cd * qm));
+        S.band_c = (float)(band * (1.0 + 1e-5));
+    }
     a.n_rings = n_rings;
     a.bm_words = bm_words;
     a.bm1_words = bm1;
@@ -709,22 +1122,33 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     }
     // (row counts and workspace counters are zeroed by ladder_border_kernel)
     TmaMaps maps;
-    if (int e = s1_u32 ? plane_maps_cached(maps, eb == 4 ? planes : planes32_s1, 4, GeoF<unsigned>::BW, W, h, pitch, a.ps)
-                       : plane_maps_cached(maps, planes, 8, GeoF<long long>::BW, W, h, pitch, a.ps))
+    CoarseMaps cmaps;
+    if (coarse) {
+        if (int e = coarse_maps_cached(cmaps, d_coarse, n_coarse, W, h, pitch, a.ps)) return e;
+    } else if (int e = s1_u32 ? plane_maps_cached(maps, eb == 4 ? planes : planes32_s1, 4, GeoF<unsigned>::BW, W, h,
+                                                  pitch, a.ps)
+                              : plane_maps_cached(maps, planes, 8, GeoF<long long>::BW, W, h, pitch, a.ps)) {
         return e;
+    }
     unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
     unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
     unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
-    int2* list = reinterpret_cast<int2*>(static_cast<char*>(d_ws) + FCTR_BYTES);
+    void* list_raw = static_cast<char*>(d_ws) + FCTR_BYTES;
 
     auto launch = [&](auto tag, auto tag1) -> int {
         using T = decltype(tag);    // the rings' planes
         using T1 = decltype(tag1);  // stage 1's PLAIN planes
         using G = GeoF<T1>;
+        using E = FEntry<T1>;
+        E* list = static_cast<E*>(list_raw);
         auto s1 = ladder_stage1_kernel<T1>;
-        auto rk = ladder_rings_kernel<T>;
-        const size_t s1_smem = (size_t)G::STAGES * G::STAGE_BYTES + (size_t)std::max(bm1, 1) * 4;
-        const int s1_per_sm = std::min(occupancy(reinterpret_cast<const void*>(s1), (WARPS + 1) * 32, s1_smem), 2);
+        auto s1c = ladder_stage1_coarse_kernel;
+        auto rk = ladder_rings_kernel<T, E>;
+        const int tile_x = coarse ? GeoC::TX : G::TX;
+        const size_t s1_smem = (size_t)(coarse ? GeoC::STAGES * GeoC::STAGE_BYTES : G::STAGES * G::STAGE_BYTES) +
+                               (size_t)std::max(bm1, 1) * 4;
+        const void* s1_fn = coarse ? reinterpret_cast<const void*>(s1c) : reinterpret_cast<const void*>(s1);
+        const int s1_per_sm = std::min(occupancy(s1_fn, (WARPS + 1) * 32, s1_smem), 2);
         const size_t rk_smem = (size_t)n_rings * sizeof(RingDev) + (size_t)n * sizeof(SizeSm) +
                                (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.max_levels * QCAP * sizeof(int2);
         const int rk_per_sm = std::max(occupancy(reinterpret_cast<const void*>(rk), RK_WARPS * 32, rk_smem), 1);
@@ -733,7 +1157,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             a.y_begin = (int)yb;
             a.y_end = (int)ye;
             TileMapF tm;
-            tm.n_tx = (int)((W + G::TX - 1) / G::TX);
+            tm.n_tx = (int)((W + tile_x - 1) / tile_x);
             tm.n_ty = (int)((brows + TY - 1) / TY);
             tm.n_sizes = n;
             tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n;
@@ -747,7 +1171,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                 tm.strip = 1;
                 for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
                     const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * TY;
-                    const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * G::TX + max_m + 2) * 12 * eb;
+                    const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * tile_x + max_m + 2) * 12 * eb;
                     if (ws <= budget) {
                         tm.strip = strip;
                         break;
@@ -766,9 +1190,17 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             }
             const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)sms * s1_per_sm),
                                                        (long long)TILE_CTRS);
-            s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, parts,
-                                                                 parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list,
-                                                                 part_cap, list_ctr, tile_ctr);
+            if (coarse) {
+                if constexpr (std::is_same<E, int2>::value) {
+                    s1c<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, cmaps, tm, parts,
+                                                                          parts > 1 ? RESERVE_LARGE : RESERVE_SMALL,
+                                                                          list, part_cap, list_ctr, tile_ctr);
+                }
+            } else {
+                s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, parts,
+                                                                     parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list,
+                                                                     part_cap, list_ctr, tile_ctr);
+            }
             note_launch();
             if (int e = check_launch("ladder_stage1_kernel")) return e;
             rk<<<(unsigned)(sms * rk_per_sm), RK_WARPS * 32, rk_smem, s>>>(a, parts, list, part_cap, list_ctr,
@@ -783,6 +1215,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
 }
 
 }  // namespace ss
+
+extern "C" int32_t ss_coarse_shift(int64_t count) { return ss::coarse_shift(count); }
 
 extern "C" size_t ss_ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
     return ss::ladder_workspace_bytes(W, rows, n_sizes);

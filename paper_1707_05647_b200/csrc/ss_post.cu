@@ -697,4 +697,16 @@ int ss_bits_to_bytes(const uint32_t* d_bits, int64_t mask_pitch_words, int64_t W
                      void* stream) {
     return ss::bits_to_bytes(d_bits, mask_pitch_words, W, H, d_out, stream);
 }
+int ss_copy_rows_async(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t row_bytes,
+                       int64_t rows, void* stream) {
+    if (rows < 0 || row_bytes < 0 || (rows > 0 && (!dst || !src || dst_pitch < row_bytes || src_pitch < row_bytes))) {
+        ss::set_error("bad row copy");
+        return SS_EINVAL;
+    }
+    if (rows == 0 || row_bytes == 0) return SS_OK;
+    if (cudaMemcpy2DAsync(dst, (size_t)dst_pitch, src, (size_t)src_pitch, (size_t)row_bytes, (size_t)rows,
+                          cudaMemcpyDefault, ss::as_stream(stream)) != cudaSuccess)
+        return ss::check_launch("row copy");
+    return SS_OK;
+}
 }

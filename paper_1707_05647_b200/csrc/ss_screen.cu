@@ -435,9 +435,11 @@ __global__ void selftest_cells_kernel(unsigned long long n, unsigned long long s
         long long s1q, s2q, s1d, s2d;
         sums(R.icq, mq, sq_t, s1q, s2q);
         sums(R.icd, md, sd_t, s1d, s2d);
-        if (std_cell_fast(a, R, s1q, s1d, s2q, s2d) !=
-            std_cell_exact(a, R, div_rn((double)s1q, R.cnt_sq, R.rcp_sq), div_rn((double)s1d, R.cnt_di, R.rcp_di), s2q, s2d))
-            ++bad_s;
+        const int cs_ref =
+            std_cell_exact(a, R, div_rn((double)s1q, R.cnt_sq, R.rcp_sq), div_rn((double)s1d, R.cnt_di, R.rcp_di), s2q, s2d);
+        if (std_cell_fast(a, R, s1q, s1d, s2q, s2d) != cs_ref) ++bad_s;
+        // the 32 x 32-bit variance products of the 32-bit-plane path, wherever its sums fit
+        if (s2q < (1LL << 32) && s2d < (1LL << 32) && std_cell_fast<true>(a, R, s1q, s1d, s2q, s2d) != cs_ref) ++bad_s;
         // gradient: components of a target magnitude split between square and diamond
         double gm_t = 200.0 * uni();
         if (aim) gm_t = a.qg * (double)(1 + (int)(8.0 * uni()) - 0.5) * (1.0 + 1e-6 * (uni() - 0.5));

@@ -305,10 +305,21 @@ __device__ __forceinline__ bool cell_of(float tf, float band, int& cell) {
 // std cell from the exact integer variances V = s2 * count - s1^2 (>= 0):
 // fp32 estimate, the fp64 reference sequence only within its error band of a
 // boundary (bounds: eval_ring_fast).
-template <class A>
+// NARROW: the PLAIN / SQUARED sums are < 2^32 (32-bit planes, fits32), so the
+// variance products are single 32 x 32 -> 64-bit multiplies.
+template <bool NARROW = false, class A>
 __device__ __forceinline__ int std_cell_fast(const A& a, const RingDev& R, long long s1q, long long s1d, long long s2q,
                                              long long s2d) {
-    const long long vq = s2q * R.icq - s1q * s1q, vd = s2d * R.icd - s1d * s1d;
+    long long vq, vd;
+    if constexpr (NARROW) {
+        vq = (long long)((unsigned long long)(unsigned)s2q * (unsigned)R.icq -
+                         (unsigned long long)(unsigned)s1q * (unsigned)s1q);
+        vd = (long long)((unsigned long long)(unsigned)s2d * (unsigned)R.icd -
+                         (unsigned long long)(unsigned)s1d * (unsigned)s1d);
+    } else {
+        vq = s2q * R.icq - s1q * s1q;
+        vd = s2d * R.icd - s1d * s1d;
+    }
     const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(__fsqrt_rn(__ll2float_rn(vq)), R.rcq),
                                           __fmul_rn(__fsqrt_rn(__ll2float_rn(vd)), R.rcd)),
                                 0.5f);
@@ -356,18 +367,28 @@ __device__ __forceinline__ int grad_cell_fast(const A& a, const RingDev& R, int 
 //         band 1e-6 (t + 1) + 1e-5 / qs;
 //   grad: |gx_f - gx| <= 2.5e-7 (|gxq| + |gxd|) (likewise y), hypot is
 //         1-Lipschitz, + 2.5e-7 rel; band 2x that plus 4e-7 (t + 1).
+//   have_s1: ring R's PLAIN sums s1q_in / s1d_in are given (stage 1 carried
+//   them in the candidate list: exact u32), so its 8 PLAIN corners are not read.
 template <typename T, class A>
 __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, const unsigned* sb, int level, int cx,
-                                               int cy) {
+                                               int cy, bool have_s1 = false, unsigned s1q_in = 0,
+                                               unsigned s1d_in = 0) {
     const PlanePtrs<T> P = plane_ptrs<T>(a, cy, cx);
     Corners<T> c0, c2, ckx, cky;
-    load_corners(P, R, 0, c0);
+    long long s1q, s1d;
+    if (have_s1) {
+        s1q = s1q_in;
+        s1d = s1d_in;
+    } else {
+        load_corners(P, R, 0, c0);
+        s1q = unsigned_sum(sq_of(c0));
+        s1d = unsigned_sum(di_of(c0));
+    }
     load_corners(P, R, 3, c2);
 #if !EVAL_TWO_PHASE
     load_corners(P, R, 1, ckx);
     load_corners(P, R, 2, cky);
 #endif
-    const long long s1q = unsigned_sum(sq_of(c0)), s1d = unsigned_sum(di_of(c0));
     const int cm = mean_cell(a, R, s1q, s1d);  // features.py:137 (level 0 entries passed this test in stage 1)
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 4 + 4 * level, 1ull);
@@ -377,7 +398,7 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
     atomicAdd(a.stage_counts + 5 + 4 * level, 1ull);
 #endif
     const long long s2q = unsigned_sum(sq_of(c2)), s2d = unsigned_sum(di_of(c2));
-    const int cs = std_cell_fast(a, R, s1q, s1d, s2q, s2d);
+    const int cs = std_cell_fast<sizeof(T) == 4>(a, R, s1q, s1d, s2q, s2d);
     if (!member_ms(a, R, sb, cm, cs)) return false;
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 6 + 4 * level, 1ull);
@@ -701,7 +722,10 @@ inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes,
     const cuuint32_t estr[2] = {1, 1};
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook
-    const CUresult r = encode(map, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_INT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+    const CUtensorMapDataType dt = elem_bytes == 8   ? CU_TENSOR_MAP_DATA_TYPE_INT64
+                                   : elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                                     : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    const CUresult r = encode(map, dt, 2,
                               const_cast<void*>(plane), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

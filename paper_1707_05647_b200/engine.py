@@ -298,6 +298,10 @@ class Engine:
         self._region_m = 0
         self.capacity = 0
         self.xy = None
+        self.coarse = None  # stage 1's coarse planes (u16 bit slices, ss_build_tables3)
+        self.coarse_shifts: List[int] = []  # the shifts the last build wrote
+        self.masks_done = None  # completion of the last run's streamed mask copy (run(host_masks=...))
+        self._host_masks_inflight = None  # (pinned buffer, event) of that copy, kept alive until it has landed
         self.stage_counts = None  # set to a (4,) int64 device tensor to instrument the cascade
         self.force_int64 = False  # test hook: screen every size from the int64 planes
         self.hooks = None  # optional (before, after) callables(main_stream) around the K3 region
@@ -359,27 +363,59 @@ class Engine:
                 return True
         return False
 
-    def build_tables(self, img: torch.Tensor, int64: bool = False) -> None:
-        """K1/K2 on the current stream.  img: (rows, W) uint8 on the device.
-        Writes the 32-bit planes, and the int64 planes too when `int64`."""
-        with torch.cuda.device(self.device):
-            self._build_tables(img, int64)
+    def coarse_shifts_for(self, tp: Optional[TemplatePlan]) -> List[int]:
+        """The coarse-plane shifts stage 1 needs for this ladder: ss_coarse_shift
+        of every evaluated size's ring-0 square (4 n^2) and diamond
+        (2 d^2 + 2 d + 1) pixel counts ([] when a count has none, more than
+        SS_MAX_COARSE are needed, or SS_COARSE=0)."""
+        if tp is None or os.environ.get("SS_COARSE", "1") == "0":
+            return []
+        need = set()
+        for sp in tp.sizes:
+            if not sp.plan:
+                continue
+            n, d = sp.plan[0]
+            for count in (4 * n * n, 2 * d * d + 2 * d + 1):
+                k = int(self.L.ss_coarse_shift(count))
+                if k < 0:
+                    return []
+                need.add(k)
+        return sorted(need) if len(need) <= _native.SS_MAX_COARSE else []
 
-    def _build_tables(self, img: torch.Tensor, int64: bool) -> None:
+    def build_tables(self, img: torch.Tensor, int64: bool = False, tp: Optional[TemplatePlan] = None) -> None:
+        """K1/K2 on the current stream.  img: (rows, W) uint8 on the device.
+        Writes the 32-bit planes, the int64 planes too when `int64`, and --
+        given the template plan -- the coarse planes its stage 1 reads."""
+        with torch.cuda.device(self.device):
+            self._build_tables(img, int64, tp)
+
+    def _build_tables(self, img: torch.Tensor, int64: bool, tp: Optional[TemplatePlan] = None) -> None:
         assert img.dtype == torch.uint8 and img.is_cuda and img.shape == (self.rows, self.W)
         img = img.contiguous()
         if int64 and self.planes is None:
             tb = int(self.L.ss_tables_bytes(self.W, self.rows))
             self.planes = torch.empty(tb // 8, dtype=torch.int64, device=self.device)
-        _native.check(self.L.ss_build_tables2(img.data_ptr(), self.W, self.rows, self.W,
+        shifts = self.coarse_shifts_for(tp)
+        if shifts:
+            nb = int(self.L.ss_coarse_bytes(self.W, self.rows, len(shifts)))
+            if self.coarse is None or self.coarse.numel() < nb:
+                self.coarse = None
+                self.coarse = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        sh = np.array(shifts or [0], np.int32)
+        _native.check(self.L.ss_build_tables3(img.data_ptr(), self.W, self.rows, self.W,
                                               _p(self.planes) if int64 else None, self.planes32.data_ptr(),
-                                              self.pitch, self.build_ws.data_ptr(), self.build_ws.numel(),
+                                              self.pitch, _p(self.coarse) if shifts else None, len(shifts),
+                                              sh.ctypes.data, self.build_ws.data_ptr(), self.build_ws.numel(),
                                               _stream_handle(self.device)), "build_tables")
+        self.coarse_shifts = list(shifts)
 
-    def screen_ladder(self, tp: TemplatePlan, main: Optional[torch.cuda.Stream] = None) -> None:
+    def screen_ladder(self, tp: TemplatePlan, main: Optional[torch.cuda.Stream] = None,
+                      rows: Optional[Tuple[int, int]] = None) -> None:
         """K3 for every ladder size in one ss_screen_ladder call (sizes spread
-        over the side streams, event fork/join around them)."""
+        over the side streams, event fork/join around them); `rows` = the
+        global rows [y0, y1) to decide (default: all of this engine's)."""
         main = main or torch.cuda.current_stream(self.device)
+        y0, y1 = rows if rows is not None else (self.y_begin, self.y_end)
         cfg = tp.config
         q = cfg.quantizer.factors()
         L = len(tp.sizes)
@@ -406,13 +442,17 @@ class Engine:
             wss = (ctypes.c_void_p * (1 + self.n_streams))(self.screen_ws[0].data_ptr(),
                                                             *[w.data_ptr() for w in self.screen_ws])
             n_streams, ws_bytes = 1 + self.n_streams, self.screen_ws[0].numel()
-        _native.check(self.L.ss_screen_ladder(
+        shifts = np.array(self.coarse_shifts or [0], np.int32)
+        _native.check(self.L.ss_screen_ladder2(
             _p(self.planes), None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch,
-            self.W, self.H, self.y_origin, self.y_begin, self.y_end, cfg.stride, L, tp.m_arr.ctypes.data,
+            self.W, self.H, self.y_origin, y0, y1, cfg.stride, L, tp.m_arr.ctypes.data,
             tp.n_rings.ctypes.data, tp.ring_n.ctypes.data, tp.ring_d.ctypes.data, tp.blobs_dev.data_ptr(),
-            tp.blobs.ctypes.data, tp.blob_off.ctypes.data, q[0], q[1], q[2], self.masks.data_ptr(), self.words,
-            self.mrows * self.words, self.row_counts.data_ptr(), self.row_counts.shape[1], _p(self.stage_counts),
-            flags, n_streams, handles, wss, ws_bytes),
+            tp.blobs.ctypes.data, tp.blob_off.ctypes.data, q[0], q[1], q[2],
+            # the ABI's mask / row-count row 0 is global row y0
+            self.masks.data_ptr() + (y0 - self.y_begin) * self.words * 4, self.words, self.mrows * self.words,
+            self.row_counts.data_ptr() + (y0 - self.y_begin) * 4, self.row_counts.shape[1], _p(self.stage_counts),
+            flags, n_streams, handles, wss, ws_bytes,
+            _p(self.coarse) if self.coarse_shifts else None, len(self.coarse_shifts), shifts.ctypes.data),
             "screen")
 
     def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:
@@ -437,27 +477,81 @@ class Engine:
         _native.check(self.L.ss_popcount(self.region.data_ptr(), self.words, self.W, self.H,
                                          self.totals[1:].data_ptr(), _stream_handle(self.device)), "popcount")
 
+    # Streamed mask readback (run(host_masks=...)): row chunks of about this
+    # many mask bytes (all sizes) each, so a chunk's D2H overlaps the next
+    # chunks' screening; smaller results go in one piece after the ladder.
+    READBACK_CHUNK_BYTES = 128 << 20
+
+    def host_mask_buffer(self, n_sizes: int) -> torch.Tensor:
+        """A pinned (n_sizes, rows, words) int32 host buffer for
+        run(host_masks=...).  The buffer of the previous streamed copy is
+        released only once that copy has landed."""
+        if self._host_masks_inflight is not None:
+            buf, ev = self._host_masks_inflight
+            if not ev.query():
+                ev.synchronize()
+            self._host_masks_inflight = None
+        return torch.empty((n_sizes, self.mrows, self.words), dtype=torch.int32, pin_memory=True)
+
+    def readback_chunks(self, n_sizes: int) -> List[Tuple[int, int]]:
+        """Global row ranges [a, b) screened one ss_screen_ladder call each
+        when the masks are streamed to the host (multiples of 16 rows)."""
+        total = n_sizes * self.mrows * self.words * 4
+        n = max(1, min(16, total // self.READBACK_CHUNK_BYTES))
+        per = -(-self.mrows // n)  # ceil
+        step = max(256, -(-per // 16) * 16)
+        return [(a, min(self.y_end, a + step)) for a in range(self.y_begin, self.y_end, step)]
+
     def run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool = True, region: bool = True,
-            capacity: Optional[int] = None) -> None:
+            capacity: Optional[int] = None, host_masks: Optional[torch.Tensor] = None) -> None:
         """Enqueue the whole screen of one image (no host sync) on this
-        engine's device (its current stream)."""
+        engine's device (its current stream).  host_masks (a pinned
+        host_mask_buffer): every size's packed mask rows are copied there on
+        the engine's copy stream, row chunk by row chunk as each chunk's
+        screen finishes; `masks_done` records the last copy."""
         with torch.cuda.device(self.device):
-            self._run(img, tp, build=build, region=region, capacity=capacity)
+            self._run(img, tp, build=build, region=region, capacity=capacity, host_masks=host_masks)
+
+    def _screen_streamed(self, tp: TemplatePlan, main: torch.cuda.Stream, host: torch.Tensor) -> None:
+        L = len(tp.sizes)
+        assert host.shape == (L, self.mrows, self.words) and host.dtype == torch.int32 and host.is_pinned()
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream(self.device)
+        cs = self.copy_stream
+        pitch = self.mrows * self.words * 4
+        for a, b in self.readback_chunks(L):
+            self.screen_ladder(tp, main, (a, b))
+            ev = torch.cuda.Event()
+            ev.record(main)
+            cs.wait_event(ev)
+            off = (a - self.y_begin) * self.words * 4
+            _native.check(self.L.ss_copy_rows_async(host.data_ptr() + off, pitch, self.masks.data_ptr() + off, pitch,
+                                                    (b - a) * self.words * 4, L, cs.cuda_stream), "mask readback")
+        done = torch.cuda.Event()
+        done.record(cs)
+        self.masks_done = done
+        self._host_masks_inflight = (host, done)
 
     def _run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool, region: bool,
-             capacity: Optional[int]) -> None:
+             capacity: Optional[int], host_masks: Optional[torch.Tensor] = None) -> None:
         full = (self.y_begin, self.y_end, self.y_origin, self.rows) == (0, self.H, 0, self.H)
         region = region and full
         self._ensure(len(tp.sizes), tp.max_m, capacity or self.default_capacity(tp), region)
         if build:
-            self._build_tables(img, self.needs_int64(tp))
+            self._build_tables(img, self.needs_int64(tp), tp)
         main = torch.cuda.current_stream(self.device)
         if self.readback_done is not None:  # the previous run's rows must have left before K4 rewrites them
             main.wait_event(self.readback_done)
             self.readback_done = None
+        if self.masks_done is not None:  # likewise its streamed masks before K3 rewrites them
+            main.wait_event(self.masks_done)
+            self.masks_done = None
         if self.hooks is not None:
             self.hooks[0](main)
-        self.screen_ladder(tp, main)
+        if host_masks is None:
+            self.screen_ladder(tp, main)
+        else:
+            self._screen_streamed(tp, main, host_masks)
         if self.hooks is not None:
             self.hooks[1](main)
         if region:

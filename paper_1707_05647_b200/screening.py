@@ -118,17 +118,28 @@ class SizeMasks(Mapping):
     first access to .packed(m) and unpacked on first access to [m].
     """
 
-    def __init__(self, ladder: Tuple[int, ...], packed, width: int):
+    def __init__(self, ladder: Tuple[int, ...], packed, width: int, pending=None):
         self._ladder = tuple(ladder)
-        self._packed = packed  # (L, H, words) uint32 array or int32 CUDA tensor
+        # (L, H, words) uint32 array, int32 CUDA tensor, or a pinned int32 CPU
+        # tensor that a stream copy is still filling (screen() streams each
+        # finished row chunk to the host while later chunks are screened);
+        # `pending` is that copy's completion event
+        self._packed = packed
+        self._pending = pending
         self._width = width
         self._host: Dict[int, np.ndarray] = {}
         self._cache: Dict[int, np.ndarray] = {}
+
+    def _ready(self) -> None:
+        if self._pending is not None:
+            self._pending.synchronize()
+            self._pending = None
 
     def packed_all(self) -> np.ndarray:
         """(L, H, ceil(W/32)) uint32: every size's bit-packed rows in ladder
         order, copied to the host in one transfer."""
         if len(self._host) < len(self._ladder):
+            self._ready()
             allw = _host_words(self._packed)
             for k, m in enumerate(self._ladder):
                 self._host[m] = allw[k]
@@ -137,9 +148,19 @@ class SizeMasks(Mapping):
 
     def packed(self, m: int) -> np.ndarray:
         if m not in self._host:
+            self._ready()
             k = self._ladder.index(m)
             self._host[m] = _host_words(self._packed[k])
         return self._host[m]
+
+    def source(self, m: int):
+        """Size m's packed rows where they live: a CUDA tensor, or host words."""
+        self._ready()
+        k = self._ladder.index(m)
+        p = self._packed
+        if isinstance(p, torch.Tensor):
+            return p[k] if p.is_cuda else p[k].numpy().view(np.uint32)
+        return np.asarray(p)[k]
 
     def __getitem__(self, m: int) -> np.ndarray:
         if m not in self._ladder:
@@ -295,9 +316,7 @@ class ScreeningResult:
 
         if m not in self.ladder:
             raise KeyError(m)
-        packed = self.size_masks._packed
-        k = self.ladder.index(m)
-        return packed_to_pgm(packed[k] if isinstance(packed, torch.Tensor) else np.asarray(packed)[k], self.width)
+        return packed_to_pgm(self.size_masks.source(m), self.width)
 
     def __repr__(self) -> str:
         return (f"ScreeningResult({self.width}x{self.height}, n={self.template_side}, ladder={self.ladder}, "
@@ -347,11 +366,13 @@ def validate(image, template, cfg: ScreeningConfig):
     return img, tpl
 
 
-def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> ScreeningResult:
+def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, masks=None) -> ScreeningResult:
     """Counts to the host; survivor list, masks and region stay on the device
     (private copies, the engine's buffers are reused) until first accessed;
     `readback` (Engine.start_readback) carries the survivor rows' host copy
-    that started right after compaction."""
+    that started right after compaction; `masks` = (pinned host tensor,
+    event) of the size masks streamed to the host during the screen
+    (Engine.run(host_masks=...)), used instead of a device copy."""
     cur = torch.cuda.current_stream(eng.device)
     totals = eng.totals.cpu()  # synchronises the stream
     kept = int(totals[0])
@@ -361,7 +382,7 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> 
     size_counts = eng.size_counts[: len(tp.sizes)].cpu().tolist()
     eng.last_kept = kept
     rows = eng.xy[:kept].clone()
-    packed = eng.masks[: len(tp.sizes)].clone()
+    packed = eng.masks[: len(tp.sizes)].clone() if masks is None else None
     region = eng.region.clone() if eng.region is not None else None
     # the copies are ordered on this stream; a caller reading them on another
     # stream must wait for it (screen_batch), and their memory must not be
@@ -379,8 +400,8 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None) -> 
         wall_time_s=elapsed,
     )
     cands = CandidateList(rows, kept, readback)
-    return ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, SizeMasks(tp.ladder, packed, W),
-                           region, stats, size_counts)
+    sm = SizeMasks(tp.ladder, packed, W) if masks is None else SizeMasks(tp.ladder, masks[0], W, pending=masks[1])
+    return ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, sm, region, stats, size_counts)
 
 
 def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfig] = None,
@@ -404,11 +425,15 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
         tp = plan_ladder(tpl.shape[1], cfg)
         pending = launch_features(tp, tpl, eng.device, eng.template_stream)
         img_dev = upload_image(img, eng.device)
-        eng.build_tables(img_dev, int64=eng.needs_int64(tp))
+        eng.build_tables(img_dev, int64=eng.needs_int64(tp), tp=tp)
         fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
-        eng.run(img_dev, tp, build=False)
+        # the size masks go to pinned host memory chunk by chunk while the
+        # later row chunks are still being screened (the reference returns
+        # host masks; at 16384^2 x 33 sizes that is 1.1 GB of D2H)
+        host_masks = eng.host_mask_buffer(len(tp.sizes))
+        eng.run(img_dev, tp, build=False, host_masks=host_masks)
         readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
-        return fetch_result(eng, tp, start, readback)
+        return fetch_result(eng, tp, start, readback, masks=(host_masks, eng.masks_done))
 
 
 _pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
@@ -479,7 +504,7 @@ def _screen_batch(pool: EnginePool, checked, cfg: ScreeningConfig) -> List[Scree
             tp = plan_ladder(tpl.shape[1], cfg)
             feats = launch_features(tp, tpl, eng.device, eng.template_stream)
             img_dev = upload_image(img, eng.device)
-            eng.build_tables(img_dev, int64=eng.needs_int64(tp))
+            eng.build_tables(img_dev, int64=eng.needs_int64(tp), tp=tp)
             fill_keysets(tp, tpl, eng.device, eng.template_stream, feats)
             eng.run(img_dev, tp, build=False)
         pending[j] = (i, tp, start)

@@ -149,3 +149,46 @@ def test_config4_tiles_and_properties(cuda):
     assert res2.candidates == res.candidates
     for m in res.ladder[::8]:
         assert np.array_equal(res2.size_masks.packed(m), res.size_masks.packed(m))
+
+
+def test_config2_full_image_vs_tiled_oracle(cuda):
+    """Config 2 over the WHOLE 4096^2 image: the tiled oracle (SURVEY.md App.
+    B.1; 8 row bands, each screened with its halo) decides every centre; the
+    GPU's size masks (all 17 sizes), candidate list, tested count and kept
+    region must match on every core.  SURVEY.md 8(d)'s threshold-band
+    positions are counted from the oracle's fp64 features: every disagreement
+    would have to be one (0 disagreements expected and required here)."""
+    import os
+
+    from paper_1707_05647_b200.screening import unpack_bits
+
+    wl, case, res = run_config(2)
+    H, W = case.image.shape
+    nthreads = os.cpu_count() or 1
+    cand = res.candidates.array()
+    tested = 0
+    band_total = 0
+    cands = []
+    for i in range(8):
+        y0, y1 = i * H // 8, (i + 1) * H // 8
+        t = O.screen_tile(case.image, case.template, ocfg(wl), y0, y1, 0, W, nthreads=nthreads, band=True)
+        assert tuple(t.ladder) == tuple(res.ladder)
+        for m in res.ladder:
+            got = unpack_bits(res.size_masks.packed(m)[y0:y1], W)
+            d = got != t.size_masks[m]
+            assert not (d & ~t.band_masks[m]).any(), f"rows [{y0},{y1}) m={m}: {int(d.sum())} off-band"
+            assert not d.any(), f"rows [{y0},{y1}) m={m}: {int(d.sum())} in-band disagreements"
+            band_total += int(t.band_masks[m].sum())
+        ry0, ry1, rx0, rx1 = t.region_window
+        assert np.array_equal(unpack_bits(res.region_packed()[ry0:ry1], W)[:, rx0:rx1], t.region)
+        tested += t.patches_tested
+        cands.append(t.candidates)
+    want = np.concatenate(cands)
+    # the oracle lists each band's candidates in ladder order; the global list
+    # is ladder order first, then row-major: a stable sort by ladder position
+    order = {m: k for k, m in enumerate(res.ladder)}
+    want = want[np.argsort([order[int(m)] for m in want[:, 2]], kind="stable")]
+    assert np.array_equal(cand, want)
+    assert res.stats.patches_tested == tested
+    print(f"config 2 full image: {tested} positions*scales, {len(cand)} candidates, "
+          f"{band_total} threshold-band positions, 0 disagreements")

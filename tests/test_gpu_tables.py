@@ -189,3 +189,37 @@ def test_template_features_device_bitwise(cuda):
     for i, k in enumerate((512, 530, 560)):
         want = template_ring_features(tpl, k, 512, plan)
         assert np.array_equal(got[i, :3].view(np.int64), want.view(np.int64))
+
+
+def _check_sat_rsat_fast(img, planes):
+    """check_planes without the brute-force pass, one kind at a time (the
+    reference-layout Rsat of a 4096^2 image is 0.5 GB per kind)."""
+    h, w = img.shape
+    for k in range(4):
+        assert np.array_equal(planes[k], O.build_sat(img, k)), f"SAT kind {k}"
+        rs = O.build_rsat(img, k)
+        ys, xs = np.mgrid[-1:h, 0:w]
+        assert np.array_equal(planes[4 + k][ys + 1, xs + 1], rs[xs + ys + 1, xs - ys + h - 1]), f"E kind {k}"
+        ys, xs = np.mgrid[-1:h - 1, -1:w]
+        assert np.array_equal(planes[8 + k][ys + 1, xs + 1], rs[xs + ys + 2, xs - ys + h - 1]), f"O kind {k}"
+        del rs
+
+
+@pytest.mark.parametrize("case", ["config1_2048sq", "random_4096x640", "bright_4096sq"])
+def test_config_scale_tables(cuda, case):
+    """K1/K2 at BASELINE scale, where the many-band carries and the u32
+    wraparound actually occur (at 4096^2 the SQUARED SAT reaches ~1.1e12 >
+    2^32): int64 planes == the oracle's Sat.cells / Rsat._h, and the 32-bit
+    planes == int64 mod 2^32 (device_planes)."""
+    if case == "config1_2048sq":
+        import workloads as WL
+
+        img = WL.make_cases(WL.CONFIGS[1])[0].image
+    elif case == "random_4096x640":
+        img = np.random.default_rng(4096).integers(0, 256, (640, 4096), dtype=np.uint8)
+    else:
+        img = np.random.default_rng(4097).integers(200, 256, (4096, 4096), dtype=np.uint8)
+    planes = device_planes(img, cuda)
+    if case == "bright_4096sq":
+        assert planes[3, -1, img.shape[1]] > 2 ** 32  # the SQUARED plane wraps mod 2^32
+    _check_sat_rsat_fast(img, planes)
