@@ -45,7 +45,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate positions x scales screened/sec"
 UNIT = "positions*scales/s"
-DTYPE = "u32 planes (cells mod 2^32; int64 planes for sizes whose sums need them) + fp32 cell estimates / fp64 fallback"
+DTYPE = ("u32 planes (cells mod 2^32) + u16 hi planes (cells mod 2^48 for sizes whose sums pass 32 bits) + u16 "
+         "coarse bit slices (stage 1); fp32 cell estimates with the fp64 sequence near a boundary")
 DEFAULT_CONFIG = 4
 BAND_CONFIGS = (2, 4)  # BASELINE.json: one large image, row bands with halo across GPUs
 POOL_ENGINES = int(os.environ.get("SS_POOL_ENGINES", "4"))  # engines screening a batch's images concurrently
@@ -528,7 +529,9 @@ def run_ours(args):
     # (32-bit cells, + int64 cells when a size needs them), the stage-1 list
     # written and read once (8 B entries), the mask bits written once
     plane_once = len(cases) * (int(eng.L.ss_tables32_bytes(eng.W, eng.rows)) +
-                               (int(eng.L.ss_tables_bytes(eng.W, eng.rows)) if eng.needs_int64(tp) else 0))
+                               (int(eng.L.ss_tables_bytes(eng.W, eng.rows)) if eng.built_int64 else 0) +
+                               (int(eng.L.ss_tables_hi16_bytes(eng.W, eng.rows)) if eng.built_hi16 else 0) +
+                               int(eng.L.ss_coarse_bytes(eng.W, eng.rows, len(eng.coarse_shifts))))
     compulsory = plane_once + 2 * 8.0 * stage[1] + positions / 8.0
     ctr = k3_counters(wl.name, len(cases))
     clock_mhz = clocks.summary().get("sm_mhz") or 1965.0
@@ -548,7 +551,8 @@ def run_ours(args):
         "k3_ms_per_step": screen_ms, "k3_share_of_step": screen_ms / (total_ms / args.steps),
         "compulsory": {"bytes_per_step": compulsory, "GBps": compulsory / k3_s / 1e9,
                        "frac": compulsory / k3_s / 1e9 / peak,
-                       "what": "each plane once per step + stage-1 list written and read (8 B entries) + mask bits"},
+                       "what": ("each plane stage 1 and the rings read (u32, hi16 / int64, coarse slices) once per "
+                                "step + stage-1 list written and read (8 B entries) + mask bits")},
         "dram": ({"bytes_per_step": ctr["dram_bytes_per_step"], "GBps": ctr["dram_bytes_per_step"] / k3_s / 1e9,
                   "frac": ctr["dram_bytes_per_step"] / k3_s / 1e9 / peak, "source": ctr["source"]}
                  if ctr else None),

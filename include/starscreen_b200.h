@@ -96,10 +96,19 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
  */
 int32_t ss_coarse_shift(int64_t count);
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse);
-/* ss_build_tables2 plus the coarse planes of h_shifts[0..n_coarse) (<= SS_MAX_COARSE). */
+/* Bytes of the 12 "hi16" planes: bits 32..47 of every exact cell (u16, same layout as the 32-bit planes). */
+size_t ss_tables_hi16_bytes(int64_t W, int64_t H);
+/*
+ * ss_build_tables2 plus, when non-NULL, the hi16 planes (with the 32-bit
+ * planes a cell is then known mod 2^48: every region sum below 2^48 is exact
+ * -- the fused rings' wide path, 6 bytes per cell instead of 8) and the
+ * coarse planes of h_shifts[0..n_coarse) (<= SS_MAX_COARSE).  d_hi16 needs
+ * d_planes32.
+ */
 int ss_build_tables3(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
-                     uint32_t* d_planes32, int64_t plane_pitch, uint16_t* d_coarse, int32_t n_coarse,
-                     const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes, void* stream);
+                     uint32_t* d_planes32, uint16_t* d_hi16, int64_t plane_pitch, uint16_t* d_coarse,
+                     int32_t n_coarse, const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* ── per-size membership sets (screening.py:100-178 FeatureSet) ──────── */
 /*
@@ -197,8 +206,12 @@ int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_
  * ss_screen_ladder with stage 1's coarse planes (ss_build_tables3): when
  * every fused size's ring-0 square and diamond have their ss_coarse_shift in
  * h_shifts[0..n_coarse), stage 1 reads the u16 bit slices (half the bytes)
- * and recomputes exact sums only near a membership boundary; same results.
- * d_coarse = NULL / n_coarse = 0 is ss_screen_ladder.
+ * and passes centres near a membership boundary on to the rings (which
+ * test ring 0's exact mean cell); same results.  d_hi16 (with d_planes32;
+ * ss_build_tables3): the fused rings of sizes beyond 32 bits read 32-bit +
+ * hi16 cells (mod 2^48) instead of the int64 planes, which may then be NULL
+ * (SS_EINVAL if a ring sum could reach 2^48, or if the fused path declines
+ * and the per-size fallback needs them).  All-NULL extras = ss_screen_ladder.
  */
 int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h, int64_t plane_pitch,
                       int64_t W, int64_t H, int64_t y_origin, int64_t y_begin, int64_t y_end, int32_t stride,
@@ -208,7 +221,7 @@ int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64
                       int64_t mask_pitch_words, int64_t size_stride_words, uint32_t* d_row_counts,
                       int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags, int32_t n_streams,
                       void* const* streams, void* const* d_workspaces, size_t workspace_bytes,
-                      const uint16_t* d_coarse, int32_t n_coarse, const int32_t* h_shifts);
+                      const uint16_t* d_coarse, int32_t n_coarse, const int32_t* h_shifts, const uint16_t* d_hi16);
 
 /* Workspace bytes for the fused ladder (flags bit 1) of n_sizes sizes over
  * `rows` decided rows: one row band of at most 4 GiB of candidate list, and

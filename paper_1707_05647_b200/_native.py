@@ -42,7 +42,9 @@ _SIGS = {
     "ss_screen_fits32": (ctypes.c_int, [c_i32, c_p, c_p]),
     "ss_coarse_shift": (c_i32, [c_i64]),
     "ss_coarse_bytes": (c_sz, [c_i64, c_i64, c_i32]),
-    "ss_build_tables3": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p, c_sz, c_p]),
+    "ss_tables_hi16_bytes": (c_sz, [c_i64, c_i64]),
+    "ss_build_tables3": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p, c_sz,
+                                        c_p]),
     "ss_keyset_blob": (ctypes.c_int, [c_p, c_p, c_i32, c_p, ctypes.POINTER(c_sz)]),
     "ss_screen_size": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32,
                                       c_i32, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),
@@ -56,7 +58,7 @@ _SIGS = {
                                         c_p, c_i32, c_i32, c_p, c_p, c_sz]),
     "ss_screen_ladder2": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32,
                                          c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_i64,
-                                         c_p, c_i64, c_p, c_i32, c_i32, c_p, c_p, c_sz, c_p, c_i32, c_p]),
+                                         c_p, c_i64, c_p, c_i32, c_i32, c_p, c_p, c_sz, c_p, c_i32, c_p, c_p]),
     "ss_ladder_keysets": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_p, c_d, c_d, c_d, c_p, c_i64, c_p, c_p, c_i64,
                                          c_p]),
     "ss_compact_workspace_bytes": (c_sz, [c_i64]),

@@ -53,6 +53,10 @@ struct BuildArgs {
     unsigned short* coarse;
     int n_coarse;
     int shift[SS_MAX_COARSE];
+    // bits 32..47 of every exact cell (nullable; 12 u16 planes, same layout
+    // as the 32-bit planes): with those, a cell is known mod 2^48 and every
+    // region sum of the 12 planes below 2^48 is exact (the rings' wide path)
+    unsigned short* hi16;
 };
 
 __device__ __forceinline__ long long shfl_down64(long long v, int d) {
@@ -143,6 +147,8 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
             }
             for (int p = 0; p < 3 * a.n_coarse; ++p)
                 *reinterpret_cast<uint2*>(a.coarse + p * a.plane_stride + c) = make_uint2(0, 0);
+            if (a.hi16)
+                for (int p = 0; p < 12; ++p) *reinterpret_cast<uint2*>(a.hi16 + p * a.plane_stride + c) = make_uint2(0, 0);
         }
     }
 
@@ -287,6 +293,15 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                                     make_uint2(lo, hi);
                             }
                         }
+                    }
+                    if (sizeof(V) == 8 && a.hi16) {
+                        auto hi = [](V v) { return (unsigned)(((unsigned long long)v >> 32) & 0xffffu); };
+                        *reinterpret_cast<uint2*>(a.hi16 + (0 * 4 + k) * a.plane_stride + off) =
+                            make_uint2(hi(S[k][0]) | hi(S[k][1]) << 16, hi(S[k][2]) | hi(S[k][3]) << 16);
+                        *reinterpret_cast<uint2*>(a.hi16 + (1 * 4 + k) * a.plane_stride + off) =
+                            make_uint2(hi(e0) | hi(e1) << 16, hi(e2) | hi(e3) << 16);
+                        *reinterpret_cast<uint2*>(a.hi16 + (2 * 4 + k) * a.plane_stride + off) =
+                            make_uint2(hi(o0) | hi(o1) << 16, hi(o2) | hi(o3) << 16);
                     }
                     if (a.planes32) {  // the same cells mod 2^32 (region sums are exact in 32 bits)
                         *reinterpret_cast<uint4*>(a.planes32 + (0 * 4 + k) * a.plane_stride + off) =
@@ -475,7 +490,7 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
 
 int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes, uint32_t* d_planes32,
                  int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream, uint16_t* d_coarse = nullptr,
-                 int n_coarse = 0, const int32_t* h_shifts = nullptr) {
+                 int n_coarse = 0, const int32_t* h_shifts = nullptr, uint16_t* d_hi16 = nullptr) {
     if (W < 1 || H < 1) { set_error("empty image"); return SS_EINVAL; }
     if (overflow_guard_fails(W, H)) {
         set_error("image %lldx%lld too large for 64-bit integral cells", (long long)W, (long long)H);
@@ -492,8 +507,9 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         return SS_EINVAL;
     }
     if (n_coarse < 0 || n_coarse > SS_MAX_COARSE || (n_coarse > 0 && (!d_coarse || !h_shifts)) ||
-        (reinterpret_cast<uintptr_t>(d_coarse) & 15)) {
-        set_error("bad coarse planes");
+        (reinterpret_cast<uintptr_t>(d_coarse) & 15) || (reinterpret_cast<uintptr_t>(d_hi16) & 15) ||
+        (d_hi16 && !d_planes32)) {
+        set_error("bad coarse / hi16 planes");
         return SS_EINVAL;
     }
     for (int i = 0; i < n_coarse; ++i)
@@ -507,7 +523,8 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
         return SS_EINVAL;
     }
     cudaStream_t s = as_stream(stream);
-    const int rb = pick_band_rows(W, H, d_planes != nullptr);
+    const bool exact = d_planes || d_hi16;  // int64 recurrences (cells beyond 32 bits are written)
+    const int rb = pick_band_rows(W, H, exact);
     BuildArgs a;
     a.img = d_img;
     a.W = W;
@@ -522,6 +539,7 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     a.state = reinterpret_cast<long long*>(static_cast<char*>(d_ws) + rowpre_bytes(W, H));
     a.slen = state_len(W, rb);
     a.n_chunks = n_chunks(W, rb);
+    a.hi16 = reinterpret_cast<unsigned short*>(d_hi16);
     a.coarse = reinterpret_cast<unsigned short*>(d_coarse);
     a.n_coarse = d_coarse ? n_coarse : 0;
     for (int i = 0; i < SS_MAX_COARSE; ++i) a.shift[i] = i < a.n_coarse ? (int)h_shifts[i] : 0;
@@ -530,8 +548,8 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
     note_launch();
     if (int e = check_launch("rowpre_kernel")) return e;
-    // exact int64 recurrences when the int64 planes are wanted, else mod 2^32
-    if (d_planes) {
+    // exact int64 recurrences when the int64 or hi16 planes are wanted, else mod 2^32
+    if (exact) {
         switch (rb) {
         case 63: return launch_bands<63, long long>(a, nbands, s);
         case 31: return launch_bands<31, long long>(a, nbands, s);
@@ -566,10 +584,12 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse) {
     return (size_t)3 * (size_t)n_coarse * (size_t)(H + 1) * ss::plane_pitch(W) * 2;
 }
+size_t ss_tables_hi16_bytes(int64_t W, int64_t H) { return (size_t)12 * (size_t)(H + 1) * ss::plane_pitch(W) * 2; }
 int ss_build_tables3(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
-                     uint32_t* d_planes32, int64_t plane_pitch, uint16_t* d_coarse, int32_t n_coarse,
-                     const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes, void* stream) {
+                     uint32_t* d_planes32, uint16_t* d_hi16, int64_t plane_pitch, uint16_t* d_coarse,
+                     int32_t n_coarse, const int32_t* h_shifts, void* d_workspace, size_t workspace_bytes,
+                     void* stream) {
     return ss::build_tables(d_img, W, H, img_pitch, d_planes, d_planes32, plane_pitch, d_workspace, workspace_bytes,
-                            stream, d_coarse, n_coarse, h_shifts);
+                            stream, d_coarse, n_coarse, h_shifts, d_hi16);
 }
 }

@@ -17,7 +17,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
                         uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
                         size_t ws_bytes, cudaStream_t s, const uint16_t* d_coarse, int n_coarse,
-                        const int32_t* h_shifts);
+                        const int32_t* h_shifts, const uint16_t* d_hi16);
 }  // namespace ss
 
 extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
@@ -30,7 +30,7 @@ extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_plan
                                  int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags,
                                  int32_t n_streams, void* const* streams, void* const* d_workspaces,
                                  size_t workspace_bytes, const uint16_t* d_coarse, int32_t n_coarse,
-                                 const int32_t* h_shifts);
+                                 const int32_t* h_shifts, const uint16_t* d_hi16);
 
 extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
                                 int64_t plane_pitch, int64_t W, int64_t H, int64_t y_origin, int64_t y_begin,
@@ -46,7 +46,7 @@ extern "C" int ss_screen_ladder(const int64_t* d_planes, const uint32_t* d_plane
                              h_m, h_n_rings, h_ring_n, h_ring_d, d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad,
                              d_masks, mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,
                              d_stage_counts, flags, n_streams, streams, d_workspaces, workspace_bytes, nullptr, 0,
-                             nullptr);
+                             nullptr, nullptr);
 }
 
 extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64_t w, int64_t h,
@@ -59,7 +59,7 @@ extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_plan
                                  int64_t row_counts_stride, unsigned long long* d_stage_counts, int32_t flags,
                                  int32_t n_streams, void* const* streams, void* const* d_workspaces,
                                  size_t workspace_bytes, const uint16_t* d_coarse, int32_t n_coarse,
-                                 const int32_t* h_shifts) {
+                                 const int32_t* h_shifts, const uint16_t* d_hi16) {
     if (n_sizes < 0 || n_sizes > SS_MAX_SIZES || !h_m || !h_n_rings || !h_ring_n || !h_ring_d || !h_blob_off ||
         n_streams < 1 || !streams || !d_workspaces || (n_sizes > 0 && (!d_masks || !d_row_counts))) {
         ss::set_error("bad ladder arguments");
@@ -92,7 +92,7 @@ extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_plan
             const std::vector<int>& ks = g == 0 ? g32 : g64;
             if (ks.empty()) continue;
             const void* planes = g == 0 ? static_cast<const void*>(d_planes32) : static_cast<const void*>(d_planes);
-            if (!planes) {
+            if (!planes && !(g == 1 && d_hi16 && d_planes32)) {
                 ss::set_error("ladder needs the int64 planes (ring sums exceed 32 bits)");
                 return SS_EINVAL;
             }
@@ -102,8 +102,12 @@ extern "C" int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_plan
                                             d_blobs, h_blobs, h_blob_off, q_mean, q_std, q_grad, d_masks,
                                             mask_pitch_words, size_stride_words, d_row_counts, row_counts_stride,
                                             d_stage_counts, d_workspaces[0], workspace_bytes, ss::as_stream(st),
-                                            d_coarse, n_coarse, h_shifts);
+                                            d_coarse, n_coarse, h_shifts, d_hi16);
             if (e == ss::SS_DECLINED) {
+                if (g == 1 && !d_planes) {
+                    ss::set_error("the per-size screen of sizes beyond 32 bits needs the int64 planes");
+                    return SS_EINVAL;
+                }
                 for (int k : ks) {
                     const int32_t* rn = h_ring_n + (size_t)k * SS_MAX_RINGS;
                     const int32_t* rd = h_ring_d + (size_t)k * SS_MAX_RINGS;

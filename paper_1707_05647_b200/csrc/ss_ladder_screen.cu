@@ -43,12 +43,15 @@ struct SizeDev {
     int c_sq, c_di;       // coarse stage 1: plane-set index of ring 0's square / diamond sums
     float fa_c, fb_c;     // coarse stage 1: 2^shift / (2 count q_mean) of the square / diamond
     float band_c;         // coarse stage 1: bound on |t_coarse - t| from the bit slices (K3L)
-    int pad;
+    float t0_c;           // coarse stage 1: 1/2 - fa_c - fb_c (estimate from the sums biased by one)
+    int contig;           // ring 0's mean projection is one run of cells [B0, B1) (or empty): w* below apply
+    float w0lo, w0hi, w1lo, w1hi;  // t within [w0lo, w0hi] of B0 or [w1lo, w1hi] of B1: undecided; else pass iff w0hi < t < w1lo
 };
 
 struct FusedArgs {
     const void* planes;  // 12 planes of T
-    const unsigned* planes32;  // the 32-bit planes (coarse stage 1's exact fallback)
+    const unsigned* planes32;  // the 32-bit planes
+    const unsigned short* hi16;  // bits 32..47 of the cells (the rings' wide48 path)
     long long pitch, ps;
     int W, H, y_origin, y_begin, y_end, stride;  // [y_begin, y_end): rows decided by this pass
     int mask_y0;
@@ -95,7 +98,34 @@ constexpr int CAND_BUF = 64;  // per-warp staging of list entries (flushed 32 at
 struct TileMapF {
     int n_tx, n_ty, strip, n_sizes;
     long long n_tiles;  // n_tx * n_ty * n_sizes
+    // float reciprocals of the divisors of tile_coords_fast (n_tiles < 2^24)
+    float r_per_strip, r_strip, r_last, r_span, r_span_last;
 };
+
+// q = n / d for n < 2^24 from a float reciprocal rd ~ 1/d, corrected to exact.
+__device__ __forceinline__ unsigned fdiv24(unsigned n, unsigned d, float rd) {
+    unsigned q = __float2uint_rz(__uint2float_rn(n) * rd);
+    const int r = (int)(n - q * d);
+    if (r < 0) --q;
+    else if (r >= (int)d) ++q;
+    return q;
+}
+// tile_coords_f without integer divisions (n_tiles < 2^24, checked on the host)
+__device__ __forceinline__ void tile_coords_fast(const TileMapF& t, unsigned i, int& tx, int& ty, int& s) {
+    const unsigned per_strip = (unsigned)t.strip * (unsigned)t.n_ty * (unsigned)t.n_sizes;
+    const unsigned st = fdiv24(i, per_strip, t.r_per_strip);
+    const int s0 = (int)(st * (unsigned)t.strip);
+    const bool last = s0 + t.strip > t.n_tx;
+    const unsigned width = last ? (unsigned)(t.n_tx - s0) : (unsigned)t.strip;
+    const unsigned r = i - st * per_strip;
+    const unsigned span = width * (unsigned)t.n_sizes;
+    const unsigned q = fdiv24(r, span, last ? t.r_span_last : t.r_span);
+    const unsigned rem = r - q * span;
+    const unsigned sz = fdiv24(rem, width, last ? t.r_last : t.r_strip);
+    ty = (int)q;
+    s = (int)sz;
+    tx = s0 + (int)(rem - sz * width);
+}
 
 // Fused stage-1 tile geometry: 16 rows x 32*CPW columns; 32-bit planes take
 // 128-column tiles (four independent centres per lane: the chains overlap),
@@ -393,17 +423,34 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     }
 }
 
-// Coarse stage-1 tiles: 16 rows x 224 columns of u16 bit slices; boxes
-// 16 x 248 (496-byte rows; measured on B200 with tools/tma_probe: 16 x 248 /
-// 16 x 256 u16 boxes stream at ~40 B/clk/SM, 16 x 192-200 at ~16, u32 16 x 196
-// at ~32), 3 stages of 62 KB.
-struct GeoC {
-    static constexpr int CPW = 7;
-    static constexpr int TX = 32 * CPW;
-    static constexpr int STAGES = 3;
+// Coarse stage-1 tiles: 16 rows x TX columns of u16 bit slices, CW consumer
+// warps (CW / 16 per tile row, CPW 32-column chunks each).  Boxes are
+// 16 x (TX + 8): measured on B200 with tools/tma_probe, 16 x 248-256 u16 boxes
+// stream at ~40 B/clk/SM, 16 x 192-200 at ~16, u32 16 x 196 at ~32.
+#ifndef COARSE_WARPS
+#define COARSE_WARPS 16
+#endif
+#ifndef COARSE_CPW
+#define COARSE_CPW 7
+#endif
+#ifndef COARSE_STAGES
+#define COARSE_STAGES 3
+#endif
+constexpr int S1_MAX_WARPS = 32;  // consumer warps a stage-1 kernel may have (a CTA holds <= 32 warps)
+template <int CW_, int CPW_, int STAGES_> struct GeoCT {
+    static constexpr int CW = CW_;
+    static constexpr int WPR = CW / TY;  // warps per tile row
+    static_assert(WPR * TY == CW && CW <= S1_MAX_WARPS, "consumer warps tile the rows");
+    static constexpr int CPW = CPW_;
+    static constexpr int TX = WPR * 32 * CPW;
+    static constexpr int STAGES = STAGES_;
     static constexpr int ALIGN = 8;  // 16-byte aligned box starts
-    static constexpr int BW = 248;
-    static_assert(BW >= TX + ALIGN - 1, "box must cover the tile at any alignment");
+#ifdef COARSE_BW
+    static constexpr int BW = COARSE_BW;
+#else
+    static constexpr int BW = TX + ALIGN;
+#endif
+    static_assert(BW <= 256 && BW >= TX + ALIGN - 1, "box must cover the tile at any alignment (TMA box <= 256)");
     static constexpr int BOX_ELEMS = BW * TY;
     static constexpr int BOX_BYTES = BOX_ELEMS * 2;
     static_assert(BOX_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
@@ -411,6 +458,7 @@ struct GeoC {
     __device__ static int floor_al(int c) { return c & ~(ALIGN - 1); }
     __device__ static int rem(int c) { return c & (ALIGN - 1); }
 };
+using GeoC = GeoCT<COARSE_WARPS, COARSE_CPW, COARSE_STAGES>;
 
 struct __align__(16) TileConstC {
     int tx, ty, sz, ylo;
@@ -420,7 +468,10 @@ struct __align__(16) TileConstC {
     int cm_lo;
     int cm_n;
     unsigned win_lo, win_hi;
-    int pad;
+    int contig;  // SizeDev::contig and its windows
+    float w0lo, w0hi, w1lo, w1hi;
+    float t0;    // 1/2 - fa - fb: the estimate from the biased sums J = I + 1
+    int pad[2];
 };
 
 // Stage 1 of every fused size from the coarse planes.  A region sum S of
@@ -430,21 +481,25 @@ struct __align__(16) TileConstC {
 // t = I_sq fa + I_di fb + 1/2 is within band (+ the fp32 terms of mean_cell)
 // of the reference's t.  A centre is decided from the estimate unless t lies
 // within that bound of a cell boundary whose two cells differ in ring-0
-// membership; those lanes recompute the exact sums from the 32-bit planes
-// (mean_cell: fp32 estimate, fp64 sequence near a boundary).  Same decisions
-// as ladder_stage1_kernel; half the TMA bytes per centre.
-__global__ void __launch_bounds__((WARPS + 1) * 32, 1)
+// membership; those centres are passed on as candidates and the rings
+// kernel's level 0 decides them from the exact sums (eval_ring_fast tests
+// ring 0's mean cell again).  The survivors equal ladder_stage1_kernel's; the
+// candidate list is a (slightly larger) superset; half the TMA bytes per
+// centre.
+__global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     ladder_stage1_coarse_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ CoarseMaps maps,
                                 const TileMapF tm, int parts, int reserve, int2* list_base, long long part_cap,
                                 unsigned* list_ctr, unsigned* tile_ctr_base) {
     using G = GeoC;
-    constexpr int STAGES = G::STAGES, CPW = G::CPW;
+    constexpr int STAGES = G::STAGES, CPW = G::CPW, CW = G::CW;
     extern __shared__ __align__(128) unsigned char dsmem[];
     unsigned char* stage_buf = dsmem;
     unsigned* sbits = reinterpret_cast<unsigned*>(dsmem + STAGES * G::STAGE_BYTES);
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-    __shared__ TileConstC tile_info[STAGES];
-    __shared__ int2 cand_buf[WARPS][CAND_BUF];
+    __shared__ int4 slot[STAGES];               // the tile in each stage: (tx, ty, size, -)
+    __shared__ TileConstC size_info[FMAX_SIZES];  // per-size constants, filled once
+    __shared__ int4 size_tma[FMAX_SIZES];         // per-size (n, d, square plane set, diamond plane set)
+    __shared__ int2 cand_buf[CW][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
         for (int s = 0; s < a.n_sizes; ++s) {
@@ -457,37 +512,18 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], WARPS);
+            mbar_init(&empty_bar[s], CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int part = (int)(blockIdx.x % parts);
-
-    if (warp == WARPS) {
-        if (lane == 0) {
-            const int tc = (int)(blockIdx.x % TILE_CTRS);
-            unsigned* tile_ctr = tile_ctr_base + tc * CTR_STRIDE;
-            unsigned t_next = atom_add_ahead(tile_ctr, 1u);
-            for (int it = 0;; ++it) {
-                const int s = it % STAGES;
-                const long long t = (long long)t_next * TILE_CTRS + tc;
-                if (t < tm.n_tiles) t_next = atom_add_ahead(tile_ctr, 1u);
-                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
-                if (t >= tm.n_tiles) {
-                    tile_info[s].tx = -1;
-                    mbar_arrive(&full_bar[s]);
-                    break;
-                }
-                int tx, ty, sz;
-                tile_coords_f(tm, t, tx, ty, sz);
-                const SizeDev& S = a.size[sz];
-                const RingDev& R0 = a.ring[S.ring0];
-                {
-                    TileConstC& tcst = tile_info[s];
-                    tcst.tx = tx;
-                    tcst.ty = ty;
+    for (int sz = threadIdx.x; sz < a.n_sizes; sz += blockDim.x) {
+        const SizeDev& S = a.size[sz];
+        const RingDev& R0 = a.ring[S.ring0];
+        {
+                    TileConstC& tcst = size_info[sz];
+                    tcst.tx = 0;
+                    tcst.ty = 0;
                     tcst.sz = sz;
                     tcst.ylo = S.lo;
                     tcst.yhi = a.H - 1 - S.hi;
@@ -509,23 +545,57 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                     tcst.band = S.band_c;
                     tcst.cm_lo = R0.cm_lo;
                     tcst.cm_n = R0.cm_n;
+                    tcst.contig = S.contig;
+                    tcst.w0lo = S.w0lo;
+                    tcst.w0hi = S.w0hi;
+                    tcst.w1lo = S.w1lo;
+                    tcst.w1hi = S.w1hi;
+                    tcst.t0 = S.t0_c;
+        }
+        size_tma[sz] = make_int4(R0.n, R0.d, S.c_sq, S.c_di);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = (int)(blockIdx.x % parts);
+
+    if (warp == CW) {
+        if (lane < NBOX) {
+            // tiles are uniform work: static round robin over the persistent
+            // CTAs (strip-major order kept: the tiles in flight stay contiguous).
+            // Lane b issues box b of every tile (measured with tools/tma_probe:
+            // 8 issuing lanes stream these u16 boxes at ~53 B/clk/SM, one lane
+            // at ~34).
+            const bool fast = tm.n_tiles < (1LL << 24);
+            const unsigned pmask = (1u << NBOX) - 1u;
+            for (int it = 0;; ++it) {
+                const int s = it % STAGES;
+                const long long t = (long long)blockIdx.x + (long long)it * gridDim.x;
+                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+                if (t >= tm.n_tiles) {
+                    if (lane == 0) {
+                        slot[s] = make_int4(-1, 0, 0, 0);
+                        mbar_arrive(&full_bar[s]);
+                    }
+                    break;
                 }
+                int tx, ty, sz;
+                if (fast) tile_coords_fast(tm, (unsigned)t, tx, ty, sz);
+                else tile_coords_f(tm, t, tx, ty, sz);
+                if (lane == 0) {
+                    slot[s] = make_int4(tx, ty, sz, 0);  // published by the arrive (complete_tx) below
+                    mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
+                }
+                __syncwarp(pmask);  // expect_tx before any of the boxes lands
+                const int4 st = size_tma[sz];
+                const int n = st.x, d = st.y, b = lane;
+                // box b: SAT (+-n+1 columns, +-n+1 rows), E (+1, d+1 / -d), O (-d / d+1, 0)
+                const int xo = b < 4 ? ((b & 1) ? 1 - n : n + 1) : (b < 6 ? 1 : (b == 6 ? -d : d + 1));
+                const int yo = b < 4 ? ((b & 2) ? 1 - n : n + 1) : (b == 4 ? d + 1 : (b == 5 ? -d : 0));
+                const CUtensorMap* m = b < 4 ? &maps.sat[st.z] : (b < 6 ? &maps.e[st.w] : &maps.o[st.w]);
                 const int x0 = tx * G::TX;
                 const int cy0 = a.y_begin + ty * TY - a.y_origin;
-                unsigned char* dst = stage_buf + s * G::STAGE_BYTES;
-                mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
-                const int n = R0.n, d = R0.d;
-                const CUtensorMap* msat = &maps.sat[S.c_sq];
-                const CUtensorMap* me = &maps.e[S.c_di];
-                const CUtensorMap* mo = &maps.o[S.c_di];
-                tma_load_2d(dst + 0 * G::BOX_BYTES, msat, G::floor_al(x0 + n + 1), cy0 + n + 1, &full_bar[s]);
-                tma_load_2d(dst + 1 * G::BOX_BYTES, msat, G::floor_al(x0 - n + 1), cy0 + n + 1, &full_bar[s]);
-                tma_load_2d(dst + 2 * G::BOX_BYTES, msat, G::floor_al(x0 + n + 1), cy0 - n + 1, &full_bar[s]);
-                tma_load_2d(dst + 3 * G::BOX_BYTES, msat, G::floor_al(x0 - n + 1), cy0 - n + 1, &full_bar[s]);
-                tma_load_2d(dst + 4 * G::BOX_BYTES, me, G::floor_al(x0 + 1), cy0 + d + 1, &full_bar[s]);
-                tma_load_2d(dst + 5 * G::BOX_BYTES, me, G::floor_al(x0 + 1), cy0 - d, &full_bar[s]);
-                tma_load_2d(dst + 6 * G::BOX_BYTES, mo, G::floor_al(x0 - d), cy0, &full_bar[s]);
-                tma_load_2d(dst + 7 * G::BOX_BYTES, mo, G::floor_al(x0 + d + 1), cy0, &full_bar[s]);
+                tma_load_2d(stage_buf + s * G::STAGE_BYTES + b * G::BOX_BYTES, m, G::floor_al(x0 + xo), cy0 + yo,
+                            &full_bar[s]);
             }
         }
         return;
@@ -544,28 +614,35 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
-        const TileConstC tc = tile_info[s];
-        if (tc.tx < 0) break;
-        const int tx = tc.tx, ty = tc.ty, sz = tc.sz;
-        const int y = a.y_begin + ty * TY + warp;
+        const int4 sl = slot[s];
+        if (sl.x < 0) break;
+        const int tx = sl.x, ty = sl.y, sz = sl.z;
+        const TileConstC& tc = size_info[sz];
+        const int row = warp / G::WPR, half = warp - row * G::WPR;  // tile row, column block of this warp
+        const int y = a.y_begin + ty * TY + row;
         const bool row_int = y < a.y_end && y >= tc.ylo && y <= tc.yhi && (unit_stride || (y % a.stride) == 0);
-        int iq[CPW], id[CPW];  // coarse sums: I with |S - I 2^k| < 2^(k+1)
+        // coarse sums biased by one: J = I + 1 in [0, 2^16 - 2], where
+        // |S - I 2^k| < 2^(k+1) (the -1 is folded into the estimate's constant)
+        unsigned jq[CPW], jd[CPW];
         if (row_int) {
             const int qr = tc.qr, ql = tc.ql, pe = 1, po0 = tc.po0, po1 = tc.po1;
             const unsigned short* box =
-                reinterpret_cast<const unsigned short*>(stage_buf + s * G::STAGE_BYTES) + warp * G::BW + lane;
+                reinterpret_cast<const unsigned short*>(stage_buf + s * G::STAGE_BYTES) + row * G::BW + half * 32 * CPW +
+                lane;
 #pragma unroll
             for (int c = 0; c < CPW; ++c) {
                 const unsigned short* b = box + 32 * c;
                 constexpr int E = G::BOX_ELEMS;
-                const unsigned vq = (unsigned)b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql];
-                const unsigned vd = (unsigned)b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe];
-                iq[c] = (int)((vq + 1u) & 0xffffu) - 1;  // I in [-1, 2^16 - 3]
-                id[c] = (int)((vd + 1u) & 0xffffu) - 1;
+                jq[c] = ((unsigned)b[0 * E + qr] - b[1 * E + ql] - b[2 * E + qr] + b[3 * E + ql] + 1u) & 0xffffu;
+                jd[c] = ((unsigned)b[4 * E + pe] - b[6 * E + po0] - b[7 * E + po1] + b[5 * E + pe] + 1u) & 0xffffu;
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
+#ifdef COARSE_NOCOMPUTE  // experiment: the producer / TMA rate alone
+        if (row_int && jq[0] == 0x12345u) list0[0] = make_int2((int)jd[1], 0);
+        continue;
+#endif
         if (!row_int) continue;
         const int cm_lo = tc.cm_lo;
         auto member = [&](int cm) -> bool {
@@ -581,23 +658,35 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
             const RingDev& R0 = a.ring[a.size[sz].ring0];
             return bsearch_eq(a.blob + R0.off_m, R0.n_m, cm);
         };
-        const int xt = tx * G::TX;
+        const int xt = tx * G::TX + half * 32 * CPW;  // this warp's first column
         unsigned pm = 0, amb = 0;
+        if (tc.contig) {
+            // one run of member cells [B0, B1): a centre is a candidate unless t
+            // lies below B0 or above B1 by more than the error bound -- those
+            // within the bound of B0 or B1 are decided by the rings kernel
+            // (windows precomputed on the host; t0 = 1/2 - fa - fb)
 #pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-            const float tf = fmaf((float)iq[c], tc.fa, fmaf((float)id[c], tc.fb, 0.5f));
-            const float dl = tc.band + fmaf(tf, 4e-6f, 4e-6f);
-            const float fl = floorf(tf);
-            const int cm = (int)fl;
-            const float fr = tf - fl;
-            const bool p = member(cm);
-            pm |= (unsigned)p << c;
-            if (fr < dl || fr > 1.0f - dl) {  // the true cell may be the neighbour
-                if (member(fr < dl ? cm - 1 : cm + 1) != p) amb |= 1u << c;
+            for (int c = 0; c < CPW; ++c) {
+                const float tf = fmaf((float)jq[c], tc.fa, fmaf((float)jd[c], tc.fb, tc.t0));
+                pm |= (unsigned)(tf >= tc.w0lo && tf <= tc.w1hi) << c;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const float tf = fmaf((float)jq[c], tc.fa, fmaf((float)jd[c], tc.fb, tc.t0));
+                const float dl = tc.band + fmaf(tf, 4e-6f, 4e-6f);
+                const float fl = floorf(tf);
+                const int cm = (int)fl;
+                const float fr = tf - fl;
+                const bool p = member(cm);
+                pm |= (unsigned)p << c;
+                if (fr < dl || fr > 1.0f - dl) {  // the true cell may be the neighbour
+                    if (member(fr < dl ? cm - 1 : cm + 1) != p) amb |= 1u << c;
+                }
             }
         }
         const int xlo = tc.xlo, xhi = tc.xhi;
-        const bool full = unit_stride && xt >= xlo && xt + G::TX - 1 <= xhi;
+        const bool full = unit_stride && xt >= xlo && xt + 32 * CPW - 1 <= xhi;
         if (!full) {
 #pragma unroll
             for (int c = 0; c < CPW; ++c) {
@@ -612,22 +701,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
         } else if (a.stage_counts) {
             n_int += 32 * CPW;
         }
-        if (__any_sync(FULL, amb != 0u)) {
-            // exact PLAIN sums from the 32-bit planes (ambiguous interior lanes only)
-            const RingDev& R0 = a.ring[a.size[sz].ring0];
-            const unsigned* rowp = a.planes32 + (long long)(y - a.y_origin) * a.pitch;
-#pragma unroll 1
-            for (int c = 0; c < CPW; ++c) {
-                if (!((amb >> c) & 1u)) continue;
-                const unsigned* q = rowp + xt + 32 * c + lane;
-                const unsigned* e = q + 4 * a.ps;
-                const unsigned* o = q + 8 * a.ps;
-                const unsigned sq = __ldg(q + R0.sa) - __ldg(q + R0.sb) - __ldg(q + R0.sc) + __ldg(q + R0.sd);
-                const unsigned sd = __ldg(e + R0.ea) - __ldg(o + R0.ob) - __ldg(o + R0.oc) + __ldg(e + R0.ed);
-                const bool p = member(mean_cell(a, R0, sq, sd));
-                pm = (pm & ~(1u << c)) | ((unsigned)p << c);
-            }
-        }
+        // undecided centres go to the rings kernel as candidates: its level 0
+        // recomputes ring 0's exact mean cell and tests it (eval_ring_fast)
+        pm |= amb;
         const int tag = y | (sz << TAG_SHIFT);
         if (!__any_sync(FULL, pm != 0u)) continue;
 #pragma unroll
@@ -882,7 +958,8 @@ int parts_for(int64_t W, int64_t rows, int n_sizes) {
 }
 long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int parts) {
     const long long ctas = (2LL * sms + parts - 1) / parts;
-    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * (TXMAX * TY) + ctas * WARPS * 2 * RESERVE_MAX;
+    constexpr int s1_warps = WARPS > GeoC::CW ? WARPS : GeoC::CW;  // list reservation slack per stage-1 warp
+    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * (TXMAX * TY) + ctas * s1_warps * 2 * RESERVE_MAX;
 }
 size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms, size_t entry = sizeof(FEntry<unsigned>)) {
     const int parts = parts_for(W, rows, n_sizes);
@@ -988,7 +1065,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                         double qs, double qg, uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride,
                         uint32_t* d_row_counts, int64_t rc_stride, unsigned long long* d_stage_counts, void* d_ws,
                         size_t ws_bytes, cudaStream_t s, const uint16_t* d_coarse, int n_coarse,
-                        const int32_t* h_shifts) {
+                        const int32_t* h_shifts, const uint16_t* d_hi16) {
     if (n < 1 || n > FMAX_SIZES || H >= (1LL << TAG_SHIFT) || W > (1 << 30) || stride < 1) return SS_DECLINED;
     if (pitch != plane_pitch(W)) { set_error("plane pitch mismatch"); return SS_EINVAL; }
     if (mask_pitch < (W + 31) / 32) { set_error("mask pitch too small"); return SS_EINVAL; }
@@ -1002,6 +1079,14 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     FusedArgs& a = *reinterpret_cast<FusedArgs*>(hostbuf.data());
     a.planes = planes;
     a.planes32 = static_cast<const unsigned*>(eb == 4 ? planes : planes32_s1);
+    a.hi16 = reinterpret_cast<const unsigned short*>(d_hi16);
+    // int64 group without int64 planes: the rings read 32-bit + hi16 cells
+    // (mod 2^48), valid while every ring sum stays below 2^48
+    const bool wide = eb == 8 && !planes;
+    if (wide && (!d_hi16 || !planes32_s1)) {
+        set_error("ladder needs the int64 planes or the 32-bit + hi16 planes");
+        return SS_EINVAL;
+    }
     a.pitch = pitch;
     a.ps = (h + 1) * pitch;
     if (3 * a.ps >= (long long)INT32_MAX) return SS_DECLINED;  // PlanePtrs: 32-bit kind offsets
@@ -1056,6 +1141,15 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                                   h_ring_d[(size_t)k * SS_MAX_RINGS + r], m, pitch, qm, hb + 1 + SS_BLOB_HDR * r,
                                   h_blob_off[k], bm_words, SMEM_BITMAP_WORDS))
                 return e;
+        if (wide)
+            for (int r = 0; r < nr; ++r) {
+                const long long rn = h_ring_n[(size_t)k * SS_MAX_RINGS + r], rd = h_ring_d[(size_t)k * SS_MAX_RINGS + r];
+                const long long cnt = std::max(4 * rn * rn, 2 * rd * rd + 2 * rd + 1);
+                if ((double)255 * (double)cnt * (double)(std::max(W, H) + 1) >= 281474976710656.0) {
+                    set_error("ring sums reach 2^48: the int64 planes are needed");
+                    return SS_EINVAL;
+                }
+            }
         // stage 1's copy of ring 0's mean-projection bits
         const int64_t* hd = hb + 1;
         S.bm1 = -1;
@@ -1097,6 +1191,25 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         S.fa_c = (float)(std::ldexp(1.0, kq) / (2.0 * (double)cq * qm));
         S.fb_c = (float)(std::ldexp(1.0, kd) / (2.0 * (double)cd * qm));
         S.band_c = (float)(band * (1.0 + 1e-5));
+        S.t0_c = (float)(0.5 - (double)S.fa_c - (double)S.fb_c);
+        // ring 0's mean projection as one run of cells [B0, B1) when its
+        // keys are consecutive (n_m == cm_n) or empty; windows = B -+ the
+        // estimate's bound (band + mean_cell's fp32 term), rounded outwards
+        const int64_t* hd = h_blobs + h_blob_off[ks[j]] + 1;
+        const int64_t n_m = hd[1], cm_lo = hd[6], cm_n = hd[7];
+        S.contig = 0;
+        if (n_m == 0 || n_m == cm_n) {
+            const double B0 = n_m ? (double)cm_lo : 1e30, B1 = n_m ? (double)(cm_lo + cm_n) : 1e30;
+            auto dn = [](double v) { return std::nextafter((float)v, -INFINITY); };
+            auto up = [](double v) { return std::nextafter((float)v, INFINITY); };
+            const double d0 = (band + 4e-6 * (B0 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7;
+            const double d1 = (band + 4e-6 * (B1 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7;
+            S.contig = 1;
+            S.w0lo = dn(B0 - d0);
+            S.w0hi = up(B0 + d0);
+            S.w1lo = dn(B1 - d1);
+            S.w1hi = up(B1 + d1);
+        }
     }
     a.n_rings = n_rings;
     a.bm_words = bm_words;
@@ -1148,7 +1261,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         const size_t s1_smem = (size_t)(coarse ? GeoC::STAGES * GeoC::STAGE_BYTES : G::STAGES * G::STAGE_BYTES) +
                                (size_t)std::max(bm1, 1) * 4;
         const void* s1_fn = coarse ? reinterpret_cast<const void*>(s1c) : reinterpret_cast<const void*>(s1);
-        const int s1_per_sm = std::min(occupancy(s1_fn, (WARPS + 1) * 32, s1_smem), 2);
+        const int s1_threads = ((coarse ? GeoC::CW : WARPS) + 1) * 32;
+        const int s1_per_sm = std::min(occupancy(s1_fn, s1_threads, s1_smem), 2);
         const size_t rk_smem = (size_t)n_rings * sizeof(RingDev) + (size_t)n * sizeof(SizeSm) +
                                (size_t)((bm_words + 1) & ~1) * 4 + (size_t)RK_WARPS * a.max_levels * QCAP * sizeof(int2);
         const int rk_per_sm = std::max(occupancy(reinterpret_cast<const void*>(rk), RK_WARPS * 32, rk_smem), 1);
@@ -1177,6 +1291,12 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                         break;
                     }
                 }
+                const int last_w = tm.n_tx - (tm.n_tx - 1) / tm.strip * tm.strip;
+                tm.r_per_strip = (float)(1.0 / ((double)tm.strip * tm.n_ty * n));
+                tm.r_strip = (float)(1.0 / tm.strip);
+                tm.r_last = (float)(1.0 / last_w);
+                tm.r_span = (float)(1.0 / ((double)tm.strip * n));
+                tm.r_span_last = (float)(1.0 / ((double)last_w * n));
             }
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
@@ -1192,7 +1312,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                                                        (long long)TILE_CTRS);
             if (coarse) {
                 if constexpr (std::is_same<E, int2>::value) {
-                    s1c<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, cmaps, tm, parts,
+                    s1c<<<(unsigned)grid, s1_threads, s1_smem, s>>>(a, cmaps, tm, parts,
                                                                           parts > 1 ? RESERVE_LARGE : RESERVE_SMALL,
                                                                           list, part_cap, list_ctr, tile_ctr);
                 }
@@ -1211,6 +1331,13 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         return SS_OK;
     };
     if (eb == 4) return launch((unsigned)0, (unsigned)0);
+    if (wide) {
+        if (!s1_u32) {
+            set_error("ring-0 PLAIN sums reach 2^32: the int64 planes are needed");
+            return SS_EINVAL;
+        }
+        return launch((wide48)0, (unsigned)0);
+    }
     return s1_u32 ? launch((long long)0, (unsigned)0) : launch((long long)0, (long long)0);
 }
 

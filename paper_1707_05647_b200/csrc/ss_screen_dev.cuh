@@ -15,6 +15,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <set>
@@ -156,6 +157,46 @@ __device__ __forceinline__ long long ldg_at(const long long* p, int off) {
         : "=l"(v) : "l"(p), "r"(off));
     return v;
 }
+// Wide cells: the 32-bit planes plus the hi16 planes (bits 32..47) give every
+// cell mod 2^48; region sums of the rings' sizes stay below 2^48 (checked on
+// the host), so A - B - C + D mod 2^48 is the exact sum.  6 bytes per cell
+// instead of the int64 planes' 8.
+using wide48 = unsigned long long;
+constexpr unsigned long long M48 = (1ull << 48) - 1;
+template <> struct PlanePtrs<wide48> {
+    const unsigned *q, *e, *o;
+    const unsigned short *qh, *eh, *oh;
+    int ks;
+};
+template <typename T, class A>
+__device__ __forceinline__ typename std::enable_if<std::is_same<T, wide48>::value, PlanePtrs<wide48>>::type
+plane_ptrs_w(const A& a, int cy, int x) {
+    const long long o = (long long)cy * a.pitch + x;
+    const unsigned* p = a.planes32 + o;
+    const unsigned short* h = a.hi16 + o;
+    return PlanePtrs<wide48>{p, p + 4 * a.ps, p + 8 * a.ps, h, h + 4 * a.ps, h + 8 * a.ps, (int)a.ps};
+}
+__device__ __forceinline__ unsigned ldg_u16_at(const unsigned short* p, int off) {
+    unsigned short v;
+    asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 2, %1;\n\tld.global.nc.u16 %0, [ad];\n\t}"
+        : "=h"(v) : "l"(p), "r"(off));
+    return v;
+}
+__device__ __forceinline__ wide48 cell48(const unsigned* lo, const unsigned short* hi, int off) {
+    return (wide48)ldg_at(lo, off) | ((wide48)ldg_u16_at(hi, off) << 32);
+}
+__device__ __forceinline__ void load_corners(const PlanePtrs<wide48>& P, const RingDev& R, int kind,
+                                             Corners<wide48>& c) {
+    const int ko = kind * P.ks;
+    c.q[0] = cell48(P.q, P.qh, ko + R.sa);
+    c.q[1] = cell48(P.q, P.qh, ko + R.sb);
+    c.q[2] = cell48(P.q, P.qh, ko + R.sc);
+    c.q[3] = cell48(P.q, P.qh, ko + R.sd);
+    c.e[0] = cell48(P.e, P.eh, ko + R.ea);
+    c.e[1] = cell48(P.e, P.eh, ko + R.ed);
+    c.o[0] = cell48(P.o, P.oh, ko + R.ob);
+    c.o[1] = cell48(P.o, P.oh, ko + R.oc);
+}
 template <typename T>
 __device__ __forceinline__ void load_corners(const PlanePtrs<T>& P, const RingDev& R, int kind, Corners<T>& c) {
     const int ko = kind * P.ks;
@@ -174,6 +215,7 @@ template <typename T> __device__ __forceinline__ T di_of(const Corners<T>& c) { 
 // exact non-negative region sum (PLAIN, SQUARED)
 __device__ __forceinline__ long long unsigned_sum(long long v) { return v; }
 __device__ __forceinline__ long long unsigned_sum(unsigned v) { return (long long)v; }
+__device__ __forceinline__ long long unsigned_sum(wide48 v) { return (long long)(v & M48); }
 // exact weighted region sum with weight (c + 1) at the centre column/row c
 __device__ __forceinline__ long long weighted_sum(long long v, long long, long long) { return v; }
 __device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long long s1) {
@@ -290,6 +332,9 @@ __device__ __forceinline__ long long centred(unsigned v, int c1, long long s1) {
     return (long long)(int)(v - (unsigned)c1 * (unsigned)s1);
 }
 __device__ __forceinline__ long long centred(long long v, int c1, long long s1) { return v - (long long)c1 * s1; }
+__device__ __forceinline__ long long centred(wide48 v, int c1, long long s1) {
+    return (long long)(v & M48) - (long long)c1 * s1;
+}
 
 // A cell floor(t) from an fp32 estimate tf with |tf - t| <= band: exact
 // unless [tf - band, tf + band] straddles an integer (returns false then).
@@ -373,7 +418,12 @@ template <typename T, class A>
 __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, const unsigned* sb, int level, int cx,
                                                int cy, bool have_s1 = false, unsigned s1q_in = 0,
                                                unsigned s1d_in = 0) {
-    const PlanePtrs<T> P = plane_ptrs<T>(a, cy, cx);
+    PlanePtrs<T> P;
+    if constexpr (std::is_same<T, wide48>::value) {
+        P = plane_ptrs_w<T>(a, cy, cx);
+    } else {
+        P = plane_ptrs<T>(a, cy, cx);
+    }
     Corners<T> c0, c2, ckx, cky;
     long long s1q, s1d;
     if (have_s1) {
@@ -393,7 +443,9 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 4 + 4 * level, 1ull);
 #endif
-    if (level > 0 && !member_m(a, R, sb, cm)) return false;
+    // level 0 too: the coarse stage 1 passes centres it could not decide
+    // (ladder_stage1_coarse_kernel); for the others this repeats its test
+    if (!member_m(a, R, sb, cm)) return false;
 #if RINGS_STATS
     atomicAdd(a.stage_counts + 5 + 4 * level, 1ull);
 #endif

@@ -298,6 +298,9 @@ class Engine:
         self._region_m = 0
         self.capacity = 0
         self.xy = None
+        self.hi16 = None  # bits 32..47 of the cells (the fused rings' wide path, instead of the int64 planes)
+        self.built_int64 = False  # what the last build wrote beyond the 32-bit planes
+        self.built_hi16 = False
         self.coarse = None  # stage 1's coarse planes (u16 bit slices, ss_build_tables3)
         self.coarse_shifts: List[int] = []  # the shifts the last build wrote
         self.masks_done = None  # completion of the last run's streamed mask copy (run(host_masks=...))
@@ -382,6 +385,29 @@ class Engine:
                 need.add(k)
         return sorted(need) if len(need) <= _native.SS_MAX_COARSE else []
 
+    def wide_as_hi16(self, tp: Optional[TemplatePlan]) -> bool:
+        """Sizes beyond 32 bits read 32-bit + hi16 cells (mod 2^48) in the
+        fused rings when the fused ladder takes their group (ss_ladder_screen.cu:
+        <= 64 sizes, <= 104 rings, <= 8 rings per size, H < 2^24), every ring
+        sum stays below 2^48 and ring 0's PLAIN sums below 2^32; otherwise
+        (and under SS_FUSED=0 / force_int64) the int64 planes are built."""
+        if tp is None or self.force_int64 or not fused_enabled() or self.H >= (1 << 24) or self.W > (1 << 30):
+            return False
+        wide = [sp for sp in tp.sizes if sp.plan and not sp.fits32]
+        if not wide or len(wide) > 64 or sum(len(sp.plan) for sp in wide) > 104:
+            return False
+        span = max(self.W, self.H) + 1
+        for sp in wide:
+            if len(sp.plan) > 8:
+                return False
+            for r, (n, d) in enumerate(sp.plan):
+                cq, cd = 4 * n * n, 2 * d * d + 2 * d + 1
+                if 255 * max(cq, cd) * span >= 1 << 48:
+                    return False
+                if r == 0 and 255 * max(cq, cd) >= 1 << 32:
+                    return False
+        return True
+
     def build_tables(self, img: torch.Tensor, int64: bool = False, tp: Optional[TemplatePlan] = None) -> None:
         """K1/K2 on the current stream.  img: (rows, W) uint8 on the device.
         Writes the 32-bit planes, the int64 planes too when `int64`, and --
@@ -392,9 +418,14 @@ class Engine:
     def _build_tables(self, img: torch.Tensor, int64: bool, tp: Optional[TemplatePlan] = None) -> None:
         assert img.dtype == torch.uint8 and img.is_cuda and img.shape == (self.rows, self.W)
         img = img.contiguous()
+        hi16 = int64 and self.wide_as_hi16(tp)
+        int64 = int64 and not hi16
         if int64 and self.planes is None:
             tb = int(self.L.ss_tables_bytes(self.W, self.rows))
             self.planes = torch.empty(tb // 8, dtype=torch.int64, device=self.device)
+        if hi16 and self.hi16 is None:
+            self.hi16 = torch.empty(int(self.L.ss_tables_hi16_bytes(self.W, self.rows)) // 2, dtype=torch.int16,
+                                    device=self.device)
         shifts = self.coarse_shifts_for(tp)
         if shifts:
             nb = int(self.L.ss_coarse_bytes(self.W, self.rows, len(shifts)))
@@ -404,10 +435,12 @@ class Engine:
         sh = np.array(shifts or [0], np.int32)
         _native.check(self.L.ss_build_tables3(img.data_ptr(), self.W, self.rows, self.W,
                                               _p(self.planes) if int64 else None, self.planes32.data_ptr(),
+                                              _p(self.hi16) if hi16 else None,
                                               self.pitch, _p(self.coarse) if shifts else None, len(shifts),
                                               sh.ctypes.data, self.build_ws.data_ptr(), self.build_ws.numel(),
                                               _stream_handle(self.device)), "build_tables")
         self.coarse_shifts = list(shifts)
+        self.built_int64, self.built_hi16 = int64, hi16
 
     def screen_ladder(self, tp: TemplatePlan, main: Optional[torch.cuda.Stream] = None,
                       rows: Optional[Tuple[int, int]] = None) -> None:
@@ -444,7 +477,8 @@ class Engine:
             n_streams, ws_bytes = 1 + self.n_streams, self.screen_ws[0].numel()
         shifts = np.array(self.coarse_shifts or [0], np.int32)
         _native.check(self.L.ss_screen_ladder2(
-            _p(self.planes), None if self.force_int64 else self.planes32.data_ptr(), self.W, self.rows, self.pitch,
+            _p(self.planes) if self.built_int64 else None, None if self.force_int64 else self.planes32.data_ptr(),
+            self.W, self.rows, self.pitch,
             self.W, self.H, self.y_origin, y0, y1, cfg.stride, L, tp.m_arr.ctypes.data,
             tp.n_rings.ctypes.data, tp.ring_n.ctypes.data, tp.ring_d.ctypes.data, tp.blobs_dev.data_ptr(),
             tp.blobs.ctypes.data, tp.blob_off.ctypes.data, q[0], q[1], q[2],
@@ -452,7 +486,8 @@ class Engine:
             self.masks.data_ptr() + (y0 - self.y_begin) * self.words * 4, self.words, self.mrows * self.words,
             self.row_counts.data_ptr() + (y0 - self.y_begin) * 4, self.row_counts.shape[1], _p(self.stage_counts),
             flags, n_streams, handles, wss, ws_bytes,
-            _p(self.coarse) if self.coarse_shifts else None, len(self.coarse_shifts), shifts.ctypes.data),
+            _p(self.coarse) if self.coarse_shifts else None, len(self.coarse_shifts), shifts.ctypes.data,
+            _p(self.hi16) if self.built_hi16 else None),
             "screen")
 
     def _ladder_array(self, tp: TemplatePlan) -> np.ndarray:

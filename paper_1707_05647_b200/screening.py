@@ -341,6 +341,8 @@ _engine_cache: Dict[Tuple[int, int, str], Engine] = {}
 def get_engine(width: int, height: int, device=None) -> Engine:
     """One cached engine per (W, H, device); the most recent shape only."""
     dev = torch.device(device if device is not None else "cuda")
+    if dev.type == "cuda" and dev.index is None:  # "cuda" and "cuda:<current>" are one engine
+        dev = torch.device("cuda", torch.cuda.current_device())
     key = (width, height, str(dev))
     with _engine_lock:
         eng = _engine_cache.get(key)

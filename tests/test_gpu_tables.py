@@ -223,3 +223,31 @@ def test_config_scale_tables(cuda, case):
     if case == "bright_4096sq":
         assert planes[3, -1, img.shape[1]] > 2 ** 32  # the SQUARED plane wraps mod 2^32
     _check_sat_rsat_fast(img, planes)
+
+
+def test_hi16_planes_are_bits_32_to_47(cuda):
+    """ss_build_tables3's hi16 planes = bits 32..47 of the exact int64 cells."""
+    import torch
+
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    img = np.random.default_rng(8).integers(150, 256, (1500, 1900), dtype=np.uint8)
+    H, W = img.shape
+    pitch = int(L.ss_plane_pitch(W))
+    p64 = torch.empty(int(L.ss_tables_bytes(W, H)) // 8, dtype=torch.int64, device=cuda)
+    p32 = torch.empty(int(L.ss_tables32_bytes(W, H)) // 4, dtype=torch.int32, device=cuda)
+    h16 = torch.empty(int(L.ss_tables_hi16_bytes(W, H)) // 2, dtype=torch.int16, device=cuda)
+    ws = torch.empty(int(L.ss_build_workspace_bytes(W, H)), dtype=torch.uint8, device=cuda)
+    d_img = torch.from_numpy(img).to(cuda)
+    sh = np.zeros(1, np.int32)
+    _native.check(L.ss_build_tables3(d_img.data_ptr(), W, H, W, p64.data_ptr(), p32.data_ptr(), h16.data_ptr(),
+                                     pitch, None, 0, sh.ctypes.data, ws.data_ptr(), ws.numel(),
+                                     torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    full = p64.view(12, H + 1, pitch).cpu().numpy()[:, :, : W + 1]
+    hi = h16.view(12, H + 1, pitch).cpu().numpy().view(np.uint16)[:, :, : W + 1]
+    lo = p32.view(12, H + 1, pitch).cpu().numpy().view(np.uint32)[:, :, : W + 1]
+    assert full.max() >= 1 << 32  # the SQUARED / weighted cells do reach past 32 bits here
+    assert np.array_equal(hi, ((full >> 32) & 0xFFFF).astype(np.uint16))
+    assert np.array_equal(lo, (full & 0xFFFFFFFF).astype(np.uint32))

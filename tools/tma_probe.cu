@@ -38,7 +38,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 constexpr int CW = 16;  // consumer warps
 
-template <typename T, int BW, int BR, int NBOX, int STAGES>
+template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     probe(const __grid_constant__ CUtensorMap map, int tiles, int cols, int rows, unsigned long long* sink) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -55,13 +55,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == CW) {
-        if (lane == 0) {
-            unsigned rng = 12345u + blockIdx.x * 7919u;
+        if (lane < NPROD) {  // NPROD lanes share each tile's boxes
+            unsigned rng = 12345u + blockIdx.x * 7919u + lane * 104729u;
             for (int t = 0; t < tiles; ++t) {
                 const int s = t % STAGES;
                 mbar_wait(&empty[s], ((t / STAGES) & 1) ^ 1);
-                mbar_expect_tx(&full[s], STAGE);
-                for (int b = 0; b < NBOX; ++b) {
+                if (lane == 0) mbar_expect_tx(&full[s], STAGE);
+                __syncwarp((1u << NPROD) - 1u);
+                for (int b = lane; b < NBOX; b += NPROD) {
                     rng = rng * 1664525u + 1013904223u;
                     const int x = (int)((rng >> 8) % (unsigned)(cols - BW)) & ~(16 / (int)sizeof(T) - 1);
                     rng = rng * 1664525u + 1013904223u;
@@ -90,7 +91,7 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <typename T, int BW, int BR, int NBOX, int STAGES>
+template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1>
 void run(const char* name, void* plane, int cols, int rows, int ctas_per_sm) {
     static EncodeFn encode = nullptr;
     if (!encode) {
@@ -110,7 +111,7 @@ void run(const char* name, void* plane, int cols, int rows, int ctas_per_sm) {
         printf("%s: encode failed\n", name);
         return;
     }
-    auto k = probe<T, BW, BR, NBOX, STAGES>;
+    auto k = probe<T, BW, BR, NBOX, STAGES, NPROD>;
     const int smem = STAGES * NBOX * BW * BR * (int)sizeof(T);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int sms = 148;
@@ -145,20 +146,14 @@ int main() {
     void* p;
     CK(cudaMalloc(&p, 64 << 20));
     CK(cudaMemset(p, 1, 64 << 20));
-    run<unsigned, 196, 16, 8, 2>("u32 8 x (16x196) x2 [stage1 now]", p, 4096, 2048, 1);
-    run<unsigned, 192, 16, 8, 2>("u32 8 x (16x192) x2 [128B rows]", p, 4096, 2048, 1);
-    run<unsigned, 224, 16, 6, 2>("u32 6 x (16x224) x2 [128B rows]", p, 4096, 2048, 1);
-    run<unsigned, 256, 8, 8, 3>("u32 8 x (8x256) x3 [128B rows]", p, 4096, 2048, 1);
-    run<unsigned, 160, 16, 8, 2>("u32 8 x (16x160) x2 [128B rows]", p, 4096, 2048, 1);
-    run<unsigned short, 200, 16, 8, 2>("u16 8 x (16x200) x2", p, 4096, 4096, 1);
-    run<unsigned short, 192, 16, 8, 4>("u16 8 x (16x192) x4 [128B rows]", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 8, 2>("u16 8 x (16x256) x2 [128B rows]", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 8, 3>("u16 8 x (16x256) x3 [128B rows]", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 6, 4>("u16 6 x (16x256) x4 [128B rows]", p, 4096, 4096, 1);
-    run<unsigned short, 256, 8, 8, 6>("u16 8 x (8x256) x6 [128B rows]", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 8, 1>("u16 8 x (16x256) x1 2cta", p, 4096, 4096, 2);
-    run<unsigned short, 248, 16, 8, 3>("u16 8 x (16x248) x3", p, 4096, 4096, 1);
-    run<unsigned short, 128, 16, 8, 6>("u16 8 x (16x128) x6 [128B rows]", p, 4096, 4096, 1);
+    run<unsigned short, 232, 16, 8, 3>("u16 8 x (16x232) x3 [coarse now]", p, 4096, 4096, 1);
+    run<unsigned short, 232, 16, 8, 3, 2>("u16 8 x (16x232) x3 2 lanes", p, 4096, 4096, 1);
+    run<unsigned short, 232, 16, 8, 3, 4>("u16 8 x (16x232) x3 4 lanes", p, 4096, 4096, 1);
+    run<unsigned short, 232, 16, 8, 3, 8>("u16 8 x (16x232) x3 8 lanes", p, 4096, 4096, 1);
+    run<unsigned short, 256, 16, 8, 3>("u16 8 x (16x256) x3", p, 4096, 4096, 1);
+    run<unsigned short, 256, 16, 8, 3, 4>("u16 8 x (16x256) x3 4 lanes", p, 4096, 4096, 1);
+    run<unsigned, 196, 16, 8, 2>("u32 8 x (16x196) x2 [stage1 u32]", p, 4096, 2048, 1);
+    run<unsigned, 196, 16, 8, 2, 4>("u32 8 x (16x196) x2 4 lanes", p, 4096, 2048, 1);
     // HBM-resident (1 GB plane): the miss path
     void* q;
     CK(cudaMalloc(&q, 1ull << 30));
