@@ -51,7 +51,7 @@ def main(path, runs=1):
 
 def record_k3(path, runs, name, rnd="r2"):
     t, b, inst = main(path, runs)
-    k3 = [k for k in t if "stage1_kernel" in k or "ring_kernel" in k or "rings_kernel" in k or "border_kernel" in k]
+    k3 = [k for k in t if "stage1" in k or "ring_kernel" in k or "rings_kernel" in k or "border_kernel" in k]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     rec = {"dram_bytes_per_step": sum(b[k] for k in k3) * 1e9 / runs,
            "k3_ms_per_step_under_ncu": sum(t[k] for k in k3) / 1e3 / runs,
