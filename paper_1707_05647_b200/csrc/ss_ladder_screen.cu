@@ -758,37 +758,39 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
 // interior bits start at 0 and the rings kernel ORs its survivors in.
 __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constant__ FusedArgs a, unsigned* ctrs,
                                                              int ctr_words) {
-    // grid (blocks, sizes); every thread handles (row, word) pairs of one size
+    // grid (row blocks, sizes): a block writes whole mask rows of one size,
+    // its threads striding over the row's words (coalesced stores)
     const int words = (a.W + 31) >> 5;
     const SizeDev& S = a.size[blockIdx.y];
     const int xlo = S.lo, xhi = a.W - 1 - S.hi;
     if (blockIdx.x == 0 && blockIdx.y == 0)  // the band's tile / list / group counters
         for (int i = threadIdx.x; i < ctr_words; i += blockDim.x) ctrs[i] = 0u;
-    const long long rows = a.y_end - a.y_begin, n = rows * words;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(t / words), w = (int)(t - (long long)r * words);
+    const int rows = a.y_end - a.y_begin;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
         const int y = a.y_begin + r;
         unsigned* row = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
-        if (w == 0) S.row_counts[y - a.mask_y0] = 0u;
+        if (threadIdx.x == 0) S.row_counts[y - a.mask_y0] = 0u;
         const bool row_grid = a.stride == 1 || y % a.stride == 0;
         const bool row_int = row_grid && y >= S.lo && y <= a.H - 1 - S.hi;
-        const int x0 = w * 32;
-        unsigned grid = 0;
-        if (row_grid) {
-            const int nb = min(32, a.W - x0);
-            if (a.stride == 1) {
-                grid = nb == 32 ? FULL : (1u << nb) - 1u;
-            } else {
-                for (int b = 0; b < nb; ++b)
-                    if ((x0 + b) % a.stride == 0) grid |= 1u << b;
+        for (int w = threadIdx.x; w < words; w += blockDim.x) {
+            const int x0 = w * 32;
+            unsigned grid = 0;
+            if (row_grid) {
+                const int nb = min(32, a.W - x0);
+                if (a.stride == 1) {
+                    grid = nb == 32 ? FULL : (1u << nb) - 1u;
+                } else {
+                    for (int b = 0; b < nb; ++b)
+                        if ((x0 + b) % a.stride == 0) grid |= 1u << b;
+                }
             }
+            unsigned inter = 0;
+            if (row_int) {
+                const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
+                if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
+            }
+            row[w] = grid & ~inter;
         }
-        unsigned inter = 0;
-        if (row_int) {
-            const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
-            if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
-        }
-        row[w] = grid & ~inter;
     }
 }
 
@@ -1301,8 +1303,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
             {
-                const long long cells = brows * ((W + 31) / 32);
-                const dim3 bg((unsigned)std::max<long long>(1, std::min<long long>((cells + 1023) / 1024, 4LL * sms)),
+                const dim3 bg((unsigned)std::max<long long>(1, std::min<long long>(brows, 8LL * sms / n + 1)),
                               (unsigned)n);
                 ladder_border_kernel<<<bg, 256, 0, s>>>(a, static_cast<unsigned*>(d_ws), (int)(FCTR_BYTES / 4));
                 note_launch();

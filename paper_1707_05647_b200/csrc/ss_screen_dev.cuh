@@ -197,6 +197,49 @@ __device__ __forceinline__ void load_corners(const PlanePtrs<wide48>& P, const R
     c.o[0] = cell48(P.o, P.oh, ko + R.ob);
     c.o[1] = cell48(P.o, P.oh, ko + R.oc);
 }
+// Corner loads from per-(plane type, kind) bases -- uniform across the warp,
+// so they live in uniform registers -- plus one 32-bit byte offset per corner
+// shared by all kinds: address = base + (u32) offset is two integer ops per
+// load (a plane is < 4 GB: ps * sizeof(cell) < 2^32, checked on the host).
+// pos = cy * pitch + cx.
+template <typename T>
+__device__ __forceinline__ T ld_plane(const void* base, unsigned byte_off) {
+    return __ldg(reinterpret_cast<const T*>(static_cast<const char*>(base) + byte_off));
+}
+template <typename T, class A>
+__device__ __forceinline__ void load_corners_u(const A& a, int pos, const RingDev& R, int kind, Corners<T>& c) {
+    constexpr unsigned B = sizeof(T) == 8 && !std::is_same<T, wide48>::value ? 8u : 4u;  // lo-cell bytes
+    const char* lo = static_cast<const char*>(std::is_same<T, wide48>::value ? static_cast<const void*>(a.planes32)
+                                                                             : a.planes);
+    const long long ps = a.ps;
+    const char* bq = lo + (0 * 4 + kind) * ps * B;
+    const char* be = lo + (1 * 4 + kind) * ps * B;
+    const char* bo = lo + (2 * 4 + kind) * ps * B;
+    const unsigned o[8] = {(unsigned)(pos + R.sa), (unsigned)(pos + R.sb), (unsigned)(pos + R.sc),
+                           (unsigned)(pos + R.sd), (unsigned)(pos + R.ea), (unsigned)(pos + R.ed),
+                           (unsigned)(pos + R.ob), (unsigned)(pos + R.oc)};
+    using L = typename std::conditional<B == 8, long long, unsigned>::type;
+    T v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (T)ld_plane<L>(j < 4 ? bq : (j < 6 ? be : bo), o[j] * B);
+    if constexpr (std::is_same<T, wide48>::value) {  // bits 32..47 from the hi16 planes
+        const char* h = reinterpret_cast<const char*>(a.hi16);
+        const char* hq = h + (0 * 4 + kind) * ps * 2;
+        const char* he = h + (1 * 4 + kind) * ps * 2;
+        const char* ho = h + (2 * 4 + kind) * ps * 2;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            v[j] |= (wide48)ld_plane<unsigned short>(j < 4 ? hq : (j < 6 ? he : ho), o[j] * 2u) << 32;
+    }
+    c.q[0] = v[0];
+    c.q[1] = v[1];
+    c.q[2] = v[2];
+    c.q[3] = v[3];
+    c.e[0] = v[4];
+    c.e[1] = v[5];
+    c.o[0] = v[6];
+    c.o[1] = v[7];
+}
 template <typename T>
 __device__ __forceinline__ void load_corners(const PlanePtrs<T>& P, const RingDev& R, int kind, Corners<T>& c) {
     const int ko = kind * P.ks;
@@ -336,6 +379,25 @@ __device__ __forceinline__ long long centred(wide48 v, int c1, long long s1) {
     return (long long)(v & M48) - (long long)c1 * s1;
 }
 
+// fp32 square root of the estimates: sqrt.approx (MUFU; relative error
+// < 2^-21 assumed in the bands below, which the self-test ss_selftest_cells
+// checks against the fp64 sequence with boundary-aimed sums) unless
+// FAST_SQRT=0 selects the correctly rounded one.
+#ifndef FAST_SQRT
+#define FAST_SQRT 1
+#endif
+__device__ __forceinline__ float est_sqrt(float x) {
+#if FAST_SQRT
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return __fsqrt_rn(x);
+#endif
+}
+constexpr float EST_STD_REL = FAST_SQRT ? 2e-6f : 1e-6f;      // std band per (t + 1)
+constexpr float EST_GRAD_REL = FAST_SQRT ? 1.6e-6f : 6e-7f;   // gradient band per (|parts| + gm) / qg
+
 // A cell floor(t) from an fp32 estimate tf with |tf - t| <= band: exact
 // unless [tf - band, tf + band] straddles an integer (returns false then).
 #ifndef CELL_BAND_SCALE
@@ -365,12 +427,12 @@ __device__ __forceinline__ int std_cell_fast(const A& a, const RingDev& R, long 
         vq = s2q * R.icq - s1q * s1q;
         vd = s2d * R.icd - s1d * s1d;
     }
-    const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(__fsqrt_rn(__ll2float_rn(vq)), R.rcq),
-                                          __fmul_rn(__fsqrt_rn(__ll2float_rn(vd)), R.rcd)),
+    const float sdf = __fmul_rn(__fadd_rn(__fmul_rn(est_sqrt(__ll2float_rn(vq)), R.rcq),
+                                          __fmul_rn(est_sqrt(__ll2float_rn(vd)), R.rcd)),
                                 0.5f);
     const float ts = __fmaf_rn(sdf, a.rqs_f, 0.5f);
     int cs;
-    if (!cell_of(ts, __fmaf_rn(ts, 1e-6f, 1e-6f) + a.band_s, cs)) {
+    if (!cell_of(ts, __fmaf_rn(ts, EST_STD_REL, EST_STD_REL) + a.band_s, cs)) {
         const double mq = div_rn((double)s1q, R.cnt_sq, R.rcp_sq), md = div_rn((double)s1d, R.cnt_di, R.rcp_di);
         cs = std_cell_exact(a, R, mq, md, s2q, s2d);
     }
@@ -385,10 +447,11 @@ __device__ __forceinline__ int grad_cell_fast(const A& a, const RingDev& R, int 
     const float gxq = __fmul_rn(__ll2float_rn(2 * dxq - s1q), R.rw2q), gyq = __fmul_rn(__ll2float_rn(2 * dyq - s1q), R.rw2q);
     const float gxd = __fmul_rn(__ll2float_rn(dxd), R.rw1d), gyd = __fmul_rn(__ll2float_rn(dyd), R.rw1d);
     const float gx = __fmul_rn(__fadd_rn(gxq, gxd), 0.5f), gy = __fmul_rn(__fadd_rn(gyq, gyd), 0.5f);
-    const float gm = __fsqrt_rn(__fmaf_rn(gx, gx, __fmul_rn(gy, gy)));
+    const float gm = est_sqrt(__fmaf_rn(gx, gx, __fmul_rn(gy, gy)));
     const float tg = __fmaf_rn(gm, a.rqg_f, 0.5f);
     const float sum = __fadd_rn(__fadd_rn(fabsf(gxq), fabsf(gxd)), __fadd_rn(fabsf(gyq), fabsf(gyd)));
-    const float bg = __fmaf_rn(__fmul_rn(__fadd_rn(sum, gm), 6e-7f), a.rqg_f, __fmaf_rn(tg, 4e-7f, 4e-7f));
+    const float bg =
+        __fmaf_rn(__fmul_rn(__fadd_rn(sum, gm), EST_GRAD_REL), a.rqg_f, __fmaf_rn(tg, 4e-7f, 4e-7f));
     int cg;
     if (!cell_of(tg, bg, cg)) {
         cg = grad_cell_exact(a, R, cx, cy, s1q, s1d, (long long)(cx + 1) * s1q + dxq, (long long)(cy + 1) * s1q + dyq,
@@ -407,17 +470,21 @@ __device__ __forceinline__ int grad_cell_fast(const A& a, const RingDev& R, int 
 // Same decisions as stage1_from + finish_of (the parity tests compare the
 // fused path, which uses this, with the oracle); the error bands:
 //   mean: mean_cell (4e-6 (t + 1));
-//   std:  |sqrt(V)/c| in fp32 <= 2.7e-7 rel, t <= 4.5e-7 (t + 1); fp64
-//         var error <= 4 * 2^-53 * 65025 => std error <= 5.4e-6 absolute;
-//         band 1e-6 (t + 1) + 1e-5 / qs;
+//   std:  |sqrt(V)/c| in fp32 <= 2.7e-7 rel (+ 4.8e-7 with sqrt.approx),
+//         t <= 4.5e-7 (t + 1) (+ 4.8e-7); fp64 var error <= 4 * 2^-53 *
+//         65025 => std error <= 5.4e-6 absolute; band EST_STD_REL (t + 1)
+//         + 1e-5 / qs;
 //   grad: |gx_f - gx| <= 2.5e-7 (|gxq| + |gxd|) (likewise y), hypot is
-//         1-Lipschitz, + 2.5e-7 rel; band 2x that plus 4e-7 (t + 1).
+//         1-Lipschitz, + 2.5e-7 rel (+ 4.8e-7 with sqrt.approx); band
+//         EST_GRAD_REL (sum + gm) / qg plus 4e-7 (t + 1).
 //   have_s1: ring R's PLAIN sums s1q_in / s1d_in are given (stage 1 carried
 //   them in the candidate list: exact u32), so its 8 PLAIN corners are not read.
 template <typename T, class A>
 __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, const unsigned* sb, int level, int cx,
                                                int cy, bool have_s1 = false, unsigned s1q_in = 0,
                                                unsigned s1d_in = 0) {
+    // (load_corners_u -- per-kind uniform bases + 32-bit byte offsets -- measured
+    // slower here: config 1 K3 0.482 -> 0.499 ms; per-centre plane pointers kept)
     PlanePtrs<T> P;
     if constexpr (std::is_same<T, wide48>::value) {
         P = plane_ptrs_w<T>(a, cy, cx);

@@ -168,18 +168,26 @@ def plan_ladder(n: int, cfg: ScreeningConfig) -> TemplatePlan:
     return tp
 
 
-def launch_features(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None):
+def launch_features(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None,
+                    owned: bool = False):
     """Start fill_keysets' GPU part early (f2 rescale features, async on
-    `stream`); pass the handle to fill_keysets.  None off the GPU path."""
+    `stream`; owned: with its own buffers, see launch_template_features);
+    pass the handle to fill_keysets.  None off the GPU path."""
     dev = torch.device(device) if device is not None else torch.device("cpu")
     geo = getattr(tp, "geometry", None)
     if dev.type != "cuda" or geo is None or not geo.evaluated:
         return None
-    return launch_template_features(template, geo.desc, dev, stream)
+    return launch_template_features(template, geo.desc, dev, stream, owned=owned)
+
+
+def upload_keysets(tp: TemplatePlan, device) -> None:
+    """The key blobs to the device on the current stream (a few KB-MB: a
+    pageable copy costs less host time than pinning a fresh buffer)."""
+    tp.blobs_dev = torch.from_numpy(tp.blobs).to(torch.device(device), non_blocking=True)
 
 
 def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optional[torch.cuda.Stream] = None,
-                 pending=None) -> None:
+                 pending=None, upload: bool = True) -> None:
     """The template-dependent part of prepare_template (build_feature_set,
     screening.py:222-250, for every size).
 
@@ -238,9 +246,8 @@ def fill_keysets(tp: TemplatePlan, template: np.ndarray, device, stream: Optiona
         tp.blobs = np.concatenate(parts) if parts else np.zeros(0, np.int64)
     if not tp.blobs.size:
         tp.blobs = np.zeros(1, np.int64)
-    if dev.type == "cuda":
-        # a few KB-MB: a pageable copy costs less host time than pinning a fresh buffer
-        tp.blobs_dev = torch.from_numpy(tp.blobs).to(dev, non_blocking=True)
+    if dev.type == "cuda" and upload:
+        upload_keysets(tp, dev)
 
 
 def prepare_template(template: np.ndarray, cfg: ScreeningConfig, device,

@@ -194,12 +194,14 @@ def _device_desc(desc: np.ndarray, dev):
     return t
 
 
-def launch_template_features(template: np.ndarray, desc: np.ndarray, device, stream=None):
+def launch_template_features(template: np.ndarray, desc: np.ndarray, device, stream=None, owned: bool = False):
     """Enqueue the ring features of the rescale instances `desc`
     (instance_descriptors) of the template: one GPU launch (f2,
     csrc/ss_featureset.cu) on `stream` (default: the current stream) and the
     copy of the result into pinned host memory.  Returns a handle for
-    wait_template_features."""
+    wait_template_features.  owned=True: the round trip gets its own buffers
+    (several may be in flight on one stream: screen_batch), else the
+    stream's cached staging buffers."""
     import torch
 
     tpl = as_gray(template)
@@ -211,7 +213,7 @@ def launch_template_features(template: np.ndarray, desc: np.ndarray, device, str
     dev = torch.device(device)
     stream = stream or torch.cuda.current_stream(dev)
     d_desc = _device_desc(desc, dev)
-    st = _staging(dev, stream, n * n, desc.shape[0])
+    st = _staging(dev, stream, n * n, desc.shape[0]) if not owned else _owned_staging(dev, n * n, desc.shape[0])
     _native.check(_native.lib().ss_template_features_async(
         tpl.ctypes.data, n, desc.shape[0], d_desc.data_ptr(), DESC_STRIDE, st["tpl"].data_ptr(), st["out"].data_ptr(),
         st["host"].data_ptr(), stream.cuda_stream, st["event"].cuda_event), "template features")
@@ -219,6 +221,17 @@ def launch_template_features(template: np.ndarray, desc: np.ndarray, device, str
 
 
 _staging_cache: dict = {}
+
+
+def _owned_staging(dev, tpl_bytes: int, n_inst: int) -> dict:
+    """Fresh f2 round-trip buffers (the caller's handle keeps them alive)."""
+    import torch
+
+    event = torch.cuda.Event()
+    return {"tpl": torch.empty(max(tpl_bytes, 1), dtype=torch.uint8, device=dev),
+            "out": torch.empty((n_inst, SS_MAX_RINGS, 3), dtype=torch.float64, device=dev),
+            "host": torch.empty((n_inst, SS_MAX_RINGS, 3), dtype=torch.float64, pin_memory=True),
+            "event": event}
 
 
 def _staging(dev, stream, tpl_bytes: int, n_inst: int) -> dict:

@@ -26,7 +26,8 @@ import numpy as np
 import torch
 
 from .config import MIN_PATCH_SIDE, ScreeningConfig
-from .engine import Engine, EnginePool, TemplatePlan, fill_keysets, launch_features, plan_ladder, prepare_template
+from .engine import (Engine, EnginePool, TemplatePlan, fill_keysets, launch_features, plan_ladder, prepare_template,
+                     upload_keysets)
 from .image import as_gray, std_dev
 
 
@@ -497,19 +498,42 @@ def _screen_batch(pool: EnginePool, checked, cfg: ScreeningConfig) -> List[Scree
         caller.wait_stream(pool.streams[j])
         pending[j] = None
 
+    # Template side first, for the whole batch: every template's f2 features
+    # (own buffers, one stream), then the host key sets on a thread pool (the
+    # native call releases the GIL) while the loop below screens.
+    starts = [time.perf_counter()] * len(checked)
+    tps = [plan_ladder(tpl.shape[1], cfg) for _, tpl in checked]
+    tstream = pool.engines[0].template_stream
+    feats = [launch_features(tp, tpl, pool.device, tstream, owned=True) for tp, (_, tpl) in zip(tps, checked)]
+    workers = _keyset_workers()
+    futs = [workers.submit(fill_keysets, tp, tpl, pool.device, None, f, False)
+            for tp, (_, tpl), f in zip(tps, checked, feats)]
     for i, (img, tpl) in enumerate(checked):
         j = i % n
         collect(j)  # the engine's previous image leaves before its buffers are reused
         eng = pool.engines[j]
-        start = time.perf_counter()
+        tp = tps[i]
         with torch.cuda.stream(pool.streams[j]):
-            tp = plan_ladder(tpl.shape[1], cfg)
-            feats = launch_features(tp, tpl, eng.device, eng.template_stream)
             img_dev = upload_image(img, eng.device)
             eng.build_tables(img_dev, int64=eng.needs_int64(tp), tp=tp)
-            fill_keysets(tp, tpl, eng.device, eng.template_stream, feats)
+            futs[i].result()  # this template's key sets (host)
+            upload_keysets(tp, eng.device)
             eng.run(img_dev, tp, build=False)
-        pending[j] = (i, tp, start)
+        pending[j] = (i, tp, starts[i])
     for j in range(n):
         collect(j)
     return results  # type: ignore[return-value]
+
+
+_keyset_pool = None
+
+
+def _keyset_workers():
+    """Host threads for screen_batch's key sets (ss_ladder_keysets releases the GIL)."""
+    global _keyset_pool
+    if _keyset_pool is None:
+        import concurrent.futures
+        import os
+
+        _keyset_pool = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _keyset_pool
