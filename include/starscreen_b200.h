@@ -96,6 +96,19 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
  */
 int32_t ss_coarse_shift(int64_t count);
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse);
+/*
+ * ss_build_tables3 for the image rows [y0, y1) only, y0 and y1 whole bands of
+ * ss_build_band_rows(W, H, exact) rows (y1 may be H; exact = the int64 or
+ * hi16 planes are wanted), after the rows above were built by earlier calls
+ * with the same workspace: table rows y0 + 1 .. y1 become final.  Only image
+ * rows [y0, y1) are read -- a caller streams the image in and builds it band
+ * by band (screen(): upload, build and screen overlap).
+ */
+int32_t ss_build_band_rows(int64_t W, int64_t H, int32_t exact);
+int ss_build_tables_rows(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                         uint32_t* d_planes32, uint16_t* d_hi16, int64_t plane_pitch, uint16_t* d_coarse,
+                         int32_t n_coarse, const int32_t* h_shifts, int64_t y0, int64_t y1, void* d_workspace,
+                         size_t workspace_bytes, void* stream);
 /* Bytes of the 12 "hi16" planes: bits 32..47 of every exact cell (u16, same layout as the 32-bit planes). */
 size_t ss_tables_hi16_bytes(int64_t W, int64_t H);
 /*

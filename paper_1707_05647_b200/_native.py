@@ -43,6 +43,9 @@ _SIGS = {
     "ss_coarse_shift": (c_i32, [c_i64]),
     "ss_coarse_bytes": (c_sz, [c_i64, c_i64, c_i32]),
     "ss_tables_hi16_bytes": (c_sz, [c_i64, c_i64]),
+    "ss_build_band_rows": (c_i32, [c_i64, c_i64, c_i32]),
+    "ss_build_tables_rows": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_i64,
+                                            c_i64, c_p, c_sz, c_p]),
     "ss_build_tables3": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p, c_sz,
                                         c_p]),
     "ss_keyset_blob": (ctypes.c_int, [c_p, c_p, c_i32, c_p, ctypes.POINTER(c_sz)]),

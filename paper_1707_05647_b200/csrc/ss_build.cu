@@ -57,6 +57,7 @@ struct BuildArgs {
     // as the 32-bit planes): with those, a cell is known mod 2^48 and every
     // region sum of the 12 planes below 2^48 is exact (the rings' wide path)
     unsigned short* hi16;
+    int64_t band0;  // first band of this launch (row-range builds: ss_build_tables_rows)
 };
 
 __device__ __forceinline__ long long shfl_down64(long long v, int d) {
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     constexpr int OFF = RB + 1;
     static_assert(CW % kGroup == 0 && (RB + 1) % kGroup == 0, "XL+1 must be group aligned");
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int64_t chunk = blockIdx.x, band = blockIdx.y;
+    const int64_t chunk = blockIdx.x, band = a.band0 + blockIdx.y;
     const int64_t c0 = chunk * CW;             // first owned plane column
     const int64_t XL = c0 - RB - 2;            // x of thread 0, column 0
     const int64_t xb = XL + (int64_t)t * COLS; // x of this thread's column 0
@@ -337,10 +338,10 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 
 // Row prefixes at group boundaries: rowpre[y][g] = sums over x < kGroup * g
 // of (v, (x+1) v, v^2), g = 0..G.  One warp per row.
-__global__ void rowpre_kernel(BuildArgs a) {
-    const int64_t y = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void rowpre_kernel(BuildArgs a, int64_t y0, int64_t y1) {
+    const int64_t y = y0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (y >= a.H) return;
+    if (y >= y1) return;
     const uint8_t* row = a.img + y * a.img_pitch;
     long long* out = const_cast<long long*>(a.rowpre) + y * (a.G + 1) * 3;
     if (lane == 0) out[0] = out[1] = out[2] = 0;
@@ -378,15 +379,17 @@ __global__ void rowpre_kernel(BuildArgs a) {
 constexpr int SCAN_BATCH = 16;
 
 // Pass 2a: inclusive band states of the SAT rows (in place).
+// Scans cover bands [bb, nb) (row-range builds continue from band bb - 1's
+// inclusive state; bb = 0 is the whole image).
 template <typename V>
-__global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
+__global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB, int64_t bb) {
     const int OFF = RB + 1;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= 4 * a.W) return;
     const int k = (int)(gid / a.W);
     const int64_t x = gid % a.W;
-    V acc = 0;
-    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
+    V acc = bb > 0 ? st_ptr<V>(a, bb - 1, k, 0)[x + OFF] : (V)0;
+    for (int64_t b0 = bb; b0 < nb; b0 += SCAN_BATCH) {
         V v[SCAN_BATCH];
 #pragma unroll
         for (int j = 0; j < SCAN_BATCH; ++j) v[j] = (b0 + j < nb) ? st_ptr<V>(a, b0 + j, k, 0)[x + OFF] : 0;
@@ -404,7 +407,7 @@ __global__ void band_scan_s_kernel(BuildArgs a, int64_t nb, int RB) {
 // (clamped to S(W-1) beyond the right edge), GG paths move right (zero at
 // x <= 0).  Each stored element is read and written by exactly one thread.
 template <typename V>
-__global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
+__global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB, int64_t bb) {
     const int OFF = RB + 1;
     const int64_t W = a.W;
     const int64_t nF = W - 1 + OFF + (nb - 1) * RB, nG = W + RB + (nb - 1) * RB;
@@ -418,7 +421,17 @@ __global__ void band_scan_fg_kernel(BuildArgs a, int64_t nb, int RB) {
     const int64_t p0 = ff ? (-OFF + i) : (1 - (nb - 1) * RB + (i - nF));
     const int64_t step = ff ? -RB : RB;
     V acc = 0;
-    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BATCH) {
+    if (bb > 0) {  // the path's inclusive value at band bb - 1 (same clamp rules as below)
+        const int64_t p = p0 + (bb - 1) * step;
+        if (ff) {
+            if (p < -OFF) return;  // the path left the stored range (moving left)
+            acc = p >= W - 1 ? st_ptr<V>(a, bb - 1, k, 0)[W - 1 + OFF] : st_ptr<V>(a, bb - 1, k, 1)[p + OFF];
+        } else {
+            if (p > W + RB) return;  // moving right, beyond the stored range
+            acc = p <= 0 ? (V)0 : st_ptr<V>(a, bb - 1, k, 2)[p + OFF];
+        }
+    }
+    for (int64_t b0 = bb; b0 < nb; b0 += SCAN_BATCH) {
         V v[SCAN_BATCH];
         int kind[SCAN_BATCH];  // 0 skip/stop, 1 accumulate+store, 2 clamp (FF: acc = S(W-1); GG: acc = 0)
 #pragma unroll
@@ -468,29 +481,38 @@ static size_t state_bytes(int64_t W, int64_t H) {
 
 size_t build_workspace_bytes(int64_t W, int64_t H) { return rowpre_bytes(W, H) + state_bytes(W, H); }
 
+// Bands [b_lo, b_hi) of an image of nbands bands: pass 1 and the scans for
+// the bands among them whose end state is needed (all but the image's last),
+// pass 3 for all of them.  Earlier bands' states must be final (a previous
+// call over [0, b_lo)).
 template <int RB, typename V>
-static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s) {
-    if (nbands > 1) {
-        band_kernel<0, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(nbands - 1)), TPB, 0, s>>>(a);
+static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s, int64_t b_lo = 0, int64_t b_hi = -1) {
+    if (b_hi < 0) b_hi = nbands;
+    const int64_t nb = nbands - 1, W = a.W;  // bands with an end state
+    const int64_t s_hi = std::min(b_hi, nb);
+    if (s_hi > b_lo) {
+        a.band0 = b_lo;
+        band_kernel<0, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(s_hi - b_lo)), TPB, 0, s>>>(a);
         note_launch();
         if (int e = check_launch("band_kernel<local>")) return e;
-        const int64_t nb = nbands - 1, W = a.W;
-        band_scan_s_kernel<V><<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        band_scan_s_kernel<V><<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, s_hi, RB, b_lo);
         note_launch();
         if (int e = check_launch("band_scan_s_kernel")) return e;
-        const int64_t per_kind = (W - 1 + (RB + 1) + (nb - 1) * RB) + (W + RB + (nb - 1) * RB);
-        band_scan_fg_kernel<V><<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, nb, RB);
+        const int64_t per_kind = (W - 1 + (RB + 1) + (s_hi - 1) * RB) + (W + RB + (s_hi - 1) * RB);
+        band_scan_fg_kernel<V><<<(unsigned)((4 * per_kind + 255) / 256), 256, 0, s>>>(a, s_hi, RB, b_lo);
         note_launch();
         if (int e = check_launch("band_scan_fg_kernel")) return e;
     }
-    band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)nbands), TPB, 0, s>>>(a);
+    a.band0 = b_lo;
+    band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo)), TPB, 0, s>>>(a);
     note_launch();
     return check_launch("band_kernel<final>");
 }
 
 int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes, uint32_t* d_planes32,
                  int64_t plane_pitch_, void* d_ws, size_t ws_bytes, void* stream, uint16_t* d_coarse = nullptr,
-                 int n_coarse = 0, const int32_t* h_shifts = nullptr, uint16_t* d_hi16 = nullptr) {
+                 int n_coarse = 0, const int32_t* h_shifts = nullptr, uint16_t* d_hi16 = nullptr, int64_t y0 = 0,
+                 int64_t y1 = -1) {
     if (W < 1 || H < 1) { set_error("empty image"); return SS_EINVAL; }
     if (overflow_guard_fails(W, H)) {
         set_error("image %lldx%lld too large for 64-bit integral cells", (long long)W, (long long)H);
@@ -544,22 +566,31 @@ int build_tables(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, 
     a.n_coarse = d_coarse ? n_coarse : 0;
     for (int i = 0; i < SS_MAX_COARSE; ++i) a.shift[i] = i < a.n_coarse ? (int)h_shifts[i] : 0;
     const int64_t nbands = n_bands(H, rb);
+    // row range [y0, y1): whole bands (a later call continues from the state
+    // of band y0 / rb - 1, which an earlier call over the rows above wrote)
+    if (y1 < 0) y1 = H;
+    if (y0 < 0 || y1 > H || y0 >= y1 || y0 % rb || (y1 % rb && y1 != H)) {
+        set_error("row range [%lld, %lld) is not a run of whole %d-row bands", (long long)y0, (long long)y1, rb);
+        return SS_EINVAL;
+    }
+    const int64_t b_lo = y0 / rb, b_hi = (y1 + rb - 1) / rb;
+    a.band0 = 0;
 
-    rowpre_kernel<<<(unsigned)((H * 32 + 255) / 256), 256, 0, s>>>(a);
+    rowpre_kernel<<<(unsigned)(((y1 - y0) * 32 + 255) / 256), 256, 0, s>>>(a, y0, y1);
     note_launch();
     if (int e = check_launch("rowpre_kernel")) return e;
     // exact int64 recurrences when the int64 or hi16 planes are wanted, else mod 2^32
     if (exact) {
         switch (rb) {
-        case 63: return launch_bands<63, long long>(a, nbands, s);
-        case 31: return launch_bands<31, long long>(a, nbands, s);
-        default: return launch_bands<15, long long>(a, nbands, s);
+        case 63: return launch_bands<63, long long>(a, nbands, s, b_lo, b_hi);
+        case 31: return launch_bands<31, long long>(a, nbands, s, b_lo, b_hi);
+        default: return launch_bands<15, long long>(a, nbands, s, b_lo, b_hi);
         }
     }
     switch (rb) {
-    case 63: return launch_bands<63, unsigned>(a, nbands, s);
-    case 31: return launch_bands<31, unsigned>(a, nbands, s);
-    default: return launch_bands<15, unsigned>(a, nbands, s);
+    case 63: return launch_bands<63, unsigned>(a, nbands, s, b_lo, b_hi);
+    case 31: return launch_bands<31, unsigned>(a, nbands, s, b_lo, b_hi);
+    default: return launch_bands<15, unsigned>(a, nbands, s, b_lo, b_hi);
     }
 }
 
@@ -583,6 +614,14 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
 }
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse) {
     return (size_t)3 * (size_t)n_coarse * (size_t)(H + 1) * ss::plane_pitch(W) * 2;
+}
+int32_t ss_build_band_rows(int64_t W, int64_t H, int32_t exact) { return ss::pick_band_rows(W, H, exact != 0); }
+int ss_build_tables_rows(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,
+                         uint32_t* d_planes32, uint16_t* d_hi16, int64_t plane_pitch, uint16_t* d_coarse,
+                         int32_t n_coarse, const int32_t* h_shifts, int64_t y0, int64_t y1, void* d_workspace,
+                         size_t workspace_bytes, void* stream) {
+    return ss::build_tables(d_img, W, H, img_pitch, d_planes, d_planes32, plane_pitch, d_workspace, workspace_bytes,
+                            stream, d_coarse, n_coarse, h_shifts, d_hi16, y0, y1);
 }
 size_t ss_tables_hi16_bytes(int64_t W, int64_t H) { return (size_t)12 * (size_t)(H + 1) * ss::plane_pitch(W) * 2; }
 int ss_build_tables3(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,

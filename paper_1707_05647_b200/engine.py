@@ -554,14 +554,23 @@ class Engine:
         with torch.cuda.device(self.device):
             self._run(img, tp, build=build, region=region, capacity=capacity, host_masks=host_masks)
 
-    def _screen_streamed(self, tp: TemplatePlan, main: torch.cuda.Stream, host: torch.Tensor) -> None:
+    def _screen_streamed(self, tp: TemplatePlan, main: torch.cuda.Stream, host: torch.Tensor,
+                         chunks: Optional[List[Tuple[int, int]]] = None, before=None) -> None:
+        """K3 row chunk by row chunk, each chunk's mask rows (every size) copied
+        to the pinned `host` on the copy stream as soon as it is screened.
+        before(k): called before chunk k is enqueued (the pipelined path
+        enqueues the table build it needs there)."""
         L = len(tp.sizes)
         assert host.shape == (L, self.mrows, self.words) and host.dtype == torch.int32 and host.is_pinned()
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(self.device)
         cs = self.copy_stream
         pitch = self.mrows * self.words * 4
-        for a, b in self.readback_chunks(L):
+        for k, (a, b) in enumerate(chunks if chunks is not None else self.readback_chunks(L)):
+            if before is not None:
+                before(k)
+            if b <= a:
+                continue
             self.screen_ladder(tp, main, (a, b))
             ev = torch.cuda.Event()
             ev.record(main)
@@ -573,6 +582,98 @@ class Engine:
         done.record(cs)
         self.masks_done = done
         self._host_masks_inflight = (host, done)
+
+    # ── upload, build and screen overlapped (large images, screen()) ─────
+    PIPELINE_MIN_BYTES = 32 << 20  # images from this size take run_pipelined
+    PIPELINE_CHUNKS = 8
+
+    def run_pipelined(self, img: np.ndarray, tp: TemplatePlan, host_masks: torch.Tensor, keysets) -> None:
+        """screen() for a large host image: the image goes up in row chunks
+        (pinned staging, its own stream), each chunk's tables are built as it
+        lands (ss_build_tables_rows: the recurrences only look up), and the
+        rows whose tables are complete (those more than the largest size's
+        lower margin above the built edge) are screened right after, their
+        masks streamed back -- upload, K1/K2, K3 and the mask D2H overlap.
+        keysets(): builds the template's key sets on the host (called once
+        the first chunk is enqueued, while the GPU works on it).  Whole-image
+        engines only; then K5 / K4 as run()."""
+        with torch.cuda.device(self.device):
+            self._run_pipelined(img, tp, host_masks, keysets)
+
+    def _run_pipelined(self, img: np.ndarray, tp: TemplatePlan, host_masks: torch.Tensor, keysets) -> None:
+        assert (self.y_begin, self.y_end, self.y_origin, self.rows) == (0, self.H, 0, self.H)
+        assert img.shape == (self.H, self.W) and img.dtype == np.uint8
+        H, W = self.H, self.W
+        self._ensure(len(tp.sizes), tp.max_m, self.default_capacity(tp), True)
+        main = torch.cuda.current_stream(self.device)
+        for ev in (self.readback_done, self.masks_done):
+            if ev is not None:
+                main.wait_event(ev)
+        self.readback_done = self.masks_done = None
+        # table planes for this template (as _build_tables)
+        wide = self.needs_int64(tp)
+        hi16 = wide and self.wide_as_hi16(tp)
+        int64 = wide and not hi16
+        if int64 and self.planes is None:
+            self.planes = torch.empty(int(self.L.ss_tables_bytes(W, H)) // 8, dtype=torch.int64, device=self.device)
+        if hi16 and self.hi16 is None:
+            self.hi16 = torch.empty(int(self.L.ss_tables_hi16_bytes(W, H)) // 2, dtype=torch.int16,
+                                    device=self.device)
+        shifts = self.coarse_shifts_for(tp)
+        if shifts:
+            nb = int(self.L.ss_coarse_bytes(W, H, len(shifts)))
+            if self.coarse is None or self.coarse.numel() < nb:
+                self.coarse = None
+                self.coarse = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        sh = np.array(shifts or [0], np.int32)
+        self.coarse_shifts = list(shifts)
+        self.built_int64, self.built_hi16 = int64, hi16
+        # image buffers: device image and pinned staging, kept by the engine
+        if getattr(self, "_img_dev", None) is None:
+            self._img_dev = torch.empty((H, W), dtype=torch.uint8, device=self.device)
+            self._img_stage = torch.empty((H, W), dtype=torch.uint8, pin_memory=True)
+            self.upload_stream = torch.cuda.Stream(self.device)
+        img_dev, stage, us = self._img_dev, self._img_stage, self.upload_stream
+        us.wait_stream(main)  # the previous screen is done reading the device image
+        # build chunks: whole bands; screen chunks: rows whose tables are final
+        rb = int(self.L.ss_build_band_rows(W, H, 1 if (int64 or hi16) else 0))
+        per = -(-H // self.PIPELINE_CHUNKS)  # ceil
+        step = max(rb, -(-per // rb) * rb)
+        ends = list(range(step, H, step)) + [H]
+        hi_max = max(((sp.m // 2) for sp in tp.sizes if sp.plan), default=0)
+        dec, prev = [], 0
+        for e in ends:
+            d = H if e == H else max(prev, e - hi_max - 1)
+            dec.append((prev, d))
+            prev = d
+        src = torch.from_numpy(img)
+
+        def build(k: int) -> None:
+            r0, r1 = (0 if k == 0 else ends[k - 1]), ends[k]
+            stage[r0:r1].copy_(src[r0:r1])  # host copy into pinned staging (torch: multi-threaded)
+            with torch.cuda.stream(us):
+                img_dev[r0:r1].copy_(stage[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(us)
+            main.wait_event(ev)
+            _native.check(self.L.ss_build_tables_rows(
+                img_dev.data_ptr(), W, H, W, _p(self.planes) if int64 else None, self.planes32.data_ptr(),
+                _p(self.hi16) if hi16 else None, self.pitch, _p(self.coarse) if shifts else None, len(shifts),
+                sh.ctypes.data, r0, r1, self.build_ws.data_ptr(), self.build_ws.numel(), main.cuda_stream),
+                "build_tables")
+            if k == 0:
+                keysets()  # host work while the GPU builds the first chunk
+
+        self._screen_streamed(tp, main, host_masks, dec, before=build)
+        rs = self.region_stream = self.region_stream or torch.cuda.Stream(self.device)
+        rs.wait_stream(main)
+        with torch.cuda.stream(rs):
+            self.region_all(tp)
+        self.compact_all(tp)
+        if self.compact_event is None:
+            self.compact_event = torch.cuda.Event()
+        self.compact_event.record(main)
+        main.wait_stream(rs)
 
     def _run(self, img: torch.Tensor, tp: TemplatePlan, *, build: bool, region: bool,
              capacity: Optional[int], host_masks: Optional[torch.Tensor] = None) -> None:

@@ -278,6 +278,7 @@ class ScreeningResult:
         self.candidates = candidates
         self.size_masks = size_masks
         self._region_packed = region_packed
+        self._region_event = None  # pending copy into a host _region_packed (fetch_result(to_host=True))
         self._region = None
         self.stats = stats
 
@@ -286,6 +287,9 @@ class ScreeningResult:
         if self._region_packed is None:
             return np.zeros((self.region_rows[1] - self.region_rows[0], (self.width + 31) // 32), np.uint32)
         if isinstance(self._region_packed, torch.Tensor):
+            if self._region_event is not None:
+                self._region_event.synchronize()
+                self._region_event = None
             self._region_packed = _host_words(self._region_packed)
         return self._region_packed
 
@@ -307,6 +311,8 @@ class ScreeningResult:
         from .pgm import packed_to_pgm
 
         src = self._region_packed
+        if isinstance(src, torch.Tensor) and not src.is_cuda:
+            src = self.region_packed()  # a host copy (waits for it)
         if src is None:
             return np.zeros((self.region_rows[1] - self.region_rows[0], self.width), np.uint8)
         return packed_to_pgm(src, self.width)
@@ -369,13 +375,17 @@ def validate(image, template, cfg: ScreeningConfig):
     return img, tpl
 
 
-def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, masks=None) -> ScreeningResult:
+def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, masks=None,
+                 to_host: bool = False) -> ScreeningResult:
     """Counts to the host; survivor list, masks and region stay on the device
     (private copies, the engine's buffers are reused) until first accessed;
     `readback` (Engine.start_readback) carries the survivor rows' host copy
     that started right after compaction; `masks` = (pinned host tensor,
     event) of the size masks streamed to the host during the screen
-    (Engine.run(host_masks=...)), used instead of a device copy."""
+    (Engine.run(host_masks=...)), used instead of a device copy.  to_host:
+    every array goes straight to pinned host memory (asynchronous on the
+    current stream, one event) instead of a device copy -- no device
+    allocation per result (screen_batch)."""
     cur = torch.cuda.current_stream(eng.device)
     totals = eng.totals.cpu()  # synchronises the stream
     kept = int(totals[0])
@@ -384,15 +394,34 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, mas
         totals = eng.totals.cpu()
     size_counts = eng.size_counts[: len(tp.sizes)].cpu().tolist()
     eng.last_kept = kept
-    rows = eng.xy[:kept].clone()
-    packed = eng.masks[: len(tp.sizes)].clone() if masks is None else None
-    region = eng.region.clone() if eng.region is not None else None
-    # the copies are ordered on this stream; a caller reading them on another
-    # stream must wait for it (screen_batch), and their memory must not be
-    # reused before those streams are done with it
-    for t in (rows, packed, region):
-        if t is not None:
-            t.record_stream(cur)
+    region_event = None
+    if to_host:
+        rows = torch.empty((kept, 3), dtype=torch.int32, pin_memory=True)
+        rows.copy_(eng.xy[:kept], non_blocking=True)
+        packed = None
+        if masks is None:
+            packed = torch.empty(eng.masks[: len(tp.sizes)].shape, dtype=torch.int32, pin_memory=True)
+            packed.copy_(eng.masks[: len(tp.sizes)], non_blocking=True)
+        region = None
+        if eng.region is not None:
+            region = torch.empty(eng.region.shape, dtype=torch.int32, pin_memory=True)
+            region.copy_(eng.region, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(cur)
+        readback = (rows, done)
+        if masks is None:
+            masks = (packed, done)
+        region_event = done
+    else:
+        rows = eng.xy[:kept].clone()
+        packed = eng.masks[: len(tp.sizes)].clone() if masks is None else None
+        region = eng.region.clone() if eng.region is not None else None
+        # the copies are ordered on this stream; a caller reading them on another
+        # stream must wait for it (screen_batch), and their memory must not be
+        # reused before those streams are done with it
+        for t in (rows, packed, region):
+            if t is not None:
+                t.record_stream(cur)
     elapsed = time.perf_counter() - start
     W, H = eng.W, eng.H
     stats = PruneStats(
@@ -404,7 +433,9 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, mas
     )
     cands = CandidateList(rows, kept, readback)
     sm = SizeMasks(tp.ladder, packed, W) if masks is None else SizeMasks(tp.ladder, masks[0], W, pending=masks[1])
-    return ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, sm, region, stats, size_counts)
+    out = ScreeningResult(W, H, tp.template_side, tp.config, tp.ladder, cands, sm, region, stats, size_counts)
+    out._region_event = region_event
+    return out
 
 
 def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfig] = None,
@@ -427,14 +458,19 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     with eng.lock, torch.cuda.device(eng.device):
         tp = plan_ladder(tpl.shape[1], cfg)
         pending = launch_features(tp, tpl, eng.device, eng.template_stream)
-        img_dev = upload_image(img, eng.device)
-        eng.build_tables(img_dev, int64=eng.needs_int64(tp), tp=tp)
-        fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
         # the size masks go to pinned host memory chunk by chunk while the
         # later row chunks are still being screened (the reference returns
         # host masks; at 16384^2 x 33 sizes that is 1.1 GB of D2H)
         host_masks = eng.host_mask_buffer(len(tp.sizes))
-        eng.run(img_dev, tp, build=False, host_masks=host_masks)
+        if img.nbytes >= eng.PIPELINE_MIN_BYTES:
+            # large image: upload, table build and screen overlap by row chunk
+            eng.run_pipelined(img, tp, host_masks,
+                              lambda: fill_keysets(tp, tpl, eng.device, eng.template_stream, pending))
+        else:
+            img_dev = upload_image(img, eng.device)
+            eng.build_tables(img_dev, int64=eng.needs_int64(tp), tp=tp)
+            fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
+            eng.run(img_dev, tp, build=False, host_masks=host_masks)
         readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
         return fetch_result(eng, tp, start, readback, masks=(host_masks, eng.masks_done))
 
@@ -492,9 +528,7 @@ def _screen_batch(pool: EnginePool, checked, cfg: ScreeningConfig) -> List[Scree
             return
         i, tp, start = pending[j]
         with torch.cuda.stream(pool.streams[j]):
-            results[i] = fetch_result(pool.engines[j], tp, start)
-        # the result's device copies were made on stream j: the caller's stream
-        # (which reads them) waits for them
+            results[i] = fetch_result(pool.engines[j], tp, start, to_host=True)
         caller.wait_stream(pool.streams[j])
         pending[j] = None
 

@@ -523,3 +523,59 @@ def test_wide48_rings_equal_int64_planes(cuda):
     assert a.candidates == b.candidates
     for m in a.ladder:
         assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
+
+
+def test_pipelined_upload_build_screen(cuda, monkeypatch):
+    """screen() on a large image uploads it, builds its tables and screens it
+    row chunk by row chunk (Engine.run_pipelined, ss_build_tables_rows): force
+    that path on a mid-size image (several build chunks, a ladder with a
+    large lower margin) and compare with the oracle."""
+    import workloads as WL
+    from paper_1707_05647_b200.engine import Engine
+
+    monkeypatch.setattr(Engine, "PIPELINE_MIN_BYTES", 1 << 10)
+    monkeypatch.setattr(Engine, "PIPELINE_CHUNKS", 6)
+    img = WL.make_image(600, 1500, seed=51, sigma=3.0, noise=2.0)
+    case = WL.make_template(img, 52, 64, (0.8, 1.3), std_threshold=10.0)
+    compare_with_oracle(img, case.template, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.25})
+    # the same with a wide (hi16) size in the ladder
+    case = WL.make_template(img, 53, 150, (0.9, 1.1), std_threshold=10.0)
+    compare_with_oracle(img, case.template, {"alpha": 1.0, "beta": 1.8, "ladder_ratio": 1.3})
+
+
+def test_build_tables_rows_equals_whole_build(cuda):
+    """ss_build_tables_rows over consecutive band runs == one ss_build_tables3."""
+    import torch
+
+    from paper_1707_05647_b200 import _native
+
+    L = _native.lib()
+    rng = np.random.default_rng(12)
+    for (H, W, exact) in ((1000, 777, 0), (2100, 513, 1)):
+        img = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        pitch = int(L.ss_plane_pitch(W))
+        ws = torch.empty(int(L.ss_build_workspace_bytes(W, H)), dtype=torch.uint8, device=cuda)
+        d_img = torch.from_numpy(img).to(cuda)
+        sh = np.array([1, 4, 7], np.int32)
+        outs = []
+        for chunked in (False, True):
+            p32 = torch.zeros(int(L.ss_tables32_bytes(W, H)) // 4, dtype=torch.int32, device=cuda)
+            h16 = torch.zeros(int(L.ss_tables_hi16_bytes(W, H)) // 2, dtype=torch.int16, device=cuda) if exact else None
+            co = torch.zeros(int(L.ss_coarse_bytes(W, H, 3)) // 2, dtype=torch.int16, device=cuda)
+            s = torch.cuda.current_stream().cuda_stream
+            if not chunked:
+                _native.check(L.ss_build_tables3(d_img.data_ptr(), W, H, W, None, p32.data_ptr(),
+                                                 None if h16 is None else h16.data_ptr(), pitch, co.data_ptr(), 3,
+                                                 sh.ctypes.data, ws.data_ptr(), ws.numel(), s))
+            else:
+                rb = int(L.ss_build_band_rows(W, H, exact))
+                edges = sorted({0, H, *range(3 * rb, H, 5 * rb), *range(7 * rb, H, 7 * rb)})
+                for y0, y1 in zip(edges[:-1], edges[1:]):
+                    _native.check(L.ss_build_tables_rows(d_img.data_ptr(), W, H, W, None, p32.data_ptr(),
+                                                         None if h16 is None else h16.data_ptr(), pitch,
+                                                         co.data_ptr(), 3, sh.ctypes.data, y0, y1, ws.data_ptr(),
+                                                         ws.numel(), s))
+            torch.cuda.synchronize()
+            outs.append([t.cpu().numpy() for t in (p32, h16, co) if t is not None])
+        for a, b in zip(*outs):
+            assert np.array_equal(a, b)
