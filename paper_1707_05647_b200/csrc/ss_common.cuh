@@ -55,6 +55,18 @@ inline bool overflow_guard_fails(int64_t W, int64_t H) {
     return b >= ((__int128)1 << 62);
 }
 
+// Debug bounds checks (the pool refuses compute-sanitizer): built with
+// -DSS_DEBUG (SS_EXTRA_NVCC), every SS_CHECK traps on violation, so a GPU test
+// run of that build is a memcheck of the checked indices; compiled out otherwise.
+#ifdef SS_DEBUG
+#define SS_CHECK(c)              \
+    do {                         \
+        if (!(c)) __trap();      \
+    } while (0)
+#else
+#define SS_CHECK(c) ((void)0)
+#endif
+
 // internal status: the fused ladder declined a group (nothing enqueued; screen per size)
 constexpr int SS_DECLINED = -1000;
 

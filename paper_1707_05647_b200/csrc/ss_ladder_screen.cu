@@ -392,6 +392,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                     if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
                     have_res = true;
                 }
+                SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
                 list0[res_base + lane] = buf[nbuf - 32 + lane];
                 res_base += 32;
                 res_left -= 32;
@@ -437,10 +438,14 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
 #define COARSE_STAGES 3
 #endif
 constexpr int S1_MAX_WARPS = 32;  // consumer warps a stage-1 kernel may have (a CTA holds <= 32 warps)
-template <int CW_, int CPW_, int STAGES_> struct GeoCT {
+#ifndef COARSE_TY
+#define COARSE_TY 16
+#endif
+template <int CW_, int CPW_, int STAGES_, int TY_ = COARSE_TY> struct GeoCT {
     static constexpr int CW = CW_;
-    static constexpr int WPR = CW / TY;  // warps per tile row
-    static_assert(WPR * TY == CW && CW <= S1_MAX_WARPS, "consumer warps tile the rows");
+    static constexpr int TYC = TY_;      // tile rows
+    static constexpr int WPR = CW / TYC;  // warps per tile row
+    static_assert(WPR * TYC == CW && CW <= S1_MAX_WARPS, "consumer warps tile the rows");
     static constexpr int CPW = CPW_;
     static constexpr int TX = WPR * 32 * CPW;
     static constexpr int STAGES = STAGES_;
@@ -451,7 +456,7 @@ template <int CW_, int CPW_, int STAGES_> struct GeoCT {
     static constexpr int BW = TX + ALIGN;
 #endif
     static_assert(BW <= 256 && BW >= TX + ALIGN - 1, "box must cover the tile at any alignment (TMA box <= 256)");
-    static constexpr int BOX_ELEMS = BW * TY;
+    static constexpr int BOX_ELEMS = BW * TYC;
     static constexpr int BOX_BYTES = BOX_ELEMS * 2;
     static_assert(BOX_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
     static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
@@ -587,13 +592,14 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                 }
                 __syncwarp(pmask);  // expect_tx before any of the boxes lands
                 const int4 st = size_tma[sz];
+                SS_CHECK(sz >= 0 && sz < a.n_sizes && st.z >= 0 && st.z < CNK && st.w >= 0 && st.w < CNK);
                 const int n = st.x, d = st.y, b = lane;
                 // box b: SAT (+-n+1 columns, +-n+1 rows), E (+1, d+1 / -d), O (-d / d+1, 0)
                 const int xo = b < 4 ? ((b & 1) ? 1 - n : n + 1) : (b < 6 ? 1 : (b == 6 ? -d : d + 1));
                 const int yo = b < 4 ? ((b & 2) ? 1 - n : n + 1) : (b == 4 ? d + 1 : (b == 5 ? -d : 0));
                 const CUtensorMap* m = b < 4 ? &maps.sat[st.z] : (b < 6 ? &maps.e[st.w] : &maps.o[st.w]);
                 const int x0 = tx * G::TX;
-                const int cy0 = a.y_begin + ty * TY - a.y_origin;
+                const int cy0 = a.y_begin + ty * G::TYC - a.y_origin;
                 tma_load_2d(stage_buf + s * G::STAGE_BYTES + b * G::BOX_BYTES, m, G::floor_al(x0 + xo), cy0 + yo,
                             &full_bar[s]);
             }
@@ -619,7 +625,7 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
         const int tx = sl.x, ty = sl.y, sz = sl.z;
         const TileConstC& tc = size_info[sz];
         const int row = warp / G::WPR, half = warp - row * G::WPR;  // tile row, column block of this warp
-        const int y = a.y_begin + ty * TY + row;
+        const int y = a.y_begin + ty * G::TYC + row;
         const bool row_int = y < a.y_end && y >= tc.ylo && y <= tc.yhi && (unit_stride || (y % a.stride) == 0);
         // coarse sums biased by one: J = I + 1 in [0, 2^16 - 2], where
         // |S - I 2^k| < 2^(k+1) (the -1 is folded into the estimate's constant)
@@ -722,6 +728,7 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                     if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
                     have_res = true;
                 }
+                SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
                 list0[res_base + lane] = buf[nbuf - 32 + lane];
                 res_base += 32;
                 res_left -= 32;
@@ -768,6 +775,7 @@ __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constan
     const int rows = a.y_end - a.y_begin;
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
         const int y = a.y_begin + r;
+        SS_CHECK(y >= a.mask_y0 && y < a.H);
         unsigned* row = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
         if (threadIdx.x == 0) S.row_counts[y - a.mask_y0] = 0u;
         const bool row_grid = a.stride == 1 || y % a.stride == 0;
@@ -866,6 +874,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     };
     auto fetch = [&]() -> E {
         const unsigned slot = cur + 32 * k + lane;
+        SS_CHECK(!(have_input && slot < cnt_q) || slot < (unsigned)part_cap);
         return (have_input && slot < cnt_q) ? in[slot] : no_entry<E>();
     };
     grab();
@@ -927,12 +936,14 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         n_surv += __popc(sb);
         if (pass && last) {
             const long long row = y - a.mask_y0;
+            SS_CHECK(row >= 0 && row < a.y_end - a.mask_y0 && e.x >= 0 && e.x < a.W);
             atomicOr(S.mask + row * a.mask_pitch + (e.x >> 5), 1u << (e.x & 31));
             atomicAdd(S.row_counts + row, 1u);
         }
         const unsigned qb = pb & ~sb;
         if (qb) {
             const int c = qget(level + 1);
+            SS_CHECK(level + 1 < levels && c + __popc(qb) <= QCAP);
             if (pass && !last) queues[(level + 1) * QCAP + c + __popc(qb & lt)] = e;
             qc += (unsigned long long)__popc(qb) << (8 * (level + 1));
             __syncwarp();  // the entries are visible to the lanes that pop them
@@ -1019,9 +1030,9 @@ int coarse_maps_cached(CoarseMaps& maps, const uint16_t* coarse, int n_coarse, i
     std::memset(&maps, 0, sizeof(maps));
     for (int c = 0; c < n_coarse; ++c) {
         const uint16_t* base = coarse + (size_t)c * 3 * (size_t)ps;
-        if (int e = encode_plane_map(&maps.sat[c], base, 2, GeoC::BW, W, h, pitch)) return e;
-        if (int e = encode_plane_map(&maps.e[c], base + ps, 2, GeoC::BW, W, h, pitch)) return e;
-        if (int e = encode_plane_map(&maps.o[c], base + 2 * ps, 2, GeoC::BW, W, h, pitch)) return e;
+        if (int e = encode_plane_map(&maps.sat[c], base, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
+        if (int e = encode_plane_map(&maps.e[c], base + ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
+        if (int e = encode_plane_map(&maps.o[c], base + 2 * ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
     }
     std::lock_guard<std::mutex> lock(mu);
     if (cache.size() > 256) cache.clear();
@@ -1274,7 +1285,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             a.y_end = (int)ye;
             TileMapF tm;
             tm.n_tx = (int)((W + tile_x - 1) / tile_x);
-            tm.n_ty = (int)((brows + TY - 1) / TY);
+            const int tile_y = coarse ? GeoC::TYC : TY;
+            tm.n_ty = (int)((brows + tile_y - 1) / tile_y);
             tm.n_sizes = n;
             tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n;
             // column strips: the widest whose working set -- (max_m + rows in
@@ -1286,7 +1298,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                 const int64_t in_flight = (int64_t)sms * s1_per_sm * G::STAGES;
                 tm.strip = 1;
                 for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
-                    const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * TY;
+                    const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * tile_y;
                     const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * tile_x + max_m + 2) * 12 * eb;
                     if (ws <= budget) {
                         tm.strip = strip;

@@ -243,6 +243,7 @@ __device__ __forceinline__ void load_corners_u(const A& a, int pos, const RingDe
 template <typename T>
 __device__ __forceinline__ void load_corners(const PlanePtrs<T>& P, const RingDev& R, int kind, Corners<T>& c) {
     const int ko = kind * P.ks;
+    SS_CHECK(kind >= 0 && kind < 4);
     c.q[0] = ldg_at(P.q, ko + R.sa);
     c.q[1] = ldg_at(P.q, ko + R.sb);
     c.q[2] = ldg_at(P.q, ko + R.sc);
@@ -483,6 +484,9 @@ template <typename T, class A>
 __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, const unsigned* sb, int level, int cx,
                                                int cy, bool have_s1 = false, unsigned s1q_in = 0,
                                                unsigned s1d_in = 0) {
+    // every corner of the ring inside the table band (rows 0..h, columns 0..W)
+    SS_CHECK(cy - (R.n - 1 > R.d ? R.n - 1 : R.d) >= 0 && cy + (R.n > R.d ? R.n : R.d) + 1 <= a.ps / a.pitch - 1 &&
+             cx - (R.n - 1 > R.d ? R.n - 1 : R.d) >= 0 && cx + (R.n > R.d ? R.n : R.d) + 1 <= a.W);
     // (load_corners_u -- per-kind uniform bases + 32-bit byte offsets -- measured
     // slower here: config 1 K3 0.482 -> 0.499 ms; per-centre plane pointers kept)
     PlanePtrs<T> P;
@@ -821,7 +825,7 @@ inline int occupancy(const void* fn, int threads, size_t smem) {
 // 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
 // h+1 rows), box BW x TY.
 inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes, int box_w, int64_t W, int64_t h,
-                            int64_t pitch) {
+                            int64_t pitch, int box_h = TY) {
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -837,7 +841,7 @@ inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes,
     }
     const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
     const cuuint64_t strides[1] = {(cuuint64_t)pitch * (cuuint64_t)elem_bytes};
-    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)TY};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
     const cuuint32_t estr[2] = {1, 1};
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook

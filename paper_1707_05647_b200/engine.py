@@ -311,6 +311,7 @@ class Engine:
         self.coarse = None  # stage 1's coarse planes (u16 bit slices, ss_build_tables3)
         self.coarse_shifts: List[int] = []  # the shifts the last build wrote
         self.masks_done = None  # completion of the last run's streamed mask copy (run(host_masks=...))
+        self.region_event = None  # K5 of the last run done (start_region_readback)
         self._host_masks_inflight = None  # (pinned buffer, event) of that copy, kept alive until it has landed
         self.stage_counts = None  # set to a (4,) int64 device tensor to instrument the cascade
         self.force_int64 = False  # test hook: screen every size from the int64 planes
@@ -641,14 +642,27 @@ class Engine:
         step = max(rb, -(-per // rb) * rb)
         ends = list(range(step, H, step)) + [H]
         hi_max = max(((sp.m // 2) for sp in tp.sizes if sp.plan), default=0)
-        dec, prev = [], 0
-        for e in ends:
+        # screen chunk k = the rows build chunk k completes, in pieces (the
+        # last in four) so that a piece's mask D2H overlaps the next piece's
+        # screen and the copy left after the last piece is short
+        dec, owner, prev = [], [], 0
+        for k, e in enumerate(ends):
             d = H if e == H else max(prev, e - hi_max - 1)
-            dec.append((prev, d))
+            parts = 4 if e == H else 2
+            cuts = [prev + (d - prev) * i // parts for i in range(parts + 1)]
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                dec.append((a, b))
+                owner.append(k)
             prev = d
         src = torch.from_numpy(img)
 
-        def build(k: int) -> None:
+        built = []
+
+        def build(i: int) -> None:
+            k = owner[i]  # screen piece i needs build chunk k
+            if k in built:
+                return
+            built.append(k)
             r0, r1 = (0 if k == 0 else ends[k - 1]), ends[k]
             stage[r0:r1].copy_(src[r0:r1])  # host copy into pinned staging (torch: multi-threaded)
             with torch.cuda.stream(us):
@@ -669,6 +683,8 @@ class Engine:
         rs.wait_stream(main)
         with torch.cuda.stream(rs):
             self.region_all(tp)
+            self.region_event = torch.cuda.Event()
+            self.region_event.record(rs)
         self.compact_all(tp)
         if self.compact_event is None:
             self.compact_event = torch.cuda.Event()
@@ -706,6 +722,8 @@ class Engine:
             rs.wait_stream(main)
             with torch.cuda.stream(rs):
                 self.region_all(tp)
+                self.region_event = torch.cuda.Event()
+                self.region_event.record(rs)
         self.compact_all(tp)
         if self.compact_event is None:
             self.compact_event = torch.cuda.Event()
@@ -732,6 +750,26 @@ class Engine:
             done = torch.cuda.Event()
             done.record(cs)
         self.readback_done = done
+        return host, done
+
+    def start_region_readback(self):
+        """Start copying the kept region (bit-packed rows) into a fresh pinned
+        buffer on the copy stream right after K5 (beside K4 and the rows'
+        copy).  Returns (buffer, event), or None without a region."""
+        ev = getattr(self, "region_event", None)
+        if ev is None or self.region is None:
+            return None
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream(self.device)
+        cs = self.copy_stream
+        host = torch.empty(self.region.shape, dtype=torch.int32, pin_memory=True)
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            host.copy_(self.region, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+        self.readback_done = done  # (the copy stream is in order: this also covers the rows' copy)
+        self.region_event = None
         return host, done
 
     def recompact(self, tp: TemplatePlan, capacity: int) -> None:

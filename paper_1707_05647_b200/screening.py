@@ -376,7 +376,7 @@ def validate(image, template, cfg: ScreeningConfig):
 
 
 def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, masks=None,
-                 to_host: bool = False) -> ScreeningResult:
+                 to_host: bool = False, region_host=None) -> ScreeningResult:
     """Counts to the host; survivor list, masks and region stay on the device
     (private copies, the engine's buffers are reused) until first accessed;
     `readback` (Engine.start_readback) carries the survivor rows' host copy
@@ -415,12 +415,15 @@ def fetch_result(eng: Engine, tp: TemplatePlan, start: float, readback=None, mas
     else:
         rows = eng.xy[:kept].clone()
         packed = eng.masks[: len(tp.sizes)].clone() if masks is None else None
-        region = eng.region.clone() if eng.region is not None else None
+        if region_host is not None:  # already on its way to pinned host memory (start_region_readback)
+            region, region_event = region_host
+        else:
+            region = eng.region.clone() if eng.region is not None else None
         # the copies are ordered on this stream; a caller reading them on another
         # stream must wait for it (screen_batch), and their memory must not be
         # reused before those streams are done with it
         for t in (rows, packed, region):
-            if t is not None:
+            if t is not None and t.is_cuda:
                 t.record_stream(cur)
     elapsed = time.perf_counter() - start
     W, H = eng.W, eng.H
@@ -472,7 +475,8 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
             fill_keysets(tp, tpl, eng.device, eng.template_stream, pending)
             eng.run(img_dev, tp, build=False, host_masks=host_masks)
         readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
-        return fetch_result(eng, tp, start, readback, masks=(host_masks, eng.masks_done))
+        region = eng.start_region_readback()  # and the region's right after K5
+        return fetch_result(eng, tp, start, readback, masks=(host_masks, eng.masks_done), region_host=region)
 
 
 _pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
