@@ -8,6 +8,7 @@
 // dilation of the bit-packed survivor mask (van Herk/Gil-Werman along
 // columns, word-parallel; log-step shift-OR doubling along rows).
 #include <algorithm>
+#include <vector>
 
 #include "ss_common.cuh"
 
@@ -434,6 +435,82 @@ __global__ void region_cols_kernel(const unsigned* Hb, int H, long long words, l
         if (out[c] && r0 + c < H) atomicOr(region + (long long)(r0 + c) * region_pitch + w, out[c]);
 }
 
+// K5, chained form (full image): the region is the union over sizes of each
+// size's interior survivors dilated by its footprint [-lo_k, hi_k] in x and y
+// (screening.py:316-330).  With the sizes in descending order and
+// J_k = [-(lo_{k-1} - lo_k), hi_{k-1} - hi_k] the footprints telescope:
+//   R_1 = S_1,  R_k = (R_{k-1} (+) J_k) | S_k,  region = R_n (+) [-lo_n, hi_n],
+// so every step dilates by a small box (the ladder's consecutive margin gaps,
+// cut to <= 31 each way) over the whole bitmap: one streaming pass per step
+// instead of one full-size dilation per size.
+// dilate_step_kernel: dst(p) = OR of src over rows / columns [p - b, p + a]
+// (| the interior survivors of `mask`, when given).  A CTA owns a tile of
+// DS_TR rows x DS_TW words: the tile plus its halo (b rows above, a below,
+// one word each side) sits in shared memory; the vertical and then the
+// horizontal window OR are shift-OR doublings.
+constexpr int DS_TR = 64, DS_TW = 32, DS_HALO = 31;
+__global__ void __launch_bounds__(256) dilate_step_kernel(const unsigned* src, const unsigned* mask, long long mask_pitch,
+                                                         int lo_k, int hi_k, unsigned* dst, long long dst_pitch, int W,
+                                                         int H, int words, int a, int b) {
+    extern __shared__ unsigned dsm[];
+    // tile words [w0 - 1, w0 + DS_TW + 3): one word left (the output's shift
+    // by b < 32), three right (the window's a + b + 1 <= 63 bits past the
+    // last output bit)
+    constexpr int NW = DS_TW + 4;
+    const int nr = DS_TR + a + b, L = a + b + 1;
+    unsigned* A = dsm;
+    unsigned* B = dsm + nr * NW;
+    const int r0 = blockIdx.y * DS_TR, w0 = blockIdx.x * DS_TW;
+    // load src rows [r0 - b, r0 + DS_TR + a), words [w0 - 1, w0 + DS_TW + 3)
+    for (int i = threadIdx.x; i < nr * NW; i += blockDim.x) {
+        const int t = i / NW, u = i - t * NW;
+        const int gy = r0 - b + t, gw = w0 - 1 + u;
+        A[i] = (src && gy >= 0 && gy < H && gw >= 0 && gw < words) ? __ldg(src + (long long)gy * words + gw) : 0u;
+    }
+    __syncthreads();
+    // vertical: F_len(t) = OR A[t .. t + len - 1] (rows past the tile read as 0)
+    int l = 1;
+    while (l < L) {
+        const int step = min(l, L - l);
+        for (int i = threadIdx.x; i < nr * NW; i += blockDim.x) {
+            const int t = i / NW;
+            B[i] = A[i] | (t + step < nr ? A[i + step * NW] : 0u);
+        }
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+        l += step;
+    }
+    // rows t in [0, DS_TR) of A now hold V(r0 + t) = OR src rows [r0 + t - b, r0 + t + a]
+    // horizontal, per row, on bits: G_len(x) = OR V[x .. x + len - 1]
+    l = 1;
+    while (l < L) {
+        const int step = min(l, L - l);
+        for (int i = threadIdx.x; i < DS_TR * NW; i += blockDim.x) {
+            const int t = i / NW, u = i - t * NW;
+            const unsigned* row = A + t * NW;
+            const unsigned lo = row[u], hi = u + 1 < NW ? row[u + 1] : 0u;
+            B[i] = lo | ((lo >> step) | (hi << (32 - step)));  // step < 32
+        }
+        __syncthreads();
+        unsigned* tmp = A; A = B; B = tmp;
+        l += step;
+    }
+    // out(x) = G_L(x - b); | the interior survivors of this size
+    const unsigned last_mask = (W & 31) ? ((1u << (W & 31)) - 1u) : 0xffffffffu;
+    for (int i = threadIdx.x; i < DS_TR * DS_TW; i += blockDim.x) {
+        const int t = i / DS_TW, u = i - t * DS_TW;
+        const int gy = r0 + t, gw = w0 + u;
+        if (gy >= H || gw >= words) continue;
+        const unsigned* row = A + t * NW;
+        const unsigned cur = row[u + 1], prev = row[u];
+        unsigned v = b == 0 ? cur : ((cur << b) | (prev >> (32 - b)));  // b < 32
+        if (mask && gy >= lo_k && gy <= H - 1 - hi_k)
+            v |= __ldg(mask + (long long)gy * mask_pitch + gw) & interior_bits(gw, lo_k, W - 1 - hi_k);
+        if (gw == words - 1) v &= last_mask;
+        dst[(long long)gy * dst_pitch + gw] = v;
+    }
+}
+
 // f4: bit-packed mask rows -> one byte per pixel, 255 kept / 0 not
 // (cli.py:97-98 _mask_to_pgm), the PGM raster.  A thread per output 16 B:
 // one 16-bit slice of a mask word, coalesced stores.
@@ -563,7 +640,8 @@ int compact_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_str
 }
 
 size_t region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t L) {
-    return (size_t)std::max<int32_t>(L, 1) * H * ((W + 31) / 32) * 4;
+    // the row-pass buffer of every size (region_ladder_rows), >= the chained form's two bitmaps
+    return (size_t)std::max<int32_t>(L, 2) * H * ((W + 31) / 32) * 4;
 }
 
 // K5 over a window of H mask rows whose row 0 is global row y0 of an Hg-row
@@ -617,8 +695,68 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
 
 int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H, int32_t L,
                   const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
-    return region_ladder_rows(d_masks, mask_pitch, size_stride, W, H, 0, H, L, h_m, stride, d_region, d_ws, ws_bytes,
-                              stream);
+    // the chained form is opt-in (SS_REGION_CHAIN=1): measured slower than the
+    // per-size row / column passes -- config 4 step 35.7 -> 36.6 ms, config 1
+    // 0.66 -> 0.75 ms (a full-bitmap pass per step, each smem-bound)
+    const char* chain = getenv("SS_REGION_CHAIN");
+    if (!chain || atoi(chain) == 0)
+        return region_ladder_rows(d_masks, mask_pitch, size_stride, W, H, 0, H, L, h_m, stride, d_region, d_ws,
+                                  ws_bytes, stream);
+    Ladder lad;
+    if (int e = fill_ladder(lad, L, h_m)) return e;
+    if (W < 1 || H < 1 || stride < 1) { set_error("bad region arguments"); return SS_EINVAL; }
+    const int64_t words = (W + 31) / 32;
+    if (ws_bytes < (size_t)2 * H * words * 4 || !d_ws) {
+        set_error("region workspace too small");
+        return SS_EINVAL;
+    }
+    // evaluated sizes in descending order (the ladder is descending; m < 8 keep no survivors)
+    std::vector<int> ks;
+    for (int k = 0; k < L; ++k)
+        if (h_m[k] >= 8) ks.push_back(k);
+    std::stable_sort(ks.begin(), ks.end(), [&](int x, int y) { return h_m[x] > h_m[y]; });
+    cudaStream_t s = as_stream(stream);
+    if (ks.empty()) return cudaMemsetAsync(d_region, 0, (size_t)H * mask_pitch * 4, s) == cudaSuccess ? SS_OK
+                                                                                                     : check_launch("region");
+    unsigned* buf[2] = {static_cast<unsigned*>(d_ws), static_cast<unsigned*>(d_ws) + H * words};
+    int cur = -1;  // buffer holding R (-1: R = 0)
+    static std::atomic<int> raised{0};
+    auto step = [&](const unsigned* mask, int lo_k, int hi_k, int a, int b, unsigned* dst, long long dst_pitch) -> int {
+        const size_t smem = (size_t)2 * (DS_TR + a + b) * (DS_TW + 4) * 4;
+        if ((int)smem > raised.load()) {
+            cudaFuncSetAttribute(dilate_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            raised.store((int)smem);
+        }
+        const dim3 grid((unsigned)((words + DS_TW - 1) / DS_TW), (unsigned)((H + DS_TR - 1) / DS_TR));
+        dilate_step_kernel<<<grid, 256, smem, s>>>(cur < 0 ? nullptr : buf[cur], mask, mask_pitch, lo_k, hi_k, dst,
+                                                   dst_pitch, (int)W, (int)H, (int)words, a, b);
+        note_launch();
+        return check_launch("dilate_step_kernel");
+    };
+    // a dilation by [-a, b] in pieces of <= DS_HALO each way; the last piece ORs `mask`
+    auto dilate = [&](int a, int b, const unsigned* mask, int lo_k, int hi_k, bool final) -> int {
+        do {
+            const int pa = std::min(a, DS_HALO), pb = std::min(b, DS_HALO);
+            a -= pa;
+            b -= pb;
+            const bool last = a == 0 && b == 0;
+            const int nxt = cur == 0 ? 1 : 0;
+            unsigned* dst = (last && final) ? d_region : buf[nxt];
+            if (int e = step(last ? mask : nullptr, lo_k, hi_k, pa, pb, dst, (last && final) ? mask_pitch : words))
+                return e;
+            cur = (last && final) ? -2 : nxt;
+        } while (a > 0 || b > 0);
+        return SS_OK;
+    };
+    int plo = 0, phi = 0;
+    for (size_t j = 0; j < ks.size(); ++j) {
+        const int k = ks[j], m = h_m[k], lo = (m - 1) / 2, hi = m / 2;
+        const unsigned* mk = d_masks + (size_t)k * size_stride;
+        if (int e = dilate(j == 0 ? 0 : plo - lo, j == 0 ? 0 : phi - hi, mk, lo, hi, false)) return e;
+        plo = lo;
+        phi = hi;
+    }
+    return dilate(plo, phi, nullptr, 0, 0, true);  // region = R_n (+) [-lo_n, hi_n]
 }
 
 int bits_to_bytes(const uint32_t* d_bits, int64_t pitch, int64_t W, int64_t H, uint8_t* d_out, void* stream) {

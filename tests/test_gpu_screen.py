@@ -579,3 +579,21 @@ def test_build_tables_rows_equals_whole_build(cuda):
             outs.append([t.cpu().numpy() for t in (p32, h16, co) if t is not None])
         for a, b in zip(*outs):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("chain", ["1", "0"])
+def test_region_chain_equals_union_of_footprints(cuda, monkeypatch, chain):
+    """K5: the chained dilation (descending sizes, telescoping footprints,
+    steps cut to <= 31 each way) and the per-size row / column passes both
+    give the union of every evaluated survivor's m x m footprint, over
+    ladders with large gaps, a single size, and odd / even sizes."""
+    import workloads as WL
+
+    monkeypatch.setenv("SS_REGION_CHAIN", chain)
+    img = WL.make_image(500, 420, seed=31, sigma=2.5, noise=3.0)
+    for seed, side, kw in ((32, 24, {"alpha": 0.4, "beta": 3.0, "ladder_ratio": 1.7}),
+                           (33, 47, {"alpha": 1.0, "beta": 1.0}),
+                           (34, 64, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.1, "stride": 2}),
+                           (35, 100, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 2.0})):  # gaps > 31
+        case = WL.make_template(img, seed, side, (0.9, 1.1), std_threshold=10.0)
+        compare_with_oracle(img, case.template, kw)
