@@ -530,7 +530,7 @@ def run_ours(args):
     # written and read once (8 B entries), the mask bits written once
     plane_once = len(cases) * (int(eng.L.ss_tables32_bytes(eng.W, eng.rows)) +
                                (int(eng.L.ss_tables_bytes(eng.W, eng.rows)) if eng.built_int64 else 0) +
-                               (int(eng.L.ss_tables_hi16_bytes(eng.W, eng.rows)) if eng.built_hi16 else 0) +
+                               (int(eng.L.ss_tables_hi16_bytes(eng.W, eng.rows)) * 3 // 4 if eng.built_hi16 else 0) +
                                int(eng.L.ss_coarse_bytes(eng.W, eng.rows, len(eng.coarse_shifts))))
     compulsory = plane_once + 2 * 8.0 * stage[1] + positions / 8.0
     ctr = k3_counters(wl.name, len(cases))

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                             }
                         }
                     }
-                    if (sizeof(V) == 8 && a.hi16) {
+                    if (sizeof(V) == 8 && a.hi16 && k != 0) {  // PLAIN ring sums stay below 2^32: no hi16
                         auto hi = [](V v) { return (unsigned)(((unsigned long long)v >> 32) & 0xffffu); };
                         *reinterpret_cast<uint2*>(a.hi16 + (0 * 4 + k) * a.plane_stride + off) =
                             make_uint2(hi(S[k][0]) | hi(S[k][1]) << 16, hi(S[k][2]) | hi(S[k][3]) << 16);

@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
                 const RingDev& Rl = sring[S.ring0 + l];
                 Corners<T> c0;
                 load_corners(P, Rl, 0, c0);
-                all = member_m(a, Rl, sbits, mean_cell(a, Rl, unsigned_sum(sq_of(c0)), unsigned_sum(di_of(c0))));
+                all = member_m(a, Rl, sbits, mean_cell(a, Rl, plain_sum(sq_of(c0)), plain_sum(di_of(c0))));
             }
             if (all) atomicAdd(a.stage_counts + 20, 1ull);
             if (all && pass) atomicAdd(a.stage_counts + 21, 1ull);

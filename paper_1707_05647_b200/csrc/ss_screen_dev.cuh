@@ -188,6 +188,17 @@ __device__ __forceinline__ wide48 cell48(const unsigned* lo, const unsigned shor
 __device__ __forceinline__ void load_corners(const PlanePtrs<wide48>& P, const RingDev& R, int kind,
                                              Corners<wide48>& c) {
     const int ko = kind * P.ks;
+    if (kind == 0) {  // PLAIN: ring sums < 2^32, the 32-bit cells alone (no hi16 plane; plain_sum)
+        c.q[0] = ldg_at(P.q, ko + R.sa);
+        c.q[1] = ldg_at(P.q, ko + R.sb);
+        c.q[2] = ldg_at(P.q, ko + R.sc);
+        c.q[3] = ldg_at(P.q, ko + R.sd);
+        c.e[0] = ldg_at(P.e, ko + R.ea);
+        c.e[1] = ldg_at(P.e, ko + R.ed);
+        c.o[0] = ldg_at(P.o, ko + R.ob);
+        c.o[1] = ldg_at(P.o, ko + R.oc);
+        return;
+    }
     c.q[0] = cell48(P.q, P.qh, ko + R.sa);
     c.q[1] = cell48(P.q, P.qh, ko + R.sb);
     c.q[2] = cell48(P.q, P.qh, ko + R.sc);
@@ -260,6 +271,11 @@ template <typename T> __device__ __forceinline__ T di_of(const Corners<T>& c) { 
 __device__ __forceinline__ long long unsigned_sum(long long v) { return v; }
 __device__ __forceinline__ long long unsigned_sum(unsigned v) { return (long long)v; }
 __device__ __forceinline__ long long unsigned_sum(wide48 v) { return (long long)(v & M48); }
+// the PLAIN (kind 0) sum of a ring: < 2^32 for every plane width (the wide
+// path reads kind 0 from the 32-bit planes only, so it is recovered mod 2^32)
+__device__ __forceinline__ long long plain_sum(unsigned v) { return (long long)v; }
+__device__ __forceinline__ long long plain_sum(long long v) { return v; }
+__device__ __forceinline__ long long plain_sum(wide48 v) { return (long long)(unsigned)v; }
 // exact weighted region sum with weight (c + 1) at the centre column/row c
 __device__ __forceinline__ long long weighted_sum(long long v, long long, long long) { return v; }
 __device__ __forceinline__ long long weighted_sum(unsigned v, long long c1, long long s1) {
@@ -502,8 +518,8 @@ __device__ __forceinline__ bool eval_ring_fast(const A& a, const RingDev& R, con
         s1d = s1d_in;
     } else {
         load_corners(P, R, 0, c0);
-        s1q = unsigned_sum(sq_of(c0));
-        s1d = unsigned_sum(di_of(c0));
+        s1q = plain_sum(sq_of(c0));
+        s1d = plain_sum(di_of(c0));
     }
     load_corners(P, R, 3, c2);
 #if !EVAL_TWO_PHASE
