@@ -16,7 +16,9 @@
  *     the message.  SS_EINVAL / SS_ECAPACITY map to Python ValueError,
  *     SS_ECUDA to RuntimeError -- the reference's error classes;
  *   - stream-ordered and reentrant; nothing here allocates device memory:
- *     workspaces are caller-owned and sized by the *_bytes() queries.
+ *     workspaces are caller-owned and sized by the *_bytes() queries --
+ *     except a screening session (ss_session_*, the native runtime of one
+ *     whole screen() call), which owns its buffers and streams.
  *
  * Device table layout ("planes"): 12 int64 planes of (H+1) rows x pitch
  * columns, plane p = type*4 + kind, kind in {PLAIN, X_WEIGHTED, Y_WEIGHTED,
@@ -417,6 +419,60 @@ int ss_match_fused(const uint8_t* d_planes, int64_t W, int64_t H, int64_t pitch,
                    int32_t row_cols, int64_t first, int64_t count, int32_t m, const uint8_t* d_bfrag, int32_t n_angles,
                    int32_t group, const long long* d_stats, double* d_part_score, long long* d_part_idx,
                    double* d_best_score, long long* d_best_idx, void* stream);
+
+/* ── screening session: the whole screen() in one call ────────────────── */
+/*
+ * Native host runtime of screen() (screening.py:474-539) for one (W, H) on
+ * one device: ss_session_screen runs the template features (f2), the image
+ * upload (pinned staging filled by host worker threads), K1/K2, the key sets
+ * (host, while the tables build), K3 (fused ladder), K4 beside K5 and the
+ * D2H of every result, with one host synchronisation -- the same kernels and
+ * results as the stream-level entry points above.  The session owns its
+ * device / pinned buffers (grown on demand) and streams; calls on one session
+ * are serialised (internal mutex); sessions are independent (one per host
+ * thread overlaps several screens on the GPU).
+ */
+typedef struct ss_session ss_session;
+
+/* The template-independent ladder of one (template side, config)
+ * (ladder_sizes screening.py:202-219, ring_plan features.py:190-211) and the
+ * f2 rescale instances of its evaluated sizes (screening.py:236-238). */
+typedef struct ss_ladder_plan {
+    int32_t n_sizes;        /* ladder sizes (<= SS_MAX_SIZES), ladder order */
+    const int32_t* m;       /* (n_sizes) */
+    const int32_t* n_rings; /* (n_sizes); 0 below MIN_PATCH_SIDE */
+    const int32_t* ring_n;  /* (n_sizes, SS_MAX_RINGS) */
+    const int32_t* ring_d;  /* (n_sizes, SS_MAX_RINGS) */
+    int32_t n_inst;         /* rescale instances (ss_template_features_device rows) */
+    const int32_t* desc;    /* (n_inst, desc_stride) */
+    int32_t desc_stride;    /* >= 4 + 2 * SS_MAX_RINGS */
+    const int32_t* nk;      /* instances per evaluated size */
+    double q_mean, q_std, q_grad; /* Quantizer (screening.py:64-78) */
+    int32_t stride;         /* ScreeningConfig.stride */
+} ss_ladder_plan;
+
+/* Host destinations and counts of one screen (ScreeningResult,
+ * screening.py:276-298).  Destinations should be pinned for full-rate D2H. */
+typedef struct ss_screen_out {
+    uint32_t* masks;       /* (n_sizes, H, ceil(W/32)) packed size masks, or NULL */
+    uint32_t* region;      /* (H, ceil(W/32)) packed kept region, or NULL */
+    int32_t* rows;         /* (rows_cap, 3) int32 (cx, cy, m): the candidates */
+    int64_t rows_cap;
+    int64_t* size_counts;  /* (n_sizes) survivors per size, or NULL */
+    int64_t kept;          /* out: patches_kept */
+    int64_t region_pixels; /* out: region_pixels_kept */
+    int64_t tested;        /* out: patches_tested */
+} ss_screen_out;
+
+int ss_session_create(int32_t device, int64_t W, int64_t H, ss_session** out);
+void ss_session_destroy(ss_session* session);
+/* Screen the W x H u8 host image h_img (rows W bytes apart) with the n x n
+ * u8 host template.  SS_ECAPACITY: out->kept > out->rows_cap (every other
+ * output is complete; fetch the rows with ss_session_rows). */
+int ss_session_screen(ss_session* session, const uint8_t* h_img, const uint8_t* h_template, int32_t n,
+                      const ss_ladder_plan* plan, ss_screen_out* out);
+/* Survivor rows [first, first + count) of the session's last screen. */
+int ss_session_rows(ss_session* session, int32_t* h_rows, int64_t first, int64_t count);
 
 #ifdef __cplusplus
 }

@@ -91,7 +91,26 @@ _SIGS = {
     "ss_template_features_device": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_i32, c_p, c_p]),
     "ss_template_features_async": (ctypes.c_int, [c_p, c_i32, c_i32, c_p, c_i32, c_p, c_p, c_p, c_p, c_p]),
     "ss_template_ring_features": (ctypes.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_p]),
+    "ss_session_create": (ctypes.c_int, [c_i32, c_i64, c_i64, c_p]),
+    "ss_session_destroy": (None, [c_p]),
+    "ss_session_screen": (ctypes.c_int, [c_p, c_p, c_p, c_i32, c_p, c_p]),
+    "ss_session_rows": (ctypes.c_int, [c_p, c_p, c_i64, c_i64]),
 }
+
+
+class LadderPlan(ctypes.Structure):
+    """struct ss_ladder_plan (include/starscreen_b200.h)."""
+
+    _fields_ = [("n_sizes", c_i32), ("m", c_p), ("n_rings", c_p), ("ring_n", c_p), ("ring_d", c_p),
+                ("n_inst", c_i32), ("desc", c_p), ("desc_stride", c_i32), ("nk", c_p),
+                ("q_mean", c_d), ("q_std", c_d), ("q_grad", c_d), ("stride", c_i32)]
+
+
+class ScreenOut(ctypes.Structure):
+    """struct ss_screen_out (include/starscreen_b200.h)."""
+
+    _fields_ = [("masks", c_p), ("region", c_p), ("rows", c_p), ("rows_cap", c_i64), ("size_counts", c_p),
+                ("kept", c_i64), ("region_pixels", c_i64), ("tested", c_i64)]
 
 
 def lib() -> ctypes.CDLL:

@@ -29,6 +29,7 @@ SOURCES = {
     "ss_ladder.cpp": [],
     "ss_ladder_screen.cu": ["-fmad=false"],
     "ss_match.cu": ["-fmad=false"],
+    "ss_session.cpp": [],
 }
 
 

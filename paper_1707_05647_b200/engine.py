@@ -655,6 +655,7 @@ class Engine:
                 owner.append(k)
             prev = d
         src = torch.from_numpy(img)
+        pinned_src = src.is_pinned()
 
         built = []
 
@@ -664,9 +665,13 @@ class Engine:
                 return
             built.append(k)
             r0, r1 = (0 if k == 0 else ends[k - 1]), ends[k]
-            stage[r0:r1].copy_(src[r0:r1])  # host copy into pinned staging (torch: multi-threaded)
+            if pinned_src:  # the caller's buffer is pinned: DMA straight from it
+                part = src[r0:r1]
+            else:
+                stage[r0:r1].copy_(src[r0:r1])  # host copy into pinned staging (torch: multi-threaded)
+                part = stage[r0:r1]
             with torch.cuda.stream(us):
-                img_dev[r0:r1].copy_(stage[r0:r1], non_blocking=True)
+                img_dev[r0:r1].copy_(part, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(us)
             main.wait_event(ev)

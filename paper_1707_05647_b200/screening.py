@@ -16,6 +16,7 @@ materialises 8.8 GB of bools or 10^7 Python tuples it is not asked for.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from collections.abc import Mapping, Sequence
@@ -29,6 +30,7 @@ from .config import MIN_PATCH_SIDE, ScreeningConfig
 from .engine import (Engine, EnginePool, TemplatePlan, fill_keysets, launch_features, plan_ladder, prepare_template,
                      upload_keysets)
 from .image import as_gray, std_dev
+from .session import Session
 
 
 class FlatTemplateError(ValueError):
@@ -453,6 +455,8 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
     img, tpl = validate(image, template, cfg)
     h, w = img.shape
     start = time.perf_counter()
+    if img.nbytes < Engine.PIPELINE_MIN_BYTES and _session_path(w, h, device):
+        return _screen_session(img, tpl, cfg, device, start)
     eng = get_engine(w, h, device)
     # The template's f2 features start first (engine's template stream), the
     # image side (upload + K1/K2 on the current stream) overlaps them, then
@@ -477,6 +481,55 @@ def screen(image: np.ndarray, template: np.ndarray, cfg: Optional[ScreeningConfi
         readback = eng.start_readback()  # the survivor rows' D2H overlaps K5 and the result bookkeeping
         region = eng.start_region_readback()  # and the region's right after K5
         return fetch_result(eng, tp, start, readback, masks=(host_masks, eng.masks_done), region_host=region)
+
+
+def _device_key(device) -> torch.device:
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+_session_cache: Dict[Tuple[int, int, str], Session] = {}
+
+
+def get_session(width: int, height: int, device=None) -> Session:
+    """One cached native session per (W, H, device); the most recent shape only."""
+    dev = _device_key(device)
+    key = (width, height, str(dev))
+    with _engine_lock:
+        ses = _session_cache.get(key)
+        if ses is None:
+            _session_cache.clear()
+            ses = Session(width, height, dev)
+            _session_cache[key] = ses
+        return ses
+
+
+def _session_path(width: int, height: int, device) -> bool:
+    """screen() runs through the native session unless an experiment / test
+    hook asks for the Python engine: SS_SESSION=0, SS_FUSED=0,
+    SS_LADDER_WS_BYTES, or the cached engine of this shape carrying
+    force_int64 / stage_counts / hooks."""
+    env = os.environ
+    if env.get("SS_SESSION", "1") == "0" or env.get("SS_FUSED", "1") == "0" or env.get("SS_LADDER_WS_BYTES"):
+        return False
+    eng = _engine_cache.get((width, height, str(_device_key(device))))
+    return eng is None or not (eng.force_int64 or eng.stage_counts is not None or eng.hooks is not None)
+
+
+def _screen_session(img: np.ndarray, tpl: np.ndarray, cfg: ScreeningConfig, device, start: float,
+                    session: Optional[Session] = None) -> ScreeningResult:
+    """screen() through one ss_session_screen call; every result lands in
+    pinned host memory before it returns."""
+    h, w = img.shape
+    geo, r = (session or get_session(w, h, device)).run(img, tpl, cfg)
+    stats = PruneStats(patches_tested=r.tested, patches_kept=r.kept, region_pixels_kept=r.region_pixels,
+                       total_pixels=w * h, wall_time_s=time.perf_counter() - start)
+    cands = CandidateList(r.rows[: r.kept].numpy(), r.kept)
+    masks = SizeMasks(geo.ladder, r.masks.numpy().view(np.uint32), w)
+    return ScreeningResult(w, h, tpl.shape[1], cfg, geo.ladder, cands, masks, r.region.numpy().view(np.uint32),
+                           stats, r.size_counts.tolist())
 
 
 _pool_cache: Dict[Tuple[int, int, str, int], EnginePool] = {}
@@ -515,9 +568,65 @@ def screen_batch(images: Sequence[np.ndarray], templates: Sequence[np.ndarray],
     h, w = checked[0][0].shape
     if any(img.shape != (h, w) for img, _ in checked):
         raise ValueError("screen_batch needs images of one shape")
-    pool = get_pool(w, h, device, max(1, min(engines, len(images))))
+    n = max(1, min(engines, len(images)))
+    if img_bytes(checked) < Engine.PIPELINE_MIN_BYTES and _session_path(w, h, device):
+        return _screen_batch_sessions(get_session_pool(w, h, device, n), checked, cfg)
+    pool = get_pool(w, h, device, n)
     with pool.lock, torch.cuda.device(pool.device):
         return _screen_batch(pool, checked, cfg)
+
+
+def img_bytes(checked) -> int:
+    return checked[0][0].nbytes
+
+
+_session_pool_cache: Dict[Tuple[int, int, str, int], List[Session]] = {}
+_session_pool_lock = threading.Lock()
+
+
+def get_session_pool(width: int, height: int, device=None, n: int = 4) -> List[Session]:
+    """n native sessions of one shape (screen_batch), cached; the most recent (shape, n) only."""
+    dev = _device_key(device)
+    key = (width, height, str(dev), n)
+    with _engine_lock:
+        pool = _session_pool_cache.get(key)
+        if pool is None:
+            _session_pool_cache.clear()
+            pool = [Session(width, height, dev) for _ in range(n)]
+            _session_pool_cache[key] = pool
+        return pool
+
+
+def _screen_batch_sessions(sessions: List[Session], checked, cfg: ScreeningConfig) -> List[ScreeningResult]:
+    """screen_batch over native sessions: host thread j screens images j, j +
+    n, ... through session j (ss_session_screen releases the GIL), so n
+    screens overlap on the GPU -- each on its session's streams -- while the
+    other threads copy their inputs and results."""
+    n = len(sessions)
+    results: List[Optional[ScreeningResult]] = [None] * len(checked)
+
+    def work(j: int) -> None:
+        for i in range(j, len(checked), n):
+            img, tpl = checked[i]
+            results[i] = _screen_session(img, tpl, cfg, None, time.perf_counter(), sessions[j])
+
+    with _session_pool_lock:  # one batch at a time over these sessions
+        futs = [_batch_workers(n).submit(work, j) for j in range(n)]
+        for f in futs:
+            f.result()
+    return results  # type: ignore[return-value]
+
+
+_batch_pool = None
+
+
+def _batch_workers(n: int):
+    global _batch_pool
+    if _batch_pool is None or _batch_pool._max_workers < n:
+        import concurrent.futures
+
+        _batch_pool = concurrent.futures.ThreadPoolExecutor(max_workers=max(n, 4))
+    return _batch_pool
 
 
 def _screen_batch(pool: EnginePool, checked, cfg: ScreeningConfig) -> List[ScreeningResult]:

@@ -256,10 +256,14 @@ def test_list_modes_vs_oracle(cuda, monkeypatch, mode):
         eng.force_int64 = False
 
 
-def test_screen_batch_matches_screen(cuda):
-    """screen_batch (engine pool, overlapped streams, engine reuse) == screen() per image."""
+@pytest.mark.parametrize("session", ["1", "0"])
+def test_screen_batch_matches_screen(cuda, monkeypatch, session):
+    """screen_batch (native sessions on host threads, or the engine pool's
+    overlapped streams; engine reuse) == screen() per image."""
     import workloads as WL
     from paper_1707_05647_b200 import screen, screen_batch
+
+    monkeypatch.setenv("SS_SESSION", session)
 
     imgs, tpls = [], []
     for i in range(7):
@@ -419,6 +423,7 @@ def test_streamed_mask_readback_in_chunks(cuda, monkeypatch):
     from paper_1707_05647_b200.engine import Engine
 
     monkeypatch.setattr(Engine, "READBACK_CHUNK_BYTES", 1 << 14)
+    monkeypatch.setenv("SS_SESSION", "0")  # the Python engine's streamed readback
     img = WL.make_image(700, 1100, seed=41, sigma=2.5, noise=3.0)
     case = WL.make_template(img, 42, 40, (0.8, 1.3), std_threshold=10.0)
     res = compare_with_oracle(img, case.template, {"alpha": 0.5, "beta": 1.8, "ladder_ratio": 1.2})
@@ -500,10 +505,10 @@ def test_coarse_planes_are_bit_slices(cuda):
             assert np.array_equal(coarse[c, t, :, : W + 1], want[:, : W + 1]), (k, t)
 
 
-def test_wide48_rings_equal_int64_planes(cuda):
+def test_wide48_rings_equal_int64_planes(cuda, monkeypatch):
     """Sizes whose ring sums exceed 32 bits: the fused rings read 32-bit +
-    hi16 cells (mod 2^48) by default and the int64 planes when forced; both
-    must give the oracle's result."""
+    hi16 cells (mod 2^48) by default (native session and Python engine) and
+    the int64 planes when forced; all must give the oracle's result."""
     import workloads as WL
     from paper_1707_05647_b200 import screen
     from paper_1707_05647_b200.screening import get_engine
@@ -511,9 +516,12 @@ def test_wide48_rings_equal_int64_planes(cuda):
     img = WL.make_image(900, 720, seed=71, sigma=4.0, noise=2.0)
     case = WL.make_template(img, 72, 160, (0.9, 1.1), std_threshold=10.0)
     kw = {"alpha": 1.0, "beta": 2.0, "ladder_ratio": 1.3, "quantizer": (6.0, 5.0, 7.0)}
-    a = compare_with_oracle(img, case.template, kw)
+    a = compare_with_oracle(img, case.template, kw)  # the session
+    monkeypatch.setenv("SS_SESSION", "0")
+    c = screen(img, case.template, pcfg(kw))
     eng = get_engine(900, 720)
     assert eng.built_hi16 and not eng.built_int64
+    assert a.candidates == c.candidates
     eng.force_int64 = True
     try:
         b = screen(img, case.template, pcfg(kw))
@@ -597,3 +605,85 @@ def test_region_chain_equals_union_of_footprints(cuda, monkeypatch, chain):
                            (35, 100, {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 2.0})):  # gaps > 31
         case = WL.make_template(img, seed, side, (0.9, 1.1), std_threshold=10.0)
         compare_with_oracle(img, case.template, kw)
+
+
+def _same_result(a, b):
+    assert tuple(a.ladder) == tuple(b.ladder)
+    assert np.array_equal(a.candidates.array(), b.candidates.array())
+    for m in a.ladder:
+        assert np.array_equal(a.size_masks.packed(m), b.size_masks.packed(m)), m
+    assert np.array_equal(a.region_packed(), b.region_packed())
+    assert (a.stats.patches_tested, a.stats.patches_kept, a.stats.region_pixels_kept, a.stats.total_pixels) == (
+        b.stats.patches_tested, b.stats.patches_kept, b.stats.region_pixels_kept, b.stats.total_pixels)
+    assert a.candidates_per_size() == b.candidates_per_size()
+
+
+@pytest.mark.parametrize("case", ["config0", "stride", "tiny", "wide", "everything", "no_coarse"])
+def test_session_equals_engine_path(cuda, monkeypatch, case):
+    """screen() through the native session (ss_session_screen: one C call) and
+    through the Python engine (stream-level entry points) on the same inputs:
+    identical results, including a ladder of sizes beyond 32 bits (hi16
+    planes), tiny sizes (whole-grid keeps), stride 3, no coarse stage 1, and a
+    screen keeping almost every centre (the survivor buffer and the output
+    rows both overflow on the first call: K4 redone, rows fetched after)."""
+    import workloads as WL
+    from paper_1707_05647_b200 import screen
+    from paper_1707_05647_b200.screening import _session_cache
+
+    if case == "config0":
+        wl = WL.CONFIGS[0]
+        c = WL.make_cases(wl)[0]
+        img, tpl = c.image, c.template
+        kw = {"alpha": wl.alpha, "beta": wl.beta, "ladder_ratio": wl.ladder_ratio, "quantizer": wl.q}
+    else:
+        img = WL.make_image(640, 400, seed=501, sigma=3.0, noise=2.0)
+        side = {"wide": 160, "tiny": 12}.get(case, 40)
+        tpl = WL.make_template(img, 502, side, (0.9, 1.1), std_threshold=8.0).template
+        kw = {"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.3}
+        if case == "stride":
+            kw["stride"] = 3
+        if case == "tiny":
+            kw.update(alpha=0.3, beta=1.0)
+        if case == "wide":
+            kw.update(alpha=1.0, beta=2.0, quantizer=(6.0, 5.0, 7.0))
+        if case == "everything":
+            kw.update(quantizer=(400.0, 400.0, 400.0))
+        if case == "no_coarse":
+            monkeypatch.setenv("SS_COARSE", "0")
+    _session_cache.clear()  # a fresh session: first-call capacities
+    a = screen(img, tpl, pcfg(kw))
+    a2 = screen(img, tpl, pcfg(kw))  # the same session again (buffers reused)
+    monkeypatch.setenv("SS_SESSION", "0")
+    b = screen(img, tpl, pcfg(kw))
+    _same_result(a, b)
+    _same_result(a2, b)
+    if case == "everything":
+        assert a.stats.patches_kept > max(1 << 16, a.stats.patches_tested // 50)
+    if case == "config0":
+        compare_with_oracle(img, tpl, kw)
+
+
+def test_session_threads_equal_serial(cuda):
+    """Several native sessions driven from host threads at once (the GIL is
+    released inside ss_session_screen) give the serial results."""
+    import concurrent.futures
+
+    import workloads as WL
+    from paper_1707_05647_b200.session import Session
+
+    cfg = pcfg({"alpha": 0.6, "beta": 1.5, "quantizer": (6.0, 6.0, 6.0)})
+    cases = []
+    for i in range(6):
+        img = WL.make_image(480, 360, seed=600 + i, sigma=2.5, noise=1.0)
+        cases.append((img, WL.make_template(img, 700 + i, 32, (0.8, 1.2), std_threshold=10.0).template))
+    sessions = [Session(480, 360, cuda) for _ in range(3)]
+
+    def run(i):
+        _, r = sessions[i % 3].run(*cases[i], cfg)
+        return r.rows[: r.kept].numpy().copy(), r.masks.numpy().copy(), r.region_pixels
+
+    serial = [run(i) for i in range(len(cases))]
+    with concurrent.futures.ThreadPoolExecutor(3) as ex:
+        par = list(ex.map(run, range(len(cases))))
+    for (ra, ma, pa), (rb, mb, pb) in zip(serial, par):
+        assert np.array_equal(ra, rb) and np.array_equal(ma, mb) and pa == pb

@@ -1,6 +1,7 @@
 """cProfile of repeated screen() calls (host overhead of the public API).
 
-usage: python tools/screen_profile.py [CONFIG] [CALLS]
+usage: python tools/screen_profile.py [CONFIG] [CALLS] [pinned]
+(pinned: the inputs in pinned host memory, as bench.py's e2e)
 """
 import cProfile
 import os
@@ -20,6 +21,12 @@ calls = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 wl = WL.CONFIGS[idx]
 case = WL.make_cases(wl, images=1)[0]
 cfg = WL.screening_config(wl)
+if len(sys.argv) > 3 and sys.argv[3] == "pinned":
+    for name in ("image", "template"):
+        a = getattr(case, name)
+        t = torch.empty(a.shape, dtype=torch.uint8, pin_memory=True)
+        t.numpy()[...] = a
+        setattr(case, name, t.numpy())
 
 
 def call():
