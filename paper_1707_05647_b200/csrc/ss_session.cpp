@@ -91,8 +91,8 @@ class Workers {
         using clock = std::chrono::steady_clock;
         uint64_t seen = gen_.load();
         for (;;) {
-            // spin up to 2 ms for new work, then sleep until notified
-            const auto until = clock::now() + std::chrono::microseconds(2000);
+            // spin up to 1 ms for new work, then sleep until notified
+            const auto until = clock::now() + std::chrono::microseconds(1000);
             while (gen_.load(std::memory_order_acquire) == seen && clock::now() < until) {
 #if defined(__x86_64__)
                 __builtin_ia32_pause();
