@@ -391,14 +391,15 @@ int64_t ss_match_plane_pitch(int64_t W);
  * image, and the high / low bytes of its squares.
  */
 int ss_match_planes(const uint8_t* d_img, int64_t W, int64_t H, uint8_t* d_planes, int64_t pitch, void* stream);
-/* Bytes of the probe fragments of ss_match_probes for size m, n_angles angles. */
+/* Bytes of the probe operand blocks of ss_match_probes for size m, n_angles angles. */
 size_t ss_match_probe_bytes(int32_t m, int32_t n_angles);
 /*
  * Probes of ladder size m for n_angles rotations of the n x n template:
  * resize_bilinear to m x m (image_io.py:164-178), then _rotate_with_mask per
  * angle (image_io.py:181-203) with the rotation's cos / sin in d_cos / d_sin
  * (computed on the host exactly as NumPy does).  Writes the masked probes
- * and supports as u8 tensor-core B fragments (groups of 40 angles) into
+ * and supports as the tcgen05 B operand (groups of 40 angles; per 64-byte K
+ * stage one 48-row block of each in the UMMA canonical K-major layout) into
  * d_bfrag (ss_match_probe_bytes), and d_stats[a] = (support pixels, sum of
  * the masked probe, sum of its squares).  d_base: m*m bytes scratch.
  */
@@ -411,7 +412,9 @@ int64_t ss_match_parts(int64_t count);
  * candidates first .. first+count-1 of d_rows (rows of row_cols int32,
  * (cx, cy, ...), all of size m): the masked NCC scores of
  * second_stage.py:136-152 (exact integer dot products, float64 in NumPy's op
- * order) and, per angle, the best score and its candidate index (relative to
+ * order; the dot products on the tensor cores: tcgen05.mma kind::i8 into
+ * TMEM, 128 candidates per CTA) and, per angle, the best score and its
+ * candidate index (relative to
  * `first`; the first candidate on equal scores, as np.argmax) into
  * d_best_score / d_best_idx[angle].  d_part_*: ss_match_parts(count) x 40.
  */

@@ -6,23 +6,29 @@
 // P the masked rotated probes, M their 0/1 supports.  Every entry is an
 // integer and every dot product an integer below 2^53, so those float64
 // matmuls are exact whatever their summation order -- and so is an integer
-// tensor-core GEMM.  One fused kernel per (size, group of <= 40 angles)
-// gathers the windows straight from the image into u8 MMA fragments
-// (mma.sync m16n8k32 u8 x u8 -> s32: W x [P | M], and W^2 as its high and
-// low bytes x M), keeps the dot products in registers (int32, spilled into
-// int64 shared memory every few rows when m is large enough to overflow),
-// replays the reference's float64 score sequence op for op (-fmad=false) and
-// reduces to the best candidate per angle with the reference's tie-break
-// (first candidate on equal scores, np.argmax).
+// tensor-core GEMM.  One fused kernel per (size, group of <= 40 angles) runs
+// it on the 5th-generation tensor cores: per CTA, 128 candidates (the UMMA M)
+// x 48 angle columns (40 + 8 zero; UMMA N) x the window pixels (K, 64 bytes
+// per pipeline stage): the CTA's threads gather the windows straight from
+// the image planes into shared memory in the UMMA canonical K-major layout,
+// the probes' B blocks come pre-laid-out from global memory, and one thread
+// issues tcgen05.mma kind::i8 (u8 x u8 -> s32) into four TMEM accumulators
+// -- I x P, I x M, (I^2 >> 8) x M, (I^2 & 255) x M -- with tcgen05.commit
+// releasing each stage.  The epilogue reads TMEM (tcgen05.ld), replays the
+// reference's float64 score sequence op for op (-fmad=false) and reduces to
+// the best candidate per angle with the reference's tie-break (first
+// candidate on equal scores, np.argmax).  When m is large enough for I x P to
+// pass 2^31, its accumulator is drained into int64 shared memory every few
+// window rows.
 //
 //   ss_match_planes   the image, and its squares' high / low bytes, as padded
 //                     u8 planes (the three A operands)
 //   ss_match_probes   resize_bilinear(template, m, m) (image_io.py:164-178) and
 //                     _rotate_with_mask per angle (image_io.py:181-203; cos/sin
-//                     from the host's libm, as NumPy computes them) as B
-//                     fragments, and per-angle sums
-//   ss_match_fused    windows x probes -> scores -> best per angle per CTA
-//   ss_match_reduce   best per angle over the CTAs, in candidate order
+//                     from the host's libm, as NumPy computes them) as the B
+//                     blocks, and per-angle sums
+//   ss_match_fused    windows x probes -> scores -> best per angle per CTA,
+//                     then the best per angle over the CTAs
 #include <algorithm>
 
 #include "ss_common.cuh"
@@ -31,12 +37,29 @@ namespace ss {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int MAX_GROUP_ANGLES = 40;          // angles per fused launch (5 n-tiles of 8)
-constexpr int NT = MAX_GROUP_ANGLES / 8;      // angle n-tiles
-constexpr int BT = 2 * NT;                    // B n-tiles: masked probe, support
-constexpr int FUSED_WARPS = 4;
-constexpr int TM = 16 * FUSED_WARPS;          // candidates per CTA
-constexpr int PLANE_PAD = 64;                 // zero columns right of each plane row
+constexpr int MAX_GROUP_ANGLES = 40;  // angles per fused launch
+constexpr int TM = 128;               // candidates per CTA: the UMMA M
+constexpr int NB = 48;                // B rows per block: 40 angles + 8 zero rows (UMMA N, a multiple of 16)
+constexpr int KB = 64;                // K bytes (window pixels) per pipeline stage: two 32-byte UMMA k-steps
+constexpr int NSTAGE = 3;  // 90 KB of stages: two CTAs per SM
+constexpr int A_BYTES = TM * KB;                             // one A plane's stage: 8 KB
+constexpr int B_BYTES = NB * KB;                             // one B block's stage: 3 KB
+constexpr int STAGE_BYTES = 3 * A_BYTES + 2 * B_BYTES;       // 30 KB
+constexpr int CM_SBO = (KB / 16) * 128;                      // bytes between 8-row core-matrix groups
+constexpr int TMEM_COLS = 256;                               // IP [0,48) IM [48,96) HI [96,144) LO [144,192)
+constexpr int PLANE_PAD = 96;  // zero columns right of each plane row (the gather reads <= 67 bytes past a window)
+
+// Byte offset of (row, k) in a UMMA canonical K-major tile without swizzle:
+// 8 x 16-byte core matrices, the KB / 16 of one 8-row group side by side
+// (LBO = 128 bytes along K), the groups CM_SBO apart along M / N.
+__host__ __device__ constexpr int canon(int row, int k) {
+    return (row >> 3) * CM_SBO + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+// window rows padded to whole 16-byte pieces (a piece never straddles two rows)
+__host__ __device__ constexpr int row_bytes(int m) { return (m + 15) / 16 * 16; }
+// pipeline stages of one window (K = m * row_bytes(m), zero-padded to whole stages)
+__host__ __device__ constexpr long long n_stages_of(int m) { return ((long long)m * row_bytes(m) + KB - 1) / KB; }
+constexpr int THREADS = 256;  // 8 warps gather; warp w & 3 owns TMEM lanes 32 (w & 3) .. in the epilogue
 
 // image_io.py:131-161 bilinear sample of img (h x w) at (xs, ys), quantized
 __device__ __forceinline__ int sample_q(const uint8_t* img, int w, int h, double xs, double ys) {
@@ -83,20 +106,19 @@ __global__ void planes_kernel(const uint8_t* __restrict__ img, int W, long long 
 
 // One CTA per angle a: _rotate_with_mask(base, angle, fill=0)
 // (image_io.py:181-203) and the angle's exact sums (support pixels, sum of
-// the masked probe b = probe * sel, sum of b^2).  The window pixel
-// (r, j) of K index r * kr + j (j < kr: the row padded to kr columns) is
-// written into the u8 m16n8k32 B fragment of its angle group:
-//   bfrag[((group * ksteps + ks) * BT + tile) * 32 + lane] = {b0, b1},
-//   b0 = B[k = 4t .. 4t+3][n = g], b1 = B[k = 16 + 4t ..][n = g]
-// (g = lane >> 2, t = lane & 3), tile < NT: masked probe, else support.
+// the masked probe b = probe * sel, sum of b^2).  Window pixel (r, j) is K
+// index p = r * kr + j (j < kr: rows padded to 16 bytes); stage
+// c = p / KB of angle group g holds two B blocks (masked probes, supports)
+// of NB rows (angle within the group) x KB bytes in the canonical layout:
+//   bops[((g * n_chunks + c) * 2 + blk) * B_BYTES + canon(angle, p % KB)].
 __global__ void probe_rotate_kernel(const uint8_t* __restrict__ base, int m, int kr, int na,
                                     const double* __restrict__ cs, const double* __restrict__ sn,
-                                    uint8_t* __restrict__ bfrag, long long* __restrict__ stats) {
+                                    uint8_t* __restrict__ bops, long long* __restrict__ stats) {
     const int a = blockIdx.x;
     const double c = cs[a], s = sn[a], ns = -sn[a];
     const double cx = __ddiv_rn((double)(m - 1), 2.0), cy = cx;
-    const int group = a / MAX_GROUP_ANGLES, ag = a % MAX_GROUP_ANGLES, nt = ag / 8, ncol = ag % 8;
-    const long long ksteps = (long long)m * kr / 32;
+    const int group = a / MAX_GROUP_ANGLES, ag = a % MAX_GROUP_ANGLES;
+    const long long n_chunks = n_stages_of(m);
     long long nm = 0, bs = 0, bq = 0;
     for (long long p = threadIdx.x; p < (long long)m * kr; p += blockDim.x) {
         const int gy = (int)(p / kr), gx = (int)(p % kr);
@@ -114,15 +136,10 @@ __global__ void probe_rotate_kernel(const uint8_t* __restrict__ base, int m, int
         nm += sel;
         bs += b;
         bq += (long long)b * b;
-        // fragment position of (k = p % 32 within k-step ks, n = ncol)
-        const long long ks = p / 32;
-        const int k = (int)(p % 32);
-        const int hi16 = k >= 16, kk = k & 15, t = kk >> 2, byte = kk & 3;
-        const int lane = ncol * 4 + t;
-        const long long slot0 = (((long long)group * ksteps + ks) * BT + nt) * 32 + lane;
-        const long long slot1 = (((long long)group * ksteps + ks) * BT + NT + nt) * 32 + lane;
-        bfrag[slot0 * 8 + hi16 * 4 + byte] = (uint8_t)b;
-        bfrag[slot1 * 8 + hi16 * 4 + byte] = (uint8_t)sel;
+        const long long blk = ((long long)group * n_chunks + p / KB) * 2;
+        const int off = canon(ag, (int)(p % KB));
+        bops[blk * B_BYTES + off] = (uint8_t)b;
+        bops[(blk + 1) * B_BYTES + off] = (uint8_t)sel;
     }
     __shared__ long long red[3][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -142,19 +159,59 @@ __global__ void probe_rotate_kernel(const uint8_t* __restrict__ base, int m, int
     }
 }
 
-__device__ __forceinline__ void mma_u8(int (&d)[4], const unsigned (&a)[4], uint2 b) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
-}
-
-// 4 bytes at an arbitrary address (two aligned loads and a funnel shift)
-__device__ __forceinline__ unsigned ld_u32_unaligned(const uint8_t* p) {
+// 16 bytes at an arbitrary address (five aligned words and funnel shifts)
+__device__ __forceinline__ uint4 ld16_unaligned(const uint8_t* p) {
     const uintptr_t u = reinterpret_cast<uintptr_t>(p);
     const unsigned* q = reinterpret_cast<const unsigned*>(u & ~(uintptr_t)3);
-    return __funnelshift_r(__ldg(q), __ldg(q + 1), (unsigned)(u & 3) * 8);
+    const unsigned sh = (unsigned)(u & 3) * 8;
+    const unsigned w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3), w4 = __ldg(q + 4);
+    return make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                      __funnelshift_r(w3, w4, sh));
 }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// shared-memory matrix descriptor: canonical K-major, no swizzle, LBO = 128
+// bytes (the next 16 bytes of K), SBO = CM_SBO (the next 8 rows), version 1
+__device__ __forceinline__ unsigned long long umma_desc(unsigned saddr) {
+    return (unsigned long long)((saddr >> 4) & 0x3fffu) | ((unsigned long long)(128 >> 4) << 16) |
+           ((unsigned long long)(CM_SBO >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A and B unsigned 8-bit,
+// both K-major, N = NB (bits 17-22 = N >> 3), M = TM (bits 24-28 = M >> 4)
+constexpr unsigned IDESC = (2u << 4) | ((unsigned)(NB >> 3) << 17) | ((unsigned)(TM >> 4) << 24);
+
+__device__ __forceinline__ void umma_u8(unsigned tmem_d, unsigned long long da, unsigned long long db, bool acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(IDESC), "r"((unsigned)acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// 8 consecutive 32-bit TMEM columns of this thread's lane (32x32b shape: warp w reads lanes 32w..32w+31)
+__device__ __forceinline__ void tmem_ld8(unsigned taddr, unsigned (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct Best {
     double score;
@@ -175,99 +232,161 @@ __device__ __forceinline__ double ncc_score(long long ab, long long a_sum_i, lon
     return __ddiv_rn(num, __dsqrt_rn(__dmul_rn(var_a, var_b)));
 }
 
-// One CTA per TM candidates, one warp per 16: K loops over the window rows
-// r (and kr/32 segments of each); every k-step gathers the 32-pixel segment
-// of the warp's 16 windows from the three planes into A fragments and runs
-// 4 x NT mma: I x probe, I x support, Hi x support, Lo x support.
-// r_flush > 0: int32 accumulators move into int64 shared memory every
-// r_flush rows (sums of up to r_flush * m pixels of 255^2 fit int32).
-__global__ void __launch_bounds__(FUSED_WARPS * 32) fused_kernel(
+// One CTA of 256 threads per TM candidates.  Stage c covers K bytes
+// [c KB, (c + 1) KB) of the windows: every thread gathers 6 of the 3 x 128 x 4
+// 16-byte pieces of the three A planes (4 consecutive threads per candidate,
+// so a warp reads 8 candidates' contiguous row segments; each piece lies in
+// one window row) and up to 2 of the 384 16-byte pieces of the stage's B
+// blocks; after a proxy fence and a barrier thread 0 issues 2 k-steps x 4
+// UMMAs and commits them to the stage's mbarrier, which the threads wait on
+// before refilling that stage NSTAGE stages later.  flush_rows > 0: every
+// flush_rows window rows each thread adds its I x P columns (24 of its
+// candidate's 48) into int64 registers and the accumulator restarts.
+__global__ void __launch_bounds__(THREADS, 1) fused_kernel(
     const uint8_t* __restrict__ planes, long long pitch, long long plane_stride, const int* __restrict__ rows,
-    int row_cols, long long first, long long count, int m, int kr, const uint2* __restrict__ bfrag, int na_g, int a0,
-    const long long* __restrict__ stats, int r_flush, double* __restrict__ part_score,
+    int row_cols, long long first, long long count, int m, int kr, const uint8_t* __restrict__ bops, int na_g,
+    int a0, const long long* __restrict__ stats, int flush_rows, double* __restrict__ part_score,
     long long* __restrict__ part_idx) {
-    extern __shared__ long long acc64[];  // [threads][4 * NT * 4] when r_flush > 0
-    __shared__ double sc[TM][MAX_GROUP_ANGLES];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-    const long long cb = (long long)blockIdx.x * TM + warp * 16;
-    const long long ci0 = cb + g, ci1 = cb + g + 8;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) unsigned long long mma_bar[NSTAGE];
+    __shared__ unsigned tmem_base_sh;
+    __shared__ long long orig[TM];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lanes 32 quad .., column half
     const int lo = (m - 1) / 2;
-    auto origin = [&](long long ci) -> long long {
+    if (tid < TM) {
+        const long long ci = (long long)blockIdx.x * TM + tid;
         const long long r = first + (ci < count ? ci : 0);
-        return (long long)(rows[r * row_cols + 1] - lo) * pitch + (rows[r * row_cols] - lo);
-    };
-    const long long o0 = origin(ci0), o1 = origin(ci1);
-    int acc[4][NT][4];
+        orig[tid] = (long long)(rows[r * row_cols + 1] - lo) * pitch + (rows[r * row_cols] - lo);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&mma_bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tmem = tmem_base_sh;
+    const unsigned sbase = smem_u32(smem);
+    const unsigned trow = tmem + ((unsigned)(quad * 32) << 16);
+    const int row = quad * 32 + (tid & 31);  // this thread's candidate row in the epilogue
+    constexpr int HALF_COLS = NB / 2;        // 24 I x P columns per thread
+    long long ipacc[HALF_COLS];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int e = 0; e < HALF_COLS; ++e) ipacc[e] = 0;
+    const long long kwin = (long long)m * kr;  // K bytes of one window
+    const int n_chunks = (int)n_stages_of(m);
+    const int kc = tid & 3;  // this thread's 16-byte piece of every row segment
+    bool ip_acc = false;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int s = c % NSTAGE;
+        if (c >= NSTAGE) mbar_wait(&mma_bar[s], (unsigned)((c / NSTAGE) - 1) & 1u);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        const long long k0 = (long long)c * KB + kc * 16;
+        const bool live = k0 < kwin;
+        const int r = live ? (int)(k0 / kr) : 0;
+        const long long roff = (long long)r * pitch + (k0 - (long long)r * kr);
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[q][j][e] = 0;
-    const int segs = kr / 32;
-    long long* my64 = acc64 + (long long)threadIdx.x * (4 * NT * 4);
-    if (r_flush > 0)
-        for (int i = 0; i < 4 * NT * 4; ++i) my64[i] = 0;
-    for (int r = 0; r < m; ++r) {
-        const long long rowoff = (long long)r * pitch;
-        for (int sg = 0; sg < segs; ++sg) {
-            const long long ks = (long long)r * segs + sg;
-            const int col = sg * 32;
-            unsigned A[3][4];
-#pragma unroll
-            for (int p = 0; p < 3; ++p) {
-                const uint8_t* pl = planes + p * plane_stride + rowoff + col + 4 * t;
-                A[p][0] = ld_u32_unaligned(pl + o0);
-                A[p][1] = ld_u32_unaligned(pl + o1);
-                A[p][2] = ld_u32_unaligned(pl + o0 + 16);
-                A[p][3] = ld_u32_unaligned(pl + o1 + 16);
-            }
-            const uint2* bf = bfrag + ks * BT * 32 + lane;
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const uint2 bp = __ldg(bf + j * 32), bm = __ldg(bf + (NT + j) * 32);
-                mma_u8(acc[0][j], A[0], bp);
-                mma_u8(acc[1][j], A[0], bm);
-                mma_u8(acc[2][j], A[1], bm);
-                mma_u8(acc[3][j], A[2], bm);
-            }
+        for (int i = 0; i < 6; ++i) {
+            const int q = tid + THREADS * i;
+            const int p = q >> 9, cand = (q >> 2) & (TM - 1);
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (live) v = ld16_unaligned(planes + p * plane_stride + orig[cand] + roff);
+            *reinterpret_cast<uint4*>(st + p * A_BYTES + canon(cand, kc * 16)) = v;
         }
-        if (r_flush > 0 && ((r + 1) % r_flush == 0 || r + 1 == m)) {
+        const uint4* bsrc = reinterpret_cast<const uint4*>(bops + (size_t)c * 2 * B_BYTES);
+        uint4* bdst = reinterpret_cast<uint4*>(st + 3 * A_BYTES);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+        for (int i = 0; i < 2; ++i) {
+            const int q = tid + THREADS * i;
+            if (q < 2 * B_BYTES / 16) bdst[q] = __ldg(bsrc + q);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const unsigned sa = sbase + s * STAGE_BYTES;
 #pragma unroll
-                for (int j = 0; j < NT; ++j)
+            for (int ks = 0; ks < KB / 32; ++ks) {
+                const unsigned k = ks * 256;  // 32 bytes of K = two core matrices
+                const unsigned long long dbp = umma_desc(sa + 3 * A_BYTES + k);
+                const unsigned long long dbm = umma_desc(sa + 3 * A_BYTES + B_BYTES + k);
+                const bool acc = c > 0 || ks > 0;
+                umma_u8(tmem + 0, umma_desc(sa + k), dbp, ip_acc || ks > 0);
+                umma_u8(tmem + NB, umma_desc(sa + k), dbm, acc);
+                umma_u8(tmem + 2 * NB, umma_desc(sa + A_BYTES + k), dbm, acc);
+                umma_u8(tmem + 3 * NB, umma_desc(sa + 2 * A_BYTES + k), dbm, acc);
+            }
+            umma_commit(&mma_bar[s]);
+        }
+        ip_acc = true;
+        // the window row the next stage starts in
+        const long long k_next = (long long)(c + 1) * KB;
+        if (flush_rows > 0 && k_next < kwin && (k_next / kr) / flush_rows != ((long long)c * KB / kr) / flush_rows) {
+            // drain I x P (< 2^31 so far) into int64 and restart it
+            mbar_wait(&mma_bar[s], (unsigned)(c / NSTAGE) & 1u);
+            tc_fence_after();
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        my64[(q * NT + j) * 4 + e] += acc[q][j][e];
-                        acc[q][j][e] = 0;
-                    }
+            for (int j = 0; j < HALF_COLS / 8; ++j) {
+                unsigned v[8];
+                tmem_ld8(trow + HALF_COLS * half + 8 * j, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ipacc[8 * j + e] += (long long)v[e];
+            }
+            tc_fence_before();
+            __syncthreads();
+            ip_acc = false;
         }
     }
-    // epilogue: this thread holds rows g, g+8 x columns 2t, 2t+1 of every n-tile
+    {
+        const int cl = n_chunks - 1;
+        mbar_wait(&mma_bar[cl % NSTAGE], (unsigned)(cl / NSTAGE) & 1u);
+    }
+    tc_fence_after();
+    // epilogue: this thread = candidate `row` (TMEM lane), angles [24 half, 24 half + 24)
+    double* sc = reinterpret_cast<double*>(smem);  // [TM][MAX_GROUP_ANGLES]: the stages are idle now
+    const long long ci = (long long)blockIdx.x * TM + row;
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+    for (int j = 0; j < HALF_COLS / 8; ++j) {
+        const int col = HALF_COLS * half + 8 * j;
+        if (col >= MAX_GROUP_ANGLES) break;
+        unsigned ip[8], im[8], hi[8], lw[8];
+        tmem_ld8(trow + col, ip);
+        tmem_ld8(trow + NB + col, im);
+        tmem_ld8(trow + 2 * NB + col, hi);
+        tmem_ld8(trow + 3 * NB + col, lw);
+        tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int row = warp * 16 + g + (e >= 2 ? 8 : 0);
-            const int ag = j * 8 + 2 * t + (e & 1);
-            long long v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = r_flush > 0 ? my64[(q * NT + j) * 4 + e] : (long long)acc[q][j][e];
-            const long long ci = (long long)blockIdx.x * TM + row;
+        for (int e = 0; e < 8; ++e) {
+            const int ag = col + e;
+            const long long vip = (long long)ip[e] + ipacc[8 * j + e];
             double score = -1.0 / 0.0;
-            if (ag < na_g && ci < count) score = ncc_score(v[0], v[1], 256 * v[2] + v[3], stats + (a0 + ag) * 3);
-            sc[row][ag] = score;
+            if (ag < na_g && ci < count)
+                score = ncc_score(vip, (long long)im[e], 256LL * hi[e] + lw[e], stats + (a0 + ag) * 3);
+            sc[row * MAX_GROUP_ANGLES + ag] = score;
         }
+    }
+    tc_fence_before();
     __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+    }
     // best per angle over this CTA's candidates (np.argmax: the first on ties)
-    for (int ag = threadIdx.x; ag < na_g; ag += blockDim.x) {
+    for (int ag = tid; ag < na_g; ag += THREADS) {
         Best b{-1.0 / 0.0, -1};
-        for (int row = 0; row < TM; ++row) {
-            const long long ci = (long long)blockIdx.x * TM + row;
-            if (ci >= count) break;
-            const Best c{sc[row][ag], ci};
-            if (b.idx < 0 || better(c, b)) b = c;
+        for (int rr = 0; rr < TM; ++rr) {
+            const long long cr = (long long)blockIdx.x * TM + rr;
+            if (cr >= count) break;
+            const Best cb{sc[rr * MAX_GROUP_ANGLES + ag], cr};
+            if (b.idx < 0 || better(cb, b)) b = cb;
         }
         part_score[(long long)blockIdx.x * MAX_GROUP_ANGLES + ag] = b.score;
         part_idx[(long long)blockIdx.x * MAX_GROUP_ANGLES + ag] = b.idx;
@@ -322,8 +441,8 @@ int ss_match_planes(const uint8_t* d_img, int64_t W, int64_t H, uint8_t* d_plane
 }
 
 size_t ss_match_probe_bytes(int32_t m, int32_t n_angles) {
-    const int64_t kr = (m + 31) / 32 * 32, groups = (n_angles + ss::MAX_GROUP_ANGLES - 1) / ss::MAX_GROUP_ANGLES;
-    return (size_t)groups * (size_t)(m * kr / 32) * ss::BT * 32 * 8;
+    const int64_t groups = (n_angles + ss::MAX_GROUP_ANGLES - 1) / ss::MAX_GROUP_ANGLES;
+    return (size_t)groups * (size_t)ss::n_stages_of(m) * 2 * ss::B_BYTES;
 }
 
 int ss_match_probes(const uint8_t* d_template, int32_t n, int32_t m, int32_t n_angles, const double* d_cos,
@@ -338,7 +457,7 @@ int ss_match_probes(const uint8_t* d_template, int32_t n, int32_t m, int32_t n_a
     ss::probe_base_kernel<<<(unsigned)((m * m + 255) / 256), 256, 0, s>>>(d_template, n, m, d_base);
     ss::note_launch();
     if (int e = ss::check_launch("probe_base_kernel")) return e;
-    ss::probe_rotate_kernel<<<(unsigned)n_angles, 256, 0, s>>>(d_base, m, (m + 31) / 32 * 32, n_angles, d_cos, d_sin,
+    ss::probe_rotate_kernel<<<(unsigned)n_angles, 256, 0, s>>>(d_base, m, ss::row_bytes(m), n_angles, d_cos, d_sin,
                                                               d_bfrag, d_stats);
     ss::note_launch();
     return ss::check_launch("probe_rotate_kernel");
@@ -357,20 +476,19 @@ int ss_match_fused(const uint8_t* d_planes, int64_t W, int64_t H, int64_t pitch,
         return SS_EINVAL;
     }
     cudaStream_t s = ss::as_stream(stream);
-    const int kr = (m + 31) / 32 * 32;
+    const int kr = ss::row_bytes(m);
     const int a0 = group * ss::MAX_GROUP_ANGLES, na_g = std::min(ss::MAX_GROUP_ANGLES, (int)n_angles - a0);
-    const long long ksteps = (long long)m * kr / 32;
-    const uint2* bf = reinterpret_cast<const uint2*>(d_bfrag) + (long long)group * ksteps * ss::BT * 32;
-    // rows of m pixels whose sums fit int32 (255^2 per pixel)
+    const uint8_t* bops = d_bfrag + (size_t)group * ss::n_stages_of(m) * 2 * ss::B_BYTES;
+    // window rows whose I x P sums fit int32 (255^2 per pixel); a stage can
+    // straddle a flush boundary by part of one row (kr >= 192 when flushing)
     const long long rows_fit = 2147483647LL / (65025LL * m);
-    const int r_flush = rows_fit >= m ? 0 : (int)std::max<long long>(1, rows_fit);
-    const size_t smem = r_flush > 0 ? (size_t)ss::FUSED_WARPS * 32 * 4 * ss::NT * 4 * sizeof(long long) : 0;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(ss::fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int flush_rows = rows_fit >= m ? 0 : (int)std::max<long long>(1, rows_fit - 1);
+    const size_t smem = (size_t)ss::NSTAGE * ss::STAGE_BYTES;
+    cudaFuncSetAttribute(ss::fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const long long parts = ss_match_parts(count);
-    ss::fused_kernel<<<(unsigned)parts, ss::FUSED_WARPS * 32, smem, s>>>(
-        d_planes, pitch, pitch * H, d_rows, row_cols, first, count, m, kr, bf, na_g, a0, d_stats, r_flush,
-        d_part_score, d_part_idx);
+    ss::fused_kernel<<<(unsigned)parts, ss::THREADS, smem, s>>>(d_planes, pitch, pitch * H, d_rows, row_cols, first,
+                                                              count, m, kr, bops, na_g, a0, d_stats, flush_rows,
+                                                              d_part_score, d_part_idx);
     ss::note_launch();
     if (int e = ss::check_launch("fused_kernel")) return e;
     ss::reduce_kernel<<<(unsigned)na_g, 256, 0, s>>>(d_part_score, d_part_idx, parts, na_g, d_best_score + a0,

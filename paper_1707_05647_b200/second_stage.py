@@ -13,11 +13,12 @@ Per ladder size (ascending, as the reference iterates ``sorted(by_size)``):
   the rotation's cos / sin come from NumPy, as in the reference, so the
   probes are bit-identical;
 * ``ss_match_fused`` gathers the candidates' windows straight from the
-  image into u8 tensor-core fragments and computes ``W @ [P | M]`` and
-  ``(W * W) @ M`` (second_stage.py:136-150; W^2 as its high and low bytes)
-  with u8 x u8 -> s32 MMAs -- exact integers, like the reference's float64
-  products of integer data -- then replays the reference's float64 score
-  sequence op for op and reduces to the best candidate per angle.
+  image into shared memory (the UMMA canonical layout) and computes
+  ``W @ [P | M]`` and ``(W * W) @ M`` (second_stage.py:136-150; W^2 as its
+  high and low bytes) with tcgen05.mma kind::i8 (u8 x u8 -> s32, TMEM
+  accumulators) -- exact integers, like the reference's float64 products of
+  integer data -- then replays the reference's float64 score sequence op for
+  op and reduces to the best candidate per angle.
 
 There is no CPU fallback.
 """

@@ -284,6 +284,21 @@ def match_fixture():
         out[f"{key}/template"] = tpl
         out[f"{key}/step"] = np.array(10.0)
         out[f"{key}/result"] = np.array([r.cx, r.cy, r.scale, r.angle, r.score], np.float64)
+    # ladder sizes whose I x P dot products pass 2^31 (m >= 182): the GPU
+    # kernel drains that accumulator into int64 every few window rows
+    flush = {"flush192": (300, 260, 777, 80, 100, 96, 30.0), "flush264": (380, 330, 778, 100, 120, 132, 45.0)}
+    for key, (w, h, seed, y0, x0, side, step) in flush.items():
+        scene = make_textured_scene(w, h, seed=seed)
+        tpl = np.ascontiguousarray(scene[y0:y0 + side, x0:x0 + side])
+        kw = {"alpha": 1.9, "beta": 2.0, "quantizer": (16.0, 16.0, 16.0)}
+        res = S.screen(scene, tpl, _cfg(kw))
+        r = M.match_candidates(scene, tpl, res, angle_step=step)
+        names.append(key)
+        out[f"{key}/image"] = scene
+        out[f"{key}/template"] = tpl
+        out[f"{key}/cfg"] = np.array(json.dumps(kw))
+        out[f"{key}/step"] = np.array(step)
+        out[f"{key}/result"] = np.array([r.cx, r.cy, r.scale, r.angle, r.score], np.float64)
     out["names"] = np.array(names)
     np.savez_compressed(os.path.join(HERE, "match.npz"), **out)
 

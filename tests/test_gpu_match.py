@@ -32,7 +32,8 @@ def test_match_candidates_matches_reference(cuda, key):
     z = golden("match.npz")
     step = float(z[f"{key}/step"])
     if f"{key}/image" in z.files:
-        img, tpl, cfg = z[f"{key}/image"], z[f"{key}/template"], ScreeningConfig()
+        img, tpl = z[f"{key}/image"], z[f"{key}/template"]
+        cfg = _cfg(json.loads(str(z[f"{key}/cfg"]))) if f"{key}/cfg" in z.files else ScreeningConfig()
     else:
         c = load_screen_case(key.split("@")[0])
         img, tpl, cfg = c["image"], c["template"], _cfg(c["cfg"])
