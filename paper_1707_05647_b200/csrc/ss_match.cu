@@ -47,7 +47,7 @@ constexpr int B_BYTES = NB * KB;                             // one B block's st
 constexpr int STAGE_BYTES = 3 * A_BYTES + 2 * B_BYTES;       // 30 KB
 constexpr int CM_SBO = (KB / 16) * 128;                      // bytes between 8-row core-matrix groups
 constexpr int TMEM_COLS = 256;                               // IP [0,48) IM [48,96) HI [96,144) LO [144,192)
-constexpr int PLANE_PAD = 96;  // zero columns right of each plane row (the gather reads <= 67 bytes past a window)
+constexpr int PLANE_PAD = 96;  // zero columns right of each plane row (the gather reads < 80 bytes past a window)
 
 // Byte offset of (row, k) in a UMMA canonical K-major tile without swizzle:
 // 8 x 16-byte core matrices, the KB / 16 of one 8-row group side by side
@@ -159,14 +159,19 @@ __global__ void probe_rotate_kernel(const uint8_t* __restrict__ base, int m, int
     }
 }
 
-// 16 bytes at an arbitrary address (five aligned words and funnel shifts)
+// 16 bytes at an arbitrary address: the two aligned 16-byte blocks that
+// hold them, words wo .. wo + 4 selected, then funnel-shifted by the byte offset
 __device__ __forceinline__ uint4 ld16_unaligned(const uint8_t* p) {
     const uintptr_t u = reinterpret_cast<uintptr_t>(p);
-    const unsigned* q = reinterpret_cast<const unsigned*>(u & ~(uintptr_t)3);
-    const unsigned sh = (unsigned)(u & 3) * 8;
-    const unsigned w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3), w4 = __ldg(q + 4);
-    return make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
-                      __funnelshift_r(w3, w4, sh));
+    const uint4* q = reinterpret_cast<const uint4*>(u & ~(uintptr_t)15);
+    const uint4 a = __ldg(q), b = __ldg(q + 1);
+    const unsigned off = (unsigned)(u & 15), sh = (off & 3) * 8;
+    const bool w2 = off & 8, w1 = off & 4;
+    const unsigned t0 = w2 ? a.z : a.x, t1 = w2 ? a.w : a.y, t2 = w2 ? b.x : a.z, t3 = w2 ? b.y : a.w,
+                   t4 = w2 ? b.z : b.x, t5 = w2 ? b.w : b.y;
+    const unsigned s0 = w1 ? t1 : t0, s1 = w1 ? t2 : t1, s2 = w1 ? t3 : t2, s3 = w1 ? t4 : t3, s4 = w1 ? t5 : t4;
+    return make_uint4(__funnelshift_r(s0, s1, sh), __funnelshift_r(s1, s2, sh), __funnelshift_r(s2, s3, sh),
+                      __funnelshift_r(s3, s4, sh));
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
