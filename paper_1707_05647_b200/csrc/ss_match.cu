@@ -60,6 +60,13 @@ __host__ __device__ constexpr int row_bytes(int m) { return (m + 15) / 16 * 16; 
 // pipeline stages of one window (K = m * row_bytes(m), zero-padded to whole stages)
 __host__ __device__ constexpr long long n_stages_of(int m) { return ((long long)m * row_bytes(m) + KB - 1) / KB; }
 constexpr int THREADS = 256;  // 8 warps gather; warp w & 3 owns TMEM lanes 32 (w & 3) .. in the epilogue
+// Candidates per CTA: 128 (the full UMMA M) unless that leaves SMs of a
+// 148-SM B200 idle: then 64 or 32, the remaining accumulator rows unused
+// (measured: 128 -> 64 at 32k candidates of m = 128 is slower, the MMAs'
+// share is not negligible; below one CTA per SM the smaller tiles win).
+__host__ __device__ constexpr int tile_log2(long long count) {
+    return (count + 127) / 128 >= 148 ? 7 : ((count + 63) / 64 >= 148 ? 6 : 5);
+}
 
 // image_io.py:131-161 bilinear sample of img (h x w) at (xs, ys), quantized
 __device__ __forceinline__ int sample_q(const uint8_t* img, int w, int h, double xs, double ys) {
@@ -250,9 +257,10 @@ __device__ __forceinline__ double ncc_score(long long ab, long long a_sum_i, lon
 __global__ void __launch_bounds__(THREADS, 1) fused_kernel(
     const uint8_t* __restrict__ planes, long long pitch, long long plane_stride, const int* __restrict__ rows,
     int row_cols, long long first, long long count, int m, int kr, const uint8_t* __restrict__ bops, int na_g,
-    int a0, const long long* __restrict__ stats, int flush_rows, double* __restrict__ part_score,
+    int a0, const long long* __restrict__ stats, int flush_rows, int tl, double* __restrict__ part_score,
     long long* __restrict__ part_idx) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    const int tm = 1 << tl;  // candidates of this CTA (rows tm.. of the tile are unused)
     __shared__ __align__(8) unsigned long long mma_bar[NSTAGE];
     __shared__ unsigned tmem_base_sh;
     __shared__ long long orig[TM];
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(
     const int quad = warp & 3, half = warp >> 2;  // TMEM lanes 32 quad .., column half
     const int lo = (m - 1) / 2;
     if (tid < TM) {
-        const long long ci = (long long)blockIdx.x * TM + tid;
+        const long long ci = (long long)blockIdx.x * tm + (tid < tm ? tid : 0);
         const long long r = first + (ci < count ? ci : 0);
         orig[tid] = (long long)(rows[r * row_cols + 1] - lo) * pitch + (rows[r * row_cols] - lo);
     }
@@ -300,10 +308,12 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
             const int q = tid + THREADS * i;
-            const int p = q >> 9, cand = (q >> 2) & (TM - 1);
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (live) v = ld16_unaligned(planes + p * plane_stride + orig[cand] + roff);
-            *reinterpret_cast<uint4*>(st + p * A_BYTES + canon(cand, kc * 16)) = v;
+            const int p = q >> (tl + 2), cand = (q >> 2) & (tm - 1);
+            if (p < 3) {
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (live) v = ld16_unaligned(planes + p * plane_stride + orig[cand] + roff);
+                *reinterpret_cast<uint4*>(st + p * A_BYTES + canon(cand, kc * 16)) = v;
+            }
         }
         const uint4* bsrc = reinterpret_cast<const uint4*>(bops + (size_t)c * 2 * B_BYTES);
         uint4* bdst = reinterpret_cast<uint4*>(st + 3 * A_BYTES);
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(
     tc_fence_after();
     // epilogue: this thread = candidate `row` (TMEM lane), angles [24 half, 24 half + 24)
     double* sc = reinterpret_cast<double*>(smem);  // [TM][MAX_GROUP_ANGLES]: the stages are idle now
-    const long long ci = (long long)blockIdx.x * TM + row;
+    const long long ci = row < tm ? (long long)blockIdx.x * tm + row : count;
 #pragma unroll
     for (int j = 0; j < HALF_COLS / 8; ++j) {
         const int col = HALF_COLS * half + 8 * j;
@@ -387,8 +397,8 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(
     // best per angle over this CTA's candidates (np.argmax: the first on ties)
     for (int ag = tid; ag < na_g; ag += THREADS) {
         Best b{-1.0 / 0.0, -1};
-        for (int rr = 0; rr < TM; ++rr) {
-            const long long cr = (long long)blockIdx.x * TM + rr;
+        for (int rr = 0; rr < tm; ++rr) {
+            const long long cr = (long long)blockIdx.x * tm + rr;
             if (cr >= count) break;
             const Best cb{sc[rr * MAX_GROUP_ANGLES + ag], cr};
             if (b.idx < 0 || better(cb, b)) b = cb;
@@ -468,7 +478,10 @@ int ss_match_probes(const uint8_t* d_template, int32_t n, int32_t m, int32_t n_a
     return ss::check_launch("probe_rotate_kernel");
 }
 
-int64_t ss_match_parts(int64_t count) { return (count + ss::TM - 1) / ss::TM; }
+int64_t ss_match_parts(int64_t count) {
+    const int64_t tm = 1LL << ss::tile_log2(count);
+    return (count + tm - 1) / tm;
+}
 
 int ss_match_fused(const uint8_t* d_planes, int64_t W, int64_t H, int64_t pitch, const int32_t* d_rows,
                    int32_t row_cols, int64_t first, int64_t count, int32_t m, const uint8_t* d_bfrag, int32_t n_angles,
@@ -493,7 +506,7 @@ int ss_match_fused(const uint8_t* d_planes, int64_t W, int64_t H, int64_t pitch,
     const long long parts = ss_match_parts(count);
     ss::fused_kernel<<<(unsigned)parts, ss::THREADS, smem, s>>>(d_planes, pitch, pitch * H, d_rows, row_cols, first,
                                                               count, m, kr, bops, na_g, a0, d_stats, flush_rows,
-                                                              d_part_score, d_part_idx);
+                                                              ss::tile_log2(count), d_part_score, d_part_idx);
     ss::note_launch();
     if (int e = ss::check_launch("fused_kernel")) return e;
     ss::reduce_kernel<<<(unsigned)na_g, 256, 0, s>>>(d_part_score, d_part_idx, parts, na_g, d_best_score + a0,
