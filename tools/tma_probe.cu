@@ -38,7 +38,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 constexpr int CW = 16;  // consumer warps
 
-template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1>
+template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1, bool ODD = false>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     probe(const __grid_constant__ CUtensorMap map, int tiles, int cols, int rows, unsigned long long* sink) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -64,7 +64,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
                 __syncwarp((1u << NPROD) - 1u);
                 for (int b = lane; b < NBOX; b += NPROD) {
                     rng = rng * 1664525u + 1013904223u;
-                    const int x = (int)((rng >> 8) % (unsigned)(cols - BW)) & ~(16 / (int)sizeof(T) - 1);
+                    const int x = ODD ? (int)((rng >> 8) % (unsigned)(cols - BW))  // any element
+                                      : (int)((rng >> 8) % (unsigned)(cols - BW)) & ~(16 / (int)sizeof(T) - 1);
                     rng = rng * 1664525u + 1013904223u;
                     const int y = (int)((rng >> 8) % (unsigned)(rows - BR));
                     tma_load_2d(sm + s * STAGE + b * BOX, &map, x, y, &full[s]);
@@ -91,7 +92,7 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1>
+template <typename T, int BW, int BR, int NBOX, int STAGES, int NPROD = 1, bool ODD = false>
 void run(const char* name, void* plane, int cols, int rows, int ctas_per_sm) {
     static EncodeFn encode = nullptr;
     if (!encode) {
@@ -111,7 +112,7 @@ void run(const char* name, void* plane, int cols, int rows, int ctas_per_sm) {
         printf("%s: encode failed\n", name);
         return;
     }
-    auto k = probe<T, BW, BR, NBOX, STAGES, NPROD>;
+    auto k = probe<T, BW, BR, NBOX, STAGES, NPROD, ODD>;
     const int smem = STAGES * NBOX * BW * BR * (int)sizeof(T);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int sms = 148;
@@ -146,14 +147,9 @@ int main() {
     void* p;
     CK(cudaMalloc(&p, 64 << 20));
     CK(cudaMemset(p, 1, 64 << 20));
-    run<unsigned short, 232, 16, 8, 3>("u16 8 x (16x232) x3 [coarse now]", p, 4096, 4096, 1);
-    run<unsigned short, 232, 16, 8, 3, 2>("u16 8 x (16x232) x3 2 lanes", p, 4096, 4096, 1);
-    run<unsigned short, 232, 16, 8, 3, 4>("u16 8 x (16x232) x3 4 lanes", p, 4096, 4096, 1);
-    run<unsigned short, 232, 16, 8, 3, 8>("u16 8 x (16x232) x3 8 lanes", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 8, 3>("u16 8 x (16x256) x3", p, 4096, 4096, 1);
-    run<unsigned short, 256, 16, 8, 3, 4>("u16 8 x (16x256) x3 4 lanes", p, 4096, 4096, 1);
-    run<unsigned, 196, 16, 8, 2>("u32 8 x (16x196) x2 [stage1 u32]", p, 4096, 2048, 1);
-    run<unsigned, 196, 16, 8, 2, 4>("u32 8 x (16x196) x2 4 lanes", p, 4096, 2048, 1);
+    run<unsigned short, 232, 16, 8, 3, 8>("u16 8 x (16x232) x3 8 lanes [r2]", p, 4096, 4096, 1);
+    run<unsigned short, 256, 16, 8, 3, 8>("u16 8 x (16x256) x3 8 lanes aligned", p, 4096, 4096, 1);
+    run<unsigned short, 256, 16, 8, 3, 8, true>("u16 8 x (16x256) x3 8 lanes any start", p, 4096, 4096, 1);
     // HBM-resident (1 GB plane): the miss path
     void* q;
     CK(cudaMalloc(&q, 1ull << 30));
