@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constan
         if (threadIdx.x == 0) S.row_counts[y - a.mask_y0] = 0u;
         const bool row_grid = a.stride == 1 || y % a.stride == 0;
         const bool row_int = row_grid && y >= S.lo && y <= a.H - 1 - S.hi;
-        for (int w = threadIdx.x; w < words; w += blockDim.x) {
+        auto word = [&](int w) -> unsigned {
             const int x0 = w * 32;
             unsigned grid = 0;
             if (row_grid) {
@@ -797,8 +797,13 @@ __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constan
                 const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
                 if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
             }
-            row[w] = grid & ~inter;
-        }
+            return grid & ~inter;
+        };
+        // 16-byte stores where the rows allow (the masks are ~1 GB per step at config 4)
+        const int quads = (reinterpret_cast<uintptr_t>(row) & 15) == 0 ? words >> 2 : 0;
+        for (int q = threadIdx.x; q < quads; q += blockDim.x)
+            reinterpret_cast<uint4*>(row)[q] = make_uint4(word(4 * q), word(4 * q + 1), word(4 * q + 2), word(4 * q + 3));
+        for (int w = 4 * quads + threadIdx.x; w < words; w += blockDim.x) row[w] = word(w);
     }
 }
 
