@@ -49,7 +49,7 @@ DTYPE = ("u32 planes (cells mod 2^32) + u16 hi planes (cells mod 2^48 for sizes 
          "coarse bit slices (stage 1); fp32 cell estimates with the fp64 sequence near a boundary")
 DEFAULT_CONFIG = 4
 BAND_CONFIGS = (2, 4)  # BASELINE.json: one large image, row bands with halo across GPUs
-POOL_ENGINES = int(os.environ.get("SS_POOL_ENGINES", "4"))  # engines screening a batch's images concurrently
+POOL_ENGINES = int(os.environ.get("SS_POOL_ENGINES", "6"))  # sessions screening a batch's images concurrently (measured: 6 beats 2, 4, 8)
 ISSUE_PER_CLK = 4  # warp instructions issued per SM per clock (4 SMSPs)
 
 

@@ -207,6 +207,20 @@ int64_t grid_count(int64_t limit, int64_t lo, int64_t hi, int64_t stride) {
 
 constexpr int MIN_PATCH_SIDE = 8;  // screening.py:50
 
+// restores the calling thread's current device (a session call switches to the session's)
+struct DeviceGuard {
+    int dev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&dev) != cudaSuccess) {
+            cudaGetLastError();
+            dev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (dev >= 0) cudaSetDevice(dev);
+    }
+};
+
 // SS_SESSION_TRACE=1: per-phase host times and main-stream GPU times to stderr (experiments)
 struct Trace {
     bool on = false;
@@ -535,6 +549,7 @@ int screen_locked(ss_session& s, const uint8_t* h_img, const uint8_t* h_tpl, int
 
 void destroy(ss_session* s) {
     if (!s) return;
+    DeviceGuard guard;
     cudaSetDevice(s->device);
     for (DevBuf* b : {&s->img, &s->planes32, &s->planes64, &s->hi16, &s->coarse, &s->build_ws, &s->ladder_ws,
                       &s->masks, &s->row_counts, &s->counts, &s->compact_ws, &s->region, &s->region_ws, &s->xy,
@@ -557,6 +572,7 @@ extern "C" int ss_session_create(int32_t device, int64_t W, int64_t H, ss_sessio
         return SS_EINVAL;
     }
     *out = nullptr;
+    DeviceGuard guard;
     ss_session* s = new ss_session();
     s->device = device;
     s->W = W;
@@ -589,6 +605,7 @@ extern "C" int ss_session_screen(ss_session* s, const uint8_t* h_img, const uint
     }
     std::lock_guard<std::mutex> lk(s->mu);
     out->kept = out->region_pixels = out->tested = 0;
+    DeviceGuard guard;  // the caller's current device is restored on return
     return screen_locked(*s, h_img, h_template, n, *plan, *out);
 }
 
@@ -604,6 +621,7 @@ extern "C" int ss_session_rows(ss_session* s, int32_t* h_rows, int64_t first, in
         return SS_EINVAL;
     }
     if (count == 0) return SS_OK;
+    DeviceGuard guard;
     SS_TRY(cuda_ok(cudaSetDevice(s->device), "set device"));
     return cuda_ok(cudaMemcpy(h_rows, static_cast<const int32_t*>(s->xy.p) + first * 3, (size_t)count * 12,
                               cudaMemcpyDeviceToHost),
