@@ -336,6 +336,142 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     }
 }
 
+// Pass 1, direct form: a band's zero-carry end state without running the row
+// recurrences.  Unrolling them over the band's rows y0..e (e = y0 + RB - 1):
+//   S_e(x)  = sum_y P_y(x)
+//   FF_e(x) = sum_y P_y(x + e - y)            (P_y(z) = P_y(W-1) for z >= W)
+//   GG_e(x) = sum_y P_y(x - 1 - e + y)        (P_y(z) = 0 for z < 0)
+// With a group-aligned base B <= every z a tile needs, P_y(z) = R_y +
+// sum_{B <= i <= z} v(i,y) (R_y = rowpre_y(B)), so each state is sum_y R_y
+// plus a prefix over x of line sums of the band's pixels: column sums C(p)
+// for S, anti-diagonal sums A(u) = sum_y v(u + e - y, y) for FF, diagonal sums
+// D(w) = sum_y v(w - 1 - e + y, y) for GG (pixels left of B count as zero).
+// Per line three small sums (v, y_local v, v^2) give all four kinds; the
+// image tile is staged in shared memory; one block scan per state.  Replaces
+// band_kernel<0>'s RB row steps of 12 recurrences (config 4: 2.8 ms).
+constexpr int P1_TPB = 256;
+constexpr int P1_K = 3;  // line positions per thread
+constexpr int P1_L = P1_TPB * P1_K;
+// state columns owned per CTA: the positions also cover the halo P0 .. xa
+// (at most 2 RB + 15 columns)
+__host__ __device__ constexpr int p1_cw(int rb) { return P1_L - 2 * rb - 16; }
+// tile columns: the L positions, RB on each side, and up to 15 of 16-byte alignment
+__host__ __device__ constexpr int p1_tw(int rb) { return (P1_L + 2 * rb + 15 + 15) & ~15; }
+__host__ __device__ constexpr size_t p1_smem(int rb) { return (size_t)rb * p1_tw(rb); }
+
+template <int RB, typename V>
+__global__ void __launch_bounds__(P1_TPB) band_state_kernel(BuildArgs a) {
+    constexpr int L = P1_L, CW = p1_cw(RB), TW = p1_tw(RB);
+    constexpr int OFF = RB + 1;
+    extern __shared__ __align__(16) unsigned char p1_tile[];
+    auto tile = reinterpret_cast<unsigned char(*)[TW]>(p1_tile);
+    __shared__ V wtot[3][P1_TPB / 32][4];
+    __shared__ V sR[4];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t W = a.W;
+    const int64_t band = a.band0 + blockIdx.y;
+    const int64_t y0 = band * RB;
+    const int64_t xa = -OFF + (int64_t)blockIdx.x * CW;  // owned x in [xa, xa + CW)
+    int64_t B = xa - RB - 1;
+    B = B <= 0 ? 0 : (B / kGroup) * kGroup;
+    const int64_t P0 = B - RB + 1 < xa ? B - RB + 1 : xa;  // first line position
+    const int64_t T0 = (P0 - RB) & ~(int64_t)15;            // tile column 0 (16-aligned image column)
+    const int OC = (int)(P0 - T0);                          // tile column of position P0 (RB .. RB + 15)
+    // stage the band's pixels of columns [T0, T0 + TW): zero left of B and from W on
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.img) | (uintptr_t)a.img_pitch) & 15) == 0;
+    for (int q = t; q < RB * (TW / 16); q += P1_TPB) {
+        const int r = q / (TW / 16), c = (q - r * (TW / 16)) * 16;
+        const int64_t i = T0 + c;
+        const uint8_t* src = a.img + (y0 + r) * a.img_pitch + i;
+        uint4 v;
+        if (vec && i >= B && i + 16 <= W) {
+            v = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+            unsigned w[4] = {0, 0, 0, 0};
+            for (int b = 0; b < 16; ++b)
+                if (i + b >= B && i + b < W) w[b >> 2] |= (unsigned)__ldg(src + b) << (8 * (b & 3));
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        *reinterpret_cast<uint4*>(&tile[r][c]) = v;
+    }
+    // sum_y R_y per kind (PLAIN, X, Y, SQ), R_y = rowpre_y(B): warp 0 over the band's rows
+    if (warp == 0) {
+        long long R[4] = {0, 0, 0, 0};
+        const int64_t g = B / kGroup;
+        for (int r = lane; r < RB; r += 32) {
+            const long long r0 = rowpre_at(a, y0 + r, g, 0);
+            R[0] += r0;
+            R[1] += rowpre_at(a, y0 + r, g, 1);
+            R[2] += (long long)(y0 + r + 1) * r0;
+            R[3] += rowpre_at(a, y0 + r, g, 2);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) R[k] += shfl_down64(R[k], d);
+            if (lane == 0) sR[k] = (V)R[k];
+        }
+    }
+    __syncthreads();
+    // type 0 (S): column lines (p, y); type 1 (FF): anti-diagonals (p + e - y, y);
+    // type 2 (GG): diagonals (p - 1 - e + y, y) = (p - RB + r, y0 + r).
+    // X weight of a pixel on the line of p: (p + xo) + dr r.
+#pragma unroll 1
+    for (int ty = 0; ty < 3; ++ty) {
+        const int cb = OC + (ty == 0 ? 0 : (ty == 1 ? RB - 1 : -RB));
+        const int dr = ty == 0 ? 0 : (ty == 1 ? -1 : 1);
+        const V xo = (V)(ty == 0 ? 1 : (ty == 1 ? RB : 1 - RB));
+        V inc[P1_K][4];
+#pragma unroll
+        for (int j = 0; j < P1_K; ++j) {
+            const int pc = t * P1_K + j;  // p - P0
+            const unsigned char* col = &tile[0][cb + pc];
+            int sv = 0, sy = 0, sq = 0;
+#pragma unroll 9
+            for (int r = 0; r < RB; ++r) {
+                const int v = col[r * (TW + dr)];
+                sv += v;
+                sy += r * v;
+                sq += v * v;
+            }
+            const V p = (V)(P0 + pc);
+            inc[j][0] = (V)sv;
+            inc[j][1] = (p + xo) * (V)sv + (V)(dr * sy);
+            inc[j][2] = (V)(y0 + 1) * (V)sv + (V)sy;
+            inc[j][3] = (V)sq;
+        }
+        // inclusive prefix over positions: thread-local, warp, block
+#pragma unroll
+        for (int j = 1; j < P1_K; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) inc[j][k] += inc[j - 1][k];
+        V ex[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            V v = inc[P1_K - 1][k];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const V o = shfl_up64(v, d);
+                if (lane >= d) v += o;
+            }
+            if (lane == 31) wtot[ty][warp][k] = v;
+            ex[k] = v - inc[P1_K - 1][k] + sR[k];
+        }
+        __syncthreads();
+        for (int w = 0; w < warp; ++w)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ex[k] += wtot[ty][w][k];
+        const int64_t lo = ty == 0 ? 0 : (ty == 1 ? -OFF : 1), hi = ty == 0 ? W - 1 : (ty == 1 ? W - 2 : W + RB);
+#pragma unroll
+        for (int j = 0; j < P1_K; ++j) {
+            const int64_t x = P0 + t * P1_K + j;
+            if (x < xa || x >= xa + CW || x < lo || x > hi) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) st_ptr<V>(a, band, k, ty)[x + OFF] = ex[k] + inc[j][k];
+        }
+    }
+}
+
 // Row prefixes at group boundaries: rowpre[y][g] = sums over x < kGroup * g
 // of (v, (x+1) v, v^2), g = 0..G.  One warp per row.
 __global__ void rowpre_kernel(BuildArgs a, int64_t y0, int64_t y1) {
@@ -492,9 +628,29 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s, int64_t b_
     const int64_t s_hi = std::min(b_hi, nb);
     if (s_hi > b_lo) {
         a.band0 = b_lo;
-        band_kernel<0, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(s_hi - b_lo)), TPB, 0, s>>>(a);
+        // SS_BUILD_PASS1=rec: the recurrence form of pass 1 (A/B and tests)
+        static const bool rec = [] {
+            const char* e = getenv("SS_BUILD_PASS1");
+            return e && e[0] == 'r';
+        }();
+        if (rec) {
+            band_kernel<0, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(s_hi - b_lo)), TPB, 0, s>>>(a);
+        } else {
+            constexpr size_t smem = p1_smem(RB);
+            if (smem > 48 * 1024) {
+                static const cudaError_t attr = cudaFuncSetAttribute(
+                    band_state_kernel<RB, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (attr != cudaSuccess) {
+                    set_error("band_state_kernel smem attribute: %s", cudaGetErrorString(attr));
+                    return SS_ECUDA;
+                }
+            }
+            const int64_t span = W + 2 * (RB + 1);  // state x in [-(RB+1), W+RB]
+            const unsigned nx = (unsigned)((span + p1_cw(RB) - 1) / p1_cw(RB));
+            band_state_kernel<RB, V><<<dim3(nx, (unsigned)(s_hi - b_lo)), P1_TPB, smem, s>>>(a);
+        }
         note_launch();
-        if (int e = check_launch("band_kernel<local>")) return e;
+        if (int e = check_launch("band pass 1")) return e;
         band_scan_s_kernel<V><<<(unsigned)((4 * W + 255) / 256), 256, 0, s>>>(a, s_hi, RB, b_lo);
         note_launch();
         if (int e = check_launch("band_scan_s_kernel")) return e;
