@@ -92,8 +92,14 @@ __device__ __forceinline__ long long rowpre_at(const BuildArgs& a, int64_t y, in
 // mod 2^32: every operation is + - x, so the low 32 bits of the exact cells
 // follow from 32-bit arithmetic; writes the 32-bit planes only, with half the
 // registers, shuffles and band-state traffic).
-template <int kMode, int RB, typename V>
+// NK = 4: one CTA runs all four kinds; NK = 2: blockIdx.z picks the kinds
+// {0, 2} (PLAIN, Y) or {1, 3} (X, SQ) -- half the recurrence registers, so the
+// int64 build keeps more warps resident (pass 3 at config 4 ran 3 CTAs / SM).
+template <int kMode, int RB, typename V, int NK = 4>
 __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
+    static_assert(NK == 4 || NK == 2, "kinds per CTA");
+    const int kg = NK == 4 ? 0 : (int)blockIdx.z;
+    auto KIND = [&](int kk) { return NK == 4 ? kk : kg + 2 * kk; };
     constexpr int CW = kTileCols - 2 * RB - 2;
     constexpr int OFF = RB + 1;
     static_assert(CW % kGroup == 0 && (RB + 1) % kGroup == 0, "XL+1 must be group aligned");
@@ -111,10 +117,11 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
     __shared__ V sEdgeQ[2][TPB / 32][4];      // lane-31 GG_old[3]+P[3]
     __shared__ V sEdgeP[2][TPB / 32][4];      // lane-0 P[0]
 
-    V S[4][COLS], FF[4][COLS], GG[4][COLS];
+    V S[NK][COLS], FF[NK][COLS], GG[NK][COLS];
     // carry: state at row y0-1
     if (kMode == 1 && band > 0) {
-        for (int k = 0; k < 4; ++k) {
+        for (int kk = 0; kk < NK; ++kk) {
+            const int k = KIND(kk);
             const V* pS = st_ptr<V>(a, band - 1, k, 0);
             const V* pF = st_ptr<V>(a, band - 1, k, 1);
             const V* pG = st_ptr<V>(a, band - 1, k, 2);
@@ -122,16 +129,16 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 #pragma unroll
             for (int j = 0; j < COLS; ++j) {
                 const int64_t x = xb + j;
-                S[k][j] = (x < 0) ? 0 : (x > W - 1 ? swk : pS[x + OFF]);
-                FF[k][j] = (x >= W - 1) ? swk : (x < -OFF ? 0 : pF[x + OFF]);
-                GG[k][j] = (x <= 0 || x > W + RB) ? 0 : pG[x + OFF];
+                S[kk][j] = (x < 0) ? 0 : (x > W - 1 ? swk : pS[x + OFF]);
+                FF[kk][j] = (x >= W - 1) ? swk : (x < -OFF ? 0 : pF[x + OFF]);
+                GG[kk][j] = (x <= 0 || x > W + RB) ? 0 : pG[x + OFF];
             }
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int kk = 0; kk < NK; ++kk)
 #pragma unroll
-            for (int j = 0; j < COLS; ++j) S[k][j] = FF[k][j] = GG[k][j] = 0;
+            for (int j = 0; j < COLS; ++j) S[kk][j] = FF[kk][j] = GG[kk][j] = 0;
     }
 
     if (kMode == 1 && band == 0) {
@@ -139,6 +146,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
         const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;
         if (c >= c0 && c < c0 + CW && c < a.pitch) {
             for (int p = 0; p < 12; ++p) {
+                if (NK == 2 && (p & 1) != kg) continue;  // plane p holds kind p % 4
                 if (sizeof(V) == 8 && a.planes) {
                     long long* dst = a.planes + p * a.plane_stride + c;
                     reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(0, 0);
@@ -146,10 +154,12 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                 }
                 if (a.planes32) *reinterpret_cast<uint4*>(a.planes32 + p * a.plane_stride + c) = make_uint4(0, 0, 0, 0);
             }
-            for (int p = 0; p < 3 * a.n_coarse; ++p)
-                *reinterpret_cast<uint2*>(a.coarse + p * a.plane_stride + c) = make_uint2(0, 0);
+            if (kg == 0)
+                for (int p = 0; p < 3 * a.n_coarse; ++p)
+                    *reinterpret_cast<uint2*>(a.coarse + p * a.plane_stride + c) = make_uint2(0, 0);
             if (a.hi16)
-                for (int p = 0; p < 12; ++p) *reinterpret_cast<uint2*>(a.hi16 + p * a.plane_stride + c) = make_uint2(0, 0);
+                for (int p = 0; p < 12; ++p)
+                    if (NK == 4 || (p & 1) == kg) *reinterpret_cast<uint2*>(a.hi16 + p * a.plane_stride + c) = make_uint2(0, 0);
         }
     }
 
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
         if (lane == 31) { sTot[buf][warp][0] = tv; sTot[buf][warp][1] = tx; sTot[buf][warp][2] = tq; }
         if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) { sEdgeFF[buf][warp][k][0] = FF[k][0]; sEdgeFF[buf][warp][k][1] = FF[k][1]; }
+            for (int kk = 0; kk < NK; ++kk) { sEdgeFF[buf][warp][kk][0] = FF[kk][0]; sEdgeFF[buf][warp][kk][1] = FF[kk][1]; }
         }
         // exclusive thread prefix within the warp
         int ev = __shfl_up_sync(FULL, tv, 1), ex = __shfl_up_sync(FULL, tx, 1), eq = __shfl_up_sync(FULL, tq, 1);
@@ -208,60 +218,66 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
 
         // ── B: full row prefixes P for the 4 kinds ───────────────────────
         for (int w = 0; w < warp; ++w) { ev += sTot[buf][w][0]; ex += sTot[buf][w][1]; eq += sTot[buf][w][2]; }
-        V P[4][COLS];
+        V P[NK][COLS];
 #pragma unroll
         for (int j = 0; j < COLS; ++j) {
             const V cv = (V)(ev + lv[j]);
-            P[0][j] = (V)bv + cv;
-            P[1][j] = (V)bx + (V)(ex + lx[j]) + (V)(XL + 1) * cv;  // (i+1) = (i-XL) + (XL+1)
-            P[2][j] = (V)(y + 1) * P[0][j];
-            P[3][j] = (V)bq + (V)(eq + lq[j]);
-        }
-        V Q[4];
+            const V p0 = (V)bv + cv;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) Q[k] = GG[k][COLS - 1] + P[k][COLS - 1];
+            for (int kk = 0; kk < NK; ++kk) {
+                const int k = KIND(kk);
+                P[kk][j] = k == 0 ? p0
+                         : k == 1 ? (V)bx + (V)(ex + lx[j]) + (V)(XL + 1) * cv  // (i+1) = (i-XL) + (XL+1)
+                         : k == 2 ? (V)(y + 1) * p0
+                                  : (V)bq + (V)(eq + lq[j]);
+            }
+        }
+        V Q[NK];
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) Q[kk] = GG[kk][COLS - 1] + P[kk][COLS - 1];
         if (lane == 31) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sEdgeQ[buf][warp][k] = Q[k];
+            for (int kk = 0; kk < NK; ++kk) sEdgeQ[buf][warp][kk] = Q[kk];
         }
         if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sEdgeP[buf][warp][k] = P[k][0];
+            for (int kk = 0; kk < NK; ++kk) sEdgeP[buf][warp][kk] = P[kk][0];
         }
         __syncthreads();
 
         // ── C: advance the recurrences, emit planes ──────────────────────
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int kk = 0; kk < NK; ++kk) {
+            const int k = KIND(kk);
             // FF_new(x) = FF_old(x+1) + P(x)
-            V nf0 = shfl_down64(FF[k][0], 1);
-            V nf1 = shfl_down64(FF[k][1], 1);
-            V np0 = shfl_down64(P[k][0], 1);
+            V nf0 = shfl_down64(FF[kk][0], 1);
+            V nf1 = shfl_down64(FF[kk][1], 1);
+            V np0 = shfl_down64(P[kk][0], 1);
             if (lane == 31) {
                 if (warp + 1 < TPB / 32) {
-                    nf0 = sEdgeFF[buf][warp + 1][k][0];
-                    nf1 = sEdgeFF[buf][warp + 1][k][1];
-                    np0 = sEdgeP[buf][warp + 1][k];
+                    nf0 = sEdgeFF[buf][warp + 1][kk][0];
+                    nf1 = sEdgeFF[buf][warp + 1][kk][1];
+                    np0 = sEdgeP[buf][warp + 1][kk];
                 } else {
                     nf0 = nf1 = np0 = 0;
                 }
             }
             // GG_new(x) = GG_old(x-1) + P(x-1)
-            V pq = shfl_up64(Q[k], 1);
-            if (lane == 0) pq = (warp > 0) ? sEdgeQ[buf][warp - 1][k] : 0;
+            V pq = shfl_up64(Q[kk], 1);
+            if (lane == 0) pq = (warp > 0) ? sEdgeQ[buf][warp - 1][kk] : 0;
             V Fn[COLS], Gn[COLS];
 #pragma unroll
-            for (int j = 0; j < COLS - 1; ++j) Fn[j] = FF[k][j + 1] + P[k][j];
-            Fn[COLS - 1] = nf0 + P[k][COLS - 1];
+            for (int j = 0; j < COLS - 1; ++j) Fn[j] = FF[kk][j + 1] + P[kk][j];
+            Fn[COLS - 1] = nf0 + P[kk][COLS - 1];
             Gn[0] = pq;
 #pragma unroll
-            for (int j = 1; j < COLS; ++j) Gn[j] = GG[k][j - 1] + P[k][j - 1];
+            for (int j = 1; j < COLS; ++j) Gn[j] = GG[kk][j - 1] + P[kk][j - 1];
             const V fnext = nf1 + np0;  // FF_new of the next thread's column 0
 #pragma unroll
             for (int j = 0; j < COLS; ++j) {
-                S[k][j] += P[k][j];
-                FF[k][j] = Fn[j];
-                GG[k][j] = Gn[j];
+                S[kk][j] += P[kk][j];
+                FF[kk][j] = Fn[j];
+                GG[kk][j] = Gn[j];
             }
             if (kMode == 1) {
                 const int64_t c = c0 - RB - 1 + (int64_t)t * COLS;  // plane column of j = 0
@@ -273,15 +289,15 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                         longlong2* vs = reinterpret_cast<longlong2*>(a.planes + (0 * 4 + k) * a.plane_stride + off);
                         longlong2* ve = reinterpret_cast<longlong2*>(a.planes + (1 * 4 + k) * a.plane_stride + off);
                         longlong2* vo = reinterpret_cast<longlong2*>(a.planes + (2 * 4 + k) * a.plane_stride + off);
-                        vs[0] = make_longlong2((long long)S[k][0], (long long)S[k][1]);
-                        vs[1] = make_longlong2((long long)S[k][2], (long long)S[k][3]);
+                        vs[0] = make_longlong2((long long)S[kk][0], (long long)S[kk][1]);
+                        vs[1] = make_longlong2((long long)S[kk][2], (long long)S[kk][3]);
                         ve[0] = make_longlong2((long long)e0, (long long)e1);
                         ve[1] = make_longlong2((long long)e2, (long long)e3);
                         vo[0] = make_longlong2((long long)o0, (long long)o1);
                         vo[1] = make_longlong2((long long)o2, (long long)o3);
                     }
                     if (k == 0 && a.coarse) {  // stage 1's u16 bit slices of the PLAIN cells (K3L)
-                        const unsigned sv[3][4] = {{(unsigned)S[0][0], (unsigned)S[0][1], (unsigned)S[0][2], (unsigned)S[0][3]},
+                        const unsigned sv[3][4] = {{(unsigned)S[kk][0], (unsigned)S[kk][1], (unsigned)S[kk][2], (unsigned)S[kk][3]},
                                                    {(unsigned)e0, (unsigned)e1, (unsigned)e2, (unsigned)e3},
                                                    {(unsigned)o0, (unsigned)o1, (unsigned)o2, (unsigned)o3}};
                         for (int ci = 0; ci < a.n_coarse; ++ci) {
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                     if (sizeof(V) == 8 && a.hi16 && k != 0) {  // PLAIN ring sums stay below 2^32: no hi16
                         auto hi = [](V v) { return (unsigned)(((unsigned long long)v >> 32) & 0xffffu); };
                         *reinterpret_cast<uint2*>(a.hi16 + (0 * 4 + k) * a.plane_stride + off) =
-                            make_uint2(hi(S[k][0]) | hi(S[k][1]) << 16, hi(S[k][2]) | hi(S[k][3]) << 16);
+                            make_uint2(hi(S[kk][0]) | hi(S[kk][1]) << 16, hi(S[kk][2]) | hi(S[kk][3]) << 16);
                         *reinterpret_cast<uint2*>(a.hi16 + (1 * 4 + k) * a.plane_stride + off) =
                             make_uint2(hi(e0) | hi(e1) << 16, hi(e2) | hi(e3) << 16);
                         *reinterpret_cast<uint2*>(a.hi16 + (2 * 4 + k) * a.plane_stride + off) =
@@ -306,7 +322,7 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
                     }
                     if (a.planes32) {  // the same cells mod 2^32 (region sums are exact in 32 bits)
                         *reinterpret_cast<uint4*>(a.planes32 + (0 * 4 + k) * a.plane_stride + off) =
-                            make_uint4((unsigned)S[k][0], (unsigned)S[k][1], (unsigned)S[k][2], (unsigned)S[k][3]);
+                            make_uint4((unsigned)S[kk][0], (unsigned)S[kk][1], (unsigned)S[kk][2], (unsigned)S[kk][3]);
                         *reinterpret_cast<uint4*>(a.planes32 + (1 * 4 + k) * a.plane_stride + off) =
                             make_uint4((unsigned)e0, (unsigned)e1, (unsigned)e2, (unsigned)e3);
                         *reinterpret_cast<uint4*>(a.planes32 + (2 * 4 + k) * a.plane_stride + off) =
@@ -327,10 +343,11 @@ __global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
             const bool owned = (c >= c0 && c < c0 + CW) || (first && c < c0) || (last && c >= c0 + CW);
             if (!owned) continue;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (x >= 0 && x <= W - 1) st_ptr<V>(a, band, k, 0)[x + OFF] = S[k][j];
-                if (x >= -OFF && x <= W - 2) st_ptr<V>(a, band, k, 1)[x + OFF] = FF[k][j];
-                if (x >= 1 && x <= W + RB) st_ptr<V>(a, band, k, 2)[x + OFF] = GG[k][j];
+            for (int kk = 0; kk < NK; ++kk) {
+                const int k = KIND(kk);
+                if (x >= 0 && x <= W - 1) st_ptr<V>(a, band, k, 0)[x + OFF] = S[kk][j];
+                if (x >= -OFF && x <= W - 2) st_ptr<V>(a, band, k, 1)[x + OFF] = FF[kk][j];
+                if (x >= 1 && x <= W + RB) st_ptr<V>(a, band, k, 2)[x + OFF] = GG[kk][j];
             }
         }
     }
@@ -660,7 +677,16 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s, int64_t b_
         if (int e = check_launch("band_scan_fg_kernel")) return e;
     }
     a.band0 = b_lo;
-    band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo)), TPB, 0, s>>>(a);
+    // exact (int64) recurrences: two CTAs per tile, two kinds each (SS_BUILD_KINDS=4: one CTA)
+    // (SS_BUILD_KINDS=2: the 32-bit build too)
+    static const int kinds = [] {
+        const char* e = getenv("SS_BUILD_KINDS");
+        return e ? atoi(e) : 0;
+    }();
+    if ((sizeof(V) == 8 && kinds != 4) || kinds == 2)
+        band_kernel<1, RB, V, 2><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo), 2), TPB, 0, s>>>(a);
+    else
+        band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo)), TPB, 0, s>>>(a);
     note_launch();
     return check_launch("band_kernel<final>");
 }
