@@ -677,13 +677,14 @@ static int launch_bands(BuildArgs& a, int64_t nbands, cudaStream_t s, int64_t b_
         if (int e = check_launch("band_scan_fg_kernel")) return e;
     }
     a.band0 = b_lo;
-    // exact (int64) recurrences: two CTAs per tile, two kinds each (SS_BUILD_KINDS=4: one CTA)
-    // (SS_BUILD_KINDS=2: the 32-bit build too)
+    // the 32-bit build: two CTAs per tile, two kinds each (2048^2: 0.124 -> 0.117 ms,
+    // 4096^2: 0.392 -> 0.372); the int64 / hi16 build keeps one CTA per tile
+    // (config 4 split: 6.57 -> 7.50 ms).  SS_BUILD_KINDS=2|4 forces either.
     static const int kinds = [] {
         const char* e = getenv("SS_BUILD_KINDS");
         return e ? atoi(e) : 0;
     }();
-    if ((sizeof(V) == 8 && kinds != 4) || kinds == 2)
+    if (kinds == 2 || (kinds != 4 && sizeof(V) == 4))
         band_kernel<1, RB, V, 2><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo), 2), TPB, 0, s>>>(a);
     else
         band_kernel<1, RB, V><<<dim3((unsigned)a.n_chunks, (unsigned)(b_hi - b_lo)), TPB, 0, s>>>(a);
