@@ -13,7 +13,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstarscreen_b200.so")
+# SS_LIB_PATH: experiment hook (an alternative build of the same library)
+LIB_PATH = os.environ.get("SS_LIB_PATH") or os.path.join(_HERE, "libstarscreen_b200.so")
 
 SS_OK, SS_EINVAL, SS_ECAPACITY, SS_ECUDA = 0, 1, 2, 3
 SS_MAX_RINGS = 16
