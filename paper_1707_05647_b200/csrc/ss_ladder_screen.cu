@@ -29,7 +29,8 @@
 namespace ss {
 namespace {
 
-constexpr int FMAX_SIZES = SS_MAX_SIZES;
+constexpr int FMAX_SIZES = 48;  // sizes per fused group (larger groups are declined: per-size path); bounded by the 32 KB of kernel parameters
+static_assert(FMAX_SIZES <= SS_MAX_SIZES, "fused group size");
 constexpr int FMAX_RINGS = 104;  // rings over all fused sizes (kernel parameters <= 32 KB)
 constexpr int TAG_SHIFT = 24;    // list entry .y = row | size << TAG_SHIFT
 constexpr int YMASK = (1 << TAG_SHIFT) - 1;
@@ -46,6 +47,7 @@ struct SizeDev {
     float t0_c;           // coarse stage 1: 1/2 - fa_c - fb_c (estimate from the sums biased by one)
     int contig;           // ring 0's mean projection is one run of cells [B0, B1) (or empty): w* below apply
     float w0lo, w0hi, w1lo, w1hi;  // t within [w0lo, w0hi] of B0 or [w1lo, w1hi] of B1: undecided; else pass iff w0hi < t < w1lo
+    int s1_step;          // coarse stage 1 tests one centre row in s1_step (1, 2, 4): see ladder_stage1_coarse_kernel
 };
 
 struct FusedArgs {
@@ -68,10 +70,18 @@ struct FusedArgs {
 // Stage 1 from coarse planes: per shift set c, the u16 bit slices (cell >>
 // shift) & 0xffff of the SAT / E / O PLAIN cells (ss_build_tables3).
 constexpr int CNK = SS_MAX_COARSE;
+// [v]: the view that takes every (1 << v)-th row -- a 3-D map (column, row
+// mod step, row / step) of the same plane, so a 16-row box at (x, row mod
+// step, row / step) holds rows row, row + step, ... (stage 1's row steps).
+constexpr int S1_VIEWS = 3;       // row steps 1, 2, 4
+constexpr int S1_SUPER = 4;       // tile-row blocks per super row (= the largest step)
+#ifndef S1_SLACK_DEFAULT
+#define S1_SLACK_DEFAULT 0.4
+#endif
 struct CoarseMaps {
-    CUtensorMap sat[CNK], e[CNK], o[CNK];
+    CUtensorMap sat[S1_VIEWS][CNK], e[S1_VIEWS][CNK], o[S1_VIEWS][CNK];
 };
-static_assert(sizeof(FusedArgs) + sizeof(CoarseMaps) <= 31000, "fused ladder parameters exceed the kernel parameter limit");
+static_assert(sizeof(FusedArgs) + sizeof(CoarseMaps) + 256 <= 32764, "fused ladder parameters exceed the kernel parameter limit");
 static_assert(sizeof(RingDev) % 4 == 0, "RingDev is copied to shared memory by words");
 
 // Candidate-list entries: (x, y | size << TAG_SHIFT), plus -- when stage 1
@@ -503,7 +513,8 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     __shared__ int4 slot[STAGES];               // the tile in each stage: (tx, ty, size, -)
     __shared__ TileConstC size_info[FMAX_SIZES];  // per-size constants, filled once
-    __shared__ int4 size_tma[FMAX_SIZES];         // per-size (n, d, square plane set, diamond plane set)
+    __shared__ int4 size_tma[FMAX_SIZES];         // per-size (n, d, square plane set | view << 8, diamond plane set)
+    __shared__ unsigned short entries[S1_SUPER * FMAX_SIZES];  // tile-row entries of a super row: size | sub-block << 8
     __shared__ int2 cand_buf[CW][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
@@ -557,7 +568,18 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                     tcst.w1hi = S.w1hi;
                     tcst.t0 = S.t0_c;
         }
-        size_tma[sz] = make_int4(R0.n, R0.d, S.c_sq, S.c_di);
+        const int view = S.s1_step >= 4 ? 2 : (S.s1_step == 2 ? 1 : 0);
+        size_tma[sz] = make_int4(R0.n, R0.d, S.c_sq | (view << 8), S.c_di);
+    }
+    if (threadIdx.x == 0) {
+        // a super row is S1_SUPER tile rows of 16 image rows; a size of row
+        // step s covers it with S1_SUPER / s tiles of 16 s rows each
+        int ne = 0;
+        for (int sz = 0; sz < a.n_sizes; ++sz) {
+            const int st = a.size[sz].s1_step >= 4 ? 4 : (a.size[sz].s1_step == 2 ? 2 : 1);
+            for (int sub = 0; sub < S1_SUPER / st; ++sub) entries[ne++] = (unsigned short)(sz | (sub << 8));
+        }
+        SS_CHECK(ne == tm.n_sizes);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -572,36 +594,48 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
             // at ~34).
             const bool fast = tm.n_tiles < (1LL << 24);
             const unsigned pmask = (1u << NBOX) - 1u;
-            for (int it = 0;; ++it) {
-                const int s = it % STAGES;
+            for (int it = 0, k = 0;; ++it) {
+                const int s = k % STAGES;
                 const long long t = (long long)blockIdx.x + (long long)it * gridDim.x;
-                mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
                 if (t >= tm.n_tiles) {
+                    mbar_wait(&empty_bar[s], ((k / STAGES) & 1) ^ 1);
                     if (lane == 0) {
                         slot[s] = make_int4(-1, 0, 0, 0);
                         mbar_arrive(&full_bar[s]);
                     }
                     break;
                 }
-                int tx, ty, sz;
-                if (fast) tile_coords_fast(tm, (unsigned)t, tx, ty, sz);
-                else tile_coords_f(tm, t, tx, ty, sz);
+                int tx, ty, en;
+                if (fast) tile_coords_fast(tm, (unsigned)t, tx, ty, en);
+                else tile_coords_f(tm, t, tx, ty, en);
+                const int ent = entries[en];
+                const int sz = ent & 0xff, sub = ent >> 8;
+                const int4 st = size_tma[sz];
+                const int view = st.z >> 8, csq = st.z & 0xff, step = 1 << view;
+                // the tile: 16 groups of `step` rows from image row y_begin + r0
+                const int r0 = (ty * S1_SUPER + sub * step) * G::TYC;
+                if (a.y_begin + r0 >= a.y_end) continue;  // past the band's last row
+                mbar_wait(&empty_bar[s], ((k / STAGES) & 1) ^ 1);
+                ++k;
                 if (lane == 0) {
-                    slot[s] = make_int4(tx, ty, sz, 0);  // published by the arrive (complete_tx) below
+                    slot[s] = make_int4(tx, r0, sz, step);  // published by the arrive (complete_tx) below
                     mbar_expect_tx(&full_bar[s], G::STAGE_BYTES);
                 }
                 __syncwarp(pmask);  // expect_tx before any of the boxes lands
-                const int4 st = size_tma[sz];
-                SS_CHECK(sz >= 0 && sz < a.n_sizes && st.z >= 0 && st.z < CNK && st.w >= 0 && st.w < CNK);
+                SS_CHECK(sz >= 0 && sz < a.n_sizes && csq >= 0 && csq < CNK && st.w >= 0 && st.w < CNK && view < S1_VIEWS);
                 const int n = st.x, d = st.y, b = lane;
                 // box b: SAT (+-n+1 columns, +-n+1 rows), E (+1, d+1 / -d), O (-d / d+1, 0)
                 const int xo = b < 4 ? ((b & 1) ? 1 - n : n + 1) : (b < 6 ? 1 : (b == 6 ? -d : d + 1));
                 const int yo = b < 4 ? ((b & 2) ? 1 - n : n + 1) : (b == 4 ? d + 1 : (b == 5 ? -d : 0));
-                const CUtensorMap* m = b < 4 ? &maps.sat[st.z] : (b < 6 ? &maps.e[st.w] : &maps.o[st.w]);
+                const CUtensorMap* m =
+                    b < 4 ? &maps.sat[view][csq] : (b < 6 ? &maps.e[view][st.w] : &maps.o[view][st.w]);
                 const int x0 = tx * G::TX;
-                const int cy0 = a.y_begin + ty * G::TYC - a.y_origin;
-                tma_load_2d(stage_buf + s * G::STAGE_BYTES + b * G::BOX_BYTES, m, G::floor_al(x0 + xo), cy0 + yo,
-                            &full_bar[s]);
+                // tile row j tests the centre row y_begin + r0 + j step + step / 2 for its group of `step` rows
+                const int cy0 = a.y_begin + r0 + (step >> 1) - a.y_origin;
+                void* dst = stage_buf + s * G::STAGE_BYTES + b * G::BOX_BYTES;
+                const int row = cy0 + yo;
+                if (view == 0) tma_load_2d(dst, m, G::floor_al(x0 + xo), row, &full_bar[s]);
+                else tma_load_3d(dst, m, G::floor_al(x0 + xo), row & (step - 1), row >> view, &full_bar[s]);
             }
         }
         return;
@@ -622,11 +656,15 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
         mbar_wait(&full_bar[s], (it / STAGES) & 1);
         const int4 sl = slot[s];
         if (sl.x < 0) break;
-        const int tx = sl.x, ty = sl.y, sz = sl.z;
+        const int tx = sl.x, sz = sl.z, step = sl.w;
         const TileConstC& tc = size_info[sz];
         const int row = warp / G::WPR, half = warp - row * G::WPR;  // tile row, column block of this warp
-        const int y = a.y_begin + ty * G::TYC + row;
-        const bool row_int = y < a.y_end && y >= tc.ylo && y <= tc.yhi && (unit_stride || (y % a.stride) == 0);
+        // this warp's group of `step` rows [g0, g0 + step) and the row it tests
+        const int g0 = a.y_begin + sl.y + row * step;
+        const int y = g0 + (step >> 1);
+        const int gv0 = max(g0, tc.ylo), gv1 = min(min(g0 + step - 1, tc.yhi), a.y_end - 1);  // the group's interior rows
+        const bool grp_int = gv0 <= gv1 && (step > 1 || unit_stride || (g0 % a.stride) == 0);
+        const bool row_int = grp_int && y >= gv0 && y <= gv1;  // the tested row is interior itself
         // coarse sums biased by one: J = I + 1 in [0, 2^16 - 2], where
         // |S - I 2^k| < 2^(k+1) (the -1 is folded into the estimate's constant)
         unsigned jq[CPW], jd[CPW];
@@ -649,7 +687,7 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
         if (row_int && jq[0] == 0x12345u) list0[0] = make_int2((int)jd[1], 0);
         continue;
 #endif
-        if (!row_int) continue;
+        if (!grp_int) continue;
         const int cm_lo = tc.cm_lo;
         auto member = [&](int cm) -> bool {
             if (tc.bm1 == -2) {
@@ -666,7 +704,11 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
         };
         const int xt = tx * G::TX + half * 32 * CPW;  // this warp's first column
         unsigned pm = 0, amb = 0;
-        if (tc.contig) {
+        if (!row_int) {
+            // the tested row lies outside the interior (first / last rows of a
+            // size, band ends): every centre of the group's rows is a candidate
+            pm = (1u << CPW) - 1u;
+        } else if (tc.contig) {
             // one run of member cells [B0, B1): a centre is a candidate unless t
             // lies below B0 or above B1 by more than the error bound -- those
             // within the bound of B0 or B1 are decided by the rings kernel
@@ -702,38 +744,41 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                     pm &= ~(1u << c);
                     amb &= ~(1u << c);
                 }
-                if (a.stage_counts) n_int += __popc(__ballot_sync(FULL, interior));
+                if (a.stage_counts) n_int += (unsigned)(gv1 - gv0 + 1) * __popc(__ballot_sync(FULL, interior));
             }
         } else if (a.stage_counts) {
-            n_int += 32 * CPW;
+            n_int += 32 * CPW * (gv1 - gv0 + 1);
         }
         // undecided centres go to the rings kernel as candidates: its level 0
         // recomputes ring 0's exact mean cell and tests it (eval_ring_fast)
         pm |= amb;
-        const int tag = y | (sz << TAG_SHIFT);
         if (!__any_sync(FULL, pm != 0u)) continue;
+        // a passing column is a candidate on every interior row of the group
+        for (int yg = gv0; yg <= gv1; ++yg) {
+            const int tag = yg | (sz << TAG_SHIFT);
 #pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-            const bool p = (pm >> c) & 1u;
-            const unsigned pb = __ballot_sync(FULL, p);
-            if (p) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
-            nbuf += __popc(pb);
-            n_pass += __popc(pb);
-            if (nbuf >= 32) {
-                __syncwarp();
-                if (res_left == 0) {
-                    if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
-                    res_base = __shfl_sync(FULL, res, 0);
-                    res_left = reserve;
-                    if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
-                    have_res = true;
+            for (int c = 0; c < CPW; ++c) {
+                const bool p = (pm >> c) & 1u;
+                const unsigned pb = __ballot_sync(FULL, p);
+                if (p) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
+                nbuf += __popc(pb);
+                n_pass += __popc(pb);
+                if (nbuf >= 32) {
+                    __syncwarp();
+                    if (res_left == 0) {
+                        if (!have_res && lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                        res_base = __shfl_sync(FULL, res, 0);
+                        res_left = reserve;
+                        if (lane == 0) res = atom_add_ahead(count0, (unsigned)reserve);
+                        have_res = true;
+                    }
+                    SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
+                    list0[res_base + lane] = buf[nbuf - 32 + lane];
+                    res_base += 32;
+                    res_left -= 32;
+                    nbuf -= 32;
+                    __syncwarp();
                 }
-                SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
-                list0[res_base + lane] = buf[nbuf - 32 + lane];
-                res_base += 32;
-                res_left -= 32;
-                nbuf -= 32;
-                __syncwarp();
             }
         }
     }
@@ -977,7 +1022,10 @@ int parts_for(int64_t W, int64_t rows, int n_sizes) {
 long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int parts) {
     const long long ctas = (2LL * sms + parts - 1) / parts;
     constexpr int s1_warps = WARPS > GeoC::CW ? WARPS : GeoC::CW;  // list reservation slack per stage-1 warp
-    return (tiles_of(W, rows) * n_sizes + parts - 1) / parts * (TXMAX * TY) + ctas * s1_warps * 2 * RESERVE_MAX;
+    // partitioned lists: 1/16 headroom for the uneven shares of a round-robin
+    // hand-out (148 CTAs over 8 partitions, tiles of 1 / 2 / 4 row steps)
+    const long long share = (tiles_of(W, rows) * n_sizes + parts - 1) / parts;
+    return (share + (parts > 1 ? share / 16 + 64 : 0)) * (TXMAX * TY) + ctas * s1_warps * 2 * RESERVE_MAX;
 }
 size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms, size_t entry = sizeof(FEntry<unsigned>)) {
     const int parts = parts_for(W, rows, n_sizes);
@@ -1033,12 +1081,14 @@ int coarse_maps_cached(CoarseMaps& maps, const uint16_t* coarse, int n_coarse, i
         }
     }
     std::memset(&maps, 0, sizeof(maps));
-    for (int c = 0; c < n_coarse; ++c) {
-        const uint16_t* base = coarse + (size_t)c * 3 * (size_t)ps;
-        if (int e = encode_plane_map(&maps.sat[c], base, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
-        if (int e = encode_plane_map(&maps.e[c], base + ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
-        if (int e = encode_plane_map(&maps.o[c], base + 2 * ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC)) return e;
-    }
+    for (int v = 0; v < S1_VIEWS; ++v)
+        for (int c = 0; c < n_coarse; ++c) {
+            const uint16_t* base = coarse + (size_t)c * 3 * (size_t)ps;
+            if (int e = encode_plane_map(&maps.sat[v][c], base, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
+            if (int e = encode_plane_map(&maps.e[v][c], base + ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
+            if (int e = encode_plane_map(&maps.o[v][c], base + 2 * ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v))
+                return e;
+        }
     std::lock_guard<std::mutex> lock(mu);
     if (cache.size() > 256) cache.clear();
     cache[key] = maps;
@@ -1066,7 +1116,9 @@ size_t ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
     const int sms = device_sms();
     const int64_t S = std::max<int32_t>(n_sizes, 1);
     int64_t band = std::max<int64_t>(rows, 1);
-    while (band > 4 * TY && fused_ws_bytes(W, band, (int)S, sms) > FUSED_WS_CAP) band = (band / 2 + TY - 1) / TY * TY;
+    constexpr int BAND_AL = TY * S1_SUPER;  // as the launch loop of ladder_screen
+    while (band > 4 * TY && fused_ws_bytes(W, band, (int)S, sms) > FUSED_WS_CAP)
+        band = (band / 2 + BAND_AL - 1) / BAND_AL * BAND_AL;
     return std::max(fused_ws_bytes(W, band, (int)S, sms), screen_workspace_bytes(W, std::max<int64_t>(rows, 1)));
 }
 
@@ -1191,6 +1243,9 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     // stays well inside a cell; SS_COARSE=0 forces the 32-bit stage 1.
     bool coarse = d_coarse && n_coarse > 0 && h_shifts && a.planes32;
     if (const char* e = getenv("SS_COARSE")) coarse = coarse && atoi(e) != 0;
+    // SS_S1_SLACK: the cells ring 0's mean may move inside a row group (0: every row is tested)
+    double s1_slack = S1_SLACK_DEFAULT;
+    if (const char* e = getenv("SS_S1_SLACK")) s1_slack = atof(e);
     for (int j = 0; j < n && coarse; ++j) {
         SizeDev& S = a.size[j];
         const RingDev& R0 = a.ring[S.ring0];
@@ -1216,12 +1271,33 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         const int64_t* hd = h_blobs + h_blob_off[ks[j]] + 1;
         const int64_t n_m = hd[1], cm_lo = hd[6], cm_n = hd[7];
         S.contig = 0;
+        S.s1_step = 1;
         if (n_m == 0 || n_m == cm_n) {
             const double B0 = n_m ? (double)cm_lo : 1e30, B1 = n_m ? (double)(cm_lo + cm_n) : 1e30;
             auto dn = [](double v) { return std::nextafter((float)v, -INFINITY); };
             auto up = [](double v) { return std::nextafter((float)v, INFINITY); };
-            const double d0 = (band + 4e-6 * (B0 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7;
-            const double d1 = (band + 4e-6 * (B1 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7;
+            // Row steps: moving a centre by one row swaps one row of the square
+            // (2n pixels) and the 2d + 1 boundary pixels of the diamond, so
+            // |S_sq(y+1) - S_sq(y)| <= 255 * 2n and |S_di(y+1) - S_di(y)| <=
+            // 255 (2d + 1), i.e. the mean cell coordinate t moves by at most
+            // lip = (255 * 2n / c_sq + 255 (2d + 1) / c_di) / (2 q_mean) per row.
+            // A size whose t cannot move by more than `slack` cells over
+            // step / 2 rows tests one centre row per group of `step` rows
+            // against the window widened by that bound; a passing column sends
+            // the centres of all the group's rows to the rings kernel, whose
+            // level 0 decides each from its exact ring-0 sums.
+            const double lip = (255.0 * 2.0 * R0.n / (double)cq + 255.0 * (2.0 * R0.d + 1.0) / (double)cd) / (2.0 * qm);
+            double extra = 0.0;
+            if (stride == 1 && s1_slack > 0.0) {
+                for (int st = 1 << (S1_VIEWS - 1); st > 1; st >>= 1)
+                    if ((st / 2) * lip <= s1_slack) {
+                        S.s1_step = st;
+                        extra = (st / 2) * lip * (1.0 + 1e-6);
+                        break;
+                    }
+            }
+            const double d0 = (band + 4e-6 * (B0 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
+            const double d1 = (band + 4e-6 * (B1 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
             S.contig = 1;
             S.w0lo = dn(B0 - d0);
             S.w0hi = up(B0 + d0);
@@ -1236,7 +1312,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     const int sms = device_sms();
     // row bands: as many rows per pass as the workspace holds
     int64_t band = rows;
-    while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + TY - 1) / TY * TY;
+    constexpr int BAND_AL = TY * S1_SUPER;  // whole super rows of the coarse stage 1
+    while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + BAND_AL - 1) / BAND_AL * BAND_AL;
     if (!d_ws || fused_ws_bytes(W, band, n, sms) > ws_bytes) return SS_DECLINED;
 
     // Stage 1 reads only the ring-0 PLAIN sums: when they fit 32 bits for
@@ -1293,7 +1370,14 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             const int tile_y = coarse ? GeoC::TYC : TY;
             tm.n_ty = (int)((brows + tile_y - 1) / tile_y);
             tm.n_sizes = n;
-            tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n;
+            if (coarse) {
+                // super rows of S1_SUPER tile rows; a size of row step s has S1_SUPER / s tile-row entries in each
+                tm.n_ty = (int)((brows + tile_y * S1_SUPER - 1) / (tile_y * S1_SUPER));
+                tm.n_sizes = 0;
+                for (int j = 0; j < n; ++j) tm.n_sizes += S1_SUPER / std::max(1, std::min(a.size[j].s1_step, S1_SUPER));
+            }
+            const int n_ent = tm.n_sizes;
+            tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n_ent;
             // column strips: the widest whose working set -- (max_m + rows in
             // flight) x (strip + max_m) columns of all 12 planes -- fits the L2
             // budget (the rings that follow touch every plane of those rows)
@@ -1303,7 +1387,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                 const int64_t in_flight = (int64_t)sms * s1_per_sm * G::STAGES;
                 tm.strip = 1;
                 for (int strip = tm.n_tx; strip >= 1; strip = (strip > 8) ? strip * 3 / 4 : strip - 1) {
-                    const int64_t rws = (in_flight + (int64_t)strip * n - 1) / ((int64_t)strip * n) * tile_y;
+                    const int64_t rws = (in_flight + (int64_t)strip * n_ent - 1) / ((int64_t)strip * n_ent) * tile_y *
+                                        (coarse ? S1_SUPER : 1);
                     const int64_t ws = (max_m + 2 + rws) * ((int64_t)strip * tile_x + max_m + 2) * 12 * eb;
                     if (ws <= budget) {
                         tm.strip = strip;
@@ -1311,11 +1396,11 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                     }
                 }
                 const int last_w = tm.n_tx - (tm.n_tx - 1) / tm.strip * tm.strip;
-                tm.r_per_strip = (float)(1.0 / ((double)tm.strip * tm.n_ty * n));
+                tm.r_per_strip = (float)(1.0 / ((double)tm.strip * tm.n_ty * n_ent));
                 tm.r_strip = (float)(1.0 / tm.strip);
                 tm.r_last = (float)(1.0 / last_w);
-                tm.r_span = (float)(1.0 / ((double)tm.strip * n));
-                tm.r_span_last = (float)(1.0 / ((double)last_w * n));
+                tm.r_span = (float)(1.0 / ((double)tm.strip * n_ent));
+                tm.r_span_last = (float)(1.0 / ((double)last_w * n_ent));
             }
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);

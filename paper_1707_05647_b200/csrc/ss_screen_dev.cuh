@@ -684,6 +684,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        : "memory");
+}
+
 struct TmaMaps {
     CUtensorMap sat, e, o;  // PLAIN SAT / E / O planes: 2-D (cols, rows) of T
 };
@@ -840,8 +849,12 @@ inline int occupancy(const void* fn, int threads, size_t smem) {
 }
 // 2-D TMA descriptor of one plane (int64 or u32 elements): dims (W+1 columns,
 // h+1 rows), box BW x TY.
+// row_step > 1: the 3-D view (column, row mod row_step, row / row_step) of the
+// plane; a box of box_h rows at (x, r % row_step, r / row_step) holds rows r,
+// r + row_step, ...  Rows of the last (partial) group past the plane's end lie
+// in the next plane or in the padding ss_coarse_bytes adds.
 inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes, int box_w, int64_t W, int64_t h,
-                            int64_t pitch, int box_h = TY) {
+                            int64_t pitch, int box_h = TY, int row_step = 1) {
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -855,16 +868,19 @@ inline int encode_plane_map(CUtensorMap* map, const void* plane, int elem_bytes,
         }
         encode = reinterpret_cast<EncodeFn>(fn);
     }
-    const cuuint64_t dims[2] = {(cuuint64_t)(W + 1), (cuuint64_t)(h + 1)};
-    const cuuint64_t strides[1] = {(cuuint64_t)pitch * (cuuint64_t)elem_bytes};
-    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
-    const cuuint32_t estr[2] = {1, 1};
+    const bool v3 = row_step > 1;
+    const cuuint64_t dims[3] = {(cuuint64_t)(W + 1), v3 ? (cuuint64_t)row_step : (cuuint64_t)(h + 1),
+                                (cuuint64_t)((h + row_step) / row_step)};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch * (cuuint64_t)elem_bytes,
+                                   (cuuint64_t)pitch * (cuuint64_t)elem_bytes * (cuuint64_t)row_step};
+    const cuuint32_t box[3] = {(cuuint32_t)box_w, v3 ? 1u : (cuuint32_t)box_h, (cuuint32_t)box_h};
+    const cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (const char* e = getenv("SS_TMA_PROMO")) promo = (CUtensorMapL2promotion)atoi(e);  // experiment hook
     const CUtensorMapDataType dt = elem_bytes == 8   ? CU_TENSOR_MAP_DATA_TYPE_INT64
                                    : elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
                                                      : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-    const CUresult r = encode(map, dt, 2,
+    const CUresult r = encode(map, dt, v3 ? 3 : 2,
                               const_cast<void*>(plane), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -477,6 +477,56 @@ def test_coarse_stage1_equals_exact_stage1(cuda, monkeypatch, q, which):
     assert np.array_equal(ma, mb)
 
 
+def _step_image(which, seed=3):
+    """Images whose ring-0 mean moves as fast as it can from one centre row to
+    the next (the row-step bound of stage 1 is the worst case over images)."""
+    import workloads as WL
+
+    rng = np.random.default_rng(seed)
+    h, w = 520, 640
+    if which == "stripes":  # full-contrast horizontal stripes of many periods + a little noise
+        img = np.zeros((h, w), np.int32)
+        y = 0
+        while y < h:
+            t = int(rng.integers(3, 90))
+            img[y:y + t] = int(rng.integers(0, 2)) * 255
+            y += t
+        img[:, w // 2:] = 255 - img[:, w // 2:]
+        img = np.clip(img + rng.integers(-6, 7, size=img.shape), 0, 255).astype(np.uint8)
+    elif which == "blocks":
+        img = np.kron(rng.integers(0, 2, size=(h // 20, w // 20)) * 255, np.ones((20, 20))).astype(np.uint8)
+        img = np.clip(img.astype(np.int32) + rng.integers(-20, 21, size=img.shape), 0, 255).astype(np.uint8)
+    else:
+        img = WL.make_image(w, h, seed=seed, sigma=3.0, noise=1.0)
+    return np.ascontiguousarray(img)
+
+
+@pytest.mark.parametrize("slack", ["0.4", "1.5", "4.0"])
+@pytest.mark.parametrize("which", ["stripes", "blocks", "smooth"])
+def test_stage1_row_steps_keep_every_ring0_passer(cuda, monkeypatch, which, slack):
+    """Coarse stage 1 tests one centre row per group of 2 or 4 rows for sizes
+    whose ring-0 mean cannot move by more than SS_S1_SLACK cells inside a
+    group (window widened by the worst-case bound) and sends the whole
+    group's columns on as candidates.  With std / gradient steps so large that
+    membership is the mean test alone, the ring-0 passer count would drop if
+    any true passer were skipped: counts and masks must equal those of the
+    every-row stage 1 (slack 0), on images built for the bound's worst case."""
+    img = _step_image(which)
+    tpl = np.ascontiguousarray(img[200:264, 300:364])
+    for q in ((8.0, 1e6, 1e6), (16.0, 8.0, 1e6)):
+        cfg = pcfg({"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.25, "quantizer": q})
+        monkeypatch.setenv("SS_S1_SLACK", slack)
+        ca, ma, shifts = _stage_counts(img, tpl, cfg, cuda)
+        monkeypatch.setenv("SS_S1_SLACK", "0")
+        cb, mb, _ = _stage_counts(img, tpl, cfg, cuda)
+        assert shifts
+        assert (ca[0], ca[2], ca[3]) == (cb[0], cb[2], cb[3]), (q, ca, cb)
+        assert ca[1] >= cb[1]
+        assert np.array_equal(ma, mb)
+        if q[1] > 1e5:
+            assert cb[2] > 0  # the comparison is not vacuous
+
+
 def test_coarse_planes_are_bit_slices(cuda):
     """ss_build_tables3's u16 planes are (cell >> shift) & 0xffff of the
     SAT / E / O PLAIN cells for every shift."""
