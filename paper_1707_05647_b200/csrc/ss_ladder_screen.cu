@@ -31,7 +31,7 @@ namespace {
 
 constexpr int FMAX_SIZES = 48;  // sizes per fused group (larger groups are declined: per-size path); bounded by the 32 KB of kernel parameters
 static_assert(FMAX_SIZES <= SS_MAX_SIZES, "fused group size");
-constexpr int FMAX_RINGS = 104;  // rings over all fused sizes (kernel parameters <= 32 KB)
+constexpr int FMAX_RINGS = 100;  // rings over all fused sizes (kernel parameters <= 32 KB)
 constexpr int TAG_SHIFT = 24;    // list entry .y = row | size << TAG_SHIFT
 constexpr int YMASK = (1 << TAG_SHIFT) - 1;
 constexpr int S1_BITS_WORDS = 4096;  // stage-1 mean-projection bits of all sizes
@@ -46,8 +46,11 @@ struct SizeDev {
     float band_c;         // coarse stage 1: bound on |t_coarse - t| from the bit slices (K3L)
     float t0_c;           // coarse stage 1: 1/2 - fa_c - fb_c (estimate from the sums biased by one)
     int contig;           // ring 0's mean projection is one run of cells [B0, B1) (or empty): w* below apply
-    float w0lo, w0hi, w1lo, w1hi;  // t within [w0lo, w0hi] of B0 or [w1lo, w1hi] of B1: undecided; else pass iff w0hi < t < w1lo
-    int s1_step;          // coarse stage 1 tests one centre row in s1_step (1, 2, 4): see ladder_stage1_coarse_kernel
+    // candidate window of the estimate per row-step view v (rows tested: one in
+    // 1 << v): [B0, B1) widened by the estimate's bound and by the most t can
+    // move inside a row group (ladder_stage1_coarse_kernel)
+    float wlo[3], whi[3];
+    int s1_views;         // views 0 .. s1_views - 1 are allowed for this size (>= 1)
 };
 
 struct FusedArgs {
@@ -76,10 +79,20 @@ constexpr int CNK = SS_MAX_COARSE;
 constexpr int S1_VIEWS = 3;       // row steps 1, 2, 4
 constexpr int S1_SUPER = 4;       // tile-row blocks per super row (= the largest step)
 #ifndef S1_SLACK_DEFAULT
-#define S1_SLACK_DEFAULT 0.4
+#define S1_SLACK_DEFAULT 4.0
+#endif
+#ifndef S1_RATIO_DEFAULT
+#define S1_RATIO_DEFAULT 13.0
 #endif
 struct CoarseMaps {
     CUtensorMap sat[S1_VIEWS][CNK], e[S1_VIEWS][CNK], o[S1_VIEWS][CNK];
+};
+// Stage 1's row steps, chosen on the device per call (ladder_plan_kernel).
+struct S1Plan {
+    int view[FMAX_SIZES];         // the chosen view (row step 1 << view) per size
+    unsigned cnt[FMAX_SIZES][4];  // samples inside the window of view 0, 1, 2; samples taken
+    unsigned ticket;
+    int pad[3];
 };
 static_assert(sizeof(FusedArgs) + sizeof(CoarseMaps) + 256 <= 32764, "fused ladder parameters exceed the kernel parameter limit");
 static_assert(sizeof(RingDev) % 4 == 0, "RingDev is copied to shared memory by words");
@@ -489,6 +502,100 @@ struct __align__(16) TileConstC {
     int pad[2];
 };
 
+// Row steps of the coarse stage 1, chosen per size from a sample of the image
+// (ladder_plan_kernel -> S1Plan, read by ladder_stage1_coarse_kernel; no host
+// round trip, so the ladder stays one graph-capturable chain).  A size at view
+// v tests one centre row per group of 1 << v rows against the window widened
+// by the most the ring-0 mean can move inside the group, and sends every row
+// of a passing column to the rings kernel: stage 1 costs 1 / step per centre,
+// but centres inside the widened window and outside the plain one become
+// false candidates (each decided exactly, and rejected, by the rings kernel's
+// level 0).  The kernel evaluates ring 0's mean on a lattice of <= PLAN_N x
+// PLAN_N centres per size from the 32-bit PLAIN planes, counts the samples in
+// each view's window, and picks the view minimising
+//     1 / step + ratio * (P_view - P_0),
+// ratio = cost of a false candidate in the rings kernel / cost of a stage-1
+// centre (measured ~13 on B200: ~28 ps against ~2 ps).
+constexpr int PLAN_N = 64;
+constexpr int PLAN_BLOCKS = 8;  // blocks per size (two samples per thread)
+// below this many positions x sizes per call the plan cannot repay its launch
+// (config 1: stage 1 is 0.15 ms): every size keeps row step 1
+constexpr long long PLAN_MIN_WORK = 100000000LL;
+__global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant__ FusedArgs a, S1Plan* plan, int y_lo,
+                                                          int y_hi, float ratio, int force) {
+    const int sz = blockIdx.x / PLAN_BLOCKS, part = blockIdx.x % PLAN_BLOCKS;
+    const SizeDev& S = a.size[sz];
+    const RingDev& R0 = a.ring[S.ring0];
+    __shared__ unsigned c_sh[4];
+    __shared__ bool last_sh;
+    if (threadIdx.x < 4) c_sh[threadIdx.x] = 0;
+    __syncthreads();
+    const int xlo = S.lo, xhi = a.W - 1 - S.hi;
+    const int ylo = max(y_lo, S.lo), yhi = min(y_hi - 1, a.H - 1 - S.hi);
+    if (S.s1_views > 1 && !force && xlo <= xhi && ylo <= yhi) {
+        const int wx = xhi - xlo + 1, wy = yhi - ylo + 1;
+        const int nx = min(PLAN_N, wx), ny = min(PLAN_N, wy);
+        const unsigned* P = a.planes32;  // plane type * 4 + kind: PLAIN SAT 0, E 4, O 8
+        const long long ps = a.ps, pitch = a.pitch;
+        const int n = R0.n, d = R0.d;
+        const float fa = (float)(0.5 / ((double)(4LL * n * n) * a.qm));
+        const float fb = (float)(0.5 / ((double)(2LL * d * d + 2LL * d + 1) * a.qm));
+        unsigned c0 = 0, c1 = 0, c2 = 0, ct = 0;
+#pragma unroll 2
+        for (int i = part * 256 + threadIdx.x; i < nx * ny; i += PLAN_BLOCKS * 256) {
+            const int iy = i / nx, ix = i - iy * nx;
+            const int cx = xlo + (int)(((long long)(2 * ix + 1) * wx) / (2 * nx));
+            const int cy = ylo + (int)(((long long)(2 * iy + 1) * wy) / (2 * ny));
+            const long long r = cy - a.y_origin;  // table row of image row cy - 1
+            const unsigned* sat = P;
+            const unsigned* e = P + 4 * ps;
+            const unsigned* o = P + 8 * ps;
+            const unsigned sq = __ldg(sat + (r + n + 1) * pitch + cx + n + 1) - __ldg(sat + (r + n + 1) * pitch + cx - n + 1) -
+                                __ldg(sat + (r - n + 1) * pitch + cx + n + 1) + __ldg(sat + (r - n + 1) * pitch + cx - n + 1);
+            const unsigned di = __ldg(e + (r + d + 1) * pitch + cx + 1) - __ldg(o + r * pitch + cx - d) -
+                                __ldg(o + r * pitch + cx + d + 1) + __ldg(e + (r - d) * pitch + cx + 1);
+            const float t = fmaf((float)sq, fa, fmaf((float)di, fb, 0.5f));
+            ++ct;
+            c0 += t >= S.wlo[0] && t <= S.whi[0];
+            c1 += t >= S.wlo[1] && t <= S.whi[1];
+            c2 += t >= S.wlo[2] && t <= S.whi[2];
+        }
+        atomicAdd(&c_sh[0], c0);
+        atomicAdd(&c_sh[1], c1);
+        atomicAdd(&c_sh[2], c2);
+        atomicAdd(&c_sh[3], ct);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; ++k)
+            if (c_sh[k]) atomicAdd(&plan->cnt[sz][k], c_sh[k]);
+        __threadfence();
+        last_sh = atomicAdd(&plan->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+    for (int j = threadIdx.x; j < a.n_sizes; j += blockDim.x) {
+        const SizeDev& Sj = a.size[j];
+        const volatile unsigned* c = plan->cnt[j];
+        int best = 0;
+        if (force) {
+            best = Sj.s1_views - 1;
+        } else if (Sj.s1_views > 1 && c[3] > 0) {
+            const float inv = 1.0f / (float)c[3];
+            float cost = 1.0f;
+            for (int v = 1; v < Sj.s1_views; ++v) {
+                const float cv = 1.0f / (float)(1 << v) + ratio * (float)(c[v] - c[0]) * inv;
+                if (cv < cost) {
+                    cost = cv;
+                    best = v;
+                }
+            }
+        }
+        plan->view[j] = best;
+    }
+}
+
 // Stage 1 of every fused size from the coarse planes.  A region sum S of
 // `count` pixels whose slices have shift k is recovered as the integer I with
 // |S - I 2^k| < 2^(k+1) (four floors of cell / 2^k; no wrap since
@@ -503,8 +610,8 @@ struct __align__(16) TileConstC {
 // centre.
 __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     ladder_stage1_coarse_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ CoarseMaps maps,
-                                const TileMapF tm, int parts, int reserve, int2* list_base, long long part_cap,
-                                unsigned* list_ctr, unsigned* tile_ctr_base) {
+                                const TileMapF tm_in, int parts, int reserve, int2* list_base, long long part_cap,
+                                unsigned* list_ctr, unsigned* tile_ctr_base, const S1Plan* plan) {
     using G = GeoC;
     constexpr int STAGES = G::STAGES, CPW = G::CPW, CW = G::CW;
     extern __shared__ __align__(128) unsigned char dsmem[];
@@ -515,6 +622,7 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     __shared__ TileConstC size_info[FMAX_SIZES];  // per-size constants, filled once
     __shared__ int4 size_tma[FMAX_SIZES];         // per-size (n, d, square plane set | view << 8, diamond plane set)
     __shared__ unsigned short entries[S1_SUPER * FMAX_SIZES];  // tile-row entries of a super row: size | sub-block << 8
+    __shared__ TileMapF tm;  // tm_in with the entry count of the plan's row steps
     __shared__ int2 cand_buf[CW][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
@@ -562,24 +670,31 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                     tcst.cm_lo = R0.cm_lo;
                     tcst.cm_n = R0.cm_n;
                     tcst.contig = S.contig;
-                    tcst.w0lo = S.w0lo;
-                    tcst.w0hi = S.w0hi;
-                    tcst.w1lo = S.w1lo;
-                    tcst.w1hi = S.w1hi;
+                    const int view = plan ? min(max(__ldg(&plan->view[sz]), 0), S.s1_views - 1) : 0;
+                    tcst.w0lo = S.wlo[view];
+                    tcst.w0hi = S.wlo[view];
+                    tcst.w1lo = S.whi[view];
+                    tcst.w1hi = S.whi[view];
                     tcst.t0 = S.t0_c;
+                    size_tma[sz] = make_int4(R0.n, R0.d, S.c_sq | (view << 8), S.c_di);
         }
-        const int view = S.s1_step >= 4 ? 2 : (S.s1_step == 2 ? 1 : 0);
-        size_tma[sz] = make_int4(R0.n, R0.d, S.c_sq | (view << 8), S.c_di);
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         // a super row is S1_SUPER tile rows of 16 image rows; a size of row
         // step s covers it with S1_SUPER / s tiles of 16 s rows each
         int ne = 0;
         for (int sz = 0; sz < a.n_sizes; ++sz) {
-            const int st = a.size[sz].s1_step >= 4 ? 4 : (a.size[sz].s1_step == 2 ? 2 : 1);
+            const int st = 1 << (size_tma[sz].z >> 8);
             for (int sub = 0; sub < S1_SUPER / st; ++sub) entries[ne++] = (unsigned short)(sz | (sub << 8));
         }
-        SS_CHECK(ne == tm.n_sizes);
+        tm = tm_in;
+        tm.n_sizes = ne;
+        tm.n_tiles = (long long)tm.n_tx * tm.n_ty * ne;
+        const int last_w = tm.n_tx - (tm.n_tx - 1) / tm.strip * tm.strip;
+        tm.r_per_strip = (float)(1.0 / ((double)tm.strip * tm.n_ty * ne));
+        tm.r_span = (float)(1.0 / ((double)tm.strip * ne));
+        tm.r_span_last = (float)(1.0 / ((double)last_w * ne));
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1006,6 +1121,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
 }
 
 constexpr size_t FCTR_BYTES = (2 + GROUP_CTRS) * MAX_PARTS * CTR_STRIDE * 4;
+constexpr size_t PLAN_BYTES = (sizeof(S1Plan) + 255) / 256 * 256;  // after the counters (the border kernel zeroes those per band)
 #ifndef FUSED_LARGE_TILES_MACRO
 #define FUSED_LARGE_TILES_MACRO 32768
 #endif
@@ -1029,7 +1145,7 @@ long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int part
 }
 size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms, size_t entry = sizeof(FEntry<unsigned>)) {
     const int parts = parts_for(W, rows, n_sizes);
-    return FCTR_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * entry;
+    return FCTR_BYTES + PLAN_BYTES + (size_t)parts * (size_t)fused_part_cap(W, rows, n_sizes, sms, parts) * entry;
 }
 
 // The three PLAIN-plane TMA descriptors (SAT / E / O) of a plane buffer,
@@ -1243,9 +1359,16 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     // stays well inside a cell; SS_COARSE=0 forces the 32-bit stage 1.
     bool coarse = d_coarse && n_coarse > 0 && h_shifts && a.planes32;
     if (const char* e = getenv("SS_COARSE")) coarse = coarse && atoi(e) != 0;
-    // SS_S1_SLACK: the cells ring 0's mean may move inside a row group (0: every row is tested)
-    double s1_slack = S1_SLACK_DEFAULT;
+    // SS_S1_SLACK: the most cells ring 0's mean may move inside a row group for a
+    // row-step view to be allowed (0: every row is tested); SS_S1_RATIO: the
+    // plan's cost ratio; SS_S1_FORCE=1: the largest allowed view (tests)
+    double s1_slack = S1_SLACK_DEFAULT, s1_ratio = S1_RATIO_DEFAULT;
+    int s1_force = 0;
     if (const char* e = getenv("SS_S1_SLACK")) s1_slack = atof(e);
+    if (const char* e = getenv("SS_S1_RATIO")) s1_ratio = atof(e);
+    if (const char* e = getenv("SS_S1_FORCE")) s1_force = atoi(e);
+    long long s1_min_work = PLAN_MIN_WORK;
+    if (const char* e = getenv("SS_S1_MIN_WORK")) s1_min_work = atoll(e);
     for (int j = 0; j < n && coarse; ++j) {
         SizeDev& S = a.size[j];
         const RingDev& R0 = a.ring[S.ring0];
@@ -1271,7 +1394,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         const int64_t* hd = h_blobs + h_blob_off[ks[j]] + 1;
         const int64_t n_m = hd[1], cm_lo = hd[6], cm_n = hd[7];
         S.contig = 0;
-        S.s1_step = 1;
+        S.s1_views = 1;
+        for (int v = 0; v < S1_VIEWS; ++v) S.wlo[v] = S.whi[v] = 0.0f;
         if (n_m == 0 || n_m == cm_n) {
             const double B0 = n_m ? (double)cm_lo : 1e30, B1 = n_m ? (double)(cm_lo + cm_n) : 1e30;
             auto dn = [](double v) { return std::nextafter((float)v, -INFINITY); };
@@ -1281,28 +1405,22 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             // |S_sq(y+1) - S_sq(y)| <= 255 * 2n and |S_di(y+1) - S_di(y)| <=
             // 255 (2d + 1), i.e. the mean cell coordinate t moves by at most
             // lip = (255 * 2n / c_sq + 255 (2d + 1) / c_di) / (2 q_mean) per row.
-            // A size whose t cannot move by more than `slack` cells over
-            // step / 2 rows tests one centre row per group of `step` rows
-            // against the window widened by that bound; a passing column sends
-            // the centres of all the group's rows to the rings kernel, whose
-            // level 0 decides each from its exact ring-0 sums.
+            // View v tests the row at offset step / 2 of each group of step =
+            // 1 << v rows, at most step / 2 rows from any row of the group:
+            // its window is [B0, B1) widened by the estimate's bound and by
+            // (step / 2) lip.  Views whose widening stays within s1_slack
+            // cells are allowed; ladder_plan_kernel picks among them.
             const double lip = (255.0 * 2.0 * R0.n / (double)cq + 255.0 * (2.0 * R0.d + 1.0) / (double)cd) / (2.0 * qm);
-            double extra = 0.0;
-            if (stride == 1 && s1_slack > 0.0) {
-                for (int st = 1 << (S1_VIEWS - 1); st > 1; st >>= 1)
-                    if ((st / 2) * lip <= s1_slack) {
-                        S.s1_step = st;
-                        extra = (st / 2) * lip * (1.0 + 1e-6);
-                        break;
-                    }
-            }
-            const double d0 = (band + 4e-6 * (B0 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
-            const double d1 = (band + 4e-6 * (B1 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
             S.contig = 1;
-            S.w0lo = dn(B0 - d0);
-            S.w0hi = up(B0 + d0);
-            S.w1lo = dn(B1 - d1);
-            S.w1hi = up(B1 + d1);
+            for (int v = 0; v < S1_VIEWS; ++v) {
+                const double extra = v ? (double)(1 << (v - 1)) * lip * (1.0 + 1e-6) : 0.0;
+                if (v && !(stride == 1 && extra <= s1_slack)) break;
+                const double d0 = (band + 4e-6 * (B0 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
+                const double d1 = (band + 4e-6 * (B1 + 1.0 + band)) * (1.0 + 1e-5) + 1e-7 + extra;
+                S.wlo[v] = dn(B0 - d0);
+                S.whi[v] = up(B1 + d1);
+                S.s1_views = v + 1;
+            }
         }
     }
     a.n_rings = n_rings;
@@ -1341,7 +1459,21 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     unsigned* tile_ctr = static_cast<unsigned*>(d_ws);
     unsigned* list_ctr = tile_ctr + MAX_PARTS * CTR_STRIDE;
     unsigned* group_ctr = list_ctr + MAX_PARTS * CTR_STRIDE;
-    void* list_raw = static_cast<char*>(d_ws) + FCTR_BYTES;
+    S1Plan* plan = reinterpret_cast<S1Plan*>(static_cast<char*>(d_ws) + FCTR_BYTES);
+    void* list_raw = static_cast<char*>(d_ws) + FCTR_BYTES + PLAN_BYTES;
+    bool any_views = false;
+    for (int j = 0; j < n; ++j) any_views = any_views || a.size[j].s1_views > 1;
+    if (!coarse || !any_views || (!s1_force && (long long)rows * W * n < s1_min_work)) plan = nullptr;
+    if (plan) {
+        // stage 1's row steps for this call's rows (once, before the row bands)
+        if (cudaMemsetAsync(plan, 0, sizeof(S1Plan), s) != cudaSuccess) {
+            set_error("plan memset failed");
+            return SS_ECUDA;
+        }
+        ladder_plan_kernel<<<n * PLAN_BLOCKS, 256, 0, s>>>(a, plan, (int)y_begin, (int)y_end, (float)s1_ratio, s1_force);
+        note_launch();
+        if (int e = check_launch("ladder_plan_kernel")) return e;
+    }
 
     auto launch = [&](auto tag, auto tag1) -> int {
         using T = decltype(tag);    // the rings' planes
@@ -1373,8 +1505,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             if (coarse) {
                 // super rows of S1_SUPER tile rows; a size of row step s has S1_SUPER / s tile-row entries in each
                 tm.n_ty = (int)((brows + tile_y * S1_SUPER - 1) / (tile_y * S1_SUPER));
-                tm.n_sizes = 0;
-                for (int j = 0; j < n; ++j) tm.n_sizes += S1_SUPER / std::max(1, std::min(a.size[j].s1_step, S1_SUPER));
+                tm.n_sizes = n * S1_SUPER;  // every size at row step 1: the kernel recounts from the plan
             }
             const int n_ent = tm.n_sizes;
             tm.n_tiles = (long long)tm.n_tx * tm.n_ty * n_ent;
@@ -1417,7 +1548,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                 if constexpr (std::is_same<E, int2>::value) {
                     s1c<<<(unsigned)grid, s1_threads, s1_smem, s>>>(a, cmaps, tm, parts,
                                                                           parts > 1 ? RESERVE_LARGE : RESERVE_SMALL,
-                                                                          list, part_cap, list_ctr, tile_ctr);
+                                                                          list, part_cap, list_ctr, tile_ctr, plan);
                 }
             } else {
                 s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem, s>>>(a, maps, tm, parts,

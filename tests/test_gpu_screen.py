@@ -504,9 +504,9 @@ def _step_image(which, seed=3):
 @pytest.mark.parametrize("slack", ["0.4", "1.5", "4.0"])
 @pytest.mark.parametrize("which", ["stripes", "blocks", "smooth"])
 def test_stage1_row_steps_keep_every_ring0_passer(cuda, monkeypatch, which, slack):
-    """Coarse stage 1 tests one centre row per group of 2 or 4 rows for sizes
-    whose ring-0 mean cannot move by more than SS_S1_SLACK cells inside a
-    group (window widened by the worst-case bound) and sends the whole
+    """Coarse stage 1 may test one centre row per group of 2 or 4 rows for
+    sizes whose ring-0 mean cannot move by more than SS_S1_SLACK cells inside
+    a group (window widened by the worst-case bound), sending the whole
     group's columns on as candidates.  With std / gradient steps so large that
     membership is the mean test alone, the ring-0 passer count would drop if
     any true passer were skipped: counts and masks must equal those of the
@@ -515,14 +515,22 @@ def test_stage1_row_steps_keep_every_ring0_passer(cuda, monkeypatch, which, slac
     tpl = np.ascontiguousarray(img[200:264, 300:364])
     for q in ((8.0, 1e6, 1e6), (16.0, 8.0, 1e6)):
         cfg = pcfg({"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.25, "quantizer": q})
-        monkeypatch.setenv("SS_S1_SLACK", slack)
-        ca, ma, shifts = _stage_counts(img, tpl, cfg, cuda)
         monkeypatch.setenv("SS_S1_SLACK", "0")
+        monkeypatch.delenv("SS_S1_FORCE", raising=False)
         cb, mb, _ = _stage_counts(img, tpl, cfg, cuda)
-        assert shifts
-        assert (ca[0], ca[2], ca[3]) == (cb[0], cb[2], cb[3]), (q, ca, cb)
-        assert ca[1] >= cb[1]
-        assert np.array_equal(ma, mb)
+        # forced: the largest row step the slack allows for each size;
+        # planned: the step ladder_plan_kernel picks from its image sample
+        for force in ("1", "0"):
+            monkeypatch.setenv("SS_S1_SLACK", slack)
+            monkeypatch.setenv("SS_S1_FORCE", force)
+            monkeypatch.setenv("SS_S1_MIN_WORK", "0")  # plan even this small image
+            ca, ma, shifts = _stage_counts(img, tpl, cfg, cuda)
+            assert shifts
+            assert (ca[0], ca[2], ca[3]) == (cb[0], cb[2], cb[3]), (q, force, ca, cb)
+            assert ca[1] >= cb[1]
+            if force == "1" and float(slack) > 1.0:
+                assert ca[1] > cb[1]  # groups were formed (more candidates than the every-row test)
+            assert np.array_equal(ma, mb)
         if q[1] > 1e5:
             assert cb[2] > 0  # the comparison is not vacuous
 
@@ -548,7 +556,7 @@ def test_coarse_planes_are_bit_slices(cuda):
                                      torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     planes = p32.view(12, H + 1, pitch).cpu().numpy().view(np.uint32)
-    coarse = co.view(5, 3, H + 1, pitch).cpu().numpy().view(np.uint16)
+    coarse = co[: 5 * 3 * (H + 1) * pitch].view(5, 3, H + 1, pitch).cpu().numpy().view(np.uint16)  # (+ 4 rows of padding)
     for c, k in enumerate(shifts):
         for t, p in enumerate((0, 4, 8)):  # PLAIN SAT, E, O
             want = ((planes[p] >> np.uint32(k)) & np.uint32(0xFFFF)).astype(np.uint16)
