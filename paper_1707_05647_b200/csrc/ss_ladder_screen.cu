@@ -933,37 +933,45 @@ __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constan
     if (blockIdx.x == 0 && blockIdx.y == 0)  // the band's tile / list / group counters
         for (int i = threadIdx.x; i < ctr_words; i += blockDim.x) ctrs[i] = 0u;
     const int rows = a.y_end - a.y_begin;
-    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-        const int y = a.y_begin + r;
-        SS_CHECK(y >= a.mask_y0 && y < a.H);
-        unsigned* row = S.mask + (long long)(y - a.mask_y0) * a.mask_pitch;
-        if (threadIdx.x == 0) S.row_counts[y - a.mask_y0] = 0u;
+    auto word = [&](int y, int w) -> unsigned {
         const bool row_grid = a.stride == 1 || y % a.stride == 0;
-        const bool row_int = row_grid && y >= S.lo && y <= a.H - 1 - S.hi;
-        auto word = [&](int w) -> unsigned {
-            const int x0 = w * 32;
-            unsigned grid = 0;
-            if (row_grid) {
-                const int nb = min(32, a.W - x0);
-                if (a.stride == 1) {
-                    grid = nb == 32 ? FULL : (1u << nb) - 1u;
-                } else {
-                    for (int b = 0; b < nb; ++b)
-                        if ((x0 + b) % a.stride == 0) grid |= 1u << b;
-                }
-            }
-            unsigned inter = 0;
-            if (row_int) {
-                const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
-                if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
-            }
-            return grid & ~inter;
-        };
-        // 16-byte stores where the rows allow (the masks are ~1 GB per step at config 4)
-        const int quads = (reinterpret_cast<uintptr_t>(row) & 15) == 0 ? words >> 2 : 0;
-        for (int q = threadIdx.x; q < quads; q += blockDim.x)
-            reinterpret_cast<uint4*>(row)[q] = make_uint4(word(4 * q), word(4 * q + 1), word(4 * q + 2), word(4 * q + 3));
-        for (int w = 4 * quads + threadIdx.x; w < words; w += blockDim.x) row[w] = word(w);
+        const int x0 = w * 32;
+        const int nb = min(32, a.W - x0);
+        if (!row_grid || nb <= 0) return 0u;
+        unsigned grid = 0;
+        if (a.stride == 1) {
+            grid = nb == 32 ? FULL : (1u << nb) - 1u;
+        } else {
+            for (int b = 0; b < nb; ++b)
+                if ((x0 + b) % a.stride == 0) grid |= 1u << b;
+        }
+        unsigned inter = 0;
+        if (y >= S.lo && y <= a.H - 1 - S.hi) {
+            const int lb = max(xlo - x0, 0), hb = min(xhi - x0, 31);
+            if (lb <= hb) inter = (hb == 31 ? FULL : (1u << (hb + 1)) - 1u) & ~((1u << lb) - 1u);
+        }
+        return grid & ~inter;
+    };
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+    for (int r = tid; r < rows; r += nthr) S.row_counts[a.y_begin + r - a.mask_y0] = 0u;
+    unsigned* base = S.mask + (long long)(a.y_begin - a.mask_y0) * a.mask_pitch;
+    SS_CHECK(a.y_begin >= a.mask_y0 && a.y_end <= a.H);
+    const int qpr = (words + 3) >> 2;  // 16-byte pieces per row (the masks are ~1 GB per step at config 4)
+    if ((reinterpret_cast<uintptr_t>(base) & 15) == 0 && (a.mask_pitch & 3) == 0 && 4LL * qpr <= a.mask_pitch) {
+        // every thread of the grid stores 16 bytes per turn, rows x pieces flattened
+        const long long total = (long long)rows * qpr;
+        for (long long i = tid; i < total; i += nthr) {
+            const int r = (int)(i / qpr), q = (int)(i - (long long)r * qpr);
+            const int y = a.y_begin + r;
+            reinterpret_cast<uint4*>(base + (long long)r * a.mask_pitch)[q] =
+                make_uint4(word(y, 4 * q), word(y, 4 * q + 1), word(y, 4 * q + 2), word(y, 4 * q + 3));
+        }
+    } else {
+        const long long total = (long long)rows * words;
+        for (long long i = tid; i < total; i += nthr) {
+            const int r = (int)(i / words), w = (int)(i - (long long)r * words);
+            base[(long long)r * a.mask_pitch + w] = word(a.y_begin + r, w);
+        }
     }
 }
 
@@ -1536,7 +1544,9 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             const int parts = parts_for(W, brows, n);
             const long long part_cap = fused_part_cap(W, brows, n, sms, parts);
             {
-                const dim3 bg((unsigned)std::max<long long>(1, std::min<long long>(brows, 8LL * sms / n + 1)),
+                // 16 bytes per thread and turn over (rows x row pieces) of each size
+                const long long pieces = brows * ((((W + 31) >> 5) + 3) >> 2);
+                const dim3 bg((unsigned)std::max<long long>(1, std::min<long long>((pieces + 255) / 256, 16LL * sms / n + 1)),
                               (unsigned)n);
                 ladder_border_kernel<<<bg, 256, 0, s>>>(a, static_cast<unsigned*>(d_ws), (int)(FCTR_BYTES / 4));
                 note_launch();
