@@ -796,9 +796,9 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
                             stream);
 }
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse) {
-    // + 4 rows: stage 1's row-step TMA views (row mod step, row / step) address
-    // whole groups of up to 4 rows, the last of which may end past row H
-    return (size_t)3 * (size_t)n_coarse * (size_t)(H + 1) * ss::plane_pitch(W) * 2 + (size_t)4 * ss::plane_pitch(W) * 2;
+    // + 16 rows: stage 1's row-step TMA views (row mod step, row / step) address
+    // whole groups of up to 16 rows, the last of which may end past row H
+    return (size_t)3 * (size_t)n_coarse * (size_t)(H + 1) * ss::plane_pitch(W) * 2 + (size_t)16 * ss::plane_pitch(W) * 2;
 }
 int32_t ss_build_band_rows(int64_t W, int64_t H, int32_t exact) { return ss::pick_band_rows(W, H, exact != 0); }
 int ss_build_tables_rows(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pitch, int64_t* d_planes,

@@ -29,12 +29,15 @@
 namespace ss {
 namespace {
 
-constexpr int FMAX_SIZES = 48;  // sizes per fused group (larger groups are declined: per-size path); bounded by the 32 KB of kernel parameters
+constexpr int FMAX_SIZES = 64;  // sizes per fused group (larger groups are declined: per-size path); bounded by the 32 KB of kernel parameters
 static_assert(FMAX_SIZES <= SS_MAX_SIZES, "fused group size");
-constexpr int FMAX_RINGS = 100;  // rings over all fused sizes (kernel parameters <= 32 KB)
+constexpr int FMAX_RINGS = 104;  // rings over all fused sizes (kernel parameters <= 32 KB)
 constexpr int TAG_SHIFT = 24;    // list entry .y = row | size << TAG_SHIFT
 constexpr int YMASK = (1 << TAG_SHIFT) - 1;
 constexpr int S1_BITS_WORDS = 4096;  // stage-1 mean-projection bits of all sizes
+
+constexpr int S1_VIEWS = 5;                    // row steps 1, 2, 4, 8, 16
+constexpr int S1_SUPER = 1 << (S1_VIEWS - 1);  // tile-row blocks per super row (= the largest step)
 
 struct SizeDev {
     unsigned* mask;        // this size's mask; row 0 is global row mask_y0
@@ -49,7 +52,7 @@ struct SizeDev {
     // candidate window of the estimate per row-step view v (rows tested: one in
     // 1 << v): [B0, B1) widened by the estimate's bound and by the most t can
     // move inside a row group (ladder_stage1_coarse_kernel)
-    float wlo[3], whi[3];
+    float wlo[S1_VIEWS], whi[S1_VIEWS];
     int s1_views;         // views 0 .. s1_views - 1 are allowed for this size (>= 1)
 };
 
@@ -73,24 +76,27 @@ struct FusedArgs {
 // Stage 1 from coarse planes: per shift set c, the u16 bit slices (cell >>
 // shift) & 0xffff of the SAT / E / O PLAIN cells (ss_build_tables3).
 constexpr int CNK = SS_MAX_COARSE;
-// [v]: the view that takes every (1 << v)-th row -- a 3-D map (column, row
+// Row-step views: view v takes every (1 << v)-th row -- a 3-D map (column, row
 // mod step, row / step) of the same plane, so a 16-row box at (x, row mod
 // step, row / step) holds rows row, row + step, ... (stage 1's row steps).
-constexpr int S1_VIEWS = 3;       // row steps 1, 2, 4
-constexpr int S1_SUPER = 4;       // tile-row blocks per super row (= the largest step)
+// View 0 (plain 2-D maps) travels in the kernel parameters; views 1.. live in
+// device memory (CoarseViewMaps, written once per plane buffer).
+struct CoarseMaps {
+    CUtensorMap sat[CNK], e[CNK], o[CNK];
+};
+struct CoarseViewMaps {
+    CUtensorMap sat[S1_VIEWS - 1][CNK], e[S1_VIEWS - 1][CNK], o[S1_VIEWS - 1][CNK];
+};
 #ifndef S1_SLACK_DEFAULT
 #define S1_SLACK_DEFAULT 4.0
 #endif
 #ifndef S1_RATIO_DEFAULT
 #define S1_RATIO_DEFAULT 13.0
 #endif
-struct CoarseMaps {
-    CUtensorMap sat[S1_VIEWS][CNK], e[S1_VIEWS][CNK], o[S1_VIEWS][CNK];
-};
 // Stage 1's row steps, chosen on the device per call (ladder_plan_kernel).
 struct S1Plan {
     int view[FMAX_SIZES];         // the chosen view (row step 1 << view) per size
-    unsigned cnt[FMAX_SIZES][4];  // samples inside the window of view 0, 1, 2; samples taken
+    unsigned cnt[FMAX_SIZES][S1_VIEWS + 1];  // samples inside the window of each view; samples taken
     unsigned ticket;
     int pad[3];
 };
@@ -526,9 +532,9 @@ __global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant_
     const int sz = blockIdx.x / PLAN_BLOCKS, part = blockIdx.x % PLAN_BLOCKS;
     const SizeDev& S = a.size[sz];
     const RingDev& R0 = a.ring[S.ring0];
-    __shared__ unsigned c_sh[4];
+    __shared__ unsigned c_sh[S1_VIEWS + 1];
     __shared__ bool last_sh;
-    if (threadIdx.x < 4) c_sh[threadIdx.x] = 0;
+    if (threadIdx.x <= S1_VIEWS) c_sh[threadIdx.x] = 0;
     __syncthreads();
     const int xlo = S.lo, xhi = a.W - 1 - S.hi;
     const int ylo = max(y_lo, S.lo), yhi = min(y_hi - 1, a.H - 1 - S.hi);
@@ -540,7 +546,9 @@ __global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant_
         const int n = R0.n, d = R0.d;
         const float fa = (float)(0.5 / ((double)(4LL * n * n) * a.qm));
         const float fb = (float)(0.5 / ((double)(2LL * d * d + 2LL * d + 1) * a.qm));
-        unsigned c0 = 0, c1 = 0, c2 = 0, ct = 0;
+        unsigned c[S1_VIEWS + 1];
+#pragma unroll
+        for (int v = 0; v <= S1_VIEWS; ++v) c[v] = 0;
 #pragma unroll 2
         for (int i = part * 256 + threadIdx.x; i < nx * ny; i += PLAN_BLOCKS * 256) {
             const int iy = i / nx, ix = i - iy * nx;
@@ -555,19 +563,17 @@ __global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant_
             const unsigned di = __ldg(e + (r + d + 1) * pitch + cx + 1) - __ldg(o + r * pitch + cx - d) -
                                 __ldg(o + r * pitch + cx + d + 1) + __ldg(e + (r - d) * pitch + cx + 1);
             const float t = fmaf((float)sq, fa, fmaf((float)di, fb, 0.5f));
-            ++ct;
-            c0 += t >= S.wlo[0] && t <= S.whi[0];
-            c1 += t >= S.wlo[1] && t <= S.whi[1];
-            c2 += t >= S.wlo[2] && t <= S.whi[2];
+            ++c[S1_VIEWS];
+#pragma unroll
+            for (int v = 0; v < S1_VIEWS; ++v) c[v] += v < S.s1_views && t >= S.wlo[v] && t <= S.whi[v];
         }
-        atomicAdd(&c_sh[0], c0);
-        atomicAdd(&c_sh[1], c1);
-        atomicAdd(&c_sh[2], c2);
-        atomicAdd(&c_sh[3], ct);
+#pragma unroll
+        for (int v = 0; v <= S1_VIEWS; ++v)
+            if (c[v]) atomicAdd(&c_sh[v], c[v]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k <= S1_VIEWS; ++k)
             if (c_sh[k]) atomicAdd(&plan->cnt[sz][k], c_sh[k]);
         __threadfence();
         last_sh = atomicAdd(&plan->ticket, 1u) == gridDim.x - 1;
@@ -581,8 +587,8 @@ __global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant_
         int best = 0;
         if (force) {
             best = Sj.s1_views - 1;
-        } else if (Sj.s1_views > 1 && c[3] > 0) {
-            const float inv = 1.0f / (float)c[3];
+        } else if (Sj.s1_views > 1 && c[S1_VIEWS] > 0) {
+            const float inv = 1.0f / (float)c[S1_VIEWS];
             float cost = 1.0f;
             for (int v = 1; v < Sj.s1_views; ++v) {
                 const float cv = 1.0f / (float)(1 << v) + ratio * (float)(c[v] - c[0]) * inv;
@@ -610,7 +616,7 @@ __global__ void __launch_bounds__(256) ladder_plan_kernel(const __grid_constant_
 // centre.
 __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     ladder_stage1_coarse_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__ CoarseMaps maps,
-                                const TileMapF tm_in, int parts, int reserve, int2* list_base, long long part_cap,
+                                const CoarseViewMaps* __restrict__ vmaps, const TileMapF tm_in, int parts, int reserve, int2* list_base, long long part_cap,
                                 unsigned* list_ctr, unsigned* tile_ctr_base, const S1Plan* plan) {
     using G = GeoC;
     constexpr int STAGES = G::STAGES, CPW = G::CPW, CW = G::CW;
@@ -743,7 +749,9 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                 const int xo = b < 4 ? ((b & 1) ? 1 - n : n + 1) : (b < 6 ? 1 : (b == 6 ? -d : d + 1));
                 const int yo = b < 4 ? ((b & 2) ? 1 - n : n + 1) : (b == 4 ? d + 1 : (b == 5 ? -d : 0));
                 const CUtensorMap* m =
-                    b < 4 ? &maps.sat[view][csq] : (b < 6 ? &maps.e[view][st.w] : &maps.o[view][st.w]);
+                    view == 0 ? (b < 4 ? &maps.sat[csq] : (b < 6 ? &maps.e[st.w] : &maps.o[st.w]))
+                              : (b < 4 ? &vmaps->sat[view - 1][csq]
+                                       : (b < 6 ? &vmaps->e[view - 1][st.w] : &vmaps->o[view - 1][st.w]));
                 const int x0 = tx * G::TX;
                 // tile row j tests the centre row y_begin + r0 + j step + step / 2 for its group of `step` rows
                 const int cy0 = a.y_begin + r0 + (step >> 1) - a.y_origin;
@@ -1188,11 +1196,15 @@ int plane_maps_cached(TmaMaps& maps, const void* planes, int eb, int bw, int64_t
 
 // The coarse TMA descriptors (u16 SAT / E / O bit-slice planes of every
 // shift set), cached like plane_maps_cached.
-int coarse_maps_cached(CoarseMaps& maps, const uint16_t* coarse, int n_coarse, int64_t W, int64_t h, int64_t pitch,
-                       long long ps) {
+int coarse_maps_cached(CoarseMaps& maps, const CoarseViewMaps*& d_vmaps, const uint16_t* coarse, int n_coarse, int64_t W,
+                       int64_t h, int64_t pitch, long long ps) {
     using Key = std::tuple<const void*, int, int64_t, int64_t, int64_t, int>;
+    struct Val {
+        CoarseMaps maps;
+        CoarseViewMaps* d_views;
+    };
     static std::mutex mu;
-    static std::map<Key, CoarseMaps> cache;
+    static std::map<Key, Val> cache;
     int dev = 0;
     cudaGetDevice(&dev);
     const Key key{coarse, n_coarse, W, h, pitch, dev};
@@ -1200,22 +1212,41 @@ int coarse_maps_cached(CoarseMaps& maps, const uint16_t* coarse, int n_coarse, i
         std::lock_guard<std::mutex> lock(mu);
         const auto it = cache.find(key);
         if (it != cache.end()) {
-            maps = it->second;
+            maps = it->second.maps;
+            d_vmaps = it->second.d_views;
             return SS_OK;
         }
     }
     std::memset(&maps, 0, sizeof(maps));
+    std::vector<CoarseViewMaps> hv(1);
+    std::memset(hv.data(), 0, sizeof(CoarseViewMaps));
     for (int v = 0; v < S1_VIEWS; ++v)
         for (int c = 0; c < n_coarse; ++c) {
             const uint16_t* base = coarse + (size_t)c * 3 * (size_t)ps;
-            if (int e = encode_plane_map(&maps.sat[v][c], base, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
-            if (int e = encode_plane_map(&maps.e[v][c], base + ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
-            if (int e = encode_plane_map(&maps.o[v][c], base + 2 * ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v))
-                return e;
+            CUtensorMap* ms = v ? &hv[0].sat[v - 1][c] : &maps.sat[c];
+            CUtensorMap* me = v ? &hv[0].e[v - 1][c] : &maps.e[c];
+            CUtensorMap* mo = v ? &hv[0].o[v - 1][c] : &maps.o[c];
+            if (int e = encode_plane_map(ms, base, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
+            if (int e = encode_plane_map(me, base + ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
+            if (int e = encode_plane_map(mo, base + 2 * ps, 2, GeoC::BW, W, h, pitch, GeoC::TYC, 1 << v)) return e;
         }
+    // the row-step views go to device memory once per plane buffer (a blocking
+    // copy: the first screen from a buffer, never inside a graph capture that
+    // replays an already cached buffer)
+    CoarseViewMaps* d_views = nullptr;
+    if (cudaMalloc(&d_views, sizeof(CoarseViewMaps)) != cudaSuccess ||
+        cudaMemcpy(d_views, hv.data(), sizeof(CoarseViewMaps), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("row-step TMA views: %s", cudaGetErrorString(cudaGetLastError()));
+        if (d_views) cudaFree(d_views);
+        return SS_ECUDA;
+    }
+    d_vmaps = d_views;
     std::lock_guard<std::mutex> lock(mu);
-    if (cache.size() > 256) cache.clear();
-    cache[key] = maps;
+    if (cache.size() > 256) {
+        for (auto& kv : cache) cudaFree(kv.second.d_views);
+        cache.clear();
+    }
+    cache[key] = Val{maps, d_views};
     return SS_OK;
 }
 
@@ -1233,6 +1264,14 @@ int coarse_shift(long long count) {
 
 size_t screen_workspace_bytes(int64_t W, int64_t rows);  // ss_screen.cu
 
+// Half a row band, on whole super rows of the coarse stage 1 (16 x 16 rows)
+// while that still shrinks it, else on whole tile rows.
+int64_t halve_band(int64_t band) {
+    constexpr int AL = TY * S1_SUPER;
+    const int64_t b = (band / 2 + AL - 1) / AL * AL;
+    return b < band ? b : (band / 2 + TY - 1) / TY * TY;
+}
+
 // Workspace of the fused ladder for `n_sizes` sizes: one row band up to
 // FUSED_WS_CAP (taller images run in several bands), and never less than the
 // per-size screen needs (the fallback shares it).
@@ -1240,9 +1279,7 @@ size_t ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes) {
     const int sms = device_sms();
     const int64_t S = std::max<int32_t>(n_sizes, 1);
     int64_t band = std::max<int64_t>(rows, 1);
-    constexpr int BAND_AL = TY * S1_SUPER;  // as the launch loop of ladder_screen
-    while (band > 4 * TY && fused_ws_bytes(W, band, (int)S, sms) > FUSED_WS_CAP)
-        band = (band / 2 + BAND_AL - 1) / BAND_AL * BAND_AL;
+    while (band > 4 * TY && fused_ws_bytes(W, band, (int)S, sms) > FUSED_WS_CAP) band = halve_band(band);
     return std::max(fused_ws_bytes(W, band, (int)S, sms), screen_workspace_bytes(W, std::max<int64_t>(rows, 1)));
 }
 
@@ -1438,8 +1475,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     const int sms = device_sms();
     // row bands: as many rows per pass as the workspace holds
     int64_t band = rows;
-    constexpr int BAND_AL = TY * S1_SUPER;  // whole super rows of the coarse stage 1
-    while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = (band / 2 + BAND_AL - 1) / BAND_AL * BAND_AL;
+    while (band > 4 * TY && fused_ws_bytes(W, band, n, sms) > ws_bytes) band = halve_band(band);
     if (!d_ws || fused_ws_bytes(W, band, n, sms) > ws_bytes) return SS_DECLINED;
 
     // Stage 1 reads only the ring-0 PLAIN sums: when they fit 32 bits for
@@ -1457,8 +1493,9 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     // (row counts and workspace counters are zeroed by ladder_border_kernel)
     TmaMaps maps;
     CoarseMaps cmaps;
+    const CoarseViewMaps* d_vmaps = nullptr;
     if (coarse) {
-        if (int e = coarse_maps_cached(cmaps, d_coarse, n_coarse, W, h, pitch, a.ps)) return e;
+        if (int e = coarse_maps_cached(cmaps, d_vmaps, d_coarse, n_coarse, W, h, pitch, a.ps)) return e;
     } else if (int e = s1_u32 ? plane_maps_cached(maps, eb == 4 ? planes : planes32_s1, 4, GeoF<unsigned>::BW, W, h,
                                                   pitch, a.ps)
                               : plane_maps_cached(maps, planes, 8, GeoF<long long>::BW, W, h, pitch, a.ps)) {
@@ -1556,7 +1593,7 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
                                                        (long long)TILE_CTRS);
             if (coarse) {
                 if constexpr (std::is_same<E, int2>::value) {
-                    s1c<<<(unsigned)grid, s1_threads, s1_smem, s>>>(a, cmaps, tm, parts,
+                    s1c<<<(unsigned)grid, s1_threads, s1_smem, s>>>(a, cmaps, d_vmaps, tm, parts,
                                                                           parts > 1 ? RESERVE_LARGE : RESERVE_SMALL,
                                                                           list, part_cap, list_ctr, tile_ctr, plan);
                 }

@@ -647,12 +647,16 @@ class Engine:
         # screen and the copy left after the last piece is short
         dec, owner, prev = [], [], 0
         for k, e in enumerate(ends):
-            d = H if e == H else max(prev, e - hi_max - 1)
+            # cuts on multiples of 16 rows: stage 1 decides groups of up to 16
+            # rows from one tested row, and a group cut by a piece's end falls
+            # back to "every column is a candidate"
+            d = H if e == H else max(prev, (e - hi_max - 1) // 16 * 16)
             parts = 4 if e == H else 2
-            cuts = [prev + (d - prev) * i // parts for i in range(parts + 1)]
+            cuts = [prev] + [max(prev, (prev + (d - prev) * i // parts) // 16 * 16) for i in range(1, parts)] + [d]
             for a, b in zip(cuts[:-1], cuts[1:]):
-                dec.append((a, b))
-                owner.append(k)
+                if b > a:
+                    dec.append((a, b))
+                    owner.append(k)
             prev = d
         src = torch.from_numpy(img)
         pinned_src = src.is_pinned()
@@ -660,9 +664,11 @@ class Engine:
         built = []
 
         def build(i: int) -> None:
-            k = owner[i]  # screen piece i needs build chunk k
-            if k in built:
-                return
+            # screen piece i needs the build chunks up to owner[i] (chunks go up in order)
+            for k in range(len(built), owner[i] + 1):
+                build_chunk(k)
+
+        def build_chunk(k: int) -> None:
             built.append(k)
             r0, r1 = (0 if k == 0 else ends[k - 1]), ends[k]
             if pinned_src:  # the caller's buffer is pinned: DMA straight from it
