@@ -876,16 +876,26 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
         // recomputes ring 0's exact mean cell and tests it (eval_ring_fast)
         pm |= amb;
         if (!__any_sync(FULL, pm != 0u)) continue;
-        // a passing column is a candidate on every interior row of the group
+        // a passing column is a candidate on every interior row of the group:
+        // the columns' places in the staging buffer are found once (one ballot
+        // per 32-column chunk), then each row appends its entries
+        unsigned long long cnt6 = 0;  // per-chunk counts (<= 32), 6 bits each
+        int off[CPW];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            const unsigned pb = __ballot_sync(FULL, (pm >> c) & 1u);
+            off[c] = __popc(pb & lt);
+            cnt6 |= (unsigned long long)__popc(pb) << (6 * c);
+        }
         for (int yg = gv0; yg <= gv1; ++yg) {
             const int tag = yg | (sz << TAG_SHIFT);
 #pragma unroll
             for (int c = 0; c < CPW; ++c) {
-                const bool p = (pm >> c) & 1u;
-                const unsigned pb = __ballot_sync(FULL, p);
-                if (p) buf[nbuf + __popc(pb & lt)] = make_int2(xt + 32 * c + lane, tag);
-                nbuf += __popc(pb);
-                n_pass += __popc(pb);
+                const int cc = (int)((cnt6 >> (6 * c)) & 63ull);
+                if (cc == 0) continue;  // warp-uniform
+                if ((pm >> c) & 1u) buf[nbuf + off[c]] = make_int2(xt + 32 * c + lane, tag);
+                nbuf += cc;
+                n_pass += cc;
                 if (nbuf >= 32) {
                     __syncwarp();
                     if (res_left == 0) {
@@ -1518,6 +1528,18 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
         ladder_plan_kernel<<<n * PLAN_BLOCKS, 256, 0, s>>>(a, plan, (int)y_begin, (int)y_end, (float)s1_ratio, s1_force);
         note_launch();
         if (int e = check_launch("ladder_plan_kernel")) return e;
+        if (getenv("SS_S1_DEBUG")) {  // experiments: print the plan (blocks the stream)
+            S1Plan hp;
+            cudaStreamSynchronize(s);
+            cudaMemcpy(&hp, plan, sizeof(hp), cudaMemcpyDeviceToHost);
+            for (int j = 0; j < n; ++j) {
+                const RingDev& R0 = a.ring[a.size[j].ring0];
+                std::fprintf(stderr, "[s1 plan] size %d n=%d d=%d views=%d -> step %d; samples %u in-window", j, R0.n, R0.d,
+                             a.size[j].s1_views, 1 << hp.view[j], hp.cnt[j][S1_VIEWS]);
+                for (int v = 0; v < a.size[j].s1_views; ++v) std::fprintf(stderr, " %u", hp.cnt[j][v]);
+                std::fprintf(stderr, "\n");
+            }
+        }
     }
 
     auto launch = [&](auto tag, auto tag1) -> int {
