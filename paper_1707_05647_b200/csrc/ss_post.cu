@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
                                                                     long long words, long long P,
                                                                     const Ladder lad, unsigned* Hb,
                                                                     unsigned* region, long long region_pitch,
-                                                                    int y0, int Hg) {
+                                                                    int y0, int Hg, unsigned char* live_rows) {
     extern __shared__ unsigned rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long task = (long long)blockIdx.x * RP_WARPS + warp;
@@ -358,10 +358,11 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
         A[i] = v;
         any |= v;
     }
-    if (!__any_sync(FULL, any != 0u)) {
-        for (long long i = lane; i < words; i += 32) out[i] = 0u;
-        return;
-    }
+    // rows without a survivor (3 in 4 at config 4) are only flagged: the column
+    // pass reads live_rows and never touches their H_k row
+    const bool has = __any_sync(FULL, any != 0u);
+    if (lane == 0) live_rows[(long long)k * H + y] = has ? 1 : 0;
+    if (!has) return;
     __syncwarp();
     const int L = m;
     int l = 1;
@@ -392,22 +393,37 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
 // for C outputs (van Herk / Gil-Werman).  Sizes with L < C take every window
 // directly.
 template <int C>
-__global__ void region_cols_kernel(const unsigned* Hb, int H, long long words, long long chunks, const Ladder lad,
-                                   unsigned* region, long long region_pitch) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (long long)lad.L * chunks * words) return;
-    const long long w = gid % words, t = gid / words;
-    const long long ch = t % chunks;
-    const int k = (int)(t / chunks);
+__global__ void __launch_bounds__(128) region_cols_kernel(const unsigned* Hb, int H, long long words, long long wblocks,
+                                                          long long chunks, const Ladder lad, unsigned* region,
+                                                          long long region_pitch, const unsigned char* live_rows) {
+    // a block: 128 word columns of one (size, row chunk); the live flags of
+    // the rows its windows cover are staged once, and a block none of whose
+    // rows holds a survivor leaves at once
+    const long long t = blockIdx.x;
+    const long long wb = t % wblocks, ch = (t / wblocks) % chunks;
+    const int k = (int)(t / (wblocks * chunks));
     const int m = lad.m[k];
     if (m < 8) return;
     const int lo = (m - 1) / 2, hi = m / 2, L = m;
-    const unsigned* col = Hb + (long long)k * H * words + w;
-    auto ld = [&](int j) -> unsigned { return (j >= 0 && j < H) ? __ldg(col + (long long)j * words) : 0u; };
     const int r0 = (int)(ch * C);
+    const int a0 = r0 - hi, span = L + C - 1;  // rows a0 .. a0 + span - 1
+    extern __shared__ unsigned char live_sh[];
+    const unsigned char* lv = live_rows + (long long)k * H;
+    int any = 0;
+    for (int i = threadIdx.x; i < span; i += blockDim.x) {
+        const int j = a0 + i;
+        const unsigned char f = (j >= 0 && j < H) ? lv[j] : 0;
+        live_sh[i] = f;
+        any |= f;
+    }
+    if (!__syncthreads_or(any)) return;
+    const long long w = wb * 128 + threadIdx.x;
+    if (w >= words) return;
+    const unsigned* col = Hb + (long long)k * H * words + w;
+    auto ld = [&](int j) -> unsigned { return live_sh[j - a0] ? __ldg(col + (long long)j * words) : 0u; };
     unsigned out[C];
     if (L >= C) {
-        const int a0 = r0 - hi, b = a0 + L - 1;
+        const int b = a0 + L - 1;
         unsigned s = 0;
 #pragma unroll 16
         for (int j = b; j >= a0 + C; --j) s |= ld(j);  // independent loads: 16 in flight
@@ -641,7 +657,8 @@ int compact_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_str
 
 size_t region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t L) {
     // the row-pass buffer of every size (region_ladder_rows), >= the chained form's two bitmaps
-    return (size_t)std::max<int32_t>(L, 2) * H * ((W + 31) / 32) * 4;
+    // + one live flag per (size, row)
+    return (size_t)std::max<int32_t>(L, 2) * H * ((W + 31) / 32) * 4 + ((size_t)std::max<int32_t>(L, 2) * H + 255) / 256 * 256;
 }
 
 // K5 over a window of H mask rows whose row 0 is global row y0 of an Hg-row
@@ -662,6 +679,7 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
     for (int k = 0; k < L; ++k) m_max = std::max(m_max, (int)h_m[k]);
     const int64_t words = (W + 31) / 32;
     unsigned* Hb = static_cast<unsigned*>(d_ws);
+    unsigned char* live_rows = reinterpret_cast<unsigned char*>(Hb + (size_t)std::max<int32_t>(L, 2) * H * words);
     cudaStream_t s = as_stream(stream);
     {
         const int64_t P = m_max / 32 + 2;  // left padding (words) >= ceil(hi / 32)
@@ -675,7 +693,7 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
         const long long tasks = (long long)L * H;
         region_rows_kernel<<<(unsigned)((tasks + RP_WARPS - 1) / RP_WARPS), RP_WARPS * 32, smem, s>>>(
             d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb, d_region, mask_pitch, (int)y0,
-            (int)Hg);
+            (int)Hg, live_rows);
         note_launch();
         if (int e = check_launch("region_rows_kernel")) return e;
     }
@@ -683,12 +701,15 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
     const bool tall = m_max >= 128;
     const int C = tall ? 32 : 16;
     const long long chunks = (H + C - 1) / C;
-    const long long threads = (long long)L * chunks * words;
-    const unsigned grid = (unsigned)((threads + 127) / 128);
+    const long long wblocks = (words + 127) / 128;
+    const unsigned grid = (unsigned)((long long)L * chunks * wblocks);
+    const size_t fl = (size_t)(m_max + C - 1 + 15) / 16 * 16;  // the live flags of a block's rows
     if (tall)
-        region_cols_kernel<32><<<grid, 128, 0, s>>>(Hb, (int)H, words, chunks, lad, d_region, mask_pitch);
+        region_cols_kernel<32><<<grid, 128, fl, s>>>(Hb, (int)H, words, wblocks, chunks, lad, d_region, mask_pitch,
+                                                      live_rows);
     else
-        region_cols_kernel<16><<<grid, 128, 0, s>>>(Hb, (int)H, words, chunks, lad, d_region, mask_pitch);
+        region_cols_kernel<16><<<grid, 128, fl, s>>>(Hb, (int)H, words, wblocks, chunks, lad, d_region, mask_pitch,
+                                                      live_rows);
     note_launch();
     return check_launch("region_cols_kernel");
 }
