@@ -96,7 +96,15 @@ __device__ __forceinline__ long long rowpre_at(const BuildArgs& a, int64_t y, in
 // {0, 2} (PLAIN, Y) or {1, 3} (X, SQ) -- half the recurrence registers, so the
 // int64 build keeps more warps resident (pass 3 at config 4 ran 3 CTAs / SM).
 template <int kMode, int RB, typename V, int NK = 4>
-__global__ void __launch_bounds__(TPB) band_kernel(BuildArgs a) {
+#ifndef BAND_MINB64
+#define BAND_MINB64 3  // 168 registers, no spills: 3 CTAs per SM (config 4 build 6.3 -> 5.6 ms); 4 spills and is slower
+#endif
+#ifndef BAND_MINB32
+#define BAND_MINB32 5  // 96 registers, no spills (config 1 step 0.646 -> 0.629 ms, config 2 1.72 -> 1.70)
+#endif
+__global__ void __launch_bounds__(TPB, (kMode == 1 && sizeof(V) == 8 && NK == 4)   ? BAND_MINB64
+                                       : (kMode == 1 && sizeof(V) == 4 && NK == 2) ? BAND_MINB32
+                                                                                   : 1) band_kernel(BuildArgs a) {
     static_assert(NK == 4 || NK == 2, "kinds per CTA");
     const int kg = NK == 4 ? 0 : (int)blockIdx.z;
     auto KIND = [&](int kk) { return NK == 4 ? kk : kg + 2 * kk; };

@@ -27,6 +27,7 @@ def main(path, runs=1):
     b = defaultdict(float)
     n = defaultdict(int)
     inst = defaultdict(float)
+    l2 = defaultdict(float)
     for r in rows[1:]:
         if len(r) < len(hdr):
             continue
@@ -39,6 +40,8 @@ def main(path, runs=1):
             b[name] += val * SCALE_B[unit]
         elif metric == "smsp__inst_executed.sum":
             inst[name] += val
+        elif metric == "lts__t_bytes.sum":
+            l2[name] += val * SCALE_B[unit]
     tot = sum(t.values())
     print(f"{'kernel':40s} {'launch':>7s} {'ms/run':>9s} {'share':>6s} {'GB/run':>8s} {'GB/s':>7s}")
     for k in sorted(t, key=lambda k: -t[k]):
@@ -46,6 +49,7 @@ def main(path, runs=1):
         gb = b[k] / runs
         print(f"{k[:40]:40s} {n[k] // runs:7d} {ms:9.3f} {t[k] / tot:6.1%} {gb:8.2f} {gb / (ms / 1e3) if ms else 0:7.0f}")
     print(f"total ms/run {tot / 1e3 / runs:.3f}")
+    main.l2 = l2
     return t, b, inst
 
 
@@ -60,6 +64,14 @@ def record_k3(path, runs, name, rnd="r2"):
         rec["inst_per_step"] = sum(inst[k] for k in k3) / runs
         rec["inst_stage1_per_step"] = sum(inst[k] for k in k3 if "stage1" in k) / runs
         rec["inst_rings_per_step"] = sum(inst[k] for k in k3 if "ring" in k) / runs
+    # per-kernel-family times (ms per step under ncu) and stage 1's L2 bytes
+    fam = {"stage1": "stage1", "rings": "ring", "border": "border_kernel", "build": "band_", "region": "region_",
+           "rowpre": "rowpre", "compact": "_xy_", "plan": "plan_kernel"}
+    rec["ms_per_step_under_ncu"] = {f: sum(t[k] for k in t if sub in k) / 1e3 / runs for f, sub in fam.items()}
+    l2 = getattr(main, "l2", {})
+    if l2:
+        rec["l2_bytes_stage1_per_step"] = sum(l2[k] for k in l2 if "stage1" in k) * 1e9 / runs
+        rec["l2_bytes_rings_per_step"] = sum(l2[k] for k in l2 if "ring" in k) * 1e9 / runs
     out = os.path.join(root, "profiles", rnd, "k3_traffic.json")
     data = json.load(open(out)) if os.path.exists(out) else {}
     data[name] = rec
