@@ -1519,13 +1519,14 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
     bool any_views = false;
     for (int j = 0; j < n; ++j) any_views = any_views || a.size[j].s1_views > 1;
     if (!coarse || !any_views || (!s1_force && (long long)rows * W * n < s1_min_work)) plan = nullptr;
-    if (plan) {
-        // stage 1's row steps for this call's rows (once, before the row bands)
+    // stage 1's row steps, planned per row band (the candidate density varies
+    // along an image: config 4's last 3 of 16 bands hold 60% of the rings' work)
+    auto plan_rows = [&](int64_t yb, int64_t ye) -> int {
         if (cudaMemsetAsync(plan, 0, sizeof(S1Plan), s) != cudaSuccess) {
             set_error("plan memset failed");
             return SS_ECUDA;
         }
-        ladder_plan_kernel<<<n * PLAN_BLOCKS, 256, 0, s>>>(a, plan, (int)y_begin, (int)y_end, (float)s1_ratio, s1_force);
+        ladder_plan_kernel<<<n * PLAN_BLOCKS, 256, 0, s>>>(a, plan, (int)yb, (int)ye, (float)s1_ratio, s1_force);
         note_launch();
         if (int e = check_launch("ladder_plan_kernel")) return e;
         if (getenv("SS_S1_DEBUG")) {  // experiments: print the plan (blocks the stream)
@@ -1534,13 +1535,15 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             cudaMemcpy(&hp, plan, sizeof(hp), cudaMemcpyDeviceToHost);
             for (int j = 0; j < n; ++j) {
                 const RingDev& R0 = a.ring[a.size[j].ring0];
-                std::fprintf(stderr, "[s1 plan] size %d n=%d d=%d views=%d -> step %d; samples %u in-window", j, R0.n, R0.d,
-                             a.size[j].s1_views, 1 << hp.view[j], hp.cnt[j][S1_VIEWS]);
+                std::fprintf(stderr, "[s1 plan] rows [%lld, %lld) size %d n=%d d=%d views=%d -> step %d; samples %u in-window",
+                             (long long)yb, (long long)ye, j, R0.n, R0.d, a.size[j].s1_views, 1 << hp.view[j],
+                             hp.cnt[j][S1_VIEWS]);
                 for (int v = 0; v < a.size[j].s1_views; ++v) std::fprintf(stderr, " %u", hp.cnt[j][v]);
                 std::fprintf(stderr, "\n");
             }
         }
-    }
+        return SS_OK;
+    };
 
     auto launch = [&](auto tag, auto tag1) -> int {
         using T = decltype(tag);    // the rings' planes
@@ -1564,6 +1567,8 @@ int screen_ladder_fused(const void* planes, int eb, const void* planes32_s1, int
             const int64_t ye = std::min<int64_t>(y_end, yb + band), brows = ye - yb;
             a.y_begin = (int)yb;
             a.y_end = (int)ye;
+            if (plan)
+                if (int e = plan_rows(yb, ye)) return e;
             TileMapF tm;
             tm.n_tx = (int)((W + tile_x - 1) / tile_x);
             const int tile_y = coarse ? GeoC::TYC : TY;
