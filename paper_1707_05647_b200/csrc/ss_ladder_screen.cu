@@ -422,7 +422,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
                     have_res = true;
                 }
                 SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
-                list0[res_base + lane] = buf[nbuf - 32 + lane];
+                if (res_base + lane < (unsigned)part_cap) list0[res_base + lane] = buf[nbuf - 32 + lane];
                 res_base += 32;
                 res_left -= 32;
                 nbuf -= 32;
@@ -438,14 +438,16 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
             left = reserve;
         } else {
             const unsigned ahead = __shfl_sync(FULL, res, 0);
-            for (unsigned i = lane; i < (unsigned)reserve; i += 32) list0[ahead + i] = no_entry<E>();
+            for (unsigned i = lane; i < (unsigned)reserve; i += 32)
+                if (ahead + i < (unsigned)part_cap) list0[ahead + i] = no_entry<E>();
         }
-        for (unsigned i = lane; i < left; i += 32) list0[base + i] = i < (unsigned)nbuf ? buf[i] : no_entry<E>();
+        for (unsigned i = lane; i < left; i += 32)
+            if (base + i < (unsigned)part_cap) list0[base + i] = i < (unsigned)nbuf ? buf[i] : no_entry<E>();
     } else if (nbuf > 0) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
         base = __shfl_sync(FULL, base, 0);
-        if (lane < nbuf) list0[base + lane] = buf[lane];
+        if (lane < nbuf && base + lane < (unsigned)part_cap) list0[base + lane] = buf[lane];
     }
     if (a.stage_counts && lane == 0) {
         atomicAdd(a.stage_counts + 0, (unsigned long long)n_int);
@@ -522,7 +524,7 @@ struct __align__(16) TileConstC {
 //     1 / step + ratio * (P_view - P_0),
 // ratio = cost of a false candidate in the rings kernel / cost of a stage-1
 // centre (measured ~13 on B200: ~28 ps against ~2 ps).
-constexpr int PLAN_N = 64;
+constexpr int PLAN_N = 64;  // lattice points per axis and size (each sample costs 8 sectors: config 4 plans 24 bands x 33 sizes)
 constexpr int PLAN_BLOCKS = 8;  // blocks per size (two samples per thread)
 // below this many positions x sizes per call the plan cannot repay its launch
 // (config 1: stage 1 is 0.15 ms): every size keeps row step 1
@@ -906,7 +908,7 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
                         have_res = true;
                     }
                     SS_CHECK(res_base + lane < (unsigned)part_cap && nbuf - 32 + lane < CAND_BUF);
-                    list0[res_base + lane] = buf[nbuf - 32 + lane];
+                    if (res_base + lane < (unsigned)part_cap) list0[res_base + lane] = buf[nbuf - 32 + lane];
                     res_base += 32;
                     res_left -= 32;
                     nbuf -= 32;
@@ -923,14 +925,16 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
             left = reserve;
         } else {
             const unsigned ahead = __shfl_sync(FULL, res, 0);
-            for (unsigned i = lane; i < (unsigned)reserve; i += 32) list0[ahead + i] = make_int2(-1, -1);
+            for (unsigned i = lane; i < (unsigned)reserve; i += 32)
+                if (ahead + i < (unsigned)part_cap) list0[ahead + i] = make_int2(-1, -1);
         }
-        for (unsigned i = lane; i < left; i += 32) list0[base + i] = i < (unsigned)nbuf ? buf[i] : make_int2(-1, -1);
+        for (unsigned i = lane; i < left; i += 32)
+            if (base + i < (unsigned)part_cap) list0[base + i] = i < (unsigned)nbuf ? buf[i] : make_int2(-1, -1);
     } else if (nbuf > 0) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(count0, (unsigned)nbuf);
         base = __shfl_sync(FULL, base, 0);
-        if (lane < nbuf) list0[base + lane] = buf[lane];
+        if (lane < nbuf && base + lane < (unsigned)part_cap) list0[base + lane] = buf[lane];
     }
     if (a.stage_counts && lane == 0) {
         atomicAdd(a.stage_counts + 0, (unsigned long long)n_int);
@@ -1039,7 +1043,8 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     const unsigned wid = blockIdx.x * RK_WARPS + warp;
     int q = (int)(wid % parts), visited = 1;
     const unsigned gc = (wid / parts) % GROUP_CTRS;
-    unsigned cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
+    // (a list never extends past its partition: stage 1 drops what would not fit)
+    unsigned cnt_q = min(__ldg(list_ctr + q * CTR_STRIDE), (unsigned)part_cap);
     const E* in = list_base + q * part_cap;
     unsigned g_raw = 0;
     if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
@@ -1058,7 +1063,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
             }
             ++visited;
             q = q + 1 == parts ? 0 : q + 1;
-            cnt_q = __ldg(list_ctr + q * CTR_STRIDE);
+            cnt_q = min(__ldg(list_ctr + q * CTR_STRIDE), (unsigned)part_cap);
             in = list_base + q * part_cap;
             if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
         }
