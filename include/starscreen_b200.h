@@ -296,6 +296,14 @@ size_t ss_region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t n_sizes);
 int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
                      int32_t n_sizes, const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_workspace,
                      size_t workspace_bytes, void* stream);
+/* ss_region_ladder with K3's per-row survivor counts (d_row_counts + k *
+ * row_counts_stride + y: interior survivors of size k in mask row y, as the
+ * ss_screen_* calls leave them; may be NULL): rows without a survivor are
+ * skipped without reading their mask row (3 in 4 rows of BASELINE config 4). */
+int ss_region_ladder2(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
+                      int32_t n_sizes, const int32_t* h_m, int32_t stride, const uint32_t* d_row_counts,
+                      int64_t row_counts_stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes,
+                      void* stream);
 /*
  * K5 over a window of `rows` mask rows (per size, same layout) whose row 0 is
  * global row y0 of an H-row image: interior status (which survivors count,

@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
                                                                     long long words, long long P,
                                                                     const Ladder lad, unsigned* Hb,
                                                                     unsigned* region, long long region_pitch,
-                                                                    int y0, int Hg, unsigned char* live_rows) {
+                                                                    int y0, int Hg, unsigned char* live_rows,
+                                                                    const unsigned* row_counts, long long rc_stride) {
     extern __shared__ unsigned rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long task = (long long)blockIdx.x * RP_WARPS + warp;
@@ -342,6 +343,12 @@ __global__ void __launch_bounds__(RP_WARPS * 32) region_rows_kernel(const unsign
         for (long long i = lane; i < words; i += 32) region[(long long)y * region_pitch + i] = 0u;
     const int m = lad.m[k];
     const int lo = (m - 1) / 2, hi = m / 2;
+    // K3's per-row survivor counts, when the caller has them: a row without
+    // an interior survivor is flagged dead without reading its mask row
+    if (row_counts && row_counts[(long long)k * rc_stride + y] == 0u) {
+        if (lane == 0) live_rows[(long long)k * H + y] = 0;
+        return;
+    }
     unsigned* out = Hb + ((long long)k * H + y) * words;
     const unsigned* mrow = masks + (long long)k * size_stride + (long long)y * mask_pitch;
     // F is needed at x - hi >= -hi: the row sits at word offset P of a
@@ -667,7 +674,8 @@ size_t region_ladder_workspace_bytes(int64_t W, int64_t H, int32_t L) {
 // survivor that covers the rows the caller keeps.
 int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H,
                        int64_t y0, int64_t Hg, int32_t L, const int32_t* h_m, int32_t stride, uint32_t* d_region,
-                       void* d_ws, size_t ws_bytes, void* stream) {
+                       void* d_ws, size_t ws_bytes, void* stream, const uint32_t* d_row_counts = nullptr,
+                       int64_t rc_stride = 0) {
     Ladder lad;
     if (int e = fill_ladder(lad, L, h_m)) return e;
     if (W < 1 || H < 1 || stride < 1 || y0 < 0 || y0 + H > Hg) { set_error("bad region arguments"); return SS_EINVAL; }
@@ -693,7 +701,7 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
         const long long tasks = (long long)L * H;
         region_rows_kernel<<<(unsigned)((tasks + RP_WARPS - 1) / RP_WARPS), RP_WARPS * 32, smem, s>>>(
             d_masks, mask_pitch, size_stride, (int)W, (int)H, words, P, lad, Hb, d_region, mask_pitch, (int)y0,
-            (int)Hg, live_rows);
+            (int)Hg, live_rows, d_row_counts, (long long)rc_stride);
         note_launch();
         if (int e = check_launch("region_rows_kernel")) return e;
     }
@@ -715,14 +723,15 @@ int region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch, int64_t size
 }
 
 int region_ladder(const uint32_t* d_masks, int64_t mask_pitch, int64_t size_stride, int64_t W, int64_t H, int32_t L,
-                  const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream) {
+                  const int32_t* h_m, int32_t stride, uint32_t* d_region, void* d_ws, size_t ws_bytes, void* stream,
+                  const uint32_t* d_row_counts = nullptr, int64_t rc_stride = 0) {
     // the chained form is opt-in (SS_REGION_CHAIN=1): measured slower than the
     // per-size row / column passes -- config 4 step 35.7 -> 36.6 ms, config 1
     // 0.66 -> 0.75 ms (a full-bitmap pass per step, each smem-bound)
     const char* chain = getenv("SS_REGION_CHAIN");
     if (!chain || atoi(chain) == 0)
         return region_ladder_rows(d_masks, mask_pitch, size_stride, W, H, 0, H, L, h_m, stride, d_region, d_ws,
-                                  ws_bytes, stream);
+                                  ws_bytes, stream, d_row_counts, rc_stride);
     Ladder lad;
     if (int e = fill_ladder(lad, L, h_m)) return e;
     if (W < 1 || H < 1 || stride < 1) { set_error("bad region arguments"); return SS_EINVAL; }
@@ -841,6 +850,13 @@ int ss_region_ladder(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t 
                      size_t workspace_bytes, void* stream) {
     return ss::region_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, n_sizes, h_m, stride, d_region,
                              d_workspace, workspace_bytes, stream);
+}
+int ss_region_ladder2(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W, int64_t H,
+                      int32_t n_sizes, const int32_t* h_m, int32_t stride, const uint32_t* d_row_counts,
+                      int64_t row_counts_stride, uint32_t* d_region, void* d_workspace, size_t workspace_bytes,
+                      void* stream) {
+    return ss::region_ladder(d_masks, mask_pitch_words, size_stride_words, W, H, n_sizes, h_m, stride, d_region,
+                             d_workspace, workspace_bytes, stream, d_row_counts, row_counts_stride);
 }
 int ss_region_ladder_rows(const uint32_t* d_masks, int64_t mask_pitch_words, int64_t size_stride_words, int64_t W,
                           int64_t rows, int64_t y0, int64_t H, int32_t n_sizes, const int32_t* h_m, int32_t stride,

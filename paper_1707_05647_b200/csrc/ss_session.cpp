@@ -486,8 +486,9 @@ int screen_locked(ss_session& s, const uint8_t* h_img, const uint8_t* h_tpl, int
     // K5 + popcount + the region's D2H on the region stream
     unsigned long long* d_counts = static_cast<unsigned long long*>(s.counts.p);
     SS_TRY(cuda_ok(cudaStreamWaitEvent(s.s_region, s.e_k3, 0), "event wait"));
-    SS_TRY(ss_region_ladder(static_cast<const uint32_t*>(s.masks.p), words, H * words, W, H, L, p.m, p.stride,
-                            static_cast<uint32_t*>(s.region.p), s.region_ws.p, s.region_ws.n, s.s_region));
+    SS_TRY(ss_region_ladder2(static_cast<const uint32_t*>(s.masks.p), words, H * words, W, H, L, p.m, p.stride,
+                             static_cast<const uint32_t*>(s.row_counts.p), H, static_cast<uint32_t*>(s.region.p),
+                             s.region_ws.p, s.region_ws.n, s.s_region));
     tr.mark("k5_kernels", s.s_region);
     SS_TRY(ss_popcount(static_cast<const uint32_t*>(s.region.p), words, W, H, d_counts + 1, s.s_region));
     unsigned long long* h_counts = static_cast<unsigned long long*>(s.counts_h.p);

@@ -513,10 +513,10 @@ class Engine:
     def region_all(self, tp: TemplatePlan) -> None:
         """K5 for every size in one pass, then the region popcount."""
         ms = tp.m_arr if tp.m_arr is not None else self._ladder_array(tp)
-        _native.check(self.L.ss_region_ladder(
+        _native.check(self.L.ss_region_ladder2(
             self.masks.data_ptr(), self.words, self.mrows * self.words, self.W, self.H, len(ms), ms.ctypes.data,
-            tp.config.stride, self.region.data_ptr(), self.region_ws.data_ptr(), self.region_ws.numel(),
-            _stream_handle(self.device)), "region")
+            tp.config.stride, self.row_counts.data_ptr(), self.row_counts.shape[1], self.region.data_ptr(),
+            self.region_ws.data_ptr(), self.region_ws.numel(), _stream_handle(self.device)), "region")
         _native.check(self.L.ss_popcount(self.region.data_ptr(), self.words, self.W, self.H,
                                          self.totals[1:].data_ptr(), _stream_handle(self.device)), "popcount")
 
