@@ -665,6 +665,39 @@ def test_region_chain_equals_union_of_footprints(cuda, monkeypatch, chain):
         compare_with_oracle(img, case.template, kw)
 
 
+def test_region_with_and_without_row_counts(cuda):
+    """K5 skips rows whose K3 survivor count is zero without reading them
+    (ss_region_ladder2); without the counts (ss_region_ladder: it finds the
+    empty rows itself) the region must be the same, on a sparse result (most
+    rows empty) and a dense one."""
+    import torch
+    import workloads as WL
+    from paper_1707_05647_b200 import _native
+    from paper_1707_05647_b200.engine import Engine, fill_keysets, plan_ladder
+
+    L = _native.lib()
+    img = WL.make_image(900, 700, seed=41, sigma=3.0, noise=1.0)
+    for seed, q in ((42, (8.0, 8.0, 8.0)), (43, (64.0, 64.0, 64.0))):
+        tpl = WL.make_template(img, seed, 48, (0.8, 1.3), std_threshold=10.0).template
+        cfg = pcfg({"alpha": 0.5, "beta": 2.0, "ladder_ratio": 1.2, "quantizer": q})
+        h, w = img.shape
+        eng = Engine(w, h, cuda)
+        tp = plan_ladder(tpl.shape[1], cfg)
+        fill_keysets(tp, tpl, cuda)
+        eng.run(torch.from_numpy(np.ascontiguousarray(img)).to(cuda), tp)
+        torch.cuda.synchronize()
+        with_counts = eng.region.clone()
+        ms = np.array([sp.m for sp in tp.sizes], np.int32)
+        other = torch.full_like(eng.region, -1)
+        _native.check(L.ss_region_ladder(eng.masks.data_ptr(), eng.words, eng.mrows * eng.words, w, h, len(ms),
+                                         ms.ctypes.data, cfg.stride, other.data_ptr(), eng.region_ws.data_ptr(),
+                                         eng.region_ws.numel(), torch.cuda.current_stream().cuda_stream), "region")
+        torch.cuda.synchronize()
+        assert torch.equal(with_counts, other)
+        empty = int((eng.row_counts[: len(ms)] == 0).sum())
+        assert 0 < empty < eng.row_counts[: len(ms)].numel()  # both kinds of rows occur
+
+
 def _same_result(a, b):
     assert tuple(a.ladder) == tuple(b.ladder)
     assert np.array_equal(a.candidates.array(), b.candidates.array())

@@ -50,6 +50,7 @@ def main(path, runs=1):
         print(f"{k[:40]:40s} {n[k] // runs:7d} {ms:9.3f} {t[k] / tot:6.1%} {gb:8.2f} {gb / (ms / 1e3) if ms else 0:7.0f}")
     print(f"total ms/run {tot / 1e3 / runs:.3f}")
     main.l2 = l2
+    main.n = n
     return t, b, inst
 
 
@@ -60,6 +61,8 @@ def record_k3(path, runs, name, rnd="r2"):
     rec = {"dram_bytes_per_step": sum(b[k] for k in k3) * 1e9 / runs,
            "k3_ms_per_step_under_ncu": sum(t[k] for k in k3) / 1e3 / runs,
            "source": os.path.relpath(os.path.abspath(path), root)}
+    # images per step (config 3 screens 64): one rowpre launch per image build
+    rec["images"] = max(1, sum(main.n[k] for k in main.n if "rowpre" in k) // runs)
     if inst:
         rec["inst_per_step"] = sum(inst[k] for k in k3) / runs
         rec["inst_stage1_per_step"] = sum(inst[k] for k in k3 if "stage1" in k) / runs
