@@ -586,7 +586,7 @@ class Engine:
 
     # ── upload, build and screen overlapped (large images, screen()) ─────
     PIPELINE_MIN_BYTES = 32 << 20  # images from this size take run_pipelined
-    PIPELINE_CHUNKS = 8
+    PIPELINE_CHUNKS = 10  # measured at config 4 (e2e ms): 4: 27.6, 5: 26.7, 8: 26.4, 10: 26.2, 12+: 31 (two pieces per chunk)
 
     def run_pipelined(self, img: np.ndarray, tp: TemplatePlan, host_masks: torch.Tensor, keysets) -> None:
         """screen() for a large host image: the image goes up in row chunks
@@ -638,20 +638,24 @@ class Engine:
         us.wait_stream(main)  # the previous screen is done reading the device image
         # build chunks: whole bands; screen chunks: rows whose tables are final
         rb = int(self.L.ss_build_band_rows(W, H, 1 if (int64 or hi16) else 0))
-        per = -(-H // self.PIPELINE_CHUNKS)  # ceil
+        n_chunks = int(os.environ.get("SS_PIPE_CHUNKS", self.PIPELINE_CHUNKS))  # experiment hooks
+        last_parts = int(os.environ.get("SS_PIPE_LAST_PARTS", 2))
+        mid_parts = int(os.environ.get("SS_PIPE_MID_PARTS", 1))
+        per = -(-H // n_chunks)  # ceil
         step = max(rb, -(-per // rb) * rb)
         ends = list(range(step, H, step)) + [H]
         hi_max = max(((sp.m // 2) for sp in tp.sizes if sp.plan), default=0)
-        # screen chunk k = the rows build chunk k completes, in pieces (the
-        # last in four) so that a piece's mask D2H overlaps the next piece's
-        # screen and the copy left after the last piece is short
+        # screen chunk k = the rows build chunk k completes; the last chunk
+        # in two pieces so that the copy left after the last piece is short
+        # (every piece costs launches and pipeline ramps: more pieces measured
+        # slower)
         dec, owner, prev = [], [], 0
         for k, e in enumerate(ends):
             # cuts on multiples of 16 rows: stage 1 decides groups of up to 16
             # rows from one tested row, and a group cut by a piece's end falls
             # back to "every column is a candidate"
             d = H if e == H else max(prev, (e - hi_max - 1) // 16 * 16)
-            parts = 4 if e == H else 2
+            parts = last_parts if e == H else mid_parts
             cuts = [prev] + [max(prev, (prev + (d - prev) * i // parts) // 16 * 16) for i in range(1, parts)] + [d]
             for a, b in zip(cuts[:-1], cuts[1:]):
                 if b > a:
