@@ -230,10 +230,10 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     __shared__ E cand_buf[WARPS][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
-        for (int s = 0; s < a.n_sizes; ++s) {
+        for (int s = threadIdx.x >> 5; s < a.n_sizes; s += blockDim.x >> 5) {  // a warp per size
             const SizeDev& S = a.size[s];
             if (S.bm1 < 0) continue;
-            for (int i = threadIdx.x; i < S.wm1; i += blockDim.x)
+            for (int i = threadIdx.x & 31; i < S.wm1; i += 32)
                 sbits[S.bm1 + i] = S.bsrc1 >= 0 ? __ldg(blob32 + S.bsrc1 + i) : 0u;
         }
     }
@@ -634,10 +634,10 @@ __global__ void __launch_bounds__((GeoC::CW + 1) * 32, 1)
     __shared__ int2 cand_buf[CW][CAND_BUF];
     {
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
-        for (int s = 0; s < a.n_sizes; ++s) {
+        for (int s = threadIdx.x >> 5; s < a.n_sizes; s += blockDim.x >> 5) {  // a warp per size
             const SizeDev& S = a.size[s];
             if (S.bm1 < 0) continue;
-            for (int i = threadIdx.x; i < S.wm1; i += blockDim.x)
+            for (int i = threadIdx.x & 31; i < S.wm1; i += 32)
                 sbits[S.bm1 + i] = S.bsrc1 >= 0 ? __ldg(blob32 + S.bsrc1 + i) : 0u;
         }
     }
@@ -1022,11 +1022,14 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
         for (int s = threadIdx.x; s < a.n_sizes; s += blockDim.x)
             ssize[s] = SizeSm{a.size[s].mask, a.size[s].row_counts, a.size[s].ring0, a.size[s].n_rings};
+        // a warp per ring: the rings' bitmap loads go out together (one ring
+        // after another, each copy waited out a global-load round trip -- ~75
+        // in a row per CTA and launch at config 4)
         const unsigned* blob32 = reinterpret_cast<const unsigned*>(a.blob);
-        for (int r = 0; r < a.n_rings; ++r) {
+        for (int r = threadIdx.x >> 5; r < a.n_rings; r += blockDim.x >> 5) {
             const RingDev& R = a.ring[r];
             if (R.bm < 0) continue;
-            for (int i = threadIdx.x; i < R.bwords; i += blockDim.x)
+            for (int i = threadIdx.x & 31; i < R.bwords; i += 32)
                 sbits[R.bm + i] = R.bsrc >= 0 ? __ldg(blob32 + R.bsrc + i) : 0u;
         }
     }
