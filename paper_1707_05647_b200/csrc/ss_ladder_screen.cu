@@ -982,11 +982,20 @@ __global__ void __launch_bounds__(256) ladder_border_kernel(const __grid_constan
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0 && (a.mask_pitch & 3) == 0 && 4LL * qpr <= a.mask_pitch) {
         // every thread of the grid stores 16 bytes per turn, rows x pieces flattened
         const long long total = (long long)rows * qpr;
-        for (long long i = tid; i < total; i += nthr) {
-            const int r = (int)(i / qpr), q = (int)(i - (long long)r * qpr);
-            const int y = a.y_begin + r;
-            reinterpret_cast<uint4*>(base + (long long)r * a.mask_pitch)[q] =
-                make_uint4(word(y, 4 * q), word(y, 4 * q + 1), word(y, 4 * q + 2), word(y, 4 * q + 3));
+        if (total < (1LL << 31)) {  // 32-bit index arithmetic (a 64-bit division per store is ~100 instructions)
+            for (unsigned i = (unsigned)tid; i < (unsigned)total; i += (unsigned)nthr) {
+                const int r = (int)(i / (unsigned)qpr), q = (int)(i - (unsigned)r * (unsigned)qpr);
+                const int y = a.y_begin + r;
+                reinterpret_cast<uint4*>(base + (long long)r * a.mask_pitch)[q] =
+                    make_uint4(word(y, 4 * q), word(y, 4 * q + 1), word(y, 4 * q + 2), word(y, 4 * q + 3));
+            }
+        } else {
+            for (long long i = tid; i < total; i += nthr) {
+                const int r = (int)(i / qpr), q = (int)(i - (long long)r * qpr);
+                const int y = a.y_begin + r;
+                reinterpret_cast<uint4*>(base + (long long)r * a.mask_pitch)[q] =
+                    make_uint4(word(y, 4 * q), word(y, 4 * q + 1), word(y, 4 * q + 2), word(y, 4 * q + 3));
+            }
         }
     } else {
         const long long total = (long long)rows * words;
