@@ -535,6 +535,24 @@ def test_stage1_row_steps_keep_every_ring0_passer(cuda, monkeypatch, which, slac
             assert cb[2] > 0  # the comparison is not vacuous
 
 
+def test_dense_candidates_with_partitioned_lists(cuda):
+    """A periodic texture screened with one of its periods: ring 0's mean is
+    the same almost everywhere, so nearly every centre of every size passes
+    stage 1 -- the candidate lists (8 partitions from 32768 tiles) fill close
+    to their capacity and the row-step plan picks its largest steps.  Masks,
+    candidates and region must still equal the oracle's."""
+    import workloads as WL
+
+    rng = np.random.default_rng(77)
+    period = WL.make_image(64, 64, seed=78, sigma=2.0, noise=0.0)
+    img = np.tile(period, (64, 64))  # 4096 x 4096
+    img = np.clip(img.astype(np.int32) + rng.integers(-2, 3, size=img.shape), 0, 255).astype(np.uint8)
+    tpl = np.ascontiguousarray(img[1024:1088, 2048:2112])
+    res = compare_with_oracle(img, tpl, {"alpha": 0.7, "beta": 1.5, "ladder_ratio": 1.15,
+                                         "quantizer": (8.0, 8.0, 8.0)})
+    assert len(res.ladder) >= 5
+
+
 def test_coarse_planes_are_bit_slices(cuda):
     """ss_build_tables3's u16 planes are (cell >> shift) & 0xffff of the
     SAT / E / O PLAIN cells for every shift."""
