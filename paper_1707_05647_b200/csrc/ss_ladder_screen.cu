@@ -1169,7 +1169,13 @@ constexpr size_t PLAN_BYTES = (sizeof(S1Plan) + 255) / 256 * 256;  // after the 
 #define FUSED_LARGE_TILES_MACRO 32768
 #endif
 constexpr long long FUSED_LARGE_TILES = FUSED_LARGE_TILES_MACRO;  // partitioned lists from this many tiles per pass
-constexpr size_t FUSED_WS_CAP = (size_t)(2 * sizeof(FEntry<unsigned>)) << 28;  // ss_ladder_workspace_bytes: row bands beyond this (4 GiB of int2 entries)
+// 16 GiB: config 4 runs 8 + 2 row bands per step instead of 16 + 8 at 4 GiB
+// (every band costs a plan, a border, a stage-1 and a rings launch with their
+// prologues and pipeline ramps: step 19.04 -> 18.46 ms; 32 GiB: 18.42)
+#ifndef FUSED_WS_CAP_SHIFT
+#define FUSED_WS_CAP_SHIFT 30
+#endif
+constexpr size_t FUSED_WS_CAP = (size_t)(2 * sizeof(FEntry<unsigned>)) << FUSED_WS_CAP_SHIFT;  // ss_ladder_workspace_bytes: row bands beyond this
 
 // capacity in tiles of TXMAX x TY centres (covers either fused tile width)
 long long tiles_of(int64_t W, int64_t rows) {
