@@ -53,8 +53,9 @@ def test_ladder_workspace_query():
         one = L.ss_ladder_workspace_bytes(W, H, 1)
         assert one >= L.ss_screen_workspace_bytes(W, H)
         assert L.ss_ladder_workspace_bytes(W, H, 9) > one
-    big = L.ss_ladder_workspace_bytes(16384, 16384, 33)
-    assert big <= max(5 << 30, L.ss_screen_workspace_bytes(16384, 16384))
+    big = L.ss_ladder_workspace_bytes(16384, 16384, 33)  # config 4: 16 GiB cap, row bands of 2048 rows
+    assert big <= max(17 << 30, L.ss_screen_workspace_bytes(16384, 16384))
+    assert big < 33 * 16384 * 16384 * 8  # less than one entry per centre of the whole image
 
 
 def test_argument_errors_map_to_value_error():
