@@ -97,6 +97,10 @@ int ss_build_tables2(const uint8_t* d_img, int64_t W, int64_t H, int64_t img_pit
  * sums cannot wrap), -1 if none.
  */
 int32_t ss_coarse_shift(int64_t count);
+/* Bytes of the coarse-plane buffer: the 3 * n_coarse planes plus 16 rows of
+ * padding (stage 1's row-step TMA views address whole groups of up to 16 rows;
+ * the last group of the last plane may end past row H).  Allocate at least
+ * this much for d_coarse. */
 size_t ss_coarse_bytes(int64_t W, int64_t H, int32_t n_coarse);
 /*
  * ss_build_tables3 for the image rows [y0, y1) only, y0 and y1 whole bands of
@@ -201,7 +205,7 @@ int ss_selftest_cells(uint64_t n, uint64_t seed, int32_t ring_n, int32_t ring_d,
  * d_workspaces[i] (ss_screen_workspace_bytes each) belongs to streams[i].
  * flags bit 0: screen every size from the int64 planes (test hook).
  * flags bit 1: fused ladder -- the sizes that share a plane width are
- * screened in lock-step (ss_ladder_screen.cu: two launches per row band, each
+ * screened in lock-step (ss_ladder_screen.cu: a few launches per row band, each
  * plane row read from HBM about once per band instead of once per size), all
  * on streams[0] with d_workspaces[0], whose workspace_bytes should be
  * ss_ladder_workspace_bytes(W, y_end - y_begin, n_sizes) (a smaller one
@@ -239,7 +243,7 @@ int ss_screen_ladder2(const int64_t* d_planes, const uint32_t* d_planes32, int64
                       const uint16_t* d_coarse, int32_t n_coarse, const int32_t* h_shifts, const uint16_t* d_hi16);
 
 /* Workspace bytes for the fused ladder (flags bit 1) of n_sizes sizes over
- * `rows` decided rows: one row band of at most 4 GiB of candidate list, and
+ * `rows` decided rows: one row band of at most 16 GiB of candidate list, and
  * at least ss_screen_workspace_bytes (the per-size fallback shares it). */
 size_t ss_ladder_workspace_bytes(int64_t W, int64_t rows, int32_t n_sizes);
 
