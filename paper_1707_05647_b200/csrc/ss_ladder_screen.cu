@@ -1055,8 +1055,18 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
     const unsigned wid = blockIdx.x * RK_WARPS + warp;
     int q = (int)(wid % parts), visited = 1;
     const unsigned gc = (wid / parts) % GROUP_CTRS;
-    // (a list never extends past its partition: stage 1 drops what would not fit)
-    unsigned cnt_q = min(__ldg(list_ctr + q * CTR_STRIDE), (unsigned)part_cap);
+    // A list never extends past its partition (stage 1 does not store what
+    // would not fit); a partition that did overflow -- impossible with a
+    // workspace of ss_ladder_workspace_bytes unless the tile hand-out were
+    // skewed beyond its 1/16 headroom on an image where every centre is a
+    // candidate -- must not yield a silently incomplete screen: trap, so the
+    // caller's next synchronisation reports a CUDA error.
+    auto list_len = [&](int part_i) -> unsigned {
+        const unsigned c = __ldg(list_ctr + part_i * CTR_STRIDE);
+        if (c > (unsigned)part_cap) asm volatile("trap;");
+        return c;
+    };
+    unsigned cnt_q = list_len(q);
     const E* in = list_base + q * part_cap;
     unsigned g_raw = 0;
     if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
@@ -1075,7 +1085,7 @@ __global__ void __launch_bounds__(RK_WARPS * 32, FUSED_RINGS_MINB)
             }
             ++visited;
             q = q + 1 == parts ? 0 : q + 1;
-            cnt_q = min(__ldg(list_ctr + q * CTR_STRIDE), (unsigned)part_cap);
+            cnt_q = list_len(q);
             in = list_base + q * part_cap;
             if (lane == 0) g_raw = atom_add_ahead(group_ctr + (q * GROUP_CTRS + gc) * CTR_STRIDE, 1u);
         }
