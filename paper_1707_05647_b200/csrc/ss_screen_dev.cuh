@@ -725,13 +725,16 @@ constexpr int TILE_POS = TX * TY;  // centres per tile
 constexpr int MAX_PARTS = 8;
 constexpr int TILE_CTRS = MAX_PARTS;  // stage-1 tile counters (partition p's CTAs use counter p)
 // List slots a stage-1 warp reserves per atomic (a multiple of 32): fewer
-// atomics on the list counter vs. the padding of each warp's last blocks
-// (measured: 64 for the single list, 128 for the partitioned lists).
+// atomics on the list counter vs. the padding of each warp's last blocks.
+// Re-measured at the end of round 2 (row steps emit whole groups of rows at
+// once): single list 64 / 128 / 256 -> config 1 step 0.617 / 0.597 / 0.595 ms,
+// config 3 16.9 / 16.35 / 16.4; partitioned lists 128 / 256 / 512 / 1024 /
+// 2048 -> config 4 step 18.48 / 17.97 / 17.78 / 17.72 / 17.85 ms.
 #ifndef RESERVE_SMALL_MACRO
-#define RESERVE_SMALL_MACRO 64
+#define RESERVE_SMALL_MACRO 128
 #endif
 #ifndef RESERVE_LARGE_MACRO
-#define RESERVE_LARGE_MACRO 128
+#define RESERVE_LARGE_MACRO 1024
 #endif
 constexpr int RESERVE_SMALL = RESERVE_SMALL_MACRO, RESERVE_LARGE = RESERVE_LARGE_MACRO,
               RESERVE_MAX = RESERVE_SMALL > RESERVE_LARGE ? RESERVE_SMALL : RESERVE_LARGE;
