@@ -1200,7 +1200,8 @@ long long fused_part_cap(int64_t W, int64_t rows, int n_sizes, int sms, int part
     // partitioned lists: 1/16 headroom for the uneven shares of a round-robin
     // hand-out (148 CTAs over 8 partitions, tiles of 1 / 2 / 4 row steps)
     const long long share = (tiles_of(W, rows) * n_sizes + parts - 1) / parts;
-    return (share + (parts > 1 ? share / 16 + 64 : 0)) * (TXMAX * TY) + ctas * s1_warps * 2 * RESERVE_MAX;
+    return (share + (parts > 1 ? share / 16 + 64 : 0)) * (TXMAX * TY) +
+           ctas * s1_warps * 2 * (parts > 1 ? RESERVE_LARGE : RESERVE_SMALL);
 }
 size_t fused_ws_bytes(int64_t W, int64_t rows, int n_sizes, int sms, size_t entry = sizeof(FEntry<unsigned>)) {
     const int parts = parts_for(W, rows, n_sizes);

@@ -492,7 +492,7 @@ static long long n_tiles_of(int64_t W, int64_t rows) {
 }
 static long long part_cap_of(int64_t W, int64_t rows, int sms, int parts) {
     const long long ctas = (2LL * sms + parts - 1) / parts;
-    return (n_tiles_of(W, rows) + parts - 1) / parts * TILE_POS + ctas * WARPS * 2 * RESERVE_MAX;
+    return (n_tiles_of(W, rows) + parts - 1) / parts * TILE_POS + ctas * WARPS * 2 * PS_RESERVE_MAX;
 }
 static size_t list_bytes(int64_t W, int64_t rows, int sms, bool large) {
     return large ? (size_t)MAX_PARTS * part_cap_of(W, rows, sms, MAX_PARTS) * sizeof(int4)
@@ -568,7 +568,7 @@ static int launch_k3(K3Launch& L, int parts) {
         const long long grid = std::max<long long>(std::min<long long>(tm.n_tiles, (long long)L.sms * s1_per_sm),
                                                    (long long)TILE_CTRS);
         s1<<<(unsigned)grid, (WARPS + 1) * 32, s1_smem_all, L.s>>>(a, L.maps, tm, parts,
-                                                                  parts > 1 ? RESERVE_LARGE : RESERVE_SMALL, list, part_cap, L.list_ctr,
+                                                                  parts > 1 ? PS_RESERVE_LARGE : PS_RESERVE_SMALL, list, part_cap, L.list_ctr,
                                                                   L.tile_ctr);
         note_launch();
         if (int e = check_launch("stage1_kernel")) return e;

@@ -738,6 +738,9 @@ constexpr int TILE_CTRS = MAX_PARTS;  // stage-1 tile counters (partition p's CT
 #endif
 constexpr int RESERVE_SMALL = RESERVE_SMALL_MACRO, RESERVE_LARGE = RESERVE_LARGE_MACRO,
               RESERVE_MAX = RESERVE_SMALL > RESERVE_LARGE ? RESERVE_SMALL : RESERVE_LARGE;
+// the per-size kernels (ss_screen.cu) keep their round-1 reservations (their
+// workspace is the floor of every ladder workspace)
+constexpr int PS_RESERVE_SMALL = 64, PS_RESERVE_LARGE = 128, PS_RESERVE_MAX = 128;
 #ifndef GROUP_CTRS
 #define GROUP_CTRS 8u  // rings group counters per partition
 #endif
